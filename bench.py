@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Packed-training throughput on B200 — the BASELINE.json metric.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+                    [--workload config0|k16]
+
+A "step" is one packed train step (forward + backward + every member's
+optimizer update) of the workload's K members over one batch each.
+  value  = K x b / device time of the step, inputs resident in HBM, L2
+           flushed (256 MiB write) before every timed step; max over ranks.
+  e2e    = the same metric through the public drop-in API
+           (`packing.packed_step` on host numpy datasets): per step the step
+           descriptor goes H2D from pinned memory and losses come back D2H.
+  speedup_vs_unpacked = the same K members trained one after another as
+           one-member packs (standalone_step) on the same GPU.
+Multi-GPU (torchrun): one independent pack per GPU (weak scaling, no
+collective on the data path; the timing max uses NCCL).
+`--impl reference` times the float64 CPU port of the reference path
+(oracle/, numpy) on this host's cores for the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packed train samples/sec (K models) & speedup vs unpacked; Hyperband wall time"
+UNIT = "samples/s (x K members)"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+WORKLOADS = {
+    # BASELINE.json configs[0]: the reference-runnable, parity-pinned config
+    "config0": dict(n=10000, dim=784, classes=10, hidden=(256,), act="relu", batch=32,
+                    members=[("sgd", 0.1), ("sgd", 0.01)]),
+    # same member shape, a 16-member hyperparameter sweep (SGD/Adam/Momentum/Adagrad)
+    "k16": dict(n=10000, dim=784, classes=10, hidden=(256,), act="relu", batch=32,
+                members=[(("sgd", "adam", "momentum", "adagrad")[i % 4], 10.0 ** -(1 + i % 4))
+                         for i in range(16)]),
+}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def _make(wl, data, packing, seed=0):
+    ds = data.synth_dataset(wl["n"], wl["dim"], wl["classes"], seed=seed)
+    arch = packing.MLPArch(wl["dim"], tuple(wl["hidden"]), wl["classes"], wl["act"])
+    hs = [packing.make_handle(f"m{i}", arch, opt, lr, wl["batch"], 10 ** 9, "train", seed)
+          for i, (opt, lr) in enumerate(wl["members"])]
+    return {"train": ds}, hs
+
+
+def _phase_bytes(wl, kind, layer, es=4):
+    """Algorithmic HBM bytes of one phase launch: every
+    tensor the phase must touch, once; the shared input rows once per group."""
+    dims = (wl["dim"], *wl["hidden"], wl["classes"])
+    b = wl["batch"]
+    K = len(wl["members"])
+    slots = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
+    L = len(dims) - 1
+    total = 0
+    for opt, _ in wl["members"]:
+        if kind == 0:  # forward: W, bias, write Z (+A if hidden); input rows
+            i, o = dims[layer], dims[layer + 1]
+            total += (i * o + o + b * o * (2 if layer + 1 < L else 1)) * es
+            if layer > 0:
+                total += b * i * es
+        elif kind == 1:  # head: read logits, write dlogits
+            total += 2 * b * dims[-1] * es
+        elif kind == 2:  # W/b + slots read and written, A_in and dZ read; dgrad
+            i, o = dims[layer], dims[layer + 1]
+            p = i * o + o
+            total += 2 * p * (1 + slots[opt]) * es + b * o * es
+            if layer > 0:
+                total += b * i * es + 3 * b * i * es  # A_in; Z, A read + dZ_prev write
+    if kind in (0, 2) and layer == 0:
+        total += b * dims[0] * es  # the group's shared input rows, once
+    return total
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9]
+        if not sm:
+            return None
+        reasons = set()
+        for r in rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_02885_b200 import data, packing, runtime
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    runtime.set_device(local)
+    runtime.set_precision(args.precision)
+    rt = runtime.runtime()
+    stream = torch.cuda.Stream()
+    rt.set_stream(stream.cuda_stream)
+    wl = WORKLOADS[args.workload]
+    K, b = len(wl["members"]), wl["batch"]
+    datasets, hs = _make(wl, data, packing, seed=rank)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+
+    for _ in range(args.warmup):
+        packing.packed_step(packed, datasets)
+
+    def device_loop(pk, members, steps):
+        """Σ per-step device time (events on the pack's stream), L2 cold."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        for i in range(steps):
+            flush_l2()
+            active = packing._active_members(pk, datasets, False)
+            plan = packing._plan_step(pk, active, datasets, None, None)
+            ev[i][0].record(stream)
+            t = plan.dpack.step_async()
+            ev[i][1].record(stream)
+            code, who, where, _, losses = plan.dpack.wait(t)
+            packing._apply_result(pk, active, plan, code, who, where, losses)
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(z) for a, z in ev)
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms = device_loop(packed, hs, args.steps)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    # e2e: public API on host datasets (descriptor H2D, losses D2H per step)
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        flush_l2()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        packing.packed_step(packed, datasets)
+        e2e_s += time.perf_counter() - t0
+    # e2e with the batch rows gathered on the host and copied H2D every step
+    spec = data.PreprocessSpec(stages=(("normalize", 0.0, 1.0),))
+    hb_s = 0.0
+    for _ in range(args.steps):
+        flush_l2()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        packing.packed_step(packed, datasets, preprocess_spec=spec)
+        hb_s += time.perf_counter() - t0
+
+    # unpacked: the same K members, one-member packs stepped one after another
+    _, solo = _make(wl, data, packing, seed=rank)
+    solo_packs = [packing.pack_models([h]) for h in solo]
+    for sp in solo_packs:
+        for _ in range(args.warmup):
+            packing.packed_step(sp, datasets)
+    un_ms = 0.0
+    for sp in solo_packs:
+        un_ms += device_loop(sp, sp.members, args.steps)
+
+    # per-phase profile (un-graphed, events around each launch)
+    prof = []
+    for _ in range(max(3, min(args.steps, 20))):
+        flush_l2()
+        active = packing._active_members(packed, datasets, False)
+        plan = packing._plan_step(packed, active, datasets, None, None)
+        code, phases, losses = plan.dpack.profile()
+        packing._apply_result(packed, active, plan, code, -1, -1, losses)
+        prof.append(phases)
+    phases = []
+    for i, (kind, layer, ctas, _) in enumerate(prof[0]):
+        phases.append({"kind": ("fwd", "head", "bwd+update", "finalize")[kind], "layer": layer,
+                       "ctas": ctas, "ms": statistics.median(p[i][3] for p in prof),
+                       "bytes": _phase_bytes(wl, kind, layer) if kind < 3 else 0})
+    top = max(phases, key=lambda p: p["ms"])
+
+    t = torch.tensor([dev_ms, e2e_s * 1e3, hb_s * 1e3, un_ms], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms, hb_ms, un_ms = t.tolist()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    peaks, peak_kind = _peaks()
+    ms_step = dev_ms / args.steps
+    value = world * K * b * args.steps / (dev_ms / 1e3)
+    launches = packed._dev[1].launches
+    ach = top["bytes"] / (top["ms"] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload, {}).get(
+            f"{top['kind']}:{top['layer']}")
+    desc_bytes = 16 + K * (40 if args.precision == "f32" else 40)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic (reference synth_dataset, seeded)",
+        "config": {"workload": args.workload, "members": K, "batch": b,
+                   "arch": [wl["dim"], *wl["hidden"], wl["classes"]], "act": wl["act"],
+                   "optimizers": [o for o, _ in wl["members"]],
+                   "parallelism": f"independent pack per GPU x{world}",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "speedup_vs_unpacked": un_ms / dev_ms,
+        "unpacked_ms_per_step": un_ms / args.steps,
+        "e2e": {"value": world * K * b * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": desc_bytes, "d2h_bytes_per_step": 16 + 8 * K,
+                "api": "packing.packed_step (host numpy datasets, resident on device)"},
+        "e2e_host_batches": {"value": world * K * b * args.steps / (hb_ms / 1e3), "unit": UNIT,
+                             "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
+                             "d2h_bytes_per_step": 16 + 8 * K,
+                             "api": "packed_step(preprocess_spec=normalize(0,1)): host gather"},
+        "roofline": {"bound": "hbm", "kernel": f"{top['kind']} layer {top['layer']}",
+                     "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": ach / peaks["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes": top["bytes"], "launch_ms": top["ms"],
+                     "peak_source": peak_kind},
+        "phases": phases,
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+    }
+    cpu = _cpu_baseline(wl, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
+    line["cpu_baseline"] = cpu
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max(i.get("num_threads", 1) for i in threadpool_info()) or 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _cpu_baseline(wl, seconds=10.0, steps=None):
+    """The float64 CPU port of the reference path (oracle/) on this host:
+    packed steps of the same workload, bounded to ~`seconds`."""
+    from oracle import mlp64 as O
+    did, x, y = O.synth_blobs(wl["n"], wl["dim"], wl["classes"], 0)
+    datasets = {"train": O.OracleDataset(did, x, y)}
+    dims = (wl["dim"], *wl["hidden"], wl["classes"])
+    ms = [O.OracleMember.make(f"m{i}", dims, wl["act"], opt, lr, wl["batch"], 10 ** 9, "train", 0)
+          for i, (opt, lr) in enumerate(wl["members"])]
+    for _ in range(3):
+        O.oracle_packed_step(ms, datasets)
+    t0 = time.perf_counter()
+    n = 0
+    while (steps is None and time.perf_counter() - t0 < seconds) or (steps is not None and n < steps):
+        O.oracle_packed_step(ms, datasets)
+        n += 1
+    dt = time.perf_counter() - t0
+    K, b = len(ms), wl["batch"]
+    return {"value": K * b * n / dt, "unit": UNIT, "cores": _cpu_threads(), "kind": "port",
+            "sample": f"{n} packed steps of {len(ms)} x {dims} b={b} ({dt:.1f} s, numpy f64)",
+            "ms_per_step": dt / n * 1e3}
+
+
+def _reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    wl = WORKLOADS[args.workload]
+    _cpu_baseline(wl, steps=args.warmup)
+    r = _cpu_baseline(wl, steps=args.steps)
+    return {"metric": METRIC, "value": r["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "members": len(wl["members"]),
+                       "batch": wl["batch"]},
+            "cpu_baseline": r,
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config0", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    line = _reference(args) if args.impl == "reference" else _b200(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

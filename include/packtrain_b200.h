@@ -1,0 +1,168 @@
+/*
+ * packtrain_b200.h — C-ABI of the B200-native pack primitive.
+ *
+ * K static MLPs ("members") are trained as one packed network on one B200,
+ * fed by shared input streams.  This ABI is the boundary a host binding
+ * (ctypes here; cgo/JNI would bind the same symbols) calls in place of the
+ * reference's numpy engine.  Every entry point names the reference function
+ * it replaces (paths relative to /root/reference/pkg/src/packtrain/).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch / CUDA types in signatures
+ *     (a stream is passed as `void*` holding a cudaStream_t).
+ *   - Host buffers are borrowed for the duration of a call only.
+ *   - Every function returns a PK_* status; details via pk_ctx_last_error().
+ *   - Parameters cross the boundary as float64 in the reference's layout:
+ *     per affine layer l = 0..n_layers-1, W_l row-major [dims[l], dims[l+1]]
+ *     (x @ W, engine.py:201) then b_l [dims[l+1]].  Optimizer slots follow
+ *     the same flat layout, one block per slot in the order
+ *     momentum:{velocity} adagrad:{accum} adam:{m, v} (engine.py:307-317).
+ *   - Device precision is chosen per context (PK_F32 default, PK_F64);
+ *     f64 -> f32 conversion is IEEE round-to-nearest, so get(set(x)) ==
+ *     float32(x) bit-exactly.
+ *   - Not thread-safe per context: one host thread drives one context
+ *     (the reference's packed_step is not reentrant).
+ */
+#ifndef PACKTRAIN_B200_H
+#define PACKTRAIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_ABI_VERSION 1
+#define PK_MAX_LAYERS 8 /* affine layers per member (hidden <= 7) */
+
+/* status codes */
+#define PK_OK 0
+#define PK_ERR_ARG 1            /* bad argument / shape (ShapeMismatch, PackError) */
+#define PK_ERR_NONFINITE_VALUE 2 /* forward node non-finite: EngineError, engine.py:233-235 */
+#define PK_ERR_NONFINITE_GRAD 3  /* NonFiniteGradient, engine.py:297-299 */
+#define PK_ERR_OOM 4            /* device allocation failed */
+#define PK_ERR_CUDA 5           /* CUDA runtime error */
+#define PK_ERR_STATE 6          /* API misuse (e.g. pending async step) */
+
+/* enums follow the reference tuples' order (engine.py:21-22) */
+#define PK_ACT_SIGMOID 0
+#define PK_ACT_LEAKY_RELU 1
+#define PK_ACT_TANH 2
+#define PK_ACT_RELU 3
+#define PK_OPT_SGD 0
+#define PK_OPT_MOMENTUM 1
+#define PK_OPT_ADAM 2
+#define PK_OPT_ADAGRAD 3
+#define PK_F32 0
+#define PK_F64 1
+
+typedef struct pk_ctx pk_ctx;
+typedef struct pk_dataset pk_dataset;
+typedef struct pk_order pk_order;
+typedef struct pk_member pk_member;
+typedef struct pk_pack pk_pack;
+
+/* Static description of one member (replaces MLPArch + make_optimizer,
+ * packing.py:32-38 / engine.py:99-105). */
+typedef struct {
+  int32_t n_layers;                   /* affine layers = len(hidden) + 1 */
+  int32_t dims[PK_MAX_LAYERS + 1];    /* input_dim, hidden..., classes */
+  int32_t activation;                 /* PK_ACT_* (hidden layers) */
+  int32_t optimizer;                  /* PK_OPT_* */
+  double learning_rate;               /* > 0 */
+  double weight_decay;                /* coupled L2 extension; 0 = reference */
+  int32_t max_rows;                   /* batch_size: rows per step <= this */
+  int32_t reserved;
+} pk_member_desc;
+
+/* One member's input for one packed step (replaces _next_batch + pad/mask,
+ * packing.py:161-172, :213-239).  Row r of the batch is dataset row
+ * order[pos + r] (or pos + r when order is NULL), r < take.  take == 0
+ * marks the member inactive for this step (finished / parked). */
+typedef struct {
+  const pk_dataset* data;
+  const pk_order* order;
+  int64_t pos;
+  int32_t take;
+  int32_t group; /* input-group id (members with equal ids share rows) */
+} pk_feed;
+
+/* Outcome of one packed step (reference exception semantics,
+ * packing.py:246-253): on PK_ERR_NONFINITE_VALUE nothing commits; on
+ * PK_ERR_NONFINITE_GRAD the members before `member` (pack order) commit. */
+typedef struct {
+  int32_t code;      /* PK_OK / PK_ERR_NONFINITE_VALUE / PK_ERR_NONFINITE_GRAD */
+  int32_t member;    /* offending member index in the pack, else -1 */
+  int32_t index;     /* value error: node index (0=in, 2l+1=aff l, 2l+2=act l,
+                        2n=loss); grad error: position in the grads order
+                        W_{n-1}, b_{n-1}, ..., W_0, b_0 (engine.py:270-271) */
+  int32_t committed; /* members whose update committed */
+} pk_status;
+
+/* ---- context ------------------------------------------------------------ */
+int pk_abi_version(void);
+int pk_ctx_create(int32_t device, int32_t dtype, pk_ctx** out);
+int pk_ctx_destroy(pk_ctx* ctx);
+const char* pk_ctx_last_error(const pk_ctx* ctx);
+int pk_ctx_set_stream(pk_ctx* ctx, void* cuda_stream); /* NULL = own stream */
+int pk_ctx_synchronize(pk_ctx* ctx);
+int pk_ctx_mem_info(pk_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes,
+                    uint64_t* ctx_bytes);
+
+/* ---- data (replaces Dataset / epoch_permutation / batch_at storage,
+ *      data.py:18-39, :124-136): device-resident copies ------------------- */
+int pk_dataset_create(pk_ctx* ctx, int64_t n, int32_t dim, pk_dataset** out);
+/* write rows [row0, row0+rows) from host f64 features / int64 labels */
+int pk_dataset_write(pk_dataset* ds, int64_t row0, int64_t rows,
+                     const double* features, const int64_t* labels);
+int pk_dataset_destroy(pk_dataset* ds);
+int pk_order_create(pk_ctx* ctx, const int64_t* perm, int64_t n, pk_order** out);
+int pk_order_destroy(pk_order* order);
+
+/* ---- members (replaces ModelHandle params + OptimizerState,
+ *      packing.py:52-81, engine.py:85-96) -------------------------------- */
+int pk_member_create(pk_ctx* ctx, const pk_member_desc* desc, pk_member** out);
+int pk_member_destroy(pk_member* m);
+int64_t pk_member_param_count(const pk_member* m);
+int32_t pk_member_slot_count(const pk_member* m);
+int64_t pk_member_device_bytes(const pk_member* m);
+int pk_member_set_lr(pk_member* m, double learning_rate);
+/* upload params (and slots when non-NULL, else zeros) + step counter */
+int pk_member_set_state(pk_member* m, const double* params, const double* slots,
+                        int64_t step_counter);
+/* download committed params / slots (either may be NULL) + step counter */
+int pk_member_get_state(pk_member* m, double* params, double* slots,
+                        int64_t* step_counter);
+/* testing hook (fault injection): the member's next step sees a NaN in the
+ * gradient tensor at `grad_position` (grads order, see pk_status.index);
+ * -1 clears.  Exercises the NonFiniteGradient commit rules. */
+int pk_member_inject_fault(pk_member* m, int32_t grad_position);
+
+/* ---- packs (replaces pack_models / packed_step / standalone_step,
+ *      packing.py:136-142, :185-282) ------------------------------------- */
+int pk_pack_create(pk_ctx* ctx, pk_member* const* members, int32_t k, pk_pack** out);
+int pk_pack_destroy(pk_pack* p);
+/* one synchronous packed step: losses[k] (float64) for active members */
+int pk_pack_step(pk_pack* p, const pk_feed* feeds, double* losses, pk_status* st);
+/* asynchronous form for pipelined drivers: enqueue, then wait by ticket */
+int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* ticket);
+int pk_pack_step_wait(pk_pack* p, int64_t ticket, double* losses, pk_status* st);
+/* forward-only mean softmax-xent of every member on `rows` rows of one
+ * dataset (order NULL = rows 0..rows-1); replaces EngineExecutor._val_loss
+ * (tuner.py:460-464).  Nothing is updated. */
+int pk_pack_eval(pk_pack* p, const pk_dataset* data, const pk_order* order,
+                 int64_t pos, int64_t rows, double* losses, pk_status* st);
+/* profiling: run one real step un-graphed with CUDA events around every
+ * phase (state advances as for pk_pack_step).  Arrays hold
+ * pk_pack_launches_per_step(p) entries: device ms, kind (0 forward, 1 head,
+ * 2 backward+update, 3 finalize), layer index, and tile (CTA) count. */
+int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* phase_ms,
+                         int32_t* phase_kind, int32_t* phase_layer,
+                         int32_t* phase_ctas, double* losses, pk_status* st);
+/* number of kernel launches one pk_pack_step enqueues */
+int32_t pk_pack_launches_per_step(const pk_pack* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACKTRAIN_B200_H */

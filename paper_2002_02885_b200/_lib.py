@@ -1,0 +1,133 @@
+"""ctypes binding of the C-ABI in include/packtrain_b200.h.
+
+The library is built in-tree (`libpk_b200.so`, see csrc/Makefile).  There is
+no fallback: if the library or a CUDA device is missing, `lib()` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpk_b200.so")
+
+PK_MAX_LAYERS = 8
+PK_OK, PK_ERR_ARG, PK_ERR_NONFINITE_VALUE, PK_ERR_NONFINITE_GRAD = 0, 1, 2, 3
+PK_ERR_OOM, PK_ERR_CUDA, PK_ERR_STATE = 4, 5, 6
+PK_F32, PK_F64 = 0, 1
+# enum order = the reference tuples (engine.py:21-22)
+ACT_CODES = {"sigmoid": 0, "leaky_relu": 1, "tanh": 2, "relu": 3}
+OPT_CODES = {"sgd": 0, "momentum": 1, "adam": 2, "adagrad": 3}
+
+# every symbol the header declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "pk_abi_version", "pk_ctx_create", "pk_ctx_destroy", "pk_ctx_last_error",
+    "pk_ctx_set_stream", "pk_ctx_synchronize", "pk_ctx_mem_info",
+    "pk_dataset_create", "pk_dataset_write", "pk_dataset_destroy",
+    "pk_order_create", "pk_order_destroy",
+    "pk_member_create", "pk_member_destroy", "pk_member_param_count",
+    "pk_member_slot_count", "pk_member_device_bytes", "pk_member_set_lr",
+    "pk_member_set_state", "pk_member_get_state", "pk_member_inject_fault",
+    "pk_pack_create", "pk_pack_destroy", "pk_pack_step", "pk_pack_step_async",
+    "pk_pack_step_wait", "pk_pack_eval", "pk_pack_profile_step",
+    "pk_pack_launches_per_step",
+)
+
+
+class MemberDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32),
+                ("dims", C.c_int32 * (PK_MAX_LAYERS + 1)),
+                ("activation", C.c_int32),
+                ("optimizer", C.c_int32),
+                ("learning_rate", C.c_double),
+                ("weight_decay", C.c_double),
+                ("max_rows", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class Feed(C.Structure):
+    _fields_ = [("data", C.c_void_p),
+                ("order", C.c_void_p),
+                ("pos", C.c_int64),
+                ("take", C.c_int32),
+                ("group", C.c_int32)]
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("member", C.c_int32),
+                ("index", C.c_int32), ("committed", C.c_int32)]
+
+
+class PKError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        super().__init__(f"pk error {code}: {msg}")
+
+
+_LIB = None
+_LOCK = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load the shared library and declare signatures (no device needed)."""
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    sig = {
+        "pk_abi_version": (C.c_int, []),
+        "pk_ctx_create": (C.c_int, [i32, i32, P(vp)]),
+        "pk_ctx_destroy": (C.c_int, [vp]),
+        "pk_ctx_last_error": (C.c_char_p, [vp]),
+        "pk_ctx_set_stream": (C.c_int, [vp, vp]),
+        "pk_ctx_synchronize": (C.c_int, [vp]),
+        "pk_ctx_mem_info": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
+        "pk_dataset_create": (C.c_int, [vp, i64, i32, P(vp)]),
+        "pk_dataset_write": (C.c_int, [vp, i64, i64, vp, vp]),
+        "pk_dataset_destroy": (C.c_int, [vp]),
+        "pk_order_create": (C.c_int, [vp, vp, i64, P(vp)]),
+        "pk_order_destroy": (C.c_int, [vp]),
+        "pk_member_create": (C.c_int, [vp, P(MemberDesc), P(vp)]),
+        "pk_member_destroy": (C.c_int, [vp]),
+        "pk_member_param_count": (i64, [vp]),
+        "pk_member_slot_count": (i32, [vp]),
+        "pk_member_device_bytes": (i64, [vp]),
+        "pk_member_set_lr": (C.c_int, [vp, dbl]),
+        "pk_member_set_state": (C.c_int, [vp, vp, vp, i64]),
+        "pk_member_get_state": (C.c_int, [vp, vp, vp, P(i64)]),
+        "pk_member_inject_fault": (C.c_int, [vp, i32]),
+        "pk_pack_create": (C.c_int, [vp, P(vp), i32, P(vp)]),
+        "pk_pack_destroy": (C.c_int, [vp]),
+        "pk_pack_step": (C.c_int, [vp, P(Feed), P(dbl), P(Status)]),
+        "pk_pack_step_async": (C.c_int, [vp, P(Feed), P(i64)]),
+        "pk_pack_step_wait": (C.c_int, [vp, i64, P(dbl), P(Status)]),
+        "pk_pack_eval": (C.c_int, [vp, vp, vp, i64, i64, P(dbl), P(Status)]),
+        "pk_pack_profile_step": (C.c_int, [vp, P(Feed), P(C.c_float), P(i32), P(i32),
+                                           P(i32), P(dbl), P(Status)]),
+        "pk_pack_launches_per_step": (i32, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    with _LOCK:
+        if _LIB is None:
+            _LIB = load_library()
+    return _LIB
+
+
+def check(ctx_ptr, rc):
+    """Raise PKError for non-OK codes that are not step outcomes."""
+    if rc in (PK_OK,):
+        return rc
+    msg = lib().pk_ctx_last_error(ctx_ptr) if ctx_ptr else b""
+    raise PKError(rc, (msg or b"").decode(errors="replace"))

@@ -1,0 +1,82 @@
+"""B200 memory model for pack grouping.
+
+The reference sizes packs with a calibrated 16 GB simulator
+(device_sim.py:72-85, :222-244).  Here a member's footprint is the exact
+size of its device slab (csrc/pk_runtime.cu pk_member_create): ping-pong
+parameters, ping-pong optimizer slots, per-layer Z/A/dZ workspace for
+`batch_size` rows and the control block, each 256-byte aligned; capacity is
+the GPU's real HBM.  `OOMError` / `DeviceAccountant` keep the reference's
+interface so `pack_opt_*` and `load_model(device=...)` work unchanged.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+_CTL_BYTES = 48          # sizeof(pk::MemberCtl)
+_ALIGN = 256
+_SLOTS = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
+
+
+class OOMError(Exception):
+    def __init__(self, demand, capacity, what="pack"):
+        self.demand = int(demand)
+        self.capacity = int(capacity)
+        self.deficit = int(demand - capacity)
+        super().__init__(f"{what}: demand {self.demand} B exceeds capacity "
+                         f"{self.capacity} B by {self.deficit} B")
+
+
+def _al(v):
+    return (v + _ALIGN - 1) // _ALIGN * _ALIGN
+
+
+def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") -> int:
+    """Bytes pk_member_create allocates for this member (exact)."""
+    es = 8 if precision == "f64" else 4
+    dims = (arch.input_dim, *arch.hidden, arch.classes)
+    P = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
+    ns = _SLOTS[optimizer.lower()]
+    total = 2 * _al(P * es) + 2 * _al(ns * P * es)
+    n = len(dims) - 1
+    for layer in range(n):
+        act = batch_size * dims[layer + 1] * es
+        total += _al(act) + _al(act if layer + 1 < n else 0) + _al(act)
+    return total + _al(_CTL_BYTES)
+
+
+@dataclass(frozen=True)
+class B200Device:
+    """Device profile consumed by the tuner's grouping (`memory_capacity`)."""
+    memory_capacity: int
+    name: str = "NVIDIA B200"
+
+    @classmethod
+    def detect(cls, reserve_fraction=0.05):
+        from .runtime import runtime
+        free, total, _ = runtime().mem_info()
+        return cls(memory_capacity=int(total * (1.0 - reserve_fraction)))
+
+
+class DeviceAccountant:
+    """Which members occupy a device and how many bytes (device_sim.py:222-244)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.resident: dict = {}
+
+    @property
+    def used(self) -> int:
+        return sum(self.resident.values())
+
+    def register(self, model_id: str, nbytes: int):
+        if model_id in self.resident:
+            raise ValueError(f"{model_id!r} is already resident")
+        if self.used + nbytes > self.device.memory_capacity:
+            raise OOMError(self.used + nbytes, self.device.memory_capacity,
+                           what=f"load {model_id!r}")
+        self.resident[model_id] = int(nbytes)
+
+    def release(self, model_id: str) -> int:
+        if model_id not in self.resident:
+            raise ValueError(f"{model_id!r} is not resident")
+        return self.resident.pop(model_id)

@@ -1,0 +1,655 @@
+"""The pack / load / free primitives — drop-in for the reference's
+`packtrain.packing` (packing.py:1-489) with the step executed on a B200.
+
+Host side (this file): member handles, cursors, input grouping, epoch plans,
+checkpoints — the same observable semantics as the reference.  Device side
+(`pk_pack_step`): the whole packed train step — batch gather through the
+epoch order, forward, softmax-xent, backward and every member's optimizer
+update — as one CUDA-graph launch over all K members, with losses and a
+commit status returned through a host-mapped ring.
+
+State ownership: a handle's parameters and optimizer slots live on the GPU
+once it has stepped.  `handle.params` / `handle.optimizer.slots` download on
+read (float32 → float64 exactly) and mark the host copy authoritative, so an
+in-place edit made by the caller is uploaded before the next step.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import engine
+from . import runtime as _rt
+from .data import Dataset, batch_at, epoch_permutation, preprocess
+from .engine import ComputationGraph
+from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE
+
+CHECKPOINT_MAGIC = b"PKCK"
+CHECKPOINT_VERSION = 1
+
+
+class PackError(Exception):
+    pass
+
+
+class ReplanNeeded(PackError):
+    """No member can take a step under the current epoch plan."""
+
+
+@dataclass(frozen=True)
+class MLPArch:
+    input_dim: int
+    hidden: tuple
+    classes: int
+    activation: str = "relu"
+
+    @property
+    def dims(self):
+        return (self.input_dim, *self.hidden, self.classes)
+
+
+@dataclass
+class ProgressCursor:
+    steps_done: int = 0
+    epoch_index: int = 0
+    pos: int = 0
+    samples_used: np.ndarray | None = None
+
+    def start_epoch(self, n: int):
+        self.pos = 0
+        self.samples_used = np.zeros(n, dtype=np.int64)
+
+
+def _param_names(model_id, n_layers):
+    out = []
+    for i in range(n_layers):
+        out += [f"{model_id}/L{i}/W", f"{model_id}/L{i}/b"]
+    return out
+
+
+class ModelHandle:
+    """One member: arch, params, optimizer, batch size, target, cursor
+    (packing.py:52-66), with its state mirrored in a device slab."""
+
+    def __init__(self, model_id, arch: MLPArch, graph: ComputationGraph, params: dict,
+                 optimizer: engine.OptimizerState, batch_size: int, target_steps: int,
+                 dataset_binding: str, cursor: ProgressCursor | None = None,
+                 weight_decay: float = 0.0):
+        self.model_id = model_id
+        self.arch = arch
+        self.graph = graph
+        self._params = params
+        self.optimizer = optimizer
+        optimizer._owner = self
+        self.batch_size = batch_size
+        self.target_steps = target_steps
+        self.dataset_binding = dataset_binding
+        self.cursor = cursor if cursor is not None else ProgressCursor()
+        self.weight_decay = float(weight_decay)
+        self._dev = None          # runtime.DeviceMember
+        self._where = "host"      # host | device | synced
+        self._solo = None         # cached singleton pack for standalone_step
+
+    # -- observable state ---------------------------------------------------
+    @property
+    def params(self) -> dict:
+        self._pull()
+        self._host_authoritative()
+        return self._params
+
+    @params.setter
+    def params(self, value):
+        self._pull()
+        self._params = value
+        self._where = "host"
+
+    @property
+    def finished(self) -> bool:
+        return self.cursor.steps_done >= self.target_steps
+
+    @property
+    def n_layers(self):
+        return len(self.arch.hidden) + 1
+
+    def __repr__(self):
+        return (f"ModelHandle(model_id={self.model_id!r}, arch={self.arch!r}, "
+                f"batch_size={self.batch_size}, target_steps={self.target_steps}, "
+                f"steps_done={self.cursor.steps_done})")
+
+    # -- device sync ----------------------------------------------------------
+    def _flat_params(self, params):
+        return np.concatenate([np.asarray(params[n], dtype=np.float64).ravel()
+                               for n in _param_names(self.model_id, self.n_layers)])
+
+    def _flat_slots(self):
+        names = engine.SLOT_NAMES[self.optimizer.kind]
+        slots = self.optimizer._slots
+        if not names or not slots:
+            return None
+        parts = []
+        for s in names:
+            for n in _param_names(self.model_id, self.n_layers):
+                arr = slots.get(n, {}).get(s)
+                parts.append(np.zeros(int(np.prod(self._params[n].shape)))
+                             if arr is None else np.asarray(arr, dtype=np.float64).ravel())
+        return np.concatenate(parts)
+
+    def _device(self, rt) -> "_rt.DeviceMember":
+        """The member's device slab on runtime `rt`, uploaded if stale."""
+        if self._dev is None or self._dev.rt is not rt:
+            if self._dev is not None:
+                self._pull()
+            self._dev = _rt.DeviceMember(rt, self.arch.dims, self.arch.activation,
+                                         self.optimizer.kind, self.optimizer.learning_rate,
+                                         self.batch_size, self.weight_decay)
+            self._where = "host"
+            self._solo = None
+        if self._where == "host":
+            self._dev.upload(self._flat_params(self._params), self._flat_slots(),
+                             self.optimizer._step)
+            self._where = "synced"
+        return self._dev
+
+    def _pull(self):
+        if self._where != "device":
+            return
+        flat, sflat, step = self._dev.download()
+        off = 0
+        for n in _param_names(self.model_id, self.n_layers):
+            a = self._params[n]
+            cnt = a.size
+            np.copyto(a, flat[off:off + cnt].reshape(a.shape))
+            off += cnt
+        self.optimizer._step = int(step)
+        names = engine.SLOT_NAMES[self.optimizer.kind]
+        if names and (step > 0 or self.optimizer._slots):
+            slots = self.optimizer._slots
+            off = 0
+            for s in names:
+                for n in _param_names(self.model_id, self.n_layers):
+                    shape = self._params[n].shape
+                    cnt = int(np.prod(shape))
+                    per = slots.setdefault(n, {})
+                    v = sflat[off:off + cnt].reshape(shape)
+                    if s in per and per[s].shape == shape:
+                        np.copyto(per[s], v)
+                    else:
+                        per[s] = v.copy()
+                    off += cnt
+        self._where = "synced"
+
+    def _host_authoritative(self):
+        if self._where == "synced":
+            self._where = "host"
+
+    def _lr_changed(self):
+        if self._dev is not None:
+            self._dev.set_lr(self.optimizer.learning_rate)
+
+    def _committed(self):
+        self.optimizer._step += 1
+        self._where = "device"
+
+
+def make_handle(model_id, arch: MLPArch, optimizer, learning_rate, batch_size,
+                target_steps, dataset_binding, seed, weight_decay=0.0) -> ModelHandle:
+    """packing.py:69-81; `weight_decay` is the coupled-L2 extension."""
+    if batch_size < 1 or target_steps < 1:
+        raise PackError("batch_size and target_steps must be >= 1")
+    graph = engine.build_mlp(model_id, arch.input_dim, arch.hidden, arch.classes,
+                             arch.activation, dataset_binding)
+    if len(arch.hidden) + 1 > 8:
+        raise PackError("at most 7 hidden layers per member on the device path")
+    return ModelHandle(model_id, arch, graph, engine.init_parameters(graph, seed),
+                       engine.make_optimizer(optimizer, learning_rate), batch_size,
+                       target_steps, dataset_binding, weight_decay=weight_decay)
+
+
+def _fuse(members) -> ComputationGraph:
+    """Merged graph description (packing.py:84-100)."""
+    nodes, ins, labels, outs, heads, shapes = [], {}, {}, {}, {}, {}
+    for h in members:
+        g = h.graph
+        nodes += g.nodes
+        ins.update(g.input_ports)
+        labels.update(g.label_ports)
+        outs.update(g.output_ports)
+        heads.update(g.loss_heads)
+        shapes.update(g.param_shapes)
+    return ComputationGraph("pack(" + ",".join(h.model_id for h in members) + ")",
+                            nodes, ins, labels, outs, heads, shapes)
+
+
+@dataclass
+class PackedModel:
+    members: list
+    fused_graph: ComputationGraph
+    share_inputs: bool = False
+    last_step_stats: dict = field(default_factory=dict)
+    _dev: object = field(default=None, repr=False, compare=False)
+
+    @property
+    def driver_batch(self) -> int:
+        b = [m.batch_size for m in self.members if not m.finished]
+        return max(b) if b else 0
+
+    def member(self, model_id) -> ModelHandle:
+        for h in self.members:
+            if h.model_id == model_id:
+                return h
+        raise PackError(f"unknown model_id {model_id!r}")
+
+    def input_groups(self):
+        """Members partitioned by (dataset, epoch, cursor, batch) (packing.py:121-128)."""
+        g: dict = {}
+        for h in self.members:
+            g.setdefault((h.dataset_binding, h.cursor.epoch_index, h.cursor.pos,
+                          h.batch_size), []).append(h)
+        return [g[k] for k in sorted(g)]
+
+    def pad_slice_plan(self):
+        return {h.model_id: (0, h.batch_size) for h in self.members if not h.finished}
+
+    def _device_pack(self, rt):
+        """The pk_pack over all members (finished ones simply get take=0)."""
+        key = (rt, tuple(id(h) for h in self.members))
+        cached = self._dev
+        devs = [h._device(rt) for h in self.members]
+        if cached is None or cached[0] != key or any(
+                a is not b for a, b in zip(cached[1].members, devs)):
+            self._dev = (key, _rt.DevicePack(rt, devs), {})
+        return self._dev[1]
+
+    def _staging(self, rt, gi, rows, dim):
+        stg = self._dev[2]
+        d = stg.get(gi)
+        if d is None or d.n < rows or d.dim != dim:
+            d = _rt.DeviceDataset(rt, max(rows, self.driver_batch), dim)
+            stg[gi] = d
+        return d
+
+
+def pack_models(handles) -> PackedModel:
+    """packing.py:136-142."""
+    if not handles:
+        raise PackError("pack needs at least one model")
+    ids = [h.model_id for h in handles]
+    if len(set(ids)) != len(ids):
+        raise PackError(f"duplicate model_id in pack: {sorted(ids)}")
+    return PackedModel(members=list(handles), fused_graph=_fuse(handles))
+
+
+def dedup_inputs(packed: PackedModel) -> PackedModel:
+    """Members of one input group share one physical input (packing.py:145-151).
+    On the device every group is always read once; this flag only changes the
+    reported `physical_inputs`, exactly as in the reference."""
+    return replace(packed, share_inputs=True)
+
+
+def _dataset_max_label(rt, ds):
+    key = ("maxlabel", ds.dataset_id, id(ds.labels))
+    v = rt._datasets.get(key)
+    if v is None:
+        v = int(np.max(ds.labels))
+        rt._datasets[key] = v
+    return v
+
+
+def _order_fn(ds, epoch):
+    return lambda: epoch_permutation(ds.dataset_id, ds.n, epoch)
+
+
+def _roll_if_needed(handle: ModelHandle, datasets):
+    """packing.py:175-182."""
+    n = datasets[handle.dataset_binding].n
+    cur = handle.cursor
+    if cur.samples_used is None:
+        cur.start_epoch(n)
+    if cur.pos >= n:
+        cur.epoch_index += 1
+        cur.start_epoch(n)
+
+
+def _node_name(h: ModelHandle, idx: int) -> str:
+    n = h.n_layers
+    if idx == 0:
+        return f"{h.model_id}/in"
+    if idx == 2 * n:
+        return f"{h.model_id}/loss"
+    return f"{h.model_id}/aff{(idx - 1) // 2}" if idx % 2 == 1 else f"{h.model_id}/act{(idx - 2) // 2}"
+
+
+def _grad_name(h: ModelHandle, pos: int) -> str:
+    layer = h.n_layers - 1 - pos // 2
+    return f"{h.model_id}/L{layer}/{'W' if pos % 2 == 0 else 'b'}"
+
+
+class _StepPlan:
+    __slots__ = ("dpack", "index", "takes", "n_groups", "physical", "driver")
+
+
+def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
+    """Host half of a packed step: input groups, batch rows and the per-member
+    device feeds (packing.py:206-239).  Reads cursors, changes nothing."""
+    rt = _rt.runtime()
+    plan = _StepPlan()
+    plan.driver = max(h.batch_size for h in active)
+    groups: dict = {}
+    for h in active:
+        groups.setdefault((h.dataset_binding, h.cursor.epoch_index, h.cursor.pos,
+                           h.batch_size), []).append(h)
+    dpack = packed._device_pack(rt)
+    plan.dpack = dpack
+    plan.index = index = {id(h): k for k, h in enumerate(packed.members)}
+    dpack.clear_feeds()
+    plan.takes = takes = {}
+    physical = 0
+    for gi, key in enumerate(sorted(groups)):
+        grp = groups[key]
+        lead = grp[0]
+        ds: Dataset = datasets[lead.dataset_binding]
+        for h in grp:
+            if ds.dim != h.arch.input_dim:
+                raise engine.ShapeMismatch(f"{h.model_id}/x", ("batch", h.arch.input_dim),
+                                           (plan.driver, ds.dim))
+        cur = lead.cursor
+        take = min(lead.batch_size, ds.n - cur.pos)
+        perm = rt.host_order(ds.dataset_id, ds.n, cur.epoch_index, _order_fn(ds, cur.epoch_index))
+        idx = perm[cur.pos:cur.pos + take]
+        if _dataset_max_label(rt, ds) >= min(h.arch.classes for h in grp):
+            bad = [h for h in grp if int(ds.labels[idx].max()) >= h.arch.classes]
+            if bad:
+                raise IndexError(f"label out of bounds for member {bad[0].model_id!r} "
+                                 f"with {bad[0].arch.classes} classes")
+        if preprocess_spec is not None and preprocess_spec.stages:
+            x, y, idx = batch_at(ds, perm, cur.pos, take)
+            x = preprocess(preprocess_spec, x, idx, ds.dataset_id, cache)
+            stg = packed._staging(rt, gi, take, ds.dim)
+            stg.write(0, x, y)
+            src, order, pos = stg, None, 0
+        else:
+            src = rt.dataset(ds)
+            order = rt.order(ds.dataset_id, ds.n, cur.epoch_index, _order_fn(ds, cur.epoch_index))
+            pos = cur.pos
+        physical += 1 if packed.share_inputs else len(grp)
+        for h in grp:
+            dpack.set_feed(index[id(h)], src, order, pos, take, gi)
+            takes[id(h)] = (idx, take)
+    plan.n_groups = len(groups)
+    plan.physical = physical
+    return plan
+
+
+def _apply_result(packed: PackedModel, active, plan: _StepPlan, code, who, where, losses):
+    """Device status → the reference's exceptions and cursor updates
+    (packing.py:246-257): a forward error commits nothing; a gradient error
+    at member k leaves members before k committed."""
+    if code == PK_ERR_NONFINITE_VALUE:
+        raise engine.EngineError(
+            f"non-finite value at node {_node_name(packed.members[who], where)!r}")
+    out = {}
+    for h in active:
+        k = plan.index[id(h)]
+        if code == PK_ERR_NONFINITE_GRAD and k == who:
+            raise engine.NonFiniteGradient(_grad_name(h, where))
+        h._committed()
+        idx, take = plan.takes[id(h)]
+        h.cursor.steps_done += 1
+        h.cursor.pos += take
+        h.cursor.samples_used[idx] += 1
+        out[h.model_id] = losses[k]
+    return out
+
+
+def _device_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
+    plan = _plan_step(packed, active, datasets, preprocess_spec, cache)
+    code, who, where, _, losses = plan.dpack.step()
+    out = _apply_result(packed, active, plan, code, who, where, losses)
+    return out, plan.n_groups, plan.physical, plan.driver
+
+
+def _active_members(packed, datasets, stop_at_epoch_end):
+    active = [h for h in packed.members if not h.finished]
+    if not stop_at_epoch_end:
+        for h in active:
+            _roll_if_needed(h, datasets)
+    else:
+        for h in active:
+            if h.cursor.samples_used is None:
+                h.cursor.start_epoch(datasets[h.dataset_binding].n)
+        active = [h for h in active if h.cursor.pos < datasets[h.dataset_binding].n]
+    if not active:
+        raise ReplanNeeded("no member has both remaining steps and epoch data")
+    return active
+
+
+def packed_step(packed: PackedModel, datasets, preprocess_spec=None, cache=None,
+                stop_at_epoch_end=False):
+    """Train every active member for exactly one synchronized step
+    (packing.py:185-264).  Returns {model_id: loss}."""
+    active = _active_members(packed, datasets, stop_at_epoch_end)
+    losses, n_groups, physical, driver = _device_step(packed, active, datasets,
+                                                      preprocess_spec, cache)
+    packed.last_step_stats = {"physical_inputs": physical, "groups": n_groups,
+                              "driver_batch": driver}
+    return losses
+
+
+def standalone_step(handle: ModelHandle, datasets, preprocess_spec=None, cache=None):
+    """One unpacked step (packing.py:267-282): the same device kernels on a
+    one-member pack, so a packed member's trajectory equals its standalone
+    one bit for bit."""
+    if handle.finished:
+        raise PackError(f"{handle.model_id}: no remaining steps")
+    _roll_if_needed(handle, datasets)
+    if handle._solo is None or handle._solo.members[0] is not handle:
+        handle._solo = pack_models([handle])
+    losses, _, _, _ = _device_step(handle._solo, [handle], datasets, preprocess_spec, cache)
+    return losses[handle.model_id]
+
+
+def make_epoch_plan(members, datasets):
+    """Phases (driver model_id, steps) covering one epoch (packing.py:285-319)."""
+    if not members:
+        raise PackError("epoch plan needs at least one member")
+    state = {}
+    for h in members:
+        n = datasets[h.dataset_binding].n
+        state[h.model_id] = [h.cursor.pos if h.cursor.samples_used is not None else 0, n]
+    batch = {h.model_id: h.batch_size for h in members}
+    plan = []
+    while any(p < n for p, n in state.values()):
+        live = [mid for mid, (p, n) in state.items() if p < n]
+        driver = min(live, key=lambda mid: (-batch[mid], mid))
+        steps = 0
+        done = False
+        while not done:
+            for mid in live:
+                p, n = state[mid]
+                if p >= n:
+                    continue
+                p += min(batch[mid], n - p)
+                state[mid][0] = p
+                done = done or p >= n
+            steps += 1
+        plan.append((driver, steps))
+    return plan
+
+
+def run_epoch(packed: PackedModel, datasets, preprocess_spec=None, cache=None):
+    """Packed steps until every member's epoch is exhausted (packing.py:322-330)."""
+    out = []
+    while True:
+        try:
+            out.append(packed_step(packed, datasets, preprocess_spec, cache,
+                                   stop_at_epoch_end=True))
+        except ReplanNeeded:
+            return out
+
+
+# ------------------------------------------------------------ checkpoints --
+# PKCK v1, byte-compatible with packing.py:333-417: magic, u32 version,
+# payload, sha256(payload).
+
+@dataclass(frozen=True)
+class Checkpoint:
+    model_id: str
+    payload: bytes
+    digest: bytes
+
+    def to_bytes(self) -> bytes:
+        return CHECKPOINT_MAGIC + struct.pack("<I", CHECKPOINT_VERSION) + self.payload + self.digest
+
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "Checkpoint":
+        if raw[:4] != CHECKPOINT_MAGIC:
+            raise PackError("bad checkpoint magic")
+        (ver,) = struct.unpack_from("<I", raw, 4)
+        if ver != CHECKPOINT_VERSION:
+            raise PackError(f"unsupported checkpoint version {ver}")
+        payload, digest = raw[8:-32], raw[-32:]
+        if hashlib.sha256(payload).digest() != digest:
+            raise PackError("checkpoint digest mismatch")
+        mid, _ = _Reader(payload).str_()
+        return cls(model_id=mid, payload=payload, digest=digest)
+
+
+class _Writer:
+    def __init__(self):
+        self.parts = []
+
+    def raw(self, fmt, *v):
+        self.parts.append(struct.pack(fmt, *v))
+
+    def str_(self, s: str):
+        b = s.encode()
+        self.raw("<H", len(b))
+        self.parts.append(b)
+
+    def tensor(self, a):
+        a = np.asarray(a, dtype=np.float64)
+        self.raw("<B", a.ndim)
+        if a.ndim:
+            self.raw(f"<{a.ndim}Q", *a.shape)
+        self.parts.append(a.astype("<f8").tobytes())
+
+    def bytes(self):
+        return b"".join(self.parts)
+
+
+class _Reader:
+    def __init__(self, buf):
+        self.buf, self.off = buf, 0
+
+    def raw(self, fmt):
+        v = struct.unpack_from(fmt, self.buf, self.off)
+        self.off += struct.calcsize(fmt)
+        return v
+
+    def str_(self):
+        (n,) = self.raw("<H")
+        s = self.buf[self.off:self.off + n].decode()
+        self.off += n
+        return s, self.off
+
+    def tensor(self):
+        (nd,) = self.raw("<B")
+        shape = self.raw(f"<{nd}Q") if nd else ()
+        cnt = int(np.prod(shape)) if shape else 1
+        a = np.frombuffer(self.buf, dtype="<f8", count=cnt, offset=self.off)
+        self.off += 8 * cnt
+        return a.reshape(shape).copy()
+
+
+def checkpoint_model(handle: ModelHandle) -> Checkpoint:
+    """Device → host download into the PKCK payload (packing.py:387-417)."""
+    params = handle.params
+    opt = handle.optimizer
+    w = _Writer()
+    w.str_(handle.model_id)
+    a = handle.arch
+    w.raw("<IIB", a.input_dim, a.classes, len(a.hidden))
+    if a.hidden:
+        w.raw(f"<{len(a.hidden)}I", *a.hidden)
+    w.str_(a.activation)
+    w.str_(handle.dataset_binding)
+    w.raw("<IQ", handle.batch_size, handle.target_steps)
+    w.str_(opt.kind)
+    w.raw("<dQ", opt.learning_rate, opt.step_counter)
+    names = sorted(params)
+    w.raw("<I", len(names))
+    for n in names:
+        w.str_(n)
+        w.tensor(params[n])
+    slots = opt.slots
+    items = [(p, s, slots[p][s]) for p in sorted(slots) for s in sorted(slots[p])]
+    w.raw("<I", len(items))
+    for p, s, arr in items:
+        w.str_(p)
+        w.str_(s)
+        w.tensor(arr)
+    c = handle.cursor
+    w.raw("<QQQ", c.steps_done, c.epoch_index, c.pos)
+    payload = w.bytes()
+    return Checkpoint(handle.model_id, payload, hashlib.sha256(payload).digest())
+
+
+def restore_handle(ckpt: Checkpoint, datasets=None) -> ModelHandle:
+    """packing.py:420-465."""
+    r = _Reader(ckpt.payload)
+    mid, _ = r.str_()
+    input_dim, classes, nh = r.raw("<IIB")
+    hidden = r.raw(f"<{nh}I") if nh else ()
+    act, _ = r.str_()
+    binding, _ = r.str_()
+    batch, target = r.raw("<IQ")
+    kind, _ = r.str_()
+    lr, step = r.raw("<dQ")
+    (np_,) = r.raw("<I")
+    params = {}
+    for _ in range(np_):
+        n, _ = r.str_()
+        params[n] = r.tensor()
+    (ns,) = r.raw("<I")
+    opt = engine.make_optimizer(kind, lr)
+    opt._step = step
+    for _ in range(ns):
+        p, _ = r.str_()
+        s, _ = r.str_()
+        opt._slots.setdefault(p, {})[s] = r.tensor()
+    steps_done, epoch, pos = r.raw("<QQQ")
+    arch = MLPArch(input_dim, tuple(hidden), classes, act)
+    graph = engine.build_mlp(mid, input_dim, tuple(hidden), classes, act, binding)
+    cur = ProgressCursor(steps_done=steps_done, epoch_index=epoch, pos=pos)
+    if datasets is not None and binding in datasets:
+        ds = datasets[binding]
+        cur.samples_used = np.zeros(ds.n, dtype=np.int64)
+        cur.samples_used[epoch_permutation(ds.dataset_id, ds.n, epoch)[:pos]] = 1
+    return ModelHandle(mid, arch, graph, params, opt, batch, target, binding, cur)
+
+
+def free_model(packed: PackedModel, model_id):
+    """Checkpoint one member and drop it from the pack (packing.py:468-478)."""
+    h = packed.member(model_id)
+    rest = [m for m in packed.members if m.model_id != model_id]
+    ckpt = checkpoint_model(h)
+    h._dev = None  # release the member's device slab
+    h._where = "host"
+    h._solo = None
+    return ckpt, PackedModel(members=rest, fused_graph=_fuse(rest),
+                             share_inputs=packed.share_inputs)
+
+
+def load_model(obj, device=None, datasets=None) -> ModelHandle:
+    """Restore a checkpoint (or take a handle) and register its device bytes
+    with an accountant (packing.py:481-489).  `device` is any object with a
+    `register(model_id, nbytes)` method, e.g. device.DeviceAccountant."""
+    h = restore_handle(obj, datasets) if isinstance(obj, Checkpoint) else obj
+    if device is not None:
+        from .device import member_device_bytes
+        device.register(h.model_id, member_device_bytes(h.arch, h.optimizer.kind,
+                                                        h.batch_size, _rt.default_precision()))
+    return h

@@ -1,0 +1,321 @@
+"""Device objects over the C-ABI: runtime (one per process/GPU), resident
+datasets and epoch orders, member slabs and packs.
+
+This is plumbing for `packing.py`; it keeps no numerics of its own.  Every
+call goes to `libpk_b200.so` — if the library or the GPU is missing the
+first use raises (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import weakref
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _lib as L
+
+_RUNTIMES: dict = {}
+_DEFAULT = {"device": None, "dtype": None}
+
+
+def set_device(device: int):
+    """Select the GPU used by subsequently created handles/packs."""
+    _DEFAULT["device"] = int(device)
+
+
+def set_precision(dtype: str):
+    """'f32' (default) or 'f64' device arithmetic for new runtimes."""
+    if dtype not in ("f32", "f64"):
+        raise ValueError("precision must be 'f32' or 'f64'")
+    _DEFAULT["dtype"] = dtype
+
+
+def default_device() -> int:
+    if _DEFAULT["device"] is not None:
+        return _DEFAULT["device"]
+    return int(os.environ.get("PACKTRAIN_DEVICE", "0"))
+
+
+def default_precision() -> str:
+    return _DEFAULT["dtype"] or os.environ.get("PACKTRAIN_PRECISION", "f32")
+
+
+def runtime(device: int | None = None, dtype: str | None = None) -> "Runtime":
+    dev = default_device() if device is None else int(device)
+    dt = dtype or default_precision()
+    key = (dev, dt)
+    rt = _RUNTIMES.get(key)
+    if rt is None:
+        rt = Runtime(dev, dt)
+        _RUNTIMES[key] = rt
+    return rt
+
+
+class Runtime:
+    """One pk_ctx: a device, a precision, a stream and the resident data."""
+
+    ORDER_CACHE = 16
+
+    def __init__(self, device: int, dtype: str):
+        self.lib = L.lib()
+        self.device = device
+        self.dtype = dtype
+        ptr = C.c_void_p()
+        rc = self.lib.pk_ctx_create(device, L.PK_F64 if dtype == "f64" else L.PK_F32,
+                                    C.byref(ptr))
+        if rc != L.PK_OK:
+            raise L.PKError(rc, f"cannot create context on cuda:{device} "
+                                "(is a GPU visible and libpk_b200.so built for sm_100a?)")
+        self.ptr = ptr
+        self._datasets: dict = {}
+        self._orders: OrderedDict = OrderedDict()
+        self._host_orders: OrderedDict = OrderedDict()
+
+    def check(self, rc):
+        return L.check(self.ptr, rc)
+
+    def set_stream(self, stream_handle: int | None):
+        self.check(self.lib.pk_ctx_set_stream(self.ptr, C.c_void_p(stream_handle or 0)))
+
+    def synchronize(self):
+        self.check(self.lib.pk_ctx_synchronize(self.ptr))
+
+    def mem_info(self):
+        f, t, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.check(self.lib.pk_ctx_mem_info(self.ptr, C.byref(f), C.byref(t), C.byref(m)))
+        return f.value, t.value, m.value
+
+    # ---- data -------------------------------------------------------------
+    def dataset(self, ds) -> "DeviceDataset":
+        """Device-resident copy of a reference-style Dataset (uploaded once)."""
+        key = (ds.dataset_id, id(ds.features), ds.features.shape)
+        d = self._datasets.get(key)
+        if d is None:
+            d = DeviceDataset(self, ds.n, ds.dim)
+            d.write(0, ds.features, ds.labels)
+            d._src = weakref.ref(ds.features) if _weakrefable(ds.features) else None
+            self._datasets[key] = d
+        return d
+
+    def host_order(self, dataset_id: str, n: int, epoch: int, make) -> np.ndarray:
+        key = (dataset_id, n, epoch)
+        o = self._host_orders.get(key)
+        if o is None:
+            o = make()
+            self._host_orders[key] = o
+            while len(self._host_orders) > self.ORDER_CACHE:
+                self._host_orders.popitem(last=False)
+        else:
+            self._host_orders.move_to_end(key)
+        return o
+
+    def order(self, dataset_id: str, n: int, epoch: int, make) -> "DeviceOrder":
+        key = (dataset_id, n, epoch)
+        o = self._orders.get(key)
+        if o is None:
+            o = DeviceOrder(self, self.host_order(dataset_id, n, epoch, make))
+            self._orders[key] = o
+            while len(self._orders) > self.ORDER_CACHE:
+                self._orders.popitem(last=False)
+        else:
+            self._orders.move_to_end(key)
+        return o
+
+
+def _weakrefable(a):
+    try:
+        weakref.ref(a)
+        return True
+    except TypeError:
+        return False
+
+
+class DeviceDataset:
+    def __init__(self, rt: Runtime, n: int, dim: int):
+        self.rt, self.n, self.dim = rt, int(n), int(dim)
+        ptr = C.c_void_p()
+        rt.check(rt.lib.pk_dataset_create(rt.ptr, self.n, self.dim, C.byref(ptr)))
+        self.ptr = ptr
+
+    def write(self, row0: int, features, labels):
+        x = np.ascontiguousarray(features, dtype=np.float64)
+        y = np.ascontiguousarray(labels, dtype=np.int64)
+        rows = x.shape[0]
+        self.rt.check(self.rt.lib.pk_dataset_write(
+            self.ptr, int(row0), rows, x.ctypes.data_as(C.c_void_p),
+            y.ctypes.data_as(C.c_void_p)))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.rt.lib.pk_dataset_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class DeviceOrder:
+    def __init__(self, rt: Runtime, perm: np.ndarray):
+        self.rt = rt
+        p = np.ascontiguousarray(perm, dtype=np.int64)
+        self.n = len(p)
+        ptr = C.c_void_p()
+        rt.check(rt.lib.pk_order_create(rt.ptr, p.ctypes.data_as(C.c_void_p), self.n,
+                                        C.byref(ptr)))
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.rt.lib.pk_order_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class DeviceMember:
+    """A member's device slab: ping-pong params/slots, workspace, control."""
+
+    def __init__(self, rt: Runtime, dims, activation: str, optimizer: str, lr: float,
+                 max_rows: int, weight_decay: float = 0.0):
+        if len(dims) - 1 > L.PK_MAX_LAYERS:
+            raise ValueError(f"at most {L.PK_MAX_LAYERS} affine layers per member")
+        self.rt = rt
+        d = L.MemberDesc()
+        d.n_layers = len(dims) - 1
+        for i, v in enumerate(dims):
+            d.dims[i] = int(v)
+        d.activation = L.ACT_CODES[activation]
+        d.optimizer = L.OPT_CODES[optimizer]
+        d.learning_rate = float(lr)
+        d.weight_decay = float(weight_decay)
+        d.max_rows = int(max_rows)
+        ptr = C.c_void_p()
+        rt.check(rt.lib.pk_member_create(rt.ptr, C.byref(d), C.byref(ptr)))
+        self.ptr = ptr
+        self.desc = d
+        self.n_params = rt.lib.pk_member_param_count(ptr)
+        self.n_slots = rt.lib.pk_member_slot_count(ptr)
+        self.device_bytes = rt.lib.pk_member_device_bytes(ptr)
+
+    def inject_fault(self, grad_position: int):
+        """Testing hook: NaN in gradient tensor `grad_position` next step."""
+        self.rt.check(self.rt.lib.pk_member_inject_fault(self.ptr, int(grad_position)))
+
+    def set_lr(self, lr: float):
+        self.rt.check(self.rt.lib.pk_member_set_lr(self.ptr, float(lr)))
+
+    def upload(self, flat_params: np.ndarray, flat_slots, step_counter: int):
+        p = np.ascontiguousarray(flat_params, dtype=np.float64)
+        assert p.size == self.n_params
+        sp = None
+        if flat_slots is not None and self.n_slots:
+            s = np.ascontiguousarray(flat_slots, dtype=np.float64)
+            assert s.size == self.n_slots * self.n_params
+            sp = s.ctypes.data_as(C.c_void_p)
+        self.rt.check(self.rt.lib.pk_member_set_state(
+            self.ptr, p.ctypes.data_as(C.c_void_p), sp, int(step_counter)))
+
+    def download(self, want_slots=True):
+        p = np.empty(self.n_params, dtype=np.float64)
+        s = np.empty(self.n_slots * self.n_params, dtype=np.float64) if (
+            want_slots and self.n_slots) else None
+        t = C.c_int64()
+        self.rt.check(self.rt.lib.pk_member_get_state(
+            self.ptr, p.ctypes.data_as(C.c_void_p),
+            s.ctypes.data_as(C.c_void_p) if s is not None else None, C.byref(t)))
+        return p, s, t.value
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.rt.lib.pk_member_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class DevicePack:
+    """pk_pack over an ordered list of DeviceMembers (kept alive here)."""
+
+    def __init__(self, rt: Runtime, members):
+        self.rt = rt
+        self.members = list(members)  # keep member slabs alive
+        self.K = len(self.members)
+        arr = (C.c_void_p * self.K)(*[m.ptr.value for m in self.members])
+        ptr = C.c_void_p()
+        rt.check(rt.lib.pk_pack_create(rt.ptr, arr, self.K, C.byref(ptr)))
+        self.ptr = ptr
+        self._feeds = (L.Feed * self.K)()
+        self._losses = (C.c_double * self.K)()
+        self._status = L.Status()
+        self.launches = rt.lib.pk_pack_launches_per_step(ptr)
+
+    def set_feed(self, k, ddata, dorder, pos, take, group=0):
+        f = self._feeds[k]
+        f.data = ddata.ptr.value if ddata is not None else None
+        f.order = dorder.ptr.value if dorder is not None else None
+        f.pos = int(pos)
+        f.take = int(take)
+        f.group = int(group)
+
+    def clear_feeds(self):
+        for k in range(self.K):
+            self._feeds[k].take = 0
+            self._feeds[k].data = None
+            self._feeds[k].order = None
+
+    def step(self):
+        """Synchronous step: returns (status code, member, index, committed, losses)."""
+        rc = self.rt.lib.pk_pack_step(self.ptr, self._feeds, self._losses,
+                                      C.byref(self._status))
+        if rc not in (L.PK_OK, L.PK_ERR_NONFINITE_VALUE, L.PK_ERR_NONFINITE_GRAD):
+            self.rt.check(rc)
+        st = self._status
+        return st.code, st.member, st.index, st.committed, list(self._losses)
+
+    def step_async(self) -> int:
+        t = C.c_int64()
+        self.rt.check(self.rt.lib.pk_pack_step_async(self.ptr, self._feeds, C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int):
+        rc = self.rt.lib.pk_pack_step_wait(self.ptr, int(ticket), self._losses,
+                                           C.byref(self._status))
+        if rc not in (L.PK_OK, L.PK_ERR_NONFINITE_VALUE, L.PK_ERR_NONFINITE_GRAD):
+            self.rt.check(rc)
+        st = self._status
+        return st.code, st.member, st.index, st.committed, list(self._losses)
+
+    def profile(self):
+        """One real step, un-graphed, timed per phase with CUDA events.
+        Returns (status code, [(kind, layer, ctas, ms)], losses)."""
+        n = self.launches
+        ms = (C.c_float * n)()
+        kind, layer, ctas = (C.c_int32 * n)(), (C.c_int32 * n)(), (C.c_int32 * n)()
+        rc = self.rt.lib.pk_pack_profile_step(self.ptr, self._feeds, ms, kind, layer, ctas,
+                                              self._losses, C.byref(self._status))
+        if rc not in (L.PK_OK, L.PK_ERR_NONFINITE_VALUE, L.PK_ERR_NONFINITE_GRAD):
+            self.rt.check(rc)
+        phases = [(kind[i], layer[i], ctas[i], ms[i]) for i in range(n)]
+        return self._status.code, phases, list(self._losses)
+
+    def eval(self, ddata, dorder, pos, rows):
+        rc = self.rt.lib.pk_pack_eval(self.ptr, ddata.ptr,
+                                      dorder.ptr if dorder is not None else None,
+                                      int(pos), int(rows), self._losses,
+                                      C.byref(self._status))
+        if rc not in (L.PK_OK, L.PK_ERR_NONFINITE_VALUE):
+            self.rt.check(rc)
+        st = self._status
+        return st.code, st.member, st.index, list(self._losses)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.rt.lib.pk_pack_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass

@@ -1,0 +1,85 @@
+"""Shared test helpers: lockstep device-vs-oracle comparison."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import mlp64 as O
+
+# fp32 device vs float64 oracle, one step from identical state
+# (BASELINE north_star: "rel 1e-4 per step"; SURVEY §8c absolute floor 1e-6)
+RTOL, ATOL = 1e-4, 1e-6
+
+
+def has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def oracle_dataset(ds, round32=True):
+    x = f32(ds.features) if round32 else ds.features
+    return O.OracleDataset(ds.dataset_id, x, ds.labels)
+
+
+def oracle_from_handle(h):
+    """An OracleMember holding exactly the handle's current device state."""
+    params = h.params
+    n = len(h.arch.hidden) + 1
+    layers = [[params[f"{h.model_id}/L{i}/W"].copy(), params[f"{h.model_id}/L{i}/b"].copy()]
+              for i in range(n)]
+    slots = {}
+    for pname, d in h.optimizer.slots.items():
+        i = int(pname.split("/L")[1].split("/")[0])
+        which = pname.rsplit("/", 1)[1]
+        slots[(i, which)] = {k: v.copy() for k, v in d.items()}
+    c = h.cursor
+    m = O.OracleMember(h.model_id, h.arch.dims, h.arch.activation, h.optimizer.kind,
+                       h.optimizer.learning_rate, h.batch_size, h.target_steps,
+                       h.dataset_binding, layers, slots, h.optimizer.step_counter,
+                       c.steps_done, c.epoch_index, c.pos,
+                       None if c.samples_used is None else c.samples_used.copy(),
+                       weight_decay=h.weight_decay)
+    return m
+
+
+def assert_close_member(h, m, rtol=RTOL, atol=ATOL, what=""):
+    p = h.params
+    for i, (w, b) in enumerate(m.layers):
+        for name, ref in ((f"{h.model_id}/L{i}/W", w), (f"{h.model_id}/L{i}/b", b)):
+            got = p[name]
+            err = np.abs(got - ref) - (rtol * np.abs(ref) + atol)
+            assert err.max() <= 0, f"{what} {name}: worst excess {err.max():.3e}"
+    for (i, which), d in m.slots.items():
+        for sname, ref in d.items():
+            got = h.optimizer.slots[f"{h.model_id}/L{i}/{which}"][sname]
+            err = np.abs(got - ref) - (rtol * np.abs(ref) + atol)
+            assert err.max() <= 0, f"{what} slot {i}{which}/{sname}: excess {err.max():.3e}"
+    assert h.optimizer.step_counter == m.t
+    assert h.cursor.steps_done == m.steps_done
+    assert h.cursor.pos == m.pos and h.cursor.epoch_index == m.epoch
+
+
+def lockstep(packed, datasets, steps, share_inputs=True, packing=None):
+    """Run `steps` packed steps; before each, load the oracle with the
+    device's exact state and compare one step (losses, params, slots,
+    cursors, stats)."""
+    odata = {k: oracle_dataset(v) for k, v in datasets.items()}
+    for s in range(steps):
+        oms = [oracle_from_handle(h) for h in packed.members]
+        try:
+            want, wstats = O.oracle_packed_step(oms, odata, share_inputs=share_inputs)
+        except StopIteration:
+            return
+        got = packing.packed_step(packed, datasets)
+        assert set(got) == set(want)
+        for k in want:
+            assert abs(got[k] - want[k]) <= RTOL * abs(want[k]) + ATOL, (s, k, got[k], want[k])
+        assert packed.last_step_stats == wstats
+        for h, m in zip(packed.members, oms):
+            assert_close_member(h, m, what=f"step {s}")

@@ -218,8 +218,24 @@ def micro_tuning(data, tuner):
         json.dump(out, fh, sort_keys=True)
 
 
+def checkpoints(data, packing):
+    """PKCK bytes of a fresh handle and of one after 7 Adam steps
+    (tests/test_pack.py:197-215 scenario)."""
+    ds = data.synth_dataset(120, 6, 3, seed=0)
+    arch = packing.MLPArch(6, (8,), 3)
+    fresh = packing.make_handle("m", arch, "adam", 0.001, 10, 30, "d", 0)
+    h = packing.make_handle("m", arch, "adam", 0.001, 10, 30, "d", 0)
+    for _ in range(7):
+        packing.standalone_step(h, {"d": ds})
+    with open(os.path.join(HERE, "ckpt_fresh.pkck"), "wb") as fh:
+        fh.write(packing.checkpoint_model(fresh).to_bytes())
+    with open(os.path.join(HERE, "ckpt_adam7.pkck"), "wb") as fh:
+        fh.write(packing.checkpoint_model(h).to_bytes())
+
+
 def main():
     data, engine, packing, tuner = _ref()
+    checkpoints(data, packing)
     known_answers(engine)
     config0(data, packing)
     small_pairs(data, packing, engine)

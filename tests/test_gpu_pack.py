@@ -1,0 +1,453 @@
+"""GPU parity of the packed train step (runs on a B200).
+
+Two kinds of checks, mirroring the reference's test strategy:
+  * lockstep parity: before every step the float64 oracle is loaded with the
+    device's exact state and both take one step; losses, params, optimizer
+    slots, cursors and stats must agree to rel 1e-4 + abs 1e-6 (fp32 device
+    vs f64 oracle, BASELINE north_star).  Integer/indexing state is exact.
+  * self-consistency, exact: packed == standalone, gradient isolation and
+    dedup are bit-identical on the device (tests/test_pack.py:31-82).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from _helpers import (ATOL, RTOL, assert_close_member, has_gpu, lockstep, oracle_dataset,
+                      oracle_from_handle)
+from oracle import mlp64 as O
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+from paper_2002_02885_b200 import data, engine, packing, runtime, tuner  # noqa: E402
+
+ARCH = packing.MLPArch(input_dim=6, hidden=(8,), classes=3)
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _ds(n=120, seed=0, d=6, c=3):
+    return {"d": data.synth_dataset(n, d, c, seed=seed)}
+
+
+def _h(mid, batch=10, steps=20, opt="sgd", lr=0.05, seed=0, arch=ARCH, binding="d"):
+    return packing.make_handle(mid, arch, opt, lr, batch, steps, binding, seed)
+
+
+def _maxdiff(a, b):
+    return max(float(np.max(np.abs(a.params[k] - b.params[k]))) for k in a.params)
+
+
+# ------------------------------------------------------- oracle parity --
+
+def test_config0_lockstep_three_steps():
+    """BASELINE configs[0]: K=2 784-256-10, SGD 0.1 / 0.01, b=32."""
+    ds = data.synth_dataset(10000, 784, 10, seed=0)
+    arch = packing.MLPArch(784, (256,), 10, "relu")
+    hs = [packing.make_handle(f"m{i}", arch, "sgd", lr, 32, 100, "train", 0)
+          for i, lr in ((0, 0.1), (1, 0.01))]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, {"train": ds}, 3, packing=packing)
+    z = np.load(os.path.join(G, "config0.npz"))
+    assert packed.last_step_stats == {"physical_inputs": 1, "groups": 1, "driver_batch": 32}
+    # the first-step losses agree with the reference's own numbers
+    hs2 = [packing.make_handle(f"m{i}", arch, "sgd", lr, 32, 100, "train", 0)
+           for i, lr in ((0, 0.1), (1, 0.01))]
+    out = packing.packed_step(packing.dedup_inputs(packing.pack_models(hs2)), {"train": ds})
+    np.testing.assert_allclose([out["m0"], out["m1"]], z["losses"][0], rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("opt", engine.OPTIMIZERS)
+@pytest.mark.parametrize("act", engine.ACTIVATIONS)
+def test_small_pair_lockstep(opt, act):
+    arch = packing.MLPArch(6, (8,), 3, act)
+    hs = [_h("a", opt=opt, seed=1, arch=arch), _h("b", opt=opt, lr=0.01, seed=2, arch=arch)]
+    lockstep(packing.dedup_inputs(packing.pack_models(hs)), _ds(), 6, packing=packing)
+
+
+@pytest.mark.parametrize("opt", engine.OPTIMIZERS)
+def test_deep_ragged_pack_lockstep(opt):
+    """Members of different depth/width/activation/optimizer in one pack."""
+    datasets = _ds(n=300, d=5, seed=8)
+    hs = [packing.make_handle("deep", packing.MLPArch(5, (8, 8, 7), 3, "tanh"), opt, 0.01,
+                              16, 50, "d", 1),
+          packing.make_handle("wide", packing.MLPArch(5, (40,), 3, "sigmoid"), "adam", 0.003,
+                              16, 50, "d", 2),
+          packing.make_handle("lin", packing.MLPArch(5, (), 3, "relu"), "momentum", 0.02, 9,
+                              50, "d", 3)]
+    lockstep(packing.dedup_inputs(packing.pack_models(hs)), datasets, 8, packing=packing)
+
+
+def test_wide_layers_cross_tile_boundaries():
+    """Dims not multiples of the tile sizes, batch > one row tile."""
+    datasets = _ds(n=500, d=77, c=13, seed=3)
+    hs = [packing.make_handle("x", packing.MLPArch(77, (45, 33), 13, "leaky_relu"), "adam",
+                              0.002, 70, 20, "d", 1),
+          packing.make_handle("y", packing.MLPArch(77, (130,), 13, "relu"), "adagrad", 0.05,
+                              37, 20, "d", 2)]
+    lockstep(packing.pack_models(hs), datasets, 5, share_inputs=False, packing=packing)
+
+
+def test_misaligned_batches_coverage_and_parity():
+    """tests/test_pack.py:113-138 + per-step oracle parity."""
+    n = 1000
+    datasets = {"d": data.synth_dataset(n, 6, 3, seed=4)}
+    specs = [("m20", 20, 50), ("m50", 50, 20), ("m100", 100, 10)]
+    members = [_h(mid, batch=b, steps=s, seed=i) for i, (mid, b, s) in enumerate(specs)]
+    packed = packing.pack_models(members)
+    lockstep(packed, datasets, 10, share_inputs=False, packing=packing)
+    assert members[2].finished
+    assert members[1].cursor.pos == n // 2
+    while any(not h.finished for h in members):
+        packing.packed_step(packed, datasets)
+    for h, (mid, b, s) in zip(members, specs):
+        assert h.cursor.steps_done == s
+        np.testing.assert_array_equal(h.cursor.samples_used, 1)
+    z = np.load(os.path.join(G, "deep_misaligned.npz"))
+    for h in members:  # whole trajectory vs the reference (fp32 drift bound)
+        flat = h._flat_params(h.params)
+        np.testing.assert_allclose(flat, z[f"mis_{h.model_id}"], rtol=1e-3, atol=1e-4)
+
+
+def test_golden_trajectories_f32():
+    """5 packed steps from the reference's init vs its golden params."""
+    z = np.load(os.path.join(G, "small_pairs.npz"))
+    for opt in engine.OPTIMIZERS:
+        arch = packing.MLPArch(6, (8,), 3, "tanh")
+        a = _h("a", opt=opt, seed=1, arch=arch)
+        b = _h("b", opt=opt, lr=0.01, seed=2, arch=arch)
+        packed = packing.dedup_inputs(packing.pack_models([a, b]))
+        ls = [list(packing.packed_step(packed, _ds()).values()) for _ in range(5)]
+        np.testing.assert_allclose(ls, z[f"{opt}_tanh_losses"], rtol=1e-3, atol=1e-5)
+        np.testing.assert_allclose(b._flat_params(b.params), z[f"{opt}_tanh_b_p5"],
+                                   rtol=1e-3, atol=1e-5)
+
+
+# ------------------------------------------------ exact self-consistency --
+
+def test_singleton_pack_matches_standalone_exactly():
+    datasets = _ds()
+    ph, solo = _h("m", seed=3), _h("m", seed=3)
+    packed = packing.pack_models([ph])
+    for _ in range(20):
+        packing.packed_step(packed, datasets)
+        packing.standalone_step(solo, datasets)
+    assert _maxdiff(ph, solo) == 0.0
+
+
+@pytest.mark.parametrize("opt", engine.OPTIMIZERS)
+def test_packed_pair_reproduces_standalone_bitwise(opt):
+    datasets = _ds()
+    pa, pb = _h("a", opt=opt, seed=1), _h("b", opt=opt, seed=2)
+    sa, sb = _h("a", opt=opt, seed=1), _h("b", opt=opt, seed=2)
+    packed = packing.pack_models([pa, pb])
+    for _ in range(20):
+        packing.packed_step(packed, datasets)
+    for _ in range(20):
+        packing.standalone_step(sa, datasets)
+        packing.standalone_step(sb, datasets)
+    assert _maxdiff(pa, sa) == 0.0 and _maxdiff(pb, sb) == 0.0
+
+
+def test_gradient_isolation_members_do_not_interact():
+    datasets = _ds()
+    alone, with_b = _h("a", seed=1), _h("a", seed=1)
+    packed = packing.pack_models([with_b, _h("b", batch=7, seed=9, opt="adam", lr=0.001)])
+    packing.standalone_step(alone, datasets)
+    packing.packed_step(packed, datasets)
+    assert _maxdiff(alone, with_b) == 0.0
+
+
+def test_k_invariance_large_pack():
+    """A member's trajectory is bit-identical inside a 16-member pack."""
+    datasets = {"t": data.synth_dataset(2000, 64, 10, seed=5)}
+    arch = packing.MLPArch(64, (96,), 10, "relu")
+    hs = [packing.make_handle(f"k{i}", arch, ("sgd", "adam", "momentum", "adagrad")[i % 4],
+                              0.01 * (1 + i % 3), 32 + 4 * (i % 3), 30, "t", i)
+          for i in range(16)]
+    solo = packing.make_handle("k5", arch, "adam", 0.01 * (1 + 5 % 3), 32 + 4 * (5 % 3), 30,
+                               "t", 5)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    for _ in range(12):
+        packing.packed_step(packed, datasets)
+        packing.standalone_step(solo, datasets)
+    assert _maxdiff(hs[5], solo) == 0.0
+
+
+def test_dedup_inputs_is_value_preserving_and_collapses_transfers():
+    datasets = _ds()
+    plain = [_h("a", seed=1), _h("b", seed=2)]
+    deduped = [_h("a", seed=1), _h("b", seed=2)]
+    p1, p2 = packing.pack_models(plain), packing.dedup_inputs(packing.pack_models(deduped))
+    for _ in range(10):
+        packing.packed_step(p1, datasets)
+        packing.packed_step(p2, datasets)
+    assert p1.last_step_stats["physical_inputs"] == 2
+    assert p2.last_step_stats["physical_inputs"] == 1
+    for a, b in zip(plain, deduped):
+        assert _maxdiff(a, b) == 0.0
+
+
+# --------------------------------------------------------- pack semantics --
+
+def test_driver_batch_tracks_largest_active_member():
+    datasets = _ds(n=100)
+    big, small = _h("big", batch=50, steps=2), _h("small", batch=10, steps=10)
+    packed = packing.pack_models([big, small])
+    packing.packed_step(packed, datasets)
+    assert packed.last_step_stats["driver_batch"] == 50
+    packing.packed_step(packed, datasets)
+    assert big.finished
+    packing.packed_step(packed, datasets)
+    assert packed.driver_batch == 10 and packed.last_step_stats["driver_batch"] == 10
+
+
+def test_partial_final_batch_never_spans_epochs():
+    datasets = _ds(n=25)
+    h = _h("m", batch=10, steps=6)
+    packed = packing.pack_models([h])
+    for _ in range(3):
+        packing.packed_step(packed, datasets)
+    assert h.cursor.pos == 25 and h.cursor.epoch_index == 0
+    packing.packed_step(packed, datasets)
+    assert h.cursor.epoch_index == 1 and h.cursor.pos == 10
+
+
+def test_run_epoch_and_replan():
+    datasets = _ds(n=100)
+    members = [_h("a", batch=50, steps=100), _h("b", batch=20, steps=100)]
+    plan = packing.make_epoch_plan(members, datasets)
+    losses = packing.run_epoch(packing.pack_models(members), datasets)
+    assert len(losses) == sum(s for _, s in plan)
+    for h in members:
+        np.testing.assert_array_equal(h.cursor.samples_used, 1)
+
+
+def test_finished_members_are_left_alone():
+    datasets = _ds()
+    done, working = _h("done", steps=1), _h("working", steps=3)
+    packed = packing.pack_models([done, working])
+    packing.packed_step(packed, datasets)
+    frozen = {k: v.copy() for k, v in done.params.items()}
+    packing.packed_step(packed, datasets)
+    for k in frozen:
+        np.testing.assert_array_equal(done.params[k], frozen[k])
+    working.cursor.steps_done = working.target_steps
+    with pytest.raises(packing.ReplanNeeded):
+        packing.packed_step(packed, datasets)
+
+
+def test_host_edit_of_params_is_uploaded():
+    datasets = _ds()
+    a, b = _h("a", seed=1), _h("a", seed=1)
+    pa = packing.pack_models([a])
+    packing.packed_step(pa, datasets)
+    packing.standalone_step(b, datasets)
+    a.params["a/L0/W"][0, 0] += 0.5  # in-place edit, as reference users do
+    b.params["a/L0/W"][0, 0] += 0.5
+    packing.packed_step(pa, datasets)
+    packing.standalone_step(b, datasets)
+    assert _maxdiff(a, b) == 0.0
+
+
+# ------------------------------------------------------------ failures --
+
+def test_nonfinite_input_raises_engine_error_and_commits_nothing():
+    ds = data.synth_dataset(120, 6, 3, seed=0)
+    x = ds.features.copy()
+    perm = data.epoch_permutation(ds.dataset_id, ds.n, 0)
+    x[perm[3], 2] = np.nan
+    bad = data.Dataset(ds.dataset_id + "-nan", x, ds.labels, 3)
+    a, b = _h("a", seed=1), _h("b", seed=2)
+    packed = packing.pack_models([a, b])
+    before = {k: v.copy() for k, v in a.params.items()}
+    with pytest.raises(engine.EngineError, match="non-finite value at node 'a/in'"):
+        packing.packed_step(packed, {"d": bad})
+    assert a.cursor.steps_done == 0 and a.optimizer.step_counter == 0
+    for k in before:
+        np.testing.assert_array_equal(a.params[k], before[k])
+
+
+def test_nonfinite_param_names_the_affine_node():
+    a = _h("a", seed=1)
+    a.params["a/L1/W"][0, 0] = np.inf
+    with pytest.raises(engine.EngineError, match="a/aff1"):
+        packing.packed_step(packing.pack_models([a]), _ds())
+
+
+def test_nonfinite_gradient_commit_rules():
+    """engine.py:297-299 + packing.py:250-253: members before the bad one
+    commit, the bad one and later ones do not; counters stay put."""
+    datasets = _ds()
+    a, b, c = _h("a", seed=1), _h("b", seed=2), _h("c", seed=3)
+    sa = _h("a", seed=1)
+    packed = packing.pack_models([a, b, c])
+    rt = runtime.runtime()
+    packed._device_pack(rt)
+    pb = {k: v.copy() for k, v in b.params.items()}
+    pc = {k: v.copy() for k, v in c.params.items()}
+    b._dev.inject_fault(2)  # grads order: L1/W, L1/b, L0/W, L0/b → "b/L0/W"
+    with pytest.raises(engine.NonFiniteGradient) as err:
+        packing.packed_step(packed, datasets)
+    assert err.value.param == "b/L0/W"
+    packing.standalone_step(sa, datasets)
+    assert _maxdiff(a, sa) == 0.0 and a.optimizer.step_counter == 1
+    assert a.cursor.steps_done == 1
+    assert b.optimizer.step_counter == 0 and b.cursor.steps_done == 0
+    assert c.optimizer.step_counter == 0 and c.cursor.steps_done == 0
+    for k in pb:
+        np.testing.assert_array_equal(b.params[k], pb[k])
+    for k in pc:
+        np.testing.assert_array_equal(c.params[k], pc[k])
+    # the fault is one-shot: the next step succeeds for b and c
+    out = packing.packed_step(packed, datasets)
+    assert set(out) == {"a", "b", "c"}
+
+
+def test_shape_mismatch_names_the_port():
+    h = packing.make_handle("m", packing.MLPArch(5, (4,), 3), "sgd", 0.1, 4, 2, "d", 0)
+    with pytest.raises(engine.ShapeMismatch) as err:
+        packing.packed_step(packing.pack_models([h]), _ds())
+    assert err.value.port == "m/x"
+
+
+# ---------------------------------------------------------- checkpoints --
+
+def test_checkpoint_round_trip_is_exact():
+    datasets = _ds()
+    h = _h("m", opt="adam", lr=0.001, steps=30)
+    for _ in range(7):
+        packing.standalone_step(h, datasets)
+    raw = packing.checkpoint_model(h).to_bytes()
+    back = packing.restore_handle(packing.Checkpoint.from_bytes(raw), datasets)
+    assert back.optimizer.step_counter == 7 and back.cursor.pos == h.cursor.pos
+    for k in h.params:
+        np.testing.assert_array_equal(back.params[k], h.params[k])
+    for p in h.optimizer.slots:
+        for s in h.optimizer.slots[p]:
+            np.testing.assert_array_equal(back.optimizer.slots[p][s], h.optimizer.slots[p][s])
+
+
+def test_free_load_resume_equals_uninterrupted():
+    datasets = _ds()
+    interrupted = _h("m", opt="momentum", steps=40, seed=5)
+    straight = _h("m", opt="momentum", steps=40, seed=5)
+    packed = packing.pack_models([interrupted])
+    for _ in range(15):
+        packing.packed_step(packed, datasets)
+    ckpt, packed = packing.free_model(packed, "m")
+    assert packed.members == []
+    resumed = packing.load_model(packing.Checkpoint.from_bytes(ckpt.to_bytes()),
+                                 datasets=datasets)
+    packed = packing.pack_models([resumed])
+    while not resumed.finished:
+        packing.packed_step(packed, datasets)
+    while not straight.finished:
+        packing.standalone_step(straight, datasets)
+    assert _maxdiff(resumed, straight) == 0.0
+
+
+def test_mid_pack_replacement_scenario():
+    datasets = _ds(n=200)
+    short = _h("short", batch=20, steps=10, seed=1)
+    long_p, long_s = _h("long", batch=10, steps=40, seed=2), _h("long", batch=10, steps=40, seed=2)
+    packed = packing.pack_models([short, long_p])
+    for _ in range(10):
+        packing.packed_step(packed, datasets)
+    assert short.finished and not long_p.finished
+    ckpt, packed = packing.free_model(packed, "short")
+    newcomer = _h("late", batch=30, steps=15, seed=3)
+    packed = packing.pack_models(packed.members + [newcomer])
+    while any(not h.finished for h in packed.members):
+        packing.packed_step(packed, datasets)
+    assert long_p.cursor.steps_done == 40 and newcomer.cursor.steps_done == 15
+    while not long_s.finished:
+        packing.standalone_step(long_s, datasets)
+    assert _maxdiff(long_p, long_s) == 0.0
+
+
+def test_preprocessing_inside_pack_matches_standalone():
+    datasets = _ds()
+    spec = data.PreprocessSpec(stages=(("normalize", 0.5, 2.0), ("jitter", 7)))
+    cache = data.PreprocessCache()
+    pa, sa = _h("a", seed=1), _h("a", seed=1)
+    packed = packing.dedup_inputs(packing.pack_models([pa, _h("b", seed=2)]))
+    for _ in range(5):
+        packing.packed_step(packed, datasets, preprocess_spec=spec, cache=cache)
+        packing.standalone_step(sa, datasets, preprocess_spec=spec, cache=cache)
+    assert _maxdiff(pa, sa) == 0.0
+    assert cache.hits > 0
+
+
+# ------------------------------------------------------------ f64 mode --
+
+def test_f64_context_reproduces_reference_golden_to_1e10():
+    """With a float64 device context the B200 path reproduces the reference's
+    own trajectories (tests/golden/small_pairs.npz) to ~1e-12."""
+    z = np.load(os.path.join(G, "small_pairs.npz"))
+    runtime.set_precision("f64")
+    try:
+        for opt in engine.OPTIMIZERS:
+            for act in engine.ACTIVATIONS:
+                arch = packing.MLPArch(6, (8,), 3, act)
+                a = _h("a", opt=opt, seed=1, arch=arch)
+                b = _h("b", opt=opt, lr=0.01, seed=2, arch=arch)
+                packed = packing.dedup_inputs(packing.pack_models([a, b]))
+                ls = [list(packing.packed_step(packed, _ds()).values()) for _ in range(5)]
+                np.testing.assert_allclose(ls, z[f"{opt}_{act}_losses"], rtol=1e-10, atol=1e-13)
+                np.testing.assert_allclose(b._flat_params(b.params), z[f"{opt}_{act}_b_p5"],
+                                           rtol=1e-10, atol=1e-13)
+    finally:
+        runtime.set_precision("f32")
+
+
+# ------------------------------------------------------ device memory --
+
+def test_member_device_bytes_matches_allocation():
+    from paper_2002_02885_b200 import device
+    rt = runtime.runtime()
+    for arch, opt, b in [(ARCH, "sgd", 10), (packing.MLPArch(784, (256,), 10), "adam", 32),
+                         (packing.MLPArch(5, (8, 8, 7), 3), "momentum", 17)]:
+        m = runtime.DeviceMember(rt, arch.dims, arch.activation, opt, 0.1, b)
+        assert m.device_bytes == device.member_device_bytes(arch, opt, b)
+
+
+# ------------------------------------------------------------- tuning --
+
+def test_val_loss_matches_oracle():
+    ds = data.synth_dataset(300, 5, 3, seed=30)
+    ex = tuner.B200Executor(ds, hidden=(6,), seed=0)
+    space = tuner.ConfigSpace()
+    cfgs = [space.config(i) for i in (3, 100, 555)]
+    hs = [ex._handle(c) for c in cfgs]
+    got = ex.val_losses(hs)
+    vx = oracle_dataset(ex.val).features
+    for h, g in zip(hs, got):
+        m = oracle_from_handle(h)
+        want, _ = O.member_forward_loss(m.layers, m.act, vx, ex.val.labels)
+        assert abs(g - want) <= RTOL * abs(want) + ATOL
+
+
+def test_engine_micro_tuning_matches_reference_records():
+    """Acceptance C10 on the device: original and knn agree per config
+    (<= 1e-6), and both agree with the reference's own records."""
+    ref = json.load(open(os.path.join(G, "tuning.json")))
+    dataset = data.synth_dataset(120, 5, 3, seed=30)
+    space = tuner.ConfigSpace(batch_sizes=(10, 20, 30), optimizers=("sgd", "adam"),
+                              learning_rates=(1e-3, 1e-2), activations=("relu", "tanh"))
+    res = {}
+    for strategy in ("original", "knn"):
+        ex = tuner.B200Executor(dataset, hidden=(6,), seed=0)
+        res[strategy] = tuner.packed_hyperband(4, 2, ex, seed=0, strategy=strategy, space=space)
+    by = {(r.bracket, r.rung, r.config_id): r.loss for r in res["original"].records}
+    for r in res["knn"].records:
+        assert abs(r.loss - by[(r.bracket, r.rung, r.config_id)]) <= 1e-6
+    assert res["knn"].best_config.config_id == res["original"].best_config.config_id
+    for strategy in ("original", "knn"):
+        want = {(b, ru, c): loss for b, ru, g, c, e, loss in ref[strategy]["records"]}
+        for r in res[strategy].records:
+            w = want[(r.bracket, r.rung, r.config_id)]
+            assert abs(r.loss - w) <= 1e-3 * abs(w) + 1e-4
+        assert res[strategy].best_config.config_id == ref[strategy]["best"]
