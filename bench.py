@@ -64,32 +64,64 @@ def _make(wl, data, packing, seed=0):
     return {"train": ds}, hs
 
 
-def _phase_bytes(wl, kind, layer, es=4):
-    """Algorithmic HBM bytes of one phase launch: every
-    tensor the phase must touch, once; the shared input rows once per group."""
+TK = ("FWD", "TAIL", "HEAD", "DGRAD", "WGRAD")
+SLOTS = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
+
+
+def _stages(dims, tail=True):
+    """Python mirror of csrc/pk_pack.cuh member_stages()."""
+    L = len(dims) - 2
+    st = [[("FWD", l)] for l in range(L)]
+    if tail:
+        st.append([("TAIL", L)])
+    else:
+        st += [[("FWD", L)], [("HEAD", L)]] + ([[("DGRAD", L)]] if L >= 1 else [])
+    if L == 0:
+        st.append([("WGRAD", 0)])
+    else:
+        st.append([("WGRAD", L), ("WGRAD", L - 1)] + ([("DGRAD", L - 1)] if L >= 2 else []))
+        for l in range(L - 2, -1, -1):
+            st.append([("WGRAD", l)] + ([("DGRAD", l)] if l >= 1 else []))
+    return st
+
+
+def _item_bytes(dims, opt, kind, l, b, es):
+    """Algorithmic HBM bytes of one member's work item: each
+    tensor the item must touch, once.  The layer-0 input rows are counted
+    once per input group by the caller."""
+    i, o = dims[l], dims[l + 1]
+    hidden = l + 1 < len(dims) - 1
+    x_in = 0 if l == 0 else b * i  # layer-0 rows: shared, counted per group
+    if kind == "FWD":
+        return es * ((i * o + o) + x_in + b * o * (2 if hidden else 1))
+    if kind == "TAIL":
+        t = (i * o + o) + x_in + 2 * b * o + 2 * b + (3 * b * i if l >= 1 else 0)
+        return es * t + 8 * b
+    if kind == "HEAD":
+        return es * (2 * b * o + b) + 8 * b
+    if kind == "DGRAD":
+        return es * (b * o + i * o + 3 * b * i)
+    p = i * o + o  # WGRAD + optimizer: W (+slots) read and written
+    return es * (2 * p * (1 + SLOTS[opt]) + x_in + b * o)
+
+
+def _phase_plan(wl, es=4):
+    """[(label, algorithmic bytes)] per train phase of the workload's pack
+    (all members share one input group in these workloads)."""
     dims = (wl["dim"], *wl["hidden"], wl["classes"])
     b = wl["batch"]
-    K = len(wl["members"])
-    slots = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
-    L = len(dims) - 1
-    total = 0
-    for opt, _ in wl["members"]:
-        if kind == 0:  # forward: W, bias, write Z (+A if hidden); input rows
-            i, o = dims[layer], dims[layer + 1]
-            total += (i * o + o + b * o * (2 if layer + 1 < L else 1)) * es
-            if layer > 0:
-                total += b * i * es
-        elif kind == 1:  # head: read logits, write dlogits
-            total += 2 * b * dims[-1] * es
-        elif kind == 2:  # W/b + slots read and written, A_in and dZ read; dgrad
-            i, o = dims[layer], dims[layer + 1]
-            p = i * o + o
-            total += 2 * p * (1 + slots[opt]) * es + b * o * es
-            if layer > 0:
-                total += b * i * es + 3 * b * i * es  # A_in; Z, A read + dZ_prev write
-    if kind in (0, 2) and layer == 0:
-        total += b * dims[0] * es  # the group's shared input rows, once
-    return total
+    st = _stages(dims)
+    out = []
+    for items in st:
+        tot, x_once = 0, False
+        for opt, _ in wl["members"]:
+            for kind, l in items:
+                tot += _item_bytes(dims, opt, kind, l, b, es)
+                x_once |= (l == 0 and kind in ("FWD", "TAIL", "WGRAD"))
+        if x_once:
+            tot += es * b * dims[0]
+        out.append(("+".join(f"{k}{l}" for k, l in items), tot))
+    return out
 
 
 class Clocks:
@@ -225,10 +257,11 @@ def _b200(args):
         packing._apply_result(packed, active, plan, code, -1, -1, losses)
         prof.append(phases)
     phases = []
+    plan_b = _phase_plan(wl, 8 if args.precision == "f64" else 4)
     for i, (kind, layer, ctas, _) in enumerate(prof[0]):
-        phases.append({"kind": ("fwd", "head", "bwd+update", "finalize")[kind], "layer": layer,
-                       "ctas": ctas, "ms": statistics.median(p[i][3] for p in prof),
-                       "bytes": _phase_bytes(wl, kind, layer) if kind < 3 else 0})
+        label, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind]}{layer}", 0)
+        phases.append({"phase": label, "ctas": ctas,
+                       "ms": statistics.median(p[i][3] for p in prof), "bytes": nbytes})
     top = max(phases, key=lambda p: p["ms"])
 
     t = torch.tensor([dev_ms, e2e_s * 1e3, hb_s * 1e3, un_ms], dtype=torch.float64,
@@ -250,7 +283,7 @@ def _b200(args):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(args.workload, {}).get(
-            f"{top['kind']}:{top['layer']}")
+            top["phase"])
     desc_bytes = 16 + K * (40 if args.precision == "f32" else 40)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -271,7 +304,7 @@ def _b200(args):
                              "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
                              "d2h_bytes_per_step": 16 + 8 * K,
                              "api": "packed_step(preprocess_spec=normalize(0,1)): host gather"},
-        "roofline": {"bound": "hbm", "kernel": f"{top['kind']} layer {top['layer']}",
+        "roofline": {"bound": "hbm", "kernel": f"k_phase[{top['phase']}]",
                      "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / peaks["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes": top["bytes"], "launch_ms": top["ms"],

@@ -1,27 +1,37 @@
 // pk_kernels.cuh — sm_100a kernels of the packed MLP train step.
 //
-// One packed step = FWD(l) for l = 0..Lmax-1  →  HEAD  →  BWD(l) for
-// l = Lmax-1..0  →  FINALIZE, each a single grouped launch over all members
-// (reference: packing.py:185-264 → engine.forward :180-238, backward
-// :241-292, apply_update :295-326).
+// A packed step (reference: packing.py:185-264 → engine.forward :180-238,
+// backward :241-292, apply_update :295-326) is a short sequence of *phases*;
+// every phase is ONE launch of `k_phase` over a list of tiles drawn from all
+// K members (grouped launch), chained with programmatic dependent launch so a
+// phase's CTAs start (and prefetch their weights) while the previous phase
+// drains.  Tile kinds:
 //
-//  * FWD tiles compute Z = A·W + b and A' = act(Z) for a [32 x 16] block of
-//    one member's layer; layer 0 reads its rows straight from the device
-//    dataset through the epoch order (shared-input gather, data.py:131-136
-//    fused; members of one input group read the same rows, which stay L2
-//    resident, so the batch is fetched from HBM once per group).
-//  * BWD tiles are of two kinds in the same launch: DGRAD tiles produce the
-//    next gradient dZ_{l-1} = (dZ_l·W_lᵀ) ⊙ act'(Z_{l-1}); WGRAD tiles form
-//    dW_l = A_{l-1}ᵀ·dZ_l (and db_l) in shared memory and apply the member's
-//    optimizer in the epilogue, so the gradient never touches HBM.  The
-//    update writes the member's *other* parameter/slot buffer (ping-pong),
-//    which (a) removes the WAR hazard with DGRAD reading the old W in the
-//    same launch and (b) lets FINALIZE commit or drop a member's update
-//    atomically after the finite checks (engine.py:297-299 semantics).
-//  * Every output element is reduced in an order fixed by the layer's shape
-//    only (chunk = SK·BK, slice order 0..SK-1), never by K or by which other
-//    members share the launch, so a member's packed trajectory is
-//    bit-identical to its standalone one (tests/test_pack.py:57-82).
+//   FWD   Z_l = A_{l-1}·W_l + b_l, A_l = act(Z_l) for a [32 x 8] block; for
+//         l = 0 the rows are gathered straight from the device dataset
+//         through the epoch order (data.py:131-136 fused): members of one
+//         input group read the same rows, so the batch crosses HBM once.
+//   TAIL  the member's last layer + softmax-xent + the first backward GEMM
+//         for a block of 32 rows: logits, loss terms, dZ_L and
+//         dZ_{L-1} = (dZ_L·W_Lᵀ) ⊙ act'(Z_{L-1}) in one CTA (W_L resident in
+//         shared memory).
+//   HEAD  softmax-xent alone (members whose last layer is too big for TAIL).
+//   DGRAD dZ_{l-1} = (dZ_l·W_lᵀ) ⊙ act'(Z_{l-1}).
+//   WGRAD dW_l = A_{l-1}ᵀ·dZ_l (+ db_l) formed in shared memory and consumed by
+//         the member's optimizer in the epilogue — gradients never reach
+//         HBM.  The update writes the member's *other* params/slots buffer
+//         (ping-pong): no hazard with DGRAD reading the old W in the same
+//         phase, and the commit is a parity flip decided after the finite
+//         checks (engine.py:297-299).
+//
+// The last CTA of the last phase runs FINALIZE (loss reduction, commit rules
+// of packing.py:250-253, status + losses into a host-mapped ring).
+//
+// GEMM tiles stream operands through a multi-stage cp.async pipeline.  Every
+// output element is reduced in an order fixed by the tile kind and the
+// member's own shape — chunk KC, slice order 0..SK-1 — never by K or by the
+// other members, so a member's packed trajectory is bit-identical to its
+// standalone one (tests/test_pack.py:57-82).
 #pragma once
 
 #include <cstdint>
@@ -32,13 +42,13 @@
 
 namespace pk {
 
-constexpr int NT = 256;  // threads per CTA for every tile kernel
+constexpr int NT = 256;        // threads per CTA
+constexpr int ROWCAP = 1024;   // rows whose gather index is cached in smem
 
-enum TileKind : int16_t { TK_FWD = 0, TK_DGRAD = 1, TK_WGRAD = 2 };
+enum TileKind : int16_t { TK_FWD = 0, TK_TAIL = 1, TK_HEAD = 2, TK_DGRAD = 3, TK_WGRAD = 4 };
 
-// device-resident per-member control block
 struct MemberCtl {
-  int32_t parity;      // which params/slots buffer is committed
+  int32_t parity;      // committed params/slots buffer
   int32_t bad_node;    // min non-finite forward node index, INT_MAX = none
   int32_t bad_grad;    // min non-finite grad position, INT_MAX = none
   int32_t fault_grad;  // testing hook: poison this grad position (-1 none)
@@ -52,7 +62,7 @@ template <typename T>
 struct MemberDev {
   int32_t n_layers, act, opt, max_rows;
   int32_t dims[PK_MAX_LAYERS + 1];
-  int32_t n_slots, pad0;
+  int32_t n_slots, tail;  // tail: last layer handled by a TAIL tile
   double wd;
   int64_t n_params;
   int64_t w_off[PK_MAX_LAYERS];
@@ -62,6 +72,7 @@ struct MemberDev {
   T* Z[PK_MAX_LAYERS];   // pre-activation  [max_rows][dims[l+1]]
   T* A[PK_MAX_LAYERS];   // post-activation [max_rows][dims[l+1]] (hidden)
   T* dZ[PK_MAX_LAYERS];  // dLoss/dZ_l      [max_rows][dims[l+1]]
+  double* rowloss;       // per-row −log p[y]  [max_rows]
   MemberCtl* ctl;
 };
 
@@ -85,9 +96,44 @@ struct Tile {
 struct StepHdr {
   int32_t K;
   int32_t slot;   // result ring slot (host-mapped)
-  int32_t mode;   // 0 train, 1 eval chunk (no backward, accumulate losses)
+  int32_t mode;   // 0 train, 1 eval chunk (forward + loss terms only)
   int32_t pad;
 };
+
+template <typename T>
+struct PhaseArgs {
+  const MemberDev<T>* mems;
+  const FeedDev<T>* feeds;
+  const StepHdr* hdr;
+  const Tile* tiles;
+  int32_t* done;       // CTA-completion counter (last phase)
+  char* ring;          // host-mapped results
+  int32_t ring_stride;
+  int32_t K;
+  int32_t is_last;     // run FINALIZE in the last CTA
+  int32_t prefetch;    // issue L2 prefetch of params/slots (first phase)
+};
+
+// ------------------------------------------------------------ PTX glue --
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  const int n = pred ? BYTES : 0;  // src-size 0 → zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+               "n"(BYTES), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// bulk (TMA-engine) prefetch of a global range into L2
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // -------------------------------------------------------------- math ----
 
@@ -113,8 +159,8 @@ __device__ __forceinline__ T act_fwd(int act, T z) {
   }
 }
 
-// engine.py:274-290 — relu keys on z > 0, leaky on z >= 0; sigmoid/tanh
-// use the stored output a.
+// engine.py:274-290 — relu keys on z > 0, leaky on z >= 0; sigmoid/tanh use
+// the stored output a.
 template <typename T>
 __device__ __forceinline__ T act_bwd(int act, T z, T a, T d) {
   switch (act) {
@@ -125,8 +171,7 @@ __device__ __forceinline__ T act_bwd(int act, T z, T a, T d) {
   }
 }
 
-// engine.py:302-324 for one element; returns the new weight.  c = current
-// buffer, n = next buffer.  bc1/bc2 are Adam's bias corrections for t.
+// engine.py:302-324 for one element (c = committed buffer, n = next buffer)
 template <typename T>
 __device__ __forceinline__ void opt_apply(int opt, T lr, T wd, T bc1, T bc2,
                                           const T* __restrict__ wc, T* __restrict__ wn,
@@ -162,52 +207,82 @@ __device__ __forceinline__ void opt_apply(int opt, T lr, T wd, T bc1, T bc2,
   }
 }
 
-// ------------------------------------------------------- tile GEMM core --
+// ------------------------------------------------------- GEMM tile core --
 //
-// C[m][n] = Σ_k A(m,k)·B(k,n) over a BM x BN tile; the reduction runs in
-// chunks of SK·BK, slice s of the CTA taking sub-chunk s.  Partial tiles are
-// left in shared memory `red[SK][BM][BN]`; the caller's epilogue sums them in
-// slice order.  A(m,k) / B(k,n) are fetched by functors; AKF / BKF say
-// whether k is the contiguous (fast) index in global memory.
+// C[m][n] = Σ_k A(m,k)·B(k,n) for one BM x BN tile.  Operands are row-major
+// matrices read through `Mat` (row r lives at base + idx(r)·ld, idx from an
+// optional gather list).  AK/BK say whether k is the matrix's column
+// (contiguous) index: A(m,k) = M[m][k] if AK else M[k][m]; B(k,n) = M[n][k]
+// if BK else M[k][n].  Shared-memory stage layouts follow the global ones so
+// cp.async copies straight through; STAGES chunks of KC are in flight.
+// Slice s of the CTA reduces sub-chunk s; partial tiles end in shared memory
+// and value() sums them in slice order.
 
-template <typename T, int BM, int BN, int BK, int SK, int TM, int TN>
-struct TileGemm {
+template <typename T>
+struct Mat {
+  const T* base;
+  const int32_t* rows;  // gather list for the row index, or nullptr
+  int64_t row0;         // identity offset when rows == nullptr
+  int64_t ld;
+};
+
+template <typename T, int BM, int BN, int KC, int TM, int TN, int SK, int STAGES, bool AK, bool BK>
+struct Gemm {
   static constexpr int TPS = NT / SK;
-  static constexpr int RS = BM / TM;  // row stride inside a thread's micro-tile
+  static constexpr int RS = BM / TM;
   static constexpr int CS = BN / TN;
   static_assert(RS * CS == TPS, "micro-tile does not cover the tile");
-  static constexpr int KC = SK * BK;  // reduction chunk
-  static constexpr int LDA = BM + 1, LDB = BN + 1;
-  static constexpr int STAGE = KC * LDA + KC * LDB;
+  static_assert(KC % SK == 0, "chunk not divisible by slices");
+  static constexpr int KS = KC / SK;
+  static constexpr int A_ELEMS = BM * KC, B_ELEMS = BN * KC;
+  static constexpr int A_LD = AK ? KC + 1 : BM + 1;  // padded smem row
+  static constexpr int B_LD = BK ? KC + 1 : BN + 1;
+  static constexpr int A_STAGE = AK ? BM * A_LD : KC * A_LD;
+  static constexpr int B_STAGE = BK ? BN * B_LD : KC * B_LD;
+  static constexpr int PIPE = STAGES * (A_STAGE + B_STAGE);
   static constexpr int RED = SK * BM * BN;
-  static constexpr int SMEM = (STAGE > RED ? STAGE : RED);
+  static constexpr int SMEM_T = PIPE > RED ? PIPE : RED;  // in elements of T
 
-  template <bool KFAST, int MM, int LD, class F>
-  __device__ __forceinline__ static bool stage(T* S, F get, int k0, int m0, int kmax,
-                                               int mmax) {
-    bool bad = false;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < KC * MM; e += NT) {
-      int kk, mm;
-      if (KFAST) { kk = e % KC; mm = e / KC; }
-      else { mm = e % MM; kk = e / MM; }
-      const int k = k0 + kk, m = m0 + mm;
-      T v = T(0);
-      if (k < kmax && m < mmax) {
-        v = get(m, k);
-        bad |= !finite(v);
-      }
-      S[kk * LD + mm] = v;
-    }
-    return bad;
+  // gather offsets for the gathered dimension of A (m if AK, k otherwise)
+  __device__ __forceinline__ static int64_t a_row(const Mat<T>& a, const int32_t* srow, int r) {
+    if (!a.rows) return (a.row0 + r) * a.ld;
+    return (int64_t)(r < ROWCAP ? srow[r] : a.rows[r]) * a.ld;
   }
 
-  // returns (block-wide) whether any staged A element was non-finite
-  template <bool AKF, bool BKF, class FA, class FB>
-  __device__ __forceinline__ static bool run(T* smem, FA getA, FB getB, int m0, int n0, int M,
-                                             int N, int Kred) {
-    T* As = smem;
-    T* Bs = smem + KC * LDA;
+  __device__ __forceinline__ static void load_chunk(T* sA, T* sB, const Mat<T>& a, const Mat<T>& b,
+                                                    const int32_t* srow, int chunk, int m0, int n0,
+                                                    int M, int N, int Kr) {
+    const int k0 = chunk * KC;
+#pragma unroll 2
+    for (int e = threadIdx.x; e < A_ELEMS; e += NT) {
+      int kk, mm;
+      if (AK) { kk = e % KC; mm = e / KC; } else { mm = e % BM; kk = e / BM; }
+      const int k = k0 + kk, m = m0 + mm;
+      const bool ok = (k < Kr) && (m < M);
+      const T* g = a.base;
+      if (ok) g = AK ? a.base + a_row(a, srow, m - 0) + k : a.base + a_row(a, srow, k) + m;
+      T* s = AK ? sA + mm * A_LD + kk : sA + kk * A_LD + mm;
+      cp_async<sizeof(T)>(s, g, ok);
+    }
+#pragma unroll 2
+    for (int e = threadIdx.x; e < B_ELEMS; e += NT) {
+      int kk, nn;
+      if (BK) { kk = e % KC; nn = e / KC; } else { nn = e % BN; kk = e / BN; }
+      const int k = k0 + kk, n = n0 + nn;
+      const bool ok = (k < Kr) && (n < N);
+      const T* g = b.base;
+      if (ok) g = BK ? b.base + (int64_t)n * b.ld + k : b.base + (int64_t)k * b.ld + n;
+      T* s = BK ? sB + nn * B_LD + kk : sB + kk * B_LD + nn;
+      cp_async<sizeof(T)>(s, g, ok);
+    }
+  }
+
+  // srow: gather indices for A's gathered dimension, already in smem (for
+  // AK the tile's rows m0.., i.e. srow[m - m0] is NOT used: pass rows
+  // relative to 0 via a.rows/row0 and srow indexed by absolute row).
+  __device__ __forceinline__ static void run(T* smem, const Mat<T>& a, const Mat<T>& b,
+                                             const int32_t* srow, int m0, int n0, int M, int N,
+                                             int Kr) {
     const int slice = threadIdx.x / TPS, lt = threadIdx.x % TPS;
     const int tc = lt % CS, tr = lt / CS;
     T acc[TM][TN];
@@ -215,36 +290,51 @@ struct TileGemm {
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
-    bool badA = false;
-    for (int k0 = 0; k0 < Kred; k0 += KC) {
-      badA |= stage<AKF, BM, LDA>(As, getA, k0, m0, Kred, M);
-      stage<BKF, BN, LDB>(Bs, getB, k0, n0, Kred, N);
+    const int nch = (Kr + KC - 1) / KC;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nch)
+        load_chunk(smem + s * (A_STAGE + B_STAGE), smem + s * (A_STAGE + B_STAGE) + A_STAGE, a,
+                   b, srow, s, m0, n0, M, N, Kr);
+      cp_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+      const int pre = c + STAGES - 1;
+      if (pre < nch) {
+        T* st = smem + (pre % STAGES) * (A_STAGE + B_STAGE);
+        load_chunk(st, st + A_STAGE, a, b, srow, pre, m0, n0, M, N, Kr);
+      }
+      cp_commit();
+      cp_wait<STAGES - 1>();
       __syncthreads();
-      const T* a_s = As + (slice * BK) * LDA + tr;
-      const T* b_s = Bs + (slice * BK) * LDB + tc;
+      const T* sA = smem + (c % STAGES) * (A_STAGE + B_STAGE);
+      const T* sB = sA + A_STAGE;
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        T a[TM], b[TN];
+      for (int q = 0; q < KS; ++q) {
+        const int kk = slice * KS + q;
+        T av[TM], bv[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = a_s[kk * LDA + i * RS];
+        for (int i = 0; i < TM; ++i)
+          av[i] = AK ? sA[(tr + i * RS) * A_LD + kk] : sA[kk * A_LD + tr + i * RS];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = b_s[kk * LDB + j * CS];
+        for (int j = 0; j < TN; ++j)
+          bv[j] = BK ? sB[(tc + j * CS) * B_LD + kk] : sB[kk * B_LD + tc + j * CS];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
       }
       __syncthreads();
     }
+    cp_wait<0>();
     T* red = smem + slice * (BM * BN);
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) red[(tr + i * RS) * BN + tc + j * CS] = acc[i][j];
-    return __syncthreads_or(badA);
+    __syncthreads();
   }
 
-  // reduced value of tile element (mm, nn), fixed slice order
   __device__ __forceinline__ static T value(const T* smem, int mm, int nn) {
     T v = smem[mm * BN + nn];
 #pragma unroll
@@ -253,134 +343,283 @@ struct TileGemm {
   }
 };
 
-// tile shapes (fixed per kernel kind, never per pack → K-invariant)
-template <typename T> using FwdGemm = TileGemm<T, 32, 16, 8, 8, 4, 4>;
-template <typename T> using DgradGemm = TileGemm<T, 32, 16, 8, 8, 4, 4>;
-template <typename T> using WgradGemm = TileGemm<T, 32, 32, 8, 4, 4, 4>;
-constexpr int FWD_BM = 32, FWD_BN = 16;
+// tile shapes: fixed per tile kind (never per pack) → K-invariant
+template <typename T> using FwdG = Gemm<T, 32, 8, 64, 4, 4, 16, 6, true, false>;
+template <typename T> using TailG = Gemm<T, 32, 32, 64, 4, 4, 4, 4, true, false>;
+template <typename T> using DgradG = Gemm<T, 32, 16, 64, 4, 4, 8, 4, true, true>;
+template <typename T> using WgradG = Gemm<T, 32, 32, 32, 4, 4, 4, 4, false, false>;
+constexpr int FWD_BM = 32, FWD_BN = 8;
+constexpr int TAIL_BM = 32, TAIL_MAXC = 32;
+constexpr int HEAD_BM = 32;
 constexpr int DG_BM = 32, DG_BN = 16;
 constexpr int WG_BM = 32, WG_BN = 32;
 
-__device__ __forceinline__ void flag_min(int32_t* p, int v) { atomicMin(p, v); }
-
-// ------------------------------------------------------------- kernels --
-
+// smem (bytes) a tile kind needs besides the GEMM pipeline
 template <typename T>
-struct SmemBuf {
-  static constexpr int N =
-      (FwdGemm<T>::SMEM > WgradGemm<T>::SMEM ? FwdGemm<T>::SMEM : WgradGemm<T>::SMEM);
+struct Smem {
+  static constexpr int ROWS = ROWCAP * 4;
+  static constexpr int FWD = FwdG<T>::SMEM_T * (int)sizeof(T) + ROWS;
+  static constexpr int WGRAD = WgradG<T>::SMEM_T * (int)sizeof(T) + ROWS;
+  static constexpr int DGRAD = DgradG<T>::SMEM_T * (int)sizeof(T);
+  static constexpr int HEAD = ROWS;
+  // TAIL: pipeline + resident W_L [in x C] + dZ block [32 x 33] + rows
+  __host__ __device__ static int tail(int in, int C) {
+    return TailG<T>::SMEM_T * (int)sizeof(T) + in * C * (int)sizeof(T) +
+           TAIL_BM * (TAIL_MAXC + 1) * (int)sizeof(T) + ROWS;
+  }
 };
 
-// Forward of layer `t.layer` for one [32 x 16] output tile.
+__device__ __forceinline__ void flag_min(int32_t* p, int v) { atomicMin(p, v); }
+
 template <typename T>
-__device__ __forceinline__ void fwd_tile(T* smem, const MemberDev<T>& M, const FeedDev<T>& f,
-                                         const Tile& t) {
-  using G = FwdGemm<T>;
+__device__ __forceinline__ int64_t feed_row(const FeedDev<T>& f, int r) {
+  return f.rows ? (int64_t)f.rows[r] : f.row0 + r;
+}
+
+// cache the batch's gather indices (rows [0, n)) in shared memory
+template <typename T>
+__device__ __forceinline__ void stage_rows(int32_t* srow, const FeedDev<T>& f, int n) {
+  n = n < ROWCAP ? n : ROWCAP;
+  for (int r = threadIdx.x; r < n; r += NT) srow[r] = (int32_t)feed_row(f, r);
+}
+
+template <typename T>
+__device__ __forceinline__ Mat<T> input_mat(const MemberDev<T>& M, const FeedDev<T>& f, int l) {
+  if (l == 0) return Mat<T>{f.feat, f.rows, f.row0, f.ld};
+  return Mat<T>{M.A[l - 1], nullptr, 0, M.dims[l]};
+}
+
+// ---------------------------------------------------------------- FWD --
+template <typename T>
+__device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t) {
+  using G = FwdG<T>;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
   const int R = f.take;
+  T* smem = reinterpret_cast<T*>(sm);
+  int32_t* srow = reinterpret_cast<int32_t*>(sm + G::SMEM_T * sizeof(T));
   const int par = M.ctl->parity;
   const T* W = M.params[par] + M.w_off[l];
   const T* bias = M.params[par] + M.b_off[l];
-  auto getB = [&](int n, int k) { return W[(int64_t)k * out + n]; };
-  bool badX;
-  if (l == 0) {
-    const T* X = f.feat;
-    const int32_t* rows = f.rows;
-    const int64_t row0 = f.row0, ld = f.ld;
-    auto getA = [&](int m, int k) {
-      const int64_t r = rows ? (int64_t)rows[m] : row0 + m;
-      return X[r * ld + k];
-    };
-    badX = G::template run<true, false>(smem, getA, getB, t.m0, t.n0, R, out, in);
-  } else {
-    const T* Ain = M.A[l - 1];
-    auto getA = [&](int m, int k) { return Ain[(int64_t)m * in + k]; };
-    badX = G::template run<true, false>(smem, getA, getB, t.m0, t.n0, R, out, in);
-    badX = false;  // hidden inputs were checked where they were produced
-  }
+  if (l == 0) stage_rows(srow, f, R);
+  if (l > 0) pdl_wait();  // A_{l-1} comes from the previous phase
+  __syncthreads();
+  const Mat<T> a = input_mat(M, f, l);
+  const Mat<T> b{W, nullptr, 0, out};
+  G::run(smem, a, b, srow, t.m0, t.n0, R, out, in);
   const bool last = (l == M.n_layers - 1);
-  T* Z = M.Z[l];
-  T* A = M.A[l];
   int bad = INT_MAX;
   for (int e = threadIdx.x; e < FWD_BM * FWD_BN; e += NT) {
     const int mm = e / FWD_BN, nn = e % FWD_BN;
     const int m = t.m0 + mm, n = t.n0 + nn;
     if (m >= R || n >= out) continue;
     const T z = G::value(smem, mm, nn) + bias[n];
-    Z[(int64_t)m * out + n] = z;
+    M.Z[l][(int64_t)m * out + n] = z;
     if (!finite(z)) bad = min(bad, 1 + 2 * l);
     if (!last) {
-      const T a = act_fwd(M.act, z);
-      A[(int64_t)m * out + n] = a;
-      if (!finite(a)) bad = min(bad, 2 + 2 * l);
+      const T av = act_fwd(M.act, z);
+      M.A[l][(int64_t)m * out + n] = av;
+      if (!finite(av)) bad = min(bad, 2 + 2 * l);
     }
   }
-  if (badX && threadIdx.x == 0) flag_min(&M.ctl->bad_node, 0);
+  if (l == 0) {  // the input node (engine.py:233-235 checks it too)
+    bool badx = false;
+    for (int e = threadIdx.x; e < FWD_BM * in; e += NT) {
+      const int mm = e / in, k = e % in;
+      if (t.m0 + mm >= R || t.n0 != 0) break;
+      badx |= !finite(f.feat[feed_row(f, t.m0 + mm) * f.ld + k]);
+    }
+    if (badx) bad = 0;
+  }
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
 }
 
+// ------------------------------------------------------- softmax-xent --
+// One warp per row (lanes over classes): loss term −logp[y] into rowloss,
+// dlogits = (p − onehot(y)) / R (engine.py:211-230, :252-264).
 template <typename T>
-__global__ void __launch_bounds__(NT) k_fwd(const MemberDev<T>* __restrict__ mems,
-                                            const FeedDev<T>* __restrict__ feeds,
-                                            const Tile* __restrict__ tiles) {
-  __shared__ __align__(16) T smem[SmemBuf<T>::N];
-  const Tile t = tiles[blockIdx.x];
-  const FeedDev<T> f = feeds[t.member];
-  if (f.take == 0 || t.m0 >= f.take) return;
-  fwd_tile<T>(smem, mems[t.member], f, t);
+__device__ __forceinline__ void xent_row(const T* z, T* dz, int C, int y, int R, bool train,
+                                         double* rowloss) {
+  const int lane = threadIdx.x & 31;
+  T mx = -INFINITY;
+  for (int c = lane; c < C; c += 32) mx = max(mx, z[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  T s = T(0);
+  for (int c = lane; c < C; c += 32) s += ex(z[c] - mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const T zy = z[y];  // before dz (which may alias z) is written
+  __syncwarp();
+  if (train) {
+    const T inv = T(1) / s, nv = T(R);
+    for (int c = lane; c < C; c += 32) {
+      T p = ex(z[c] - mx) * inv;
+      if (c == y) p -= T(1);
+      dz[c] = p / nv;
+    }
+  }
+  if (lane == 0) *rowloss = -(double)((zy - mx) - lg(s));
 }
 
-// DGRAD: dZ_{l-1}[r][i] = act'(Z,A)[r][i] · Σ_j dZ_l[r][j] W_l[i][j]
 template <typename T>
-__device__ __forceinline__ void dgrad_tile(T* smem, const MemberDev<T>& M, const FeedDev<T>& f,
-                                           const Tile& t) {
-  using G = DgradGemm<T>;
+__device__ void head_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t,
+                          bool train) {
+  const int L = M.n_layers - 1, C = M.dims[L + 1];
+  const int R = f.take;
+  pdl_wait();
+  const int warp = threadIdx.x >> 5;
+  for (int r = t.m0 + warp; r < min(R, t.m0 + HEAD_BM); r += NT / 32) {
+    const int y = f.labels[feed_row(f, r)];
+    xent_row(M.Z[L] + (int64_t)r * C, M.dZ[L] + (int64_t)r * C, C, y, R, train,
+             M.rowloss + r);
+  }
+  (void)sm;
+}
+
+// --------------------------------------------------------------- TAIL --
+template <typename T>
+__device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t,
+                          bool train) {
+  using G = TailG<T>;
+  const int L = M.n_layers - 1, in = M.dims[L], C = M.dims[L + 1];
+  const int R = f.take;
+  T* smem = reinterpret_cast<T*>(sm);
+  T* sW = smem + G::SMEM_T;                 // W_L [in][C]
+  T* sD = sW + in * C;                      // dZ block [32][TAIL_MAXC+1]
+  int32_t* srow = reinterpret_cast<int32_t*>(sD + TAIL_BM * (TAIL_MAXC + 1));
+  const int par = M.ctl->parity;
+  const T* W = M.params[par] + M.w_off[L];
+  const T* bias = M.params[par] + M.b_off[L];
+  // W_L is a parameter: stage it before waiting on the previous phase
+  const bool dgrad = train && L > 0;
+  if (dgrad) {
+    for (int e = threadIdx.x; e < in * C; e += NT) cp_async<sizeof(T)>(sW + e, W + e, true);
+    cp_commit();
+  }
+  if (L == 0) stage_rows(srow, f, R);
+  if (L > 0) pdl_wait();
+  __syncthreads();
+  const Mat<T> a = input_mat(M, f, L);
+  const Mat<T> b{W, nullptr, 0, C};
+  G::run(smem, a, b, srow, t.m0, 0, R, C, in);
+  // logits (+ bias) → Z_L and into sD; input / logit finite checks
+  int bad = INT_MAX;
+  for (int e = threadIdx.x; e < TAIL_BM * TAIL_MAXC; e += NT) {
+    const int mm = e / TAIL_MAXC, c = e % TAIL_MAXC;
+    const int m = t.m0 + mm;
+    if (m >= R || c >= C) continue;
+    const T z = G::value(smem, mm, c) + bias[c];
+    M.Z[L][(int64_t)m * C + c] = z;
+    sD[mm * (TAIL_MAXC + 1) + c] = z;
+    if (!finite(z)) bad = min(bad, 1 + 2 * L);
+  }
+  if (L == 0) {
+    bool badx = false;
+    for (int e = threadIdx.x; e < TAIL_BM * in; e += NT) {
+      const int mm = e / in, k = e % in;
+      if (t.m0 + mm >= R) break;
+      badx |= !finite(f.feat[feed_row(f, t.m0 + mm) * f.ld + k]);
+    }
+    if (badx) bad = 0;
+  }
+  if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  __syncthreads();
+  // softmax-xent per row, in place in sD (logits → dlogits)
+  const int warp = threadIdx.x >> 5;
+  for (int mm = warp; mm < TAIL_BM; mm += NT / 32) {
+    const int m = t.m0 + mm;
+    if (m >= R) break;
+    const int y = f.labels[feed_row(f, m)];
+    T* row = sD + mm * (TAIL_MAXC + 1);
+    xent_row(row, row, C, y, R, train, M.rowloss + m);
+    __syncwarp();
+  }
+  if (!train) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < TAIL_BM * C; e += NT) {
+    const int mm = e / C, c = e % C;
+    if (t.m0 + mm < R) M.dZ[L][(int64_t)(t.m0 + mm) * C + c] = sD[mm * (TAIL_MAXC + 1) + c];
+  }
+  if (!dgrad) return;
+  cp_wait<0>();
+  __syncthreads();
+  // dZ_{L-1}[m][i] = act'(Z,A)[m][i] · Σ_c dZ_L[m][c] W_L[i][c]
+  const T* Zp = M.Z[L - 1];
+  const T* Ap = M.A[L - 1];
+  T* dZp = M.dZ[L - 1];
+  for (int e = threadIdx.x; e < TAIL_BM * in; e += NT) {
+    const int mm = e / in, i = e % in;
+    const int m = t.m0 + mm;
+    if (m >= R) break;
+    const T* d = sD + mm * (TAIL_MAXC + 1);
+    const T* w = sW + i * C;
+    T s = T(0);
+    for (int c = 0; c < C; ++c) s = fma(d[c], w[c], s);
+    const int64_t o = (int64_t)m * in + i;
+    dZp[o] = act_bwd(M.act, Zp[o], Ap[o], s);
+  }
+}
+
+// -------------------------------------------------------------- DGRAD --
+template <typename T>
+__device__ void dgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t) {
+  using G = DgradG<T>;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
   const int R = f.take;
+  T* smem = reinterpret_cast<T*>(sm);
   const int par = M.ctl->parity;
   const T* W = M.params[par] + M.w_off[l];
-  const T* dZ = M.dZ[l];
-  auto getA = [&](int m, int k) { return dZ[(int64_t)m * out + k]; };
-  auto getB = [&](int n, int k) { return W[(int64_t)n * out + k]; };
-  G::template run<true, true>(smem, getA, getB, t.m0, t.n0, R, in, out);
-  const T* Zp = M.Z[l - 1];
-  const T* Ap = M.A[l - 1];
-  T* dZp = M.dZ[l - 1];
+  pdl_wait();
+  const Mat<T> a{M.dZ[l], nullptr, 0, out};
+  const Mat<T> b{W, nullptr, 0, out};  // B(k=j, n=i) = W[i][j]
+  G::run(smem, a, b, nullptr, t.m0, t.n0, R, in, out);
   for (int e = threadIdx.x; e < DG_BM * DG_BN; e += NT) {
     const int mm = e / DG_BN, nn = e % DG_BN;
     const int m = t.m0 + mm, n = t.n0 + nn;
     if (m >= R || n >= in) continue;
     const int64_t o = (int64_t)m * in + n;
-    dZp[o] = act_bwd(M.act, Zp[o], Ap[o], G::value(smem, mm, nn));
+    M.dZ[l - 1][o] = act_bwd(M.act, M.Z[l - 1][o], M.A[l - 1][o], G::value(smem, mm, nn));
   }
 }
 
-// WGRAD + optimizer: W_l' = opt(W_l, A_{l-1}ᵀ·dZ_l); tiles with m0 == 0 also
-// reduce and update the bias.  Grad finiteness is flagged per tensor.
+// -------------------------------------------------------------- WGRAD --
 template <typename T>
-__device__ __forceinline__ void wgrad_tile(T* smem, const MemberDev<T>& M, const FeedDev<T>& f,
-                                           const Tile& t) {
-  using G = WgradGemm<T>;
+__device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t) {
+  using G = WgradG<T>;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
   const int R = f.take;
-  const int par = M.ctl->parity;
-  const T* dZ = M.dZ[l];
-  auto getB = [&](int n, int k) { return dZ[(int64_t)k * out + n]; };
-  if (l == 0) {
-    const T* X = f.feat;
-    const int32_t* rows = f.rows;
-    const int64_t row0 = f.row0, ld = f.ld;
-    auto getA = [&](int m, int k) {
-      const int64_t r = rows ? (int64_t)rows[k] : row0 + k;
-      return X[r * ld + m];
-    };
-    G::template run<false, false>(smem, getA, getB, t.m0, t.n0, in, out, R);
-  } else {
-    const T* Ain = M.A[l - 1];
-    auto getA = [&](int m, int k) { return Ain[(int64_t)k * in + m]; };
-    G::template run<false, false>(smem, getA, getB, t.m0, t.n0, in, out, R);
-  }
+  T* smem = reinterpret_cast<T*>(sm);
+  int32_t* srow = reinterpret_cast<int32_t*>(sm + G::SMEM_T * sizeof(T));
   const MemberCtl* ctl = M.ctl;
+  const int par = ctl->parity;
+  const int64_t P = M.n_params;
+  const T* wc = M.params[par];
+  T* wn = M.params[par ^ 1];
+  const T* sc = M.slots[par];
+  T* sn = M.slots[par ^ 1];
+  // pull this tile's weights + slots toward L2 while the previous phase drains
+  {
+    const int r = threadIdx.x;
+    if (r < WG_BM && t.m0 + r < in) {
+      const int64_t row = M.w_off[l] + (int64_t)(t.m0 + r) * out + t.n0;
+      const int cnt = min(WG_BN, out - t.n0);
+      for (int s = -1; s < M.n_slots; ++s) {
+        const T* base = s < 0 ? wc : sc + (int64_t)s * P;
+        const char* p0 = reinterpret_cast<const char*>(base + row);
+        const char* p1 = reinterpret_cast<const char*>(base + row + cnt);
+        const char* a0 = reinterpret_cast<const char*>((uintptr_t)p0 & ~(uintptr_t)15);
+        const uint32_t bytes = (uint32_t)(((p1 - a0) + 15) & ~15);
+        l2_prefetch(a0, bytes);
+      }
+    }
+  }
+  if (l == 0) stage_rows(srow, f, R);
+  pdl_wait();
+  __syncthreads();
+  // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]
+  const Mat<T> a = input_mat(M, f, l);
+  const Mat<T> b{M.dZ[l], nullptr, 0, out};
+  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R);
   const T lr = T(ctl->lr), wd = T(M.wd);
   T bc1 = T(1), bc2 = T(1);
   if (M.opt == PK_OPT_ADAM) {
@@ -388,13 +627,10 @@ __device__ __forceinline__ void wgrad_tile(T* smem, const MemberDev<T>& M, const
     bc1 = T(1.0 - pow(0.9, tt));
     bc2 = T(1.0 - pow(0.999, tt));
   }
-  const int64_t P = M.n_params;
-  const T* wc = M.params[par];
-  T* wn = M.params[par ^ 1];
-  const T* sc = M.slots[par];
-  T* sn = M.slots[par ^ 1];
-  const T* s0c = sc; T* s0n = sn;
-  const T* s1c = sc ? sc + P : nullptr; T* s1n = sn ? sn + P : nullptr;
+  const T* s0c = sc;
+  T* s0n = sn;
+  const T* s1c = sc ? sc + P : nullptr;
+  T* s1n = sn ? sn + P : nullptr;
   const int gpos = 2 * (M.n_layers - 1 - l);
   bool badW = false, badB = false;
   for (int e = threadIdx.x; e < WG_BM * WG_BN; e += NT) {
@@ -410,6 +646,7 @@ __device__ __forceinline__ void wgrad_tile(T* smem, const MemberDev<T>& M, const
   if (t.m0 == 0 && threadIdx.x < WG_BN) {
     const int n = t.n0 + threadIdx.x;
     if (n < out) {
+      const T* dZ = M.dZ[l];
       T g = T(0);
       for (int r = 0; r < R; ++r) g += dZ[(int64_t)r * out + n];
       if (ctl->fault_grad == gpos + 1) g = T(NAN);
@@ -421,115 +658,50 @@ __device__ __forceinline__ void wgrad_tile(T* smem, const MemberDev<T>& M, const
   if (badB) flag_min(&M.ctl->bad_grad, gpos + 1);
 }
 
+// ----------------------------------------------------------- FINALIZE --
+// Run by the last CTA of the last phase.  Loss = Σ rowloss / R in a fixed
+// order (thread-strided, fixed tree); commit rules of packing.py:246-253: a
+// forward non-finite value aborts the step, else members commit in pack
+// order until the first one with a non-finite gradient.
 template <typename T>
-__global__ void __launch_bounds__(NT) k_bwd(const MemberDev<T>* __restrict__ mems,
-                                            const FeedDev<T>* __restrict__ feeds,
-                                            const Tile* __restrict__ tiles) {
-  __shared__ __align__(16) T smem[SmemBuf<T>::N];
-  const Tile t = tiles[blockIdx.x];
-  const FeedDev<T> f = feeds[t.member];
-  if (f.take == 0) return;
-  if (t.kind == TK_DGRAD) {
-    if (t.m0 >= f.take) return;
-    dgrad_tile<T>(smem, mems[t.member], f, t);
-  } else {
-    wgrad_tile<T>(smem, mems[t.member], f, t);
-  }
-}
-
-// ---------------------------------------------------------------- head --
-// Softmax cross-entropy over the member's valid rows (engine.py:211-230,
-// :252-264): one CTA per member, one warp per row.  Loss = −mean(logp[y]),
-// summed in a fixed order (thread-strided, then a fixed tree) in float64.
-template <typename T>
-__global__ void __launch_bounds__(NT) k_head(const MemberDev<T>* __restrict__ mems,
-                                             const FeedDev<T>* __restrict__ feeds,
-                                             const StepHdr* __restrict__ hdr) {
+__device__ void finalize(const PhaseArgs<T>& P, bool train) {
   __shared__ double part[NT];
-  const int k = blockIdx.x;
-  const FeedDev<T> f = feeds[k];
-  const int R = f.take;
-  if (R == 0) return;
-  const MemberDev<T>& M = mems[k];
-  const int L = M.n_layers - 1, C = M.dims[L + 1];
-  const T* Zl = M.Z[L];
-  T* dZ = M.dZ[L];
-  const bool train = (hdr->mode == 0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // per-row loss terms are written to part-of-thread slots in a fixed map:
-  // row r is owned by thread (r % NT)'s running sum (rows visited in order)
-  double mysum = 0.0;
-  for (int r0 = 0; r0 < R; r0 += NT / 32 * 32) {
-    // each warp handles 32 consecutive rows of this batch-chunk, one at a time
-    for (int rr = 0; rr < 32; ++rr) {
-      const int r = r0 + warp * 32 + rr;
-      if (r >= R) break;
-      const T* z = Zl + (int64_t)r * C;
-      T mx = -INFINITY;
-      for (int c = lane; c < C; c += 32) mx = max(mx, z[c]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      T s = T(0);
-      for (int c = lane; c < C; c += 32) s += ex(z[c] - mx);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const int64_t src = f.rows ? (int64_t)f.rows[r] : f.row0 + r;
-      const int y = f.labels[src];
+  const int K = P.K;
+  for (int k = 0; k < K; ++k) {
+    const FeedDev<T>& f = P.feeds[k];
+    if (!f.take) continue;  // block-uniform
+    const MemberDev<T>& M = P.mems[k];
+    double s = 0.0;
+    for (int r = threadIdx.x; r < f.take; r += NT) s += M.rowloss[r];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = NT / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
       if (train) {
-        const T inv = T(1) / s;
-        const T nv = T(R);
-        for (int c = lane; c < C; c += 32) {
-          T p = ex(z[c] - mx) * inv;
-          if (c == y) p -= T(1);
-          dZ[(int64_t)r * C + c] = p / nv;
-        }
-      }
-      if (lane == (r & 31)) {
-        const T logp = (z[y] - mx) - lg(s);
-        mysum += -(double)logp;
+        const double loss = part[0] / double(f.take);
+        M.ctl->loss = loss;
+        if (!isfinite(loss)) M.ctl->bad_node = min(M.ctl->bad_node, 2 * M.n_layers);
+      } else {
+        M.ctl->eval_acc += part[0];
       }
     }
-  }
-  part[threadIdx.x] = mysum;
-  __syncthreads();
-  for (int w = NT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    MemberCtl* ctl = M.ctl;
-    if (train) {
-      const double loss = part[0] / double(R);
-      ctl->loss = loss;
-      if (!isfinite(loss)) atomicMin(&ctl->bad_node, 2 * M.n_layers);
-    } else {
-      ctl->eval_acc += part[0];
-    }
-  }
-}
-
-// ------------------------------------------------------------ finalize --
-// Commit rules of packing.py:246-253: a forward non-finite value aborts the
-// whole step; otherwise members commit in pack order until the first member
-// with a non-finite gradient.  Writes {status, losses} to the host ring.
-template <typename T>
-__global__ void k_finalize(const MemberDev<T>* __restrict__ mems,
-                           const FeedDev<T>* __restrict__ feeds,
-                           const StepHdr* __restrict__ hdr, char* __restrict__ ring,
-                           int32_t ring_stride) {
-  if (threadIdx.x != 0) return;
-  const int K = hdr->K;
-  int32_t* st = reinterpret_cast<int32_t*>(ring + (int64_t)hdr->slot * ring_stride);
+  if (threadIdx.x != 0 || !train) return;
+  int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)P.hdr->slot * P.ring_stride);
   double* losses = reinterpret_cast<double*>(st + 4);
   int code = PK_OK, who = -1, idx = -1, committed = 0;
   for (int k = 0; k < K; ++k) {
-    if (!feeds[k].take) continue;
-    const int b = mems[k].ctl->bad_node;
+    if (!P.feeds[k].take) continue;
+    const int b = P.mems[k].ctl->bad_node;
     if (b != INT_MAX) { code = PK_ERR_NONFINITE_VALUE; who = k; idx = b; break; }
   }
   for (int k = 0; k < K; ++k) {
-    MemberCtl* c = mems[k].ctl;
-    const bool act = feeds[k].take != 0;
+    MemberCtl* c = P.mems[k].ctl;
+    const bool act = P.feeds[k].take != 0;
     losses[k] = act ? c->loss : 0.0;
     if (act && code == PK_OK) {
       if (c->bad_grad != INT_MAX) {
@@ -542,12 +714,86 @@ __global__ void k_finalize(const MemberDev<T>* __restrict__ mems,
     }
   }
   for (int k = 0; k < K; ++k) {
-    mems[k].ctl->bad_node = INT_MAX;
-    mems[k].ctl->bad_grad = INT_MAX;
-    if (feeds[k].take) mems[k].ctl->fault_grad = -1;  // one-shot
+    MemberCtl* c = P.mems[k].ctl;
+    c->bad_node = INT_MAX;
+    c->bad_grad = INT_MAX;
+    if (P.feeds[k].take) c->fault_grad = -1;  // one-shot
   }
   st[0] = code; st[1] = who; st[2] = idx; st[3] = committed;
   __threadfence_system();
+}
+
+// ------------------------------------------------------------- kernels --
+
+// L2 prefetch of every active member's committed params + slots (first
+// phase): the step's dominant HBM stream overlaps the forward pass.
+template <typename T>
+__device__ void prefetch_params(const PhaseArgs<T>& P) {
+  constexpr uint32_t CH = 16384;
+  const int64_t gt = (int64_t)blockIdx.x * NT + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * NT;
+  int64_t base = 0;
+  for (int k = 0; k < P.K; ++k) {
+    if (!P.feeds[k].take) continue;
+    const MemberDev<T>& M = P.mems[k];
+    const int par = M.ctl->parity;
+    for (int s = -1; s < M.n_slots; ++s) {
+      const char* p = reinterpret_cast<const char*>(s < 0 ? M.params[par]
+                                                          : M.slots[par] + (int64_t)s * M.n_params);
+      const int64_t bytes = ((int64_t)M.n_params * (int64_t)sizeof(T) + 15) & ~15LL;
+      const int64_t nch = (bytes + CH - 1) / CH;
+      for (int64_t c = (gt - base % gs + gs) % gs; c < nch; c += gs) {
+        const int64_t off = c * CH;
+        const int64_t left = bytes - off;
+        l2_prefetch(p + off, (uint32_t)(left < (int64_t)CH ? left : (int64_t)CH));
+      }
+      base += nch;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
+  extern __shared__ __align__(16) char smem_raw[];
+  pdl_launch();
+  if (P.prefetch) prefetch_params(P);
+  const Tile t = P.tiles[blockIdx.x];
+  const FeedDev<T> f = P.feeds[t.member];
+  const bool train = (P.hdr->mode == 0);
+  if (f.take != 0) {
+    const MemberDev<T>& M = P.mems[t.member];
+    switch (t.kind) {
+      case TK_FWD:
+        if (t.m0 < f.take) fwd_tile<T>(smem_raw, M, f, t);
+        break;
+      case TK_TAIL:
+        if (t.m0 < f.take) tail_tile<T>(smem_raw, M, f, t, train);
+        break;
+      case TK_HEAD:
+        if (t.m0 < f.take) head_tile<T>(smem_raw, M, f, t, train);
+        break;
+      case TK_DGRAD:
+        if (t.m0 < f.take) dgrad_tile<T>(smem_raw, M, f, t);
+        break;
+      default:
+        wgrad_tile<T>(smem_raw, M, f, t);
+        break;
+    }
+  }
+  if (!P.is_last) return;
+  // last CTA to finish runs FINALIZE
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(P.done, 1) == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  pdl_wait();  // all earlier phases complete (a no-op when none pending)
+  finalize<T>(P, train);
+  if (threadIdx.x == 0) *P.done = 0;
 }
 
 // eval: after the last chunk, losses[k] = eval_acc / rows and reset

@@ -1,0 +1,543 @@
+// pk_pack.cuh — the pack half of the runtime (included by pk_runtime.cu so
+// the whole library is one translation unit).
+//
+// A pack is an ordered list of members.  Its packed step is a fixed
+// schedule of phases built once from the members' shapes:
+//
+//   member stages:  FWD(0) .. FWD(L-1) | TAIL                 (or FWD(L), HEAD, DGRAD(L))
+//                   | WGRAD(L) WGRAD(L-1) DGRAD(L-1) | WGRAD(L-2) DGRAD(L-2) | .. | WGRAD(0)
+//   phase p      =  stage p of every member (one grouped launch of k_phase)
+//
+// Phases are launched with programmatic dependent launch and captured once
+// into a CUDA graph; a step is then one H2D descriptor copy + one graph
+// launch.  The last CTA of the last phase runs FINALIZE and writes
+// {status, losses} into a host-mapped ring slot.
+
+#pragma once
+
+struct Phase {
+  std::vector<Tile> host;  // tiles (host copy, for schedule inspection)
+  Tile* tiles = nullptr;   // device copy
+  int ntiles = 0;
+  int smem = 0;            // dynamic shared memory bytes
+  int kind = 0;            // dominant tile kind (reporting)
+  int layer = -1;          // dominant layer (reporting)
+};
+
+struct pk_pack {
+  pk_ctx* ctx;
+  std::vector<pk_member*> members;
+  int K;
+  void* d_members = nullptr;  // MemberDev<T>[K]
+  char* d_blob = nullptr;     // StepHdr + FeedDev<T>[K]
+  size_t blob_bytes = 0;
+  int32_t* d_done = nullptr;  // CTA-completion counter for FINALIZE
+  Tile* d_tiles = nullptr;
+  std::vector<Phase> train;   // phases of a train step
+  std::vector<Phase> eval;    // forward-only phases (validation loss)
+  char* h_desc = nullptr;     // pinned ring of descriptors
+  char* h_ring = nullptr;     // host-mapped result ring
+  char* d_ring = nullptr;
+  int32_t ring_stride = 0;
+  cudaEvent_t ev[kRing];
+  bool ev_pending[kRing];
+  int64_t next_ticket = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+
+template <typename T>
+static MemberDev<T> member_dev(const pk_member* m, int tail) {
+  MemberDev<T> d{};
+  d.n_layers = m->desc.n_layers;
+  d.act = m->desc.activation;
+  d.opt = m->desc.optimizer;
+  d.max_rows = m->desc.max_rows;
+  for (int i = 0; i <= d.n_layers; ++i) d.dims[i] = m->desc.dims[i];
+  d.n_slots = m->n_slots;
+  d.tail = tail;
+  d.wd = m->desc.weight_decay;
+  d.n_params = m->P;
+  for (int l = 0; l < d.n_layers; ++l) {
+    d.w_off[l] = m->w_off[l];
+    d.b_off[l] = m->b_off[l];
+    d.Z[l] = (T*)m->Z[l];
+    d.A[l] = (T*)m->A[l];
+    d.dZ[l] = (T*)m->dZ[l];
+  }
+  for (int b = 0; b < 2; ++b) {
+    d.params[b] = (T*)m->params[b];
+    d.slots[b] = (T*)m->slots[b];
+  }
+  d.rowloss = m->rowloss;
+  d.ctl = m->ctl;
+  return d;
+}
+
+static size_t feed_size(int dtype) {
+  return dtype == PK_F64 ? sizeof(FeedDev<double>) : sizeof(FeedDev<float>);
+}
+
+constexpr int kSmemMax = 227 * 1024;
+
+// whether the member's last layer + head + first dgrad fit one TAIL tile
+static bool tail_ok(const pk_member* m, int dtype) {
+  const int L = m->desc.n_layers - 1;
+  const int in = m->desc.dims[L], C = m->desc.dims[L + 1];
+  if (C > pk::TAIL_MAXC) return false;
+  const int need = dtype == PK_F64 ? pk::Smem<double>::tail(in, C) : pk::Smem<float>::tail(in, C);
+  return need <= kSmemMax;
+}
+
+static int kind_smem(int kind, const pk_member* m, int dtype) {
+  const bool d = dtype == PK_F64;
+  const int L = m->desc.n_layers - 1;
+  switch (kind) {
+    case pk::TK_FWD: return d ? pk::Smem<double>::FWD : pk::Smem<float>::FWD;
+    case pk::TK_TAIL:
+      return d ? pk::Smem<double>::tail(m->desc.dims[L], m->desc.dims[L + 1])
+               : pk::Smem<float>::tail(m->desc.dims[L], m->desc.dims[L + 1]);
+    case pk::TK_HEAD: return d ? pk::Smem<double>::HEAD : pk::Smem<float>::HEAD;
+    case pk::TK_DGRAD: return d ? pk::Smem<double>::DGRAD : pk::Smem<float>::DGRAD;
+    default: return d ? pk::Smem<double>::WGRAD : pk::Smem<float>::WGRAD;
+  }
+}
+
+static int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// tiles of one (member, kind, layer) work item
+static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, int l) {
+  const auto& d = m->desc;
+  switch (kind) {
+    case pk::TK_FWD:
+      for (int mb = 0; mb < cdiv(d.max_rows, pk::FWD_BM); ++mb)
+        for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::FWD_BN); ++nb)
+          out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::FWD_BM, nb * pk::FWD_BN});
+      break;
+    case pk::TK_TAIL:
+      for (int mb = 0; mb < cdiv(d.max_rows, pk::TAIL_BM); ++mb)
+        out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::TAIL_BM, 0});
+      break;
+    case pk::TK_HEAD:
+      for (int mb = 0; mb < cdiv(d.max_rows, pk::HEAD_BM); ++mb)
+        out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::HEAD_BM, 0});
+      break;
+    case pk::TK_DGRAD:
+      for (int mb = 0; mb < cdiv(d.max_rows, pk::DG_BM); ++mb)
+        for (int nb = 0; nb < cdiv(d.dims[l], pk::DG_BN); ++nb)
+          out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::DG_BM, nb * pk::DG_BN});
+      break;
+    default:  // WGRAD over W_l [in x out]
+      for (int mb = 0; mb < cdiv(d.dims[l], pk::WG_BM); ++mb)
+        for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::WG_BN); ++nb)
+          out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::WG_BM, nb * pk::WG_BN});
+      break;
+  }
+}
+
+using Stage = std::vector<std::pair<int, int>>;  // (kind, layer)
+
+// per-member stage sequence; `fwd_stages` = how many form the forward pass
+static std::vector<Stage> member_stages(const pk_member* m, bool tail, int* fwd_stages) {
+  const int L = m->desc.n_layers - 1;
+  std::vector<Stage> st;
+  for (int l = 0; l < L; ++l) st.push_back({{pk::TK_FWD, l}});
+  if (tail) {
+    st.push_back({{pk::TK_TAIL, L}});
+    *fwd_stages = (int)st.size();
+  } else {
+    st.push_back({{pk::TK_FWD, L}});
+    st.push_back({{pk::TK_HEAD, L}});
+    *fwd_stages = (int)st.size();
+    if (L >= 1) st.push_back({{pk::TK_DGRAD, L}});
+  }
+  if (L == 0) {
+    st.push_back({{pk::TK_WGRAD, 0}});
+  } else {
+    Stage s{{pk::TK_WGRAD, L}, {pk::TK_WGRAD, L - 1}};
+    if (L - 1 >= 1) s.push_back({pk::TK_DGRAD, L - 1});
+    st.push_back(s);
+    for (int l = L - 2; l >= 0; --l) {
+      Stage s2{{pk::TK_WGRAD, l}};
+      if (l >= 1) s2.push_back({pk::TK_DGRAD, l});
+      st.push_back(s2);
+    }
+  }
+  return st;
+}
+
+static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
+  const int dt = p->ctx->dtype;
+  std::vector<std::vector<Stage>> seq(p->K);
+  size_t nph = 0;
+  for (int k = 0; k < p->K; ++k) {
+    int nf = 0;
+    seq[k] = member_stages(p->members[k], tail_ok(p->members[k], dt), &nf);
+    if (eval) seq[k].resize(nf);
+    nph = std::max(nph, seq[k].size());
+  }
+  phases.assign(nph, Phase{});
+  for (size_t ph = 0; ph < nph; ++ph) {
+    Phase& P = phases[ph];
+    double best = -1;
+    for (int k = 0; k < p->K; ++k) {
+      if (ph >= seq[k].size()) continue;
+      for (auto [kind, layer] : seq[k][ph]) {
+        const size_t before = P.host.size();
+        emit(P.host, k, p->members[k], kind, layer);
+        P.smem = std::max(P.smem, kind_smem(kind, p->members[k], dt));
+        const double w = double(P.host.size() - before);
+        if (w > best) { best = w; P.kind = kind; P.layer = layer; }
+      }
+    }
+    P.ntiles = (int)P.host.size();
+  }
+}
+
+template <typename T>
+static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
+  cudaStream_t s = p->ctx->stream;
+  for (size_t i = 0; i < phases.size(); ++i) {
+    const Phase& ph = phases[i];
+    if (!ph.ntiles) continue;
+    pk::PhaseArgs<T> a{};
+    a.mems = (const MemberDev<T>*)p->d_members;
+    a.hdr = (const StepHdr*)p->d_blob;
+    a.feeds = (const FeedDev<T>*)(p->d_blob + sizeof(StepHdr));
+    a.tiles = ph.tiles;
+    a.done = p->d_done;
+    a.ring = p->d_ring;
+    a.ring_stride = p->ring_stride;
+    a.K = p->K;
+    a.is_last = (i + 1 == phases.size());
+    a.prefetch = (i == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ph.ntiles);
+    cfg.blockDim = dim3(pk::NT);
+    cfg.dynamicSmemBytes = ph.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, pk::k_phase<T>, a);
+    if (e != cudaSuccess) {
+      p->ctx->err = std::string("launch phase: ") + cudaGetErrorString(e);
+      return PK_ERR_CUDA;
+    }
+  }
+  return PK_OK;
+}
+
+static int launch(pk_pack* p, const std::vector<Phase>& ph) {
+  return p->ctx->dtype == PK_F64 ? launch_phases<double>(p, ph) : launch_phases<float>(p, ph);
+}
+
+static bool g_smem_attr[2] = {false, false};
+
+extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, pk_pack** out) {
+  if (!c || !out || !members || k < 1) return arg_err(c, "pack needs at least one member");
+  cudaSetDevice(c->device);
+  for (int i = 0; i < k; ++i) {
+    if (!members[i] || members[i]->ctx != c) return arg_err(c, "pack: member from another context");
+    for (int j = 0; j < i; ++j)
+      if (members[j] == members[i]) return arg_err(c, "pack: duplicate member");
+  }
+  if (!g_smem_attr[c->dtype]) {
+    cudaError_t e = c->dtype == PK_F64
+                        ? cudaFuncSetAttribute(pk::k_phase<double>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax)
+                        : cudaFuncSetAttribute(pk::k_phase<float>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    CK_CTX(c, e);
+    g_smem_attr[c->dtype] = true;
+  }
+  auto* p = new pk_pack();
+  p->ctx = c;
+  p->members.assign(members, members + k);
+  p->K = k;
+  size_t mdsz = c->dtype == PK_F64 ? sizeof(MemberDev<double>) : sizeof(MemberDev<float>);
+  std::vector<char> hm(mdsz * k);
+  for (int i = 0; i < k; ++i) {
+    const int tl = tail_ok(members[i], c->dtype);
+    if (c->dtype == PK_F64) {
+      auto d = member_dev<double>(members[i], tl);
+      memcpy(hm.data() + i * mdsz, &d, mdsz);
+    } else {
+      auto d = member_dev<float>(members[i], tl);
+      memcpy(hm.data() + i * mdsz, &d, mdsz);
+    }
+  }
+  build_phases(p, false, p->train);
+  build_phases(p, true, p->eval);
+  std::vector<Tile> all;
+  for (auto* v : {&p->train, &p->eval})
+    for (auto& ph : *v) all.insert(all.end(), ph.host.begin(), ph.host.end());
+  p->blob_bytes = sizeof(StepHdr) + feed_size(c->dtype) * k;
+  p->ring_stride = (int32_t)align_up(16 + 8 * (size_t)k, 64);
+  auto fail = [&](cudaError_t e) {
+    c->err = std::string("pack alloc: ") + cudaGetErrorString(e);
+    if (p->d_members) cudaFree(p->d_members);
+    if (p->d_blob) cudaFree(p->d_blob);
+    if (p->d_tiles) cudaFree(p->d_tiles);
+    if (p->d_done) cudaFree(p->d_done);
+    if (p->h_desc) cudaFreeHost(p->h_desc);
+    if (p->h_ring) cudaFreeHost(p->h_ring);
+    delete p;
+    return e == cudaErrorMemoryAllocation ? PK_ERR_OOM : PK_ERR_CUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->d_members, hm.size())) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc((void**)&p->d_blob, p->blob_bytes)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc((void**)&p->d_done, 16)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc((void**)&p->d_tiles, std::max<size_t>(1, all.size()) * sizeof(Tile))) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaHostAlloc((void**)&p->h_desc, p->blob_bytes * kRing, cudaHostAllocDefault)) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaHostAlloc((void**)&p->h_ring, (size_t)p->ring_stride * kRing, cudaHostAllocMapped)) !=
+      cudaSuccess)
+    return fail(e);
+  if ((e = cudaHostGetDevicePointer((void**)&p->d_ring, p->h_ring, 0)) != cudaSuccess) return fail(e);
+  memset(p->h_ring, 0, (size_t)p->ring_stride * kRing);
+  cudaMemsetAsync(p->d_done, 0, 16, c->stream);
+  cudaMemcpyAsync(p->d_members, hm.data(), hm.size(), cudaMemcpyHostToDevice, c->stream);
+  if (!all.empty())
+    cudaMemcpyAsync(p->d_tiles, all.data(), all.size() * sizeof(Tile), cudaMemcpyHostToDevice, c->stream);
+  size_t off = 0;
+  for (auto* v : {&p->train, &p->eval})
+    for (auto& ph : *v) {
+      ph.tiles = p->d_tiles + off;
+      off += ph.host.size();
+    }
+  for (int i = 0; i < kRing; ++i) {
+    cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
+    p->ev_pending[i] = false;
+  }
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return fail(e);
+  c->bytes += hm.size() + p->blob_bytes + all.size() * sizeof(Tile);
+  *out = p;
+  return PK_OK;
+}
+
+extern "C" int pk_pack_destroy(pk_pack* p) {
+  if (!p) return PK_ERR_ARG;
+  pk_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  for (int i = 0; i < kRing; ++i) cudaEventDestroy(p->ev[i]);
+  cudaFree(p->d_members);
+  cudaFree(p->d_blob);
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_done);
+  cudaFreeHost(p->h_desc);
+  cudaFreeHost(p->h_ring);
+  delete p;
+  return PK_OK;
+}
+
+extern "C" int32_t pk_pack_launches_per_step(const pk_pack* p) {
+  if (!p) return -1;
+  int n = 0;
+  for (auto& ph : p->train) n += ph.ntiles > 0;
+  return n;
+}
+
+template <typename T>
+static int fill_feeds(pk_pack* p, const pk_feed* feeds, char* dst) {
+  auto* fd = reinterpret_cast<FeedDev<T>*>(dst);
+  for (int k = 0; k < p->K; ++k) {
+    const pk_feed& f = feeds[k];
+    FeedDev<T> d{};
+    if (f.take > 0) {
+      const pk_member* m = p->members[k];
+      if (!f.data) return arg_err(p->ctx, "feed: missing dataset for active member");
+      if (f.data->ctx != p->ctx) return arg_err(p->ctx, "feed: dataset from another context");
+      if (f.data->dim != m->desc.dims[0]) return arg_err(p->ctx, "feed: dataset dim != member input_dim");
+      if (f.take > m->desc.max_rows) return arg_err(p->ctx, "feed: take exceeds member max_rows");
+      if (f.pos < 0 || f.pos + f.take > f.data->n) return arg_err(p->ctx, "feed: rows exceed dataset");
+      if (f.order && f.order->n != f.data->n) return arg_err(p->ctx, "feed: order length != dataset rows");
+      d.feat = (const T*)f.data->feat;
+      d.labels = f.data->labels;
+      d.rows = f.order ? f.order->perm + f.pos : nullptr;
+      d.row0 = f.order ? 0 : f.pos;
+      d.ld = f.data->dim;
+      d.take = f.take;
+    }
+    fd[k] = d;
+  }
+  return PK_OK;
+}
+
+static int acquire_slot(pk_pack* p, int64_t ticket, int* slot) {
+  const int s = (int)(ticket % kRing);
+  if (p->ev_pending[s]) {
+    CK_CTX(p->ctx, cudaEventSynchronize(p->ev[s]));
+    p->ev_pending[s] = false;
+  }
+  *slot = s;
+  return PK_OK;
+}
+
+static int launch_desc(pk_pack* p, int slot, int mode, const pk_feed* feeds) {
+  char* h = p->h_desc + (size_t)slot * p->blob_bytes;
+  StepHdr hdr{p->K, slot, mode, 0};
+  memcpy(h, &hdr, sizeof(hdr));
+  int rc = p->ctx->dtype == PK_F64 ? fill_feeds<double>(p, feeds, h + sizeof(StepHdr))
+                                   : fill_feeds<float>(p, feeds, h + sizeof(StepHdr));
+  if (rc) return rc;
+  CK_CTX(p->ctx, cudaMemcpyAsync(p->d_blob, h, p->blob_bytes, cudaMemcpyHostToDevice, p->ctx->stream));
+  return PK_OK;
+}
+
+extern "C" int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* ticket) {
+  if (!p || !feeds) return PK_ERR_ARG;
+  pk_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  const int64_t t = p->next_ticket;
+  int slot;
+  int rc = acquire_slot(p, t, &slot);
+  if (rc) return rc;
+  if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
+  if (!p->exec) {
+    cudaGraph_t g;
+    CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = launch(p, p->train);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (rc) return rc;
+    CK_CTX(c, e);
+    e = cudaGraphInstantiate(&p->exec, g, 0);
+    cudaGraphDestroy(g);
+    CK_CTX(c, e);
+  }
+  CK_CTX(c, cudaGraphLaunch(p->exec, c->stream));
+  CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
+  p->ev_pending[slot] = true;
+  p->next_ticket = t + 1;
+  if (ticket) *ticket = t;
+  return PK_OK;
+}
+
+static int read_result(pk_pack* p, int slot, double* losses, pk_status* st) {
+  const int32_t* s = reinterpret_cast<const int32_t*>(p->h_ring + (size_t)slot * p->ring_stride);
+  const double* l = reinterpret_cast<const double*>(s + 4);
+  if (st) {
+    st->code = s[0];
+    st->member = s[1];
+    st->index = s[2];
+    st->committed = s[3];
+  }
+  if (losses) memcpy(losses, l, sizeof(double) * p->K);
+  return s[0];
+}
+
+extern "C" int pk_pack_step_wait(pk_pack* p, int64_t ticket, double* losses, pk_status* st) {
+  if (!p || ticket < 0 || ticket >= p->next_ticket || ticket < p->next_ticket - kRing)
+    return PK_ERR_STATE;
+  pk_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  const int slot = (int)(ticket % kRing);
+  if (p->ev_pending[slot]) {
+    CK_CTX(c, cudaEventSynchronize(p->ev[slot]));
+    p->ev_pending[slot] = false;
+  }
+  return read_result(p, slot, losses, st);
+}
+
+extern "C" int pk_pack_step(pk_pack* p, const pk_feed* feeds, double* losses, pk_status* st) {
+  int64_t t;
+  int rc = pk_pack_step_async(p, feeds, &t);
+  if (rc) return rc;
+  return pk_pack_step_wait(p, t, losses, st);
+}
+
+extern "C" int pk_pack_eval(pk_pack* p, const pk_dataset* data, const pk_order* order, int64_t pos,
+                            int64_t rows, double* losses, pk_status* st) {
+  if (!p || !data) return PK_ERR_ARG;
+  pk_ctx* c = p->ctx;
+  if (rows < 1 || pos < 0 || pos + rows > data->n) return arg_err(c, "eval: bad row range");
+  cudaSetDevice(c->device);
+  int64_t max_chunks = 0;
+  for (auto* m : p->members)
+    max_chunks = std::max<int64_t>(max_chunks, (rows + m->desc.max_rows - 1) / m->desc.max_rows);
+  std::vector<pk_feed> feeds(p->K);
+  int slot = 0;
+  for (int64_t ch = 0; ch < max_chunks; ++ch) {
+    for (int k = 0; k < p->K; ++k) {
+      const int64_t mr = p->members[k]->desc.max_rows;
+      const int64_t off = ch * mr;
+      const int64_t tk = std::max<int64_t>(0, std::min<int64_t>(mr, rows - off));
+      feeds[k] = pk_feed{data, order, pos + (tk ? off : 0), (int32_t)tk, 0};
+    }
+    const int64_t t = p->next_ticket++;
+    int rc = acquire_slot(p, t, &slot);
+    if (rc) return rc;
+    if ((rc = launch_desc(p, slot, 1, feeds.data()))) return rc;
+    if ((rc = launch(p, p->eval))) return rc;
+    CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
+    p->ev_pending[slot] = true;
+  }
+  const int64_t t = p->next_ticket++;
+  int rc = acquire_slot(p, t, &slot);
+  if (rc) return rc;
+  if (c->dtype == PK_F64)
+    pk::k_eval_finish<double><<<1, 32, 0, c->stream>>>((const MemberDev<double>*)p->d_members, p->K,
+                                                         rows, p->d_ring, slot, p->ring_stride);
+  else
+    pk::k_eval_finish<float><<<1, 32, 0, c->stream>>>((const MemberDev<float>*)p->d_members, p->K,
+                                                        rows, p->d_ring, slot, p->ring_stride);
+  CK_CTX(c, cudaGetLastError());
+  CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
+  CK_CTX(c, cudaEventSynchronize(p->ev[slot]));
+  p->ev_pending[slot] = false;
+  return read_result(p, slot, losses, st);
+}
+
+extern "C" int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* phase_ms,
+                                    int32_t* phase_kind, int32_t* phase_layer,
+                                    int32_t* phase_ctas, double* losses, pk_status* st) {
+  if (!p || !feeds) return PK_ERR_ARG;
+  pk_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  const int64_t t = p->next_ticket++;
+  int slot;
+  int rc = acquire_slot(p, t, &slot);
+  if (rc) return rc;
+  if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
+  std::vector<int> idx;
+  for (int i = 0; i < (int)p->train.size(); ++i)
+    if (p->train[i].ntiles) idx.push_back(i);
+  const int n = (int)idx.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) CK_CTX(c, cudaEventCreate(&e));
+  // phases launched one at a time (no PDL overlap) so each is timed alone;
+  // the last one keeps is_last so FINALIZE commits the step
+  for (int j = 0; j < n; ++j) {
+    CK_CTX(c, cudaEventRecord(ev[j], c->stream));
+    std::vector<Phase> one;
+    for (int i = 0; i <= idx[j]; ++i) {
+      Phase ph = p->train[i];
+      if (i != idx[j]) ph.ntiles = 0;
+      one.push_back(ph);
+    }
+    if (j + 1 < n) {  // not last: suppress FINALIZE
+      Phase tail_off{};
+      tail_off.ntiles = 0;
+      one.push_back(tail_off);
+    }
+    if ((rc = launch(p, one))) return rc;
+  }
+  CK_CTX(c, cudaEventRecord(ev[n], c->stream));
+  CK_CTX(c, cudaEventSynchronize(ev[n]));
+  for (int j = 0; j < n; ++j) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[j], ev[j + 1]);
+    const Phase& ph = p->train[idx[j]];
+    if (phase_ms) phase_ms[j] = ms;
+    if (phase_kind) phase_kind[j] = ph.kind;
+    if (phase_layer) phase_layer[j] = ph.layer;
+    if (phase_ctas) phase_ctas[j] = ph.ntiles;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return read_result(p, slot, losses, st);
+}

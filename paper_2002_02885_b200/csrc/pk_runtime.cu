@@ -66,42 +66,11 @@ struct pk_member {
   void* Z[PK_MAX_LAYERS];
   void* A[PK_MAX_LAYERS];
   void* dZ[PK_MAX_LAYERS];
+  double* rowloss;
   MemberCtl* ctl;
 };
 
-struct Phase {
-  int kind;  // 0 fwd, 1 head, 2 bwd, 3 finalize
-  Tile* tiles;
-  int ntiles;
-  int layer;
-};
-
-struct Span {
-  int kind;
-  size_t start;
-  int layer;
-};
-
-struct pk_pack {
-  pk_ctx* ctx;
-  std::vector<pk_member*> members;
-  int K;
-  void* d_members = nullptr;  // MemberDev<T>[K]
-  char* d_blob = nullptr;     // StepHdr + FeedDev<T>[K]
-  size_t blob_bytes = 0;
-  Tile* d_tiles = nullptr;
-  std::vector<Phase> phases;
-  std::vector<Phase> fwd_phases;  // eval reuses forward + head
-  char* h_desc = nullptr;         // pinned ring of descriptors
-  char* h_ring = nullptr;         // host-mapped result ring
-  char* d_ring = nullptr;
-  int32_t ring_stride = 0;
-  cudaEvent_t ev[kRing];
-  bool ev_pending[kRing];
-  int64_t next_ticket = 0;
-  cudaGraphExec_t exec = nullptr;
-  int launches = 0;
-};
+struct pk_pack;
 
 #define CK_CTX(ctx, call)                                                        \
   do {                                                                           \
@@ -310,6 +279,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
     o_a[l] = take(l + 1 < d->n_layers ? act : 0);
     o_dz[l] = take(act);
   }
+  const size_t o_loss = take((size_t)d->max_rows * sizeof(double));
   const size_t o_ctl = take(sizeof(MemberCtl));
   m->slab_bytes = off;
   cudaError_t e = cudaMalloc((void**)&m->slab, off);
@@ -328,6 +298,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
     m->A[l] = (l + 1 < d->n_layers) ? m->slab + o_a[l] : nullptr;
     m->dZ[l] = m->slab + o_dz[l];
   }
+  m->rowloss = reinterpret_cast<double*>(m->slab + o_loss);
   m->ctl = reinterpret_cast<MemberCtl*>(m->slab + o_ctl);
   CK_CTX(c, cudaMemsetAsync(m->slab, 0, off, c->stream));
   MemberCtl ctl{};
@@ -413,12 +384,14 @@ extern "C" int pk_member_set_state(pk_member* m, const double* params, const dou
     }
   }
   MemberCtl ctl{};
+  CK_CTX(c, cudaMemcpy(&ctl, m->ctl, sizeof(ctl), cudaMemcpyDeviceToHost));  // keeps fault_grad
   ctl.parity = 0;
   ctl.bad_node = INT_MAX;
   ctl.bad_grad = INT_MAX;
-  ctl.fault_grad = -1;
   ctl.step_counter = step_counter;
   ctl.lr = m->desc.learning_rate;
+  ctl.loss = 0.0;
+  ctl.eval_acc = 0.0;
   CK_CTX(c, cudaMemcpyAsync(m->ctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, c->stream));
   CK_CTX(c, cudaStreamSynchronize(c->stream));
   return PK_OK;
@@ -450,382 +423,6 @@ extern "C" int pk_member_get_state(pk_member* m, double* params, double* slots, 
   return PK_OK;
 }
 
+
 // ---------------------------------------------------------------- packs --
-template <typename T>
-static MemberDev<T> member_dev(const pk_member* m) {
-  MemberDev<T> d{};
-  d.n_layers = m->desc.n_layers;
-  d.act = m->desc.activation;
-  d.opt = m->desc.optimizer;
-  d.max_rows = m->desc.max_rows;
-  for (int i = 0; i <= d.n_layers; ++i) d.dims[i] = m->desc.dims[i];
-  d.n_slots = m->n_slots;
-  d.wd = m->desc.weight_decay;
-  d.n_params = m->P;
-  for (int l = 0; l < d.n_layers; ++l) {
-    d.w_off[l] = m->w_off[l];
-    d.b_off[l] = m->b_off[l];
-    d.Z[l] = (T*)m->Z[l];
-    d.A[l] = (T*)m->A[l];
-    d.dZ[l] = (T*)m->dZ[l];
-  }
-  for (int b = 0; b < 2; ++b) {
-    d.params[b] = (T*)m->params[b];
-    d.slots[b] = (T*)m->slots[b];
-  }
-  d.ctl = m->ctl;
-  return d;
-}
-
-static size_t feed_size(int dtype) {
-  return dtype == PK_F64 ? sizeof(FeedDev<double>) : sizeof(FeedDev<float>);
-}
-
-// Tile schedule: fixed for the pack's composition and the members' max_rows.
-static void build_schedule(pk_pack* p, std::vector<Tile>& all, std::vector<Span>& spans) {
-  int lmax = 0;
-  for (auto* m : p->members) lmax = std::max(lmax, (int)m->desc.n_layers);
-  auto cdiv = [](int a, int b) { return (a + b - 1) / b; };
-  // forward phases
-  for (int l = 0; l < lmax; ++l) {
-    size_t s = all.size();
-    for (int k = 0; k < p->K; ++k) {
-      const auto& d = p->members[k]->desc;
-      if (l >= d.n_layers) continue;
-      for (int mb = 0; mb < cdiv(d.max_rows, pk::FWD_BM); ++mb)
-        for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::FWD_BN); ++nb)
-          all.push_back(Tile{k, (int16_t)l, pk::TK_FWD, mb * pk::FWD_BM, nb * pk::FWD_BN});
-    }
-    spans.push_back({0, s, l});
-  }
-  spans.push_back({1, all.size(), lmax - 1});  // head
-  for (int l = lmax - 1; l >= 0; --l) {
-    size_t s = all.size();
-    for (int k = 0; k < p->K; ++k) {
-      const auto& d = p->members[k]->desc;
-      if (l >= d.n_layers) continue;
-      // weight-gradient + update tiles first: they are the long pole
-      for (int mb = 0; mb < cdiv(d.dims[l], pk::WG_BM); ++mb)
-        for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::WG_BN); ++nb)
-          all.push_back(Tile{k, (int16_t)l, pk::TK_WGRAD, mb * pk::WG_BM, nb * pk::WG_BN});
-      if (l >= 1)
-        for (int mb = 0; mb < cdiv(d.max_rows, pk::DG_BM); ++mb)
-          for (int nb = 0; nb < cdiv(d.dims[l], pk::DG_BN); ++nb)
-            all.push_back(Tile{k, (int16_t)l, pk::TK_DGRAD, mb * pk::DG_BM, nb * pk::DG_BN});
-    }
-    spans.push_back({2, s, l});
-  }
-  spans.push_back({3, all.size(), -1});
-}
-
-template <typename T>
-static int enqueue_kernels(pk_pack* p, const std::vector<Phase>& phases, int mode) {
-  cudaStream_t s = p->ctx->stream;
-  const auto* mems = (const MemberDev<T>*)p->d_members;
-  const auto* hdr = (const StepHdr*)p->d_blob;
-  const auto* feeds = (const FeedDev<T>*)(p->d_blob + sizeof(StepHdr));
-  for (const Phase& ph : phases) {
-    switch (ph.kind) {
-      case 0:
-        if (ph.ntiles) pk::k_fwd<T><<<ph.ntiles, pk::NT, 0, s>>>(mems, feeds, ph.tiles);
-        break;
-      case 1:
-        pk::k_head<T><<<p->K, pk::NT, 0, s>>>(mems, feeds, hdr);
-        break;
-      case 2:
-        if (ph.ntiles) pk::k_bwd<T><<<ph.ntiles, pk::NT, 0, s>>>(mems, feeds, ph.tiles);
-        break;
-      case 3:
-        pk::k_finalize<T><<<1, 32, 0, s>>>(mems, feeds, hdr, p->d_ring, p->ring_stride);
-        break;
-    }
-  }
-  (void)mode;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    p->ctx->err = std::string("launch: ") + cudaGetErrorString(e);
-    return PK_ERR_CUDA;
-  }
-  return PK_OK;
-}
-
-static int enqueue(pk_pack* p, const std::vector<Phase>& ph, int mode) {
-  return p->ctx->dtype == PK_F64 ? enqueue_kernels<double>(p, ph, mode)
-                                 : enqueue_kernels<float>(p, ph, mode);
-}
-
-extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, pk_pack** out) {
-  if (!c || !out || !members || k < 1) return arg_err(c, "pack needs at least one member");
-  cudaSetDevice(c->device);
-  for (int i = 0; i < k; ++i) {
-    if (!members[i] || members[i]->ctx != c) return arg_err(c, "pack: member from another context");
-    for (int j = 0; j < i; ++j)
-      if (members[j] == members[i]) return arg_err(c, "pack: duplicate member");
-  }
-  auto* p = new pk_pack();
-  p->ctx = c;
-  p->members.assign(members, members + k);
-  p->K = k;
-  const size_t es = c->esize();
-  (void)es;
-  // device member table
-  size_t mdsz = c->dtype == PK_F64 ? sizeof(MemberDev<double>) : sizeof(MemberDev<float>);
-  std::vector<char> hm(mdsz * k);
-  for (int i = 0; i < k; ++i) {
-    if (c->dtype == PK_F64) {
-      auto d = member_dev<double>(members[i]);
-      memcpy(hm.data() + i * mdsz, &d, mdsz);
-    } else {
-      auto d = member_dev<float>(members[i]);
-      memcpy(hm.data() + i * mdsz, &d, mdsz);
-    }
-  }
-  std::vector<Tile> tiles;
-  std::vector<Span> spans;
-  build_schedule(p, tiles, spans);
-  p->blob_bytes = sizeof(StepHdr) + feed_size(c->dtype) * k;
-  p->ring_stride = (int32_t)align_up(16 + 8 * (size_t)k, 64);
-  auto fail = [&](cudaError_t e) {
-    c->err = std::string("pack alloc: ") + cudaGetErrorString(e);
-    if (p->d_members) cudaFree(p->d_members);
-    if (p->d_blob) cudaFree(p->d_blob);
-    if (p->d_tiles) cudaFree(p->d_tiles);
-    if (p->h_desc) cudaFreeHost(p->h_desc);
-    if (p->h_ring) cudaFreeHost(p->h_ring);
-    delete p;
-    return e == cudaErrorMemoryAllocation ? PK_ERR_OOM : PK_ERR_CUDA;
-  };
-  cudaError_t e;
-  if ((e = cudaMalloc(&p->d_members, hm.size())) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc((void**)&p->d_blob, p->blob_bytes)) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc((void**)&p->d_tiles, std::max<size_t>(1, tiles.size()) * sizeof(Tile))) != cudaSuccess)
-    return fail(e);
-  if ((e = cudaHostAlloc((void**)&p->h_desc, p->blob_bytes * kRing, cudaHostAllocDefault)) != cudaSuccess)
-    return fail(e);
-  if ((e = cudaHostAlloc((void**)&p->h_ring, (size_t)p->ring_stride * kRing, cudaHostAllocMapped)) !=
-      cudaSuccess)
-    return fail(e);
-  if ((e = cudaHostGetDevicePointer((void**)&p->d_ring, p->h_ring, 0)) != cudaSuccess) return fail(e);
-  memset(p->h_ring, 0, (size_t)p->ring_stride * kRing);
-  cudaMemcpyAsync(p->d_members, hm.data(), hm.size(), cudaMemcpyHostToDevice, c->stream);
-  if (!tiles.empty())
-    cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, c->stream);
-  for (int i = 0; i < kRing; ++i) {
-    cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
-    p->ev_pending[i] = false;
-  }
-  for (size_t i = 0; i < spans.size(); ++i) {
-    const size_t s = spans[i].start;
-    const size_t e2 = (i + 1 < spans.size()) ? spans[i + 1].start : tiles.size();
-    Phase ph{spans[i].kind, p->d_tiles + s, (int)(e2 - s), spans[i].layer};
-    if ((ph.kind == 0 || ph.kind == 2) && ph.ntiles == 0) continue;
-    p->phases.push_back(ph);
-    if (ph.kind <= 1) p->fwd_phases.push_back(ph);
-  }
-  p->launches = (int)p->phases.size();
-  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return fail(e);
-  c->bytes += hm.size() + p->blob_bytes + tiles.size() * sizeof(Tile);
-  *out = p;
-  return PK_OK;
-}
-
-extern "C" int pk_pack_destroy(pk_pack* p) {
-  if (!p) return PK_ERR_ARG;
-  pk_ctx* c = p->ctx;
-  cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
-  if (p->exec) cudaGraphExecDestroy(p->exec);
-  for (int i = 0; i < kRing; ++i) cudaEventDestroy(p->ev[i]);
-  cudaFree(p->d_members);
-  cudaFree(p->d_blob);
-  cudaFree(p->d_tiles);
-  cudaFreeHost(p->h_desc);
-  cudaFreeHost(p->h_ring);
-  delete p;
-  return PK_OK;
-}
-
-extern "C" int32_t pk_pack_launches_per_step(const pk_pack* p) { return p ? p->launches : -1; }
-
-template <typename T>
-static int fill_feeds(pk_pack* p, const pk_feed* feeds, char* dst) {
-  auto* fd = reinterpret_cast<FeedDev<T>*>(dst);
-  for (int k = 0; k < p->K; ++k) {
-    const pk_feed& f = feeds[k];
-    FeedDev<T> d{};
-    if (f.take > 0) {
-      const pk_member* m = p->members[k];
-      if (!f.data) return arg_err(p->ctx, "feed: missing dataset for active member");
-      if (f.data->ctx != p->ctx) return arg_err(p->ctx, "feed: dataset from another context");
-      if (f.data->dim != m->desc.dims[0]) return arg_err(p->ctx, "feed: dataset dim != member input_dim");
-      if (f.take > m->desc.max_rows) return arg_err(p->ctx, "feed: take exceeds member max_rows");
-      if (f.pos < 0 || f.pos + f.take > f.data->n) return arg_err(p->ctx, "feed: rows exceed dataset");
-      if (f.order && f.order->n != f.data->n) return arg_err(p->ctx, "feed: order length != dataset rows");
-      d.feat = (const T*)f.data->feat;
-      d.labels = f.data->labels;
-      d.rows = f.order ? f.order->perm + f.pos : nullptr;
-      d.row0 = f.order ? 0 : f.pos;
-      d.ld = f.data->dim;
-      d.take = f.take;
-    }
-    fd[k] = d;
-  }
-  return PK_OK;
-}
-
-static int acquire_slot(pk_pack* p, int64_t ticket, int* slot) {
-  const int s = (int)(ticket % kRing);
-  if (p->ev_pending[s]) {
-    CK_CTX(p->ctx, cudaEventSynchronize(p->ev[s]));
-    p->ev_pending[s] = false;
-  }
-  *slot = s;
-  return PK_OK;
-}
-
-static int launch_desc(pk_pack* p, int slot, int mode, const pk_feed* feeds) {
-  char* h = p->h_desc + (size_t)slot * p->blob_bytes;
-  StepHdr hdr{p->K, slot, mode, 0};
-  memcpy(h, &hdr, sizeof(hdr));
-  int rc = p->ctx->dtype == PK_F64 ? fill_feeds<double>(p, feeds, h + sizeof(StepHdr))
-                                   : fill_feeds<float>(p, feeds, h + sizeof(StepHdr));
-  if (rc) return rc;
-  CK_CTX(p->ctx, cudaMemcpyAsync(p->d_blob, h, p->blob_bytes, cudaMemcpyHostToDevice, p->ctx->stream));
-  return PK_OK;
-}
-
-extern "C" int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* ticket) {
-  if (!p || !feeds) return PK_ERR_ARG;
-  pk_ctx* c = p->ctx;
-  cudaSetDevice(c->device);
-  const int64_t t = p->next_ticket;
-  int slot;
-  int rc = acquire_slot(p, t, &slot);
-  if (rc) return rc;
-  if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
-  if (!p->exec) {
-    cudaGraph_t g;
-    CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    rc = enqueue(p, p->phases, 0);
-    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-    if (rc) return rc;
-    CK_CTX(c, e);
-    e = cudaGraphInstantiate(&p->exec, g, 0);
-    cudaGraphDestroy(g);
-    CK_CTX(c, e);
-  }
-  CK_CTX(c, cudaGraphLaunch(p->exec, c->stream));
-  CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
-  p->ev_pending[slot] = true;
-  p->next_ticket = t + 1;
-  if (ticket) *ticket = t;
-  return PK_OK;
-}
-
-static int read_result(pk_pack* p, int slot, double* losses, pk_status* st) {
-  const int32_t* s = reinterpret_cast<const int32_t*>(p->h_ring + (size_t)slot * p->ring_stride);
-  const double* l = reinterpret_cast<const double*>(s + 4);
-  if (st) {
-    st->code = s[0];
-    st->member = s[1];
-    st->index = s[2];
-    st->committed = s[3];
-  }
-  if (losses) memcpy(losses, l, sizeof(double) * p->K);
-  return s[0];
-}
-
-extern "C" int pk_pack_step_wait(pk_pack* p, int64_t ticket, double* losses, pk_status* st) {
-  if (!p || ticket < 0 || ticket >= p->next_ticket || ticket < p->next_ticket - kRing)
-    return PK_ERR_STATE;
-  pk_ctx* c = p->ctx;
-  cudaSetDevice(c->device);
-  const int slot = (int)(ticket % kRing);
-  if (p->ev_pending[slot]) {
-    CK_CTX(c, cudaEventSynchronize(p->ev[slot]));
-    p->ev_pending[slot] = false;
-  }
-  return read_result(p, slot, losses, st);
-}
-
-extern "C" int pk_pack_step(pk_pack* p, const pk_feed* feeds, double* losses, pk_status* st) {
-  int64_t t;
-  int rc = pk_pack_step_async(p, feeds, &t);
-  if (rc) return rc;
-  return pk_pack_step_wait(p, t, losses, st);
-}
-
-extern "C" int pk_pack_eval(pk_pack* p, const pk_dataset* data, const pk_order* order, int64_t pos,
-                            int64_t rows, double* losses, pk_status* st) {
-  if (!p || !data) return PK_ERR_ARG;
-  pk_ctx* c = p->ctx;
-  if (rows < 1 || pos < 0 || pos + rows > data->n) return arg_err(c, "eval: bad row range");
-  cudaSetDevice(c->device);
-  int64_t max_chunks = 0;
-  for (auto* m : p->members) max_chunks = std::max<int64_t>(max_chunks, (rows + m->desc.max_rows - 1) / m->desc.max_rows);
-  std::vector<pk_feed> feeds(p->K);
-  int slot = 0;
-  for (int64_t ch = 0; ch < max_chunks; ++ch) {
-    for (int k = 0; k < p->K; ++k) {
-      const int64_t mr = p->members[k]->desc.max_rows;
-      const int64_t off = ch * mr;
-      const int64_t tk = std::max<int64_t>(0, std::min<int64_t>(mr, rows - off));
-      feeds[k] = pk_feed{data, order, pos + (tk ? off : 0), (int32_t)tk, 0};
-    }
-    const int64_t t = p->next_ticket++;
-    int rc = acquire_slot(p, t, &slot);
-    if (rc) return rc;
-    if ((rc = launch_desc(p, slot, 1, feeds.data()))) return rc;
-    if ((rc = enqueue(p, p->fwd_phases, 1))) return rc;
-    CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
-    p->ev_pending[slot] = true;
-  }
-  const int64_t t = p->next_ticket++;
-  int rc = acquire_slot(p, t, &slot);
-  if (rc) return rc;
-  if (c->dtype == PK_F64)
-    pk::k_eval_finish<double><<<1, 32, 0, c->stream>>>((const MemberDev<double>*)p->d_members, p->K,
-                                                         rows, p->d_ring, slot, p->ring_stride);
-  else
-    pk::k_eval_finish<float><<<1, 32, 0, c->stream>>>((const MemberDev<float>*)p->d_members, p->K,
-                                                        rows, p->d_ring, slot, p->ring_stride);
-  CK_CTX(c, cudaGetLastError());
-  CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));
-  CK_CTX(c, cudaEventSynchronize(p->ev[slot]));
-  p->ev_pending[slot] = false;
-  return read_result(p, slot, losses, st);
-}
-
-extern "C" int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* phase_ms,
-                                    int32_t* phase_kind, int32_t* phase_layer,
-                                    int32_t* phase_ctas, double* losses, pk_status* st) {
-  if (!p || !feeds) return PK_ERR_ARG;
-  pk_ctx* c = p->ctx;
-  cudaSetDevice(c->device);
-  const int64_t t = p->next_ticket++;
-  int slot;
-  int rc = acquire_slot(p, t, &slot);
-  if (rc) return rc;
-  if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
-  const int n = (int)p->phases.size();
-  std::vector<cudaEvent_t> ev(n + 1);
-  for (auto& e : ev) CK_CTX(c, cudaEventCreate(&e));
-  for (int i = 0; i < n; ++i) {
-    CK_CTX(c, cudaEventRecord(ev[i], c->stream));
-    std::vector<Phase> one{p->phases[i]};
-    if ((rc = enqueue(p, one, 0))) return rc;
-  }
-  CK_CTX(c, cudaEventRecord(ev[n], c->stream));
-  CK_CTX(c, cudaEventSynchronize(ev[n]));
-  for (int i = 0; i < n; ++i) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-    const Phase& ph = p->phases[i];
-    if (phase_ms) phase_ms[i] = ms;
-    if (phase_kind) phase_kind[i] = ph.kind;
-    if (phase_layer) phase_layer[i] = ph.layer;
-    if (phase_ctas) phase_ctas[i] = ph.kind == 1 ? p->K : (ph.kind == 3 ? 1 : ph.ntiles);
-  }
-  for (auto& e : ev) cudaEventDestroy(e);
-  return read_result(p, slot, losses, st);
-}
+#include "pk_pack.cuh"

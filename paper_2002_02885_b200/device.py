@@ -41,6 +41,7 @@ def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") 
     for layer in range(n):
         act = batch_size * dims[layer + 1] * es
         total += _al(act) + _al(act if layer + 1 < n else 0) + _al(act)
+    total += _al(batch_size * 8)  # per-row loss terms (float64)
     return total + _al(_CTL_BYTES)
 
 

@@ -257,7 +257,7 @@ def test_host_edit_of_params_is_uploaded():
 def test_nonfinite_input_raises_engine_error_and_commits_nothing():
     ds = data.synth_dataset(120, 6, 3, seed=0)
     x = ds.features.copy()
-    perm = data.epoch_permutation(ds.dataset_id, ds.n, 0)
+    perm = data.epoch_permutation(ds.dataset_id + "-nan", ds.n, 0)
     x[perm[3], 2] = np.nan
     bad = data.Dataset(ds.dataset_id + "-nan", x, ds.labels, 3)
     a, b = _h("a", seed=1), _h("b", seed=2)
