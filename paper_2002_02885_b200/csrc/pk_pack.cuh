@@ -77,7 +77,24 @@ static size_t feed_size(int dtype) {
   return dtype == PK_F64 ? sizeof(FeedDev<double>) : sizeof(FeedDev<float>);
 }
 
-constexpr int kSmemMax = 227 * 1024;
+// dynamic shared memory a k_phase CTA may use (opt-in limit minus the
+// kernel's static smem), set once per precision by pk_pack_create
+static int g_smem_max[2] = {0, 0};
+
+static int smem_budget(int dtype) { return g_smem_max[dtype]; }
+
+template <typename T>
+static cudaError_t init_smem_limit(int device, int* out) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa{};
+  if ((e = cudaFuncGetAttributes(&fa, pk::k_phase<T>)) != cudaSuccess) return e;
+  const int dyn = optin - (int)fa.sharedSizeBytes;
+  e = cudaFuncSetAttribute(pk::k_phase<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (e == cudaSuccess) *out = dyn;
+  return e;
+}
 
 // whether the member's last layer + head + first dgrad fit one TAIL tile
 static bool tail_ok(const pk_member* m, int dtype) {
@@ -85,7 +102,7 @@ static bool tail_ok(const pk_member* m, int dtype) {
   const int in = m->desc.dims[L], C = m->desc.dims[L + 1];
   if (C > pk::TAIL_MAXC) return false;
   const int need = dtype == PK_F64 ? pk::Smem<double>::tail(in, C) : pk::Smem<float>::tail(in, C);
-  return need <= kSmemMax;
+  return need <= smem_budget(dtype);
 }
 
 static int kind_smem(int kind, const pk_member* m, int dtype) {
@@ -233,8 +250,6 @@ static int launch(pk_pack* p, const std::vector<Phase>& ph) {
   return p->ctx->dtype == PK_F64 ? launch_phases<double>(p, ph) : launch_phases<float>(p, ph);
 }
 
-static bool g_smem_attr[2] = {false, false};
-
 extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, pk_pack** out) {
   if (!c || !out || !members || k < 1) return arg_err(c, "pack needs at least one member");
   cudaSetDevice(c->device);
@@ -243,14 +258,14 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
     for (int j = 0; j < i; ++j)
       if (members[j] == members[i]) return arg_err(c, "pack: duplicate member");
   }
-  if (!g_smem_attr[c->dtype]) {
-    cudaError_t e = c->dtype == PK_F64
-                        ? cudaFuncSetAttribute(pk::k_phase<double>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax)
-                        : cudaFuncSetAttribute(pk::k_phase<float>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (!g_smem_max[c->dtype]) {
+    cudaError_t e = c->dtype == PK_F64 ? init_smem_limit<double>(c->device, &g_smem_max[1])
+                                       : init_smem_limit<float>(c->device, &g_smem_max[0]);
     CK_CTX(c, e);
-    g_smem_attr[c->dtype] = true;
+  }
+  for (int i = 0; i < k; ++i) {  // FWD/WGRAD/DGRAD tiles must fit regardless of shape
+    const int need = c->dtype == PK_F64 ? pk::Smem<double>::FWD : pk::Smem<float>::FWD;
+    if (need > g_smem_max[c->dtype]) return arg_err(c, "pack: shared memory budget too small");
   }
   auto* p = new pk_pack();
   p->ctx = c;
