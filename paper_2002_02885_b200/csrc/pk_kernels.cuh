@@ -171,39 +171,29 @@ __device__ __forceinline__ T act_bwd(int act, T z, T a, T d) {
   }
 }
 
-// engine.py:302-324 for one element (c = committed buffer, n = next buffer)
+// engine.py:302-324 for one element, on registers: w, s0, s1 in/out
+// (s0 = velocity | accum | m, s1 = v); bc1/bc2 are Adam's bias corrections
 template <typename T>
-__device__ __forceinline__ void opt_apply(int opt, T lr, T wd, T bc1, T bc2,
-                                          const T* __restrict__ wc, T* __restrict__ wn,
-                                          const T* __restrict__ s0c, T* __restrict__ s0n,
-                                          const T* __restrict__ s1c, T* __restrict__ s1n,
-                                          int64_t i, T g) {
-  T w = wc[i];
+__device__ __forceinline__ void opt_step(int opt, T lr, T wd, T bc1, T bc2, T& w, T& s0, T& s1,
+                                         T g) {
   if (wd != T(0)) g = g + wd * w;
   switch (opt) {
     case PK_OPT_SGD:
-      wn[i] = w - lr * g;
+      w = w - lr * g;
       break;
-    case PK_OPT_MOMENTUM: {
-      T v = s0c[i] * T(0.9) + g;
-      s0n[i] = v;
-      wn[i] = w - lr * v;
+    case PK_OPT_MOMENTUM:
+      s0 = s0 * T(0.9) + g;
+      w = w - lr * s0;
       break;
-    }
-    case PK_OPT_ADAGRAD: {
-      T a = s0c[i] + g * g;
-      s0n[i] = a;
-      wn[i] = w - lr * g / (sq(a) + T(1e-10));
+    case PK_OPT_ADAGRAD:
+      s0 = s0 + g * g;
+      w = w - lr * g / (sq(s0) + T(1e-10));
       break;
-    }
-    default: {  // adam
-      T m = s0c[i] * T(0.9) + (T(1) - T(0.9)) * g;
-      T v = s1c[i] * T(0.999) + (T(1) - T(0.999)) * g * g;
-      s0n[i] = m;
-      s1n[i] = v;
-      wn[i] = w - lr * (m / bc1) / (sq(v / bc2) + T(1e-8));
+    default:  // adam
+      s0 = s0 * T(0.9) + (T(1) - T(0.9)) * g;
+      s1 = s1 * T(0.999) + (T(1) - T(0.999)) * g * g;
+      w = w - lr * (s0 / bc1) / (sq(s1 / bc2) + T(1e-8));
       break;
-    }
   }
 }
 
@@ -235,8 +225,11 @@ struct Gemm {
   static_assert(KC % SK == 0, "chunk not divisible by slices");
   static constexpr int KS = KC / SK;
   static constexpr int A_ELEMS = BM * KC, B_ELEMS = BN * KC;
-  static constexpr int A_LD = AK ? KC + 1 : BM + 1;  // padded smem row
-  static constexpr int B_LD = BK ? KC + 1 : BN + 1;
+  static constexpr int VEC = 16 / (int)sizeof(T);  // elements per 16-byte cp.async
+  // smem rows padded by one 16-byte vector: keeps vector alignment and
+  // spreads the k-major reads of consecutive rows over different banks
+  static constexpr int A_LD = AK ? KC + VEC : BM + VEC;
+  static constexpr int B_LD = BK ? KC + VEC : BN + VEC;
   static constexpr int A_STAGE = AK ? BM * A_LD : KC * A_LD;
   static constexpr int B_STAGE = BK ? BN * B_LD : KC * B_LD;
   static constexpr int PIPE = STAGES * (A_STAGE + B_STAGE);
@@ -249,10 +242,46 @@ struct Gemm {
     return (int64_t)(r < ROWCAP ? srow[r] : a.rows[r]) * a.ld;
   }
 
+  // 16-byte path: the contiguous dimension is walked in VEC-element vectors;
+  // the caller guarantees alignment and that extents are VEC multiples
+  __device__ __forceinline__ static void load_chunk_vec(T* sA, T* sB, const Mat<T>& a,
+                                                        const Mat<T>& b, const int32_t* srow,
+                                                        int k0, int m0, int n0, int M, int N,
+                                                        int Kr, bool va, bool vb) {
+    if (va) {
+      for (int e = threadIdx.x; e < A_ELEMS / VEC; e += NT) {
+        int kk, mm;
+        if (AK) { kk = (e % (KC / VEC)) * VEC; mm = e / (KC / VEC); }
+        else { mm = (e % (BM / VEC)) * VEC; kk = e / (BM / VEC); }
+        const int k = k0 + kk, m = m0 + mm;
+        const bool ok = (k < Kr) && (m < M);
+        const T* g = a.base;
+        if (ok) g = AK ? a.base + a_row(a, srow, m) + k : a.base + a_row(a, srow, k) + m;
+        T* s = AK ? sA + mm * A_LD + kk : sA + kk * A_LD + mm;
+        cp_async<16>(s, g, ok);
+      }
+    }
+    if (vb) {
+      for (int e = threadIdx.x; e < B_ELEMS / VEC; e += NT) {
+        int kk, nn;
+        if (BK) { kk = (e % (KC / VEC)) * VEC; nn = e / (KC / VEC); }
+        else { nn = (e % (BN / VEC)) * VEC; kk = e / (BN / VEC); }
+        const int k = k0 + kk, n = n0 + nn;
+        const bool ok = (k < Kr) && (n < N);
+        const T* g = b.base;
+        if (ok) g = BK ? b.base + (int64_t)n * b.ld + k : b.base + (int64_t)k * b.ld + n;
+        T* s = BK ? sB + nn * B_LD + kk : sB + kk * B_LD + nn;
+        cp_async<16>(s, g, ok);
+      }
+    }
+  }
+
   __device__ __forceinline__ static void load_chunk(T* sA, T* sB, const Mat<T>& a, const Mat<T>& b,
                                                     const int32_t* srow, int chunk, int m0, int n0,
-                                                    int M, int N, int Kr) {
+                                                    int M, int N, int Kr, bool va, bool vb) {
     const int k0 = chunk * KC;
+    load_chunk_vec(sA, sB, a, b, srow, k0, m0, n0, M, N, Kr, va, vb);
+    if (!va)
 #pragma unroll 2
     for (int e = threadIdx.x; e < A_ELEMS; e += NT) {
       int kk, mm;
@@ -264,6 +293,7 @@ struct Gemm {
       T* s = AK ? sA + mm * A_LD + kk : sA + kk * A_LD + mm;
       cp_async<sizeof(T)>(s, g, ok);
     }
+    if (!vb)
 #pragma unroll 2
     for (int e = threadIdx.x; e < B_ELEMS; e += NT) {
       int kk, nn;
@@ -277,12 +307,23 @@ struct Gemm {
     }
   }
 
-  // srow: gather indices for A's gathered dimension, already in smem (for
-  // AK the tile's rows m0.., i.e. srow[m - m0] is NOT used: pass rows
-  // relative to 0 via a.rows/row0 and srow indexed by absolute row).
-  __device__ __forceinline__ static void run(T* smem, const Mat<T>& a, const Mat<T>& b,
-                                             const int32_t* srow, int m0, int n0, int M, int N,
-                                             int Kr) {
+  // whether an operand may take the 16-byte path: aligned base, row pitch
+  // and the extent of its contiguous dimension all multiples of VEC
+  __device__ __forceinline__ static bool vec_ok(const Mat<T>& x, int contig_extent) {
+    return ((reinterpret_cast<uintptr_t>(x.base) & 15) == 0) && (x.ld % VEC == 0) &&
+           (contig_extent % VEC == 0);
+  }
+
+  // srow: gather indices for A's gathered dimension (m if AK, k otherwise),
+  // staged in smem, indexed by absolute row.  CHECK_A: return whether any A
+  // element of the tile is non-finite (block-wide).  COLSUM: threads t < BN
+  // accumulate Σ_k B(k, n0+t) into *colsum, k ascending (the bias gradient).
+  template <bool CHECK_A = false, bool COLSUM = false>
+  __device__ __forceinline__ static int run(T* smem, const Mat<T>& a, const Mat<T>& b,
+                                            const int32_t* srow, int m0, int n0, int M, int N,
+                                            int Kr, T* colsum = nullptr) {
+    const bool va = vec_ok(a, AK ? Kr : M);
+    const bool vb = vec_ok(b, BK ? Kr : N);
     const int slice = threadIdx.x / TPS, lt = threadIdx.x % TPS;
     const int tc = lt % CS, tr = lt / CS;
     T acc[TM][TN];
@@ -290,19 +331,21 @@ struct Gemm {
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    bool bad = false;
+    T csum = T(0);
     const int nch = (Kr + KC - 1) / KC;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < nch)
         load_chunk(smem + s * (A_STAGE + B_STAGE), smem + s * (A_STAGE + B_STAGE) + A_STAGE, a,
-                   b, srow, s, m0, n0, M, N, Kr);
+                   b, srow, s, m0, n0, M, N, Kr, va, vb);
       cp_commit();
     }
     for (int c = 0; c < nch; ++c) {
       const int pre = c + STAGES - 1;
       if (pre < nch) {
         T* st = smem + (pre % STAGES) * (A_STAGE + B_STAGE);
-        load_chunk(st, st + A_STAGE, a, b, srow, pre, m0, n0, M, N, Kr);
+        load_chunk(st, st + A_STAGE, a, b, srow, pre, m0, n0, M, N, Kr, va, vb);
       }
       cp_commit();
       cp_wait<STAGES - 1>();
@@ -314,8 +357,10 @@ struct Gemm {
         const int kk = slice * KS + q;
         T av[TM], bv[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i) {
           av[i] = AK ? sA[(tr + i * RS) * A_LD + kk] : sA[kk * A_LD + tr + i * RS];
+          if (CHECK_A) bad |= !finite(av[i]);
+        }
 #pragma unroll
         for (int j = 0; j < TN; ++j)
           bv[j] = BK ? sB[(tc + j * CS) * B_LD + kk] : sB[kk * B_LD + tc + j * CS];
@@ -324,15 +369,21 @@ struct Gemm {
 #pragma unroll
           for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
       }
+      if (COLSUM && threadIdx.x < BN) {
+#pragma unroll 8
+        for (int kk = 0; kk < KC; ++kk)
+          csum += BK ? sB[threadIdx.x * B_LD + kk] : sB[kk * B_LD + threadIdx.x];
+      }
       __syncthreads();
     }
     cp_wait<0>();
+    if (COLSUM && threadIdx.x < BN) *colsum = csum;
     T* red = smem + slice * (BM * BN);
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) red[(tr + i * RS) * BN + tc + j * CS] = acc[i][j];
-    __syncthreads();
+    return __syncthreads_or(bad);
   }
 
   __device__ __forceinline__ static T value(const T* smem, int mm, int nn) {
@@ -365,7 +416,7 @@ struct Smem {
   // TAIL: pipeline + resident W_L [in x C] + dZ block [32 x 33] + rows
   __host__ __device__ static int tail(int in, int C) {
     return TailG<T>::SMEM_T * (int)sizeof(T) + in * C * (int)sizeof(T) +
-           TAIL_BM * (TAIL_MAXC + 1) * (int)sizeof(T) + ROWS;
+           TAIL_BM * (TAIL_MAXC + 1) * (int)sizeof(T) + ROWS + TAIL_BM * 4;
   }
 };
 
@@ -405,9 +456,12 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   __syncthreads();
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{W, nullptr, 0, out};
-  G::run(smem, a, b, srow, t.m0, t.n0, R, out, in);
+  // layer 0: the input node's finite check (engine.py:233-235) rides on the
+  // A operand already staged in shared memory
+  const int badx = (l == 0) ? G::template run<true>(smem, a, b, srow, t.m0, t.n0, R, out, in)
+                            : G::template run<false>(smem, a, b, srow, t.m0, t.n0, R, out, in);
   const bool last = (l == M.n_layers - 1);
-  int bad = INT_MAX;
+  int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < FWD_BM * FWD_BN; e += NT) {
     const int mm = e / FWD_BN, nn = e % FWD_BN;
     const int m = t.m0 + mm, n = t.n0 + nn;
@@ -420,15 +474,6 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
       M.A[l][(int64_t)m * out + n] = av;
       if (!finite(av)) bad = min(bad, 2 + 2 * l);
     }
-  }
-  if (l == 0) {  // the input node (engine.py:233-235 checks it too)
-    bool badx = false;
-    for (int e = threadIdx.x; e < FWD_BM * in; e += NT) {
-      const int mm = e / in, k = e % in;
-      if (t.m0 + mm >= R || t.n0 != 0) break;
-      badx |= !finite(f.feat[feed_row(f, t.m0 + mm) * f.ld + k]);
-    }
-    if (badx) bad = 0;
   }
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
 }
@@ -466,14 +511,17 @@ __device__ void head_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
                           bool train) {
   const int L = M.n_layers - 1, C = M.dims[L + 1];
   const int R = f.take;
+  int32_t* ylab = reinterpret_cast<int32_t*>(sm);
+  if (threadIdx.x < HEAD_BM && t.m0 + (int)threadIdx.x < R)
+    ylab[threadIdx.x] = f.labels[feed_row(f, t.m0 + threadIdx.x)];
   pdl_wait();
+  __syncthreads();
   const int warp = threadIdx.x >> 5;
-  for (int r = t.m0 + warp; r < min(R, t.m0 + HEAD_BM); r += NT / 32) {
-    const int y = f.labels[feed_row(f, r)];
-    xent_row(M.Z[L] + (int64_t)r * C, M.dZ[L] + (int64_t)r * C, C, y, R, train,
+  for (int mm = warp; mm < HEAD_BM && t.m0 + mm < R; mm += NT / 32) {
+    const int r = t.m0 + mm;
+    xent_row(M.Z[L] + (int64_t)r * C, M.dZ[L] + (int64_t)r * C, C, ylab[mm], R, train,
              M.rowloss + r);
   }
-  (void)sm;
 }
 
 // --------------------------------------------------------------- TAIL --
@@ -485,25 +533,29 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   const int R = f.take;
   T* smem = reinterpret_cast<T*>(sm);
   T* sW = smem + G::SMEM_T;                 // W_L [in][C]
-  T* sD = sW + in * C;                      // dZ block [32][TAIL_MAXC+1]
+  T* sD = sW + in * C;                      // logits → dlogits block [32][TAIL_MAXC+1]
   int32_t* srow = reinterpret_cast<int32_t*>(sD + TAIL_BM * (TAIL_MAXC + 1));
+  int32_t* ylab = srow + ROWCAP;            // labels of the block's rows
   const int par = M.ctl->parity;
   const T* W = M.params[par] + M.w_off[L];
   const T* bias = M.params[par] + M.b_off[L];
-  // W_L is a parameter: stage it before waiting on the previous phase
+  // parameters and labels do not depend on the previous phase: fetch them
+  // before waiting on it
   const bool dgrad = train && L > 0;
   if (dgrad) {
     for (int e = threadIdx.x; e < in * C; e += NT) cp_async<sizeof(T)>(sW + e, W + e, true);
     cp_commit();
   }
+  if (threadIdx.x < TAIL_BM && t.m0 + (int)threadIdx.x < R)
+    ylab[threadIdx.x] = f.labels[feed_row(f, t.m0 + threadIdx.x)];
   if (L == 0) stage_rows(srow, f, R);
   if (L > 0) pdl_wait();
   __syncthreads();
   const Mat<T> a = input_mat(M, f, L);
   const Mat<T> b{W, nullptr, 0, C};
-  G::run(smem, a, b, srow, t.m0, 0, R, C, in);
-  // logits (+ bias) → Z_L and into sD; input / logit finite checks
-  int bad = INT_MAX;
+  const int badx = (L == 0) ? G::template run<true>(smem, a, b, srow, t.m0, 0, R, C, in)
+                            : G::template run<false>(smem, a, b, srow, t.m0, 0, R, C, in);
+  int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < TAIL_BM * TAIL_MAXC; e += NT) {
     const int mm = e / TAIL_MAXC, c = e % TAIL_MAXC;
     const int m = t.m0 + mm;
@@ -513,26 +565,13 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
     sD[mm * (TAIL_MAXC + 1) + c] = z;
     if (!finite(z)) bad = min(bad, 1 + 2 * L);
   }
-  if (L == 0) {
-    bool badx = false;
-    for (int e = threadIdx.x; e < TAIL_BM * in; e += NT) {
-      const int mm = e / in, k = e % in;
-      if (t.m0 + mm >= R) break;
-      badx |= !finite(f.feat[feed_row(f, t.m0 + mm) * f.ld + k]);
-    }
-    if (badx) bad = 0;
-  }
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   __syncthreads();
   // softmax-xent per row, in place in sD (logits → dlogits)
   const int warp = threadIdx.x >> 5;
-  for (int mm = warp; mm < TAIL_BM; mm += NT / 32) {
-    const int m = t.m0 + mm;
-    if (m >= R) break;
-    const int y = f.labels[feed_row(f, m)];
+  for (int mm = warp; mm < TAIL_BM && t.m0 + mm < R; mm += NT / 32) {
     T* row = sD + mm * (TAIL_MAXC + 1);
-    xent_row(row, row, C, y, R, train, M.rowloss + m);
-    __syncwarp();
+    xent_row(row, row, C, ylab[mm], R, train, M.rowloss + t.m0 + mm);
   }
   if (!train) return;
   __syncthreads();
@@ -543,20 +582,36 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   if (!dgrad) return;
   cp_wait<0>();
   __syncthreads();
-  // dZ_{L-1}[m][i] = act'(Z,A)[m][i] · Σ_c dZ_L[m][c] W_L[i][c]
-  const T* Zp = M.Z[L - 1];
-  const T* Ap = M.A[L - 1];
-  T* dZp = M.dZ[L - 1];
-  for (int e = threadIdx.x; e < TAIL_BM * in; e += NT) {
-    const int mm = e / in, i = e % in;
-    const int m = t.m0 + mm;
-    if (m >= R) break;
-    const T* d = sD + mm * (TAIL_MAXC + 1);
-    const T* w = sW + i * C;
-    T s = T(0);
-    for (int c = 0; c < C; ++c) s = fma(d[c], w[c], s);
-    const int64_t o = (int64_t)m * in + i;
-    dZp[o] = act_bwd(M.act, Zp[o], Ap[o], s);
+  // dZ_{L-1}[m][i] = act'(Z,A)[m][i] · Σ_c dZ_L[m][c] W_L[i][c]; the Z/A
+  // operands of a batch of outputs are loaded before any is computed
+  const T* __restrict__ Zp = M.Z[L - 1];
+  const T* __restrict__ Ap = M.A[L - 1];
+  T* __restrict__ dZp = M.dZ[L - 1];
+  const int rows = min(TAIL_BM, R - t.m0);
+  const int total = rows * in;
+  constexpr int B8 = 8;
+  for (int e0 = 0; e0 < total; e0 += NT * B8) {
+    T zv[B8], avv[B8];
+#pragma unroll
+    for (int u = 0; u < B8; ++u) {
+      const int e = e0 + u * NT + threadIdx.x;
+      if (e < total) {
+        const int64_t o = (int64_t)(t.m0 + e / in) * in + e % in;
+        zv[u] = Zp[o];
+        avv[u] = Ap[o];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B8; ++u) {
+      const int e = e0 + u * NT + threadIdx.x;
+      if (e >= total) break;
+      const int mm = e / in, i = e % in;
+      const T* d = sD + mm * (TAIL_MAXC + 1);
+      const T* w = sW + i * C;
+      T s = T(0);
+      for (int c = 0; c < C; ++c) s = fma(d[c], w[c], s);
+      dZp[(int64_t)(t.m0 + mm) * in + i] = act_bwd(M.act, zv[u], avv[u], s);
+    }
   }
 }
 
@@ -573,12 +628,24 @@ __device__ void dgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const Mat<T> a{M.dZ[l], nullptr, 0, out};
   const Mat<T> b{W, nullptr, 0, out};  // B(k=j, n=i) = W[i][j]
   G::run(smem, a, b, nullptr, t.m0, t.n0, R, in, out);
-  for (int e = threadIdx.x; e < DG_BM * DG_BN; e += NT) {
+  constexpr int PER = DG_BM * DG_BN / NT;
+  T zv[PER], avv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = u * NT + threadIdx.x;
+    const int m = t.m0 + e / DG_BN, n = t.n0 + e % DG_BN;
+    if (m < R && n < in) {
+      zv[u] = M.Z[l - 1][(int64_t)m * in + n];
+      avv[u] = M.A[l - 1][(int64_t)m * in + n];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = u * NT + threadIdx.x;
     const int mm = e / DG_BN, nn = e % DG_BN;
     const int m = t.m0 + mm, n = t.n0 + nn;
-    if (m >= R || n >= in) continue;
-    const int64_t o = (int64_t)m * in + n;
-    M.dZ[l - 1][o] = act_bwd(M.act, M.Z[l - 1][o], M.A[l - 1][o], G::value(smem, mm, nn));
+    if (m < R && n < in)
+      M.dZ[l - 1][(int64_t)m * in + n] = act_bwd(M.act, zv[u], avv[u], G::value(smem, mm, nn));
   }
 }
 
@@ -593,33 +660,31 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const MemberCtl* ctl = M.ctl;
   const int par = ctl->parity;
   const int64_t P = M.n_params;
-  const T* wc = M.params[par];
-  T* wn = M.params[par ^ 1];
+  const T* __restrict__ wc = M.params[par];
+  T* __restrict__ wn = M.params[par ^ 1];
   const T* sc = M.slots[par];
   T* sn = M.slots[par ^ 1];
   // pull this tile's weights + slots toward L2 while the previous phase drains
-  {
-    const int r = threadIdx.x;
-    if (r < WG_BM && t.m0 + r < in) {
-      const int64_t row = M.w_off[l] + (int64_t)(t.m0 + r) * out + t.n0;
-      const int cnt = min(WG_BN, out - t.n0);
-      for (int s = -1; s < M.n_slots; ++s) {
-        const T* base = s < 0 ? wc : sc + (int64_t)s * P;
-        const char* p0 = reinterpret_cast<const char*>(base + row);
-        const char* p1 = reinterpret_cast<const char*>(base + row + cnt);
-        const char* a0 = reinterpret_cast<const char*>((uintptr_t)p0 & ~(uintptr_t)15);
-        const uint32_t bytes = (uint32_t)(((p1 - a0) + 15) & ~15);
-        l2_prefetch(a0, bytes);
-      }
+  if ((int)threadIdx.x < WG_BM && t.m0 + (int)threadIdx.x < in) {
+    const int64_t row = M.w_off[l] + (int64_t)(t.m0 + threadIdx.x) * out + t.n0;
+    const int cnt = min(WG_BN, out - t.n0);
+    for (int s = -1; s < M.n_slots; ++s) {
+      const T* base = s < 0 ? wc : sc + (int64_t)s * P;
+      const uintptr_t p0 = reinterpret_cast<uintptr_t>(base + row) & ~(uintptr_t)15;
+      const uintptr_t p1 = reinterpret_cast<uintptr_t>(base + row + cnt);
+      l2_prefetch(reinterpret_cast<const void*>(p0), (uint32_t)((p1 - p0 + 15) & ~(uintptr_t)15));
     }
   }
   if (l == 0) stage_rows(srow, f, R);
   pdl_wait();
   __syncthreads();
-  // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]
+  // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]; tiles on the first
+  // row block also sum dZ_l's columns (the bias gradient) from the staged B
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{M.dZ[l], nullptr, 0, out};
-  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R);
+  T gb = T(0);
+  if (t.m0 == 0) G::template run<false, true>(smem, a, b, srow, t.m0, t.n0, in, out, R, &gb);
+  else G::template run<false, false>(smem, a, b, srow, t.m0, t.n0, in, out, R);
   const T lr = T(ctl->lr), wd = T(M.wd);
   T bc1 = T(1), bc2 = T(1);
   if (M.opt == PK_OPT_ADAM) {
@@ -627,32 +692,53 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
     bc1 = T(1.0 - pow(0.9, tt));
     bc2 = T(1.0 - pow(0.999, tt));
   }
-  const T* s0c = sc;
-  T* s0n = sn;
-  const T* s1c = sc ? sc + P : nullptr;
-  T* s1n = sn ? sn + P : nullptr;
+  const T* __restrict__ s0c = sc;
+  T* __restrict__ s0n = sn;
+  const T* __restrict__ s1c = sc ? sc + P : nullptr;
+  T* __restrict__ s1n = sn ? sn + P : nullptr;
   const int gpos = 2 * (M.n_layers - 1 - l);
-  bool badW = false, badB = false;
-  for (int e = threadIdx.x; e < WG_BM * WG_BN; e += NT) {
-    const int mm = e / WG_BN, nn = e % WG_BN;
-    const int m = t.m0 + mm, n = t.n0 + nn;
-    if (m >= in || n >= out) continue;
-    T g = G::value(smem, mm, nn);
-    if (ctl->fault_grad == gpos) g = T(NAN);
-    badW |= !finite(g);
-    opt_apply(M.opt, lr, wd, bc1, bc2, wc, wn, s0c, s0n, s1c, s1n,
-              M.w_off[l] + (int64_t)m * out + n, g);
-  }
-  if (t.m0 == 0 && threadIdx.x < WG_BN) {
-    const int n = t.n0 + threadIdx.x;
-    if (n < out) {
-      const T* dZ = M.dZ[l];
-      T g = T(0);
-      for (int r = 0; r < R; ++r) g += dZ[(int64_t)r * out + n];
-      if (ctl->fault_grad == gpos + 1) g = T(NAN);
-      badB = !finite(g);
-      opt_apply(M.opt, lr, wd, bc1, bc2, wc, wn, s0c, s0n, s1c, s1n, M.b_off[l] + n, g);
+  const int fault = ctl->fault_grad;
+  // optimizer epilogue: gather every operand of the thread's elements first,
+  // then update — one memory round trip per tensor, not per element
+  constexpr int PER = WG_BM * WG_BN / NT;
+  int64_t idx[PER];
+  bool ok[PER];
+  T w[PER], s0[PER], s1[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = u * NT + threadIdx.x;
+    const int m = t.m0 + e / WG_BN, n = t.n0 + e % WG_BN;
+    ok[u] = (m < in && n < out);
+    idx[u] = M.w_off[l] + (int64_t)m * out + n;
+    if (ok[u]) {
+      w[u] = wc[idx[u]];
+      if (M.n_slots >= 1) s0[u] = s0c[idx[u]];
+      if (M.n_slots >= 2) s1[u] = s1c[idx[u]];
     }
+  }
+  bool badW = false;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    if (!ok[u]) continue;
+    const int e = u * NT + threadIdx.x;
+    T g = G::value(smem, e / WG_BN, e % WG_BN);
+    if (fault == gpos) g = T(NAN);
+    badW |= !finite(g);
+    opt_step(M.opt, lr, wd, bc1, bc2, w[u], s0[u], s1[u], g);
+    wn[idx[u]] = w[u];
+    if (M.n_slots >= 1) s0n[idx[u]] = s0[u];
+    if (M.n_slots >= 2) s1n[idx[u]] = s1[u];
+  }
+  bool badB = false;
+  if (t.m0 == 0 && (int)threadIdx.x < WG_BN && t.n0 + (int)threadIdx.x < out) {
+    const int64_t i = M.b_off[l] + t.n0 + threadIdx.x;
+    if (fault == gpos + 1) gb = T(NAN);
+    badB = !finite(gb);
+    T bw = wc[i], b0 = M.n_slots >= 1 ? s0c[i] : T(0), b1 = M.n_slots >= 2 ? s1c[i] : T(0);
+    opt_step(M.opt, lr, wd, bc1, bc2, bw, b0, b1, gb);
+    wn[i] = bw;
+    if (M.n_slots >= 1) s0n[i] = b0;
+    if (M.n_slots >= 2) s1n[i] = b1;
   }
   if (badW) flag_min(&M.ctl->bad_grad, gpos);
   if (badB) flag_min(&M.ctl->bad_grad, gpos + 1);
@@ -738,9 +824,13 @@ __device__ void prefetch_params(const PhaseArgs<T>& P) {
     const MemberDev<T>& M = P.mems[k];
     const int par = M.ctl->parity;
     for (int s = -1; s < M.n_slots; ++s) {
-      const char* p = reinterpret_cast<const char*>(s < 0 ? M.params[par]
-                                                          : M.slots[par] + (int64_t)s * M.n_params);
-      const int64_t bytes = ((int64_t)M.n_params * (int64_t)sizeof(T) + 15) & ~15LL;
+      // bulk prefetch needs 16-byte aligned address and size: round the
+      // region out (slab regions are 256-byte padded, so this stays inside)
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(
+          s < 0 ? M.params[par] : M.slots[par] + (int64_t)s * M.n_params);
+      const uintptr_t hi = lo + (uintptr_t)M.n_params * sizeof(T);
+      const char* p = reinterpret_cast<const char*>(lo & ~(uintptr_t)15);
+      const int64_t bytes = (int64_t)(((hi + 15) & ~(uintptr_t)15) - (lo & ~(uintptr_t)15));
       const int64_t nch = (bytes + CH - 1) / CH;
       for (int64_t c = (gt - base % gs + gs) % gs; c < nch; c += gs) {
         const int64_t off = c * CH;
