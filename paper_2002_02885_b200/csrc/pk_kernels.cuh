@@ -56,7 +56,16 @@ struct MemberCtl {
   double lr;
   double loss;         // last step loss
   double eval_acc;     // eval: running sum of per-row losses
+  double bc1, bc2;     // Adam bias corrections 1-β^t for t = step_counter + 1
 };
+
+// 1 - beta^t in float64, t = the update about to be applied (engine.py:322-323)
+__host__ __device__ inline void adam_bias_corrections(int64_t step_counter, double* bc1,
+                                                      double* bc2) {
+  const double t = double(step_counter + 1);
+  *bc1 = 1.0 - pow(0.9, t);
+  *bc2 = 1.0 - pow(0.999, t);
+}
 
 template <typename T>
 struct MemberDev {
@@ -318,10 +327,10 @@ struct Gemm {
   // staged in smem, indexed by absolute row.  CHECK_A: return whether any A
   // element of the tile is non-finite (block-wide).  COLSUM: threads t < BN
   // accumulate Σ_k B(k, n0+t) into *colsum, k ascending (the bias gradient).
-  template <bool CHECK_A = false, bool COLSUM = false>
   __device__ __forceinline__ static int run(T* smem, const Mat<T>& a, const Mat<T>& b,
                                             const int32_t* srow, int m0, int n0, int M, int N,
-                                            int Kr, T* colsum = nullptr) {
+                                            int Kr, bool CHECK_A = false, T* colsum = nullptr) {
+    const bool COLSUM = colsum != nullptr;
     const bool va = vec_ok(a, AK ? Kr : M);
     const bool vb = vec_ok(b, BK ? Kr : N);
     const int slice = threadIdx.x / TPS, lt = threadIdx.x % TPS;
@@ -352,7 +361,7 @@ struct Gemm {
       __syncthreads();
       const T* sA = smem + (c % STAGES) * (A_STAGE + B_STAGE);
       const T* sB = sA + A_STAGE;
-#pragma unroll
+#pragma unroll 4
       for (int q = 0; q < KS; ++q) {
         const int kk = slice * KS + q;
         T av[TM], bv[TN];
@@ -458,8 +467,8 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   const Mat<T> b{W, nullptr, 0, out};
   // layer 0: the input node's finite check (engine.py:233-235) rides on the
   // A operand already staged in shared memory
-  const int badx = (l == 0) ? G::template run<true>(smem, a, b, srow, t.m0, t.n0, R, out, in)
-                            : G::template run<false>(smem, a, b, srow, t.m0, t.n0, R, out, in);
+  const int badx = (l == 0) ? G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, true)
+                            : G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, false);
   const bool last = (l == M.n_layers - 1);
   int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < FWD_BM * FWD_BN; e += NT) {
@@ -553,8 +562,8 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   __syncthreads();
   const Mat<T> a = input_mat(M, f, L);
   const Mat<T> b{W, nullptr, 0, C};
-  const int badx = (L == 0) ? G::template run<true>(smem, a, b, srow, t.m0, 0, R, C, in)
-                            : G::template run<false>(smem, a, b, srow, t.m0, 0, R, C, in);
+  const int badx = (L == 0) ? G::run(smem, a, b, srow, t.m0, 0, R, C, in, true)
+                            : G::run(smem, a, b, srow, t.m0, 0, R, C, in, false);
   int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < TAIL_BM * TAIL_MAXC; e += NT) {
     const int mm = e / TAIL_MAXC, c = e % TAIL_MAXC;
@@ -683,14 +692,12 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{M.dZ[l], nullptr, 0, out};
   T gb = T(0);
-  if (t.m0 == 0) G::template run<false, true>(smem, a, b, srow, t.m0, t.n0, in, out, R, &gb);
-  else G::template run<false, false>(smem, a, b, srow, t.m0, t.n0, in, out, R);
+  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr);
   const T lr = T(ctl->lr), wd = T(M.wd);
   T bc1 = T(1), bc2 = T(1);
   if (M.opt == PK_OPT_ADAM) {
-    const double tt = double(ctl->step_counter + 1);
-    bc1 = T(1.0 - pow(0.9, tt));
-    bc2 = T(1.0 - pow(0.999, tt));
+    bc1 = T(ctl->bc1);
+    bc2 = T(ctl->bc2);
   }
   const T* __restrict__ s0c = sc;
   T* __restrict__ s0n = sn;
@@ -750,7 +757,7 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
 // forward non-finite value aborts the step, else members commit in pack
 // order until the first one with a non-finite gradient.
 template <typename T>
-__device__ void finalize(const PhaseArgs<T>& P, bool train) {
+__device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   __shared__ double part[NT];
   const int K = P.K;
   for (int k = 0; k < K; ++k) {
@@ -795,6 +802,7 @@ __device__ void finalize(const PhaseArgs<T>& P, bool train) {
       } else {
         c->parity ^= 1;
         c->step_counter += 1;
+        adam_bias_corrections(c->step_counter, &c->bc1, &c->bc2);
         ++committed;
       }
     }
@@ -814,7 +822,7 @@ __device__ void finalize(const PhaseArgs<T>& P, bool train) {
 // L2 prefetch of every active member's committed params + slots (first
 // phase): the step's dominant HBM stream overlaps the forward pass.
 template <typename T>
-__device__ void prefetch_params(const PhaseArgs<T>& P) {
+__device__ __noinline__ void prefetch_params(const PhaseArgs<T>& P) {
   constexpr uint32_t CH = 16384;
   const int64_t gt = (int64_t)blockIdx.x * NT + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * NT;
@@ -842,7 +850,13 @@ __device__ void prefetch_params(const PhaseArgs<T>& P) {
   }
 }
 
-template <typename T>
+// Kind masks: one lean kernel per tile kind (plus WGRAD|DGRAD and a generic
+// all-kinds kernel for mixed phases of ragged packs).  Keeping each kernel's
+// code to the one path it runs keeps it resident in the SM instruction cache.
+constexpr int KM_FWD = 1 << TK_FWD, KM_TAIL = 1 << TK_TAIL, KM_HEAD = 1 << TK_HEAD;
+constexpr int KM_DGRAD = 1 << TK_DGRAD, KM_WGRAD = 1 << TK_WGRAD, KM_ALL = 31;
+
+template <typename T, int MASK>
 __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
   extern __shared__ __align__(16) char smem_raw[];
   pdl_launch();
@@ -852,22 +866,16 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
   const bool train = (P.hdr->mode == 0);
   if (f.take != 0) {
     const MemberDev<T>& M = P.mems[t.member];
-    switch (t.kind) {
-      case TK_FWD:
-        if (t.m0 < f.take) fwd_tile<T>(smem_raw, M, f, t);
-        break;
-      case TK_TAIL:
-        if (t.m0 < f.take) tail_tile<T>(smem_raw, M, f, t, train);
-        break;
-      case TK_HEAD:
-        if (t.m0 < f.take) head_tile<T>(smem_raw, M, f, t, train);
-        break;
-      case TK_DGRAD:
-        if (t.m0 < f.take) dgrad_tile<T>(smem_raw, M, f, t);
-        break;
-      default:
-        wgrad_tile<T>(smem_raw, M, f, t);
-        break;
+    if ((MASK & KM_FWD) && t.kind == TK_FWD) {
+      if (t.m0 < f.take) fwd_tile<T>(smem_raw, M, f, t);
+    } else if ((MASK & KM_TAIL) && t.kind == TK_TAIL) {
+      if (t.m0 < f.take) tail_tile<T>(smem_raw, M, f, t, train);
+    } else if ((MASK & KM_HEAD) && t.kind == TK_HEAD) {
+      if (t.m0 < f.take) head_tile<T>(smem_raw, M, f, t, train);
+    } else if ((MASK & KM_DGRAD) && t.kind == TK_DGRAD) {
+      if (t.m0 < f.take) dgrad_tile<T>(smem_raw, M, f, t);
+    } else if ((MASK & KM_WGRAD) && t.kind == TK_WGRAD) {
+      wgrad_tile<T>(smem_raw, M, f, t);
     }
   }
   if (!P.is_last) return;

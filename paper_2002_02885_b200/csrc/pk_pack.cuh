@@ -21,6 +21,7 @@ struct Phase {
   int ntiles = 0;
   int smem = 0;            // dynamic shared memory bytes
   int kind = 0;            // dominant tile kind (reporting)
+  int mask = 0;            // OR of (1 << tile kind) present → which kernel
   int layer = -1;          // dominant layer (reporting)
 };
 
@@ -84,15 +85,40 @@ static int g_smem_max[2] = {0, 0};
 static int smem_budget(int dtype) { return g_smem_max[dtype]; }
 
 template <typename T>
+using PhaseKernel = void (*)(const pk::PhaseArgs<T>);
+
+// the lean kernel for a phase's kind mask (see KM_* in pk_kernels.cuh)
+template <typename T>
+static PhaseKernel<T> kernel_for(int mask) {
+  switch (mask) {
+    case pk::KM_FWD: return pk::k_phase<T, pk::KM_FWD>;
+    case pk::KM_TAIL: return pk::k_phase<T, pk::KM_TAIL>;
+    case pk::KM_HEAD: return pk::k_phase<T, pk::KM_HEAD>;
+    case pk::KM_DGRAD: return pk::k_phase<T, pk::KM_DGRAD>;
+    case pk::KM_WGRAD: return pk::k_phase<T, pk::KM_WGRAD>;
+    case pk::KM_WGRAD | pk::KM_DGRAD: return pk::k_phase<T, pk::KM_WGRAD | pk::KM_DGRAD>;
+    default: return pk::k_phase<T, pk::KM_ALL>;
+  }
+}
+
+template <typename T>
 static cudaError_t init_smem_limit(int device, int* out) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  cudaFuncAttributes fa{};
-  if ((e = cudaFuncGetAttributes(&fa, pk::k_phase<T>)) != cudaSuccess) return e;
-  const int dyn = optin - (int)fa.sharedSizeBytes;
-  e = cudaFuncSetAttribute(pk::k_phase<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  if (e == cudaSuccess) *out = dyn;
+  const int masks[] = {pk::KM_FWD, pk::KM_TAIL, pk::KM_HEAD, pk::KM_DGRAD, pk::KM_WGRAD,
+                       pk::KM_WGRAD | pk::KM_DGRAD, pk::KM_ALL};
+  int dyn = optin;
+  for (int mk : masks) {
+    cudaFuncAttributes fa{};
+    if ((e = cudaFuncGetAttributes(&fa, kernel_for<T>(mk))) != cudaSuccess) return e;
+    dyn = std::min(dyn, optin - (int)fa.sharedSizeBytes);
+  }
+  for (int mk : masks)
+    if ((e = cudaFuncSetAttribute(kernel_for<T>(mk), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  dyn)) != cudaSuccess)
+      return e;
+  *out = dyn;
   return e;
 }
 
@@ -204,6 +230,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
         P.smem = std::max(P.smem, kind_smem(kind, p->members[k], dt));
         const double w = double(P.host.size() - before);
         if (w > best) { best = w; P.kind = kind; P.layer = layer; }
+        P.mask |= 1 << kind;
       }
     }
     P.ntiles = (int)P.host.size();
@@ -237,7 +264,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, pk::k_phase<T>, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for<T>(ph.mask), a);
     if (e != cudaSuccess) {
       p->ctx->err = std::string("launch phase: ") + cudaGetErrorString(e);
       return PK_ERR_CUDA;

@@ -307,6 +307,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   ctl.bad_grad = INT_MAX;
   ctl.fault_grad = -1;
   ctl.step_counter = 0;
+  pk::adam_bias_corrections(0, &ctl.bc1, &ctl.bc2);
   ctl.lr = d->learning_rate;
   CK_CTX(c, cudaMemcpyAsync(m->ctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, c->stream));
   CK_CTX(c, cudaStreamSynchronize(c->stream));
@@ -389,6 +390,7 @@ extern "C" int pk_member_set_state(pk_member* m, const double* params, const dou
   ctl.bad_node = INT_MAX;
   ctl.bad_grad = INT_MAX;
   ctl.step_counter = step_counter;
+  pk::adam_bias_corrections(step_counter, &ctl.bc1, &ctl.bc2);
   ctl.lr = m->desc.learning_rate;
   ctl.loss = 0.0;
   ctl.eval_acc = 0.0;

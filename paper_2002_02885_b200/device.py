@@ -12,7 +12,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-_CTL_BYTES = 48          # sizeof(pk::MemberCtl)
+_CTL_BYTES = 64          # sizeof(pk::MemberCtl)
 _ALIGN = 256
 _SLOTS = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
 
