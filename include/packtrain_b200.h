@@ -159,6 +159,12 @@ int pk_pack_eval(pk_pack* p, const pk_dataset* data, const pk_order* order,
 int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* phase_ms,
                          int32_t* phase_kind, int32_t* phase_layer,
                          int32_t* phase_ctas, double* losses, pk_status* st);
+/* profiling: with PK_TRACE=1 in the environment at pack creation, every CTA
+ * of every train phase stamps %globaltimer (ns) at 8 stage boundaries
+ * (entry, operands ready, GEMM done, epilogue 1, epilogue 2, tile done,
+ * finalize start, finalize end) of the most recent step.  Layout:
+ * [phase][cta][8].  Returns the element count (-1 when tracing is off). */
+int64_t pk_pack_trace(pk_pack* p, uint64_t* out, int64_t cap);
 /* number of kernel launches one pk_pack_step enqueues */
 int32_t pk_pack_launches_per_step(const pk_pack* p);
 

@@ -30,7 +30,7 @@ EXPORTS = (
     "pk_member_slot_count", "pk_member_device_bytes", "pk_member_set_lr",
     "pk_member_set_state", "pk_member_get_state", "pk_member_inject_fault",
     "pk_pack_create", "pk_pack_destroy", "pk_pack_step", "pk_pack_step_async",
-    "pk_pack_step_wait", "pk_pack_eval", "pk_pack_profile_step",
+    "pk_pack_step_wait", "pk_pack_eval", "pk_pack_profile_step", "pk_pack_trace",
     "pk_pack_launches_per_step",
 )
 
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pk_pack_eval": (C.c_int, [vp, vp, vp, i64, i64, P(dbl), P(Status)]),
         "pk_pack_profile_step": (C.c_int, [vp, P(Feed), P(C.c_float), P(i32), P(i32),
                                            P(i32), P(dbl), P(Status)]),
+        "pk_pack_trace": (i64, [vp, vp, i64]),
         "pk_pack_launches_per_step": (i32, [vp]),
     }
     for name, (res, args) in sig.items():

@@ -121,7 +121,24 @@ struct PhaseArgs {
   int32_t K;
   int32_t is_last;     // run FINALIZE in the last CTA
   int32_t prefetch;    // issue L2 prefetch of params/slots (first phase)
+  unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
 };
+
+// ---- stage tracing (profiling builds of a step, PK_TRACE=1) -------------
+// Thread 0 of a CTA stamps %globaltimer at stage boundaries:
+//   0 entry, 1 operands/prologue ready, 2 GEMM done, 3 epilogue part 1,
+//   4 epilogue part 2, 5 tile done, 6 finalize start, 7 finalize end.
+constexpr int kTraceSlots = 8;
+__shared__ unsigned long long* pk_trace_slots;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PK_TRACE(i)                                         \
+  do {                                                      \
+    if (threadIdx.x == 0 && pk_trace_slots) pk_trace_slots[(i)] = gtimer(); \
+  } while (0)
 
 // ------------------------------------------------------------ PTX glue --
 
@@ -467,8 +484,10 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   const Mat<T> b{W, nullptr, 0, out};
   // layer 0: the input node's finite check (engine.py:233-235) rides on the
   // A operand already staged in shared memory
+  PK_TRACE(1);
   const int badx = (l == 0) ? G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, true)
                             : G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, false);
+  PK_TRACE(2);
   const bool last = (l == M.n_layers - 1);
   int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < FWD_BM * FWD_BN; e += NT) {
@@ -562,8 +581,10 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   __syncthreads();
   const Mat<T> a = input_mat(M, f, L);
   const Mat<T> b{W, nullptr, 0, C};
+  PK_TRACE(1);
   const int badx = (L == 0) ? G::run(smem, a, b, srow, t.m0, 0, R, C, in, true)
                             : G::run(smem, a, b, srow, t.m0, 0, R, C, in, false);
+  PK_TRACE(2);
   int bad = badx ? 0 : INT_MAX;
   for (int e = threadIdx.x; e < TAIL_BM * TAIL_MAXC; e += NT) {
     const int mm = e / TAIL_MAXC, c = e % TAIL_MAXC;
@@ -582,6 +603,7 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
     T* row = sD + mm * (TAIL_MAXC + 1);
     xent_row(row, row, C, ylab[mm], R, train, M.rowloss + t.m0 + mm);
   }
+  PK_TRACE(3);
   if (!train) return;
   __syncthreads();
   for (int e = threadIdx.x; e < TAIL_BM * C; e += NT) {
@@ -591,6 +613,7 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   if (!dgrad) return;
   cp_wait<0>();
   __syncthreads();
+  PK_TRACE(4);
   // dZ_{L-1}[m][i] = act'(Z,A)[m][i] · Σ_c dZ_L[m][c] W_L[i][c]; the Z/A
   // operands of a batch of outputs are loaded before any is computed
   const T* __restrict__ Zp = M.Z[L - 1];
@@ -692,7 +715,9 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{M.dZ[l], nullptr, 0, out};
   T gb = T(0);
+  PK_TRACE(1);
   G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr);
+  PK_TRACE(2);
   const T lr = T(ctl->lr), wd = T(M.wd);
   T bc1 = T(1), bc2 = T(1);
   if (M.opt == PK_OPT_ADAM) {
@@ -859,6 +884,9 @@ constexpr int KM_DGRAD = 1 << TK_DGRAD, KM_WGRAD = 1 << TK_WGRAD, KM_ALL = 31;
 template <typename T, int MASK>
 __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
   extern __shared__ __align__(16) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
   pdl_launch();
   if (P.prefetch) prefetch_params(P);
   const Tile t = P.tiles[blockIdx.x];
@@ -878,6 +906,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
       wgrad_tile<T>(smem_raw, M, f, t);
     }
   }
+  PK_TRACE(5);
   if (!P.is_last) return;
   // last CTA to finish runs FINALIZE
   __shared__ int last;
@@ -890,7 +919,9 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
   if (!last) return;
   __threadfence();
   pdl_wait();  // all earlier phases complete (a no-op when none pending)
+  PK_TRACE(6);
   finalize<T>(P, train);
+  PK_TRACE(7);
   if (threadIdx.x == 0) *P.done = 0;
 }
 

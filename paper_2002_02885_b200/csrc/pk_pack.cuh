@@ -33,6 +33,8 @@ struct pk_pack {
   char* d_blob = nullptr;     // StepHdr + FeedDev<T>[K]
   size_t blob_bytes = 0;
   int32_t* d_done = nullptr;  // CTA-completion counter for FINALIZE
+  unsigned long long* d_trace = nullptr;  // PK_TRACE=1: stage stamps per CTA
+  size_t trace_len = 0;
   Tile* d_tiles = nullptr;
   std::vector<Phase> train;   // phases of a train step
   std::vector<Phase> eval;    // forward-only phases (validation loss)
@@ -254,6 +256,11 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
     a.K = p->K;
     a.is_last = (i + 1 == phases.size());
     a.prefetch = (i == 0);
+    if (p->d_trace && &phases == &p->train) {  // train phases: [phase][cta][slot]
+      size_t off = 0;
+      for (size_t j = 0; j < i; ++j) off += (size_t)phases[j].ntiles * pk::kTraceSlots;
+      a.trace = p->d_trace + off;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ph.ntiles);
     cfg.blockDim = dim3(pk::NT);
@@ -355,10 +362,26 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
     cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
     p->ev_pending[i] = false;
   }
+  const char* tr = getenv("PK_TRACE");
+  if (tr && tr[0] == '1') {
+    for (auto& ph : p->train) p->trace_len += (size_t)ph.ntiles * pk::kTraceSlots;
+    if ((e = cudaMalloc((void**)&p->d_trace, p->trace_len * 8)) != cudaSuccess) return fail(e);
+    cudaMemsetAsync(p->d_trace, 0, p->trace_len * 8, c->stream);
+  }
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return fail(e);
   c->bytes += hm.size() + p->blob_bytes + all.size() * sizeof(Tile);
   *out = p;
   return PK_OK;
+}
+
+extern "C" int64_t pk_pack_trace(pk_pack* p, uint64_t* out, int64_t cap) {
+  if (!p || !p->d_trace) return -1;
+  cudaSetDevice(p->ctx->device);
+  if (cudaStreamSynchronize(p->ctx->stream) != cudaSuccess) return -1;
+  const int64_t n = std::min<int64_t>(cap, (int64_t)p->trace_len);
+  if (out && n > 0 && cudaMemcpy(out, p->d_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return (int64_t)p->trace_len;
 }
 
 extern "C" int pk_pack_destroy(pk_pack* p) {
@@ -372,6 +395,7 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
   cudaFree(p->d_blob);
   cudaFree(p->d_tiles);
   cudaFree(p->d_done);
+  if (p->d_trace) cudaFree(p->d_trace);
   cudaFreeHost(p->h_desc);
   cudaFreeHost(p->h_ring);
   delete p;

@@ -1,0 +1,73 @@
+"""Stage timeline of one packed step from in-kernel %globaltimer stamps.
+
+    PK_TRACE=1 python tools/trace_step.py [--workload config0] [--warm]
+
+Runs warm-up steps, flushes L2 (unless --warm), runs one traced step through
+the CUDA graph and prints, per phase, when its CTAs entered, had operands,
+finished the GEMM / epilogue parts and retired — relative to the first CTA
+of the step.  A profiling aid, not a benchmark.
+"""
+import argparse
+import ctypes as C
+import os
+import statistics
+import sys
+
+os.environ.setdefault("PK_TRACE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
+
+STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="config0", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--warm", action="store_true", help="no L2 flush before the traced step")
+    ap.add_argument("--steps", type=int, default=3, help="traced steps (last one printed)")
+    a = ap.parse_args()
+    import torch
+    rt = runtime.runtime()
+    stream = torch.cuda.Stream()
+    rt.set_stream(stream.cuda_stream)
+    wl = bench.WORKLOADS[a.workload]
+    datasets, hs = bench._make(wl, data, packing)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    for _ in range(5):
+        packing.packed_step(packed, datasets)
+    flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    for _ in range(a.steps):
+        if not a.warm:
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+        packing.packed_step(packed, datasets)
+    dp = packed._dev[1]
+    n = rt.lib.pk_pack_trace(dp.ptr, None, 0)
+    if n < 0:
+        sys.exit("tracing is off (PK_TRACE=1 must be set before the pack is created)")
+    buf = (C.c_uint64 * n)()
+    rt.lib.pk_pack_trace(dp.ptr, buf, n)
+    arr = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(-1, 8)
+    code, phases, _ = dp.profile()  # only for per-phase CTA counts
+    t0 = arr[arr[:, 0] > 0, 0].min()
+    off = 0
+    plan = bench._phase_plan(wl)
+    for i, (kind, layer, ctas, _) in enumerate(phases):
+        blk = arr[off:off + ctas]
+        off += ctas
+        label = plan[i][0] if i < len(plan) else f"phase{i}"
+        print(f"phase {i} {label:16s} ctas={ctas}")
+        for s, name in enumerate(STAGES):
+            v = blk[:, s]
+            v = v[v > 0] - t0
+            if len(v):
+                print(f"   {name:6s} min {v.min() / 1e3:8.2f}  med {statistics.median(v) / 1e3:8.2f}"
+                      f"  max {v.max() / 1e3:8.2f} us   (n={len(v)})")
+
+
+if __name__ == "__main__":
+    main()
