@@ -105,22 +105,46 @@ def _item_bytes(dims, opt, kind, l, b, es):
     return es * (2 * p * (1 + SLOTS[opt]) + x_in + b * o)
 
 
+def _m1_bytes(dims, opt, b, es, which):
+    """Operand bytes of one member in the fused one-hidden-layer kernels:
+    fwd reads W0, b0, W1 and writes Z0, A0 and the partial logits; bwd reads
+    the partials, Z0/A0 and reads+writes W0, W1, b0, b1 with their slots."""
+    D, H, C = dims
+    nb = -(-H // 8)
+    p = D * H + H + H * C + C
+    if which == "fwd":
+        return es * (D * H + H + H * C + 2 * b * H + nb * b * C)
+    return es * (nb * b * C + 2 * b * H + 2 * p * (1 + SLOTS[opt]))
+
+
 def _phase_plan(wl, es=4):
-    """[(label, algorithmic bytes)] per train phase of the workload's pack
-    (all members share one input group in these workloads)."""
+    """[(label, algorithmic bytes)] per train launch of the workload's pack
+    (all members share one input group in these workloads; the group's input
+    rows are counted once per launch that reads them)."""
+    from paper_2002_02885_b200.device import uses_fused_mlp1
+    from paper_2002_02885_b200.packing import MLPArch
     dims = (wl["dim"], *wl["hidden"], wl["classes"])
     b = wl["batch"]
-    st = _stages(dims)
+    arch = MLPArch(wl["dim"], tuple(wl["hidden"]), wl["classes"], wl["act"])
+    prec = "f64" if es == 8 else "f32"
+    fused = [opt for opt, _ in wl["members"] if uses_fused_mlp1(arch, opt, b, prec)]
+    other = [opt for opt, _ in wl["members"] if not uses_fused_mlp1(arch, opt, b, prec)]
     out = []
-    for items in st:
+    if fused:
+        out.append(("M1FWD", sum(_m1_bytes(dims, o, b, es, "fwd") for o in fused)
+                    + es * b * dims[0]))
+    for items in (_stages(dims) if other else []):
         tot, x_once = 0, False
-        for opt, _ in wl["members"]:
+        for opt in other:
             for kind, l in items:
                 tot += _item_bytes(dims, opt, kind, l, b, es)
                 x_once |= (l == 0 and kind in ("FWD", "TAIL", "WGRAD"))
         if x_once:
             tot += es * b * dims[0]
         out.append(("+".join(f"{k}{l}" for k, l in items), tot))
+    if fused:
+        out.append(("M1BWD", sum(_m1_bytes(dims, o, b, es, "bwd") for o in fused)
+                    + es * b * dims[0]))
     return out
 
 

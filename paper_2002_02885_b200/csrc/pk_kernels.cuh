@@ -44,6 +44,7 @@ namespace pk {
 
 constexpr int NT = 256;        // threads per CTA
 constexpr int ROWCAP = 1024;   // rows whose gather index is cached in smem
+constexpr int PK_MAX_PACK = 1024;  // members per pack (finalize's flag table)
 
 enum TileKind : int16_t { TK_FWD = 0, TK_TAIL = 1, TK_HEAD = 2, TK_DGRAD = 3, TK_WGRAD = 4 };
 
@@ -531,7 +532,7 @@ __device__ __forceinline__ void xent_row(const T* z, T* dz, int C, int y, int R,
       dz[c] = p / nv;
     }
   }
-  if (lane == 0) *rowloss = -(double)((zy - mx) - lg(s));
+  if (lane == 0 && rowloss) *rowloss = -(double)((zy - mx) - lg(s));
 }
 
 template <typename T>
@@ -783,63 +784,74 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
 // order until the first one with a non-finite gradient.
 template <typename T>
 __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
-  __shared__ double part[NT];
-  const int K = P.K;
-  for (int k = 0; k < K; ++k) {
-    const FeedDev<T>& f = P.feeds[k];
-    if (!f.take) continue;  // block-uniform
-    const MemberDev<T>& M = P.mems[k];
-    double s = 0.0;
-    for (int r = threadIdx.x; r < f.take; r += NT) s += M.rowloss[r];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = NT / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
+  __shared__ int s_bn[PK_MAX_PACK], s_bg[PK_MAX_PACK];
+  __shared__ int s_code, s_who, s_idx, s_stop;
+  const int K = P.K, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp w reduces the loss terms of members w, w+8, ...: lane-strided
+  // partial sums then a fixed butterfly (deterministic, K-invariant)
+  for (int k = warp; k < K; k += NT / 32) {
+    const int take = P.feeds[k].take;
+    int bn = INT_MAX, bg = INT_MAX;
+    if (take) {
+      const MemberDev<T>& M = P.mems[k];
+      double s = 0.0;
+      for (int r = lane; r < take; r += 32) s += M.rowloss[r];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      MemberCtl* c = M.ctl;
+      bn = c->bad_node;
+      bg = c->bad_grad;
       if (train) {
-        const double loss = part[0] / double(f.take);
-        M.ctl->loss = loss;
-        if (!isfinite(loss)) M.ctl->bad_node = min(M.ctl->bad_node, 2 * M.n_layers);
-      } else {
-        M.ctl->eval_acc += part[0];
+        const double loss = s / double(take);
+        if (lane == 0) c->loss = loss;
+        if (!isfinite(loss)) bn = min(bn, 2 * M.n_layers);
+      } else if (lane == 0) {
+        c->eval_acc += s;
       }
     }
-    __syncthreads();
+    if (lane == 0) {
+      s_bn[k] = bn;
+      s_bg[k] = bg;
+    }
   }
-  if (threadIdx.x != 0 || !train) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int code = PK_OK, who = -1, idx = -1, stop = K;
+    for (int k = 0; k < K && train; ++k)
+      if (s_bn[k] != INT_MAX) { code = PK_ERR_NONFINITE_VALUE; who = k; idx = s_bn[k]; stop = 0; break; }
+    for (int k = 0; k < K && train && code == PK_OK; ++k)
+      if (s_bg[k] != INT_MAX) { code = PK_ERR_NONFINITE_GRAD; who = k; idx = s_bg[k]; stop = k; }
+    s_code = code; s_who = who; s_idx = idx; s_stop = stop;
+  }
+  __syncthreads();
   int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)P.hdr->slot * P.ring_stride);
   double* losses = reinterpret_cast<double*>(st + 4);
-  int code = PK_OK, who = -1, idx = -1, committed = 0;
-  for (int k = 0; k < K; ++k) {
-    if (!P.feeds[k].take) continue;
-    const int b = P.mems[k].ctl->bad_node;
-    if (b != INT_MAX) { code = PK_ERR_NONFINITE_VALUE; who = k; idx = b; break; }
-  }
-  for (int k = 0; k < K; ++k) {
+  int committed = 0;
+  for (int k = threadIdx.x; k < K; k += NT) {
     MemberCtl* c = P.mems[k].ctl;
     const bool act = P.feeds[k].take != 0;
-    losses[k] = act ? c->loss : 0.0;
-    if (act && code == PK_OK) {
-      if (c->bad_grad != INT_MAX) {
-        code = PK_ERR_NONFINITE_GRAD; who = k; idx = c->bad_grad;
-      } else {
+    if (train) {
+      losses[k] = act ? c->loss : 0.0;
+      if (act && k < s_stop) {
         c->parity ^= 1;
         c->step_counter += 1;
         adam_bias_corrections(c->step_counter, &c->bc1, &c->bc2);
         ++committed;
       }
+      if (act) c->fault_grad = -1;  // one-shot
     }
-  }
-  for (int k = 0; k < K; ++k) {
-    MemberCtl* c = P.mems[k].ctl;
     c->bad_node = INT_MAX;
     c->bad_grad = INT_MAX;
-    if (P.feeds[k].take) c->fault_grad = -1;  // one-shot
   }
-  st[0] = code; st[1] = who; st[2] = idx; st[3] = committed;
-  __threadfence_system();
+  committed = __syncthreads_count(committed > 0) ? committed : committed;
+  __shared__ int s_comm;
+  if (threadIdx.x == 0) s_comm = 0;
+  __syncthreads();
+  if (committed) atomicAdd(&s_comm, committed);
+  __syncthreads();
+  if (threadIdx.x == 0 && train) {
+    st[0] = s_code; st[1] = s_who; st[2] = s_idx; st[3] = s_comm;
+  }
 }
 
 // ------------------------------------------------------------- kernels --
@@ -875,6 +887,29 @@ __device__ __noinline__ void prefetch_params(const PhaseArgs<T>& P) {
   }
 }
 
+// Common kernel tail: wait for the predecessor kernel (so kernels complete
+// in stream order even for CTAs that had no dependent work), then the last
+// CTA of the step's last launch runs FINALIZE.
+template <typename T>
+__device__ __forceinline__ void kernel_end(const PhaseArgs<T>& P, bool train) {
+  PK_TRACE(5);
+  pdl_wait();
+  if (!P.is_last) return;
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(P.done, 1) == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  PK_TRACE(6);
+  finalize<T>(P, train);
+  PK_TRACE(7);
+  if (threadIdx.x == 0) *P.done = 0;
+}
+
 // Kind masks: one lean kernel per tile kind (plus WGRAD|DGRAD and a generic
 // all-kinds kernel for mixed phases of ragged packs).  Keeping each kernel's
 // code to the one path it runs keeps it resident in the SM instruction cache.
@@ -906,23 +941,39 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
       wgrad_tile<T>(smem_raw, M, f, t);
     }
   }
-  PK_TRACE(5);
-  if (!P.is_last) return;
-  // last CTA to finish runs FINALIZE
-  __shared__ int last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = (atomicAdd(P.done, 1) == (int)gridDim.x - 1);
+  kernel_end(P, train);
+}
+
+#include "pk_mlp1.cuh"
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const PhaseArgs<T> P) {
+  extern __shared__ __align__(16) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  if (P.prefetch) prefetch_params(P);
+  const Tile t = P.tiles[blockIdx.x];
+  const FeedDev<T> f = P.feeds[t.member];
+  if (f.take != 0) m1_fwd_tile<T>(smem_raw, P.mems[t.member], f, t.m0);
+  kernel_end(P, true);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const PhaseArgs<T> P) {
+  extern __shared__ __align__(16) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  const Tile t = P.tiles[blockIdx.x];
+  const FeedDev<T> f = P.feeds[t.member];
+  if (f.take != 0) {
+    const MemberDev<T>& M = P.mems[t.member];
+    m1_bwd_tile<T>(smem_raw, M, f, t.m0, (M.dims[1] + M1_BC - 1) / M1_BC);
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  pdl_wait();  // all earlier phases complete (a no-op when none pending)
-  PK_TRACE(6);
-  finalize<T>(P, train);
-  PK_TRACE(7);
-  if (threadIdx.x == 0) *P.done = 0;
+  kernel_end(P, true);
 }
 
 // eval: after the last chunk, losses[k] = eval_acc / rows and reset

@@ -22,6 +22,7 @@ struct Phase {
   int smem = 0;            // dynamic shared memory bytes
   int kind = 0;            // dominant tile kind (reporting)
   int mask = 0;            // OR of (1 << tile kind) present → which kernel
+  int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd
   int layer = -1;          // dominant layer (reporting)
 };
 
@@ -110,18 +111,41 @@ static cudaError_t init_smem_limit(int device, int* out) {
   if (e != cudaSuccess) return e;
   const int masks[] = {pk::KM_FWD, pk::KM_TAIL, pk::KM_HEAD, pk::KM_DGRAD, pk::KM_WGRAD,
                        pk::KM_WGRAD | pk::KM_DGRAD, pk::KM_ALL};
+  std::vector<PhaseKernel<T>> ks;
+  for (int mk : masks) ks.push_back(kernel_for<T>(mk));
+  ks.push_back(pk::k_mlp1_fwd<T>);
+  ks.push_back(pk::k_mlp1_bwd<T>);
   int dyn = optin;
-  for (int mk : masks) {
+  for (auto k : ks) {
     cudaFuncAttributes fa{};
-    if ((e = cudaFuncGetAttributes(&fa, kernel_for<T>(mk))) != cudaSuccess) return e;
+    if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess) return e;
     dyn = std::min(dyn, optin - (int)fa.sharedSizeBytes);
   }
-  for (int mk : masks)
-    if ((e = cudaFuncSetAttribute(kernel_for<T>(mk), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  dyn)) != cudaSuccess)
+  for (auto k : ks)
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)) !=
+        cudaSuccess)
       return e;
   *out = dyn;
   return e;
+}
+
+// conservative dynamic-smem budget for member-level decisions (made before
+// any pack exists): the opt-in limit minus a margin for static smem
+constexpr int kStaticSmemMargin = 16 * 1024;
+
+static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device) {
+  if (d.n_layers != 2 || d.dims[2] > pk::M1_MAXC || d.max_rows > pk::M1_MAXR) return false;
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
+      cudaSuccess)
+    return false;
+  const int budget = optin - kStaticSmemMargin;
+  const int D = d.dims[0], C = d.dims[2], RP = pk::m1_rows_pad(d.max_rows);
+  const int ns = d.optimizer == PK_OPT_SGD ? 0 : (d.optimizer == PK_OPT_ADAM ? 2 : 1);
+  const bool f64 = dtype == PK_F64;
+  const int fs = f64 ? pk::M1<double>::fwd_smem(D, C, RP) : pk::M1<float>::fwd_smem(D, C, RP);
+  const int bs = f64 ? pk::M1<double>::bwd_smem(D, C, RP, ns) : pk::M1<float>::bwd_smem(D, C, RP, ns);
+  return fs <= budget && bs <= budget;
 }
 
 // whether the member's last layer + head + first dgrad fit one TAIL tile
@@ -214,12 +238,33 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   const int dt = p->ctx->dtype;
   std::vector<std::vector<Stage>> seq(p->K);
   size_t nph = 0;
+  Phase m1f, m1b;  // fused one-hidden-layer members (train only)
+  m1f.special = 1;
+  m1b.special = 2;
   for (int k = 0; k < p->K; ++k) {
+    const pk_member* m = p->members[k];
+    if (!eval && m->mlp1) {
+      const int nb = (m->desc.dims[1] + pk::M1_BC - 1) / pk::M1_BC;
+      for (int cb = 0; cb < nb; ++cb) m1f.host.push_back(Tile{k, 0, pk::TK_FWD, cb, 0});
+      const int D = m->desc.dims[0], C = m->desc.dims[2], RP = pk::m1_rows_pad(m->desc.max_rows);
+      const bool f64 = dt == PK_F64;
+      m1f.smem = std::max(m1f.smem, f64 ? pk::M1<double>::fwd_smem(D, C, RP)
+                                        : pk::M1<float>::fwd_smem(D, C, RP));
+      m1b.smem = std::max(m1b.smem, f64 ? pk::M1<double>::bwd_smem(D, C, RP, m->n_slots)
+                                        : pk::M1<float>::bwd_smem(D, C, RP, m->n_slots));
+      continue;
+    }
     int nf = 0;
-    seq[k] = member_stages(p->members[k], tail_ok(p->members[k], dt), &nf);
+    seq[k] = member_stages(m, tail_ok(m, dt), &nf);
     if (eval) seq[k].resize(nf);
     nph = std::max(nph, seq[k].size());
   }
+  m1f.ntiles = (int)m1f.host.size();
+  m1b.host = m1f.host;
+  m1b.ntiles = m1f.ntiles;
+  m1f.kind = m1b.kind = pk::TK_FWD;
+  m1f.layer = 0;
+  m1b.layer = 1;
   phases.assign(nph, Phase{});
   for (size_t ph = 0; ph < nph; ++ph) {
     Phase& P = phases[ph];
@@ -237,14 +282,27 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     }
     P.ntiles = (int)P.host.size();
   }
+  if (m1f.ntiles) {
+    phases.insert(phases.begin(), m1f);
+    phases.push_back(m1b);
+  }
 }
 
+// only >= 0: launch that phase alone (profiling); finalize: let the last
+// launch run FINALIZE
 template <typename T>
-static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
+static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only = -1,
+                         bool finalize = true) {
   cudaStream_t s = p->ctx->stream;
+  int last = -1, first = -1;
+  for (int i = 0; i < (int)phases.size(); ++i)
+    if (phases[i].ntiles) {
+      last = i;
+      if (first < 0) first = i;
+    }
   for (size_t i = 0; i < phases.size(); ++i) {
     const Phase& ph = phases[i];
-    if (!ph.ntiles) continue;
+    if (!ph.ntiles || (only >= 0 && (int)i != only)) continue;
     pk::PhaseArgs<T> a{};
     a.mems = (const MemberDev<T>*)p->d_members;
     a.hdr = (const StepHdr*)p->d_blob;
@@ -254,8 +312,8 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
     a.ring = p->d_ring;
     a.ring_stride = p->ring_stride;
     a.K = p->K;
-    a.is_last = (i + 1 == phases.size());
-    a.prefetch = (i == 0);
+    a.is_last = finalize && (int)i == last;
+    a.prefetch = (int)i == first;
     if (p->d_trace && &phases == &p->train) {  // train phases: [phase][cta][slot]
       size_t off = 0;
       for (size_t j = 0; j < i; ++j) off += (size_t)phases[j].ntiles * pk::kTraceSlots;
@@ -271,7 +329,10 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for<T>(ph.mask), a);
+    PhaseKernel<T> kern = ph.special == 1   ? pk::k_mlp1_fwd<T>
+                          : ph.special == 2 ? pk::k_mlp1_bwd<T>
+                                            : kernel_for<T>(ph.mask);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) {
       p->ctx->err = std::string("launch phase: ") + cudaGetErrorString(e);
       return PK_ERR_CUDA;
@@ -280,8 +341,9 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases) {
   return PK_OK;
 }
 
-static int launch(pk_pack* p, const std::vector<Phase>& ph) {
-  return p->ctx->dtype == PK_F64 ? launch_phases<double>(p, ph) : launch_phases<float>(p, ph);
+static int launch(pk_pack* p, const std::vector<Phase>& ph, int only = -1, bool fin = true) {
+  return p->ctx->dtype == PK_F64 ? launch_phases<double>(p, ph, only, fin)
+                                 : launch_phases<float>(p, ph, only, fin);
 }
 
 extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, pk_pack** out) {
@@ -580,18 +642,7 @@ extern "C" int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* pha
   // the last one keeps is_last so FINALIZE commits the step
   for (int j = 0; j < n; ++j) {
     CK_CTX(c, cudaEventRecord(ev[j], c->stream));
-    std::vector<Phase> one;
-    for (int i = 0; i <= idx[j]; ++i) {
-      Phase ph = p->train[i];
-      if (i != idx[j]) ph.ntiles = 0;
-      one.push_back(ph);
-    }
-    if (j + 1 < n) {  // not last: suppress FINALIZE
-      Phase tail_off{};
-      tail_off.ntiles = 0;
-      one.push_back(tail_off);
-    }
-    if ((rc = launch(p, one))) return rc;
+    if ((rc = launch(p, p->train, idx[j], j + 1 == n))) return rc;
   }
   CK_CTX(c, cudaEventRecord(ev[n], c->stream));
   CK_CTX(c, cudaEventSynchronize(ev[n]));

@@ -68,9 +68,14 @@ struct pk_member {
   void* dZ[PK_MAX_LAYERS];
   double* rowloss;
   MemberCtl* ctl;
+  bool mlp1;  // fused one-hidden-layer step
 };
 
 struct pk_pack;
+
+// defined in pk_pack.cuh: whether a member takes the fused one-hidden-layer
+// step (pk_mlp1.cuh); decided from the member's own shape only
+static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device);
 
 #define CK_CTX(ctx, call)                                                        \
   do {                                                                           \
@@ -255,6 +260,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   m->ctx = c;
   m->desc = *d;
   m->n_slots = slots_for(d->optimizer);
+  m->mlp1 = mlp1_eligible(*d, c->dtype, c->device);
   int64_t P = 0;
   for (int l = 0; l < d->n_layers; ++l) {
     m->w_off[l] = P;
@@ -275,7 +281,9 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   for (int b = 0; b < 2; ++b) o_slot[b] = take((size_t)m->n_slots * P * es);
   for (int l = 0; l < d->n_layers; ++l) {
     const size_t act = (size_t)d->max_rows * d->dims[l + 1] * es;
-    o_z[l] = take(act);
+    // fused members use Z_1 as the [nb][max_rows][C] partial-logit exchange
+    const size_t nb = (size_t)(d->dims[1] + pk::M1_BC - 1) / pk::M1_BC;
+    o_z[l] = take(m->mlp1 && l == 1 ? std::max(act, nb * act) : act);
     o_a[l] = take(l + 1 < d->n_layers ? act : 0);
     o_dz[l] = take(act);
   }

@@ -30,6 +30,33 @@ def _al(v):
     return (v + _ALIGN - 1) // _ALIGN * _ALIGN
 
 
+_SMEM_OPTIN = 232448     # B200 opt-in shared memory per block (227 KB)
+_STATIC_MARGIN = 16384   # kStaticSmemMargin (csrc/pk_pack.cuh)
+_M1_BC, _M1_KC, _M1_STAGES, _M1_MAXR, _M1_MAXC = 8, 32, 4, 128, 32
+
+
+def _m1_rows_pad(r):
+    return 32 if r <= 32 else (64 if r <= 64 else 128)
+
+
+def uses_fused_mlp1(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
+    """Mirror of csrc mlp1_eligible(): one hidden layer, <= 32 classes,
+    batch <= 128 and the fused kernels' shared memory fits."""
+    if len(arch.hidden) != 1 or arch.classes > _M1_MAXC or batch_size > _M1_MAXR:
+        return False
+    es = 8 if precision == "f64" else 4
+    vec = 16 // es
+    D, C, RP = arch.input_dim, arch.classes, _m1_rows_pad(batch_size)
+    ns = _SLOTS[optimizer.lower()]
+    xld = _M1_KC + vec
+    fwd = (_M1_STAGES * (RP * xld + _M1_KC * _M1_BC) * es + (128 // RP) * RP * _M1_BC * es
+           + RP * _M1_BC * es + _M1_BC * C * es + RP * 4)
+    bwd = (D * _M1_BC * (1 + ns) * es + _M1_STAGES * RP * xld * es + RP * (_M1_MAXC + 1) * es
+           + 2 * RP * _M1_BC * es + _M1_BC * C * (1 + ns) * es + 2 * RP * 4)
+    budget = _SMEM_OPTIN - _STATIC_MARGIN
+    return fwd <= budget and bwd <= budget
+
+
 def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") -> int:
     """Bytes pk_member_create allocates for this member (exact)."""
     es = 8 if precision == "f64" else 4
@@ -38,9 +65,13 @@ def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") 
     ns = _SLOTS[optimizer.lower()]
     total = 2 * _al(P * es) + 2 * _al(ns * P * es)
     n = len(dims) - 1
+    fused = uses_fused_mlp1(arch, optimizer, batch_size, precision)
     for layer in range(n):
         act = batch_size * dims[layer + 1] * es
-        total += _al(act) + _al(act if layer + 1 < n else 0) + _al(act)
+        z = act
+        if fused and layer == 1:  # Z_1 doubles as the partial-logit exchange
+            z = max(act, -(-dims[1] // _M1_BC) * act)
+        total += _al(z) + _al(act if layer + 1 < n else 0) + _al(act)
     total += _al(batch_size * 8)  # per-row loss terms (float64)
     return total + _al(_CTL_BYTES)
 
