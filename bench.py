@@ -15,8 +15,9 @@ optimizer update) of the workload's K members over one batch each.
            one-member packs (standalone_step) on the same GPU.
 Multi-GPU (torchrun): one independent pack per GPU (weak scaling, no
 collective on the data path; the timing max uses NCCL).
-`--impl reference` times the float64 CPU port of the reference path
-(oracle/, numpy) on this host's cores for the same workload.
+`--impl reference` times the reference's own CPU path (`packtrain.packed_step`
+installed unmodified in baseline/_ref; the oracle/ port if absent) on this
+host's cores for the same workload.
 """
 from __future__ import annotations
 
@@ -304,10 +305,11 @@ def _b200(args):
     launches = packed._dev[1].launches
     ach = top["bytes"] / (top["ms"] / 1e3) / 1e9
     traffic = None
+    kname = {"M1FWD": "k_mlp1_fwd", "M1BWD": "k_mlp1_bwd"}.get(top["phase"], "k_phase")
+    kname += "<double>" if args.precision == "f64" else "<float>"
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.workload, {}).get(
-            top["phase"])
+        traffic = json.load(open(tp)).get(args.workload, {}).get(kname)
     desc_bytes = 16 + K * (40 if args.precision == "f32" else 40)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -328,7 +330,7 @@ def _b200(args):
                              "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
                              "d2h_bytes_per_step": 16 + 8 * K,
                              "api": "packed_step(preprocess_spec=normalize(0,1)): host gather"},
-        "roofline": {"bound": "hbm", "kernel": f"k_phase[{top['phase']}]",
+        "roofline": {"bound": "hbm", "kernel": f"{kname}[{top['phase']}]",
                      "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / peaks["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes": top["bytes"], "launch_ms": top["ms"],
@@ -352,26 +354,58 @@ def _cpu_threads():
         return os.cpu_count() or 1
 
 
+def _ref_packtrain():
+    """The unmodified reference package installed in baseline/_ref (pure
+    Python + numpy; `pip install --target baseline/_ref`), or None."""
+    base = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(base, "packtrain")):
+        return None
+    if base not in sys.path:
+        sys.path.insert(0, base)
+    try:
+        from packtrain import data as rdata, packing as rpacking
+        return rdata, rpacking
+    except Exception:
+        return None
+
+
 def _cpu_baseline(wl, seconds=10.0, steps=None):
-    """The float64 CPU port of the reference path (oracle/) on this host:
-    packed steps of the same workload, bounded to ~`seconds`."""
-    from oracle import mlp64 as O
-    did, x, y = O.synth_blobs(wl["n"], wl["dim"], wl["classes"], 0)
-    datasets = {"train": O.OracleDataset(did, x, y)}
+    """The reference's own CPU path on this host: `packtrain.packed_step`
+    (baseline/_ref, kind "reference"; numpy f64 + OpenBLAS on every core) on
+    the same workload, bounded to ~`seconds` (or exactly `steps`).  Falls
+    back to the float64 port in oracle/ (kind "port") when the reference is
+    not installed."""
+    ref = _ref_packtrain()
+    K, b = len(wl["members"]), wl["batch"]
     dims = (wl["dim"], *wl["hidden"], wl["classes"])
-    ms = [O.OracleMember.make(f"m{i}", dims, wl["act"], opt, lr, wl["batch"], 10 ** 9, "train", 0)
-          for i, (opt, lr) in enumerate(wl["members"])]
+    if ref is not None:
+        rdata, rpacking = ref
+        ds = rdata.synth_dataset(wl["n"], wl["dim"], wl["classes"], seed=0)
+        datasets = {"train": ds}
+        arch = rpacking.MLPArch(wl["dim"], tuple(wl["hidden"]), wl["classes"], wl["act"])
+        hs = [rpacking.make_handle(f"m{i}", arch, opt, lr, b, 10 ** 9, "train", 0)
+              for i, (opt, lr) in enumerate(wl["members"])]
+        packed = rpacking.dedup_inputs(rpacking.pack_models(hs))
+        step = lambda: rpacking.packed_step(packed, datasets)  # noqa: E731
+        kind, what = "reference", "packtrain.packed_step (baseline/_ref, numpy f64)"
+    else:
+        from oracle import mlp64 as O
+        did, x, y = O.synth_blobs(wl["n"], wl["dim"], wl["classes"], 0)
+        datasets = {"train": O.OracleDataset(did, x, y)}
+        ms = [O.OracleMember.make(f"m{i}", dims, wl["act"], opt, lr, b, 10 ** 9, "train", 0)
+              for i, (opt, lr) in enumerate(wl["members"])]
+        step = lambda: O.oracle_packed_step(ms, datasets)  # noqa: E731
+        kind, what = "port", "oracle port (numpy f64)"
     for _ in range(3):
-        O.oracle_packed_step(ms, datasets)
+        step()
     t0 = time.perf_counter()
     n = 0
     while (steps is None and time.perf_counter() - t0 < seconds) or (steps is not None and n < steps):
-        O.oracle_packed_step(ms, datasets)
+        step()
         n += 1
     dt = time.perf_counter() - t0
-    K, b = len(ms), wl["batch"]
-    return {"value": K * b * n / dt, "unit": UNIT, "cores": _cpu_threads(), "kind": "port",
-            "sample": f"{n} packed steps of {len(ms)} x {dims} b={b} ({dt:.1f} s, numpy f64)",
+    return {"value": K * b * n / dt, "unit": UNIT, "cores": _cpu_threads(), "kind": kind,
+            "sample": f"{n} packed steps of {K} x {dims} b={b} ({dt:.1f} s, {what})",
             "ms_per_step": dt / n * 1e3}
 
 
