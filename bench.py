@@ -106,12 +106,13 @@ def _item_bytes(dims, opt, kind, l, b, es):
     return es * (2 * p * (1 + SLOTS[opt]) + x_in + b * o)
 
 
-def _m1_bytes(dims, opt, b, es, which):
+def _m1_bytes(dims, opt, b, es, which, blk=8):
     """Operand bytes of one member in the fused one-hidden-layer kernels:
-    fwd reads W0, b0, W1 and writes Z0, A0 and the partial logits; bwd reads
-    the partials, Z0/A0 and reads+writes W0, W1, b0, b1 with their slots."""
+    fwd reads W0, b0, W1 and writes Z0, A0 and the partial logits (one
+    [b x C] block per `blk` hidden units); bwd reads the partials, Z0/A0 and
+    reads+writes W0, W1, b0, b1 with their slots."""
     D, H, C = dims
-    nb = -(-H // 8)
+    nb = -(-H // blk)
     p = D * H + H + H * C + C
     if which == "fwd":
         return es * (D * H + H + H * C + 2 * b * H + nb * b * C)
@@ -119,21 +120,28 @@ def _m1_bytes(dims, opt, b, es, which):
 
 
 def _phase_plan(wl, es=4):
-    """[(label, algorithmic bytes)] per train launch of the workload's pack
-    (all members share one input group in these workloads; the group's input
-    rows are counted once per launch that reads them)."""
-    from paper_2002_02885_b200.device import uses_fused_mlp1
+    """[(label, kernel, algorithmic bytes)] per train launch of the workload's
+    pack (all members share one input group in these workloads; the group's
+    input rows are counted once per launch that reads them)."""
+    from paper_2002_02885_b200.device import uses_fused_mlp1, uses_m1t
     from paper_2002_02885_b200.packing import MLPArch
     dims = (wl["dim"], *wl["hidden"], wl["classes"])
     b = wl["batch"]
     arch = MLPArch(wl["dim"], tuple(wl["hidden"]), wl["classes"], wl["act"])
     prec = "f64" if es == 8 else "f32"
+    T = "<double>" if es == 8 else "<float>"
+    tens = [opt for opt, _ in wl["members"] if uses_m1t(arch, opt, b, prec)]
     fused = [opt for opt, _ in wl["members"] if uses_fused_mlp1(arch, opt, b, prec)]
-    other = [opt for opt, _ in wl["members"] if not uses_fused_mlp1(arch, opt, b, prec)]
+    other = [opt for opt, _ in wl["members"]
+             if not uses_fused_mlp1(arch, opt, b, prec) and not uses_m1t(arch, opt, b, prec)]
+    xb = es * b * dims[0]
     out = []
+    if tens:
+        out.append(("T1FWD", "k_m1t_fwd" + T,
+                    sum(_m1_bytes(dims, o, b, es, "fwd", 32) for o in tens) + xb))
     if fused:
-        out.append(("M1FWD", sum(_m1_bytes(dims, o, b, es, "fwd") for o in fused)
-                    + es * b * dims[0]))
+        out.append(("M1FWD", "k_mlp1_fwd" + T,
+                    sum(_m1_bytes(dims, o, b, es, "fwd") for o in fused) + xb))
     for items in (_stages(dims) if other else []):
         tot, x_once = 0, False
         for opt in other:
@@ -141,11 +149,14 @@ def _phase_plan(wl, es=4):
                 tot += _item_bytes(dims, opt, kind, l, b, es)
                 x_once |= (l == 0 and kind in ("FWD", "TAIL", "WGRAD"))
         if x_once:
-            tot += es * b * dims[0]
-        out.append(("+".join(f"{k}{l}" for k, l in items), tot))
+            tot += xb
+        out.append(("+".join(f"{k}{l}" for k, l in items), "k_phase" + T, tot))
     if fused:
-        out.append(("M1BWD", sum(_m1_bytes(dims, o, b, es, "bwd") for o in fused)
-                    + es * b * dims[0]))
+        out.append(("M1BWD", "k_mlp1_bwd" + T,
+                    sum(_m1_bytes(dims, o, b, es, "bwd") for o in fused) + xb))
+    if tens:
+        out.append(("T1BWD", "k_m1t_bwd" + T,
+                    sum(_m1_bytes(dims, o, b, es, "bwd", 32) for o in tens) + xb))
     return out
 
 
@@ -284,8 +295,8 @@ def _b200(args):
     phases = []
     plan_b = _phase_plan(wl, 8 if args.precision == "f64" else 4)
     for i, (kind, layer, ctas, _) in enumerate(prof[0]):
-        label, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind]}{layer}", 0)
-        phases.append({"phase": label, "ctas": ctas,
+        label, kern, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind]}{layer}", "?", 0)
+        phases.append({"phase": label, "kernel": kern, "ctas": ctas,
                        "ms": statistics.median(p[i][3] for p in prof), "bytes": nbytes})
     top = max(phases, key=lambda p: p["ms"])
 
@@ -305,8 +316,7 @@ def _b200(args):
     launches = packed._dev[1].launches
     ach = top["bytes"] / (top["ms"] / 1e3) / 1e9
     traffic = None
-    kname = {"M1FWD": "k_mlp1_fwd", "M1BWD": "k_mlp1_bwd"}.get(top["phase"], "k_phase")
-    kname += "<double>" if args.precision == "f64" else "<float>"
+    kname = top["kernel"]
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(args.workload, {}).get(kname)

@@ -36,6 +36,7 @@
 
 #include <cstdint>
 #include <climits>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "packtrain_b200.h"
@@ -58,6 +59,7 @@ struct MemberCtl {
   double loss;         // last step loss
   double eval_acc;     // eval: running sum of per-row losses
   double bc1, bc2;     // Adam bias corrections 1-β^t for t = step_counter + 1
+  double bcn1, bcn2;   // tensor path: the same for t = step_counter + 2 (next commit)
 };
 
 // 1 - beta^t in float64, t = the update about to be applied (engine.py:322-323)
@@ -73,12 +75,14 @@ struct MemberDev {
   int32_t n_layers, act, opt, max_rows;
   int32_t dims[PK_MAX_LAYERS + 1];
   int32_t n_slots, tail;  // tail: last layer handled by a TAIL tile
+  int32_t tensor, pad_;   // tensor: pk_m1t.cuh step (loss + next bc from the bwd owner CTA)
   double wd;
   int64_t n_params;
+  int64_t s_stride;      // elements between optimizer slot blocks (P rounded to 16 B)
   int64_t w_off[PK_MAX_LAYERS];
   int64_t b_off[PK_MAX_LAYERS];
   T* params[2];
-  T* slots[2];  // [n_slots][n_params] per buffer
+  T* slots[2];  // [n_slots][s_stride] per buffer
   T* Z[PK_MAX_LAYERS];   // pre-activation  [max_rows][dims[l+1]]
   T* A[PK_MAX_LAYERS];   // post-activation [max_rows][dims[l+1]] (hidden)
   T* dZ[PK_MAX_LAYERS];  // dLoss/dZ_l      [max_rows][dims[l+1]]
@@ -123,13 +127,15 @@ struct PhaseArgs {
   int32_t is_last;     // run FINALIZE in the last CTA
   int32_t prefetch;    // issue L2 prefetch of params/slots (first phase)
   unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
+  int32_t cs;          // cluster size of this launch (k_m1t_fwd: input splits)
 };
 
 // ---- stage tracing (profiling builds of a step, PK_TRACE=1) -------------
 // Thread 0 of a CTA stamps %globaltimer at stage boundaries:
 //   0 entry, 1 operands/prologue ready, 2 GEMM done, 3 epilogue part 1,
-//   4 epilogue part 2, 5 tile done, 6 finalize start, 7 finalize end.
-constexpr int kTraceSlots = 8;
+//   4 epilogue part 2, 5 tile done, 6 finalize start, 7 finalize end,
+//   8..11 kernel-specific sub-stages (pk_m1t.cuh).
+constexpr int kTraceSlots = 12;  // 8..11: kernel-specific sub-stages
 __shared__ unsigned long long* pk_trace_slots;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -692,7 +698,7 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   int32_t* srow = reinterpret_cast<int32_t*>(sm + G::SMEM_T * sizeof(T));
   const MemberCtl* ctl = M.ctl;
   const int par = ctl->parity;
-  const int64_t P = M.n_params;
+  const int64_t P = M.s_stride;  // slot block stride
   const T* __restrict__ wc = M.params[par];
   T* __restrict__ wn = M.params[par ^ 1];
   const T* sc = M.slots[par];
@@ -794,15 +800,17 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
     int bn = INT_MAX, bg = INT_MAX;
     if (take) {
       const MemberDev<T>& M = P.mems[k];
-      double s = 0.0;
-      for (int r = lane; r < take; r += 32) s += M.rowloss[r];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       MemberCtl* c = M.ctl;
+      double s = 0.0;
+      if (!(train && M.tensor)) {
+        for (int r = lane; r < take; r += 32) s += M.rowloss[r];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      }
       bn = c->bad_node;
       bg = c->bad_grad;
       if (train) {
-        const double loss = s / double(take);
+        const double loss = M.tensor ? c->loss : s / double(take);
         if (lane == 0) c->loss = loss;
         if (!isfinite(loss)) bn = min(bn, 2 * M.n_layers);
       } else if (lane == 0) {
@@ -835,7 +843,12 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
       if (act && k < s_stop) {
         c->parity ^= 1;
         c->step_counter += 1;
-        adam_bias_corrections(c->step_counter, &c->bc1, &c->bc2);
+        if (P.mems[k].tensor) {
+          c->bc1 = c->bcn1;
+          c->bc2 = c->bcn2;
+        } else {
+          adam_bias_corrections(c->step_counter, &c->bc1, &c->bc2);
+        }
         ++committed;
       }
       if (act) c->fault_grad = -1;  // one-shot
@@ -872,7 +885,7 @@ __device__ __noinline__ void prefetch_params(const PhaseArgs<T>& P) {
       // bulk prefetch needs 16-byte aligned address and size: round the
       // region out (slab regions are 256-byte padded, so this stays inside)
       const uintptr_t lo = reinterpret_cast<uintptr_t>(
-          s < 0 ? M.params[par] : M.slots[par] + (int64_t)s * M.n_params);
+          s < 0 ? M.params[par] : M.slots[par] + (int64_t)s * M.s_stride);
       const uintptr_t hi = lo + (uintptr_t)M.n_params * sizeof(T);
       const char* p = reinterpret_cast<const char*>(lo & ~(uintptr_t)15);
       const int64_t bytes = (int64_t)(((hi + 15) & ~(uintptr_t)15) - (lo & ~(uintptr_t)15));
@@ -945,6 +958,44 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
 }
 
 #include "pk_mlp1.cuh"
+#include "pk_umma.cuh"
+#include "pk_m1t.cuh"
+
+// tcgen05 3xTF32 one-hidden-layer step (fp32 members only; the f64 device
+// mode never schedules these phases)
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const PhaseArgs<T> P) {
+  extern __shared__ __align__(128) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  if constexpr (sizeof(T) == 4) {
+    const Tile t = P.tiles[blockIdx.x];
+    const FeedDev<T> f = P.feeds[t.member];
+    if (f.take != 0) m1t_fwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.n0, P.cs);
+  } else {
+    __trap();
+  }
+  kernel_end(P, true);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const PhaseArgs<T> P) {
+  extern __shared__ __align__(128) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  if constexpr (sizeof(T) == 4) {
+    const Tile t = P.tiles[blockIdx.x];
+    const FeedDev<T> f = P.feeds[t.member];
+    if (f.take != 0) m1t_bwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.n0);
+  } else {
+    __trap();
+  }
+  kernel_end(P, true);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const PhaseArgs<T> P) {

@@ -1,0 +1,546 @@
+// pk_m1t.cuh — tensor-core (tcgen05, 3xTF32) packed step for one-hidden-layer
+// fp32 members (included by pk_kernels.cuh inside namespace pk).
+//
+// Same math and commit rules as pk_mlp1.cuh (reference engine.py:180-326 for
+// MLP [D, H, C]), but the two GEMMs that carry the step's FLOPs and its
+// dominant HBM stream run on the 5th-generation tensor cores:
+//
+//   k_m1t_fwd  (member, 128-unit tile, 64-deep input split) per CTA:
+//              TMEM[128 units x RP rows] = W0[split, tile]ᵀ · X[rows, split]ᵀ
+//              W0 rows and the gathered X rows arrive by bulk copy (TMA
+//              engine) into shared memory; one staging pass splits them into
+//              tf32 hi/lo K-major operands; one thread issues
+//              3 x 8 tcgen05.mma.kind::tf32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi).
+//              The splits of a tile form one thread-block cluster; partials
+//              stay in shared memory and are reduced over DSMEM in rank order
+//              (b0, activation → Z0, A0; then the tile's partial logits per
+//              member-local 32-unit block).
+//   k_m1t_bwd  (member, 128-input tile, 32-unit tile) per CTA; prologue
+//              (before griddepcontrol.wait, overlapping k_m1t_fwd): bulk
+//              copies of W0[tile] + optimizer slots, W1 rows + slots and the
+//              tile's X columns.  Then logits = Σ_blocks partials + b1,
+//              softmax-xent (dZ1), dZ0 = (dZ1·W1ᵀ) ⊙ act'(Z0), and
+//              TMEM[128 inputs x 32 units] = X[:, tile]ᵀ · dZ0[:, units]
+//              (3xTF32, 32 rows per K chunk).  The epilogue reads the weight
+//              gradient from TMEM and applies the member's optimizer against
+//              the resident W0 tile — the gradient never reaches HBM.
+//              Input-tile 0 CTAs also update W1 rows / b0 (and b1 in unit
+//              tile 0) with the same fixed-order sums as pk_mlp1.cuh.
+//
+// Determinism / K-invariance: every output element is one MMA accumulation
+// over a k order fixed by the member's own shape (splits of 64, chunks of 32
+// rows), reduced in split order; tiles never mix members, so a member's
+// packed trajectory is bit-identical to its standalone one.
+//
+// Accuracy: 3xTF32 error ≈ 2^-21 · Σ|a·b| per output (measured 4e-7 rel on
+// B200, tools/umma_selftest.cu), inside the fp32 contract rel 1e-4.
+
+constexpr int T_UM = 128;     // fwd: hidden units per tile (MMA M)
+constexpr int T_KS = 64;      // fwd: input dims per split
+constexpr int T_XLD = T_KS + 4;   // fwd: raw X row stride (floats, 16B-aligned, conflict-free)
+constexpr int T_BK = 128;     // bwd: input dims per tile (MMA M)
+constexpr int T_BU = 32;      // bwd: hidden units per tile (MMA N)
+constexpr int T_BXLD = T_BK + 4;  // bwd: raw X row stride
+constexpr int T_LB = 32;      // member-local partial-logit block (units)
+constexpr int T_MAXC = 32;    // classes on this path
+constexpr int T_MAXR = 128;   // rows on this path
+constexpr int T_MAXCS = 16;   // max cluster size (non-portable) → D <= 1024
+
+__host__ __device__ inline int t_nsplit(int D) { return (D + T_KS - 1) / T_KS; }
+__host__ __device__ inline int t_ntile(int H) { return (H + T_UM - 1) / T_UM; }
+__host__ __device__ inline int t_nblk(int H) { return (H + T_LB - 1) / T_LB; }
+
+struct M1T {
+  // shared-memory bytes (fp32) for a member with rows padded to RP
+  __host__ __device__ static int fwd_smem(int RP) {
+    return T_KS * T_UM * 4              // raw W0 rows [k][unit]
+           + RP * T_XLD * 4            // raw X rows
+           + 2 * T_UM * T_KS * 4       // A hi/lo
+           + 2 * RP * T_KS * 4         // B hi/lo
+           + T_UM * T_MAXC * 4 + T_UM * 4  // W1 rows, b0 slice of the tile
+           + RP * 4 + 64;              // row index, barriers
+    // (the partial [RP][T_UM] reuses the A hi/lo region after the MMA)
+  }
+  __host__ __device__ static int bwd_smem(int RP, int C, int ns) {
+    return (1 + ns) * T_BK * T_BU * 4   // W0 tile + slots
+           + RP * T_BXLD * 4           // raw X rows (tile columns)
+           + 2 * T_BK * 32 * 4         // A hi/lo (one 32-row chunk)
+           + 2 * T_BU * 32 * 4         // B hi/lo
+           + RP * (T_MAXC + 1) * 4     // logits → dZ1
+           + 2 * RP * T_BU * 4         // dZ0 tile, A0 tile
+           + (1 + ns) * T_BU * C * 4   // W1 rows + slots
+           + T_MAXC * 4                // b1
+           + 2 * RP * 4 + 64;          // rows, labels, barriers
+  }
+};
+
+// ------------------------------------------------------------ forward --
+// One thread-block cluster per (member, 128-unit tile); cluster rank = input
+// split.  Each CTA leaves its TMEM partial in its own shared memory; after a
+// cluster barrier, rank q reduces member-local 32-unit block(s) q, q+CS, ...
+// by reading the CS partials over DSMEM in rank order (fixed order ⇒
+// deterministic), adds b0, applies the activation and writes Z0/A0 and the
+// block's partial logits.
+__device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
+                             int tile, int split, int CS) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
+  const int R = f.take, RP = m1_rows_pad(M.max_rows);
+  const int u0 = tile * T_UM, nu = min(T_UM, H - u0);
+  const int ks = split * T_KS, nk = max(0, min(T_KS, D - ks));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* rawA = reinterpret_cast<float*>(sm);     // [T_KS][T_UM]
+  float* rawX = rawA + T_KS * T_UM;               // [RP][T_XLD]
+  float* Ah = rawX + RP * T_XLD;                  // K-major [T_KS/4][T_UM][4]
+  float* Al = Ah + T_UM * T_KS;
+  float* Bh = Al + T_UM * T_KS;                   // K-major [T_KS/4][RP][4]
+  float* Bl = Bh + RP * T_KS;
+  float* sW1 = Bl + RP * T_KS;                    // [T_UM][C] W1 rows of the tile
+  float* sb0 = sW1 + T_UM * T_MAXC;               // [T_UM] b0 slice
+  int32_t* srow = reinterpret_cast<int32_t*>(sb0 + T_UM);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(srow + RP);  // [2] (RP even)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  float* sP = Ah;                                 // after the MMA: partial [RP][T_UM]
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
+  const uint32_t tcols = umma::tmem_cols_pow2(RP);
+  const int nu4 = (nu + 3) & ~3;
+  const int nbt = (nu + T_LB - 1) / T_LB;
+  const bool reducer = split < nbt;  // this rank reduces at least one unit block
+
+  if (tid == 32) {
+    umma::mbar_init(&bar[0], 1);
+    umma::mbar_init(&bar[1], 1);
+    umma::mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0 && (nk > 0 || reducer)) {  // W0 rows first (independent of the batch rows)
+    const uint32_t tx = (uint32_t)(nk * nu4 * 4 + R * nk * 4) +
+                        (reducer ? (uint32_t)(nu4 * C * 4 + nu4 * 4) : 0u);
+    if (lane == 0) umma::mbar_arrive_expect_tx(&bar[0], tx);
+    __syncwarp();
+    for (int k = lane; k < nk; k += 32)
+      umma::bulk_g2s(rawA + k * T_UM, W0 + (int64_t)(ks + k) * H + u0, nu4 * 4, &bar[0]);
+    if (reducer && lane == 0) {
+      umma::bulk_g2s(sW1, Pc + M.w_off[1] + (int64_t)u0 * C, nu4 * C * 4, &bar[0]);
+      umma::bulk_g2s(sb0, Pc + M.b_off[0] + u0, nu4 * 4, &bar[0]);
+    }
+    for (int r = lane; r < R; r += 32)
+      umma::bulk_g2s(rawX + r * T_XLD, f.feat + feed_row(f, r) * f.ld + ks, nk * 4, &bar[0]);
+  }
+  if (warp == 1) umma::tmem_alloc(tslot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  PK_TRACE(1);
+  if (nk > 0 || reducer) umma::mbar_wait(&bar[0], 0);
+  if (nk > 0) {
+    // split pass → tf32 hi/lo K-major operands (zero outside the valid box)
+    for (int e = tid; e < T_UM * (T_KS / 4); e += NT) {
+      const int u = e % T_UM, kq = e / T_UM;
+      float4 h, l;
+      float* hp = &h.x;
+      float* lp = &l.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = 4 * kq + j;
+        const float v = (u < nu && k < nk) ? rawA[k * T_UM + u] : 0.f;
+        umma::split3(v, hp[j], lp[j]);
+      }
+      const uint32_t o = umma::kmaj_off(u, 4 * kq, T_UM) / 4;
+      *reinterpret_cast<float4*>(Ah + o) = h;
+      *reinterpret_cast<float4*>(Al + o) = l;
+    }
+    bool badx = false;
+    for (int e = tid; e < RP * (T_KS / 4); e += NT) {
+      const int r = e % RP, kq = e / RP;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < R && 4 * kq < nk) v = *reinterpret_cast<const float4*>(rawX + r * T_XLD + 4 * kq);
+      badx |= !finite(v.x) | !finite(v.y) | !finite(v.z) | !finite(v.w);
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      const uint32_t o = umma::kmaj_off(r, 4 * kq, RP) / 4;
+      *reinterpret_cast<float4*>(Bh + o) = h;
+      *reinterpret_cast<float4*>(Bl + o) = l;
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    badx = __syncthreads_or(badx);
+    umma::fence_after();
+    if (badx && tid == 0) flag_min(&M.ctl->bad_node, 0);
+    if (tid == 0) {
+      const uint32_t idesc = umma::idesc_tf32(T_UM, RP, false, false);
+      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+      const int nks = (nk + 7) / 8;
+      for (int s = 0; s < nks; ++s) {
+        const uint64_t dah = umma::kmaj_desc(ah, T_UM, s), dal = umma::kmaj_desc(al, T_UM, s);
+        const uint64_t dbh = umma::kmaj_desc(bh, RP, s), dbl = umma::kmaj_desc(bl, RP, s);
+        umma::mma_tf32(tmem, dah, dbh, idesc, s > 0);
+        umma::mma_tf32(tmem, dah, dbl, idesc, true);
+        umma::mma_tf32(tmem, dal, dbh, idesc, true);
+      }
+      umma::commit(&bar[1]);
+    }
+    umma::mbar_wait(&bar[1], 0);
+    umma::fence_after();
+  }
+  PK_TRACE(2);
+  __syncthreads();  // every thread is past the MMA: Ah/Al may be overwritten
+  // TMEM partial → own shared memory sP[r][u] (rows r < R; zeros if no split)
+  {
+    const int q = warp & 3, half = warp >> 2;
+    const int u = 32 * q + lane;
+    for (int c = half * (RP / 2); c < (half + 1) * (RP / 2); c += 8) {
+      float v[8];
+      if (nk > 0) {
+        umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, v);
+        umma::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sP[(c + i) * T_UM + u] = v[i];
+    }
+  }
+  umma::fence_before();
+  cl.sync();  // all partials of the tile are in the cluster's shared memory
+  PK_TRACE(3);
+  if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+  // ---- rank q: member-local 32-unit blocks q, q + CS, ... of this tile ------
+  float* sA = rawA;                     // [RP][T_LB] block activations
+  int bad = INT_MAX;
+  for (int bl = split; bl < nbt; bl += CS) {
+    const int ub = bl * T_LB;
+    for (int e = tid; e < RP * T_LB; e += NT) {
+      const int r = e / T_LB, j = e % T_LB, u = ub + j;
+      float a = 0.f;
+      if (r < R && u < nu) {
+        float v[T_MAXCS];
+        const uint32_t la = umma::smem_u32(sP + r * T_UM + u);
+#pragma unroll
+        for (int s = 0; s < T_MAXCS; ++s) v[s] = s < CS ? umma::dsmem_ld(la, (uint32_t)s) : 0.f;
+        float z = v[0];
+#pragma unroll
+        for (int s = 1; s < T_MAXCS; ++s)
+          if (s < CS) z += v[s];
+        z += sb0[u];
+        a = act_fwd(M.act, z);
+        M.Z[0][(int64_t)r * H + u0 + u] = z;
+        M.A[0][(int64_t)r * H + u0 + u] = a;
+        if (!finite(z)) bad = min(bad, 1);
+        if (!finite(a)) bad = min(bad, 2);
+      }
+      sA[e] = a;
+    }
+    __syncthreads();
+    // P[blk][r][c] = Σ_{j<32} A0[r][32·blk + j] · W1[32·blk + j][c]
+    for (int e = tid; e < R * C; e += NT) {
+      const int r = e / C, c = e % C;
+      const float* a = sA + r * T_LB;
+      const float* w = sW1 + ub * C + c;  // rows u >= nu are never read: a = 0 there
+      float p = 0.f;
+#pragma unroll 8
+      for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
+      M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
+    }
+    __syncthreads();
+  }
+  if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  PK_TRACE(4);
+  cl.sync();  // peers are done reading this CTA's partial
+}
+
+// ----------------------------------------------------------- backward --
+__device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
+                             int ktile, int utile) {
+  const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
+  const int R = f.take, RP = m1_rows_pad(M.max_rows), ns = M.n_slots;
+  const int k0 = ktile * T_BK, nk = min(T_BK, D - k0);
+  const int u0 = utile * T_BU, nu = min(T_BU, H - u0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const MemberCtl* ctl = M.ctl;
+  const int par = ctl->parity;
+  const int64_t NP = M.s_stride;  // slot block stride (16-byte multiple)
+  const float* __restrict__ Pc = M.params[par];
+  float* __restrict__ Pn = M.params[par ^ 1];
+  const float* __restrict__ Sc = M.slots[par];
+  float* __restrict__ Sn = M.slots[par ^ 1];
+  // smem carve
+  float* sW = reinterpret_cast<float*>(sm);             // [1+ns][T_BK][T_BU]
+  float* sX = sW + (1 + ns) * T_BK * T_BU;              // [RP][T_BXLD]
+  float* Ah = sX + RP * T_BXLD;                         // K-major [8][T_BK][4]
+  float* Al = Ah + T_BK * 32;
+  float* Bh = Al + T_BK * 32;                           // K-major [8][T_BU][4]
+  float* Bl = Bh + T_BU * 32;
+  float* sL = Bl + T_BU * 32;                           // [RP][T_MAXC+1]
+  float* sdZ = sL + RP * (T_MAXC + 1);                  // [RP][T_BU]
+  float* sA0 = sdZ + RP * T_BU;                         // [RP][T_BU] A0 tile
+  float* sW1 = sA0 + RP * T_BU;                         // [1+ns][T_BU][C]
+  float* sb1 = sW1 + (1 + ns) * T_BU * C;               // [T_MAXC]
+  int32_t* srow = reinterpret_cast<int32_t*>(sb1 + T_MAXC);
+  int32_t* ylab = srow + RP;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // RP even → 8-aligned
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  constexpr uint32_t tcols = 32;
+
+  // ---- prologue (independent of k_m1t_fwd) --------------------------------
+  for (int r = tid; r < RP; r += NT) {
+    srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
+    ylab[r] = r < R ? f.labels[feed_row(f, r)] : 0;
+  }
+  for (int c = tid; c < C; c += NT) sb1[c] = Pc[M.b_off[1] + c];
+  if (warp == 0) umma::tmem_alloc(tslot, tcols);
+  if (tid == 32) {
+    umma::mbar_init(&bar[0], 1);
+    umma::mbar_init(&bar[1], 1);
+    umma::mbar_fence_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    const uint32_t tx = (uint32_t)((1 + ns) * nk * nu * 4 + R * nk * 4 + (1 + ns) * nu * C * 4);
+    if (lane == 0) umma::mbar_arrive_expect_tx(&bar[0], tx);
+    __syncwarp();
+    for (int s = 0; s <= ns; ++s) {
+      const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP);
+      for (int k = lane; k < nk; k += 32)
+        umma::bulk_g2s(sW + (s * T_BK + k) * T_BU, src + M.w_off[0] + (int64_t)(k0 + k) * H + u0,
+                       nu * 4, &bar[0]);
+      if (lane == 0)
+        umma::bulk_g2s(sW1 + s * T_BU * C, src + M.w_off[1] + (int64_t)u0 * C, nu * C * 4, &bar[0]);
+    }
+    for (int r = lane; r < R; r += 32)
+      umma::bulk_g2s(sX + r * T_BXLD, f.feat + (int64_t)srow[r] * f.ld + k0, nk * 4, &bar[0]);
+  }
+  pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
+  PK_TRACE(1);
+  // ---- logits = Σ_blk partials + b1 → softmax-xent → dZ1 (in sL) ----------
+  const int nb = t_nblk(H);
+  const bool owner = (ktile == 0 && utile == 0);
+  int bad = INT_MAX;
+  const int64_t bstr = (int64_t)M.max_rows * C;
+  for (int e = tid; e < R * C; e += NT) {
+    const int c = e % C;
+    const float* pp = M.Z[1] + e;
+    float z = 0.f;
+    for (int q0 = 0; q0 < nb; q0 += 8) {  // block partials in flight, summed in block order
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = q0 + j < nb ? pp[(q0 + j) * bstr] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (q0 + j < nb) z = (q0 + j == 0) ? v[j] : z + v[j];
+    }
+    const int r = e / C;
+    z += sb1[c];
+    sL[r * (T_MAXC + 1) + c] = z;
+    if (!finite(z)) bad = 3;
+  }
+  if (owner && bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  __syncthreads();
+  PK_TRACE(8);
+  for (int r = warp; r < R; r += NT / 32) {
+    float* row = sL + r * (T_MAXC + 1);
+    xent_row(row, row, C, ylab[r], R, true, owner ? M.rowloss + r : nullptr);
+  }
+  PK_TRACE(9);
+  umma::mbar_wait(&bar[0], 0);  // W0 / W1 / X tiles landed
+  __syncthreads();
+  PK_TRACE(10);
+  if (owner && warp == 0) {
+    // the member's step loss (finalize's lane-strided order) and Adam's bias
+    // corrections for the *next* update, off finalize's serial tail
+    double s = 0.0;
+    for (int r = lane; r < R; r += 32) s += M.rowloss[r];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      MemberCtl* c = M.ctl;
+      c->loss = s / double(R);
+      adam_bias_corrections(c->step_counter + 1, &c->bcn1, &c->bcn2);
+    }
+  }
+  PK_TRACE(2);
+  // ---- dZ0[:, units] = (dZ1 · W1[units, :]ᵀ) ⊙ act'(Z0, A0) ----------------
+  {
+    constexpr int PER = T_MAXR * T_BU / NT;  // elements per thread (<= 16)
+    float zr[PER], ar[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {  // every Z0/A0 load in flight at once
+      const int e = tid + i * NT, r = e / T_BU, j = e % T_BU;
+      const bool ok = e < RP * T_BU && r < R && j < nu;
+      const int64_t g = (int64_t)r * H + u0 + j;
+      zr[i] = ok ? M.Z[0][g] : 0.f;
+      ar[i] = ok ? M.A[0][g] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * NT, r = e / T_BU, j = e % T_BU;
+      if (e >= RP * T_BU) break;
+      float v = 0.f;
+      if (r < R && j < nu) {
+        float s = 0.f;
+        for (int c = 0; c < C; ++c) s = fmaf(sL[r * (T_MAXC + 1) + c], sW1[j * C + c], s);
+        v = act_bwd(M.act, zr[i], ar[i], s);
+      }
+      sdZ[e] = v;
+      sA0[e] = ar[i];
+    }
+  }
+  __syncthreads();
+  PK_TRACE(11);
+  // ---- dW0[k, u] = Σ_r X[r, k] · dZ0[r, u] on the tensor cores -------------
+  const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
+  const int nch = RP / 32;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int r0 = ch * 32;
+    for (int e = tid; e < T_BK * 8; e += NT) {  // A = Xᵀ: rows k, K = rows r
+      const int k = e % T_BK, rq = e / T_BK;
+      float4 h, l;
+      float* hp = &h.x;
+      float* lp = &l.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + 4 * rq + j;
+        const float v = (r < R && k < nk) ? sX[r * T_BXLD + k] : 0.f;
+        umma::split3(v, hp[j], lp[j]);
+      }
+      const uint32_t o = umma::kmaj_off(k, 4 * rq, T_BK) / 4;
+      *reinterpret_cast<float4*>(Ah + o) = h;
+      *reinterpret_cast<float4*>(Al + o) = l;
+    }
+    for (int e = tid; e < T_BU * 8; e += NT) {  // B = dZ0ᵀ: rows u, K = rows r
+      const int u = e % T_BU, rq = e / T_BU;
+      float4 h, l;
+      float* hp = &h.x;
+      float* lp = &l.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) umma::split3(sdZ[(r0 + 4 * rq + j) * T_BU + u], hp[j], lp[j]);
+      const uint32_t o = umma::kmaj_off(u, 4 * rq, T_BU) / 4;
+      *reinterpret_cast<float4*>(Bh + o) = h;
+      *reinterpret_cast<float4*>(Bl + o) = l;
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (tid == 0) {
+      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+      for (int s = 0; s < 4; ++s) {
+        const uint64_t dah = umma::kmaj_desc(ah, T_BK, s), dal = umma::kmaj_desc(al, T_BK, s);
+        const uint64_t dbh = umma::kmaj_desc(bh, T_BU, s), dbl = umma::kmaj_desc(bl, T_BU, s);
+        umma::mma_tf32(tmem, dah, dbh, idesc, ch > 0 || s > 0);
+        umma::mma_tf32(tmem, dah, dbl, idesc, true);
+        umma::mma_tf32(tmem, dal, dbh, idesc, true);
+      }
+      umma::commit(&bar[1]);
+    }
+    umma::mbar_wait(&bar[1], ch & 1);
+    umma::fence_after();
+  }
+  PK_TRACE(3);
+  const float lr = float(ctl->lr), wd = float(M.wd);
+  const float bc1 = M.opt == PK_OPT_ADAM ? float(ctl->bc1) : 1.f;
+  const float bc2 = M.opt == PK_OPT_ADAM ? float(ctl->bc2) : 1.f;
+  const int fault = ctl->fault_grad;
+  bool badW0 = false, badW1 = false, badb1 = false, badb0 = false;
+  // ---- epilogue: W0[k0 + k, u0 + u] update from the TMEM gradient ----------
+  {
+    const int q = warp & 3, half = warp >> 2;
+    const int k = 32 * q + lane;
+    for (int c8 = 0; c8 < 2; ++c8) {
+      const int uc = half * 16 + c8 * 8;
+      float g[8];
+      umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)uc, g);
+      umma::tmem_wait_ld();
+      if (k >= nk || uc >= nu) continue;
+      float w[8], s0[8], s1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int se = k * T_BU + uc + i;
+        w[i] = sW[se];
+        s0[i] = ns >= 1 ? sW[T_BK * T_BU + se] : 0.f;
+        s1[i] = ns >= 2 ? sW[2 * T_BK * T_BU + se] : 0.f;
+        float gi = g[i];
+        if (fault == 2) gi = NAN;
+        badW0 |= !finite(gi);
+        opt_step(M.opt, lr, wd, bc1, bc2, w[i], s0[i], s1[i], gi);
+      }
+      const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + uc;
+      // nu % 4 == 0 (H % 4 == 0): quads are all-valid or all-out
+#pragma unroll
+      for (int qd = 0; qd < 2; ++qd) {
+        if (uc + 4 * qd >= nu) break;
+        *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) =
+            make_float4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+        if (ns >= 1)
+          *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) =
+              make_float4(s0[4 * qd], s0[4 * qd + 1], s0[4 * qd + 2], s0[4 * qd + 3]);
+        if (ns >= 2)
+          *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) =
+              make_float4(s1[4 * qd], s1[4 * qd + 1], s1[4 * qd + 2], s1[4 * qd + 3]);
+      }
+    }
+  }
+  // ---- input-tile 0: W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3)
+  if (ktile == 0) {
+    for (int e = tid; e < nu * C; e += NT) {
+      const int j = e / C, c = e % C;
+      float g = 0.f;
+      for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * (T_MAXC + 1) + c], g);
+      if (fault == 0) g = NAN;
+      badW1 |= !finite(g);
+      float w = sW1[e], s0 = ns >= 1 ? sW1[T_BU * C + e] : 0.f,
+            s1 = ns >= 2 ? sW1[2 * T_BU * C + e] : 0.f;
+      opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+      const int64_t i = M.w_off[1] + (int64_t)u0 * C + e;
+      Pn[i] = w;
+      if (ns >= 1) Sn[i] = s0;
+      if (ns >= 2) Sn[NP + i] = s1;
+    }
+    if (utile == 0) {
+      for (int c = tid; c < C; c += NT) {
+        float g = 0.f;
+        for (int r = 0; r < R; ++r) g += sL[r * (T_MAXC + 1) + c];
+        if (fault == 1) g = NAN;
+        badb1 |= !finite(g);
+        const int64_t i = M.b_off[1] + c;
+        float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
+        opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+        Pn[i] = w;
+        if (ns >= 1) Sn[i] = s0;
+        if (ns >= 2) Sn[NP + i] = s1;
+      }
+    }
+    for (int j = tid; j < nu; j += NT) {
+      float g = 0.f;
+      for (int r = 0; r < R; ++r) g += sdZ[r * T_BU + j];
+      if (fault == 3) g = NAN;
+      badb0 |= !finite(g);
+      const int64_t i = M.b_off[0] + u0 + j;
+      float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
+      opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+      Pn[i] = w;
+      if (ns >= 1) Sn[i] = s0;
+      if (ns >= 2) Sn[NP + i] = s1;
+    }
+  }
+  PK_TRACE(4);
+  if (badW1) flag_min(&M.ctl->bad_grad, 0);
+  if (badb1) flag_min(&M.ctl->bad_grad, 1);
+  if (badW0) flag_min(&M.ctl->bad_grad, 2);
+  if (badb0) flag_min(&M.ctl->bad_grad, 3);
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, tcols);
+}

@@ -206,7 +206,7 @@ __device__ void m1_bwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f
   constexpr int XLD = M1<T>::XLD;
   const MemberCtl* ctl = M.ctl;
   const int par = ctl->parity;
-  const int64_t NP = M.n_params;
+  const int64_t NP = M.s_stride;  // slot block stride
   const T* __restrict__ Pc = M.params[par];
   T* __restrict__ Pn = M.params[par ^ 1];
   const T* __restrict__ Sc = M.slots[par];

@@ -22,8 +22,9 @@ struct Phase {
   int smem = 0;            // dynamic shared memory bytes
   int kind = 0;            // dominant tile kind (reporting)
   int mask = 0;            // OR of (1 << tile kind) present → which kernel
-  int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd
+  int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd, 3 k_m1t_fwd, 4 k_m1t_bwd
   int layer = -1;          // dominant layer (reporting)
+  int cs = 1;              // thread-block cluster size (k_m1t_fwd)
 };
 
 struct pk_pack {
@@ -59,8 +60,10 @@ static MemberDev<T> member_dev(const pk_member* m, int tail) {
   for (int i = 0; i <= d.n_layers; ++i) d.dims[i] = m->desc.dims[i];
   d.n_slots = m->n_slots;
   d.tail = tail;
+  d.tensor = m->m1t ? 1 : 0;
   d.wd = m->desc.weight_decay;
   d.n_params = m->P;
+  d.s_stride = m->SS;
   for (int l = 0; l < d.n_layers; ++l) {
     d.w_off[l] = m->w_off[l];
     d.b_off[l] = m->b_off[l];
@@ -74,6 +77,7 @@ static MemberDev<T> member_dev(const pk_member* m, int tail) {
   }
   d.rowloss = m->rowloss;
   d.ctl = m->ctl;
+
   return d;
 }
 
@@ -115,6 +119,8 @@ static cudaError_t init_smem_limit(int device, int* out) {
   for (int mk : masks) ks.push_back(kernel_for<T>(mk));
   ks.push_back(pk::k_mlp1_fwd<T>);
   ks.push_back(pk::k_mlp1_bwd<T>);
+  ks.push_back(pk::k_m1t_fwd<T>);
+  ks.push_back(pk::k_m1t_bwd<T>);
   int dyn = optin;
   for (auto k : ks) {
     cudaFuncAttributes fa{};
@@ -125,6 +131,10 @@ static cudaError_t init_smem_limit(int device, int* out) {
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)) !=
         cudaSuccess)
       return e;
+  // input-split clusters of k_m1t_fwd go up to 16 CTAs (non-portable size)
+  if ((e = cudaFuncSetAttribute(pk::k_m1t_fwd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                1)) != cudaSuccess)
+    return e;
   *out = dyn;
   return e;
 }
@@ -146,6 +156,24 @@ static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device) {
   const int fs = f64 ? pk::M1<double>::fwd_smem(D, C, RP) : pk::M1<float>::fwd_smem(D, C, RP);
   const int bs = f64 ? pk::M1<double>::bwd_smem(D, C, RP, ns) : pk::M1<float>::bwd_smem(D, C, RP, ns);
   return fs <= budget && bs <= budget;
+}
+
+// tensor-core path (pk_m1t.cuh): fp32, one hidden layer, <= 32 classes,
+// <= 128 rows, 16-byte aligned W0 rows / dataset rows for the bulk copies
+static bool m1t_eligible(const pk_member_desc& d, int dtype, int device) {
+  if (dtype != PK_F32 || d.n_layers != 2) return false;
+  const int D = d.dims[0], H = d.dims[1], C = d.dims[2];
+  if (C > pk::T_MAXC || d.max_rows > pk::T_MAXR || H % 4 != 0 || D % 4 != 0) return false;
+  if (pk::t_nsplit(D) > pk::T_MAXCS) return false;  // one cluster per unit tile
+  if (getenv("PK_NO_TCGEN05")) return false;  // A/B switch for measurements
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
+      cudaSuccess)
+    return false;
+  const int budget = optin - kStaticSmemMargin;
+  const int RP = pk::m1_rows_pad(d.max_rows);
+  const int ns = d.optimizer == PK_OPT_SGD ? 0 : (d.optimizer == PK_OPT_ADAM ? 2 : 1);
+  return pk::M1T::fwd_smem(RP) <= budget && pk::M1T::bwd_smem(RP, C, ns) <= budget;
 }
 
 // whether the member's last layer + head + first dgrad fit one TAIL tile
@@ -241,8 +269,25 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   Phase m1f, m1b;  // fused one-hidden-layer members (train only)
   m1f.special = 1;
   m1b.special = 2;
+  Phase tf, tb;    // tensor-core one-hidden-layer members (train only)
+  tf.special = 3;
+  tb.special = 4;
+  for (int k = 0; k < p->K; ++k)  // one cluster (= all input splits) per unit tile
+    if (!eval && p->members[k]->m1t) tf.cs = std::max(tf.cs, pk::t_nsplit(p->members[k]->desc.dims[0]));
   for (int k = 0; k < p->K; ++k) {
     const pk_member* m = p->members[k];
+    if (!eval && m->m1t) {
+      const int D = m->desc.dims[0], H = m->desc.dims[1], C = m->desc.dims[2];
+      const int RP = pk::m1_rows_pad(m->desc.max_rows);
+      for (int t = 0; t < pk::t_ntile(H); ++t)
+        for (int s = 0; s < tf.cs; ++s) tf.host.push_back(Tile{k, 0, pk::TK_FWD, t, s});
+      for (int kt = 0; kt < cdiv(D, pk::T_BK); ++kt)
+        for (int ut = 0; ut < cdiv(H, pk::T_BU); ++ut)
+          tb.host.push_back(Tile{k, 0, pk::TK_WGRAD, kt, ut});
+      tf.smem = std::max(tf.smem, pk::M1T::fwd_smem(RP));
+      tb.smem = std::max(tb.smem, pk::M1T::bwd_smem(RP, C, m->n_slots));
+      continue;
+    }
     if (!eval && m->mlp1) {
       const int nb = (m->desc.dims[1] + pk::M1_BC - 1) / pk::M1_BC;
       for (int cb = 0; cb < nb; ++cb) m1f.host.push_back(Tile{k, 0, pk::TK_FWD, cb, 0});
@@ -286,6 +331,16 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     phases.insert(phases.begin(), m1f);
     phases.push_back(m1b);
   }
+  tf.ntiles = (int)tf.host.size();
+  tb.ntiles = (int)tb.host.size();
+  tf.kind = pk::TK_FWD;
+  tb.kind = pk::TK_WGRAD;
+  tf.layer = 0;
+  tb.layer = 0;
+  if (tf.ntiles) {
+    phases.insert(phases.begin(), tf);
+    phases.push_back(tb);
+  }
 }
 
 // only >= 0: launch that phase alone (profiling); finalize: let the last
@@ -324,13 +379,23 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.blockDim = dim3(pk::NT);
     cfg.dynamicSmemBytes = ph.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    a.cs = ph.cs;
+    if (ph.cs > 1) {
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = ph.cs;
+      attr[1].val.clusterDim.y = 1;
+      attr[1].val.clusterDim.z = 1;
+      cfg.numAttrs = 2;
+    }
     PhaseKernel<T> kern = ph.special == 1   ? pk::k_mlp1_fwd<T>
                           : ph.special == 2 ? pk::k_mlp1_bwd<T>
+                          : ph.special == 3 ? pk::k_m1t_fwd<T>
+                          : ph.special == 4 ? pk::k_m1t_bwd<T>
                                             : kernel_for<T>(ph.mask);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) {

@@ -11,6 +11,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +59,7 @@ struct pk_member {
   pk_member_desc desc;
   int n_slots;
   int64_t P;
+  int64_t SS;  // slot block stride: P rounded up to 16 bytes
   int64_t w_off[PK_MAX_LAYERS], b_off[PK_MAX_LAYERS];
   char* slab;
   size_t slab_bytes;
@@ -69,6 +71,7 @@ struct pk_member {
   double* rowloss;
   MemberCtl* ctl;
   bool mlp1;  // fused one-hidden-layer step
+  bool m1t;   // tensor-core (tcgen05 3xTF32) one-hidden-layer step
 };
 
 struct pk_pack;
@@ -76,6 +79,7 @@ struct pk_pack;
 // defined in pk_pack.cuh: whether a member takes the fused one-hidden-layer
 // step (pk_mlp1.cuh); decided from the member's own shape only
 static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device);
+static bool m1t_eligible(const pk_member_desc& d, int dtype, int device);
 
 #define CK_CTX(ctx, call)                                                        \
   do {                                                                           \
@@ -260,7 +264,8 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   m->ctx = c;
   m->desc = *d;
   m->n_slots = slots_for(d->optimizer);
-  m->mlp1 = mlp1_eligible(*d, c->dtype, c->device);
+  m->m1t = m1t_eligible(*d, c->dtype, c->device);
+  m->mlp1 = !m->m1t && mlp1_eligible(*d, c->dtype, c->device);
   int64_t P = 0;
   for (int l = 0; l < d->n_layers; ++l) {
     m->w_off[l] = P;
@@ -270,6 +275,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   }
   m->P = P;
   const size_t es = c->esize();
+  m->SS = (int64_t)(align_up((size_t)P * es, 16) / es);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -278,12 +284,13 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   };
   size_t o_par[2], o_slot[2], o_z[PK_MAX_LAYERS], o_a[PK_MAX_LAYERS], o_dz[PK_MAX_LAYERS];
   for (int b = 0; b < 2; ++b) o_par[b] = take(P * es);
-  for (int b = 0; b < 2; ++b) o_slot[b] = take((size_t)m->n_slots * P * es);
+  for (int b = 0; b < 2; ++b) o_slot[b] = take((size_t)m->n_slots * m->SS * es);
   for (int l = 0; l < d->n_layers; ++l) {
     const size_t act = (size_t)d->max_rows * d->dims[l + 1] * es;
     // fused members use Z_1 as the [nb][max_rows][C] partial-logit exchange
-    const size_t nb = (size_t)(d->dims[1] + pk::M1_BC - 1) / pk::M1_BC;
-    o_z[l] = take(m->mlp1 && l == 1 ? std::max(act, nb * act) : act);
+    const size_t nb = m->m1t ? (size_t)pk::t_nblk(d->dims[1])
+                             : (size_t)(d->dims[1] + pk::M1_BC - 1) / pk::M1_BC;
+    o_z[l] = take((m->mlp1 || m->m1t) && l == 1 ? std::max(act, nb * act) : act);
     o_a[l] = take(l + 1 < d->n_layers ? act : 0);
     o_dz[l] = take(act);
   }
@@ -316,6 +323,7 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   ctl.fault_grad = -1;
   ctl.step_counter = 0;
   pk::adam_bias_corrections(0, &ctl.bc1, &ctl.bc2);
+  pk::adam_bias_corrections(1, &ctl.bcn1, &ctl.bcn2);
   ctl.lr = d->learning_rate;
   CK_CTX(c, cudaMemcpyAsync(m->ctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, c->stream));
   CK_CTX(c, cudaStreamSynchronize(c->stream));
@@ -384,12 +392,12 @@ extern "C" int pk_member_set_state(pk_member* m, const double* params, const dou
   CK_CTX(c, cudaMemcpyAsync(m->params[0], hp.data(), hp.size(), cudaMemcpyHostToDevice, c->stream));
   if (m->n_slots) {
     const int64_t ns = (int64_t)m->n_slots * m->P;
+    CK_CTX(c, cudaMemsetAsync(m->slots[0], 0, (size_t)m->n_slots * m->SS * es, c->stream));
     if (slots) {
       if (c->dtype == PK_F64) to_dev_type<double>(slots, ns, hs);
       else to_dev_type<float>(slots, ns, hs);
-      CK_CTX(c, cudaMemcpyAsync(m->slots[0], hs.data(), hs.size(), cudaMemcpyHostToDevice, c->stream));
-    } else {
-      CK_CTX(c, cudaMemsetAsync(m->slots[0], 0, ns * es, c->stream));
+      CK_CTX(c, cudaMemcpy2DAsync(m->slots[0], m->SS * es, hs.data(), m->P * es, m->P * es,
+                                  m->n_slots, cudaMemcpyHostToDevice, c->stream));
     }
   }
   MemberCtl ctl{};
@@ -399,6 +407,7 @@ extern "C" int pk_member_set_state(pk_member* m, const double* params, const dou
   ctl.bad_grad = INT_MAX;
   ctl.step_counter = step_counter;
   pk::adam_bias_corrections(step_counter, &ctl.bc1, &ctl.bc2);
+  pk::adam_bias_corrections(step_counter + 1, &ctl.bcn1, &ctl.bcn2);
   ctl.lr = m->desc.learning_rate;
   ctl.loss = 0.0;
   ctl.eval_acc = 0.0;
@@ -425,7 +434,8 @@ extern "C" int pk_member_get_state(pk_member* m, double* params, double* slots, 
   if (slots && m->n_slots) {
     const int64_t ns = (int64_t)m->n_slots * m->P;
     h.resize(ns * es);
-    CK_CTX(c, cudaMemcpy(h.data(), m->slots[ctl.parity], h.size(), cudaMemcpyDeviceToHost));
+    CK_CTX(c, cudaMemcpy2D(h.data(), m->P * es, m->slots[ctl.parity], m->SS * es, m->P * es,
+                           m->n_slots, cudaMemcpyDeviceToHost));
     if (c->dtype == PK_F64) from_dev_type<double>(h, ns, slots);
     else from_dev_type<float>(h, ns, slots);
   }

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-_CTL_BYTES = 64          # sizeof(pk::MemberCtl)
+_CTL_BYTES = 80          # sizeof(pk::MemberCtl)
 _ALIGN = 256
 _SLOTS = {"sgd": 0, "momentum": 1, "adagrad": 1, "adam": 2}
 
@@ -39,9 +39,40 @@ def _m1_rows_pad(r):
     return 32 if r <= 32 else (64 if r <= 64 else 128)
 
 
+_T_KS, _T_UM, _T_BK, _T_BU, _T_XLD, _T_BXLD, _T_LB, _T_MAXC, _T_MAXR = (
+    64, 128, 128, 32, 68, 132, 32, 32, 128)
+
+
+def _cdiv(a, b):
+    return -(-a // b)
+
+
+def uses_m1t(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
+    """Mirror of csrc m1t_eligible(): the tcgen05 3xTF32 one-hidden-layer
+    step (fp32, <= 32 classes, <= 128 rows, H and D multiples of 4, smem fits)."""
+    import os
+    if precision != "f32" or len(arch.hidden) != 1 or os.environ.get("PK_NO_TCGEN05"):
+        return False
+    D, H, C = arch.input_dim, arch.hidden[0], arch.classes
+    if C > _T_MAXC or batch_size > _T_MAXR or H % 4 or D % 4 or _cdiv(D, _T_KS) > 16:
+        return False
+    RP = _m1_rows_pad(batch_size)
+    ns = _SLOTS[optimizer.lower()]
+    fwd = _T_KS * _T_UM * 4 + RP * _T_XLD * 4 + 2 * _T_UM * _T_KS * 4 + 2 * RP * _T_KS * 4 \
+        + RP * 4 + 64
+    bwd = ((1 + ns) * _T_BK * _T_BU * 4 + RP * _T_BXLD * 4 + 2 * _T_BK * 32 * 4
+           + 2 * _T_BU * 32 * 4 + RP * (_T_MAXC + 1) * 4 + 2 * RP * _T_BU * 4
+           + (1 + ns) * _T_BU * C * 4 + 2 * RP * 4 + 64)
+    budget = _SMEM_OPTIN - _STATIC_MARGIN
+    return fwd <= budget and bwd <= budget
+
+
 def uses_fused_mlp1(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
-    """Mirror of csrc mlp1_eligible(): one hidden layer, <= 32 classes,
-    batch <= 128 and the fused kernels' shared memory fits."""
+    """Mirror of csrc mlp1_eligible() (the FFMA fused path, taken when the
+    tensor path is not): one hidden layer, <= 32 classes, batch <= 128 and
+    the fused kernels' shared memory fits."""
+    if uses_m1t(arch, optimizer, batch_size, precision):
+        return False
     if len(arch.hidden) != 1 or arch.classes > _M1_MAXC or batch_size > _M1_MAXR:
         return False
     es = 8 if precision == "f64" else 4
@@ -62,15 +93,19 @@ def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") 
     es = 8 if precision == "f64" else 4
     dims = (arch.input_dim, *arch.hidden, arch.classes)
     P = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
+    ss = _cdiv(P * es, 16) * 16 // es  # slot blocks are 16-byte strided
     ns = _SLOTS[optimizer.lower()]
-    total = 2 * _al(P * es) + 2 * _al(ns * P * es)
+    total = 2 * _al(P * es) + 2 * _al(ns * ss * es)
     n = len(dims) - 1
+    tensor = uses_m1t(arch, optimizer, batch_size, precision)
     fused = uses_fused_mlp1(arch, optimizer, batch_size, precision)
     for layer in range(n):
         act = batch_size * dims[layer + 1] * es
         z = act
         if fused and layer == 1:  # Z_1 doubles as the partial-logit exchange
             z = max(act, -(-dims[1] // _M1_BC) * act)
+        if tensor and layer == 1:
+            z = max(act, _cdiv(dims[1], _T_LB) * act)
         total += _al(z) + _al(act if layer + 1 < n else 0) + _al(act)
     total += _al(batch_size * 8)  # per-row loss terms (float64)
     return total + _al(_CTL_BYTES)

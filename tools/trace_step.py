@@ -21,7 +21,8 @@ import numpy as np  # noqa: E402
 import bench  # noqa: E402
 from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
 
-STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1")
+STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1",
+          "s8", "s9", "s10", "s11")
 
 
 def main():
@@ -51,7 +52,7 @@ def main():
         sys.exit("tracing is off (PK_TRACE=1 must be set before the pack is created)")
     buf = (C.c_uint64 * n)()
     rt.lib.pk_pack_trace(dp.ptr, buf, n)
-    arr = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(-1, 8)
+    arr = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(-1, len(STAGES))
     code, phases, _ = dp.profile()  # only for per-phase CTA counts
     t0 = arr[arr[:, 0] > 0, 0].min()
     off = 0
