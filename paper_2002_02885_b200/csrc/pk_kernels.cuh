@@ -128,14 +128,15 @@ struct PhaseArgs {
   int32_t prefetch;    // issue L2 prefetch of params/slots (first phase)
   unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
   int32_t cs;          // cluster size of this launch (k_m1t_fwd: input splits)
+  int32_t stages;      // k_m1t_bwd: input-tile stages in flight
 };
 
 // ---- stage tracing (profiling builds of a step, PK_TRACE=1) -------------
 // Thread 0 of a CTA stamps %globaltimer at stage boundaries:
 //   0 entry, 1 operands/prologue ready, 2 GEMM done, 3 epilogue part 1,
 //   4 epilogue part 2, 5 tile done, 6 finalize start, 7 finalize end,
-//   8..11 kernel-specific sub-stages (pk_m1t.cuh).
-constexpr int kTraceSlots = 12;  // 8..11: kernel-specific sub-stages
+//   8..15 kernel-specific sub-stages (pk_m1t.cuh).
+constexpr int kTraceSlots = 16;  // 8..15: kernel-specific sub-stages
 __shared__ unsigned long long* pk_trace_slots;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -990,7 +991,8 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const PhaseArgs<T> P) {
   if constexpr (sizeof(T) == 4) {
     const Tile t = P.tiles[blockIdx.x];
     const FeedDev<T> f = P.feeds[t.member];
-    if (f.take != 0) m1t_bwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.n0);
+    // m0 = first input tile, layer = input tiles in the group, n0 = unit tile
+    if (f.take != 0) m1t_bwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.layer, t.n0, P.stages);
   } else {
     __trap();
   }

@@ -41,6 +41,7 @@ constexpr int T_XLD = T_KS + 4;   // fwd: raw X row stride (floats, 16B-aligned,
 constexpr int T_BK = 128;     // bwd: input dims per tile (MMA M)
 constexpr int T_BU = 32;      // bwd: hidden units per tile (MMA N)
 constexpr int T_BXLD = T_BK + 4;  // bwd: raw X row stride
+constexpr int T_BWLD = T_BU + 4;  // bwd: W0-tile row stride (144 B: LDS.128 by row is conflict-free)
 constexpr int T_LB = 32;      // member-local partial-logit block (units)
 constexpr int T_MAXC = 32;    // classes on this path
 constexpr int T_MAXR = 128;   // rows on this path
@@ -61,9 +62,9 @@ struct M1T {
            + RP * 4 + 64;              // row index, barriers
     // (the partial [RP][T_UM] reuses the A hi/lo region after the MMA)
   }
-  __host__ __device__ static int bwd_smem(int RP, int C, int ns) {
-    return (1 + ns) * T_BK * T_BU * 4   // W0 tile + slots
-           + RP * T_BXLD * 4           // raw X rows (tile columns)
+  // S = input-tile stages in flight (2 when they fit, else 1)
+  __host__ __device__ static int bwd_smem(int RP, int C, int ns, int S) {
+    return S * ((1 + ns) * T_BK * T_BWLD * 4 + RP * T_BXLD * 4)  // W0 tile + slots, X columns
            + 2 * T_BK * 32 * 4         // A hi/lo (one 32-row chunk)
            + 2 * T_BU * 32 * 4         // B hi/lo
            + RP * (T_MAXC + 1) * 4     // logits → dZ1
@@ -73,6 +74,24 @@ struct M1T {
            + 2 * RP * 4 + 64;          // rows, labels, barriers
   }
 };
+
+// softmax-xent of one row by one thread (same formulas and order of
+// operations per element as xent_row; engine.py:211-230, :252-264):
+// z ← dlogits in place, −logp[y] into *rowloss
+__device__ __forceinline__ void xent_row_thread(float* z, int C, int y, int R, double* rowloss) {
+  float mx = z[0];
+  for (int c = 1; c < C; ++c) mx = fmaxf(mx, z[c]);
+  float s = 0.f;
+  for (int c = 0; c < C; ++c) s += ex(z[c] - mx);
+  const float zy = z[y];
+  const float inv = 1.f / s, nv = float(R);
+  for (int c = 0; c < C; ++c) {
+    float p = ex(z[c] - mx) * inv;
+    if (c == y) p -= 1.f;
+    z[c] = p / nv;
+  }
+  if (rowloss) *rowloss = -(double)((zy - mx) - lg(s));
+}
 
 // ------------------------------------------------------------ forward --
 // One thread-block cluster per (member, 128-unit tile); cluster rank = input
@@ -109,33 +128,41 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const int nbt = (nu + T_LB - 1) / T_LB;
   const bool reducer = split < nbt;  // this rank reduces at least one unit block
 
+  // 16-byte cp.async (LDGSTS) from every thread: W0 rows first (they do not
+  // depend on the batch rows), then W1 / b0 of the tile, then the X rows
+  {
+    const int cpr = nu4 / 4;
+    for (int e = tid; e < nk * cpr; e += NT) {
+      const int k = e / cpr, c = e % cpr;
+      cp_async<16>(rawA + k * T_UM + 4 * c, W0 + (int64_t)(ks + k) * H + u0 + 4 * c, true);
+    }
+    if (reducer) {
+      for (int e = tid; e < nu4 * C / 4; e += NT)
+        cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
+      for (int e = tid; e < cpr; e += NT) cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
+    }
+  }
+  for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
   if (tid == 32) {
-    umma::mbar_init(&bar[0], 1);
     umma::mbar_init(&bar[1], 1);
     umma::mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == 0 && (nk > 0 || reducer)) {  // W0 rows first (independent of the batch rows)
-    const uint32_t tx = (uint32_t)(nk * nu4 * 4 + R * nk * 4) +
-                        (reducer ? (uint32_t)(nu4 * C * 4 + nu4 * 4) : 0u);
-    if (lane == 0) umma::mbar_arrive_expect_tx(&bar[0], tx);
-    __syncwarp();
-    for (int k = lane; k < nk; k += 32)
-      umma::bulk_g2s(rawA + k * T_UM, W0 + (int64_t)(ks + k) * H + u0, nu4 * 4, &bar[0]);
-    if (reducer && lane == 0) {
-      umma::bulk_g2s(sW1, Pc + M.w_off[1] + (int64_t)u0 * C, nu4 * C * 4, &bar[0]);
-      umma::bulk_g2s(sb0, Pc + M.b_off[0] + u0, nu4 * 4, &bar[0]);
-    }
-    for (int r = lane; r < R; r += 32)
-      umma::bulk_g2s(rawX + r * T_XLD, f.feat + feed_row(f, r) * f.ld + ks, nk * 4, &bar[0]);
   }
   if (warp == 1) umma::tmem_alloc(tslot, tcols);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  {
+    const int cpr = nk / 4;
+    for (int e = tid; e < R * cpr; e += NT) {
+      const int r = e / cpr, c = e % cpr;
+      cp_async<16>(rawX + r * T_XLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + ks + 4 * c, true);
+    }
+  }
+  cp_commit();
   const uint32_t tmem = *tslot;
   PK_TRACE(1);
-  if (nk > 0 || reducer) umma::mbar_wait(&bar[0], 0);
+  cp_wait<0>();
+  __syncthreads();
   if (nk > 0) {
     // split pass → tf32 hi/lo K-major operands (zero outside the valid box)
     for (int e = tid; e < T_UM * (T_KS / 4); e += NT) {
@@ -258,11 +285,20 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 }
 
 // ----------------------------------------------------------- backward --
+// One CTA per (member, 32-unit tile, group of `ng` consecutive 128-input
+// tiles).  The per-unit-tile work — logits, softmax-xent, dZ0 — is done once
+// and the group's W0 tiles (+ slots, + X columns) stream through S shared-
+// memory stages by bulk copy while the previous tile's MMA and optimizer
+// epilogue run.  Which CTA updates an element never changes its arithmetic,
+// so the grouping (chosen per pack for occupancy) keeps K-invariance.
+__device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
+  return (1 + ns) * T_BK * T_BWLD + RP * T_BXLD;
+}
+
 __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                             int ktile, int utile) {
+                             int kt0, int ng, int utile, int S) {
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows), ns = M.n_slots;
-  const int k0 = ktile * T_BK, nk = min(T_BK, D - k0);
   const int u0 = utile * T_BU, nu = min(T_BU, H - u0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const MemberCtl* ctl = M.ctl;
@@ -272,10 +308,10 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* __restrict__ Pn = M.params[par ^ 1];
   const float* __restrict__ Sc = M.slots[par];
   float* __restrict__ Sn = M.slots[par ^ 1];
-  // smem carve
-  float* sW = reinterpret_cast<float*>(sm);             // [1+ns][T_BK][T_BU]
-  float* sX = sW + (1 + ns) * T_BK * T_BU;              // [RP][T_BXLD]
-  float* Ah = sX + RP * T_BXLD;                         // K-major [8][T_BK][4]
+  // smem carve: S stages of {W0 tile + slots [1+ns][T_BK][T_BU], X columns [RP][T_BXLD]}
+  float* stg = reinterpret_cast<float*>(sm);
+  const int SF = m1t_bwd_stage_floats(RP, ns);
+  float* Ah = stg + S * SF;                             // K-major [8][T_BK][4]
   float* Al = Ah + T_BK * 32;
   float* Bh = Al + T_BK * 32;                           // K-major [8][T_BU][4]
   float* Bl = Bh + T_BU * 32;
@@ -286,8 +322,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* sb1 = sW1 + (1 + ns) * T_BU * C;               // [T_MAXC]
   int32_t* srow = reinterpret_cast<int32_t*>(sb1 + T_MAXC);
   int32_t* ylab = srow + RP;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // RP even → 8-aligned
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // [0,1] stages, 2 W1, 3 MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
   constexpr uint32_t tcols = 32;
 
   // ---- prologue (independent of k_m1t_fwd) --------------------------------
@@ -298,34 +334,45 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   for (int c = tid; c < C; c += NT) sb1[c] = Pc[M.b_off[1] + c];
   if (warp == 0) umma::tmem_alloc(tslot, tcols);
   if (tid == 32) {
-    umma::mbar_init(&bar[0], 1);
-    umma::mbar_init(&bar[1], 1);
+    umma::mbar_init(&bar[3], 1);
     umma::mbar_fence_init();
   }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tslot;
-  if (warp == 0) {
-    const uint32_t tx = (uint32_t)((1 + ns) * nk * nu * 4 + R * nk * 4 + (1 + ns) * nu * C * 4);
-    if (lane == 0) umma::mbar_arrive_expect_tx(&bar[0], tx);
-    __syncwarp();
+  // 16-byte cp.async (LDGSTS) from every thread; one commit group per input
+  // tile, staged into stage i % S
+  auto issue = [&](int i) {
+    const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
+    float* sW = stg + (i % S) * SF;
+    float* sX = sW + (1 + ns) * T_BK * T_BWLD;
+    const int cw = nu / 4, cx = nk / 4;
     for (int s = 0; s <= ns; ++s) {
-      const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP);
-      for (int k = lane; k < nk; k += 32)
-        umma::bulk_g2s(sW + (s * T_BK + k) * T_BU, src + M.w_off[0] + (int64_t)(k0 + k) * H + u0,
-                       nu * 4, &bar[0]);
-      if (lane == 0)
-        umma::bulk_g2s(sW1 + s * T_BU * C, src + M.w_off[1] + (int64_t)u0 * C, nu * C * 4, &bar[0]);
+      const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP) + M.w_off[0] + u0;
+      for (int e = tid; e < nk * cw; e += NT) {
+        const int k = e / cw, c = e % cw;
+        cp_async<16>(sW + (s * T_BK + k) * T_BWLD + 4 * c, src + (int64_t)(k0 + k) * H + 4 * c, true);
+      }
     }
-    for (int r = lane; r < R; r += 32)
-      umma::bulk_g2s(sX + r * T_BXLD, f.feat + (int64_t)srow[r] * f.ld + k0, nk * 4, &bar[0]);
+    for (int e = tid; e < R * cx; e += NT) {
+      const int r = e / cx, c = e % cx;
+      cp_async<16>(sX + r * T_BXLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * c, true);
+    }
+    cp_commit();
+  };
+  for (int s = 0; s <= ns; ++s) {  // W1 rows (+ slots): the first commit group
+    const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP) + M.w_off[1] + (int64_t)u0 * C;
+    for (int e = tid; e < nu * C / 4; e += NT) cp_async<16>(sW1 + s * T_BU * C + 4 * e, src + 4 * e, true);
   }
+  cp_commit();
+  const int nstg = min(S, ng);
+  for (int i = 0; i < nstg; ++i) issue(i);
   pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
   PK_TRACE(1);
   // ---- logits = Σ_blk partials + b1 → softmax-xent → dZ1 (in sL) ----------
   const int nb = t_nblk(H);
-  const bool owner = (ktile == 0 && utile == 0);
+  const bool owner = (kt0 == 0 && utile == 0);
   int bad = INT_MAX;
   const int64_t bstr = (int64_t)M.max_rows * C;
   for (int e = tid; e < R * C; e += NT) {
@@ -348,12 +395,14 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   if (owner && bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   __syncthreads();
   PK_TRACE(8);
-  for (int r = warp; r < R; r += NT / 32) {
+  if (tid == 0 && pk_trace_slots) pk_trace_slots[12] = clock64();
+  for (int r = tid; r < R; r += NT) {  // one thread per row: no shuffles, C <= 32
     float* row = sL + r * (T_MAXC + 1);
-    xent_row(row, row, C, ylab[r], R, true, owner ? M.rowloss + r : nullptr);
+    xent_row_thread(row, C, ylab[r], R, owner ? M.rowloss + r : nullptr);
   }
+  if (tid == 0 && pk_trace_slots) pk_trace_slots[13] = clock64();
   PK_TRACE(9);
-  umma::mbar_wait(&bar[0], 0);  // W0 / W1 / X tiles landed
+  if (nstg == 2) cp_wait<2>(); else cp_wait<1>();  // W1 rows landed
   __syncthreads();
   PK_TRACE(10);
   if (owner && warp == 0) {
@@ -369,7 +418,6 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       adam_bias_corrections(c->step_counter + 1, &c->bcn1, &c->bcn2);
     }
   }
-  PK_TRACE(2);
   // ---- dZ0[:, units] = (dZ1 · W1[units, :]ᵀ) ⊙ act'(Z0, A0) ----------------
   {
     constexpr int PER = T_MAXR * T_BU / NT;  // elements per thread (<= 16)
@@ -398,102 +446,129 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   }
   __syncthreads();
   PK_TRACE(11);
-  // ---- dW0[k, u] = Σ_r X[r, k] · dZ0[r, u] on the tensor cores -------------
-  const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
-  const int nch = RP / 32;
-  for (int ch = 0; ch < nch; ++ch) {
-    const int r0 = ch * 32;
-    for (int e = tid; e < T_BK * 8; e += NT) {  // A = Xᵀ: rows k, K = rows r
-      const int k = e % T_BK, rq = e / T_BK;
-      float4 h, l;
-      float* hp = &h.x;
-      float* lp = &l.x;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = r0 + 4 * rq + j;
-        const float v = (r < R && k < nk) ? sX[r * T_BXLD + k] : 0.f;
-        umma::split3(v, hp[j], lp[j]);
-      }
-      const uint32_t o = umma::kmaj_off(k, 4 * rq, T_BK) / 4;
-      *reinterpret_cast<float4*>(Ah + o) = h;
-      *reinterpret_cast<float4*>(Al + o) = l;
-    }
-    for (int e = tid; e < T_BU * 8; e += NT) {  // B = dZ0ᵀ: rows u, K = rows r
-      const int u = e % T_BU, rq = e / T_BU;
-      float4 h, l;
-      float* hp = &h.x;
-      float* lp = &l.x;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) umma::split3(sdZ[(r0 + 4 * rq + j) * T_BU + u], hp[j], lp[j]);
-      const uint32_t o = umma::kmaj_off(u, 4 * rq, T_BU) / 4;
-      *reinterpret_cast<float4*>(Bh + o) = h;
-      *reinterpret_cast<float4*>(Bl + o) = l;
-    }
-    umma::fence_async_smem();
-    umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
-    if (tid == 0) {
-      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
-      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
-      for (int s = 0; s < 4; ++s) {
-        const uint64_t dah = umma::kmaj_desc(ah, T_BK, s), dal = umma::kmaj_desc(al, T_BK, s);
-        const uint64_t dbh = umma::kmaj_desc(bh, T_BU, s), dbl = umma::kmaj_desc(bl, T_BU, s);
-        umma::mma_tf32(tmem, dah, dbh, idesc, ch > 0 || s > 0);
-        umma::mma_tf32(tmem, dah, dbl, idesc, true);
-        umma::mma_tf32(tmem, dal, dbh, idesc, true);
-      }
-      umma::commit(&bar[1]);
-    }
-    umma::mbar_wait(&bar[1], ch & 1);
-    umma::fence_after();
-  }
-  PK_TRACE(3);
   const float lr = float(ctl->lr), wd = float(M.wd);
   const float bc1 = M.opt == PK_OPT_ADAM ? float(ctl->bc1) : 1.f;
   const float bc2 = M.opt == PK_OPT_ADAM ? float(ctl->bc2) : 1.f;
   const int fault = ctl->fault_grad;
   bool badW0 = false, badW1 = false, badb1 = false, badb0 = false;
-  // ---- epilogue: W0[k0 + k, u0 + u] update from the TMEM gradient ----------
-  {
-    const int q = warp & 3, half = warp >> 2;
-    const int k = 32 * q + lane;
-    for (int c8 = 0; c8 < 2; ++c8) {
-      const int uc = half * 16 + c8 * 8;
-      float g[8];
-      umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)uc, g);
-      umma::tmem_wait_ld();
-      if (k >= nk || uc >= nu) continue;
-      float w[8], s0[8], s1[8];
+  // ---- stream the group's input tiles: dW0 = X[:, tile]ᵀ · dZ0 on the tensor
+  //      cores, optimizer epilogue straight from TMEM -------------------------
+  const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
+  const int nch = RP / 32;
+  uint32_t mph = 0;
+  for (int i = 0; i < ng; ++i) {
+    const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
+    const float* sW = stg + (i % S) * SF;
+    const float* sX = sW + (1 + ns) * T_BK * T_BWLD;
+    if (S == 2 && i + 1 < ng) cp_wait<1>(); else cp_wait<0>();  // input tile i landed
+    __syncthreads();
+    // (slot 12/13 hold clock64 around the xent for a clock-rate check)
+    for (int ch = 0; ch < nch; ++ch) {
+      const int r0 = ch * 32;
+      for (int e = tid; e < T_BK * 8; e += NT) {  // A = Xᵀ: rows k, K = rows r
+        const int k = e % T_BK, rq = e / T_BK;
+        float4 h, l;
+        float* hp = &h.x;
+        float* lp = &l.x;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int se = k * T_BU + uc + i;
-        w[i] = sW[se];
-        s0[i] = ns >= 1 ? sW[T_BK * T_BU + se] : 0.f;
-        s1[i] = ns >= 2 ? sW[2 * T_BK * T_BU + se] : 0.f;
-        float gi = g[i];
-        if (fault == 2) gi = NAN;
-        badW0 |= !finite(gi);
-        opt_step(M.opt, lr, wd, bc1, bc2, w[i], s0[i], s1[i], gi);
+        for (int j = 0; j < 4; ++j) {
+          const int r = r0 + 4 * rq + j;
+          const float v = (r < R && k < nk) ? sX[r * T_BXLD + k] : 0.f;
+          umma::split3(v, hp[j], lp[j]);
+        }
+        const uint32_t o = umma::kmaj_off(k, 4 * rq, T_BK) / 4;
+        *reinterpret_cast<float4*>(Ah + o) = h;
+        *reinterpret_cast<float4*>(Al + o) = l;
       }
-      const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + uc;
-      // nu % 4 == 0 (H % 4 == 0): quads are all-valid or all-out
+      for (int e = tid; e < T_BU * 8; e += NT) {  // B = dZ0ᵀ: rows u, K = rows r
+        const int u = e % T_BU, rq = e / T_BU;
+        float4 h, l;
+        float* hp = &h.x;
+        float* lp = &l.x;
 #pragma unroll
-      for (int qd = 0; qd < 2; ++qd) {
-        if (uc + 4 * qd >= nu) break;
-        *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) =
-            make_float4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
-        if (ns >= 1)
-          *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) =
-              make_float4(s0[4 * qd], s0[4 * qd + 1], s0[4 * qd + 2], s0[4 * qd + 3]);
-        if (ns >= 2)
-          *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) =
-              make_float4(s1[4 * qd], s1[4 * qd + 1], s1[4 * qd + 2], s1[4 * qd + 3]);
+        for (int j = 0; j < 4; ++j) umma::split3(sdZ[(r0 + 4 * rq + j) * T_BU + u], hp[j], lp[j]);
+        const uint32_t o = umma::kmaj_off(u, 4 * rq, T_BU) / 4;
+        *reinterpret_cast<float4*>(Bh + o) = h;
+        *reinterpret_cast<float4*>(Bl + o) = l;
+      }
+      umma::fence_async_smem();
+      umma::fence_before();
+      __syncthreads();
+      umma::fence_after();
+      if (i == 0 && ch == 0) PK_TRACE(13);
+      if (tid == 0) {
+        const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+        const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+        for (int s = 0; s < 4; ++s) {
+          const uint64_t dah = umma::kmaj_desc(ah, T_BK, s), dal = umma::kmaj_desc(al, T_BK, s);
+          const uint64_t dbh = umma::kmaj_desc(bh, T_BU, s), dbl = umma::kmaj_desc(bl, T_BU, s);
+          umma::mma_tf32(tmem, dah, dbh, idesc, ch > 0 || s > 0);
+          umma::mma_tf32(tmem, dah, dbl, idesc, true);
+          umma::mma_tf32(tmem, dal, dbh, idesc, true);
+        }
+        umma::commit(&bar[3]);
+      }
+      umma::mbar_wait(&bar[3], mph);
+      mph ^= 1;
+      umma::fence_after();
+      if (i == 0 && ch == 0) PK_TRACE(14);
+    }
+    // epilogue: W0[k0 + k, u0 + u] update from the TMEM gradient
+    {
+      const int q = warp & 3, half = warp >> 2;
+      const int k = 32 * q + lane;
+      for (int c8 = 0; c8 < 2; ++c8) {
+        const int uc = half * 16 + c8 * 8;
+        float g[8];
+        umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)uc, g);
+        umma::tmem_wait_ld();
+        if (k >= nk || uc >= nu) continue;
+        float w[8], s0[8], s1[8];
+        {
+          const float* row = sW + k * T_BWLD + uc;  // 2 x LDS.128 per tensor
+          *reinterpret_cast<float4*>(w) = *reinterpret_cast<const float4*>(row);
+          *reinterpret_cast<float4*>(w + 4) = *reinterpret_cast<const float4*>(row + 4);
+          if (ns >= 1) {
+            *reinterpret_cast<float4*>(s0) = *reinterpret_cast<const float4*>(row + T_BK * T_BWLD);
+            *reinterpret_cast<float4*>(s0 + 4) = *reinterpret_cast<const float4*>(row + T_BK * T_BWLD + 4);
+          }
+          if (ns >= 2) {
+            *reinterpret_cast<float4*>(s1) = *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD);
+            *reinterpret_cast<float4*>(s1 + 4) = *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD + 4);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float gj = g[j];
+          if (fault == 2) gj = NAN;
+          badW0 |= !finite(gj);
+          opt_step(M.opt, lr, wd, bc1, bc2, w[j], s0[j], s1[j], gj);
+        }
+        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + uc;
+        // nu % 4 == 0 (H % 4 == 0): quads are all-valid or all-out
+#pragma unroll
+        for (int qd = 0; qd < 2; ++qd) {
+          if (uc + 4 * qd >= nu) break;
+          *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) =
+              make_float4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+          if (ns >= 1)
+            *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) =
+                make_float4(s0[4 * qd], s0[4 * qd + 1], s0[4 * qd + 2], s0[4 * qd + 3]);
+          if (ns >= 2)
+            *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) =
+                make_float4(s1[4 * qd], s1[4 * qd + 1], s1[4 * qd + 2], s1[4 * qd + 3]);
+        }
       }
     }
+    if (i == 0) PK_TRACE(15);
+    umma::fence_before();
+    __syncthreads();  // stage i % S and the accumulator are free again
+    umma::fence_after();
+    if (i + S < ng) issue(i + S);
   }
+  PK_TRACE(3);
   // ---- input-tile 0: W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3)
-  if (ktile == 0) {
+  if (kt0 == 0) {
     for (int e = tid; e < nu * C; e += NT) {
       const int j = e / C, c = e % C;
       float g = 0.f;

@@ -25,6 +25,7 @@ struct Phase {
   int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd, 3 k_m1t_fwd, 4 k_m1t_bwd
   int layer = -1;          // dominant layer (reporting)
   int cs = 1;              // thread-block cluster size (k_m1t_fwd)
+  int stages = 1;          // k_m1t_bwd input-tile stages
 };
 
 struct pk_pack {
@@ -173,7 +174,7 @@ static bool m1t_eligible(const pk_member_desc& d, int dtype, int device) {
   const int budget = optin - kStaticSmemMargin;
   const int RP = pk::m1_rows_pad(d.max_rows);
   const int ns = d.optimizer == PK_OPT_SGD ? 0 : (d.optimizer == PK_OPT_ADAM ? 2 : 1);
-  return pk::M1T::fwd_smem(RP) <= budget && pk::M1T::bwd_smem(RP, C, ns) <= budget;
+  return pk::M1T::fwd_smem(RP) <= budget && pk::M1T::bwd_smem(RP, C, ns, 1) <= budget;
 }
 
 // whether the member's last layer + head + first dgrad fit one TAIL tile
@@ -272,8 +273,22 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   Phase tf, tb;    // tensor-core one-hidden-layer members (train only)
   tf.special = 3;
   tb.special = 4;
-  for (int k = 0; k < p->K; ++k)  // one cluster (= all input splits) per unit tile
-    if (!eval && p->members[k]->m1t) tf.cs = std::max(tf.cs, pk::t_nsplit(p->members[k]->desc.dims[0]));
+  // k_m1t_fwd: one cluster (= all input splits) per unit tile.  k_m1t_bwd: a
+  // CTA per (unit tile, group of G input tiles), G sized for ~one wave; two
+  // input-tile stages in flight when every member's shared memory allows.
+  int n_ut = 0, n_kt = 1;
+  tb.stages = 2;
+  for (int k = 0; k < p->K; ++k) {
+    const pk_member* m = p->members[k];
+    if (eval || !m->m1t) continue;
+    tf.cs = std::max(tf.cs, pk::t_nsplit(m->desc.dims[0]));
+    n_ut += cdiv(m->desc.dims[1], pk::T_BU);
+    n_kt = std::max(n_kt, cdiv(m->desc.dims[0], pk::T_BK));
+    if (pk::M1T::bwd_smem(pk::m1_rows_pad(m->desc.max_rows), m->desc.dims[2], m->n_slots, 2) >
+        smem_budget(dt))
+      tb.stages = 1;
+  }
+  const int G = std::max(1, std::min(n_kt, cdiv(n_ut * n_kt, 148)));
   for (int k = 0; k < p->K; ++k) {
     const pk_member* m = p->members[k];
     if (!eval && m->m1t) {
@@ -281,11 +296,12 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
       const int RP = pk::m1_rows_pad(m->desc.max_rows);
       for (int t = 0; t < pk::t_ntile(H); ++t)
         for (int s = 0; s < tf.cs; ++s) tf.host.push_back(Tile{k, 0, pk::TK_FWD, t, s});
-      for (int kt = 0; kt < cdiv(D, pk::T_BK); ++kt)
-        for (int ut = 0; ut < cdiv(H, pk::T_BU); ++ut)
-          tb.host.push_back(Tile{k, 0, pk::TK_WGRAD, kt, ut});
+      const int nkt = cdiv(D, pk::T_BK);
+      for (int ut = 0; ut < cdiv(H, pk::T_BU); ++ut)
+        for (int kt = 0; kt < nkt; kt += G)
+          tb.host.push_back(Tile{k, (int16_t)std::min(G, nkt - kt), pk::TK_WGRAD, kt, ut});
       tf.smem = std::max(tf.smem, pk::M1T::fwd_smem(RP));
-      tb.smem = std::max(tb.smem, pk::M1T::bwd_smem(RP, C, m->n_slots));
+      tb.smem = std::max(tb.smem, pk::M1T::bwd_smem(RP, C, m->n_slots, tb.stages));
       continue;
     }
     if (!eval && m->mlp1) {
@@ -385,6 +401,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     a.cs = ph.cs;
+    a.stages = ph.stages;
     if (ph.cs > 1) {
       attr[1].id = cudaLaunchAttributeClusterDimension;
       attr[1].val.clusterDim.x = ph.cs;

@@ -22,7 +22,7 @@ import bench  # noqa: E402
 from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
 
 STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1",
-          "s8", "s9", "s10", "s11")
+          "s8", "s9", "s10", "s11", "s12", "s13", "s14", "s15")
 
 
 def main():
