@@ -305,6 +305,10 @@ def _b200(args):
                        "ms": statistics.median(p[i][3] for p in prof), "bytes": nbytes})
     top = max(phases, key=lambda p: p["ms"])
 
+    hyper = None
+    if args.hyperband_r > 0:
+        group = dist.new_group(backend="gloo") if world > 1 else None
+        hyper = _hyperband_b200(args.hyperband_r, world, group, args.hyperband_precision)
     t = torch.tensor([dev_ms, e2e_s * 1e3, hb_s * 1e3, un_ms], dtype=torch.float64,
                      device="cuda")
     if world > 1:
@@ -356,9 +360,69 @@ def _b200(args):
     }
     cpu = _cpu_baseline(wl, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
     line["cpu_baseline"] = cpu
+    line["hyperband"] = hyper
+    if hyper is not None and args.cpu_seconds > 0 and world == 1 and args.hyperband_ref_r > 0:
+        hyper["cpu_reference"] = _hyperband_reference(args.hyperband_ref_r)
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+HB = dict(n=2000, dim=784, classes=10, hidden=(16,), eta=3, seed=0,
+          strategies=("original", "knn"))
+
+
+def _hyperband_b200(R, world, group, precision="f64"):
+    """Pack-aware Hyperband (BASELINE configs[4] shape, MLP executor): wall
+    time of `original` (one config per group) and `knn` packing, rungs sharded
+    over the job's GPUs by hyperband_pool (gloo control plane); max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2002_02885_b200 import data, hyperband_pool, runtime, tuner
+    ds = data.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0)
+    out = {}
+    # float64 device arithmetic: the reference trains in f64, and some
+    # Table-4 configs (e.g. momentum lr 0.1) grow activations past the fp32
+    # range on this data — f64 keeps the trajectories (and selection) the
+    # reference's
+    prev = runtime.default_precision()
+    runtime.set_precision(precision)
+    for strategy in HB["strategies"]:
+        ex = tuner.B200Executor(ds, hidden=HB["hidden"], seed=HB["seed"])
+        if world > 1:
+            dist.barrier(group=group)
+        t0 = time.perf_counter()
+        res, pool = hyperband_pool.sharded_hyperband(R, HB["eta"], ex, HB["seed"],
+                                                     strategy=strategy, group=group)
+        wall = time.perf_counter() - t0
+        t = torch.tensor([wall], dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        out[strategy] = {"wall_s": float(t.item()), "best_config": res.best_config.config_id,
+                         "best_loss": res.best_loss, "epochs": res.total_epochs,
+                         "evaluations": len(res.records), "migrations": pool.migrations}
+    runtime.set_precision(prev)
+    return {"R": R, "dtype": precision, "eta": HB["eta"], "n_train": int(HB["n"] * 0.9), "arch": [HB["dim"], *HB["hidden"], HB["classes"]],
+            "n_gpus": world, "sharding": "rung groups LPT over GPUs (gloo control plane, no NCCL)",
+            "strategies": out,
+            "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
+
+
+def _hyperband_reference(R):
+    """The same Hyperband on the unmodified reference (baseline/_ref), CPU."""
+    if _ref_packtrain() is None:
+        return None
+    from packtrain import data as rdata, tuner as rtuner
+    ds = rdata.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0)
+    out = {}
+    for strategy in HB["strategies"]:
+        ex = rtuner.EngineExecutor(ds, hidden=HB["hidden"], seed=HB["seed"])
+        t0 = time.perf_counter()
+        res = rtuner.packed_hyperband(R, HB["eta"], ex, HB["seed"], strategy=strategy)
+        out[strategy] = {"wall_s": time.perf_counter() - t0,
+                         "best_config": res.best_config.config_id, "best_loss": res.best_loss}
+    return {"R": R, "eta": HB["eta"], "strategies": out, "cores": _cpu_threads(),
+            "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
 
 
 def _cpu_threads():
@@ -439,7 +503,9 @@ def _reference(args):
                        "batch": wl["batch"]},
             "cpu_baseline": r,
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "hyperband": (_hyperband_reference(args.hyperband_ref_r)
+                          if args.hyperband_ref_r > 0 else None)}
 
 
 def main():
@@ -451,6 +517,11 @@ def main():
     ap.add_argument("--workload", default="config0", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--hyperband-r", type=int, default=81,
+                    help="pack-aware Hyperband R on the GPUs (0 = skip)")
+    ap.add_argument("--hyperband-precision", default="f64", choices=["f32", "f64"])
+    ap.add_argument("--hyperband-ref-r", type=int, default=81,
+                    help="the same Hyperband on the CPU reference (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     line = _reference(args) if args.impl == "reference" else _b200(args)
