@@ -260,7 +260,12 @@ def _b200(args):
         dist.barrier()
     clk = clocks.stop()
 
-    # e2e: public API on host datasets (descriptor H2D, losses D2H per step)
+    # e2e: the public API (packing.packed_step) with host datasets streamed:
+    # every step gathers its batch rows on the host into pinned memory, copies
+    # them H2D with the step descriptor, and reads the losses back (D2H)
+    runtime.set_input_mode("stream")
+    for _ in range(3):
+        packing.packed_step(packed, datasets)
     e2e_s = 0.0
     for _ in range(args.steps):
         flush_l2()
@@ -268,14 +273,15 @@ def _b200(args):
         t0 = time.perf_counter()
         packing.packed_step(packed, datasets)
         e2e_s += time.perf_counter() - t0
-    # e2e with the batch rows gathered on the host and copied H2D every step
-    spec = data.PreprocessSpec(stages=(("normalize", 0.0, 1.0),))
+    runtime.set_input_mode("resident")
+    # the same API with the datasets resident on the device (uploaded once;
+    # per step only the descriptor goes H2D) — the framework's default mode
     hb_s = 0.0
     for _ in range(args.steps):
         flush_l2()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        packing.packed_step(packed, datasets, preprocess_spec=spec)
+        packing.packed_step(packed, datasets)
         hb_s += time.perf_counter() - t0
 
     # unpacked: the same K members, one-member packs stepped one after another
@@ -343,12 +349,14 @@ def _b200(args):
         "speedup_vs_unpacked": un_ms / dev_ms,
         "unpacked_ms_per_step": un_ms / args.steps,
         "e2e": {"value": world * K * b * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": desc_bytes, "d2h_bytes_per_step": 16 + 8 * K,
-                "api": "packing.packed_step (host numpy datasets, resident on device)"},
-        "e2e_host_batches": {"value": world * K * b * args.steps / (hb_ms / 1e3), "unit": UNIT,
-                             "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
-                             "d2h_bytes_per_step": 16 + 8 * K,
-                             "api": "packed_step(preprocess_spec=normalize(0,1)): host gather"},
+                "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
+                "d2h_bytes_per_step": 16 + 8 * K,
+                "api": "packing.packed_step, input_mode=stream: host gather → pinned → H2D "
+                       "per step, losses D2H"},
+        "e2e_resident": {"value": world * K * b * args.steps / (hb_ms / 1e3), "unit": UNIT,
+                         "h2d_bytes_per_step": desc_bytes, "d2h_bytes_per_step": 16 + 8 * K,
+                         "api": "packing.packed_step, input_mode=resident: dataset uploaded "
+                                "once, rows gathered on the device"},
         "roofline": {"bound": "hbm", "kernel": f"{kname}[{top['phase']}]",
                      "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / peaks["hbm_gbs"], "traffic": traffic,

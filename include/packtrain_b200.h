@@ -115,6 +115,13 @@ int pk_dataset_create(pk_ctx* ctx, int64_t n, int32_t dim, pk_dataset** out);
 /* write rows [row0, row0+rows) from host f64 features / int64 labels */
 int pk_dataset_write(pk_dataset* ds, int64_t row0, int64_t rows,
                      const double* features, const int64_t* labels);
+/* streamed inputs: rows [row0, row0+rows) already in the context's device
+ * precision (float32 / float64) and int32 labels, copied asynchronously on
+ * the context stream (the host buffers must stay valid until the next sync;
+ * pinned memory makes the copy a true DMA).  Replaces the per-step batch of
+ * _next_batch (packing.py:161-172) when datasets live on the host. */
+int pk_dataset_write_rows(pk_dataset* ds, int64_t row0, int64_t rows, const void* features,
+                          const int32_t* labels);
 int pk_dataset_destroy(pk_dataset* ds);
 int pk_order_create(pk_ctx* ctx, const int64_t* perm, int64_t n, pk_order** out);
 int pk_order_destroy(pk_order* order);

@@ -202,6 +202,23 @@ extern "C" int pk_dataset_write(pk_dataset* d, int64_t row0, int64_t rows, const
   return PK_OK;
 }
 
+// device-precision rows straight from (pinned) host memory, enqueued on the
+// context stream without a host sync: the streamed-input path of a step
+extern "C" int pk_dataset_write_rows(pk_dataset* d, int64_t row0, int64_t rows, const void* x,
+                                     const int32_t* y) {
+  if (!d) return PK_ERR_ARG;
+  pk_ctx* c = d->ctx;
+  if (row0 < 0 || rows < 0 || row0 + rows > d->n || (!x && rows) || (!y && rows))
+    return arg_err(c, "dataset_write_rows: bad range");
+  if (!rows) return PK_OK;
+  cudaSetDevice(c->device);
+  CK_CTX(c, cudaMemcpyAsync((char*)d->feat + (size_t)row0 * d->dim * c->esize(), x,
+                            (size_t)rows * d->dim * c->esize(), cudaMemcpyHostToDevice, c->stream));
+  CK_CTX(c, cudaMemcpyAsync(d->labels + row0, y, (size_t)rows * 4, cudaMemcpyHostToDevice,
+                            c->stream));
+  return PK_OK;
+}
+
 extern "C" int pk_dataset_destroy(pk_dataset* d) {
   if (!d) return PK_ERR_ARG;
   cudaSetDevice(d->ctx->device);

@@ -110,6 +110,29 @@ def _stage_row(spec: PreprocessSpec, row: np.ndarray, index: int) -> np.ndarray:
     return out
 
 
+def preprocess_all(spec: PreprocessSpec, features: np.ndarray) -> np.ndarray:
+    """Every sample through the stage list (row i keyed by dataset index i) —
+    the whole-dataset form of the per-sample memo, values identical to
+    `preprocess` row by row (pure per-index stages, data.py:156-173)."""
+    x = np.asarray(features, dtype=np.float64)
+    return np.stack([_stage_row(spec, x[i], i) for i in range(x.shape[0])]) if len(x) else x
+
+
+def account_cache(spec: PreprocessSpec, table: np.ndarray, indices, dataset_id: str,
+                  cache: PreprocessCache):
+    """The cache bookkeeping `preprocess` does for a batch (hits, misses,
+    entries keyed (dataset, spec digest, index)), with values taken from an
+    already materialized `table` (data.py:183-193)."""
+    dig = spec.digest()
+    for i in np.asarray(indices):
+        key = (dataset_id, dig, int(i))
+        if key in cache.entries:
+            cache.hits += 1
+        else:
+            cache.misses += 1
+            cache.entries[key] = table[int(i)].copy()
+
+
 def preprocess(spec: PreprocessSpec, batch: np.ndarray, indices, dataset_id: str,
                cache: PreprocessCache | None = None) -> np.ndarray:
     """Per-sample stages memoized on (dataset, spec digest, index)

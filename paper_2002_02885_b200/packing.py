@@ -23,7 +23,7 @@ import numpy as np
 
 from . import engine
 from . import runtime as _rt
-from .data import Dataset, batch_at, epoch_permutation, preprocess
+from .data import Dataset, account_cache, epoch_permutation, preprocess
 from .engine import ComputationGraph
 from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE
 
@@ -242,6 +242,14 @@ class PackedModel:
                 return h
         raise PackError(f"unknown model_id {model_id!r}")
 
+    def _stream(self, rt, gi, x, y):
+        dev, hx, hy = _stream_staging(self, rt, gi, x.shape[0], x.shape[1])
+        n = x.shape[0]
+        hx[:n] = x  # f64 → device precision, round-to-nearest (as pk_dataset_write)
+        hy[:n] = y
+        dev.write_rows(0, hx[:n], hy[:n])
+        return dev
+
     def input_groups(self):
         """Members partitioned by (dataset, epoch, cursor, batch) (packing.py:121-128)."""
         g: dict = {}
@@ -263,13 +271,26 @@ class PackedModel:
             self._dev = (key, _rt.DevicePack(rt, devs), {})
         return self._dev[1]
 
-    def _staging(self, rt, gi, rows, dim):
-        stg = self._dev[2]
-        d = stg.get(gi)
-        if d is None or d.n < rows or d.dim != dim:
-            d = _rt.DeviceDataset(rt, max(rows, self.driver_batch), dim)
-            stg[gi] = d
-        return d
+
+def _pinned(shape, dtype):
+    import torch
+    t = torch.empty(shape, dtype={np.float32: torch.float32, np.float64: torch.float64,
+                                  np.int32: torch.int32}[dtype], pin_memory=True)
+    return t.numpy()
+
+
+def _stream_staging(packed, rt, gi, rows, dim):
+    """Per (pack, input group): a device staging dataset and pinned host
+    buffers for streamed inputs (input_mode 'stream')."""
+    stg = packed._dev[2]
+    d = stg.get(gi)
+    if d is None or d[0].n < rows or d[0].dim != dim:
+        n = max(rows, packed.driver_batch)
+        d = (_rt.DeviceDataset(rt, n, dim),
+             _pinned((n, dim), np.float64 if rt.dtype == "f64" else np.float32),
+             _pinned((n,), np.int32))
+        stg[gi] = d
+    return d
 
 
 def pack_models(handles) -> PackedModel:
@@ -364,15 +385,25 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
             if bad:
                 raise IndexError(f"label out of bounds for member {bad[0].model_id!r} "
                                  f"with {bad[0].arch.classes} classes")
-        if preprocess_spec is not None and preprocess_spec.stages:
-            x, y, idx = batch_at(ds, perm, cur.pos, take)
-            x = preprocess(preprocess_spec, x, idx, ds.dataset_id, cache)
-            stg = packed._staging(rt, gi, take, ds.dim)
-            stg.write(0, x, y)
-            src, order, pos = stg, None, 0
+        if _rt.input_mode() == "stream":
+            # host gather (+ per-sample preprocess) into pinned staging, H2D
+            x = ds.features[idx]
+            if preprocess_spec is not None and preprocess_spec.stages:
+                x = preprocess(preprocess_spec, x, idx, ds.dataset_id, cache)
+            src = packed._stream(rt, gi, x, ds.labels[idx])
+            order, pos = None, 0
         else:
-            src = rt.dataset(ds)
-            order = rt.order(ds.dataset_id, ds.n, cur.epoch_index, _order_fn(ds, cur.epoch_index))
+            if preprocess_spec is not None and preprocess_spec.stages:
+                # device-resident preprocessed copy (memo over the whole
+                # dataset); the PreprocessCache sees the reference's per-sample
+                # bookkeeping
+                src, table = rt.preprocessed(ds, preprocess_spec)
+                if cache is not None:
+                    account_cache(preprocess_spec, table, idx, ds.dataset_id, cache)
+            else:
+                src = rt.dataset(ds)
+            order = rt.order(ds.dataset_id, ds.n, cur.epoch_index,
+                             _order_fn(ds, cur.epoch_index))
             pos = cur.pos
         physical += 1 if packed.share_inputs else len(grp)
         for h in grp:

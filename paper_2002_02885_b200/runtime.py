@@ -17,7 +17,21 @@ import numpy as np
 from . import _lib as L
 
 _RUNTIMES: dict = {}
-_DEFAULT = {"device": None, "dtype": None}
+_DEFAULT = {"device": None, "dtype": None, "inputs": None}
+
+
+def set_input_mode(mode: str):
+    """'resident' (default): datasets are uploaded once and steps gather
+    their rows on the device.  'stream': every step gathers its batch rows on
+    the host into pinned memory and copies them H2D (the reference's
+    per-step `_next_batch`, packing.py:161-172, as a real host→device feed)."""
+    if mode not in ("resident", "stream"):
+        raise ValueError("input mode must be 'resident' or 'stream'")
+    _DEFAULT["inputs"] = mode
+
+
+def input_mode() -> str:
+    return _DEFAULT["inputs"] or os.environ.get("PACKTRAIN_INPUTS", "resident")
 
 
 def set_device(device: int):
@@ -99,6 +113,23 @@ class Runtime:
             self._datasets[key] = d
         return d
 
+    def preprocessed(self, ds, spec):
+        """Device-resident copy of `ds` with every sample through `spec`
+        (SURVEY §8f-2): materialized once per (dataset, spec digest) on the
+        host with the reference's per-index formulas, uploaded once; steps then
+        gather rows on the device like any dataset.  Returns (device dataset,
+        host f64 table)."""
+        from .data import preprocess_all
+        key = ("pre", ds.dataset_id, spec.digest(), id(ds.features), ds.features.shape)
+        got = self._datasets.get(key)
+        if got is None:
+            table = preprocess_all(spec, ds.features)
+            d = DeviceDataset(self, ds.n, ds.dim)
+            d.write(0, table, ds.labels)
+            got = (d, table)
+            self._datasets[key] = got
+        return got
+
     def host_order(self, dataset_id: str, n: int, epoch: int, make) -> np.ndarray:
         key = (dataset_id, n, epoch)
         o = self._host_orders.get(key)
@@ -138,6 +169,13 @@ class DeviceDataset:
         ptr = C.c_void_p()
         rt.check(rt.lib.pk_dataset_create(rt.ptr, self.n, self.dim, C.byref(ptr)))
         self.ptr = ptr
+
+    def write_rows(self, row0: int, x, y):
+        """Async H2D of rows already in device precision (x) / int32 (y);
+        x and y must stay alive until the stream syncs (pinned: true DMA)."""
+        self.rt.check(self.rt.lib.pk_dataset_write_rows(
+            self.ptr, int(row0), int(x.shape[0]), x.ctypes.data_as(C.c_void_p),
+            y.ctypes.data_as(C.c_void_p)))
 
     def write(self, row0: int, features, labels):
         x = np.ascontiguousarray(features, dtype=np.float64)

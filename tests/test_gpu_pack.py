@@ -492,3 +492,26 @@ def test_pool_world1_matches_serial_and_migrates_state_bitwise():
     l1, _ = ex.evaluate([cfg], 1)
     l2, _ = twin.evaluate([cfg], 1)
     assert l1 == l2
+
+
+def test_streamed_inputs_match_resident_bitwise():
+    """input_mode 'stream' (host gather → pinned → H2D per step) trains the
+    same bits as the device-resident gather, with and without preprocessing."""
+    spec = data.PreprocessSpec(stages=(("normalize", 0.5, 2.0), ("jitter", 7)))
+    out = {}
+    for mode in ("resident", "stream"):
+        runtime.set_input_mode(mode)
+        try:
+            datasets = _ds()
+            hs = [_h("a", seed=1), _h("b", seed=2, opt="adam")]
+            packed = packing.dedup_inputs(packing.pack_models(hs))
+            cache = data.PreprocessCache()
+            losses = [packing.packed_step(packed, datasets, preprocess_spec=spec if i % 2 else None,
+                                          cache=cache) for i in range(6)]
+            out[mode] = (losses, [h._flat_params(h.params) for h in hs], cache.hits, cache.misses)
+        finally:
+            runtime.set_input_mode("resident")
+    assert out["resident"][0] == out["stream"][0]
+    for a, b in zip(out["resident"][1], out["stream"][1]):
+        np.testing.assert_array_equal(a, b)
+    assert out["resident"][2:] == out["stream"][2:]

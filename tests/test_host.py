@@ -215,3 +215,23 @@ def test_accountant_registers_and_overflows():
     with pytest.raises(device.OOMError):
         packing.load_model(big, device=acct)
     assert "big" not in acct.resident and nb > 0
+
+
+def test_preprocess_memo_matches_per_sample_path():
+    """§8f-2: the whole-dataset preprocessed table equals the per-sample
+    `preprocess` output row for row, and account_cache reproduces its
+    hit/miss/entry bookkeeping (reference data.py:176-194)."""
+    ds = data.synth_dataset(50, 6, 3, seed=4)
+    spec = data.PreprocessSpec(stages=(("normalize", 0.5, 2.0), ("jitter", 7)))
+    table = data.preprocess_all(spec, ds.features)
+    idx = np.array([3, 17, 3, 42, 0])
+    want = data.preprocess(spec, ds.features[idx], idx, ds.dataset_id)
+    np.testing.assert_array_equal(table[idx], want)
+    c1, c2 = data.PreprocessCache(), data.PreprocessCache()
+    for batch in (idx, idx[::-1], np.array([1, 2])):
+        data.preprocess(spec, ds.features[batch], batch, ds.dataset_id, c1)
+        data.account_cache(spec, table, batch, ds.dataset_id, c2)
+    assert (c1.hits, c1.misses) == (c2.hits, c2.misses)
+    assert c1.entries.keys() == c2.entries.keys()
+    for k in c1.entries:
+        np.testing.assert_array_equal(c1.entries[k], c2.entries[k])
