@@ -107,6 +107,8 @@ struct Tile {
   int32_t m0, n0;
 };
 
+constexpr int kInlineFeeds = 32;  // packs up to this K take inline step descriptors
+
 struct StepHdr {
   int32_t K;
   int32_t slot;   // result ring slot (host-mapped)
@@ -129,7 +131,22 @@ struct PhaseArgs {
   unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
   int32_t cs;          // cluster size of this launch (k_m1t_fwd: input splits)
   int32_t stages;      // k_m1t_bwd: input-tile stages in flight
+  // > 0: the step header and the first `nin` feeds travel inline in the kernel
+  // parameters (the train graph's kernel nodes are re-parameterised per step:
+  // no descriptor copy, feed reads hit the constant bank)
+  int32_t nin;
+  StepHdr hdr_in;
+  FeedDev<T> feeds_in[kInlineFeeds];
 };
+
+template <typename T>
+__device__ __forceinline__ FeedDev<T> feed_of(const PhaseArgs<T>& P, int k) {
+  return P.nin ? P.feeds_in[k] : P.feeds[k];
+}
+template <typename T>
+__device__ __forceinline__ StepHdr hdr_of(const PhaseArgs<T>& P) {
+  return P.nin ? P.hdr_in : *P.hdr;
+}
 
 // ---- stage tracing (profiling builds of a step, PK_TRACE=1) -------------
 // Thread 0 of a CTA stamps %globaltimer at stage boundaries:
@@ -797,7 +814,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   // warp w reduces the loss terms of members w, w+8, ...: lane-strided
   // partial sums then a fixed butterfly (deterministic, K-invariant)
   for (int k = warp; k < K; k += NT / 32) {
-    const int take = P.feeds[k].take;
+    const int take = feed_of(P, k).take;
     int bn = INT_MAX, bg = INT_MAX;
     if (take) {
       const MemberDev<T>& M = P.mems[k];
@@ -833,12 +850,12 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
     s_code = code; s_who = who; s_idx = idx; s_stop = stop;
   }
   __syncthreads();
-  int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)P.hdr->slot * P.ring_stride);
+  int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)hdr_of(P).slot * P.ring_stride);
   double* losses = reinterpret_cast<double*>(st + 4);
   int committed = 0;
   for (int k = threadIdx.x; k < K; k += NT) {
     MemberCtl* c = P.mems[k].ctl;
-    const bool act = P.feeds[k].take != 0;
+    const bool act = feed_of(P, k).take != 0;
     if (train) {
       losses[k] = act ? c->loss : 0.0;
       if (act && k < s_stop) {
@@ -879,7 +896,7 @@ __device__ __noinline__ void prefetch_params(const PhaseArgs<T>& P) {
   const int64_t gs = (int64_t)gridDim.x * NT;
   int64_t base = 0;
   for (int k = 0; k < P.K; ++k) {
-    if (!P.feeds[k].take) continue;
+    if (!feed_of(P, k).take) continue;
     const MemberDev<T>& M = P.mems[k];
     const int par = M.ctl->parity;
     for (int s = -1; s < M.n_slots; ++s) {
@@ -931,7 +948,7 @@ constexpr int KM_FWD = 1 << TK_FWD, KM_TAIL = 1 << TK_TAIL, KM_HEAD = 1 << TK_HE
 constexpr int KM_DGRAD = 1 << TK_DGRAD, KM_WGRAD = 1 << TK_WGRAD, KM_ALL = 31;
 
 template <typename T, int MASK>
-__global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
+__global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(16) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -939,8 +956,8 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
   pdl_launch();
   if (P.prefetch) prefetch_params(P);
   const Tile t = P.tiles[blockIdx.x];
-  const FeedDev<T> f = P.feeds[t.member];
-  const bool train = (P.hdr->mode == 0);
+  const FeedDev<T> f = feed_of(P, t.member);
+  const bool train = (hdr_of(P).mode == 0);
   if (f.take != 0) {
     const MemberDev<T>& M = P.mems[t.member];
     if ((MASK & KM_FWD) && t.kind == TK_FWD) {
@@ -965,7 +982,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const PhaseArgs<T> P) {
 // tcgen05 3xTF32 one-hidden-layer step (fp32 members only; the f64 device
 // mode never schedules these phases)
 template <typename T>
-__global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const PhaseArgs<T> P) {
+__global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(128) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -973,8 +990,15 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const PhaseArgs<T> P) {
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
     const Tile t = P.tiles[blockIdx.x];
-    const FeedDev<T> f = P.feeds[t.member];
-    if (f.take != 0) m1t_fwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.n0, P.cs);
+    const FeedDev<T> f = feed_of(P, t.member);
+    // the member's descriptor in shared memory: every field read is an LDS,
+    // not a global load on the critical path
+    __shared__ MemberDev<float> sM;
+    if (threadIdx.x < sizeof(MemberDev<float>) / 4)
+      reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
+          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+    __syncthreads();
+    if (f.take != 0) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
   } else {
     __trap();
   }
@@ -982,7 +1006,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const PhaseArgs<T> P) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const PhaseArgs<T> P) {
+__global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(128) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -990,9 +1014,14 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const PhaseArgs<T> P) {
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
     const Tile t = P.tiles[blockIdx.x];
-    const FeedDev<T> f = P.feeds[t.member];
+    const FeedDev<T> f = feed_of(P, t.member);
     // m0 = first input tile, layer = input tiles in the group, n0 = unit tile
-    if (f.take != 0) m1t_bwd_tile(smem_raw, P.mems[t.member], f, t.m0, t.layer, t.n0, P.stages);
+    __shared__ MemberDev<float> sM;
+    if (threadIdx.x < sizeof(MemberDev<float>) / 4)
+      reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
+          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+    __syncthreads();
+    if (f.take != 0) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages);
   } else {
     __trap();
   }
@@ -1000,7 +1029,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const PhaseArgs<T> P) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const PhaseArgs<T> P) {
+__global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(16) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -1008,20 +1037,20 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const PhaseArgs<T> P) {
   pdl_launch();
   if (P.prefetch) prefetch_params(P);
   const Tile t = P.tiles[blockIdx.x];
-  const FeedDev<T> f = P.feeds[t.member];
+  const FeedDev<T> f = feed_of(P, t.member);
   if (f.take != 0) m1_fwd_tile<T>(smem_raw, P.mems[t.member], f, t.m0);
   kernel_end(P, true);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const PhaseArgs<T> P) {
+__global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(16) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
   pdl_launch();
   const Tile t = P.tiles[blockIdx.x];
-  const FeedDev<T> f = P.feeds[t.member];
+  const FeedDev<T> f = feed_of(P, t.member);
   if (f.take != 0) {
     const MemberDev<T>& M = P.mems[t.member];
     m1_bwd_tile<T>(smem_raw, M, f, t.m0, (M.dims[1] + M1_BC - 1) / M1_BC);

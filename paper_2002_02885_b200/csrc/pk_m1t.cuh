@@ -102,8 +102,6 @@ __device__ __forceinline__ void xent_row_thread(float* z, int C, int y, int R, d
 // block's partial logits.
 __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
                              int tile, int split, int CS) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows);
   const int u0 = tile * T_UM, nu = min(T_UM, H - u0);
@@ -237,7 +235,7 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     }
   }
   umma::fence_before();
-  cl.sync();  // all partials of the tile are in the cluster's shared memory
+  umma::cluster_sync();  // all partials of the tile are in the cluster's shared memory
   PK_TRACE(3);
   if (warp == 1) umma::tmem_dealloc(tmem, tcols);
   // ---- rank q: member-local 32-unit blocks q, q + CS, ... of this tile ------
@@ -281,7 +279,8 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   }
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   PK_TRACE(4);
-  cl.sync();  // peers are done reading this CTA's partial
+  umma::cluster_arrive_relaxed();  // peers are done reading this CTA's partial:
+  umma::cluster_wait();            // no memory ordering needed, just the rendezvous
 }
 
 // ----------------------------------------------------------- backward --

@@ -49,6 +49,17 @@ struct pk_pack {
   bool ev_pending[kRing];
   int64_t next_ticket = 0;
   cudaGraphExec_t exec = nullptr;
+  // inline step descriptors (K <= kInlineFeeds): the train graph's kernel
+  // nodes, re-parameterised every step instead of copying a descriptor H2D
+  struct Node {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams kp;
+    std::vector<char> args;  // PhaseArgs<T> bytes
+  };
+  bool inline_desc = false;
+  cudaGraph_t graph = nullptr;
+  std::vector<Node> nodes;
+  std::vector<char> h_feeds;  // host FeedDev<T>[K] of the step being launched
 };
 
 template <typename T>
@@ -363,7 +374,8 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
 // launch run FINALIZE
 template <typename T>
 static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only = -1,
-                         bool finalize = true) {
+                         bool finalize = true, const StepHdr* hin = nullptr,
+                         std::vector<pk_pack::Node>* rec = nullptr) {
   cudaStream_t s = p->ctx->stream;
   int last = -1, first = -1;
   for (int i = 0; i < (int)phases.size(); ++i)
@@ -402,6 +414,11 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.numAttrs = 1;
     a.cs = ph.cs;
     a.stages = ph.stages;
+    if (hin) {  // inline descriptor (feeds staged in p->h_feeds by the caller)
+      a.nin = p->K;
+      a.hdr_in = *hin;
+      memcpy(a.feeds_in, p->h_feeds.data(), sizeof(FeedDev<T>) * p->K);
+    }
     if (ph.cs > 1) {
       attr[1].id = cudaLaunchAttributeClusterDimension;
       attr[1].val.clusterDim.x = ph.cs;
@@ -418,6 +435,24 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     if (e != cudaSuccess) {
       p->ctx->err = std::string("launch phase: ") + cudaGetErrorString(e);
       return PK_ERR_CUDA;
+    }
+    if (rec) {  // capturing: remember the kernel node this launch became
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      e = cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd);
+      if (e != cudaSuccess || nd != 1) {
+        p->ctx->err = "capture: cannot identify the kernel node";
+        return PK_ERR_CUDA;
+      }
+      pk_pack::Node nd_{};
+      nd_.node = deps[0];
+      nd_.args.assign(reinterpret_cast<const char*>(&a), reinterpret_cast<const char*>(&a) + sizeof(a));
+      nd_.kp.func = reinterpret_cast<void*>(kern);
+      nd_.kp.gridDim = cfg.gridDim;
+      nd_.kp.blockDim = cfg.blockDim;
+      nd_.kp.sharedMemBytes = (unsigned)cfg.dynamicSmemBytes;
+      rec->push_back(std::move(nd_));
     }
   }
   return PK_OK;
@@ -449,6 +484,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
   p->ctx = c;
   p->members.assign(members, members + k);
   p->K = k;
+  p->inline_desc = k <= pk::kInlineFeeds && !getenv("PK_NO_INLINE_DESC");
   size_t mdsz = c->dtype == PK_F64 ? sizeof(MemberDev<double>) : sizeof(MemberDev<float>);
   std::vector<char> hm(mdsz * k);
   for (int i = 0; i < k; ++i) {
@@ -534,6 +570,7 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
   for (int i = 0; i < kRing; ++i) cudaEventDestroy(p->ev[i]);
   cudaFree(p->d_members);
   cudaFree(p->d_blob);
@@ -608,17 +645,46 @@ extern "C" int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* tic
   int slot;
   int rc = acquire_slot(p, t, &slot);
   if (rc) return rc;
-  if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
-  if (!p->exec) {
-    cudaGraph_t g;
-    CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    rc = launch(p, p->train);
-    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  if (p->inline_desc) {
+    // feeds + header ride in the kernel parameters of the graph's nodes
+    p->h_feeds.resize(feed_size(c->dtype) * p->K);
+    rc = c->dtype == PK_F64 ? fill_feeds<double>(p, feeds, p->h_feeds.data())
+                            : fill_feeds<float>(p, feeds, p->h_feeds.data());
     if (rc) return rc;
-    CK_CTX(c, e);
-    e = cudaGraphInstantiate(&p->exec, g, 0);
-    cudaGraphDestroy(g);
-    CK_CTX(c, e);
+    const StepHdr hdr{p->K, slot, 0, 0};
+    if (!p->exec) {
+      CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      p->nodes.clear();
+      rc = c->dtype == PK_F64 ? launch_phases<double>(p, p->train, -1, true, &hdr, &p->nodes)
+                              : launch_phases<float>(p, p->train, -1, true, &hdr, &p->nodes);
+      cudaError_t e = cudaStreamEndCapture(c->stream, &p->graph);
+      if (rc) return rc;
+      CK_CTX(c, e);
+      CK_CTX(c, cudaGraphInstantiate(&p->exec, p->graph, 0));
+    } else {
+      const size_t o_hdr = c->dtype == PK_F64 ? offsetof(pk::PhaseArgs<double>, hdr_in)
+                                              : offsetof(pk::PhaseArgs<float>, hdr_in);
+      const size_t o_feeds = c->dtype == PK_F64 ? offsetof(pk::PhaseArgs<double>, feeds_in)
+                                                : offsetof(pk::PhaseArgs<float>, feeds_in);
+      for (auto& n : p->nodes) {
+        memcpy(n.args.data() + o_hdr, &hdr, sizeof(hdr));
+        memcpy(n.args.data() + o_feeds, p->h_feeds.data(), p->h_feeds.size());
+        void* args[1] = {n.args.data()};
+        n.kp.kernelParams = args;
+        n.kp.extra = nullptr;
+        CK_CTX(c, cudaGraphExecKernelNodeSetParams(p->exec, n.node, &n.kp));
+      }
+    }
+  } else {
+    if ((rc = launch_desc(p, slot, 0, feeds))) return rc;
+    if (!p->exec) {
+      CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      rc = launch(p, p->train);
+      cudaError_t e = cudaStreamEndCapture(c->stream, &p->graph);
+      if (rc) return rc;
+      CK_CTX(c, e);
+      CK_CTX(c, cudaGraphInstantiate(&p->exec, p->graph, 0));
+    }
   }
   CK_CTX(c, cudaGraphLaunch(p->exec, c->stream));
   CK_CTX(c, cudaEventRecord(p->ev[slot], c->stream));

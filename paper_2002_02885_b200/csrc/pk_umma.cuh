@@ -118,6 +118,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       : "memory");
 }
 
+// ---- cluster barrier ----------------------------------------------------------
+__device__ __forceinline__ void cluster_sync() {  // arrive.release + wait.acquire
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // ---- distributed shared memory ---------------------------------------------
 // load the float at local shared address `la` of cluster CTA `rank`
 __device__ __forceinline__ float dsmem_ld(uint32_t la, uint32_t rank) {
