@@ -75,22 +75,42 @@ struct M1T {
   }
 };
 
-// softmax-xent of one row by one thread (same formulas and order of
-// operations per element as xent_row; engine.py:211-230, :252-264):
-// z ← dlogits in place, −logp[y] into *rowloss
-__device__ __forceinline__ void xent_row_thread(float* z, int C, int y, int R, double* rowloss) {
-  float mx = z[0];
-  for (int c = 1; c < C; ++c) mx = fmaxf(mx, z[c]);
-  float s = 0.f;
-  for (int c = 0; c < C; ++c) s += ex(z[c] - mx);
-  const float zy = z[y];
-  const float inv = 1.f / s, nv = float(R);
-  for (int c = 0; c < C; ++c) {
-    float p = ex(z[c] - mx) * inv;
-    if (c == y) p -= 1.f;
-    z[c] = p / nv;
+// softmax-xent of one row by an aligned group of 8 lanes (classes c ≡ lane
+// mod 8, C <= 32; engine.py:211-230, :252-264): z ← dlogits in place,
+// −logp[y] into *rowloss.  `live` = false lanes join the shuffles only.
+__device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool live,
+                                          double* rowloss) {
+  const int q = threadIdx.x & 7;
+  float v[4];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = q + 8 * i;
+    v[i] = c < C ? z[c] : -INFINITY;
+    mx = fmaxf(mx, v[i]);
   }
-  if (rowloss) *rowloss = -(double)((zy - mx) - lg(s));
+#pragma unroll
+  for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o, 8));
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (q + 8 * i < C) s += ex(v[i] - mx);
+#pragma unroll
+  for (int o = 4; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 8);
+  const float zy = z[y];
+  __syncwarp();
+  if (!live) return;
+  const float inv = 1.f / s, nv = float(R);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = q + 8 * i;
+    if (c < C) {
+      float p = ex(v[i] - mx) * inv;
+      if (c == y) p -= 1.f;
+      z[c] = p / nv;
+    }
+  }
+  if (q == 0 && rowloss) *rowloss = -(double)((zy - mx) - lg(s));
 }
 
 // ------------------------------------------------------------ forward --
@@ -395,9 +415,10 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   __syncthreads();
   PK_TRACE(8);
   if (tid == 0 && pk_trace_slots) pk_trace_slots[12] = clock64();
-  for (int r = tid; r < R; r += NT) {  // one thread per row: no shuffles, C <= 32
-    float* row = sL + r * (T_MAXC + 1);
-    xent_row_thread(row, C, ylab[r], R, owner ? M.rowloss + r : nullptr);
+  for (int r0 = 0; r0 < R; r0 += NT / 8) {  // 8 lanes per row, every warp busy
+    const int r = r0 + (tid >> 3);
+    xent_row8(sL + min(r, R - 1) * (T_MAXC + 1), C, ylab[min(r, R - 1)], R, r < R,
+              owner && r < R ? M.rowloss + r : nullptr);
   }
   if (tid == 0 && pk_trace_slots) pk_trace_slots[13] = clock64();
   PK_TRACE(9);
