@@ -230,6 +230,8 @@ class PackedModel:
     share_inputs: bool = False
     last_step_stats: dict = field(default_factory=dict)
     _dev: object = field(default=None, repr=False, compare=False)
+    _spec: object = field(default=None, repr=False, compare=False)  # speculated next plan
+    _buf: int = field(default=0, repr=False, compare=False)         # stream staging parity
 
     @property
     def driver_batch(self) -> int:
@@ -242,8 +244,8 @@ class PackedModel:
                 return h
         raise PackError(f"unknown model_id {model_id!r}")
 
-    def _stream(self, rt, gi, x, y):
-        dev, hx, hy = _stream_staging(self, rt, gi, x.shape[0], x.shape[1])
+    def _stream(self, rt, gi, x, y, buf=0):
+        dev, hx, hy = _stream_staging(self, rt, (gi, buf), x.shape[0], x.shape[1])
         n = x.shape[0]
         hx[:n] = x  # f64 → device precision, round-to-nearest (as pk_dataset_write)
         hy[:n] = y
@@ -352,16 +354,18 @@ class _StepPlan:
     __slots__ = ("dpack", "index", "takes", "n_groups", "physical", "driver")
 
 
-def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
+def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache, curs=None,
+               buf=0):
     """Host half of a packed step: input groups, batch rows and the per-member
-    device feeds (packing.py:206-239).  Reads cursors, changes nothing."""
+    device feeds (packing.py:206-239).  Reads cursors (or the (epoch, pos)
+    overrides in `curs`, for speculation), changes no member state."""
     rt = _rt.runtime()
     plan = _StepPlan()
     plan.driver = max(h.batch_size for h in active)
     groups: dict = {}
     for h in active:
-        groups.setdefault((h.dataset_binding, h.cursor.epoch_index, h.cursor.pos,
-                           h.batch_size), []).append(h)
+        ep, ps = curs[id(h)] if curs is not None else (h.cursor.epoch_index, h.cursor.pos)
+        groups.setdefault((h.dataset_binding, ep, ps, h.batch_size), []).append(h)
     dpack = packed._device_pack(rt)
     plan.dpack = dpack
     plan.index = index = {id(h): k for k, h in enumerate(packed.members)}
@@ -376,10 +380,10 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
             if ds.dim != h.arch.input_dim:
                 raise engine.ShapeMismatch(f"{h.model_id}/x", ("batch", h.arch.input_dim),
                                            (plan.driver, ds.dim))
-        cur = lead.cursor
-        take = min(lead.batch_size, ds.n - cur.pos)
-        perm = rt.host_order(ds.dataset_id, ds.n, cur.epoch_index, _order_fn(ds, cur.epoch_index))
-        idx = perm[cur.pos:cur.pos + take]
+        _, c_epoch, c_pos, _ = key
+        take = min(lead.batch_size, ds.n - c_pos)
+        perm = rt.host_order(ds.dataset_id, ds.n, c_epoch, _order_fn(ds, c_epoch))
+        idx = perm[c_pos:c_pos + take]
         if _dataset_max_label(rt, ds) >= min(h.arch.classes for h in grp):
             bad = [h for h in grp if int(ds.labels[idx].max()) >= h.arch.classes]
             if bad:
@@ -390,7 +394,7 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
             x = ds.features[idx]
             if preprocess_spec is not None and preprocess_spec.stages:
                 x = preprocess(preprocess_spec, x, idx, ds.dataset_id, cache)
-            src = packed._stream(rt, gi, x, ds.labels[idx])
+            src = packed._stream(rt, gi, x, ds.labels[idx], buf)
             order, pos = None, 0
         else:
             if preprocess_spec is not None and preprocess_spec.stages:
@@ -402,9 +406,8 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
                     account_cache(preprocess_spec, table, idx, ds.dataset_id, cache)
             else:
                 src = rt.dataset(ds)
-            order = rt.order(ds.dataset_id, ds.n, cur.epoch_index,
-                             _order_fn(ds, cur.epoch_index))
-            pos = cur.pos
+            order = rt.order(ds.dataset_id, ds.n, c_epoch, _order_fn(ds, c_epoch))
+            pos = c_pos
         physical += 1 if packed.share_inputs else len(grp)
         for h in grp:
             dpack.set_feed(index[id(h)], src, order, pos, take, gi)
@@ -435,9 +438,64 @@ def _apply_result(packed: PackedModel, active, plan: _StepPlan, code, who, where
     return out
 
 
-def _device_step(packed: PackedModel, active, datasets, preprocess_spec, cache):
-    plan = _plan_step(packed, active, datasets, preprocess_spec, cache)
-    code, who, where, _, losses = plan.dpack.step()
+def _state_key(packed, active, curs, datasets, stop_at_epoch_end, dpack):
+    """Everything a step plan depends on besides member parameters."""
+    return (dpack, stop_at_epoch_end, _rt.input_mode(), packed.share_inputs,
+            tuple((id(h), curs[id(h)] if curs is not None else
+                   (h.cursor.epoch_index, h.cursor.pos), h.batch_size, h.dataset_binding,
+                   id(datasets[h.dataset_binding])) for h in active))
+
+
+def _speculate(packed, active, plan, datasets, stop_at_epoch_end, buf):
+    """While step n runs on the device, plan step n+1 assuming step n
+    commits: shadow cursors advance by their take and roll epochs exactly as
+    _active_members would (packing.py:175-204).  The plan is used only if the
+    real state at the next call matches its key."""
+    try:
+        shadow, nxt = {}, []
+        for h in packed.members:
+            c = h.cursor
+            ep, pos, steps = c.epoch_index, c.pos, c.steps_done
+            if id(h) in plan.takes:
+                steps += 1
+                pos += plan.takes[id(h)][1]
+            if steps >= h.target_steps:
+                continue
+            n = datasets[h.dataset_binding].n
+            if c.samples_used is None:
+                pos = 0
+            if pos >= n:
+                if stop_at_epoch_end:
+                    continue
+                ep, pos = ep + 1, 0
+            shadow[id(h)] = (ep, pos)
+            nxt.append(h)
+        if not nxt:
+            return None
+        nplan = _plan_step(packed, nxt, datasets, None, None, curs=shadow, buf=buf)
+        return _state_key(packed, nxt, shadow, datasets, stop_at_epoch_end, nplan.dpack), nplan
+    except Exception:  # the real call recomputes (and raises) if needed
+        return None
+
+
+def _device_step(packed: PackedModel, active, datasets, preprocess_spec, cache,
+                 stop_at_epoch_end=False):
+    spec = packed._spec
+    packed._spec = None
+    plan = None
+    plain = preprocess_spec is None or not preprocess_spec.stages
+    if spec is not None and plain:
+        dpack = packed._device_pack(_rt.runtime())  # syncs host-side parameter edits
+        if spec[0] == _state_key(packed, active, None, datasets, stop_at_epoch_end, dpack):
+            plan = spec[1]
+    if plan is None:
+        packed._buf ^= 1
+        plan = _plan_step(packed, active, datasets, preprocess_spec, cache, buf=packed._buf)
+    ticket = plan.dpack.step_async()
+    if plain:  # host planning of the next step overlaps this one on the device
+        packed._buf ^= 1
+        packed._spec = _speculate(packed, active, plan, datasets, stop_at_epoch_end, packed._buf)
+    code, who, where, _, losses = plan.dpack.wait(ticket)
     out = _apply_result(packed, active, plan, code, who, where, losses)
     return out, plan.n_groups, plan.physical, plan.driver
 
@@ -463,7 +521,8 @@ def packed_step(packed: PackedModel, datasets, preprocess_spec=None, cache=None,
     (packing.py:185-264).  Returns {model_id: loss}."""
     active = _active_members(packed, datasets, stop_at_epoch_end)
     losses, n_groups, physical, driver = _device_step(packed, active, datasets,
-                                                      preprocess_spec, cache)
+                                                      preprocess_spec, cache,
+                                                      stop_at_epoch_end)
     packed.last_step_stats = {"physical_inputs": physical, "groups": n_groups,
                               "driver_batch": driver}
     return losses
