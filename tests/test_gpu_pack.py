@@ -515,3 +515,19 @@ def test_streamed_inputs_match_resident_bitwise():
     for a, b in zip(out["resident"][1], out["stream"][1]):
         np.testing.assert_array_equal(a, b)
     assert out["resident"][2:] == out["stream"][2:]
+
+
+def test_costmodel_calibrates_on_device():
+    """§8f-4: Eqs. 1-2 fitted to packed steps timed on this GPU; packing K
+    same-batch members must be predicted (and measured) cheaper than K
+    sequential steps."""
+    from paper_2002_02885_b200 import costmodel as cm
+    dev, model = cm.calibrate(input_dim=64, hidden=(16,), classes=4, batches=(20, 40),
+                              kinds=("sgd",), pack_sizes=(2, 4), steps=10)
+    assert dev.fixed_step_overhead_ms > 0
+    assert all(v > 0 for v in model.compute_ms_per_sample.values())
+    r = cm.estimate_step_time([(model, "sgd", 40)] * 4, dev, [[0, 1, 2, 3]])
+    assert r.impv > 0
+    metric = cm.make_traintime_metric(model, dev)
+    space = tuner.ConfigSpace()
+    assert metric(space.config(0), space.config(1)) >= 0

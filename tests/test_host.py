@@ -235,3 +235,40 @@ def test_preprocess_memo_matches_per_sample_path():
     assert c1.entries.keys() == c2.entries.keys()
     for k in c1.entries:
         np.testing.assert_array_equal(c1.entries[k], c2.entries[k])
+
+
+def test_costmodel_fit_recovers_known_coefficients_and_metric():
+    """§8f-4: the Eq. 1-2 fit recovers t_fix / io / c_kind / κ from exact
+    synthetic measurements, and the traintime metric follows tuner.py:118-127."""
+    from paper_2002_02885_b200 import costmodel as cm
+    true_dev = cm.DeviceProfile(1 << 30, 0.02, 1e-4, 0.0, 0.6)
+    true_model = cm.ModelProfile("m", 0, 0, {"sgd": 2e-4, "adam": 5e-4, "momentum": 3e-4,
+                                             "adagrad": 3e-4})
+
+    def fake(hs, dsets, n):
+        specs = [(h.optimizer.kind, h.batch_size) for h in hs]
+        r = cm.estimate_step_time([(true_model, k, b) for k, b in specs], true_dev,
+                                  [list(range(len(specs)))])
+        return r.t_s_pack_ms if len(specs) > 1 else r.t_s_seq_ms
+
+    samples = []
+    for k in ("sgd", "adam"):
+        for b in (20, 45, 70):
+            samples.append((fake([_h("x", batch=b, opt=k)], None, 0), [(k, b)], 1))
+        for n in (2, 4, 8):
+            specs = [(k, 45)] * n
+            hs = [_h(f"x{i}", batch=45, opt=k) for i in range(n)]
+            samples.append((fake(hs, None, 0), specs, 1))
+    dev, model = cm.fit(samples, 1 << 30)
+    assert abs(dev.fixed_step_overhead_ms - 0.02) < 1e-6
+    assert abs(dev.contention_factor - 0.6) < 1e-3
+    for k in ("sgd", "adam"):
+        assert abs(model.compute_ms_per_sample[k] - true_model.compute_ms_per_sample[k]) < 1e-6
+    metric = cm.make_traintime_metric(model, dev)
+    space = tuner.ConfigSpace()
+    a, b = space.config(0), space.config(4)
+    assert metric(a, b) == metric(b, a) and metric(a, b) > 0
+    # usable as the kNN distance of the reference driver
+    r = tuner.packed_hyperband(9, 3, tuner.StubExecutor(lambda c, e: c.config_id), seed=0,
+                               strategy="knn", metric=metric, threshold=0.5)
+    assert r.total_epochs > 0
