@@ -131,6 +131,7 @@ struct PhaseArgs {
   unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
   int32_t cs;          // cluster size of this launch (k_m1t_fwd: input splits)
   int32_t stages;      // k_m1t_bwd: input-tile stages in flight
+  int32_t gsize;       // k_m1t_bwd: input tiles per group (G)
   // > 0: the step header and the first `nin` feeds travel inline in the kernel
   // parameters (the train graph's kernel nodes are re-parameterised per step:
   // no descriptor copy, feed reads hit the constant bank)
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const __grid_constant__ Phase
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
     __syncthreads();
-    if (f.take != 0) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages);
+    if (f.take != 0) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages, P.gsize);
   } else {
     __trap();
   }

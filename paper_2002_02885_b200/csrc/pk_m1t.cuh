@@ -45,7 +45,8 @@ constexpr int T_BWLD = T_BU + 4;  // bwd: W0-tile row stride (144 B: LDS.128 by 
 constexpr int T_LB = 32;      // member-local partial-logit block (units)
 constexpr int T_MAXC = 32;    // classes on this path
 constexpr int T_MAXR = 128;   // rows on this path
-constexpr int T_MAXCS = 16;   // max cluster size (non-portable) → D <= 1024
+constexpr int T_MAXCS = 16;
+__host__ __device__ inline int cdiv_d(int a, int b) { return (a + b - 1) / b; }   // max cluster size (non-portable) → D <= 1024
 
 __host__ __device__ inline int t_nsplit(int D) { return (D + T_KS - 1) / T_KS; }
 __host__ __device__ inline int t_ntile(int H) { return (H + T_UM - 1) / T_UM; }
@@ -143,8 +144,7 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const float* W0 = Pc + M.w_off[0];
   const uint32_t tcols = umma::tmem_cols_pow2(RP);
   const int nu4 = (nu + 3) & ~3;
-  const int nbt = (nu + T_LB - 1) / T_LB;
-  const bool reducer = split < nbt;  // this rank reduces at least one unit block
+  const bool reducer = true;  // every rank reduces a row subset of the tile
 
   // 16-byte cp.async (LDGSTS) from every thread: W0 rows first (they do not
   // depend on the batch rows), then W1 / b0 of the tile, then the X rows
@@ -258,44 +258,44 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   umma::cluster_sync();  // all partials of the tile are in the cluster's shared memory
   PK_TRACE(3);
   if (warp == 1) umma::tmem_dealloc(tmem, tcols);
-  // ---- rank q: member-local 32-unit blocks q, q + CS, ... of this tile ------
-  float* sA = rawA;                     // [RP][T_LB] block activations
+  // ---- rank q reduces rows q, q + CS, ... (all units of the tile): every CTA
+  //      of the cluster shares the epilogue ----------------------------------
+  float* sA = rawA;  // [my rows][T_UM] activations (rawA + rawX are free now)
+  const int nr = R > split ? (R - split + CS - 1) / CS : 0;
   int bad = INT_MAX;
-  for (int bl = split; bl < nbt; bl += CS) {
-    const int ub = bl * T_LB;
-    for (int e = tid; e < RP * T_LB; e += NT) {
-      const int r = e / T_LB, j = e % T_LB, u = ub + j;
-      float a = 0.f;
-      if (r < R && u < nu) {
-        float v[T_MAXCS];
-        const uint32_t la = umma::smem_u32(sP + r * T_UM + u);
+  for (int e = tid; e < nr * T_UM; e += NT) {
+    const int rl = e / T_UM, u = e % T_UM, r = split + rl * CS;
+    float a = 0.f;
+    if (u < nu) {
+      float v[T_MAXCS];
+      const uint32_t la = umma::smem_u32(sP + r * T_UM + u);
 #pragma unroll
-        for (int s = 0; s < T_MAXCS; ++s) v[s] = s < CS ? umma::dsmem_ld(la, (uint32_t)s) : 0.f;
-        float z = v[0];
+      for (int s = 0; s < T_MAXCS; ++s) v[s] = s < CS ? umma::dsmem_ld(la, (uint32_t)s) : 0.f;
+      float z = v[0];
 #pragma unroll
-        for (int s = 1; s < T_MAXCS; ++s)
-          if (s < CS) z += v[s];
-        z += sb0[u];
-        a = act_fwd(M.act, z);
-        M.Z[0][(int64_t)r * H + u0 + u] = z;
-        M.A[0][(int64_t)r * H + u0 + u] = a;
-        if (!finite(z)) bad = min(bad, 1);
-        if (!finite(a)) bad = min(bad, 2);
-      }
-      sA[e] = a;
+      for (int s = 1; s < T_MAXCS; ++s)
+        if (s < CS) z += v[s];
+      z += sb0[u];
+      a = act_fwd(M.act, z);
+      M.Z[0][(int64_t)r * H + u0 + u] = z;
+      M.A[0][(int64_t)r * H + u0 + u] = a;
+      if (!finite(z)) bad = min(bad, 1);
+      if (!finite(a)) bad = min(bad, 2);
     }
-    __syncthreads();
-    // P[blk][r][c] = Σ_{j<32} A0[r][32·blk + j] · W1[32·blk + j][c]
-    for (int e = tid; e < R * C; e += NT) {
-      const int r = e / C, c = e % C;
-      const float* a = sA + r * T_LB;
-      const float* w = sW1 + ub * C + c;  // rows u >= nu are never read: a = 0 there
-      float p = 0.f;
+    sA[e] = a;
+  }
+  __syncthreads();
+  // P[blk][r][c] = Σ_{j<32} A0[r][32·blk + j] · W1[32·blk + j][c] for my rows
+  const int nbt = (nu + T_LB - 1) / T_LB;
+  for (int e = tid; e < nbt * nr * C; e += NT) {
+    const int bl = e / (nr * C), rc = e % (nr * C), rl = rc / C, c = rc % C;
+    const int ub = bl * T_LB, r = split + rl * CS;
+    const float* a = sA + rl * T_UM + ub;
+    const float* w = sW1 + ub * C + c;  // rows u >= nu: a = 0 there
+    float p = 0.f;
 #pragma unroll 8
-      for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
-      M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
-    }
-    __syncthreads();
+    for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
+    M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
   }
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   PK_TRACE(4);
@@ -310,12 +310,33 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 // memory stages by bulk copy while the previous tile's MMA and optimizer
 // epilogue run.  Which CTA updates an element never changes its arithmetic,
 // so the grouping (chosen per pack for occupancy) keeps K-invariance.
+// A operand of the weight-gradient MMA: Xᵀ rows k (128) × K = batch rows
+// r0..r0+31, tf32 hi/lo, K-major; zero outside the valid box
+__device__ __forceinline__ void m1t_stage_xT(float* Ah, float* Al, const float* sX, int r0, int R,
+                                             int nk) {
+  for (int e = threadIdx.x; e < T_BK * 8; e += NT) {
+    const int k = e % T_BK, rq = e / T_BK;
+    float4 h, l;
+    float* hp = &h.x;
+    float* lp = &l.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + 4 * rq + j;
+      const float v = (r < R && k < nk) ? sX[r * T_BXLD + k] : 0.f;
+      umma::split3(v, hp[j], lp[j]);
+    }
+    const uint32_t o = umma::kmaj_off(k, 4 * rq, T_BK) / 4;
+    *reinterpret_cast<float4*>(Ah + o) = h;
+    *reinterpret_cast<float4*>(Al + o) = l;
+  }
+}
+
 __device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
   return (1 + ns) * T_BK * T_BWLD + RP * T_BXLD;
 }
 
 __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                             int kt0, int ng, int utile, int S) {
+                             int kt0, int ng, int utile, int S, int G) {
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows), ns = M.n_slots;
   const int u0 = utile * T_BU, nu = min(T_BU, H - u0);
@@ -387,6 +408,15 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   cp_commit();
   const int nstg = min(S, ng);
   for (int i = 0; i < nstg; ++i) issue(i);
+  const int nch = RP / 32;
+  // A = X[:, tile 0]ᵀ (hi/lo) does not depend on the forward: stage it now,
+  // overlapping k_m1t_fwd, when one 32-row chunk covers the batch
+  const bool a_ready = nch == 1;
+  if (a_ready) {
+    if (nstg == 2) cp_wait<1>(); else cp_wait<0>();
+    __syncthreads();
+    m1t_stage_xT(Ah, Al, stg + (1 + ns) * T_BK * T_BWLD, 0, R, min(T_BK, D - kt0 * T_BK));
+  }
   pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
   PK_TRACE(1);
   // ---- logits = Σ_blk partials + b1 → softmax-xent → dZ1 (in sL) ----------
@@ -474,7 +504,6 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   // ---- stream the group's input tiles: dW0 = X[:, tile]ᵀ · dZ0 on the tensor
   //      cores, optimizer epilogue straight from TMEM -------------------------
   const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
-  const int nch = RP / 32;
   uint32_t mph = 0;
   for (int i = 0; i < ng; ++i) {
     const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
@@ -485,21 +514,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     // (slot 12/13 hold clock64 around the xent for a clock-rate check)
     for (int ch = 0; ch < nch; ++ch) {
       const int r0 = ch * 32;
-      for (int e = tid; e < T_BK * 8; e += NT) {  // A = Xᵀ: rows k, K = rows r
-        const int k = e % T_BK, rq = e / T_BK;
-        float4 h, l;
-        float* hp = &h.x;
-        float* lp = &l.x;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = r0 + 4 * rq + j;
-          const float v = (r < R && k < nk) ? sX[r * T_BXLD + k] : 0.f;
-          umma::split3(v, hp[j], lp[j]);
-        }
-        const uint32_t o = umma::kmaj_off(k, 4 * rq, T_BK) / 4;
-        *reinterpret_cast<float4*>(Ah + o) = h;
-        *reinterpret_cast<float4*>(Al + o) = l;
-      }
+      if (!(a_ready && i == 0)) m1t_stage_xT(Ah, Al, sX, r0, R, nk);
       for (int e = tid; e < T_BU * 8; e += NT) {  // B = dZ0ᵀ: rows u, K = rows r
         const int u = e % T_BU, rq = e / T_BU;
         float4 h, l;
@@ -587,9 +602,11 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     if (i + S < ng) issue(i + S);
   }
   PK_TRACE(3);
-  // ---- input-tile 0: W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3)
-  if (kt0 == 0) {
-    for (int e = tid; e < nu * C; e += NT) {
+  // ---- W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3): element e
+  //      of the unit tile is updated by the tile's group gi ≡ e (mod ngr)
+  {
+    const int gi = kt0 / G, ngr = (cdiv_d(D, T_BK) + G - 1) / G;
+    for (int e = gi + ngr * tid; e < nu * C; e += ngr * NT) {
       const int j = e / C, c = e % C;
       float g = 0.f;
       for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * (T_MAXC + 1) + c], g);
@@ -604,7 +621,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       if (ns >= 2) Sn[NP + i] = s1;
     }
     if (utile == 0) {
-      for (int c = tid; c < C; c += NT) {
+      for (int c = gi + ngr * tid; c < C; c += ngr * NT) {
         float g = 0.f;
         for (int r = 0; r < R; ++r) g += sL[r * (T_MAXC + 1) + c];
         if (fault == 1) g = NAN;
@@ -617,7 +634,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
         if (ns >= 2) Sn[NP + i] = s1;
       }
     }
-    for (int j = tid; j < nu; j += NT) {
+    for (int j = gi + ngr * tid; j < nu; j += ngr * NT) {
       float g = 0.f;
       for (int r = 0; r < R; ++r) g += sdZ[r * T_BU + j];
       if (fault == 3) g = NAN;

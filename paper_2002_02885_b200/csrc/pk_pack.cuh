@@ -26,6 +26,7 @@ struct Phase {
   int layer = -1;          // dominant layer (reporting)
   int cs = 1;              // thread-block cluster size (k_m1t_fwd)
   int stages = 1;          // k_m1t_bwd input-tile stages
+  int gsize = 1;           // k_m1t_bwd input tiles per group
 };
 
 struct pk_pack {
@@ -300,6 +301,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
       tb.stages = 1;
   }
   const int G = std::max(1, std::min(n_kt, cdiv(n_ut * n_kt, 148)));
+  tb.gsize = G;
   for (int k = 0; k < p->K; ++k) {
     const pk_member* m = p->members[k];
     if (!eval && m->m1t) {
@@ -414,6 +416,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.numAttrs = 1;
     a.cs = ph.cs;
     a.stages = ph.stages;
+    a.gsize = ph.gsize;
     if (hin) {  // inline descriptor (feeds staged in p->h_feeds by the caller)
       a.nin = p->K;
       a.hdr_in = *hin;
