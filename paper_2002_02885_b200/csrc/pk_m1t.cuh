@@ -310,6 +310,60 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 // memory stages by bulk copy while the previous tile's MMA and optimizer
 // epilogue run.  Which CTA updates an element never changes its arithmetic,
 // so the grouping (chosen per pack for occupancy) keeps K-invariance.
+// the member's optimizer on four elements: one switch, four lanes per case
+// (engine.py:302-324, same arithmetic as opt_step)
+__device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1, float bc2,
+                                       float4& w, float4& s0, float4& s1, float4 g) {
+  float* W = &w.x;
+  float* S0 = &s0.x;
+  float* S1 = &s1.x;
+  const float* Gp = &g.x;
+  switch (opt) {
+    case PK_OPT_SGD:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float gi = Gp[i];
+        if (wd != 0.f) gi = gi + wd * W[i];
+        W[i] = W[i] - lr * gi;
+      }
+      break;
+    case PK_OPT_MOMENTUM:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float gi = Gp[i];
+        if (wd != 0.f) gi = gi + wd * W[i];
+        S0[i] = S0[i] * 0.9f + gi;
+        W[i] = W[i] - lr * S0[i];
+      }
+      break;
+    case PK_OPT_ADAGRAD:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float gi = Gp[i];
+        if (wd != 0.f) gi = gi + wd * W[i];
+        S0[i] = S0[i] + gi * gi;
+        W[i] = W[i] - lr * gi / (sqrtf(S0[i]) + 1e-10f);
+      }
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float gi = Gp[i];
+        if (wd != 0.f) gi = gi + wd * W[i];
+        S0[i] = S0[i] * 0.9f + (1.f - 0.9f) * gi;
+        S1[i] = S1[i] * 0.999f + (1.f - 0.999f) * gi * gi;
+        W[i] = W[i] - lr * (S0[i] / bc1) / (sqrtf(S1[i] / bc2) + 1e-8f);
+      }
+      break;
+  }
+}
+
+// scalar form for the small W1 / b0 / b1 updates (one out-of-line copy)
+__device__ __forceinline__ void opt_step1(int opt, float lr, float wd, float bc1, float bc2,
+                                       float& w, float& s0, float& s1, float g) {
+  opt_step(opt, lr, wd, bc1, bc2, w, s0, s1, g);
+}
+
 // A operand of the weight-gradient MMA: Xᵀ rows k (128) × K = batch rows
 // r0..r0+31, tf32 hi/lo, K-major; zero outside the valid box
 __device__ __forceinline__ void m1t_stage_xT(float* Ah, float* Al, const float* sX, int r0, int R,
@@ -481,17 +535,23 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       ar[i] = ok ? M.A[0][g] : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = tid + i * NT, r = e / T_BU, j = e % T_BU;
-      if (e >= RP * T_BU) break;
+    for (int i = 0; i < PER; ++i) {  // park Z0 / A0 in shared memory (own elements)
+      const int e = tid + i * NT;
+      if (e < RP * T_BU) {
+        sdZ[e] = zr[i];
+        sA0[e] = ar[i];
+      }
+    }
+#pragma unroll 1
+    for (int e = tid; e < RP * T_BU; e += NT) {  // one rolled body, one act' switch
+      const int r = e / T_BU, j = e % T_BU;
       float v = 0.f;
       if (r < R && j < nu) {
         float s = 0.f;
         for (int c = 0; c < C; ++c) s = fmaf(sL[r * (T_MAXC + 1) + c], sW1[j * C + c], s);
-        v = act_bwd(M.act, zr[i], ar[i], s);
+        v = act_bwd(M.act, sdZ[e], sA0[e], s);
       }
       sdZ[e] = v;
-      sA0[e] = ar[i];
     }
   }
   __syncthreads();
@@ -552,46 +612,33 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     {
       const int q = warp & 3, half = warp >> 2;
       const int k = 32 * q + lane;
+#pragma unroll 1
       for (int c8 = 0; c8 < 2; ++c8) {
         const int uc = half * 16 + c8 * 8;
         float g[8];
         umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)uc, g);
         umma::tmem_wait_ld();
         if (k >= nk || uc >= nu) continue;
-        float w[8], s0[8], s1[8];
-        {
-          const float* row = sW + k * T_BWLD + uc;  // 2 x LDS.128 per tensor
-          *reinterpret_cast<float4*>(w) = *reinterpret_cast<const float4*>(row);
-          *reinterpret_cast<float4*>(w + 4) = *reinterpret_cast<const float4*>(row + 4);
-          if (ns >= 1) {
-            *reinterpret_cast<float4*>(s0) = *reinterpret_cast<const float4*>(row + T_BK * T_BWLD);
-            *reinterpret_cast<float4*>(s0 + 4) = *reinterpret_cast<const float4*>(row + T_BK * T_BWLD + 4);
-          }
-          if (ns >= 2) {
-            *reinterpret_cast<float4*>(s1) = *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD);
-            *reinterpret_cast<float4*>(s1 + 4) = *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD + 4);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float gj = g[j];
-          if (fault == 2) gj = NAN;
-          badW0 |= !finite(gj);
-          opt_step(M.opt, lr, wd, bc1, bc2, w[j], s0[j], s1[j], gj);
-        }
         const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + uc;
-        // nu % 4 == 0 (H % 4 == 0): quads are all-valid or all-out
-#pragma unroll
+        const float* row = sW + k * T_BWLD + uc;  // LDS.128 per tensor and quad
+        // one rolled quad loop and one optimizer body (opt_step4): a small
+        // epilogue keeps this kernel inside the SM instruction cache
+        // (nu % 4 == 0: quads are all-valid or all-out)
+#pragma unroll 1
         for (int qd = 0; qd < 2; ++qd) {
           if (uc + 4 * qd >= nu) break;
-          *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) =
-              make_float4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
-          if (ns >= 1)
-            *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) =
-                make_float4(s0[4 * qd], s0[4 * qd + 1], s0[4 * qd + 2], s0[4 * qd + 3]);
-          if (ns >= 2)
-            *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) =
-                make_float4(s1[4 * qd], s1[4 * qd + 1], s1[4 * qd + 2], s1[4 * qd + 3]);
+          float4 gq = qd ? make_float4(g[4], g[5], g[6], g[7]) : make_float4(g[0], g[1], g[2], g[3]);
+          if (fault == 2) gq = make_float4(NAN, NAN, NAN, NAN);
+          badW0 |= !finite(gq.x) | !finite(gq.y) | !finite(gq.z) | !finite(gq.w);
+          float4 w = *reinterpret_cast<const float4*>(row + 4 * qd);
+          float4 s0 = ns >= 1 ? *reinterpret_cast<const float4*>(row + T_BK * T_BWLD + 4 * qd)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 s1 = ns >= 2 ? *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD + 4 * qd)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          opt_step4(M.opt, lr, wd, bc1, bc2, w, s0, s1, gq);
+          *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) = w;
+          if (ns >= 1) *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) = s0;
+          if (ns >= 2) *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) = s1;
         }
       }
     }
@@ -614,7 +661,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       badW1 |= !finite(g);
       float w = sW1[e], s0 = ns >= 1 ? sW1[T_BU * C + e] : 0.f,
             s1 = ns >= 2 ? sW1[2 * T_BU * C + e] : 0.f;
-      opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+      opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
       const int64_t i = M.w_off[1] + (int64_t)u0 * C + e;
       Pn[i] = w;
       if (ns >= 1) Sn[i] = s0;
@@ -628,7 +675,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
         badb1 |= !finite(g);
         const int64_t i = M.b_off[1] + c;
         float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
-        opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+        opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
         Pn[i] = w;
         if (ns >= 1) Sn[i] = s0;
         if (ns >= 2) Sn[NP + i] = s1;
@@ -641,7 +688,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       badb0 |= !finite(g);
       const int64_t i = M.b_off[0] + u0 + j;
       float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
-      opt_step(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+      opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
       Pn[i] = w;
       if (ns >= 1) Sn[i] = s0;
       if (ns >= 2) Sn[NP + i] = s1;
