@@ -138,6 +138,10 @@ struct PhaseArgs {
   int32_t nin;
   StepHdr hdr_in;
   FeedDev<T> feeds_in[kInlineFeeds];
+  // finalize fast path (K <= kInlineFeeds, every member on the tensor path):
+  // the members' control blocks, inline
+  int32_t all_tensor;
+  MemberCtl* ctl_in[kInlineFeeds];
 };
 
 template <typename T>
@@ -807,6 +811,60 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
 // order (thread-strided, fixed tree); commit rules of packing.py:246-253: a
 // forward non-finite value aborts the step, else members commit in pack
 // order until the first one with a non-finite gradient.
+// FINALIZE for packs whose members all take the tensor path (two affine
+// layers; loss and next Adam corrections already in ctl): one warp, lane =
+// member, the same commit rules via ballots.
+template <typename T>
+__device__ __noinline__ void finalize_fast(const PhaseArgs<T>& P) {
+  if (threadIdx.x >= 32) return;
+  const int K = P.K, k = threadIdx.x;
+  MemberCtl* c = k < K ? P.ctl_in[k] : nullptr;
+  const bool act = k < K && feed_of(P, k).take != 0;
+  int bn = INT_MAX, bg = INT_MAX;
+  double loss = 0.0;
+  if (act) {
+    bn = c->bad_node;
+    bg = c->bad_grad;
+    loss = c->loss;
+    if (!isfinite(loss)) bn = min(bn, 4);  // node 2·n_layers = the loss node
+  }
+  int code = PK_OK, who = -1, idx = -1, stop = K;
+  const unsigned mv = __ballot_sync(0xffffffffu, bn != INT_MAX);
+  if (mv) {
+    who = __ffs(mv) - 1;
+    idx = __shfl_sync(0xffffffffu, bn, who);
+    code = PK_ERR_NONFINITE_VALUE;
+    stop = 0;
+  } else {
+    const unsigned mg = __ballot_sync(0xffffffffu, bg != INT_MAX);
+    if (mg) {
+      who = __ffs(mg) - 1;
+      idx = __shfl_sync(0xffffffffu, bg, who);
+      code = PK_ERR_NONFINITE_GRAD;
+      stop = who;
+    }
+  }
+  const bool commit = act && k < stop;
+  const int committed = __popc(__ballot_sync(0xffffffffu, commit));
+  int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)hdr_of(P).slot * P.ring_stride);
+  double* losses = reinterpret_cast<double*>(st + 4);
+  if (k < K) {
+    losses[k] = act ? loss : 0.0;
+    if (commit) {
+      c->parity ^= 1;
+      c->step_counter += 1;
+      c->bc1 = c->bcn1;
+      c->bc2 = c->bcn2;
+    }
+    if (act) c->fault_grad = -1;  // one-shot
+    c->bad_node = INT_MAX;
+    c->bad_grad = INT_MAX;
+  }
+  if (k == 0) {
+    st[0] = code; st[1] = who; st[2] = idx; st[3] = committed;
+  }
+}
+
 template <typename T>
 __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   __shared__ int s_bn[PK_MAX_PACK], s_bg[PK_MAX_PACK];
@@ -937,7 +995,8 @@ __device__ __forceinline__ void kernel_end(const PhaseArgs<T>& P, bool train) {
   if (!last) return;
   __threadfence();
   PK_TRACE(6);
-  finalize<T>(P, train);
+  if (train && P.all_tensor) finalize_fast<T>(P);
+  else finalize<T>(P, train);
   PK_TRACE(7);
   if (threadIdx.x == 0) *P.done = 0;
 }

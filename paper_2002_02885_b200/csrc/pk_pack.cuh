@@ -416,6 +416,13 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.numAttrs = 1;
     a.cs = ph.cs;
     a.stages = ph.stages;
+    if (p->K <= pk::kInlineFeeds && &phases == &p->train) {
+      a.all_tensor = 1;
+      for (int k = 0; k < p->K; ++k) {
+        a.ctl_in[k] = p->members[k]->ctl;
+        a.all_tensor &= p->members[k]->m1t ? 1 : 0;
+      }
+    }
     a.gsize = ph.gsize;
     if (hin) {  // inline descriptor (feeds staged in p->h_feeds by the caller)
       a.nin = p->K;
