@@ -54,12 +54,12 @@ __host__ __device__ inline int t_nblk(int H) { return (H + T_LB - 1) / T_LB; }
 
 struct M1T {
   // shared-memory bytes (fp32) for a member with rows padded to RP
-  __host__ __device__ static int fwd_smem(int RP) {
+  __host__ __device__ static int fwd_smem(int RP, int C) {
     return T_KS * T_UM * 4              // raw W0 rows [k][unit]
            + RP * T_XLD * 4            // raw X rows
            + 2 * T_UM * T_KS * 4       // A hi/lo
            + 2 * RP * T_KS * 4         // B hi/lo
-           + T_UM * T_MAXC * 4 + T_UM * 4  // W1 rows, b0 slice of the tile
+           + T_UM * C * 4 + T_UM * 4   // W1 rows, b0 slice of the tile
            + RP * 4 + 64;              // row index, barriers
     // (the partial [RP][T_UM] reuses the A hi/lo region after the MMA)
   }
@@ -68,7 +68,7 @@ struct M1T {
     return S * ((1 + ns) * T_BK * T_BWLD * 4 + RP * T_BXLD * 4)  // W0 tile + slots, X columns
            + 2 * T_BK * 32 * 4         // A hi/lo (one 32-row chunk)
            + 2 * T_BU * 32 * 4         // B hi/lo
-           + RP * (T_MAXC + 1) * 4     // logits → dZ1
+           + RP * (C + 1) * 4          // logits → dZ1 (row stride C + 1)
            + 2 * RP * T_BU * 4         // dZ0 tile, A0 tile
            + (1 + ns) * T_BU * C * 4   // W1 rows + slots
            + T_MAXC * 4                // b1
@@ -135,7 +135,7 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* Bh = Al + T_UM * T_KS;                   // K-major [T_KS/4][RP][4]
   float* Bl = Bh + RP * T_KS;
   float* sW1 = Bl + RP * T_KS;                    // [T_UM][C] W1 rows of the tile
-  float* sb0 = sW1 + T_UM * T_MAXC;               // [T_UM] b0 slice
+  float* sb0 = sW1 + T_UM * C;                    // [T_UM] b0 slice
   int32_t* srow = reinterpret_cast<int32_t*>(sb0 + T_UM);
   uint64_t* bar = reinterpret_cast<uint64_t*>(srow + RP);  // [2] (RP even)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
@@ -410,7 +410,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* Bh = Al + T_BK * 32;                           // K-major [8][T_BU][4]
   float* Bl = Bh + T_BU * 32;
   float* sL = Bl + T_BU * 32;                           // [RP][T_MAXC+1]
-  float* sdZ = sL + RP * (T_MAXC + 1);                  // [RP][T_BU]
+  const int LDL = C + 1;                                // sL row stride
+  float* sdZ = sL + RP * LDL;                           // [RP][T_BU]
   float* sA0 = sdZ + RP * T_BU;                         // [RP][T_BU] A0 tile
   float* sW1 = sA0 + RP * T_BU;                         // [1+ns][T_BU][C]
   float* sb1 = sW1 + (1 + ns) * T_BU * C;               // [T_MAXC]
@@ -492,7 +493,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     }
     const int r = e / C;
     z += sb1[c];
-    sL[r * (T_MAXC + 1) + c] = z;
+    sL[r * LDL + c] = z;
     if (!finite(z)) bad = 3;
   }
   if (owner && bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
@@ -501,7 +502,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   if (tid == 0 && pk_trace_slots) pk_trace_slots[12] = clock64();
   for (int r0 = 0; r0 < R; r0 += NT / 8) {  // 8 lanes per row, every warp busy
     const int r = r0 + (tid >> 3);
-    xent_row8(sL + min(r, R - 1) * (T_MAXC + 1), C, ylab[min(r, R - 1)], R, r < R,
+    xent_row8(sL + min(r, R - 1) * LDL, C, ylab[min(r, R - 1)], R, r < R,
               owner && r < R ? M.rowloss + r : nullptr);
   }
   if (tid == 0 && pk_trace_slots) pk_trace_slots[13] = clock64();
@@ -548,7 +549,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       float v = 0.f;
       if (r < R && j < nu) {
         float s = 0.f;
-        for (int c = 0; c < C; ++c) s = fmaf(sL[r * (T_MAXC + 1) + c], sW1[j * C + c], s);
+        for (int c = 0; c < C; ++c) s = fmaf(sL[r * LDL + c], sW1[j * C + c], s);
         v = act_bwd(M.act, sdZ[e], sA0[e], s);
       }
       sdZ[e] = v;
@@ -656,7 +657,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     for (int e = gi + ngr * tid; e < nu * C; e += ngr * NT) {
       const int j = e / C, c = e % C;
       float g = 0.f;
-      for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * (T_MAXC + 1) + c], g);
+      for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * LDL + c], g);
       if (fault == 0) g = NAN;
       badW1 |= !finite(g);
       float w = sW1[e], s0 = ns >= 1 ? sW1[T_BU * C + e] : 0.f,
@@ -670,7 +671,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     if (utile == 0) {
       for (int c = gi + ngr * tid; c < C; c += ngr * NT) {
         float g = 0.f;
-        for (int r = 0; r < R; ++r) g += sL[r * (T_MAXC + 1) + c];
+        for (int r = 0; r < R; ++r) g += sL[r * LDL + c];
         if (fault == 1) g = NAN;
         badb1 |= !finite(g);
         const int64_t i = M.b_off[1] + c;

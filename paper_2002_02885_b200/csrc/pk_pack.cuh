@@ -186,7 +186,7 @@ static bool m1t_eligible(const pk_member_desc& d, int dtype, int device) {
   const int budget = optin - kStaticSmemMargin;
   const int RP = pk::m1_rows_pad(d.max_rows);
   const int ns = d.optimizer == PK_OPT_SGD ? 0 : (d.optimizer == PK_OPT_ADAM ? 2 : 1);
-  return pk::M1T::fwd_smem(RP) <= budget && pk::M1T::bwd_smem(RP, C, ns, 1) <= budget;
+  return pk::M1T::fwd_smem(RP, C) <= budget && pk::M1T::bwd_smem(RP, C, ns, 1) <= budget;
 }
 
 // whether the member's last layer + head + first dgrad fit one TAIL tile
@@ -313,7 +313,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
       for (int ut = 0; ut < cdiv(H, pk::T_BU); ++ut)
         for (int kt = 0; kt < nkt; kt += G)
           tb.host.push_back(Tile{k, (int16_t)std::min(G, nkt - kt), pk::TK_WGRAD, kt, ut});
-      tf.smem = std::max(tf.smem, pk::M1T::fwd_smem(RP));
+      tf.smem = std::max(tf.smem, pk::M1T::fwd_smem(RP, C));
       tb.smem = std::max(tb.smem, pk::M1T::bwd_smem(RP, C, m->n_slots, tb.stages));
       continue;
     }

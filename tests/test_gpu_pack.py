@@ -531,3 +531,51 @@ def test_costmodel_calibrates_on_device():
     metric = cm.make_traintime_metric(model, dev)
     space = tuner.ConfigSpace()
     assert metric(space.config(0), space.config(1)) >= 0
+
+
+# ------------------------------------------- tcgen05 path: schedule shapes --
+
+def test_tensor_path_grouped_input_tiles_lockstep():
+    """8 wide members (mixed optimizers) on the tcgen05 path: the backward
+    groups several 128-input tiles per CTA (G > 1) with two cp.async stages;
+    one-step parity with the f64 oracle and packed == standalone bitwise."""
+    from paper_2002_02885_b200 import device
+    ds = {"t": data.synth_dataset(3000, 784, 10, seed=7, spread=0.5)}
+    arch = packing.MLPArch(784, (256,), 10, "tanh")
+    opts = ("sgd", "adam", "momentum", "adagrad")
+    hs = [packing.make_handle(f"g{i}", arch, opts[i % 4], 0.01 / (1 + i), 32, 50, "t", i)
+          for i in range(8)]
+    assert all(device.uses_m1t(arch, h.optimizer.kind, 32) for h in hs)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 2, packing=packing)
+    solo = packing.make_handle("g5", arch, opts[5 % 4], 0.01 / 6, 32, 50, "t", 5)
+    for _ in range(2):
+        packing.standalone_step(solo, ds)
+    assert _maxdiff(hs[5], solo) == 0.0
+
+
+def test_tensor_path_batch_128_rows_lockstep():
+    """RP = 128 rows (batch 100): four 32-row K chunks per backward tile and
+    one input-tile stage; parity with the oracle."""
+    from paper_2002_02885_b200 import device
+    ds = {"t": data.synth_dataset(1000, 200, 7, seed=8, spread=0.5)}
+    arch = packing.MLPArch(200, (36,), 7, "sigmoid")
+    hs = [packing.make_handle("r0", arch, "adagrad", 0.01, 100, 20, "t", 1),
+          packing.make_handle("r1", arch, "momentum", 0.05, 100, 20, "t", 2)]
+    assert all(device.uses_m1t(arch, h.optimizer.kind, 100) for h in hs)
+    lockstep(packing.dedup_inputs(packing.pack_models(hs)), ds, 3, packing=packing)
+
+
+def test_pack_beyond_inline_descriptors():
+    """K = 40 > 32: step descriptors go through the H2D copy and finalize
+    takes its general path; still parity and K-invariance."""
+    ds = {"t": data.synth_dataset(400, 12, 4, seed=9)}
+    arch = packing.MLPArch(12, (8,), 4, "relu")
+    hs = [packing.make_handle(f"w{i}", arch, ("sgd", "adam")[i % 2], 0.02, 16, 10, "t", i)
+          for i in range(40)]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 2, packing=packing)
+    solo = packing.make_handle("w7", arch, "adam", 0.02, 16, 10, "t", 7)
+    for _ in range(2):
+        packing.standalone_step(solo, ds)
+    assert _maxdiff(hs[7], solo) == 0.0
