@@ -44,6 +44,11 @@ WORKLOADS = {
     # BASELINE.json configs[0]: the reference-runnable, parity-pinned config
     "config0": dict(n=10000, dim=784, classes=10, hidden=(256,), act="relu", batch=32,
                     members=[("sgd", 0.1), ("sgd", 0.01)]),
+    # a wider sweep: 16 members 784-1024-10 at batch 128 (mixed optimizers),
+    # 52 MB of fp32 parameters + slots streamed per step: the HBM-bound regime
+    "wide16": dict(n=10000, dim=784, classes=10, hidden=(1024,), act="relu", batch=128,
+                   members=[(("sgd", "adam", "momentum", "adagrad")[i % 4], 10.0 ** -(1 + i % 4))
+                            for i in range(16)]),
     # same member shape, a 16-member hyperparameter sweep (SGD/Adam/Momentum/Adagrad)
     "k16": dict(n=10000, dim=784, classes=10, hidden=(256,), act="relu", batch=32,
                 members=[(("sgd", "adam", "momentum", "adagrad")[i % 4], 10.0 ** -(1 + i % 4))
