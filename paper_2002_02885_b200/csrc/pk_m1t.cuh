@@ -303,6 +303,222 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   umma::cluster_wait();            // no memory ordering needed, just the rendezvous
 }
 
+// ------------------------------------------------ streaming forward --
+// For packs whose split-K clusters would need several waves: one CTA per
+// (member, 128-unit tile) walks the whole input dimension.  Raw 32-deep
+// chunks of W0 rows and X rows stream through an S-stage cp.async ring and
+// are split into tf32 hi/lo (double-buffered) while the tensor core works on
+// the previous chunk.  The arithmetic is the cluster forward's exactly: input
+// split s (64 deep = chunks 2s, 2s+1) accumulates alone in TMEM buffer s & 1
+// with the same MMA sequence, and its partial is read out and added into
+// running registers in split order (z = p0 + p1 + ... + b0) while split s+1
+// multiplies — so a member's result does not depend on which forward variant
+// its pack size selected (packed == standalone stays bit-exact).
+constexpr int T_SC = 32;              // input dims per streamed chunk
+constexpr int T_SXLD = T_SC + 4;      // raw X chunk row stride (16B rows, conflict-free)
+
+__host__ __device__ inline int m1s_raw_stages(int RP) { return RP >= 128 ? 2 : 4; }
+__host__ __device__ inline int m1s_fwd_smem(int RP, int C) {
+  const int S = m1s_raw_stages(RP);
+  return S * (T_SC * T_UM + RP * T_SXLD) * 4   // raw W0 / X chunks
+         + 2 * 2 * (T_UM + RP) * T_SC * 4      // hi/lo A and B, double-buffered
+         + T_UM * C * 4 + T_UM * 4             // W1 rows, b0 slice
+         + RP * 4 + 64;                        // row index, barriers
+}
+
+__device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
+                             int tile) {
+  const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
+  const int R = f.take, RP = m1_rows_pad(M.max_rows), S = m1s_raw_stages(RP);
+  const int u0 = tile * T_UM, nu = min(T_UM, H - u0), nu4 = (nu + 3) & ~3;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int RSF = T_SC * T_UM + RP * T_SXLD;        // floats per raw stage
+  float* raw = reinterpret_cast<float*>(sm);        // [S][rawA chunk, rawX chunk]
+  float* hl = raw + S * RSF;                        // [2][Ah, Al, Bh, Bl]
+  const int HLF = 2 * (T_UM + RP) * T_SC;            // floats per hi/lo buffer
+  float* sW1 = hl + 2 * HLF;
+  float* sb0 = sW1 + T_UM * C;
+  int32_t* srow = reinterpret_cast<int32_t*>(sb0 + T_UM);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(srow + RP);  // [0,1] hi/lo free, [2,3] split done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
+  const uint32_t tcols = umma::tmem_cols_pow2(2 * RP);
+  const int nch = (D + T_SC - 1) / T_SC, nsplit = t_nsplit(D);
+
+  for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
+  if (tid == 32) {
+    for (int i = 0; i < 4; ++i) umma::mbar_init(&bar[i], 1);
+    umma::mbar_fence_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tslot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  auto issue = [&](int c) {  // raw chunk c into stage c % S (one commit group)
+    float* rA = raw + (c % S) * RSF;
+    float* rX = rA + T_SC * T_UM;
+    const int k0 = c * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
+    for (int e = tid; e < nk * cpr; e += NT) {
+      const int k = e / cpr, q = e % cpr;
+      cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
+    }
+    const int cx = nk / 4;
+    for (int e = tid; e < R * cx; e += NT) {
+      const int r = e / cx, q = e % cx;
+      cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
+    }
+    cp_commit();
+  };
+  // W1 / b0 of the tile ride in the first commit group
+  for (int e = tid; e < nu4 * C / 4; e += NT)
+    cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
+  for (int e = tid; e < nu4 / 4; e += NT) cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
+  for (int c = 0; c < S - 1; ++c) {
+    if (c < nch) issue(c);
+    else cp_commit();
+  }
+  PK_TRACE(1);
+  const uint32_t idesc = umma::idesc_tf32(T_UM, RP, false, false);
+  // running split sums: warp w owns TMEM lane quarter w % 4 (units) and row
+  // half w / 4; RP/2 <= 64 rows per thread
+  const int q = warp & 3, half = warp >> 2, uu = 32 * q + lane;
+  const int rlo = half * (RP / 2);
+  float z[64];
+  bool badx = false;
+  uint32_t ph[4] = {0u, 0u, 0u, 0u};
+  auto readout = [&](int sp) {  // add split sp's partial (buffer sp & 1) into z
+    const int ab = sp & 1;
+    umma::mbar_wait(&bar[2 + ab], ph[2 + ab]);
+    ph[2 + ab] ^= 1u;
+    umma::fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      if (c0 >= RP / 2) break;
+      float v[8];
+      umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(ab * RP + rlo + c0), v);
+      umma::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z[c0 + i] = sp == 0 ? v[i] : z[c0 + i] + v[i];
+    }
+    umma::fence_before();
+  };
+  for (int c = 0; c < nch; ++c) {
+    if (c + S - 1 < nch) issue(c + S - 1);
+    else cp_commit();
+    // chunk c landed: the S - 1 newer groups (chunks c+1 .. c+S-1) may fly
+    if (S == 4) cp_wait<3>(); else cp_wait<1>();
+    __syncthreads();
+    const int b = c & 1, sp = c >> 1;
+    float* Ah = hl + b * HLF;
+    float* Al = Ah + T_UM * T_SC;
+    float* Bh = Al + T_UM * T_SC;
+    float* Bl = Bh + RP * T_SC;
+    if (c >= 2) {  // hi/lo buffer b was read by the MMAs of chunk c - 2
+      umma::mbar_wait(&bar[b], ph[b]);
+      ph[b] ^= 1u;
+      umma::fence_after();
+    }
+    const float* rA = raw + (c % S) * RSF;
+    const float* rX = rA + T_SC * T_UM;
+    const int nk = min(T_SC, D - c * T_SC);
+    for (int e = tid; e < T_UM * (T_SC / 4); e += NT) {
+      const int u = e % T_UM, kq = e / T_UM;
+      float4 h, l;
+      float* hp = &h.x;
+      float* lp = &l.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = 4 * kq + j;
+        const float v = (u < nu && k < nk) ? rA[k * T_UM + u] : 0.f;
+        umma::split3(v, hp[j], lp[j]);
+      }
+      const uint32_t o = umma::kmaj_off(u, 4 * kq, T_UM) / 4;
+      *reinterpret_cast<float4*>(Ah + o) = h;
+      *reinterpret_cast<float4*>(Al + o) = l;
+    }
+    for (int e = tid; e < RP * (T_SC / 4); e += NT) {
+      const int r = e % RP, kq = e / RP;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < R && 4 * kq < nk) v = *reinterpret_cast<const float4*>(rX + r * T_SXLD + 4 * kq);
+      badx |= !finite(v.x) | !finite(v.y) | !finite(v.z) | !finite(v.w);
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      const uint32_t o = umma::kmaj_off(r, 4 * kq, RP) / 4;
+      *reinterpret_cast<float4*>(Bh + o) = h;
+      *reinterpret_cast<float4*>(Bl + o) = l;
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();  // also: raw stage c % S is free for chunk c + S
+    umma::fence_after();
+    // split sp - 2 used this accumulator buffer: its readout finished before
+    // the __syncthreads above (readout of split sp - 1 happens below)
+    if (tid == 0) {
+      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+      const uint32_t acc = tmem + (uint32_t)((sp & 1) * RP);
+      for (int s2 = 0; s2 < (nk + 7) / 8; ++s2) {
+        const uint64_t dah = umma::kmaj_desc(ah, T_UM, s2), dal = umma::kmaj_desc(al, T_UM, s2);
+        const uint64_t dbh = umma::kmaj_desc(bh, RP, s2), dbl = umma::kmaj_desc(bl, RP, s2);
+        umma::mma_tf32(acc, dah, dbh, idesc, (c & 1) || s2 > 0);
+        umma::mma_tf32(acc, dah, dbl, idesc, true);
+        umma::mma_tf32(acc, dal, dbh, idesc, true);
+      }
+      umma::commit(&bar[b]);                                  // hi/lo buffer b free
+      if ((c & 1) || c == nch - 1) umma::commit(&bar[2 + (sp & 1)]);  // split sp done
+    }
+    // read out the previous split while this one multiplies
+    if ((c & 1) && sp >= 1) readout(sp - 1);
+  }
+  cp_wait<0>();
+  if (nsplit >= 2 && (nch & 1)) readout(nsplit - 2);  // odd tail: split nsplit-2 not read yet
+  readout(nsplit - 1);
+  badx = __syncthreads_or(badx);
+  if (badx && tid == 0) flag_min(&M.ctl->bad_node, 0);
+  PK_TRACE(2);
+  // ---- epilogue: b0, activation, Z0/A0; sA[r][u] for the logits
+  float* sA = raw;  // [RP][T_UM] (raw stages are free)
+  int bad = INT_MAX;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    if (i >= RP / 2) break;
+    const int r = rlo + i;
+    float a = 0.f;
+    if (r < R && uu < nu) {
+      const float zz = z[i] + sb0[uu];
+      a = act_fwd(M.act, zz);
+      M.Z[0][(int64_t)r * H + u0 + uu] = zz;
+      M.A[0][(int64_t)r * H + u0 + uu] = a;
+      if (!finite(zz)) bad = min(bad, 1);
+      if (!finite(a)) bad = min(bad, 2);
+    }
+    sA[r * T_UM + uu] = a;
+  }
+  if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  umma::fence_before();
+  __syncthreads();
+  PK_TRACE(3);
+  if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+  // P[blk][r][c] = Σ_{j<32} A0[r][32·blk + j] · W1[32·blk + j][c]
+  const int nbt = (nu + T_LB - 1) / T_LB;
+  for (int e = tid; e < nbt * R * C; e += NT) {
+    const int bl = e / (R * C), rc = e % (R * C), r = rc / C, c = rc % C;
+    const int ub = bl * T_LB;
+    const float* a = sA + r * T_UM + ub;
+    const float* w = sW1 + ub * C + c;
+    float p = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
+    M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
+  }
+  PK_TRACE(4);
+}
+
 // ----------------------------------------------------------- backward --
 // One CTA per (member, 32-unit tile, group of `ng` consecutive 128-input
 // tiles).  The per-unit-tile work — logits, softmax-xent, dZ0 — is done once
@@ -499,13 +715,11 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   if (owner && bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   __syncthreads();
   PK_TRACE(8);
-  if (tid == 0 && pk_trace_slots) pk_trace_slots[12] = clock64();
   for (int r0 = 0; r0 < R; r0 += NT / 8) {  // 8 lanes per row, every warp busy
     const int r = r0 + (tid >> 3);
     xent_row8(sL + min(r, R - 1) * LDL, C, ylab[min(r, R - 1)], R, r < R,
               owner && r < R ? M.rowloss + r : nullptr);
   }
-  if (tid == 0 && pk_trace_slots) pk_trace_slots[13] = clock64();
   PK_TRACE(9);
   if (nstg == 2) cp_wait<2>(); else cp_wait<1>();  // W1 rows landed
   __syncthreads();
@@ -572,7 +786,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     const float* sX = sW + (1 + ns) * T_BK * T_BWLD;
     if (S == 2 && i + 1 < ng) cp_wait<1>(); else cp_wait<0>();  // input tile i landed
     __syncthreads();
-    // (slot 12/13 hold clock64 around the xent for a clock-rate check)
+    if (i == min(1, ng - 1)) PK_TRACE(12);  // tile 1 (tile 0 when ng == 1): after cp.async wait
     for (int ch = 0; ch < nch; ++ch) {
       const int r0 = ch * 32;
       if (!(a_ready && i == 0)) m1t_stage_xT(Ah, Al, sX, r0, R, nk);
@@ -591,7 +805,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       umma::fence_before();
       __syncthreads();
       umma::fence_after();
-      if (i == 0 && ch == 0) PK_TRACE(13);
+      if (i == min(1, ng - 1) && ch == 0) PK_TRACE(13);
       if (tid == 0) {
         const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
         const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
@@ -607,7 +821,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       umma::mbar_wait(&bar[3], mph);
       mph ^= 1;
       umma::fence_after();
-      if (i == 0 && ch == 0) PK_TRACE(14);
+      if (i == min(1, ng - 1) && ch == 0) PK_TRACE(14);
     }
     // epilogue: W0[k0 + k, u0 + u] update from the TMEM gradient
     {
@@ -643,7 +857,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
         }
       }
     }
-    if (i == 0) PK_TRACE(15);
+    if (i == min(1, ng - 1)) PK_TRACE(15);
     umma::fence_before();
     __syncthreads();  // stage i % S and the accumulator are free again
     umma::fence_after();

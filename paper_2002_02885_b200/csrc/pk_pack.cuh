@@ -134,6 +134,7 @@ static cudaError_t init_smem_limit(int device, int* out) {
   ks.push_back(pk::k_mlp1_bwd<T>);
   ks.push_back(pk::k_m1t_fwd<T>);
   ks.push_back(pk::k_m1t_bwd<T>);
+  ks.push_back(pk::k_m1s_fwd<T>);
   int dyn = optin;
   for (auto k : ks) {
     cudaFuncAttributes fa{};
@@ -360,6 +361,29 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     phases.insert(phases.begin(), m1f);
     phases.push_back(m1b);
   }
+  // many clusters (several waves): stream the input dimension instead, one CTA
+  // per unit tile, when every tensor member's streaming smem fits
+  if (!eval && (int)tf.host.size() > 2 * 148 && !getenv("PK_NO_STREAM_FWD")) {
+    bool fits = true;
+    int sm = 0;
+    for (int k = 0; k < p->K; ++k) {
+      const pk_member* m = p->members[k];
+      if (!m->m1t) continue;
+      const int need = pk::m1s_fwd_smem(pk::m1_rows_pad(m->desc.max_rows), m->desc.dims[2]);
+      fits &= need <= smem_budget(dt);
+      sm = std::max(sm, need);
+    }
+    if (fits) {
+      tf.host.clear();
+      for (int k = 0; k < p->K; ++k)
+        if (p->members[k]->m1t)
+          for (int t = 0; t < pk::t_ntile(p->members[k]->desc.dims[1]); ++t)
+            tf.host.push_back(Tile{k, 0, pk::TK_FWD, t, 0});
+      tf.special = 5;
+      tf.cs = 1;
+      tf.smem = sm;
+    }
+  }
   tf.ntiles = (int)tf.host.size();
   tb.ntiles = (int)tb.host.size();
   tf.kind = pk::TK_FWD;
@@ -440,6 +464,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
                           : ph.special == 2 ? pk::k_mlp1_bwd<T>
                           : ph.special == 3 ? pk::k_m1t_fwd<T>
                           : ph.special == 4 ? pk::k_m1t_bwd<T>
+                          : ph.special == 5 ? pk::k_m1s_fwd<T>
                                             : kernel_for<T>(ph.mask);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) {

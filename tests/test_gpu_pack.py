@@ -579,3 +579,22 @@ def test_pack_beyond_inline_descriptors():
     for _ in range(2):
         packing.standalone_step(solo, ds)
     assert _maxdiff(hs[7], solo) == 0.0
+
+
+def test_streaming_forward_large_pack_lockstep():
+    """12 x 784-256-10 members: the split-K clusters would take > 2 waves, so
+    the forward streams the input dimension in one CTA per unit tile
+    (k_m1s_fwd); parity with the oracle, packed == standalone bitwise."""
+    ds = {"t": data.synth_dataset(3000, 784, 10, seed=11, spread=0.5)}
+    arch = packing.MLPArch(784, (256,), 10, "leaky_relu")
+    opts = ("sgd", "momentum", "adagrad", "adam")
+    hs = [packing.make_handle(f"s{i}", arch, opts[i % 4], 0.02 / (1 + i), 32, 50, "t", i)
+          for i in range(12)]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 2, packing=packing)
+    # the one-member pack takes the split-K cluster forward; the streaming
+    # forward reproduces its arithmetic exactly → bit-identical trajectories
+    solo = packing.make_handle("s4", arch, "sgd", 0.02 / 5, 32, 50, "t", 4)
+    for _ in range(2):
+        packing.standalone_step(solo, ds)
+    assert _maxdiff(hs[4], solo) == 0.0
