@@ -410,6 +410,7 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     // chunk c landed: the S - 1 newer groups (chunks c+1 .. c+S-1) may fly
     if (S == 4) cp_wait<3>(); else cp_wait<1>();
     __syncthreads();
+    if (c == 2) PK_TRACE(8);
     const int b = c & 1, sp = c >> 1;
     float* Ah = hl + b * HLF;
     float* Al = Ah + T_UM * T_SC;
@@ -420,6 +421,7 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       ph[b] ^= 1u;
       umma::fence_after();
     }
+    if (c == 2) PK_TRACE(9);
     const float* rA = raw + (c % S) * RSF;
     const float* rX = rA + T_SC * T_UM;
     const int nk = min(T_SC, D - c * T_SC);
@@ -452,10 +454,12 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       *reinterpret_cast<float4*>(Bh + o) = h;
       *reinterpret_cast<float4*>(Bl + o) = l;
     }
+    if (c == 2) PK_TRACE(10);
     umma::fence_async_smem();
     umma::fence_before();
     __syncthreads();  // also: raw stage c % S is free for chunk c + S
     umma::fence_after();
+    if (c == 2) PK_TRACE(11);
     // split sp - 2 used this accumulator buffer: its readout finished before
     // the __syncthreads above (readout of split sp - 1 happens below)
     if (tid == 0) {
@@ -473,7 +477,9 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       if ((c & 1) || c == nch - 1) umma::commit(&bar[2 + (sp & 1)]);  // split sp done
     }
     // read out the previous split while this one multiplies
+    if (c == 2) PK_TRACE(12);
     if ((c & 1) && sp >= 1) readout(sp - 1);
+    if (c == 3) PK_TRACE(13);
   }
   cp_wait<0>();
   if (nsplit >= 2 && (nch & 1)) readout(nsplit - 2);  // odd tail: split nsplit-2 not read yet
