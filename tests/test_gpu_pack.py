@@ -598,3 +598,25 @@ def test_streaming_forward_large_pack_lockstep():
     for _ in range(2):
         packing.standalone_step(solo, ds)
     assert _maxdiff(hs[4], solo) == 0.0
+
+
+def test_tensor_path_ragged_heterogeneous_pack():
+    """Config-3-style heterogeneous pack on the tensor path: members with
+    different hidden widths, class counts, batch sizes and input datasets
+    (dimensions) share one pack — dummy cluster splits for the shallower
+    inputs, ragged unit tiles; oracle parity and K-invariance."""
+    from paper_2002_02885_b200 import device
+    ds = {"a": data.synth_dataset(800, 784, 10, seed=12, spread=0.5),
+          "b": data.synth_dataset(600, 256, 32, seed=13, spread=0.5)}
+    specs = [("h0", packing.MLPArch(784, (16,), 10, "relu"), "adam", 0.01, 20, "a"),
+             ("h1", packing.MLPArch(784, (100,), 10, "tanh"), "sgd", 0.05, 45, "a"),
+             ("h2", packing.MLPArch(256, (256,), 32, "sigmoid"), "momentum", 0.02, 64, "b"),
+             ("h3", packing.MLPArch(256, (36,), 32, "leaky_relu"), "adagrad", 0.02, 64, "b")]
+    hs = [packing.make_handle(m, a, o, lr, b, 30, d, i) for i, (m, a, o, lr, b, d) in enumerate(specs)]
+    assert all(device.uses_m1t(h.arch, h.optimizer.kind, h.batch_size) for h in hs)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 3, packing=packing)
+    solo = packing.make_handle("h2", specs[2][1], "momentum", 0.02, 64, 30, "b", 2)
+    for _ in range(3):
+        packing.standalone_step(solo, ds)
+    assert _maxdiff(hs[2], solo) == 0.0
