@@ -1080,7 +1080,12 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
     __syncthreads();
-    if (f.take != 0) m1s_fwd_tile(smem_raw, sM, f, t.m0);
+    if (f.take != 0) {
+      if (m1_rows_pad(sM.max_rows) == 32 && t_nsplit(sM.dims[0]) * 32 <= 512)
+        m1s_fwd_tile_ws(smem_raw, sM, f, t.m0);
+      else
+        m1s_fwd_tile(smem_raw, sM, f, t.m0);
+    }
   } else {
     __trap();
   }

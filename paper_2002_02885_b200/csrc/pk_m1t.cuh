@@ -525,6 +525,213 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   PK_TRACE(4);
 }
 
+// --------------------------------- warp-specialised streaming forward --
+// RP = 32 and ≤ 16 input splits: every split owns its TMEM accumulator
+// (≤ 512 columns), so nothing is read out mid-loop and the roles separate:
+//   warps 0-6 (producers): cp.async ring → wait → tf32 hi/lo split into
+//                          buffer c & 1 → mbarrier full[c & 1]
+//   warp 7, lane 0 (MMA):  wait full → 3 × K-steps tcgen05.mma into the
+//                          split's accumulator → commit empty[c & 1]
+// so staging chunk c+1 overlaps the MMAs of chunk c.  Same per-split MMA
+// sequence and split-order sum as the cluster forward (bit-identical).
+constexpr int T_WS_PRODUCERS = NT - 32;   // 224 threads
+
+__device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
+                                int tile) {
+  const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
+  const int R = f.take, RP = 32, S = 4;
+  const int u0 = tile * T_UM, nu = min(T_UM, H - u0), nu4 = (nu + 3) & ~3;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int RSF = T_SC * T_UM + RP * T_SXLD;
+  float* raw = reinterpret_cast<float*>(sm);
+  float* hl = raw + S * RSF;
+  const int HLF = 2 * (T_UM + RP) * T_SC;
+  float* sW1 = hl + 2 * HLF;
+  float* sb0 = sW1 + T_UM * C;
+  int32_t* srow = reinterpret_cast<int32_t*>(sb0 + T_UM);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(srow + RP);  // [0,1] full, [2,3] empty, [4] done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
+  const int nch = (D + T_SC - 1) / T_SC, nsplit = t_nsplit(D);
+  constexpr uint32_t tcols = 512;
+
+  for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
+  if (tid == 32) {
+    umma::mbar_init(&bar[0], 7);  // one arrive per producer warp
+    umma::mbar_init(&bar[1], 7);
+    umma::mbar_init(&bar[2], 1);
+    umma::mbar_init(&bar[3], 1);
+    umma::mbar_init(&bar[4], 1);
+    umma::mbar_fence_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tslot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  bool badx = false;
+  if (warp < 7) {
+    // ------------------------------------------------------------ producers
+    const int pt = tid;  // 0 .. 223
+    auto issue = [&](int c) {
+      float* rA = raw + (c % S) * RSF;
+      float* rX = rA + T_SC * T_UM;
+      const int k0 = c * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
+      for (int e = pt; e < nk * cpr; e += T_WS_PRODUCERS) {
+        const int k = e / cpr, q = e % cpr;
+        cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
+      }
+      const int cx = nk / 4;
+      for (int e = pt; e < R * cx; e += T_WS_PRODUCERS) {
+        const int r = e / cx, q = e % cx;
+        cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
+      }
+      cp_commit();
+    };
+    for (int e = pt; e < nu4 * C / 4; e += T_WS_PRODUCERS)
+      cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
+    for (int e = pt; e < nu4 / 4; e += T_WS_PRODUCERS)
+      cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
+    for (int c = 0; c < S - 1; ++c) {
+      if (c < nch) issue(c);
+      else cp_commit();
+    }
+    uint32_t eph[2] = {0u, 0u};
+    for (int c = 0; c < nch; ++c) {
+      if (c + S - 1 < nch) issue(c + S - 1);
+      else cp_commit();
+      cp_wait<3>();
+      asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");  // chunk c landed
+      const int b = c & 1;
+      if (c >= 2) {  // buffer b consumed by the MMAs of chunk c - 2
+        umma::mbar_wait(&bar[2 + b], eph[b]);
+        eph[b] ^= 1u;
+      }
+      float* Ah = hl + b * HLF;
+      float* Al = Ah + T_UM * T_SC;
+      float* Bh = Al + T_UM * T_SC;
+      float* Bl = Bh + RP * T_SC;
+      const float* rA = raw + (c % S) * RSF;
+      const float* rX = rA + T_SC * T_UM;
+      const int nk = min(T_SC, D - c * T_SC);
+      for (int e = pt; e < T_UM * (T_SC / 4); e += T_WS_PRODUCERS) {
+        const int u = e % T_UM, kq = e / T_UM;
+        float4 h, l;
+        float* hp = &h.x;
+        float* lp = &l.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 4 * kq + j;
+          const float v = (u < nu && k < nk) ? rA[k * T_UM + u] : 0.f;
+          umma::split3(v, hp[j], lp[j]);
+        }
+        const uint32_t o = umma::kmaj_off(u, 4 * kq, T_UM) / 4;
+        *reinterpret_cast<float4*>(Ah + o) = h;
+        *reinterpret_cast<float4*>(Al + o) = l;
+      }
+      for (int e = pt; e < RP * (T_SC / 4); e += T_WS_PRODUCERS) {
+        const int r = e % RP, kq = e / RP;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < R && 4 * kq < nk) v = *reinterpret_cast<const float4*>(rX + r * T_SXLD + 4 * kq);
+        badx |= !finite(v.x) | !finite(v.y) | !finite(v.z) | !finite(v.w);
+        float4 h, l;
+        umma::split3(v.x, h.x, l.x);
+        umma::split3(v.y, h.y, l.y);
+        umma::split3(v.z, h.z, l.z);
+        umma::split3(v.w, h.w, l.w);
+        const uint32_t o = umma::kmaj_off(r, 4 * kq, RP) / 4;
+        *reinterpret_cast<float4*>(Bh + o) = h;
+        *reinterpret_cast<float4*>(Bl + o) = l;
+      }
+      umma::fence_async_smem();
+      // every producer is past its raw-stage reads and hi/lo writes before the
+      // stage is refilled (next iteration's issue) and before the MMA starts
+      asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[b])) : "memory");
+    }
+    cp_wait<0>();
+  } else if (lane == 0) {
+    // --------------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma::idesc_tf32(T_UM, RP, false, false);
+    uint32_t fph[2] = {0u, 0u};
+    for (int c = 0; c < nch; ++c) {
+      const int b = c & 1;
+      umma::mbar_wait(&bar[b], fph[b]);
+      fph[b] ^= 1u;
+      umma::fence_after();
+      float* Ah = hl + b * HLF;
+      float* Al = Ah + T_UM * T_SC;
+      float* Bh = Al + T_UM * T_SC;
+      float* Bl = Bh + RP * T_SC;
+      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+      const uint32_t acc = tmem + (uint32_t)((c >> 1) * RP);
+      const int nk = min(T_SC, D - c * T_SC);
+      for (int s2 = 0; s2 < (nk + 7) / 8; ++s2) {
+        const uint64_t dah = umma::kmaj_desc(ah, T_UM, s2), dal = umma::kmaj_desc(al, T_UM, s2);
+        const uint64_t dbh = umma::kmaj_desc(bh, RP, s2), dbl = umma::kmaj_desc(bl, RP, s2);
+        umma::mma_tf32(acc, dah, dbh, idesc, (c & 1) || s2 > 0);
+        umma::mma_tf32(acc, dah, dbl, idesc, true);
+        umma::mma_tf32(acc, dal, dbh, idesc, true);
+      }
+      umma::commit(&bar[2 + b]);
+    }
+    umma::commit(&bar[4]);
+  }
+  // ---- all warps: accumulators done → split-order sum, epilogue -----------
+  umma::mbar_wait(&bar[4], 0);
+  umma::fence_after();
+  badx = __syncthreads_or(badx);
+  if (badx && tid == 0) flag_min(&M.ctl->bad_node, 0);
+  PK_TRACE(2);
+  const int q = warp & 3, half = warp >> 2, uu = 32 * q + lane, rlo = half * (RP / 2);
+  float z[16];
+  for (int sp = 0; sp < nsplit; ++sp) {
+#pragma unroll
+    for (int c0 = 0; c0 < 16; c0 += 8) {
+      float v[8];
+      umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(sp * RP + rlo + c0), v);
+      umma::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z[c0 + i] = sp == 0 ? v[i] : z[c0 + i] + v[i];
+    }
+  }
+  float* sA = raw;  // [RP][T_UM]
+  int bad = INT_MAX;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = rlo + i;
+    float a = 0.f;
+    if (r < R && uu < nu) {
+      const float zz = z[i] + sb0[uu];
+      a = act_fwd(M.act, zz);
+      M.Z[0][(int64_t)r * H + u0 + uu] = zz;
+      M.A[0][(int64_t)r * H + u0 + uu] = a;
+      if (!finite(zz)) bad = min(bad, 1);
+      if (!finite(a)) bad = min(bad, 2);
+    }
+    sA[r * T_UM + uu] = a;
+  }
+  if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  umma::fence_before();
+  __syncthreads();
+  PK_TRACE(3);
+  if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+  const int nbt = (nu + T_LB - 1) / T_LB;
+  for (int e = tid; e < nbt * R * C; e += NT) {
+    const int bl = e / (R * C), rc = e % (R * C), r = rc / C, c = rc % C;
+    const int ub = bl * T_LB;
+    const float* a = sA + r * T_UM + ub;
+    const float* w = sW1 + ub * C + c;
+    float p = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
+    M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
+  }
+  PK_TRACE(4);
+}
+
 // ----------------------------------------------------------- backward --
 // One CTA per (member, 32-unit tile, group of `ng` consecutive 128-input
 // tiles).  The per-unit-tile work — logits, softmax-xent, dZ0 — is done once
