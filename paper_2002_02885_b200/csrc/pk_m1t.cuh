@@ -603,11 +603,13 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
       else cp_commit();
       cp_wait<3>();
       asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");  // chunk c landed
+      if (c == 8) PK_TRACE(8);
       const int b = c & 1;
       if (c >= 2) {  // buffer b consumed by the MMAs of chunk c - 2
         umma::mbar_wait(&bar[2 + b], eph[b]);
         eph[b] ^= 1u;
       }
+      if (c == 8) PK_TRACE(9);
       float* Ah = hl + b * HLF;
       float* Al = Ah + T_UM * T_SC;
       float* Bh = Al + T_UM * T_SC;
@@ -644,11 +646,13 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
         *reinterpret_cast<float4*>(Bh + o) = h;
         *reinterpret_cast<float4*>(Bl + o) = l;
       }
+      if (c == 8) PK_TRACE(10);
       umma::fence_async_smem();
       // every producer is past its raw-stage reads and hi/lo writes before the
       // stage is refilled (next iteration's issue) and before the MMA starts
       asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[b])) : "memory");
+      if (c == 8) PK_TRACE(11);
     }
     cp_wait<0>();
   } else if (lane == 0) {
@@ -660,6 +664,7 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
       umma::mbar_wait(&bar[b], fph[b]);
       fph[b] ^= 1u;
       umma::fence_after();
+      if (c == 8 && pk_trace_slots) pk_trace_slots[12] = gtimer();
       float* Ah = hl + b * HLF;
       float* Al = Ah + T_UM * T_SC;
       float* Bh = Al + T_UM * T_SC;
@@ -676,6 +681,7 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
         umma::mma_tf32(acc, dal, dbh, idesc, true);
       }
       umma::commit(&bar[2 + b]);
+      if (c == 8 && pk_trace_slots) pk_trace_slots[13] = gtimer();
     }
     umma::commit(&bar[4]);
   }
