@@ -143,9 +143,8 @@ def _phase_plan(wl, es=4):
     xb = es * b * dims[0]
     out = []
     if tens:
-        # mirror of build_phases: split-K clusters unless they exceed 2 waves
-        clusters = len(tens) * -(-dims[1] // 128) * -(-dims[0] // 64)
-        kern = "k_m1s_fwd" if clusters > 2 * 148 else "k_m1t_fwd"
+        # mirror of build_phases: the cluster-streaming forward (default)
+        kern = "k_m1c_fwd"
         out.append(("T1FWD", kern + T,
                     sum(_m1_bytes(dims, o, b, es, "fwd", 32) for o in tens) + xb))
     if fused:

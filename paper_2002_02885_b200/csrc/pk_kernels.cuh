@@ -1093,6 +1093,29 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
 }
 
 template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ PhaseArgs<T> P) {
+  extern __shared__ __align__(128) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  if constexpr (sizeof(T) == 4) {
+    const Tile t = P.tiles[blockIdx.x];
+    const FeedDev<T> f = feed_of(P, t.member);
+    __shared__ MemberDev<float> sM;
+    if (threadIdx.x < sizeof(MemberDev<float>) / 4)
+      reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
+          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+    __syncthreads();
+    // m0 = unit tile, n0 = cluster rank (input-split range)
+    if (f.take != 0) m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+  } else {
+    __trap();
+  }
+  kernel_end(P, true);
+}
+
+template <typename T>
 __global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(128) char smem_raw[];
   if (threadIdx.x == 0)

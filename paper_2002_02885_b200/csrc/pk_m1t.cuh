@@ -45,8 +45,8 @@ constexpr int T_BWLD = T_BU + 4;  // bwd: W0-tile row stride (144 B: LDS.128 by 
 constexpr int T_LB = 32;      // member-local partial-logit block (units)
 constexpr int T_MAXC = 32;    // classes on this path
 constexpr int T_MAXR = 128;   // rows on this path
-constexpr int T_MAXCS = 16;
-__host__ __device__ inline int cdiv_d(int a, int b) { return (a + b - 1) / b; }   // max cluster size (non-portable) → D <= 1024
+constexpr int T_MAXCS = 16;   // max cluster size (non-portable) → D <= 1024
+__host__ __device__ inline int cdiv_d(int a, int b) { return (a + b - 1) / b; }
 
 __host__ __device__ inline int t_nsplit(int D) { return (D + T_KS - 1) / T_KS; }
 __host__ __device__ inline int t_ntile(int H) { return (H + T_UM - 1) / T_UM; }
@@ -736,6 +736,261 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
     M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
   }
   PK_TRACE(4);
+}
+
+// ------------------------- cluster-streaming forward (the general form) --
+// One thread-block cluster of CS CTAs per (member, 128-unit tile); rank r
+// owns a contiguous range of the 64-deep input splits and streams their
+// 32-deep chunks through a warp-specialised pipeline (7 producer warps:
+// cp.async ring → tf32 hi/lo split; 1 MMA warp).  Every split accumulates
+// alone in its own TMEM columns with the cluster forward's MMA sequence; the
+// partials land in the CTA's shared memory and, after a cluster barrier,
+// rank r reduces rows r, r+CS, ... over DSMEM summing the splits in global
+// order (z = p0 + p1 + ... + b0).  CS is chosen per pack for occupancy
+// (CS = nsplit is the one-split-per-CTA cluster forward; small CS streams);
+// the arithmetic never depends on it, so packed == standalone bitwise.
+__host__ __device__ inline int m1c_raw_stages(int RP) { return RP >= 128 ? 2 : 4; }
+__host__ __device__ inline int m1c_region_floats(int RP) {  // raw ring + hi/lo buffers
+  return m1c_raw_stages(RP) * (T_SC * T_UM + RP * T_SXLD) + 2 * 2 * (T_UM + RP) * T_SC;
+}
+__host__ __device__ inline int m1c_fwd_smem(int RP, int C) {
+  return m1c_region_floats(RP) * 4 + T_UM * C * 4 + T_UM * 4 + RP * 4 + 2 * T_MAXCS * 4 + 64;
+}
+// most splits a CTA may own: TMEM columns and the partial + row buffers
+__host__ __device__ inline int m1c_max_local(int RP) {
+  const int by_tmem = 512 / RP;
+  const int by_smem = (m1c_region_floats(RP) - RP * T_UM) / (RP * T_UM);
+  return by_tmem < by_smem ? by_tmem : by_smem;
+}
+__host__ __device__ inline void m1c_range(int nsplit, int CS, int r, int* s0, int* n) {
+  const int base = nsplit / CS, extra = nsplit % CS;
+  *n = base + (r < extra ? 1 : 0);
+  *s0 = r * base + (r < extra ? r : extra);
+}
+
+__device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
+                             int tile, int rank, int CS) {
+  const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
+  const int R = f.take, RP = m1_rows_pad(M.max_rows), S = m1c_raw_stages(RP);
+  const int u0 = tile * T_UM, nu = min(T_UM, H - u0), nu4 = (nu + 3) & ~3;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nsplit = t_nsplit(D);
+  int sbeg, nloc;
+  m1c_range(nsplit, CS, rank, &sbeg, &nloc);
+  const int c_beg = 2 * sbeg, c_end = min(2 * (sbeg + nloc), (D + T_SC - 1) / T_SC);
+  const int nchl = c_end - c_beg;  // my chunks
+  const int RSF = T_SC * T_UM + RP * T_SXLD;
+  float* raw = reinterpret_cast<float*>(sm);
+  float* hl = raw + S * RSF;
+  const int HLF = 2 * (T_UM + RP) * T_SC;
+  float* sW1 = raw + m1c_region_floats(RP);
+  float* sb0 = sW1 + T_UM * C;
+  int32_t* srow = reinterpret_cast<int32_t*>(sb0 + T_UM);
+  int32_t* s_own = srow + RP;          // [T_MAXCS] owner rank of split s
+  int32_t* s_loc = s_own + T_MAXCS;    // [T_MAXCS] local index within the owner
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_loc + T_MAXCS);  // [0,1] full [2,3] empty [4] done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+  float* sP = raw;                      // after the loop: [nloc][RP][T_UM] partials
+  float* sA = raw + nloc * RP * T_UM;   // then my rows' activations [nr][T_UM]
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
+  const uint32_t tcols = umma::tmem_cols_pow2(max(nloc, 1) * RP);
+
+  for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
+  if (tid < CS) {
+    int b0, n0;
+    m1c_range(nsplit, CS, tid, &b0, &n0);
+    for (int i = 0; i < n0; ++i) {
+      s_own[b0 + i] = tid;
+      s_loc[b0 + i] = i;
+    }
+  }
+  if (tid == 32) {
+    umma::mbar_init(&bar[0], 7);
+    umma::mbar_init(&bar[1], 7);
+    umma::mbar_init(&bar[2], 1);
+    umma::mbar_init(&bar[3], 1);
+    umma::mbar_init(&bar[4], 1);
+    umma::mbar_fence_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tslot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  bool badx = false;
+  if (warp < 7) {
+    // ------------------------------------------------------------ producers
+    const int pt = tid;
+    auto issue = [&](int i) {  // my chunk i (global chunk c_beg + i) → stage i % S
+      float* rA = raw + (i % S) * RSF;
+      float* rX = rA + T_SC * T_UM;
+      const int k0 = (c_beg + i) * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
+      for (int e = pt; e < nk * cpr; e += T_WS_PRODUCERS) {
+        const int k = e / cpr, q = e % cpr;
+        cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
+      }
+      const int cx = nk / 4;
+      for (int e = pt; e < R * cx; e += T_WS_PRODUCERS) {
+        const int r = e / cx, q = e % cx;
+        cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
+      }
+      cp_commit();
+    };
+    for (int e = pt; e < nu4 * C / 4; e += T_WS_PRODUCERS)
+      cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
+    for (int e = pt; e < nu4 / 4; e += T_WS_PRODUCERS)
+      cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
+    for (int i = 0; i < S - 1; ++i) {
+      if (i < nchl) issue(i);
+      else cp_commit();
+    }
+    uint32_t eph[2] = {0u, 0u};
+    for (int i = 0; i < nchl; ++i) {
+      if (i + S - 1 < nchl) issue(i + S - 1);
+      else cp_commit();
+      if (S == 4) cp_wait<3>(); else cp_wait<1>();
+      asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");  // chunk i landed
+      const int b = i & 1;
+      if (i >= 2) {
+        umma::mbar_wait(&bar[2 + b], eph[b]);
+        eph[b] ^= 1u;
+      }
+      float* Ah = hl + b * HLF;
+      float* Al = Ah + T_UM * T_SC;
+      float* Bh = Al + T_UM * T_SC;
+      float* Bl = Bh + RP * T_SC;
+      const float* rA = raw + (i % S) * RSF;
+      const float* rX = rA + T_SC * T_UM;
+      const int nk = min(T_SC, D - (c_beg + i) * T_SC);
+      for (int e = pt; e < T_UM * (T_SC / 4); e += T_WS_PRODUCERS) {
+        const int u = e % T_UM, kq = e / T_UM;
+        float4 h, l;
+        float* hp = &h.x;
+        float* lp = &l.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 4 * kq + j;
+          const float v = (u < nu && k < nk) ? rA[k * T_UM + u] : 0.f;
+          umma::split3(v, hp[j], lp[j]);
+        }
+        const uint32_t o = umma::kmaj_off(u, 4 * kq, T_UM) / 4;
+        *reinterpret_cast<float4*>(Ah + o) = h;
+        *reinterpret_cast<float4*>(Al + o) = l;
+      }
+      for (int e = pt; e < RP * (T_SC / 4); e += T_WS_PRODUCERS) {
+        const int r = e % RP, kq = e / RP;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < R && 4 * kq < nk) v = *reinterpret_cast<const float4*>(rX + r * T_SXLD + 4 * kq);
+        badx |= !finite(v.x) | !finite(v.y) | !finite(v.z) | !finite(v.w);
+        float4 h, l;
+        umma::split3(v.x, h.x, l.x);
+        umma::split3(v.y, h.y, l.y);
+        umma::split3(v.z, h.z, l.z);
+        umma::split3(v.w, h.w, l.w);
+        const uint32_t o = umma::kmaj_off(r, 4 * kq, RP) / 4;
+        *reinterpret_cast<float4*>(Bh + o) = h;
+        *reinterpret_cast<float4*>(Bl + o) = l;
+      }
+      umma::fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"n"(T_WS_PRODUCERS) : "memory");
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[b]))
+                     : "memory");
+    }
+    cp_wait<0>();
+  } else if (lane == 0) {
+    // --------------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma::idesc_tf32(T_UM, RP, false, false);
+    uint32_t fph[2] = {0u, 0u};
+    for (int i = 0; i < nchl; ++i) {
+      const int b = i & 1, c = c_beg + i;
+      umma::mbar_wait(&bar[b], fph[b]);
+      fph[b] ^= 1u;
+      umma::fence_after();
+      float* Ah = hl + b * HLF;
+      float* Al = Ah + T_UM * T_SC;
+      float* Bh = Al + T_UM * T_SC;
+      float* Bl = Bh + RP * T_SC;
+      const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+      const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+      const uint32_t acc = tmem + (uint32_t)(((c >> 1) - sbeg) * RP);
+      const int nk = min(T_SC, D - c * T_SC);
+      for (int s2 = 0; s2 < (nk + 7) / 8; ++s2) {
+        const uint64_t dah = umma::kmaj_desc(ah, T_UM, s2), dal = umma::kmaj_desc(al, T_UM, s2);
+        const uint64_t dbh = umma::kmaj_desc(bh, RP, s2), dbl = umma::kmaj_desc(bl, RP, s2);
+        umma::mma_tf32(acc, dah, dbh, idesc, (c & 1) || s2 > 0);
+        umma::mma_tf32(acc, dah, dbl, idesc, true);
+        umma::mma_tf32(acc, dal, dbh, idesc, true);
+      }
+      umma::commit(&bar[2 + b]);
+    }
+    umma::commit(&bar[4]);
+  }
+  umma::mbar_wait(&bar[4], 0);
+  umma::fence_after();
+  badx = __syncthreads_or(badx);  // also: the raw / hi-lo region is free
+  if (badx && tid == 0) flag_min(&M.ctl->bad_node, 0);
+  PK_TRACE(2);
+  // ---- my split partials: TMEM → sP[local][r][u] ----------------------------
+  {
+    const int q = warp & 3, half = warp >> 2, u = 32 * q + lane;
+    for (int l = 0; l < nloc; ++l)
+      for (int c0 = half * (RP / 2); c0 < (half + 1) * (RP / 2); c0 += 8) {
+        float v[8];
+        umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(l * RP + c0), v);
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sP[(l * RP + c0 + i) * T_UM + u] = v[i];
+      }
+  }
+  umma::fence_before();
+  umma::cluster_sync();  // every split's partial is in the cluster's shared memory
+  PK_TRACE(3);
+  if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+  // ---- rank r reduces rows r, r + CS, ...: z = Σ_s p_s in split order ------
+  const int nr = R > rank ? (R - rank + CS - 1) / CS : 0;
+  int bad = INT_MAX;
+  for (int e = tid; e < nr * T_UM; e += NT) {
+    const int rl = e / T_UM, u = e % T_UM, r = rank + rl * CS;
+    float a = 0.f;
+    if (u < nu) {
+      float v[T_MAXCS];
+#pragma unroll
+      for (int sp = 0; sp < T_MAXCS; ++sp)
+        v[sp] = sp < nsplit
+                    ? umma::dsmem_ld(umma::smem_u32(sP + (s_loc[sp] * RP + r) * T_UM + u),
+                                     (uint32_t)s_own[sp])
+                    : 0.f;
+      float z = v[0];
+#pragma unroll
+      for (int sp = 1; sp < T_MAXCS; ++sp)
+        if (sp < nsplit) z += v[sp];
+      z += sb0[u];
+      a = act_fwd(M.act, z);
+      M.Z[0][(int64_t)r * H + u0 + u] = z;
+      M.A[0][(int64_t)r * H + u0 + u] = a;
+      if (!finite(z)) bad = min(bad, 1);
+      if (!finite(a)) bad = min(bad, 2);
+    }
+    sA[e] = a;
+  }
+  __syncthreads();
+  const int nbt = (nu + T_LB - 1) / T_LB;
+  for (int e = tid; e < nbt * nr * C; e += NT) {
+    const int bl = e / (nr * C), rc = e % (nr * C), rl = rc / C, c = rc % C;
+    const int ub = bl * T_LB, r = rank + rl * CS;
+    const float* a = sA + rl * T_UM + ub;
+    const float* w = sW1 + ub * C + c;
+    float p = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < T_LB; ++j) p = fmaf(a[j], ub + j < nu ? w[j * C] : 0.f, p);
+    M.Z[1][((int64_t)(u0 / T_LB + bl) * M.max_rows + r) * C + c] = p;
+  }
+  if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
+  PK_TRACE(4);
+  umma::cluster_arrive_relaxed();  // peers are done reading this CTA's partials
+  umma::cluster_wait();
 }
 
 // ----------------------------------------------------------- backward --

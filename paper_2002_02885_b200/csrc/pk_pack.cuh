@@ -135,6 +135,7 @@ static cudaError_t init_smem_limit(int device, int* out) {
   ks.push_back(pk::k_m1t_fwd<T>);
   ks.push_back(pk::k_m1t_bwd<T>);
   ks.push_back(pk::k_m1s_fwd<T>);
+  ks.push_back(pk::k_m1c_fwd<T>);
   int dyn = optin;
   for (auto k : ks) {
     cudaFuncAttributes fa{};
@@ -147,6 +148,9 @@ static cudaError_t init_smem_limit(int device, int* out) {
       return e;
   // input-split clusters of k_m1t_fwd go up to 16 CTAs (non-portable size)
   if ((e = cudaFuncSetAttribute(pk::k_m1t_fwd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                1)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(pk::k_m1c_fwd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
                                 1)) != cudaSuccess)
     return e;
   *out = dyn;
@@ -361,9 +365,36 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     phases.insert(phases.begin(), m1f);
     phases.push_back(m1b);
   }
+  // default forward: cluster-streaming (k_m1c_fwd) with the cluster size that
+  // fills about one wave; PK_FWD=split|stream selects the older variants
+  const char* fv = getenv("PK_FWD");
+  if (!eval && !tf.host.empty() && !fv) {
+    int n_tiles = 0, cs_lo = 1, ns_max = 1, sm = 0;
+    for (int k = 0; k < p->K; ++k) {
+      const pk_member* m = p->members[k];
+      if (!m->m1t) continue;
+      const int RP = pk::m1_rows_pad(m->desc.max_rows), ns = pk::t_nsplit(m->desc.dims[0]);
+      n_tiles += pk::t_ntile(m->desc.dims[1]);
+      cs_lo = std::max(cs_lo, cdiv(ns, pk::m1c_max_local(RP)));
+      ns_max = std::max(ns_max, ns);
+      sm = std::max(sm, pk::m1c_fwd_smem(RP, m->desc.dims[2]));
+    }
+    const int CS = std::max(cs_lo, std::min(cdiv(148, n_tiles), ns_max));
+    if (CS <= pk::T_MAXCS && sm <= smem_budget(dt)) {
+      tf.host.clear();
+      for (int k = 0; k < p->K; ++k)
+        if (p->members[k]->m1t)
+          for (int t = 0; t < pk::t_ntile(p->members[k]->desc.dims[1]); ++t)
+            for (int r = 0; r < CS; ++r) tf.host.push_back(Tile{k, 0, pk::TK_FWD, t, r});
+      tf.special = 6;
+      tf.cs = CS;
+      tf.smem = sm;
+    }
+  }
   // many clusters (several waves): stream the input dimension instead, one CTA
   // per unit tile, when every tensor member's streaming smem fits
-  if (!eval && (int)tf.host.size() > 2 * 148 && !getenv("PK_NO_STREAM_FWD")) {
+  if (!eval && tf.special == 3 && (int)tf.host.size() > 2 * 148 &&
+      !(fv && !strcmp(fv, "split"))) {
     bool fits = true;
     int sm = 0;
     for (int k = 0; k < p->K; ++k) {
@@ -465,6 +496,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
                           : ph.special == 3 ? pk::k_m1t_fwd<T>
                           : ph.special == 4 ? pk::k_m1t_bwd<T>
                           : ph.special == 5 ? pk::k_m1s_fwd<T>
+                          : ph.special == 6 ? pk::k_m1c_fwd<T>
                                             : kernel_for<T>(ph.mask);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) {
