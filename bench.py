@@ -143,8 +143,10 @@ def _phase_plan(wl, es=4):
     xb = es * b * dims[0]
     out = []
     if tens:
-        # mirror of build_phases: the cluster-streaming forward (default)
-        kern = "k_m1c_fwd"
+        # mirror of build_phases: one-shot split-K clusters when one split per
+        # CTA fits a wave, else the cluster-streaming forward
+        kern = "k_m1t_fwd" if len(tens) * -(-dims[1] // 128) * -(-dims[0] // 64) <= 148 \
+            else "k_m1c_fwd"
         out.append(("T1FWD", kern + T,
                     sum(_m1_bytes(dims, o, b, es, "fwd", 32) for o in tens) + xb))
     if fused:

@@ -379,8 +379,32 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
       ns_max = std::max(ns_max, ns);
       sm = std::max(sm, pk::m1c_fwd_smem(RP, m->desc.dims[2]));
     }
-    const int CS = std::max(cs_lo, std::min(cdiv(148, n_tiles), ns_max));
-    if (CS <= pk::T_MAXCS && sm <= smem_budget(dt)) {
+    // the largest cluster size whose clusters all fit co-resident (one
+    // wave); never below what TMEM / smem per CTA allow
+    int CS = cs_lo;
+    for (int cs = std::min(ns_max, pk::T_MAXCS); cs > cs_lo; --cs) {
+      if (dt != PK_F32) break;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs * n_tiles);
+      cfg.blockDim = dim3(pk::NT);
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, pk::k_m1c_fwd<float>, &cfg) == cudaSuccess &&
+          nc >= n_tiles) {
+        CS = cs;
+        break;
+      }
+    }
+    // one split per CTA fits in a wave: the one-shot split-K cluster forward
+    // (same arithmetic, no streaming pipeline) is the lower-latency choice
+    if (CS < ns_max && sm <= smem_budget(dt)) {
       tf.host.clear();
       for (int k = 0; k < p->K; ++k)
         if (p->members[k]->m1t)
