@@ -72,7 +72,7 @@ struct M1T {
            + 2 * RP * T_BU * 4         // dZ0 tile, A0 tile
            + (1 + ns) * T_BU * C * 4   // W1 rows + slots
            + T_MAXC * 4                // b1
-           + 2 * RP * 4 + 64;          // rows, labels, barriers
+           + 2 * RP * 4 + 128;         // rows, labels, barriers
   }
 };
 
@@ -1107,9 +1107,9 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* sb1 = sW1 + (1 + ns) * T_BU * C;               // [T_MAXC]
   int32_t* srow = reinterpret_cast<int32_t*>(sb1 + T_MAXC);
   int32_t* ylab = srow + RP;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // [0,1] stages, 2 W1, 3 MMA
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
-  constexpr uint32_t tcols = 32;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // [3] unused, [4..11] pipeline
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
+  constexpr uint32_t tcols = 64;  // two 32-column gradient buffers
 
   // ---- prologue (independent of k_m1t_fwd) --------------------------------
   for (int r = tid; r < RP; r += NT) {
@@ -1250,73 +1250,70 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const float bc2 = M.opt == PK_OPT_ADAM ? float(ctl->bc2) : 1.f;
   const int fault = ctl->fault_grad;
   bool badW0 = false, badW1 = false, badb1 = false, badb0 = false;
-  // ---- stream the group's input tiles: dW0 = X[:, tile]ᵀ · dZ0 on the tensor
-  //      cores, optimizer epilogue straight from TMEM -------------------------
+  // ---- stream the group's input tiles, warp-specialised -------------------
+  //   warps 0-3 (epilogue): TMEM gradient → optimizer against the resident W0
+  //                         tile → Pn/Sn; frees the TMEM buffer and the stage
+  //   warps 4-6 (producers): Xᵀ / dZ0 hi-lo staging per 32-row chunk, the
+  //                         cp.async of the next input tile
+  //   warp 7 lane 0 (MMA):  12 tcgen05.mma per chunk into TMEM buffer i & 1
+  // so tile i's optimizer epilogue overlaps tile i+1's staging and MMAs.
+  // mbarriers: 4 afull (count 3), 5 aempty, 6/7 tfull, 8/9 tempty (count 4),
+  // 10/11 sfree (count 4)
   const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
-  uint32_t mph = 0;
-  for (int i = 0; i < ng; ++i) {
-    const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
-    const float* sW = stg + (i % S) * SF;
-    const float* sX = sW + (1 + ns) * T_BK * T_BWLD;
-    if (S == 2 && i + 1 < ng) cp_wait<1>(); else cp_wait<0>();  // input tile i landed
-    __syncthreads();
-    if (i == min(1, ng - 1)) PK_TRACE(12);  // tile 1 (tile 0 when ng == 1): after cp.async wait
-    for (int ch = 0; ch < nch; ++ch) {
-      const int r0 = ch * 32;
-      if (!(a_ready && i == 0)) m1t_stage_xT(Ah, Al, sX, r0, R, nk);
-      for (int e = tid; e < T_BU * 8; e += NT) {  // B = dZ0ᵀ: rows u, K = rows r
-        const int u = e % T_BU, rq = e / T_BU;
-        float4 h, l;
-        float* hp = &h.x;
-        float* lp = &l.x;
+  cp_wait<0>();  // the prologue's stages (issued by every thread) have landed
+  if (tid == 32) {
+    umma::mbar_init(&bar[4], 3);
+    umma::mbar_init(&bar[5], 1);
+    for (int j = 6; j < 10; ++j) umma::mbar_init(&bar[j], j < 8 ? 1 : 4);
+    umma::mbar_init(&bar[10], 4);
+    umma::mbar_init(&bar[11], 4);
+    umma::mbar_fence_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  if (warp < 4) {
+    // -------------------------------------------------------------- epilogue
+    const int k = 32 * warp + lane;
+    for (int i = 0; i < ng; ++i) {
+      const int t = i & 1, st = i % S;
+      const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
+      umma::mbar_wait(&bar[6 + t], (uint32_t)((i >> 1) & 1));
+      umma::fence_after();
+      float g[32];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) umma::split3(sdZ[(r0 + 4 * rq + j) * T_BU + u], hp[j], lp[j]);
-        const uint32_t o = umma::kmaj_off(u, 4 * rq, T_BU) / 4;
-        *reinterpret_cast<float4*>(Bh + o) = h;
-        *reinterpret_cast<float4*>(Bl + o) = l;
+      for (int c8 = 0; c8 < 4; ++c8) {
+        float v[8];
+        umma::tmem_ld8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(t * T_BU + 8 * c8), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[8 * c8 + j] = v[j];
       }
-      umma::fence_async_smem();
+      umma::tmem_wait_ld();
       umma::fence_before();
-      __syncthreads();
-      umma::fence_after();
-      if (i == min(1, ng - 1) && ch == 0) PK_TRACE(13);
-      if (tid == 0) {
-        const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
-        const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
-        for (int s = 0; s < 4; ++s) {
-          const uint64_t dah = umma::kmaj_desc(ah, T_BK, s), dal = umma::kmaj_desc(al, T_BK, s);
-          const uint64_t dbh = umma::kmaj_desc(bh, T_BU, s), dbl = umma::kmaj_desc(bl, T_BU, s);
-          umma::mma_tf32(tmem, dah, dbh, idesc, ch > 0 || s > 0);
-          umma::mma_tf32(tmem, dah, dbl, idesc, true);
-          umma::mma_tf32(tmem, dal, dbh, idesc, true);
-        }
-        umma::commit(&bar[3]);
-      }
-      umma::mbar_wait(&bar[3], mph);
-      mph ^= 1;
-      umma::fence_after();
-      if (i == min(1, ng - 1) && ch == 0) PK_TRACE(14);
-    }
-    // epilogue: W0[k0 + k, u0 + u] update from the TMEM gradient
-    {
-      const int q = warp & 3, half = warp >> 2;
-      const int k = 32 * q + lane;
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[8 + t]))
+                     : "memory");
+      if (i == min(1, ng - 1)) PK_TRACE(14);
+      const float* sW = stg + st * SF;
+      if (k < nk) {
+        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0;
+        const float* row = sW + k * T_BWLD;
+        // one rolled quad loop, one optimizer body (nu % 4 == 0)
 #pragma unroll 1
-      for (int c8 = 0; c8 < 2; ++c8) {
-        const int uc = half * 16 + c8 * 8;
-        float g[8];
-        umma::tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)uc, g);
-        umma::tmem_wait_ld();
-        if (k >= nk || uc >= nu) continue;
-        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + uc;
-        const float* row = sW + k * T_BWLD + uc;  // LDS.128 per tensor and quad
-        // one rolled quad loop and one optimizer body (opt_step4): a small
-        // epilogue keeps this kernel inside the SM instruction cache
-        // (nu % 4 == 0: quads are all-valid or all-out)
-#pragma unroll 1
-        for (int qd = 0; qd < 2; ++qd) {
-          if (uc + 4 * qd >= nu) break;
-          float4 gq = qd ? make_float4(g[4], g[5], g[6], g[7]) : make_float4(g[0], g[1], g[2], g[3]);
+        for (int qd = 0; qd < 8; ++qd) {
+          if (4 * qd >= nu) break;
+          float4 gq;
+          switch (qd) {  // registers cannot be indexed dynamically: select
+            case 0: gq = make_float4(g[0], g[1], g[2], g[3]); break;
+            case 1: gq = make_float4(g[4], g[5], g[6], g[7]); break;
+            case 2: gq = make_float4(g[8], g[9], g[10], g[11]); break;
+            case 3: gq = make_float4(g[12], g[13], g[14], g[15]); break;
+            case 4: gq = make_float4(g[16], g[17], g[18], g[19]); break;
+            case 5: gq = make_float4(g[20], g[21], g[22], g[23]); break;
+            case 6: gq = make_float4(g[24], g[25], g[26], g[27]); break;
+            default: gq = make_float4(g[28], g[29], g[30], g[31]); break;
+          }
           if (fault == 2) gq = make_float4(NAN, NAN, NAN, NAN);
           badW0 |= !finite(gq.x) | !finite(gq.y) | !finite(gq.z) | !finite(gq.w);
           float4 w = *reinterpret_cast<const float4*>(row + 4 * qd);
@@ -1330,13 +1327,119 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
           if (ns >= 2) *reinterpret_cast<float4*>(Sn + NP + i0 + 4 * qd) = s1;
         }
       }
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[10 + st]))
+                     : "memory");
+      if (i == min(1, ng - 1)) PK_TRACE(15);
     }
-    if (i == min(1, ng - 1)) PK_TRACE(15);
-    umma::fence_before();
-    __syncthreads();  // stage i % S and the accumulator are free again
-    umma::fence_after();
-    if (i + S < ng) issue(i + S);
+  } else if (warp < 7) {
+    // ------------------------------------------------------------- producers
+    const int pt = tid - 128;
+    constexpr int NP3 = 96;
+    auto issue_p = [&](int i) {  // input tile i of the group → stage i % S
+      const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
+      float* sW = stg + (i % S) * SF;
+      float* sX = sW + (1 + ns) * T_BK * T_BWLD;
+      const int cw = nu / 4, cx = nk / 4;
+      for (int s2 = 0; s2 <= ns; ++s2) {
+        const float* src = (s2 == 0 ? Pc : Sc + (int64_t)(s2 - 1) * NP) + M.w_off[0] + u0;
+        for (int e = pt; e < nk * cw; e += NP3) {
+          const int kk = e / cw, c = e % cw;
+          cp_async<16>(sW + (s2 * T_BK + kk) * T_BWLD + 4 * c, src + (int64_t)(k0 + kk) * H + 4 * c, true);
+        }
+      }
+      for (int e = pt; e < R * cx; e += NP3) {
+        const int r = e / cx, c = e % cx;
+        cp_async<16>(sX + r * T_BXLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * c, true);
+      }
+      cp_commit();
+    };
+    uint32_t aph = 0;
+    bool first = true;
+    for (int i = 0; i < ng; ++i) {
+      if (i >= S) {  // issued at the end of iteration i - 1
+        cp_wait<0>();
+        asm volatile("bar.sync 2, 96;" ::: "memory");
+      }
+      const int nk = min(T_BK, D - (kt0 + i) * T_BK);
+      const float* sX = stg + (i % S) * SF + (1 + ns) * T_BK * T_BWLD;
+      for (int ch = 0; ch < nch; ++ch) {
+        if (!first) {
+          umma::mbar_wait(&bar[5], aph);
+          aph ^= 1u;
+        }
+        first = false;
+        if (!(a_ready && i == 0 && ch == 0)) {  // A = Xᵀ rows k, K = rows r
+          for (int e = pt; e < T_BK * 8; e += NP3) {
+            const int kk = e % T_BK, rq = e / T_BK;
+            float4 h, l;
+            float* hp = &h.x;
+            float* lp = &l.x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = ch * 32 + 4 * rq + j;
+              const float v = (r < R && kk < nk) ? sX[r * T_BXLD + kk] : 0.f;
+              umma::split3(v, hp[j], lp[j]);
+            }
+            const uint32_t o = umma::kmaj_off(kk, 4 * rq, T_BK) / 4;
+            *reinterpret_cast<float4*>(Ah + o) = h;
+            *reinterpret_cast<float4*>(Al + o) = l;
+          }
+        }
+        for (int e = pt; e < T_BU * 8; e += NP3) {  // B = dZ0ᵀ rows u, K = rows r
+          const int u = e % T_BU, rq = e / T_BU;
+          float4 h, l;
+          float* hp = &h.x;
+          float* lp = &l.x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) umma::split3(sdZ[(ch * 32 + 4 * rq + j) * T_BU + u], hp[j], lp[j]);
+          const uint32_t o = umma::kmaj_off(u, 4 * rq, T_BU) / 4;
+          *reinterpret_cast<float4*>(Bh + o) = h;
+          *reinterpret_cast<float4*>(Bl + o) = l;
+        }
+        umma::fence_async_smem();
+        asm volatile("bar.sync 2, 96;" ::: "memory");
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[4]))
+                       : "memory");
+      }
+      if (i + 1 < ng && i + 1 >= S) {  // refill: tile i + 1 into the stage of tile i + 1 - S
+        const int j = i + 1 - S;
+        umma::mbar_wait(&bar[10 + (j % S)], (uint32_t)((j / S) & 1));
+        issue_p(i + 1);
+      }
+    }
+    cp_wait<0>();
+  } else if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    uint32_t fph = 0;
+    const uint32_t ah = umma::smem_u32(Ah), al = umma::smem_u32(Al);
+    const uint32_t bh = umma::smem_u32(Bh), bl = umma::smem_u32(Bl);
+    for (int i = 0; i < ng; ++i) {
+      const int t = i & 1;
+      if (i >= 2) umma::mbar_wait(&bar[8 + t], (uint32_t)(((i - 2) >> 1) & 1));
+      for (int ch = 0; ch < nch; ++ch) {
+        umma::mbar_wait(&bar[4], fph);
+        fph ^= 1u;
+        umma::fence_after();
+        if (i == min(1, ng - 1) && ch == 0) PK_TRACE(13);
+        const uint32_t acc = tmem + (uint32_t)(t * T_BU);
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const uint64_t dah = umma::kmaj_desc(ah, T_BK, s2), dal = umma::kmaj_desc(al, T_BK, s2);
+          const uint64_t dbh = umma::kmaj_desc(bh, T_BU, s2), dbl = umma::kmaj_desc(bl, T_BU, s2);
+          umma::mma_tf32(acc, dah, dbh, idesc, ch > 0 || s2 > 0);
+          umma::mma_tf32(acc, dah, dbl, idesc, true);
+          umma::mma_tf32(acc, dal, dbh, idesc, true);
+        }
+        umma::commit(&bar[5]);  // A/B hi-lo buffers free
+      }
+      umma::commit(&bar[6 + t]);  // the tile's gradient is in TMEM buffer t
+    }
   }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
   PK_TRACE(3);
   // ---- W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3): element e
   //      of the unit tile is updated by the tile's group gi ≡ e (mod ngr)
