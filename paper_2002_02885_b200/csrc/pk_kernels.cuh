@@ -870,9 +870,10 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   __shared__ int s_bn[PK_MAX_PACK], s_bg[PK_MAX_PACK];
   __shared__ int s_code, s_who, s_idx, s_stop;
   const int K = P.K, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;  // kernels run 8 or 12 warps
   // warp w reduces the loss terms of members w, w+8, ...: lane-strided
   // partial sums then a fixed butterfly (deterministic, K-invariant)
-  for (int k = warp; k < K; k += NT / 32) {
+  for (int k = warp; k < K; k += nw) {
     const int take = feed_of(P, k).take;
     int bn = INT_MAX, bg = INT_MAX;
     if (take) {
@@ -912,7 +913,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)hdr_of(P).slot * P.ring_stride);
   double* losses = reinterpret_cast<double*>(st + 4);
   int committed = 0;
-  for (int k = threadIdx.x; k < K; k += NT) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
     MemberCtl* c = P.mems[k].ctl;
     const bool act = feed_of(P, k).take != 0;
     if (train) {
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NT, 1) k_m1t_bwd(const __grid_constant__ PhaseArgs<T> P) {
+__global__ void __launch_bounds__(T_BWD_NT, 1) k_m1t_bwd(const __grid_constant__ PhaseArgs<T> P) {
   extern __shared__ __align__(128) char smem_raw[];
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;

@@ -43,6 +43,7 @@ constexpr int T_BU = 32;      // bwd: hidden units per tile (MMA N)
 constexpr int T_BXLD = T_BK + 4;  // bwd: raw X row stride
 constexpr int T_BWLD = T_BU + 4;  // bwd: W0-tile row stride (144 B: LDS.128 by row is conflict-free)
 constexpr int T_LB = 32;      // member-local partial-logit block (units)
+constexpr int T_BWD_NT = 384; // k_m1t_bwd threads: 8 epilogue + 3 producer + 1 MMA warps
 constexpr int T_MAXC = 32;    // classes on this path
 constexpr int T_MAXR = 128;   // rows on this path
 constexpr int T_MAXCS = 16;   // max cluster size (non-portable) → D <= 1024
@@ -1057,8 +1058,8 @@ __device__ __forceinline__ void opt_step1(int opt, float lr, float wd, float bc1
 // A operand of the weight-gradient MMA: Xᵀ rows k (128) × K = batch rows
 // r0..r0+31, tf32 hi/lo, K-major; zero outside the valid box
 __device__ __forceinline__ void m1t_stage_xT(float* Ah, float* Al, const float* sX, int r0, int R,
-                                             int nk) {
-  for (int e = threadIdx.x; e < T_BK * 8; e += NT) {
+                                             int nk, int nthreads) {
+  for (int e = threadIdx.x; e < T_BK * 8; e += nthreads) {
     const int k = e % T_BK, rq = e / T_BK;
     float4 h, l;
     float* hp = &h.x;
@@ -1085,6 +1086,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const int R = f.take, RP = m1_rows_pad(M.max_rows), ns = M.n_slots;
   const int u0 = utile * T_BU, nu = min(T_BU, H - u0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int BT = T_BWD_NT;  // this kernel runs 12 warps
   const MemberCtl* ctl = M.ctl;
   const int par = ctl->parity;
   const int64_t NP = M.s_stride;  // slot block stride (16-byte multiple)
@@ -1112,11 +1114,11 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   constexpr uint32_t tcols = 64;  // two 32-column gradient buffers
 
   // ---- prologue (independent of k_m1t_fwd) --------------------------------
-  for (int r = tid; r < RP; r += NT) {
+  for (int r = tid; r < RP; r += BT) {
     srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
     ylab[r] = r < R ? f.labels[feed_row(f, r)] : 0;
   }
-  for (int c = tid; c < C; c += NT) sb1[c] = Pc[M.b_off[1] + c];
+  for (int c = tid; c < C; c += BT) sb1[c] = Pc[M.b_off[1] + c];
   if (warp == 0) umma::tmem_alloc(tslot, tcols);
   if (tid == 32) {
     umma::mbar_init(&bar[3], 1);
@@ -1135,12 +1137,12 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     const int cw = nu / 4, cx = nk / 4;
     for (int s = 0; s <= ns; ++s) {
       const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP) + M.w_off[0] + u0;
-      for (int e = tid; e < nk * cw; e += NT) {
+      for (int e = tid; e < nk * cw; e += BT) {
         const int k = e / cw, c = e % cw;
         cp_async<16>(sW + (s * T_BK + k) * T_BWLD + 4 * c, src + (int64_t)(k0 + k) * H + 4 * c, true);
       }
     }
-    for (int e = tid; e < R * cx; e += NT) {
+    for (int e = tid; e < R * cx; e += BT) {
       const int r = e / cx, c = e % cx;
       cp_async<16>(sX + r * T_BXLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * c, true);
     }
@@ -1148,7 +1150,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   };
   for (int s = 0; s <= ns; ++s) {  // W1 rows (+ slots): the first commit group
     const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP) + M.w_off[1] + (int64_t)u0 * C;
-    for (int e = tid; e < nu * C / 4; e += NT) cp_async<16>(sW1 + s * T_BU * C + 4 * e, src + 4 * e, true);
+    for (int e = tid; e < nu * C / 4; e += BT) cp_async<16>(sW1 + s * T_BU * C + 4 * e, src + 4 * e, true);
   }
   cp_commit();
   const int nstg = min(S, ng);
@@ -1160,7 +1162,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   if (a_ready) {
     if (nstg == 2) cp_wait<1>(); else cp_wait<0>();
     __syncthreads();
-    m1t_stage_xT(Ah, Al, stg + (1 + ns) * T_BK * T_BWLD, 0, R, min(T_BK, D - kt0 * T_BK));
+    m1t_stage_xT(Ah, Al, stg + (1 + ns) * T_BK * T_BWLD, 0, R, min(T_BK, D - kt0 * T_BK), BT);
   }
   pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
   PK_TRACE(1);
@@ -1169,7 +1171,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const bool owner = (kt0 == 0 && utile == 0);
   int bad = INT_MAX;
   const int64_t bstr = (int64_t)M.max_rows * C;
-  for (int e = tid; e < R * C; e += NT) {
+  for (int e = tid; e < R * C; e += BT) {
     const int c = e % C;
     const float* pp = M.Z[1] + e;
     float z = 0.f;
@@ -1189,7 +1191,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   if (owner && bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   __syncthreads();
   PK_TRACE(8);
-  for (int r0 = 0; r0 < R; r0 += NT / 8) {  // 8 lanes per row, every warp busy
+  for (int r0 = 0; r0 < R; r0 += BT / 8) {  // 8 lanes per row, every warp busy
     const int r = r0 + (tid >> 3);
     xent_row8(sL + min(r, R - 1) * LDL, C, ylab[min(r, R - 1)], R, r < R,
               owner && r < R ? M.rowloss + r : nullptr);
@@ -1213,11 +1215,11 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   }
   // ---- dZ0[:, units] = (dZ1 · W1[units, :]ᵀ) ⊙ act'(Z0, A0) ----------------
   {
-    constexpr int PER = T_MAXR * T_BU / NT;  // elements per thread (<= 16)
+    constexpr int PER = (T_MAXR * T_BU + BT - 1) / BT;  // elements per thread
     float zr[PER], ar[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // every Z0/A0 load in flight at once
-      const int e = tid + i * NT, r = e / T_BU, j = e % T_BU;
+      const int e = tid + i * BT, r = e / T_BU, j = e % T_BU;
       const bool ok = e < RP * T_BU && r < R && j < nu;
       const int64_t g = (int64_t)r * H + u0 + j;
       zr[i] = ok ? M.Z[0][g] : 0.f;
@@ -1225,14 +1227,14 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // park Z0 / A0 in shared memory (own elements)
-      const int e = tid + i * NT;
+      const int e = tid + i * BT;
       if (e < RP * T_BU) {
         sdZ[e] = zr[i];
         sA0[e] = ar[i];
       }
     }
 #pragma unroll 1
-    for (int e = tid; e < RP * T_BU; e += NT) {  // one rolled body, one act' switch
+    for (int e = tid; e < RP * T_BU; e += BT) {  // one rolled body, one act' switch
       const int r = e / T_BU, j = e % T_BU;
       float v = 0.f;
       if (r < R && j < nu) {
@@ -1251,40 +1253,41 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const int fault = ctl->fault_grad;
   bool badW0 = false, badW1 = false, badb1 = false, badb0 = false;
   // ---- stream the group's input tiles, warp-specialised -------------------
-  //   warps 0-3 (epilogue): TMEM gradient → optimizer against the resident W0
+  //   warps 0-7 (epilogue): TMEM gradient → optimizer against the resident W0
   //                         tile → Pn/Sn; frees the TMEM buffer and the stage
-  //   warps 4-6 (producers): Xᵀ / dZ0 hi-lo staging per 32-row chunk, the
+  //   warps 8-10 (producers): Xᵀ / dZ0 hi-lo staging per 32-row chunk, the
   //                         cp.async of the next input tile
-  //   warp 7 lane 0 (MMA):  12 tcgen05.mma per chunk into TMEM buffer i & 1
+  //   warp 11 lane 0 (MMA): 12 tcgen05.mma per chunk into TMEM buffer i & 1
   // so tile i's optimizer epilogue overlaps tile i+1's staging and MMAs.
-  // mbarriers: 4 afull (count 3), 5 aempty, 6/7 tfull, 8/9 tempty (count 4),
-  // 10/11 sfree (count 4)
+  // mbarriers: 4 afull (count 3), 5 aempty, 6/7 tfull, 8/9 tempty (count 8),
+  // 10/11 sfree (count 8)
   const uint32_t idesc = umma::idesc_tf32(T_BK, T_BU, false, false);
   cp_wait<0>();  // the prologue's stages (issued by every thread) have landed
   if (tid == 32) {
     umma::mbar_init(&bar[4], 3);
     umma::mbar_init(&bar[5], 1);
-    for (int j = 6; j < 10; ++j) umma::mbar_init(&bar[j], j < 8 ? 1 : 4);
-    umma::mbar_init(&bar[10], 4);
-    umma::mbar_init(&bar[11], 4);
+    for (int j = 6; j < 10; ++j) umma::mbar_init(&bar[j], j < 8 ? 1 : 8);
+    umma::mbar_init(&bar[10], 8);
+    umma::mbar_init(&bar[11], 8);
     umma::mbar_fence_init();
   }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  if (warp < 4) {
+  if (warp < 8) {
     // -------------------------------------------------------------- epilogue
-    const int k = 32 * warp + lane;
+    // warp w: TMEM lane quarter w % 4 (input rows k), column half w / 4
+    const int k = 32 * (warp & 3) + lane, ch16 = (warp >> 2) * 16;
     for (int i = 0; i < ng; ++i) {
       const int t = i & 1, st = i % S;
       const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
       umma::mbar_wait(&bar[6 + t], (uint32_t)((i >> 1) & 1));
       umma::fence_after();
-      float g[32];
+      float g[16];
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
+      for (int c8 = 0; c8 < 2; ++c8) {
         float v[8];
-        umma::tmem_ld8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(t * T_BU + 8 * c8), v);
+        umma::tmem_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(t * T_BU + ch16 + 8 * c8), v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[8 * c8 + j] = v[j];
       }
@@ -1297,22 +1300,18 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       if (i == min(1, ng - 1)) PK_TRACE(14);
       const float* sW = stg + st * SF;
       if (k < nk) {
-        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0;
-        const float* row = sW + k * T_BWLD;
+        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + ch16;
+        const float* row = sW + k * T_BWLD + ch16;
         // one rolled quad loop, one optimizer body (nu % 4 == 0)
 #pragma unroll 1
-        for (int qd = 0; qd < 8; ++qd) {
-          if (4 * qd >= nu) break;
+        for (int qd = 0; qd < 4; ++qd) {
+          if (ch16 + 4 * qd >= nu) break;
           float4 gq;
           switch (qd) {  // registers cannot be indexed dynamically: select
             case 0: gq = make_float4(g[0], g[1], g[2], g[3]); break;
             case 1: gq = make_float4(g[4], g[5], g[6], g[7]); break;
             case 2: gq = make_float4(g[8], g[9], g[10], g[11]); break;
-            case 3: gq = make_float4(g[12], g[13], g[14], g[15]); break;
-            case 4: gq = make_float4(g[16], g[17], g[18], g[19]); break;
-            case 5: gq = make_float4(g[20], g[21], g[22], g[23]); break;
-            case 6: gq = make_float4(g[24], g[25], g[26], g[27]); break;
-            default: gq = make_float4(g[28], g[29], g[30], g[31]); break;
+            default: gq = make_float4(g[12], g[13], g[14], g[15]); break;
           }
           if (fault == 2) gq = make_float4(NAN, NAN, NAN, NAN);
           badW0 |= !finite(gq.x) | !finite(gq.y) | !finite(gq.z) | !finite(gq.w);
@@ -1333,9 +1332,9 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
                      : "memory");
       if (i == min(1, ng - 1)) PK_TRACE(15);
     }
-  } else if (warp < 7) {
+  } else if (warp < 11) {
     // ------------------------------------------------------------- producers
-    const int pt = tid - 128;
+    const int pt = tid - 256;
     constexpr int NP3 = 96;
     auto issue_p = [&](int i) {  // input tile i of the group → stage i % S
       const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
@@ -1445,7 +1444,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   //      of the unit tile is updated by the tile's group gi ≡ e (mod ngr)
   {
     const int gi = kt0 / G, ngr = (cdiv_d(D, T_BK) + G - 1) / G;
-    for (int e = gi + ngr * tid; e < nu * C; e += ngr * NT) {
+    for (int e = gi + ngr * tid; e < nu * C; e += ngr * BT) {
       const int j = e / C, c = e % C;
       float g = 0.f;
       for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * LDL + c], g);
@@ -1460,7 +1459,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       if (ns >= 2) Sn[NP + i] = s1;
     }
     if (utile == 0) {
-      for (int c = gi + ngr * tid; c < C; c += ngr * NT) {
+      for (int c = gi + ngr * tid; c < C; c += ngr * BT) {
         float g = 0.f;
         for (int r = 0; r < R; ++r) g += sL[r * LDL + c];
         if (fault == 1) g = NAN;
@@ -1473,7 +1472,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
         if (ns >= 2) Sn[NP + i] = s1;
       }
     }
-    for (int j = gi + ngr * tid; j < nu; j += ngr * NT) {
+    for (int j = gi + ngr * tid; j < nu; j += ngr * BT) {
       float g = 0.f;
       for (int r = 0; r < R; ++r) g += sdZ[r * T_BU + j];
       if (fault == 3) g = NAN;

@@ -27,6 +27,7 @@ struct Phase {
   int cs = 1;              // thread-block cluster size (k_m1t_fwd)
   int stages = 1;          // k_m1t_bwd input-tile stages
   int gsize = 1;           // k_m1t_bwd input tiles per group
+  int nt = pk::NT;         // threads per CTA
 };
 
 struct pk_pack {
@@ -290,6 +291,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   Phase tf, tb;    // tensor-core one-hidden-layer members (train only)
   tf.special = 3;
   tb.special = 4;
+  tb.nt = pk::T_BWD_NT;
   // k_m1t_fwd: one cluster (= all input splits) per unit tile.  k_m1t_bwd: a
   // CTA per (unit tile, group of G input tiles), G sized for ~one wave; two
   // input-tile stages in flight when every member's shared memory allows.
@@ -485,7 +487,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ph.ntiles);
-    cfg.blockDim = dim3(pk::NT);
+    cfg.blockDim = dim3(ph.nt);
     cfg.dynamicSmemBytes = ph.smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
