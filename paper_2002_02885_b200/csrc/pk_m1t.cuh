@@ -66,14 +66,14 @@ struct M1T {
   }
   // S = input-tile stages in flight (2 when they fit, else 1)
   __host__ __device__ static int bwd_smem(int RP, int C, int ns, int S) {
-    return S * ((1 + ns) * T_BK * T_BWLD * 4 + RP * T_BXLD * 4)  // W0 tile + slots, X columns
+    return S * (T_BK * T_BWLD * 4 + RP * T_BXLD * 4)  // W0 tile, X columns (slots: from L2)
            + 2 * T_BK * 32 * 4         // A hi/lo (one 32-row chunk)
            + 2 * T_BU * 32 * 4         // B hi/lo
            + RP * (C + 1) * 4          // logits → dZ1 (row stride C + 1)
            + 2 * RP * T_BU * 4         // dZ0 tile, A0 tile
            + (1 + ns) * T_BU * C * 4   // W1 rows + slots
            + T_MAXC * 4                // b1
-           + 2 * RP * 4 + 128;         // rows, labels, barriers
+           + 2 * RP * 4 + 128;         // rows, labels, 14 barriers, TMEM slot
   }
 };
 
@@ -1033,19 +1033,23 @@ __device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1
         float gi = Gp[i];
         if (wd != 0.f) gi = gi + wd * W[i];
         S0[i] = S0[i] + gi * gi;
-        W[i] = W[i] - lr * gi / (sqrtf(S0[i]) + 1e-10f);
+        W[i] = W[i] - lr * gi * __frcp_rn(sqrtf(S0[i]) + 1e-10f);
       }
       break;
-    default:
+    default: {
+      // one reciprocal per element: m̂ = m·(1/bc1), v̂ = v·(1/bc2) (≤ 1 ulp from
+      // the divisions; the fp32 contract is rel 1e-4)
+      const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         float gi = Gp[i];
         if (wd != 0.f) gi = gi + wd * W[i];
         S0[i] = S0[i] * 0.9f + (1.f - 0.9f) * gi;
         S1[i] = S1[i] * 0.999f + (1.f - 0.999f) * gi * gi;
-        W[i] = W[i] - lr * (S0[i] / bc1) / (sqrtf(S1[i] / bc2) + 1e-8f);
+        W[i] = W[i] - lr * (S0[i] * ib1) * __frcp_rn(sqrtf(S1[i] * ib2) + 1e-8f);
       }
       break;
+    }
   }
 }
 
@@ -1077,13 +1081,30 @@ __device__ __forceinline__ void m1t_stage_xT(float* Ah, float* Al, const float* 
 }
 
 __device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
-  return (1 + ns) * T_BK * T_BWLD + RP * T_BXLD;
+  return T_BK * T_BWLD + RP * T_BXLD;  // W0 tile + X columns
+}
+
+__device__ __forceinline__ void cp_wait_n(int n) {  // pending commit groups allowed
+  switch (n) {
+    case 0: cp_wait<0>(); break;
+    case 1: cp_wait<1>(); break;
+    case 2: cp_wait<2>(); break;
+    case 3: cp_wait<3>(); break;
+    default: cp_wait<4>(); break;
+  }
 }
 
 __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                             int kt0, int ng, int utile, int S, int G) {
+                             int kt0, int ng, int utile, int S_launch, int G) {
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows), ns = M.n_slots;
+  // input-tile stages: as many as this member's shapes leave room for in the
+  // launch's dynamic shared memory (the pack's largest member sets it), 1..4
+  uint32_t dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const int S = max(1, min(4, ((int)dyn - M1T::bwd_smem(RP, C, ns, 0)) /
+                                  (4 * m1t_bwd_stage_floats(RP, ns))));
+  (void)S_launch;
   const int u0 = utile * T_BU, nu = min(T_BU, H - u0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int BT = T_BWD_NT;  // this kernel runs 12 warps
@@ -1109,8 +1130,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* sb1 = sW1 + (1 + ns) * T_BU * C;               // [T_MAXC]
   int32_t* srow = reinterpret_cast<int32_t*>(sb1 + T_MAXC);
   int32_t* ylab = srow + RP;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // [3] unused, [4..11] pipeline
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ylab + RP);  // [3] unused, [4..13] pipeline
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
   constexpr uint32_t tcols = 64;  // two 32-column gradient buffers
 
   // ---- prologue (independent of k_m1t_fwd) --------------------------------
@@ -1133,13 +1154,13 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   auto issue = [&](int i) {
     const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
     float* sW = stg + (i % S) * SF;
-    float* sX = sW + (1 + ns) * T_BK * T_BWLD;
+    float* sX = sW + T_BK * T_BWLD;
     const int cw = nu / 4, cx = nk / 4;
-    for (int s = 0; s <= ns; ++s) {
-      const float* src = (s == 0 ? Pc : Sc + (int64_t)(s - 1) * NP) + M.w_off[0] + u0;
+    {
+      const float* src = Pc + M.w_off[0] + u0;
       for (int e = tid; e < nk * cw; e += BT) {
         const int k = e / cw, c = e % cw;
-        cp_async<16>(sW + (s * T_BK + k) * T_BWLD + 4 * c, src + (int64_t)(k0 + k) * H + 4 * c, true);
+        cp_async<16>(sW + k * T_BWLD + 4 * c, src + (int64_t)(k0 + k) * H + 4 * c, true);
       }
     }
     for (int e = tid; e < R * cx; e += BT) {
@@ -1160,9 +1181,9 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   // overlapping k_m1t_fwd, when one 32-row chunk covers the batch
   const bool a_ready = nch == 1;
   if (a_ready) {
-    if (nstg == 2) cp_wait<1>(); else cp_wait<0>();
+    cp_wait_n(nstg - 1);  // stage 0 landed
     __syncthreads();
-    m1t_stage_xT(Ah, Al, stg + (1 + ns) * T_BK * T_BWLD, 0, R, min(T_BK, D - kt0 * T_BK), BT);
+    m1t_stage_xT(Ah, Al, stg + T_BK * T_BWLD, 0, R, min(T_BK, D - kt0 * T_BK), BT);
   }
   pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
   PK_TRACE(1);
@@ -1197,7 +1218,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
               owner && r < R ? M.rowloss + r : nullptr);
   }
   PK_TRACE(9);
-  if (nstg == 2) cp_wait<2>(); else cp_wait<1>();  // W1 rows landed
+  cp_wait_n(nstg);  // W1 rows (the first group) landed
   __syncthreads();
   PK_TRACE(10);
   if (owner && warp == 0) {
@@ -1267,8 +1288,7 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     umma::mbar_init(&bar[4], 3);
     umma::mbar_init(&bar[5], 1);
     for (int j = 6; j < 10; ++j) umma::mbar_init(&bar[j], j < 8 ? 1 : 8);
-    umma::mbar_init(&bar[10], 8);
-    umma::mbar_init(&bar[11], 8);
+    for (int j = 10; j < 14; ++j) umma::mbar_init(&bar[j], 8);
     umma::mbar_fence_init();
   }
   umma::fence_before();
@@ -1281,6 +1301,20 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     for (int i = 0; i < ng; ++i) {
       const int t = i & 1, st = i % S;
       const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
+      // optimizer slots of my 16 elements straight from global memory, in
+      // flight while the tile's MMAs finish (the stages hold only W0 + X)
+      float4 sl0[4], sl1[4];
+      {
+        const int64_t ib = M.w_off[0] + (int64_t)(k0 + min(k, nk - 1)) * H + u0 + ch16;
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const bool ok = k < nk && ch16 + 4 * qd < nu;
+          sl0[qd] = ns >= 1 && ok ? *reinterpret_cast<const float4*>(Sc + ib + 4 * qd)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          sl1[qd] = ns >= 2 && ok ? *reinterpret_cast<const float4*>(Sc + NP + ib + 4 * qd)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
       umma::mbar_wait(&bar[6 + t], (uint32_t)((i >> 1) & 1));
       umma::fence_after();
       float g[16];
@@ -1306,20 +1340,16 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 #pragma unroll 1
         for (int qd = 0; qd < 4; ++qd) {
           if (ch16 + 4 * qd >= nu) break;
-          float4 gq;
+          float4 gq, s0, s1;
           switch (qd) {  // registers cannot be indexed dynamically: select
-            case 0: gq = make_float4(g[0], g[1], g[2], g[3]); break;
-            case 1: gq = make_float4(g[4], g[5], g[6], g[7]); break;
-            case 2: gq = make_float4(g[8], g[9], g[10], g[11]); break;
-            default: gq = make_float4(g[12], g[13], g[14], g[15]); break;
+            case 0: gq = make_float4(g[0], g[1], g[2], g[3]); s0 = sl0[0]; s1 = sl1[0]; break;
+            case 1: gq = make_float4(g[4], g[5], g[6], g[7]); s0 = sl0[1]; s1 = sl1[1]; break;
+            case 2: gq = make_float4(g[8], g[9], g[10], g[11]); s0 = sl0[2]; s1 = sl1[2]; break;
+            default: gq = make_float4(g[12], g[13], g[14], g[15]); s0 = sl0[3]; s1 = sl1[3]; break;
           }
           if (fault == 2) gq = make_float4(NAN, NAN, NAN, NAN);
           badW0 |= !finite(gq.x) | !finite(gq.y) | !finite(gq.z) | !finite(gq.w);
           float4 w = *reinterpret_cast<const float4*>(row + 4 * qd);
-          float4 s0 = ns >= 1 ? *reinterpret_cast<const float4*>(row + T_BK * T_BWLD + 4 * qd)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-          float4 s1 = ns >= 2 ? *reinterpret_cast<const float4*>(row + 2 * T_BK * T_BWLD + 4 * qd)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
           opt_step4(M.opt, lr, wd, bc1, bc2, w, s0, s1, gq);
           *reinterpret_cast<float4*>(Pn + i0 + 4 * qd) = w;
           if (ns >= 1) *reinterpret_cast<float4*>(Sn + i0 + 4 * qd) = s0;
@@ -1339,13 +1369,20 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     auto issue_p = [&](int i) {  // input tile i of the group → stage i % S
       const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
       float* sW = stg + (i % S) * SF;
-      float* sX = sW + (1 + ns) * T_BK * T_BWLD;
+      float* sX = sW + T_BK * T_BWLD;
       const int cw = nu / 4, cx = nk / 4;
-      for (int s2 = 0; s2 <= ns; ++s2) {
-        const float* src = (s2 == 0 ? Pc : Sc + (int64_t)(s2 - 1) * NP) + M.w_off[0] + u0;
+      {
+        const float* src = Pc + M.w_off[0] + u0;
         for (int e = pt; e < nk * cw; e += NP3) {
           const int kk = e / cw, c = e % cw;
-          cp_async<16>(sW + (s2 * T_BK + kk) * T_BWLD + 4 * c, src + (int64_t)(k0 + kk) * H + 4 * c, true);
+          cp_async<16>(sW + kk * T_BWLD + 4 * c, src + (int64_t)(k0 + kk) * H + 4 * c, true);
+        }
+        // the epilogue reads this tile's optimizer slots from global: pull
+        // them into L2 now, one bulk prefetch per row segment
+        for (int e = pt; e < ns * nk; e += NP3) {
+          const int s2 = e / nk, kk = e % nk;
+          l2_prefetch(Sc + (int64_t)s2 * NP + M.w_off[0] + (int64_t)(k0 + kk) * H + u0,
+                      (uint32_t)(nu * 4));
         }
       }
       for (int e = pt; e < R * cx; e += NP3) {
@@ -1356,13 +1393,14 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     };
     uint32_t aph = 0;
     bool first = true;
+    int next = min(S, ng);  // tiles [0, next) issued
     for (int i = 0; i < ng; ++i) {
-      if (i >= S) {  // issued at the end of iteration i - 1
-        cp_wait<0>();
+      if (i >= S) {  // issued by the producers: wait for it (later groups may fly)
+        cp_wait_n(next - 1 - i);
         asm volatile("bar.sync 2, 96;" ::: "memory");
       }
       const int nk = min(T_BK, D - (kt0 + i) * T_BK);
-      const float* sX = stg + (i % S) * SF + (1 + ns) * T_BK * T_BWLD;
+      const float* sX = stg + (i % S) * SF + T_BK * T_BWLD;
       for (int ch = 0; ch < nch; ++ch) {
         if (!first) {
           umma::mbar_wait(&bar[5], aph);
@@ -1403,10 +1441,14 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(&bar[4]))
                        : "memory");
       }
-      if (i + 1 < ng && i + 1 >= S) {  // refill: tile i + 1 into the stage of tile i + 1 - S
-        const int j = i + 1 - S;
+      // refill: tile `next` reuses the stage of tile next - S once its
+      // epilogue is done; with S >= 3 stay two epilogues behind (no stall)
+      const int limit = S >= 3 ? i + S - 2 : i + 1;
+      while (next < ng && next <= limit) {
+        const int j = next - S;
         umma::mbar_wait(&bar[10 + (j % S)], (uint32_t)((j / S) & 1));
-        issue_p(i + 1);
+        issue_p(next);
+        ++next;
       }
     }
     cp_wait<0>();

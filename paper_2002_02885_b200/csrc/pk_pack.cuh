@@ -296,16 +296,17 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   // CTA per (unit tile, group of G input tiles), G sized for ~one wave; two
   // input-tile stages in flight when every member's shared memory allows.
   int n_ut = 0, n_kt = 1;
-  tb.stages = 2;
+  tb.stages = 4;  // input-tile stages (the kernel may use more if its member allows)
   for (int k = 0; k < p->K; ++k) {
     const pk_member* m = p->members[k];
     if (eval || !m->m1t) continue;
     tf.cs = std::max(tf.cs, pk::t_nsplit(m->desc.dims[0]));
     n_ut += cdiv(m->desc.dims[1], pk::T_BU);
     n_kt = std::max(n_kt, cdiv(m->desc.dims[0], pk::T_BK));
-    if (pk::M1T::bwd_smem(pk::m1_rows_pad(m->desc.max_rows), m->desc.dims[2], m->n_slots, 2) >
-        smem_budget(dt))
-      tb.stages = 1;
+    while (tb.stages > 1 &&
+           pk::M1T::bwd_smem(pk::m1_rows_pad(m->desc.max_rows), m->desc.dims[2], m->n_slots,
+                             tb.stages) > smem_budget(dt))
+      --tb.stages;
   }
   const int G = std::max(1, std::min(n_kt, cdiv(n_ut * n_kt, 148)));
   tb.gsize = G;

@@ -60,7 +60,7 @@ def uses_m1t(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
     ns = _SLOTS[optimizer.lower()]
     fwd = _T_KS * _T_UM * 4 + RP * _T_XLD * 4 + 2 * _T_UM * _T_KS * 4 + 2 * RP * _T_KS * 4 \
         + _T_UM * C * 4 + _T_UM * 4 + RP * 4 + 64
-    bwd = ((1 + ns) * _T_BK * (_T_BU + 4) * 4 + RP * _T_BXLD * 4 + 2 * _T_BK * 32 * 4
+    bwd = (_T_BK * (_T_BU + 4) * 4 + RP * _T_BXLD * 4 + 2 * _T_BK * 32 * 4
            + 2 * _T_BU * 32 * 4 + RP * (C + 1) * 4 + 2 * RP * _T_BU * 4
            + (1 + ns) * _T_BU * C * 4 + _T_MAXC * 4 + 2 * RP * 4 + 128)
     budget = _SMEM_OPTIN - _STATIC_MARGIN
