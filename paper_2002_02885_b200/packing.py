@@ -252,6 +252,18 @@ class PackedModel:
         dev.write_rows(0, hx[:n], hy[:n])
         return dev
 
+    def _stream_rows(self, rt, gi, ds, idx, buf=0):
+        """Streamed batch rows `idx` of `ds`: one np.take from the host copy in
+        device precision (made once per dataset; float32(x) is what the H2D
+        copy would carry anyway) into the pinned staging buffer, then H2D."""
+        x, y = rt.host_rows_source(ds)
+        n = len(idx)
+        dev, hx, hy = _stream_staging(self, rt, (gi, buf), n, ds.dim)
+        np.take(x, idx, axis=0, out=hx[:n])
+        np.take(y, idx, out=hy[:n])
+        dev.write_rows_ptr(n, hx, hy)
+        return dev
+
     def input_groups(self):
         """Members partitioned by (dataset, epoch, cursor, batch) (packing.py:121-128)."""
         g: dict = {}
@@ -391,10 +403,11 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache, cu
                                  f"with {bad[0].arch.classes} classes")
         if _rt.input_mode() == "stream":
             # host gather (+ per-sample preprocess) into pinned staging, H2D
-            x = ds.features[idx]
             if preprocess_spec is not None and preprocess_spec.stages:
-                x = preprocess(preprocess_spec, x, idx, ds.dataset_id, cache)
-            src = packed._stream(rt, gi, x, ds.labels[idx], buf)
+                x = preprocess(preprocess_spec, ds.features[idx], idx, ds.dataset_id, cache)
+                src = packed._stream(rt, gi, x, ds.labels[idx], buf)
+            else:  # gather straight from a device-precision host copy into pinned memory
+                src = packed._stream_rows(rt, gi, ds, idx, buf)
             order, pos = None, 0
         else:
             if preprocess_spec is not None and preprocess_spec.stages:

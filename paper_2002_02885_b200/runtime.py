@@ -18,6 +18,10 @@ from . import _lib as L
 
 _RUNTIMES: dict = {}
 _DEFAULT = {"device": None, "dtype": None, "inputs": None}
+# environment defaults, read once (the step path asks for them every call)
+_ENV = {"inputs": os.environ.get("PACKTRAIN_INPUTS", "resident"),
+        "device": int(os.environ.get("PACKTRAIN_DEVICE", "0")),
+        "dtype": os.environ.get("PACKTRAIN_PRECISION", "f32")}
 
 
 def set_input_mode(mode: str):
@@ -31,7 +35,7 @@ def set_input_mode(mode: str):
 
 
 def input_mode() -> str:
-    return _DEFAULT["inputs"] or os.environ.get("PACKTRAIN_INPUTS", "resident")
+    return _DEFAULT["inputs"] or _ENV["inputs"]
 
 
 def set_device(device: int):
@@ -49,11 +53,11 @@ def set_precision(dtype: str):
 def default_device() -> int:
     if _DEFAULT["device"] is not None:
         return _DEFAULT["device"]
-    return int(os.environ.get("PACKTRAIN_DEVICE", "0"))
+    return _ENV["device"]
 
 
 def default_precision() -> str:
-    return _DEFAULT["dtype"] or os.environ.get("PACKTRAIN_PRECISION", "f32")
+    return _DEFAULT["dtype"] or _ENV["dtype"]
 
 
 def runtime(device: int | None = None, dtype: str | None = None) -> "Runtime":
@@ -130,6 +134,18 @@ class Runtime:
             self._datasets[key] = got
         return got
 
+    def host_rows_source(self, ds):
+        """(features in device precision, int32 labels) host copies of `ds` for
+        streamed gathers, made once per dataset."""
+        key = ("rows", ds.dataset_id, id(ds.features), ds.features.shape)
+        got = self._datasets.get(key)
+        if got is None:
+            got = (np.ascontiguousarray(ds.features,
+                                        dtype=np.float64 if self.dtype == "f64" else np.float32),
+                   np.ascontiguousarray(ds.labels, dtype=np.int32))
+            self._datasets[key] = got
+        return got
+
     def host_order(self, dataset_id: str, n: int, epoch: int, make) -> np.ndarray:
         key = (dataset_id, n, epoch)
         o = self._host_orders.get(key)
@@ -169,6 +185,16 @@ class DeviceDataset:
         ptr = C.c_void_p()
         rt.check(rt.lib.pk_dataset_create(rt.ptr, self.n, self.dim, C.byref(ptr)))
         self.ptr = ptr
+
+    def write_rows_ptr(self, rows: int, x, y):
+        """write_rows(0, x[:rows], y[:rows]) for contiguous pinned buffers,
+        with their ctypes pointers cached."""
+        key = (x.ctypes.data, y.ctypes.data)
+        ptrs = getattr(self, "_wr_ptrs", None)
+        if ptrs is None or ptrs[0] != key:
+            ptrs = (key, C.c_void_p(key[0]), C.c_void_p(key[1]))
+            self._wr_ptrs = ptrs
+        self.rt.check(self.rt.lib.pk_dataset_write_rows(self.ptr, 0, int(rows), ptrs[1], ptrs[2]))
 
     def write_rows(self, row0: int, x, y):
         """Async H2D of rows already in device precision (x) / int32 (y);
