@@ -314,8 +314,13 @@ def _b200(args):
         prof.append(phases)
     phases = []
     plan_b = _phase_plan(wl, 8 if args.precision == "f64" else 4)
+    T = "<double>" if args.precision == "f64" else "<float>"
+    special = {17: "k_mlp1_fwd", 18: "k_mlp1_bwd", 19: "k_m1t_fwd", 20: "k_m1t_bwd",
+               21: "k_m1s_fwd", 22: "k_m1c_fwd"}
     for i, (kind, layer, ctas, _) in enumerate(prof[0]):
         label, kern, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind]}{layer}", "?", 0)
+        if kind in special:  # the kernel the runtime actually launched
+            kern = special[kind] + T
         phases.append({"phase": label, "kernel": kern, "ctas": ctas,
                        "ms": statistics.median(p[i][3] for p in prof), "bytes": nbytes})
     top = max(phases, key=lambda p: p["ms"])

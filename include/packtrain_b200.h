@@ -161,8 +161,10 @@ int pk_pack_eval(pk_pack* p, const pk_dataset* data, const pk_order* order,
                  int64_t pos, int64_t rows, double* losses, pk_status* st);
 /* profiling: run one real step un-graphed with CUDA events around every
  * phase (state advances as for pk_pack_step).  Arrays hold
- * pk_pack_launches_per_step(p) entries: device ms, kind (0 forward, 1 head,
- * 2 backward+update, 3 finalize), layer index, and tile (CTA) count. */
+ * pk_pack_launches_per_step(p) entries: device ms, kind (a k_phase tile kind
+ * 0..4, or 16 + id for the fused kernels: 17 k_mlp1_fwd, 18 k_mlp1_bwd,
+ * 19 k_m1t_fwd, 20 k_m1t_bwd, 21 k_m1s_fwd, 22 k_m1c_fwd), layer index, and
+ * tile (CTA) count. */
 int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* phase_ms,
                          int32_t* phase_kind, int32_t* phase_layer,
                          int32_t* phase_ctas, double* losses, pk_status* st);

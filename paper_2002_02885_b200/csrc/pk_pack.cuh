@@ -385,7 +385,8 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     // the largest cluster size whose clusters all fit co-resident (one
     // wave); never below what TMEM / smem per CTA allow
     int CS = cs_lo;
-    for (int cs = std::min(ns_max, pk::T_MAXCS); cs > cs_lo; --cs) {
+    bool one_wave = false;
+    for (int cs = std::min(ns_max, pk::T_MAXCS); cs >= cs_lo; --cs) {
       if (dt != PK_F32) break;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cs * n_tiles);
@@ -402,12 +403,15 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
       if (cudaOccupancyMaxActiveClusters(&nc, pk::k_m1c_fwd<float>, &cfg) == cudaSuccess &&
           nc >= n_tiles) {
         CS = cs;
+        one_wave = true;
         break;
       }
     }
     // one split per CTA fits in a wave: the one-shot split-K cluster forward
-    // (same arithmetic, no streaming pipeline) is the lower-latency choice
-    if (CS < ns_max && sm <= smem_budget(dt)) {
+    // (same arithmetic, no streaming pipeline) is the lower-latency choice.
+    // No cluster size fits a wave (many unit tiles): one streaming CTA per
+    // tile (k_m1s_fwd, below) instead.
+    if (one_wave && CS < ns_max && sm <= smem_budget(dt)) {
       tf.host.clear();
       for (int k = 0; k < p->K; ++k)
         if (p->members[k]->m1t)
@@ -421,7 +425,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   // many clusters (several waves): stream the input dimension instead, one CTA
   // per unit tile, when every tensor member's streaming smem fits
   if (!eval && tf.special == 3 && (int)tf.host.size() > 2 * 148 &&
-      !(fv && !strcmp(fv, "split"))) {
+      !(fv && !strcmp(fv, "split"))) {  // (also reached when no m1c cluster size fits a wave)
     bool fits = true;
     int sm = 0;
     for (int k = 0; k < p->K; ++k) {
@@ -893,7 +897,8 @@ extern "C" int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* pha
     cudaEventElapsedTime(&ms, ev[j], ev[j + 1]);
     const Phase& ph = p->train[idx[j]];
     if (phase_ms) phase_ms[j] = ms;
-    if (phase_kind) phase_kind[j] = ph.kind;
+    // special (fused / tensor-path) kernels report 16 + their id
+    if (phase_kind) phase_kind[j] = ph.special ? 16 + ph.special : ph.kind;
     if (phase_layer) phase_layer[j] = ph.layer;
     if (phase_ctas) phase_ctas[j] = ph.ntiles;
   }
