@@ -318,7 +318,7 @@ def _b200(args):
     special = {17: "k_mlp1_fwd", 18: "k_mlp1_bwd", 19: "k_m1t_fwd", 20: "k_m1t_bwd",
                21: "k_m1s_fwd", 22: "k_m1c_fwd"}
     for i, (kind, layer, ctas, _) in enumerate(prof[0]):
-        label, kern, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind]}{layer}", "?", 0)
+        label, kern, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind] if kind < len(TK) else kind}{layer}", "?", 0)
         if kind in special:  # the kernel the runtime actually launched
             kern = special[kind] + T
         phases.append({"phase": label, "kernel": kern, "ctas": ctas,
