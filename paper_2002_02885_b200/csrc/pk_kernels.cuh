@@ -108,6 +108,8 @@ struct Tile {
 };
 
 constexpr int kInlineFeeds = 32;  // packs up to this K take inline step descriptors
+constexpr int kInlineTiles = 160; // phases up to this many CTAs carry their tiles inline
+constexpr int kInlineMems = 4;    // packs up to this K carry member descriptors inline
 
 struct StepHdr {
   int32_t K;
@@ -142,7 +144,21 @@ struct PhaseArgs {
   // the members' control blocks, inline
   int32_t all_tensor;
   MemberCtl* ctl_in[kInlineFeeds];
+  // static per phase / pack, inline when small: a CTA's first reads hit the
+  // constant bank instead of dependent global loads
+  int32_t tin, min_;
+  Tile tiles_in[kInlineTiles];
+  MemberDev<T> mems_in[kInlineMems];
 };
+
+template <typename T>
+__device__ __forceinline__ Tile tile_of(const PhaseArgs<T>& P) {
+  return P.tin ? P.tiles_in[blockIdx.x] : P.tiles[blockIdx.x];
+}
+template <typename T>
+__device__ __forceinline__ const MemberDev<T>* mem_of(const PhaseArgs<T>& P, int k) {
+  return P.min_ ? &P.mems_in[k] : P.mems + k;
+}
 
 template <typename T>
 __device__ __forceinline__ FeedDev<T> feed_of(const PhaseArgs<T>& P, int k) {
@@ -1016,7 +1032,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
   PK_TRACE(0);
   pdl_launch();
   if (P.prefetch) prefetch_params(P);
-  const Tile t = P.tiles[blockIdx.x];
+  const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   const bool train = (hdr_of(P).mode == 0);
   if (f.take != 0) {
@@ -1050,14 +1066,14 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
   PK_TRACE(0);
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
-    const Tile t = P.tiles[blockIdx.x];
+    const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
     // the member's descriptor in shared memory: every field read is an LDS,
     // not a global load on the critical path
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
-          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+          reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     if (f.take != 0) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
   } else {
@@ -1074,12 +1090,12 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
   PK_TRACE(0);
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
-    const Tile t = P.tiles[blockIdx.x];
+    const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
-          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+          reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     if (f.take != 0) {
       if (m1_rows_pad(sM.max_rows) == 32 && t_nsplit(sM.dims[0]) * 32 <= 512)
@@ -1101,12 +1117,12 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
   PK_TRACE(0);
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
-    const Tile t = P.tiles[blockIdx.x];
+    const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
-          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+          reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     // m0 = unit tile, n0 = cluster rank (input-split range)
     if (f.take != 0) m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
@@ -1124,13 +1140,13 @@ __global__ void __launch_bounds__(T_BWD_NT, 1) k_m1t_bwd(const __grid_constant__
   PK_TRACE(0);
   pdl_launch();
   if constexpr (sizeof(T) == 4) {
-    const Tile t = P.tiles[blockIdx.x];
+    const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
     // m0 = first input tile, layer = input tiles in the group, n0 = unit tile
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
-          reinterpret_cast<const int32_t*>(P.mems + t.member)[threadIdx.x];
+          reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     if (f.take != 0) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages, P.gsize);
   } else {
@@ -1147,7 +1163,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const __grid_constant__ Phas
   PK_TRACE(0);
   pdl_launch();
   if (P.prefetch) prefetch_params(P);
-  const Tile t = P.tiles[blockIdx.x];
+  const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   if (f.take != 0) m1_fwd_tile<T>(smem_raw, P.mems[t.member], f, t.m0);
   kernel_end(P, true);
@@ -1160,7 +1176,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const __grid_constant__ Phas
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
   pdl_launch();
-  const Tile t = P.tiles[blockIdx.x];
+  const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   if (f.take != 0) {
     const MemberDev<T>& M = P.mems[t.member];

@@ -62,6 +62,7 @@ struct pk_pack {
   cudaGraph_t graph = nullptr;
   std::vector<Node> nodes;
   std::vector<char> h_feeds;  // host FeedDev<T>[K] of the step being launched
+  std::vector<char> h_mems;   // host MemberDev<T>[K] (static)
 };
 
 template <typename T>
@@ -502,6 +503,14 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     cfg.numAttrs = 1;
     a.cs = ph.cs;
     a.stages = ph.stages;
+    if (ph.ntiles <= pk::kInlineTiles) {
+      a.tin = 1;
+      memcpy(a.tiles_in, ph.host.data(), sizeof(Tile) * ph.ntiles);
+    }
+    if (p->K <= pk::kInlineMems) {
+      a.min_ = 1;
+      memcpy(a.mems_in, p->h_mems.data(), sizeof(pk::MemberDev<T>) * p->K);
+    }
     if (p->K <= pk::kInlineFeeds && &phases == &p->train) {
       a.all_tensor = 1;
       for (int k = 0; k < p->K; ++k) {
@@ -595,6 +604,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
       memcpy(hm.data() + i * mdsz, &d, mdsz);
     }
   }
+  p->h_mems = hm;
   build_phases(p, false, p->train);
   build_phases(p, true, p->eval);
   std::vector<Tile> all;
