@@ -147,6 +147,9 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   const int nu4 = (nu + 3) & ~3;
   const bool reducer = true;  // every rank reduces a row subset of the tile
 
+  // the batch's gather index: issue its load first so it flies together with
+  // the parity load below (two cold round trips overlap instead of chaining)
+  const int myrow = tid < R ? (int32_t)feed_row(f, tid) : 0;
   // 16-byte cp.async (LDGSTS) from every thread: W0 rows first (they do not
   // depend on the batch rows), then W1 / b0 of the tile, then the X rows
   {
@@ -161,7 +164,7 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       for (int e = tid; e < cpr; e += NT) cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
     }
   }
-  for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
+  if (tid < RP) srow[tid] = myrow;  // RP <= 128 < NT
   if (tid == 32) {
     umma::mbar_init(&bar[1], 1);
     umma::mbar_fence_init();
