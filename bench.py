@@ -409,6 +409,10 @@ def _hyperband_b200(R, world, group, precision="f64"):
     # reference's
     prev = runtime.default_precision()
     runtime.set_precision(precision)
+    # context creation + module load for this precision, outside the timing
+    warm = tuner.B200Executor(data.synth_dataset(64, HB["dim"], HB["classes"], seed=1),
+                              hidden=HB["hidden"], seed=HB["seed"])
+    warm.evaluate([tuner.ConfigSpace().config(0), tuner.ConfigSpace().config(1)], 1)
     for strategy in HB["strategies"]:
         ex = tuner.B200Executor(ds, hidden=HB["hidden"], seed=HB["seed"])
         if world > 1:

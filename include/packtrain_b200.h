@@ -43,6 +43,7 @@ extern "C" {
 #define PK_ERR_OOM 4            /* device allocation failed */
 #define PK_ERR_CUDA 5           /* CUDA runtime error */
 #define PK_ERR_STATE 6          /* API misuse (e.g. pending async step) */
+#define PK_SKIPPED 7            /* step status: skipped, an earlier in-flight step failed */
 
 /* enums follow the reference tuples' order (engine.py:21-22) */
 #define PK_ACT_SIGMOID 0

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libpk_b200.so")
 
 PK_MAX_LAYERS = 8
 PK_OK, PK_ERR_ARG, PK_ERR_NONFINITE_VALUE, PK_ERR_NONFINITE_GRAD = 0, 1, 2, 3
-PK_ERR_OOM, PK_ERR_CUDA, PK_ERR_STATE = 4, 5, 6
+PK_ERR_OOM, PK_ERR_CUDA, PK_ERR_STATE, PK_SKIPPED = 4, 5, 6, 7
 PK_F32, PK_F64 = 0, 1
 # enum order = the reference tuples (engine.py:21-22)
 ACT_CODES = {"sigmoid": 0, "leaky_relu": 1, "tanh": 2, "relu": 3}

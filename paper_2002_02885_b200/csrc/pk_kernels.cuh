@@ -125,6 +125,8 @@ struct PhaseArgs {
   const StepHdr* hdr;
   const Tile* tiles;
   int32_t* done;       // CTA-completion counter (last phase)
+  int32_t* halt;       // set by FINALIZE after a failed train step: later
+                       // in-flight train steps skip all work (packed_run)
   char* ring;          // host-mapped results
   int32_t ring_stride;
   int32_t K;
@@ -150,6 +152,11 @@ struct PhaseArgs {
   Tile tiles_in[kInlineTiles];
   MemberDev<T> mems_in[kInlineMems];
 };
+
+template <typename T>
+__device__ __forceinline__ bool halted(const PhaseArgs<T>& P) {
+  return P.halt && hdr_of(P).mode == 0 && *reinterpret_cast<volatile int32_t*>(P.halt) != 0;
+}
 
 template <typename T>
 __device__ __forceinline__ Tile tile_of(const PhaseArgs<T>& P) {
@@ -830,6 +837,18 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
 // FINALIZE for packs whose members all take the tensor path (two affine
 // layers; loss and next Adam corrections already in ctl): one warp, lane =
 // member, the same commit rules via ballots.
+// a train step enqueued behind a failed one did no work: report it skipped,
+// commit nothing (packed_run stops at the failed step's exception)
+template <typename T>
+__device__ __noinline__ void finalize_skipped(const PhaseArgs<T>& P) {
+  int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)hdr_of(P).slot * P.ring_stride);
+  double* losses = reinterpret_cast<double*>(st + 4);
+  for (int k = threadIdx.x; k < P.K; k += blockDim.x) losses[k] = 0.0;
+  if (threadIdx.x == 0) {
+    st[0] = PK_SKIPPED; st[1] = -1; st[2] = -1; st[3] = 0;
+  }
+}
+
 template <typename T>
 __device__ __noinline__ void finalize_fast(const PhaseArgs<T>& P) {
   if (threadIdx.x >= 32) return;
@@ -878,6 +897,7 @@ __device__ __noinline__ void finalize_fast(const PhaseArgs<T>& P) {
   }
   if (k == 0) {
     st[0] = code; st[1] = who; st[2] = idx; st[3] = committed;
+    if (code != PK_OK && P.halt) *P.halt = 1;
   }
 }
 
@@ -958,6 +978,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   __syncthreads();
   if (threadIdx.x == 0 && train) {
     st[0] = s_code; st[1] = s_who; st[2] = s_idx; st[3] = s_comm;
+    if (s_code != PK_OK && P.halt) *P.halt = 1;
   }
 }
 
@@ -1012,7 +1033,8 @@ __device__ __forceinline__ void kernel_end(const PhaseArgs<T>& P, bool train) {
   if (!last) return;
   __threadfence();
   PK_TRACE(6);
-  if (train && P.all_tensor) finalize_fast<T>(P);
+  if (train && halted(P)) finalize_skipped<T>(P);
+  else if (train && P.all_tensor) finalize_fast<T>(P);
   else finalize<T>(P, train);
   PK_TRACE(7);
   if (threadIdx.x == 0) *P.done = 0;
@@ -1035,7 +1057,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   const bool train = (hdr_of(P).mode == 0);
-  if (f.take != 0) {
+  if (f.take != 0 && !halted(P)) {
     const MemberDev<T>& M = P.mems[t.member];
     if ((MASK & KM_FWD) && t.kind == TK_FWD) {
       if (t.m0 < f.take) fwd_tile<T>(smem_raw, M, f, t);
@@ -1075,7 +1097,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
-    if (f.take != 0) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+    if (f.take != 0 && !halted(P)) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
   } else {
     __trap();
   }
@@ -1097,7 +1119,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
-    if (f.take != 0) {
+    if (f.take != 0 && !halted(P)) {
       if (m1_rows_pad(sM.max_rows) == 32 && t_nsplit(sM.dims[0]) * 32 <= 512)
         m1s_fwd_tile_ws(smem_raw, sM, f, t.m0);
       else
@@ -1125,7 +1147,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     // m0 = unit tile, n0 = cluster rank (input-split range)
-    if (f.take != 0) m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+    if (f.take != 0 && !halted(P)) m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
   } else {
     __trap();
   }
@@ -1148,7 +1170,7 @@ __global__ void __launch_bounds__(T_BWD_NT, 1) k_m1t_bwd(const __grid_constant__
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
-    if (f.take != 0) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages, P.gsize);
+    if (f.take != 0 && !halted(P)) m1t_bwd_tile(smem_raw, sM, f, t.m0, t.layer, t.n0, P.stages, P.gsize);
   } else {
     __trap();
   }
@@ -1165,7 +1187,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const __grid_constant__ Phas
   if (P.prefetch) prefetch_params(P);
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
-  if (f.take != 0) m1_fwd_tile<T>(smem_raw, P.mems[t.member], f, t.m0);
+  if (f.take != 0 && !halted(P)) m1_fwd_tile<T>(smem_raw, P.mems[t.member], f, t.m0);
   kernel_end(P, true);
 }
 
@@ -1178,7 +1200,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const __grid_constant__ Phas
   pdl_launch();
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
-  if (f.take != 0) {
+  if (f.take != 0 && !halted(P)) {
     const MemberDev<T>& M = P.mems[t.member];
     m1_bwd_tile<T>(smem_raw, M, f, t.m0, (M.dims[1] + M1_BC - 1) / M1_BC);
   }

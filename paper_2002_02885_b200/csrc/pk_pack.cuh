@@ -63,6 +63,7 @@ struct pk_pack {
   std::vector<Node> nodes;
   std::vector<char> h_feeds;  // host FeedDev<T>[K] of the step being launched
   std::vector<char> h_mems;   // host MemberDev<T>[K] (static)
+  bool halt_dirty = false;    // a failed step set the device halt flag
 };
 
 template <typename T>
@@ -481,6 +482,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     a.feeds = (const FeedDev<T>*)(p->d_blob + sizeof(StepHdr));
     a.tiles = ph.tiles;
     a.done = p->d_done;
+    a.halt = p->d_done + 1;
     a.ring = p->d_ring;
     a.ring_stride = p->ring_stride;
     a.K = p->K;
@@ -753,6 +755,10 @@ extern "C" int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* tic
   int slot;
   int rc = acquire_slot(p, t, &slot);
   if (rc) return rc;
+  if (p->halt_dirty) {  // steps enqueued behind the failure have been skipped
+    CK_CTX(c, cudaMemsetAsync(p->d_done + 1, 0, 4, c->stream));
+    p->halt_dirty = false;
+  }
   if (p->inline_desc) {
     // feeds + header ride in the kernel parameters of the graph's nodes
     p->h_feeds.resize(feed_size(c->dtype) * p->K);
@@ -804,6 +810,7 @@ extern "C" int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* tic
 
 static int read_result(pk_pack* p, int slot, double* losses, pk_status* st) {
   const int32_t* s = reinterpret_cast<const int32_t*>(p->h_ring + (size_t)slot * p->ring_stride);
+  if (s[0] != PK_OK) p->halt_dirty = true;  // cleared before the next launch
   const double* l = reinterpret_cast<const double*>(s + 4);
   if (st) {
     st->code = s[0];

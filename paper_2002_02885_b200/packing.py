@@ -25,7 +25,7 @@ from . import engine
 from . import runtime as _rt
 from .data import Dataset, account_cache, epoch_permutation, preprocess
 from .engine import ComputationGraph
-from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE
+from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE, PK_SKIPPED
 
 CHECKPOINT_MAGIC = b"PKCK"
 CHECKPOINT_VERSION = 1
@@ -434,6 +434,8 @@ def _apply_result(packed: PackedModel, active, plan: _StepPlan, code, who, where
     """Device status → the reference's exceptions and cursor updates
     (packing.py:246-257): a forward error commits nothing; a gradient error
     at member k leaves members before k committed."""
+    if code == PK_SKIPPED:
+        raise PackError("step skipped: an earlier in-flight step failed")
     if code == PK_ERR_NONFINITE_VALUE:
         raise engine.EngineError(
             f"non-finite value at node {_node_name(packed.members[who], where)!r}")
@@ -489,6 +491,58 @@ def _speculate(packed, active, plan, datasets, stop_at_epoch_end, buf):
         return _state_key(packed, nxt, shadow, datasets, stop_at_epoch_end, nplan.dpack), nplan
     except Exception:  # the real call recomputes (and raises) if needed
         return None
+
+
+def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16) -> list:
+    """Up to `max_steps` packed_step calls (reference semantics, packing.py:185-264)
+    with up to `depth` steps in flight on the device: the host plans steps
+    n+1.. from shadow cursors (epoch rolls and finished members exactly as
+    _active_members) and enqueues them while step n runs.  If a step raises
+    (non-finite value / gradient), the device has skipped every later step
+    (halt flag), so the state is exactly the reference's at that exception.
+    Stops early when no member is left; returns the per-step loss dicts."""
+    out = []
+    while len(out) < max_steps:
+        try:
+            active = _active_members(packed, datasets, False)
+        except ReplanNeeded:
+            break
+        shadow = {id(h): (h.cursor.epoch_index, h.cursor.pos, h.cursor.steps_done)
+                  for h in packed.members}
+        chain = []
+        act, curs = active, None
+        while len(chain) < min(depth, max_steps - len(out)):
+            plan = _plan_step(packed, act, datasets, None, None, curs=curs)
+            chain.append((act, plan, plan.dpack.step_async()))
+            # shadow state after this step commits → the next step's members
+            nact, ncurs = [], {}
+            for h in packed.members:
+                ep, pos, steps = shadow[id(h)]
+                if id(h) in plan.takes:
+                    steps += 1
+                    pos += plan.takes[id(h)][1]
+                shadow[id(h)] = (ep, pos, steps)
+                if steps >= h.target_steps:
+                    continue
+                n = datasets[h.dataset_binding].n
+                if pos >= n:
+                    ep, pos = ep + 1, 0
+                    shadow[id(h)] = (ep, pos, steps)
+                ncurs[id(h)] = (ep, pos)
+                nact.append(h)
+            if not nact:
+                break
+            act, curs = nact, ncurs
+        for j, (act, plan, ticket) in enumerate(chain):
+            code, who, where, _, losses = plan.dpack.wait(ticket)
+            if j:  # the reference rolls epochs at the top of each packed_step
+                for h in act:
+                    _roll_if_needed(h, datasets)
+            out.append(_apply_result(packed, act, plan, code, who, where, losses))
+            packed.last_step_stats = {"physical_inputs": plan.physical,
+                                      "groups": plan.n_groups, "driver_batch": plan.driver}
+    packed._spec = None
+    return out
 
 
 def _device_step(packed: PackedModel, active, datasets, preprocess_spec, cache,

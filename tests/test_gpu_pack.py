@@ -620,3 +620,63 @@ def test_tensor_path_ragged_heterogeneous_pack():
     for _ in range(3):
         packing.standalone_step(solo, ds)
     assert _maxdiff(hs[2], solo) == 0.0
+
+
+# ------------------------------------------------- pipelined packed_run --
+
+def _run_pair(ds, steps, depth):
+    arch = packing.MLPArch(40, (24,), 5, "tanh")
+    hs = [packing.make_handle("p0", arch, "adam", 0.01, 16, 23, "t", 1),
+          packing.make_handle("p1", arch, "sgd", 0.05, 16, 40, "t", 2),
+          packing.make_handle("p2", arch, "momentum", 0.02, 12, 31, "t", 3)]
+    return hs, packing.dedup_inputs(packing.pack_models(hs))
+
+
+def test_packed_run_equals_packed_step_loop():
+    """packed_run (16 steps in flight, shadow cursors) reproduces the
+    packed_step loop bit for bit across epoch rolls, ragged batches and members
+    finishing at different steps."""
+    ds = {"t": data.synth_dataset(100, 40, 5, seed=21)}
+    ha, pa = _run_pair(ds, 0, 0)
+    la = []
+    while any(not h.finished for h in ha):
+        la.append(packing.packed_step(pa, ds))
+    hb, pb = _run_pair(ds, 0, 0)
+    lb = packing.packed_run(pb, ds, 1 << 30, depth=16)
+    assert la == lb
+    for a, b in zip(ha, hb):
+        assert _maxdiff(a, b) == 0.0
+        assert (a.cursor.steps_done, a.cursor.epoch_index, a.cursor.pos) == \
+            (b.cursor.steps_done, b.cursor.epoch_index, b.cursor.pos)
+        np.testing.assert_array_equal(a.cursor.samples_used, b.cursor.samples_used)
+        assert a.optimizer.step_counter == b.optimizer.step_counter
+    assert pa.last_step_stats == pb.last_step_stats
+
+
+def test_packed_run_stops_exactly_at_a_failing_step():
+    """A non-finite gradient inside a pipelined run raises at that step; the
+    device skipped every step enqueued behind it, so the state equals the
+    packed_step loop's at the same exception (commit rules packing.py:246-253)."""
+    ds = {"t": data.synth_dataset(100, 40, 5, seed=22)}
+    results = []
+    for mode in ("loop", "run"):
+        hs, pk = _run_pair(ds, 0, 0)
+        for _ in range(3):
+            packing.packed_step(pk, ds)
+        rt = runtime.runtime()
+        hs[1]._device(rt).inject_fault(2)  # member p1's next step: NaN in dW0
+        with pytest.raises(engine.NonFiniteGradient):
+            if mode == "loop":
+                for _ in range(10):
+                    packing.packed_step(pk, ds)
+            else:
+                packing.packed_run(pk, ds, 10, depth=8)
+        # the pack keeps training normally afterwards
+        after = packing.packed_step(pk, ds)
+        results.append((hs, after))
+    (ha, la), (hb, lb) = results
+    assert la == lb
+    for a, b in zip(ha, hb):
+        assert _maxdiff(a, b) == 0.0
+        assert a.cursor.steps_done == b.cursor.steps_done
+        assert a.optimizer.step_counter == b.optimizer.step_counter
