@@ -367,7 +367,7 @@ class _StepPlan:
 
 
 def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache, curs=None,
-               buf=0):
+               buf=0, dpack=None):
     """Host half of a packed step: input groups, batch rows and the per-member
     device feeds (packing.py:206-239).  Reads cursors (or the (epoch, pos)
     overrides in `curs`, for speculation), changes no member state."""
@@ -378,7 +378,8 @@ def _plan_step(packed: PackedModel, active, datasets, preprocess_spec, cache, cu
     for h in active:
         ep, ps = curs[id(h)] if curs is not None else (h.cursor.epoch_index, h.cursor.pos)
         groups.setdefault((h.dataset_binding, ep, ps, h.batch_size), []).append(h)
-    dpack = packed._device_pack(rt)
+    if dpack is None:
+        dpack = packed._device_pack(rt)
     plan.dpack = dpack
     plan.index = index = {id(h): k for k, h in enumerate(packed.members)}
     dpack.clear_feeds()
@@ -511,8 +512,9 @@ def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16) -
                   for h in packed.members}
         chain = []
         act, curs = active, None
+        dpack = packed._device_pack(_rt.runtime())  # synced once per burst
         while len(chain) < min(depth, max_steps - len(out)):
-            plan = _plan_step(packed, act, datasets, None, None, curs=curs)
+            plan = _plan_step(packed, act, datasets, None, None, curs=curs, dpack=dpack)
             chain.append((act, plan, plan.dpack.step_async()))
             # shadow state after this step commits → the next step's members
             nact, ncurs = [], {}

@@ -29,6 +29,7 @@ def main():
     print(f"wall {time.perf_counter() - t0:.2f} s, packed/standalone steps {ex.steps}, "
           f"best {res.best_config.config_id}")
     pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
 
 
 if __name__ == "__main__":
