@@ -190,7 +190,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define PK_TRACE(i)                                         \
   do {                                                      \
-    if (threadIdx.x == 0 && pk_trace_slots) pk_trace_slots[(i)] = gtimer(); \
+    if (threadIdx.x == 0) {                                 \
+      /* volatile: the load may not be hoisted above the tid test */ \
+      unsigned long long* pk_ts_ = *(unsigned long long* volatile*)&pk_trace_slots; \
+      if (pk_ts_) pk_ts_[(i)] = gtimer();                   \
+    }                                                       \
   } while (0)
 
 // ------------------------------------------------------------ PTX glue --

@@ -88,7 +88,7 @@ __device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool li
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int c = q + 8 * i;
-    v[i] = c < C ? z[c] : -INFINITY;
+    v[i] = live && c < C ? z[c] : -INFINITY;  // idle lanes never touch smem
     mx = fmaxf(mx, v[i]);
   }
 #pragma unroll
@@ -99,9 +99,9 @@ __device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool li
     if (q + 8 * i < C) s += ex(v[i] - mx);
 #pragma unroll
   for (int o = 4; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 8);
-  const float zy = z[y];
-  __syncwarp();
   if (!live) return;
+  const float zy = z[y];
+  __syncwarp(0xffu << (threadIdx.x & 24));  // the row's 8 lanes read z[y] first
   const float inv = 1.f / s, nv = float(R);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
