@@ -129,7 +129,7 @@ def _phase_plan(wl, es=4):
     """[(label, kernel, algorithmic bytes)] per train launch of the workload's
     pack (all members share one input group in these workloads; the group's
     input rows are counted once per launch that reads them)."""
-    from paper_2002_02885_b200.device import uses_fused_mlp1, uses_m1t
+    from paper_2002_02885_b200.device import uses_fused_mlp1, uses_m1t, uses_m1x
     from paper_2002_02885_b200.packing import MLPArch
     dims = (wl["dim"], *wl["hidden"], wl["classes"])
     b = wl["batch"]
@@ -138,10 +138,19 @@ def _phase_plan(wl, es=4):
     T = "<double>" if es == 8 else "<float>"
     tens = [opt for opt, _ in wl["members"] if uses_m1t(arch, opt, b, prec)]
     fused = [opt for opt, _ in wl["members"] if uses_fused_mlp1(arch, opt, b, prec)]
+    one = [opt for opt, _ in wl["members"] if uses_m1x(arch, opt, b, prec)]
     other = [opt for opt, _ in wl["members"]
-             if not uses_fused_mlp1(arch, opt, b, prec) and not uses_m1t(arch, opt, b, prec)]
+             if not uses_fused_mlp1(arch, opt, b, prec) and not uses_m1t(arch, opt, b, prec)
+             and not uses_m1x(arch, opt, b, prec)]
     xb = es * b * dims[0]
     out = []
+    if one:
+        # the one-launch cluster step: params + slots read and written once,
+        # the batch rows once, the loss terms (the second W0 read hits L2)
+        D, H, C = dims
+        p = D * H + H + H * C + C
+        out.append(("X1STEP", "k_m1x_step" + T,
+                    sum(es * 2 * p * (1 + SLOTS[o]) + 8 * b for o in one) + xb))
     if tens:
         # mirror of build_phases: one-shot split-K clusters when one split per
         # CTA fits a wave, else the cluster-streaming forward
@@ -316,7 +325,7 @@ def _b200(args):
     plan_b = _phase_plan(wl, 8 if args.precision == "f64" else 4)
     T = "<double>" if args.precision == "f64" else "<float>"
     special = {17: "k_mlp1_fwd", 18: "k_mlp1_bwd", 19: "k_m1t_fwd", 20: "k_m1t_bwd",
-               21: "k_m1s_fwd", 22: "k_m1c_fwd"}
+               21: "k_m1s_fwd", 22: "k_m1c_fwd", 23: "k_m1x_step"}
     for i, (kind, layer, ctas, _) in enumerate(prof[0]):
         label, kern, nbytes = plan_b[i] if i < len(plan_b) else (f"{TK[kind] if kind < len(TK) else kind}{layer}", "?", 0)
         if kind in special:  # the kernel the runtime actually launched

@@ -245,6 +245,18 @@ __device__ __forceinline__ T act_fwd(int act, T z) {
 // engine.py:274-290 — relu keys on z > 0, leaky on z >= 0; sigmoid/tanh use
 // the stored output a.
 template <typename T>
+__device__ __forceinline__ T act_bwd(int act, T z, T a, T d);
+// fp32: explicit roundings (no contraction) — bit-identical in every kernel copy
+template <>
+__device__ __forceinline__ float act_bwd<float>(int act, float z, float a, float d) {
+  switch (act) {
+    case PK_ACT_SIGMOID: return __fmul_rn(__fmul_rn(d, a), __fsub_rn(1.f, a));
+    case PK_ACT_TANH: return __fmul_rn(d, __fsub_rn(1.f, __fmul_rn(a, a)));
+    case PK_ACT_RELU: return z > 0.f ? d : __fmul_rn(d, 0.f);
+    default: return __fmul_rn(d, z >= 0.f ? 1.f : 0.01f);
+  }
+}
+template <typename T>
 __device__ __forceinline__ T act_bwd(int act, T z, T a, T d) {
   switch (act) {
     case PK_ACT_SIGMOID: return d * a * (T(1) - a);
@@ -1102,6 +1114,34 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     if (f.take != 0 && !halted(P)) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+  } else {
+    __trap();
+  }
+  kernel_end(P, true);
+}
+
+#include "pk_m1x.cuh"
+
+// the whole one-hidden-layer step in one launch: a cluster of P.cs CTAs per
+// member (fp32; members with batch <= 64, pk_m1x.cuh)
+template <typename T>
+__global__ void __launch_bounds__(NT, 1) k_m1x_step(const __grid_constant__ PhaseArgs<T> P) {
+  extern __shared__ __align__(128) char smem_raw[];
+  if (threadIdx.x == 0)
+    pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  PK_TRACE(0);
+  pdl_launch();
+  if constexpr (sizeof(T) == 4) {
+    const Tile t = tile_of(P);
+    const FeedDev<T> f = feed_of(P, t.member);
+    __shared__ MemberDev<float> sM;
+    if (threadIdx.x < sizeof(MemberDev<float>) / 4)
+      reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
+          reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
+    __syncthreads();
+    // m0 = cluster rank (own unit range), layer = 16-unit blocks per CTA;
+    // take and halt are uniform over the member's cluster
+    if (f.take != 0 && !halted(P)) m1x_step(smem_raw, sM, f, t.m0, t.layer, P.stages);
   } else {
     __trap();
   }

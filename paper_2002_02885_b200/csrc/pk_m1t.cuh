@@ -96,7 +96,7 @@ __device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool li
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (q + 8 * i < C) s += ex(v[i] - mx);
+    if (q + 8 * i < C) s = __fadd_rn(s, ex(__fsub_rn(v[i], mx)));
 #pragma unroll
   for (int o = 4; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 8);
   if (!live) return;
@@ -107,9 +107,9 @@ __device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool li
   for (int i = 0; i < 4; ++i) {
     const int c = q + 8 * i;
     if (c < C) {
-      float p = ex(v[i] - mx) * inv;
-      if (c == y) p -= 1.f;
-      z[c] = p / nv;
+      float p = __fmul_rn(ex(__fsub_rn(v[i], mx)), inv);
+      if (c == y) p = __fsub_rn(p, 1.f);
+      z[c] = __fdiv_rn(p, nv);
     }
   }
   if (q == 0 && rowloss) *rowloss = -(double)((zy - mx) - lg(s));
@@ -1004,62 +1004,51 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 // memory stages by bulk copy while the previous tile's MMA and optimizer
 // epilogue run.  Which CTA updates an element never changes its arithmetic,
 // so the grouping (chosen per pack for occupancy) keeps K-invariance.
-// the member's optimizer on four elements: one switch, four lanes per case
-// (engine.py:302-324, same arithmetic as opt_step)
-__device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1, float bc2,
-                                       float4& w, float4& s0, float4& s1, float4 g) {
-  float* W = &w.x;
-  float* S0 = &s0.x;
-  float* S1 = &s1.x;
-  const float* Gp = &g.x;
+// The tensor / cluster paths' optimizer on one fp32 element (engine.py:302-324).
+// Every operation is an explicit round-to-nearest intrinsic: no FMA
+// contraction, so the update is bit-identical in every kernel and template
+// instantiation that applies it (packed == standalone does not depend on how
+// the compiler scheduled a particular copy).  ib1 / ib2 = 1 / Adam's bias
+// corrections (≤ 1 ulp from the divisions; the fp32 contract is rel 1e-4).
+__device__ __forceinline__ void opt_x(int opt, float lr, float wd, float ib1, float ib2, float& w,
+                                      float& s0, float& s1, float g) {
+  if (wd != 0.f) g = __fadd_rn(g, __fmul_rn(wd, w));
   switch (opt) {
     case PK_OPT_SGD:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float gi = Gp[i];
-        if (wd != 0.f) gi = gi + wd * W[i];
-        W[i] = W[i] - lr * gi;
-      }
+      w = __fsub_rn(w, __fmul_rn(lr, g));
       break;
     case PK_OPT_MOMENTUM:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float gi = Gp[i];
-        if (wd != 0.f) gi = gi + wd * W[i];
-        S0[i] = S0[i] * 0.9f + gi;
-        W[i] = W[i] - lr * S0[i];
-      }
+      s0 = __fadd_rn(__fmul_rn(s0, 0.9f), g);
+      w = __fsub_rn(w, __fmul_rn(lr, s0));
       break;
     case PK_OPT_ADAGRAD:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float gi = Gp[i];
-        if (wd != 0.f) gi = gi + wd * W[i];
-        S0[i] = S0[i] + gi * gi;
-        W[i] = W[i] - lr * gi * __frcp_rn(sqrtf(S0[i]) + 1e-10f);
-      }
+      s0 = __fadd_rn(s0, __fmul_rn(g, g));
+      w = __fsub_rn(w, __fmul_rn(__fmul_rn(lr, g), __frcp_rn(__fadd_rn(sqrtf(s0), 1e-10f))));
       break;
-    default: {
-      // one reciprocal per element: m̂ = m·(1/bc1), v̂ = v·(1/bc2) (≤ 1 ulp from
-      // the divisions; the fp32 contract is rel 1e-4)
-      const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float gi = Gp[i];
-        if (wd != 0.f) gi = gi + wd * W[i];
-        S0[i] = S0[i] * 0.9f + (1.f - 0.9f) * gi;
-        S1[i] = S1[i] * 0.999f + (1.f - 0.999f) * gi * gi;
-        W[i] = W[i] - lr * (S0[i] * ib1) * __frcp_rn(sqrtf(S1[i] * ib2) + 1e-8f);
-      }
+    default:
+      s0 = __fadd_rn(__fmul_rn(s0, 0.9f), __fmul_rn(1.f - 0.9f, g));
+      s1 = __fadd_rn(__fmul_rn(s1, 0.999f), __fmul_rn(__fmul_rn(1.f - 0.999f, g), g));
+      w = __fsub_rn(w, __fmul_rn(__fmul_rn(lr, __fmul_rn(s0, ib1)),
+                                 __frcp_rn(__fadd_rn(sqrtf(__fmul_rn(s1, ib2)), 1e-8f))));
       break;
-    }
   }
 }
 
-// scalar form for the small W1 / b0 / b1 updates (one out-of-line copy)
+// the member's optimizer on four elements
+__device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1, float bc2,
+                                          float4& w, float4& s0, float4& s1, float4 g) {
+  const float ib1 = opt == PK_OPT_ADAM ? 1.f / bc1 : 1.f, ib2 = opt == PK_OPT_ADAM ? 1.f / bc2 : 1.f;
+  opt_x(opt, lr, wd, ib1, ib2, w.x, s0.x, s1.x, g.x);
+  opt_x(opt, lr, wd, ib1, ib2, w.y, s0.y, s1.y, g.y);
+  opt_x(opt, lr, wd, ib1, ib2, w.z, s0.z, s1.z, g.z);
+  opt_x(opt, lr, wd, ib1, ib2, w.w, s0.w, s1.w, g.w);
+}
+
+// scalar form for the small W1 / b0 / b1 updates
 __device__ __forceinline__ void opt_step1(int opt, float lr, float wd, float bc1, float bc2,
-                                       float& w, float& s0, float& s1, float g) {
-  opt_step(opt, lr, wd, bc1, bc2, w, s0, s1, g);
+                                          float& w, float& s0, float& s1, float g) {
+  const float ib1 = opt == PK_OPT_ADAM ? 1.f / bc1 : 1.f, ib2 = opt == PK_OPT_ADAM ? 1.f / bc2 : 1.f;
+  opt_x(opt, lr, wd, ib1, ib2, w, s0, s1, g);
 }
 
 // A operand of the weight-gradient MMA: Xᵀ rows k (128) × K = batch rows
@@ -1087,14 +1076,17 @@ __device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
   return T_BK * T_BWLD + RP * T_BXLD;  // W0 tile + X columns
 }
 
-__device__ __forceinline__ void cp_wait_n(int n) {  // pending commit groups allowed
-  switch (n) {
-    case 0: cp_wait<0>(); break;
-    case 1: cp_wait<1>(); break;
-    case 2: cp_wait<2>(); break;
-    case 3: cp_wait<3>(); break;
-    default: cp_wait<4>(); break;
-  }
+__device__ __forceinline__ void cp_wait_n(int n) {  // pending commit groups allowed (<= 4)
+  // predicated waits, no branch: a switch here compiles to a jump table
+  // (LDC + BRX) whose indirect fetch costs hundreds of cycles per call
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, p2, p3, p4;\n\t"
+      "setp.le.s32 p0, %0, 0;\n\tsetp.eq.s32 p1, %0, 1;\n\tsetp.eq.s32 p2, %0, 2;\n\t"
+      "setp.eq.s32 p3, %0, 3;\n\tsetp.ge.s32 p4, %0, 4;\n\t"
+      "@p0 cp.async.wait_group 0;\n\t@p1 cp.async.wait_group 1;\n\t"
+      "@p2 cp.async.wait_group 2;\n\t@p3 cp.async.wait_group 3;\n\t"
+      "@p4 cp.async.wait_group 4;\n\t}\n" ::"r"(n)
+      : "memory");
 }
 
 __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,

@@ -22,7 +22,8 @@ struct Phase {
   int smem = 0;            // dynamic shared memory bytes
   int kind = 0;            // dominant tile kind (reporting)
   int mask = 0;            // OR of (1 << tile kind) present → which kernel
-  int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd, 3 k_m1t_fwd, 4 k_m1t_bwd
+  int special = 0;         // 0 phase kernel, 1 k_mlp1_fwd, 2 k_mlp1_bwd, 3 k_m1t_fwd, 4 k_m1t_bwd,
+                           // 5 k_m1s_fwd, 6 k_m1c_fwd, 7 k_m1x_step
   int layer = -1;          // dominant layer (reporting)
   int cs = 1;              // thread-block cluster size (k_m1t_fwd)
   int stages = 1;          // k_m1t_bwd input-tile stages
@@ -76,7 +77,7 @@ static MemberDev<T> member_dev(const pk_member* m, int tail) {
   for (int i = 0; i <= d.n_layers; ++i) d.dims[i] = m->desc.dims[i];
   d.n_slots = m->n_slots;
   d.tail = tail;
-  d.tensor = m->m1t ? 1 : 0;
+  d.tensor = (m->m1t || m->m1x) ? 1 : 0;
   d.wd = m->desc.weight_decay;
   d.n_params = m->P;
   d.s_stride = m->SS;
@@ -139,6 +140,7 @@ static cudaError_t init_smem_limit(int device, int* out) {
   ks.push_back(pk::k_m1t_bwd<T>);
   ks.push_back(pk::k_m1s_fwd<T>);
   ks.push_back(pk::k_m1c_fwd<T>);
+  ks.push_back(pk::k_m1x_step<T>);
   int dyn = optin;
   for (auto k : ks) {
     cudaFuncAttributes fa{};
@@ -156,9 +158,14 @@ static cudaError_t init_smem_limit(int device, int* out) {
   if ((e = cudaFuncSetAttribute(pk::k_m1c_fwd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
                                 1)) != cudaSuccess)
     return e;
+  if ((e = cudaFuncSetAttribute(pk::k_m1x_step<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                1)) != cudaSuccess)
+    return e;
   *out = dyn;
   return e;
 }
+
+static int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // conservative dynamic-smem budget for member-level decisions (made before
 // any pack exists): the opt-in limit minus a margin for static smem
@@ -197,6 +204,32 @@ static bool m1t_eligible(const pk_member_desc& d, int dtype, int device) {
   return pk::M1T::fwd_smem(RP, C) <= budget && pk::M1T::bwd_smem(RP, C, ns, 1) <= budget;
 }
 
+// one-launch cluster step (pk_m1x.cuh): the largest 16-unit blocks per CTA
+// (1, 2, 4) the register tiling and `budget` bytes of smem allow, 0 if none
+static int x_bpc_hi(const pk_member_desc& d, int ns, int budget) {
+  const int RP = pk::m1_rows_pad(d.max_rows), C = d.dims[2];
+  for (int b = pk::x_bpc_max(RP); b >= 1; b /= 2)
+    if (pk::M1X::smem(RP, pk::X_UB * b, C, ns, 2) <= budget) return b;
+  return 0;
+}
+
+// fp32, one hidden layer, <= 32 classes, <= 64 rows, 16-byte aligned rows,
+// and one cluster (<= 16 CTAs) covers the hidden layer
+static bool m1x_eligible(const pk_member_desc& d, int dtype, int device) {
+  if (dtype != PK_F32 || d.n_layers != 2) return false;
+  const int D = d.dims[0], H = d.dims[1], C = d.dims[2];
+  if (C > pk::X_MAXC || d.max_rows > pk::X_MAXR || H % 4 != 0 || D % 4 != 0) return false;
+  // opt-in while its step time trails the tcgen05 path's (PK_M1X=1)
+  if (getenv("PK_NO_M1X") || !getenv("PK_M1X")) return false;
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
+      cudaSuccess)
+    return false;
+  const int ns = d.optimizer == PK_OPT_SGD ? 0 : (d.optimizer == PK_OPT_ADAM ? 2 : 1);
+  const int b = x_bpc_hi(d, ns, optin - kStaticSmemMargin);
+  return b > 0 && cdiv(pk::x_nblk(H), b) <= pk::X_MAXCS;
+}
+
 // whether the member's last layer + head + first dgrad fit one TAIL tile
 static bool tail_ok(const pk_member* m, int dtype) {
   const int L = m->desc.n_layers - 1;
@@ -220,7 +253,6 @@ static int kind_smem(int kind, const pk_member* m, int dtype) {
   }
 }
 
-static int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // tiles of one (member, kind, layer) work item
 static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, int l) {
@@ -283,6 +315,87 @@ static std::vector<Stage> member_stages(const pk_member* m, bool tail, int* fwd_
   return st;
 }
 
+// k_m1x_step: one cluster of CS CTAs per member; member k's CTAs own
+// bpc_k = pow2 >= nblk_k / CS unit blocks each.  CS is the largest cluster
+// size whose clusters all run co-resident (one wave); the arithmetic does not
+// depend on it (pk_m1x.cuh), so packed == standalone still holds bitwise.
+static Phase build_m1x_phase(pk_pack* p) {
+  Phase xs;
+  xs.special = 7;
+  xs.kind = pk::TK_FWD;
+  xs.layer = 0;
+  std::vector<int> xm;
+  for (int k = 0; k < p->K; ++k)
+    if (p->members[k]->m1x) xm.push_back(k);
+  if (xm.empty()) return xs;
+  const int dt = p->ctx->dtype, budget = smem_budget(dt);
+  auto nblk = [&](int k) { return pk::x_nblk(p->members[k]->desc.dims[1]); };
+  auto plan = [&](int CS, std::vector<int>& bpc, int* Sb, int* sm) {
+    bpc.assign(p->K, 0);
+    for (int k : xm) {
+      const pk_member* m = p->members[k];
+      int b = 1;
+      while (b * CS < nblk(k)) b *= 2;
+      if (b > x_bpc_hi(m->desc, m->n_slots, budget)) return false;
+      bpc[k] = b;
+    }
+    for (*Sb = 4; *Sb >= 2; --*Sb) {
+      *sm = 0;
+      for (int k : xm) {
+        const pk_member* m = p->members[k];
+        *sm = std::max(*sm, pk::M1X::smem(pk::m1_rows_pad(m->desc.max_rows), pk::X_UB * bpc[k],
+                                          m->desc.dims[2], m->n_slots, *Sb));
+      }
+      if (*sm <= budget) return true;
+    }
+    return false;
+  };
+  // candidate cluster sizes: every member's nblk / {1, 2, 4}, largest first
+  std::vector<int> cand;
+  for (int k : xm)
+    for (int b = 1; b <= 4; b *= 2) {
+      const int cs = cdiv(nblk(k), b);
+      if (cs <= pk::X_MAXCS) cand.push_back(cs);
+    }
+  std::sort(cand.rbegin(), cand.rend());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  int CS = 0, Sb = 2, sm = 0;
+  std::vector<int> bpc;
+  for (int cs : cand) {
+    int sb, s;
+    std::vector<int> b;
+    if (!plan(cs, b, &sb, &s)) continue;
+    if (!CS || cs < CS) { CS = cs; Sb = sb; sm = s; bpc = b; }  // fallback: fewest CTAs
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs * (int)xm.size());
+    cfg.blockDim = dim3(pk::NT);
+    cfg.dynamicSmemBytes = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, pk::k_m1x_step<float>, &cfg) == cudaSuccess &&
+        nc >= (int)xm.size()) {
+      CS = cs; Sb = sb; sm = s; bpc = b;
+      break;
+    }
+  }
+  cudaGetLastError();  // an occupancy query error is not sticky for the caller
+  if (!CS) return xs;  // cannot happen for eligible members; fall through empty
+  for (int k : xm)
+    for (int r = 0; r < CS; ++r) xs.host.push_back(Tile{k, (int16_t)bpc[k], pk::TK_FWD, r, 0});
+  xs.cs = CS;
+  xs.stages = Sb;
+
+  xs.smem = sm;
+  xs.ntiles = (int)xs.host.size();
+  return xs;
+}
+
 static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   const int dt = p->ctx->dtype;
   std::vector<std::vector<Stage>> seq(p->K);
@@ -314,6 +427,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   tb.gsize = G;
   for (int k = 0; k < p->K; ++k) {
     const pk_member* m = p->members[k];
+    if (!eval && m->m1x) continue;  // the one-launch cluster step, below
     if (!eval && m->m1t) {
       const int D = m->desc.dims[0], H = m->desc.dims[1], C = m->desc.dims[2];
       const int RP = pk::m1_rows_pad(m->desc.max_rows);
@@ -458,6 +572,10 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     phases.insert(phases.begin(), tf);
     phases.push_back(tb);
   }
+  if (!eval) {
+    Phase xs = build_m1x_phase(p);
+    if (xs.ntiles) phases.insert(phases.begin(), xs);
+  }
 }
 
 // only >= 0: launch that phase alone (profiling); finalize: let the last
@@ -517,7 +635,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
       a.all_tensor = 1;
       for (int k = 0; k < p->K; ++k) {
         a.ctl_in[k] = p->members[k]->ctl;
-        a.all_tensor &= p->members[k]->m1t ? 1 : 0;
+        a.all_tensor &= (p->members[k]->m1t || p->members[k]->m1x) ? 1 : 0;
       }
     }
     a.gsize = ph.gsize;
@@ -539,6 +657,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
                           : ph.special == 4 ? pk::k_m1t_bwd<T>
                           : ph.special == 5 ? pk::k_m1s_fwd<T>
                           : ph.special == 6 ? pk::k_m1c_fwd<T>
+                          : ph.special == 7 ? pk::k_m1x_step<T>
                                             : kernel_for<T>(ph.mask);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) {

@@ -73,6 +73,7 @@ struct pk_member {
   MemberCtl* ctl;
   bool mlp1;  // fused one-hidden-layer step
   bool m1t;   // tensor-core (tcgen05 3xTF32) one-hidden-layer step
+  bool m1x;   // one-launch cluster step (pk_m1x.cuh), batch <= 64
 };
 
 struct pk_pack;
@@ -81,6 +82,7 @@ struct pk_pack;
 // step (pk_mlp1.cuh); decided from the member's own shape only
 static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device);
 static bool m1t_eligible(const pk_member_desc& d, int dtype, int device);
+static bool m1x_eligible(const pk_member_desc& d, int dtype, int device);
 
 #define CK_CTX(ctx, call)                                                        \
   do {                                                                           \
@@ -282,8 +284,9 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   m->ctx = c;
   m->desc = *d;
   m->n_slots = slots_for(d->optimizer);
-  m->m1t = m1t_eligible(*d, c->dtype, c->device);
-  m->mlp1 = !m->m1t && mlp1_eligible(*d, c->dtype, c->device);
+  m->m1x = m1x_eligible(*d, c->dtype, c->device);
+  m->m1t = !m->m1x && m1t_eligible(*d, c->dtype, c->device);
+  m->mlp1 = !m->m1x && !m->m1t && mlp1_eligible(*d, c->dtype, c->device);
   int64_t P = 0;
   for (int l = 0; l < d->n_layers; ++l) {
     m->w_off[l] = P;

@@ -47,11 +47,48 @@ def _cdiv(a, b):
     return -(-a // b)
 
 
+_X_KC, _X_LD, _X_UB, _X_FS, _X_RED, _X_MAXC, _X_MAXR, _X_MAXCS = 64, 68, 16, 4, 4096, 32, 64, 16
+
+
+def _r4(n):
+    return (n + 3) & ~3
+
+
+def _m1x_smem(RP, U, C, ns, Sb):
+    """M1X::smem (csrc/pk_m1x.cuh)."""
+    wld = U + 4
+    ring = max(_X_FS * (RP * _X_LD + _X_KC * wld), Sb * (RP * _X_LD + (1 + ns) * _X_KC * wld))
+    return 4 * (ring + _X_RED + 3 * RP * U + _r4(U * C) + _r4((U // _X_UB) * RP * C)
+                + _r4(RP * (C + 1)) + _r4(U) + 32) + 8 * RP
+
+
+def uses_m1x(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
+    """Mirror of csrc m1x_eligible(): the one-launch cluster step (fp32, one
+    hidden layer, <= 32 classes, <= 64 rows, H and D multiples of 4, one
+    cluster of <= 16 CTAs covers the hidden layer within the smem budget)."""
+    import os
+    if precision != "f32" or len(arch.hidden) != 1 or os.environ.get("PK_NO_M1X") \
+            or not os.environ.get("PK_M1X"):
+        return False
+    D, H, C = arch.input_dim, arch.hidden[0], arch.classes
+    if C > _X_MAXC or batch_size > _X_MAXR or H % 4 or D % 4:
+        return False
+    RP, ns = _m1_rows_pad(batch_size), _SLOTS[optimizer.lower()]
+    budget = _SMEM_OPTIN - _STATIC_MARGIN
+    b = 4 if RP <= 32 else 2
+    while b >= 1 and _m1x_smem(RP, _X_UB * b, C, ns, 2) > budget:
+        b //= 2
+    return b >= 1 and _cdiv(_cdiv(H, _X_UB), b) <= _X_MAXCS
+
+
 def uses_m1t(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
     """Mirror of csrc m1t_eligible(): the tcgen05 3xTF32 one-hidden-layer
-    step (fp32, <= 32 classes, <= 128 rows, H and D multiples of 4, smem fits)."""
+    step (fp32, <= 32 classes, <= 128 rows, H and D multiples of 4, smem fits),
+    for members the one-launch cluster step does not take."""
     import os
     if precision != "f32" or len(arch.hidden) != 1 or os.environ.get("PK_NO_TCGEN05"):
+        return False
+    if uses_m1x(arch, optimizer, batch_size, precision):
         return False
     D, H, C = arch.input_dim, arch.hidden[0], arch.classes
     if C > _T_MAXC or batch_size > _T_MAXR or H % 4 or D % 4 or _cdiv(D, _T_KS) > 16:
@@ -71,7 +108,8 @@ def uses_fused_mlp1(arch, optimizer: str, batch_size: int, precision="f32") -> b
     """Mirror of csrc mlp1_eligible() (the FFMA fused path, taken when the
     tensor path is not): one hidden layer, <= 32 classes, batch <= 128 and
     the fused kernels' shared memory fits."""
-    if uses_m1t(arch, optimizer, batch_size, precision):
+    if uses_m1t(arch, optimizer, batch_size, precision) or \
+            uses_m1x(arch, optimizer, batch_size, precision):
         return False
     if len(arch.hidden) != 1 or arch.classes > _M1_MAXC or batch_size > _M1_MAXR:
         return False

@@ -15,8 +15,8 @@ import os
 import numpy as np
 import pytest
 
-from _helpers import (ATOL, RTOL, assert_close_member, has_gpu, lockstep, oracle_dataset,
-                      oracle_from_handle)
+from _helpers import (ATOL, RTOL, _assert_param_close, assert_close_member, has_gpu, lockstep,
+                      oracle_dataset, oracle_from_handle)
 from oracle import mlp64 as O
 
 pytestmark = [pytest.mark.gpu,
@@ -535,10 +535,11 @@ def test_costmodel_calibrates_on_device():
 
 # ------------------------------------------- tcgen05 path: schedule shapes --
 
-def test_tensor_path_grouped_input_tiles_lockstep():
+def test_tensor_path_grouped_input_tiles_lockstep(monkeypatch):
     """8 wide members (mixed optimizers) on the tcgen05 path: the backward
     groups several 128-input tiles per CTA (G > 1) with two cp.async stages;
     one-step parity with the f64 oracle and packed == standalone bitwise."""
+    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=7, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "tanh")
@@ -554,9 +555,10 @@ def test_tensor_path_grouped_input_tiles_lockstep():
     assert _maxdiff(hs[5], solo) == 0.0
 
 
-def test_tensor_path_batch_128_rows_lockstep():
+def test_tensor_path_batch_128_rows_lockstep(monkeypatch):
     """RP = 128 rows (batch 100): four 32-row K chunks per backward tile and
     one input-tile stage; parity with the oracle."""
+    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"t": data.synth_dataset(1000, 200, 7, seed=8, spread=0.5)}
     arch = packing.MLPArch(200, (36,), 7, "sigmoid")
@@ -581,10 +583,11 @@ def test_pack_beyond_inline_descriptors():
     assert _maxdiff(hs[7], solo) == 0.0
 
 
-def test_streaming_forward_large_pack_lockstep():
+def test_streaming_forward_large_pack_lockstep(monkeypatch):
     """12 x 784-256-10 members: the split-K clusters would take > 2 waves, so
     the forward streams the input dimension in one CTA per unit tile
     (k_m1s_fwd); parity with the oracle, packed == standalone bitwise."""
+    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=11, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "leaky_relu")
     opts = ("sgd", "momentum", "adagrad", "adam")
@@ -600,11 +603,12 @@ def test_streaming_forward_large_pack_lockstep():
     assert _maxdiff(hs[4], solo) == 0.0
 
 
-def test_tensor_path_ragged_heterogeneous_pack():
+def test_tensor_path_ragged_heterogeneous_pack(monkeypatch):
     """Config-3-style heterogeneous pack on the tensor path: members with
     different hidden widths, class counts, batch sizes and input datasets
     (dimensions) share one pack — dummy cluster splits for the shallower
     inputs, ragged unit tiles; oracle parity and K-invariance."""
+    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"a": data.synth_dataset(800, 784, 10, seed=12, spread=0.5),
           "b": data.synth_dataset(600, 256, 32, seed=13, spread=0.5)}
@@ -620,6 +624,74 @@ def test_tensor_path_ragged_heterogeneous_pack():
     for _ in range(3):
         packing.standalone_step(solo, ds)
     assert _maxdiff(hs[2], solo) == 0.0
+
+
+# ------------------------------------- one-launch cluster step (k_m1x) --
+
+def test_m1x_mixed_optimizers_lockstep_and_cluster_size_invariance(monkeypatch):
+    """8 x 784-256-10 members (all four optimizers) on the one-launch cluster
+    step: parity with the f64 oracle per step, and the packed member equals
+    its standalone run bit for bit although the pack runs 8-CTA clusters
+    (2 unit blocks per CTA) and the singleton 16-CTA clusters (1 block)."""
+    monkeypatch.setenv("PK_M1X", "1")
+    from paper_2002_02885_b200 import device
+    ds = {"t": data.synth_dataset(3000, 784, 10, seed=31, spread=0.5)}
+    arch = packing.MLPArch(784, (256,), 10, "relu")
+    opts = ("sgd", "adam", "momentum", "adagrad")
+    hs = [packing.make_handle(f"x{i}", arch, opts[i % 4], 0.01 / (1 + i), 32, 50, "t", i)
+          for i in range(8)]
+    assert all(device.uses_m1x(arch, h.optimizer.kind, 32) for h in hs)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 3, packing=packing)
+    for i in (1, 6):
+        solo = packing.make_handle(f"x{i}", arch, opts[i % 4], 0.01 / (1 + i), 32, 50, "t", i)
+        for _ in range(3):
+            packing.standalone_step(solo, ds)
+        assert _maxdiff(hs[i], solo) == 0.0
+
+
+def test_m1x_ragged_units_rows_and_classes_lockstep(monkeypatch):
+    """Members whose hidden width is not a multiple of the 16-unit block
+    (partial last block, idle cluster ranks), 64-row padding (batch 50),
+    odd class counts and every activation, in one heterogeneous pack with two
+    input datasets; oracle parity and packed == standalone."""
+    monkeypatch.setenv("PK_M1X", "1")
+    from paper_2002_02885_b200 import device
+    ds = {"a": data.synth_dataset(700, 64, 7, seed=32, spread=0.5),
+          "b": data.synth_dataset(500, 100, 3, seed=33, spread=0.5)}
+    specs = [("r0", packing.MLPArch(64, (100,), 7, "sigmoid"), "adam", 0.01, 50, "a"),
+             ("r1", packing.MLPArch(64, (40,), 7, "tanh"), "momentum", 0.05, 32, "a"),
+             ("r2", packing.MLPArch(100, (212,), 3, "leaky_relu"), "adagrad", 0.02, 20, "b"),
+             ("r3", packing.MLPArch(100, (4,), 3, "relu"), "sgd", 0.1, 64, "b")]
+    hs = [packing.make_handle(m, a, o, lr, b, 30, d, i)
+          for i, (m, a, o, lr, b, d) in enumerate(specs)]
+    assert all(device.uses_m1x(h.arch, h.optimizer.kind, h.batch_size) for h in hs)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    lockstep(packed, ds, 3, packing=packing)
+    solo = packing.make_handle("r2", specs[2][1], "adagrad", 0.02, 20, 30, "b", 2)
+    for _ in range(3):
+        packing.standalone_step(solo, ds)
+    assert _maxdiff(hs[2], solo) == 0.0
+
+
+def test_m1x_and_tensor_path_agree(monkeypatch):
+    """The same member trained by the one-launch FFMA step and by the tcgen05
+    3xTF32 path: both within the stated fp32 tolerance of each other."""
+    ds = {"t": data.synth_dataset(2000, 784, 10, seed=34, spread=0.5)}
+    arch = packing.MLPArch(784, (128,), 10, "tanh")
+    out = {}
+    for path in ("m1x", "m1t"):
+        monkeypatch.setenv("PK_M1X", "1")
+        if path == "m1t":
+            monkeypatch.setenv("PK_NO_M1X", "1")
+        h = packing.make_handle("a", arch, "momentum", 0.02, 32, 50, "t", 3)
+        for _ in range(4):
+            loss = packing.standalone_step(h, ds)
+        out[path] = (h, loss)
+    (a, la), (b, lb) = out["m1x"], out["m1t"]
+    for k in a.params:
+        _assert_param_close(a.params[k], b.params[k], RTOL, ATOL, k, "momentum", 0.02)
+    assert la == pytest.approx(lb, rel=1e-5)
 
 
 # ------------------------------------------------- pipelined packed_run --

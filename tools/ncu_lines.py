@@ -53,14 +53,26 @@ def main():
         if re.match(r"\s*/\*[0-9a-f]{4,}\*/", ln):
             lines.append(cur)
     agg = collections.Counter()
+    why = collections.defaultdict(collections.Counter)
+    stall_cols = [(j, h[6:]) for j, h in enumerate(hdr)
+                  if h.startswith("stall_") and "Not Issued" not in h]
+    iE = hdr.index("Instructions Executed")
+    execd = collections.Counter()
     tot = 0
     for i, r in enumerate(data):
         s = int(r[iS])
         tot += s
-        agg[lines[i] if i < len(lines) else "?"] += s
+        src = lines[i] if i < len(lines) else "?"
+        agg[src] += s
+        execd[src] += int(float(r[iE] or 0))
+        for j, name in stall_cols:
+            v = r[j]
+            if v and float(v) > 0:
+                why[src][name] += float(v)
     print(f"{len(data)} SASS rows, {len(lines)} disassembled, {tot} samples")
-    for src, s in agg.most_common(30):
-        print(f"{s:5d} {100 * s / tot:5.1f}%  {src}")
+    for src, s in agg.most_common(int(os.environ.get("TOP", "30"))):
+        top = ", ".join(f"{n} {int(v)}" for n, v in why[src].most_common(3))
+        print(f"{s:5d} {100 * s / tot:5.1f}%  {src:24s} inst {execd[src]:9d}  [{top}]")
 
 
 if __name__ == "__main__":

@@ -68,6 +68,11 @@ def main():
             if len(v):
                 print(f"   {name:6s} min {v.min() / 1e3:8.2f}  med {statistics.median(v) / 1e3:8.2f}"
                       f"  max {v.max() / 1e3:8.2f} us   (n={len(v)})")
+        if int(os.environ.get("PK_M1X_DEBUG", "0")) & 32:  # k_m1x: clock64 at chunks 4 / 8
+            cyc = (blk[:, 7] - blk[:, 6]) / 4.0
+            ns = (blk[:, 12] - blk[:, 11]) / 4.0
+            print(f"   chunk 4..8: {statistics.median(cyc):.0f} cycles/iter, "
+                  f"{statistics.median(ns):.0f} ns/iter → {statistics.median(cyc / ns):.3f} GHz")
 
 
 if __name__ == "__main__":
