@@ -123,6 +123,14 @@ int pk_dataset_write(pk_dataset* ds, int64_t row0, int64_t rows,
  * _next_batch (packing.py:161-172) when datasets live on the host. */
 int pk_dataset_write_rows(pk_dataset* ds, int64_t row0, int64_t rows, const void* features,
                           const int32_t* labels);
+/* Streamed inputs in one call: gather host rows idx[0..rows) (device
+ * precision, row stride src_ld elements; labels int32) into the pinned
+ * staging buffers, then enqueue the same H2D as pk_dataset_write_rows into
+ * rows [0, rows).  Replaces the reference's per-step batch gather
+ * (reference data.py:131-136) on the host-resident input path. */
+int pk_dataset_gather_rows(pk_dataset* ds, int64_t rows, const void* src_features, int64_t src_ld,
+                           const int32_t* src_labels, const int64_t* idx, void* stage_features,
+                           int32_t* stage_labels);
 int pk_dataset_destroy(pk_dataset* ds);
 int pk_order_create(pk_ctx* ctx, const int64_t* perm, int64_t n, pk_order** out);
 int pk_order_destroy(pk_order* order);

@@ -24,7 +24,8 @@ OPT_CODES = {"sgd": 0, "momentum": 1, "adam": 2, "adagrad": 3}
 EXPORTS = (
     "pk_abi_version", "pk_ctx_create", "pk_ctx_destroy", "pk_ctx_last_error",
     "pk_ctx_set_stream", "pk_ctx_synchronize", "pk_ctx_mem_info",
-    "pk_dataset_create", "pk_dataset_write", "pk_dataset_write_rows", "pk_dataset_destroy",
+    "pk_dataset_create", "pk_dataset_write", "pk_dataset_write_rows", "pk_dataset_gather_rows",
+    "pk_dataset_destroy",
     "pk_order_create", "pk_order_destroy",
     "pk_member_create", "pk_member_destroy", "pk_member_param_count",
     "pk_member_slot_count", "pk_member_device_bytes", "pk_member_set_lr",
@@ -89,6 +90,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pk_dataset_create": (C.c_int, [vp, i64, i32, P(vp)]),
         "pk_dataset_write": (C.c_int, [vp, i64, i64, vp, vp]),
         "pk_dataset_write_rows": (C.c_int, [vp, i64, i64, vp, vp]),
+        "pk_dataset_gather_rows": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, vp]),
         "pk_dataset_destroy": (C.c_int, [vp]),
         "pk_order_create": (C.c_int, [vp, vp, i64, P(vp)]),
         "pk_order_destroy": (C.c_int, [vp]),

@@ -206,8 +206,12 @@ template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   const int n = pred ? BYTES : 0;  // src-size 0 → zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
-               "n"(BYTES), "r"(n));
+  if constexpr (BYTES == 16)  // L2 only: with most of the SM's SRAM carved out as shared
+    // memory, L1-allocating copies (.ca) thrash the small L1 and throttle issue
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+                 "n"(BYTES), "r"(n));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>

@@ -441,11 +441,28 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
   // partial of (d = 4dq + dd, units 4buq..) at float4 slot (bgrp·CW + buq)·64 +
   // 4dq + (dd ^ ((dq >> 1) & 3)): the store of 16 lanes fills two wavefronts
   const int sw = (dq >> 1) & 3;
+  // the dZ0 operand does not change across chunks: keep this thread's slice
+  // in registers (NI <= 2) so a row costs one shared load per 16 FMA
+  constexpr bool DZR = NI <= 2;
+  float4 dzr[DZR ? NI : 1][8];
+  if constexpr (DZR) {
+#pragma unroll
+    for (int it = 0; it < NI; ++it)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = 8 * (bgrp * NI + it) + j;
+        dzr[it][j] = r < R ? *reinterpret_cast<const float4*>(sdZ + r * U + 4 * buq)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  }
   if (work) {
     for (int c = 0; c < nch; ++c) {
+      if (c == 4) PK_TRACE(10);
       cp_wait_n(issued_b - c - 1);
       __syncthreads();  // chunk c landed; chunk c-1's optimizer pass is done
+      if (c == 4) PK_TRACE(11);
       if (c >= 1 && c - 1 + Sb < nch) issue_b(c - 1 + Sb);
+      if (c == 4) PK_TRACE(12);
       const float* X = ring + (c % Sb) * SB;
       const float* W = X + RP * X_LD;
       const int k0 = c * X_KC, nk = min(X_KC, D - k0);
@@ -462,7 +479,9 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
           const int rb = 8 * (bgrp * NI + it);
           auto row = [&](int r) {
             const float4 xv = *reinterpret_cast<const float4*>(Xd + r * X_LD);
-            const float4 dv = *reinterpret_cast<const float4*>(Zd + r * U);
+            float4 dv;
+            if constexpr (DZR) dv = dzr[it][r - rb];
+            else dv = *reinterpret_cast<const float4*>(Zd + r * U);
             const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
             const float ds[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
@@ -475,6 +494,7 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
 #pragma unroll
             for (int j = 0; j < 8; ++j) row(rb + j);
           } else {
+#pragma unroll
             for (int j = 0; j < 8; ++j)
               if (rb + j < R) row(rb + j);
           }
@@ -486,7 +506,9 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
         red4[(bgrp * CW + buq) * 64 + 4 * dq + (dd ^ sw)] =
             make_float4(x_fold<NI>(bacc, 4 * dd), x_fold<NI>(bacc, 4 * dd + 1),
                         x_fold<NI>(bacc, 4 * dd + 2), x_fold<NI>(bacc, 4 * dd + 3));
+      if (c == 4) PK_TRACE(13);
       __syncthreads();
+      if (c == 4) PK_TRACE(14);
       // optimizer pass: lane pairs (j even/odd) on 16 consecutive rows d → full
       // 32-byte sectors to HBM, conflict-free shared reads
 #pragma unroll

@@ -222,6 +222,26 @@ extern "C" int pk_dataset_write_rows(pk_dataset* d, int64_t row0, int64_t rows, 
   return PK_OK;
 }
 
+// streamed inputs in one call: gather rows idx[0..rows) of a host dataset
+// (device precision, row stride src_ld elements) into pinned staging, then
+// the same async H2D as pk_dataset_write_rows (the batch gather of
+// data.py:131-136, done by memcpy instead of two numpy takes + a copy call)
+extern "C" int pk_dataset_gather_rows(pk_dataset* d, int64_t rows, const void* src_x,
+                                      int64_t src_ld, const int32_t* src_y, const int64_t* idx,
+                                      void* stage_x, int32_t* stage_y) {
+  if (!d) return PK_ERR_ARG;
+  pk_ctx* c = d->ctx;
+  if (rows < 0 || rows > d->n || src_ld < d->dim || (rows && (!src_x || !src_y || !idx ||
+                                                              !stage_x || !stage_y)))
+    return arg_err(c, "dataset_gather_rows: bad args");
+  const size_t es = c->esize(), rb = (size_t)d->dim * es;
+  for (int64_t i = 0; i < rows; ++i) {
+    memcpy((char*)stage_x + (size_t)i * rb, (const char*)src_x + (size_t)idx[i] * src_ld * es, rb);
+    stage_y[i] = src_y[idx[i]];
+  }
+  return pk_dataset_write_rows(d, 0, rows, stage_x, stage_y);
+}
+
 extern "C" int pk_dataset_destroy(pk_dataset* d) {
   if (!d) return PK_ERR_ARG;
   cudaSetDevice(d->ctx->device);

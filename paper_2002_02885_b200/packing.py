@@ -25,6 +25,7 @@ from . import engine
 from . import runtime as _rt
 from .data import Dataset, account_cache, epoch_permutation, preprocess
 from .engine import ComputationGraph
+from . import _lib
 from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE, PK_SKIPPED
 
 CHECKPOINT_MAGIC = b"PKCK"
@@ -259,9 +260,7 @@ class PackedModel:
         x, y = rt.host_rows_source(ds)
         n = len(idx)
         dev, hx, hy = _stream_staging(self, rt, (gi, buf), n, ds.dim)
-        np.take(x, idx, axis=0, out=hx[:n])
-        np.take(y, idx, out=hy[:n])
-        dev.write_rows_ptr(n, hx, hy)
+        dev.gather_rows(n, x, y, idx, hx, hy)
         return dev
 
     def input_groups(self):
@@ -496,54 +495,72 @@ def _speculate(packed, active, plan, datasets, stop_at_epoch_end, buf):
 
 def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16) -> list:
     """Up to `max_steps` packed_step calls (reference semantics, packing.py:185-264)
-    with up to `depth` steps in flight on the device: the host plans steps
-    n+1.. from shadow cursors (epoch rolls and finished members exactly as
-    _active_members) and enqueues them while step n runs.  If a step raises
-    (non-finite value / gradient), the device has skipped every later step
-    (halt flag), so the state is exactly the reference's at that exception.
-    Stops early when no member is left; returns the per-step loss dicts."""
+    with up to `depth` steps in flight on the device: a sliding window — the
+    host plans step n+depth from shadow cursors (epoch rolls and finished
+    members exactly as _active_members) and enqueues it as soon as step n's
+    result has been applied, so the device never drains between steps.  If a
+    step raises (non-finite value / gradient), the device has skipped every
+    later step (halt flag), so the state is exactly the reference's at that
+    exception.  Stops early when no member is left; returns the per-step loss
+    dicts."""
+    from collections import deque
     out = []
-    while len(out) < max_steps:
-        try:
-            active = _active_members(packed, datasets, False)
-        except ReplanNeeded:
-            break
-        shadow = {id(h): (h.cursor.epoch_index, h.cursor.pos, h.cursor.steps_done)
-                  for h in packed.members}
-        chain = []
-        act, curs = active, None
-        dpack = packed._device_pack(_rt.runtime())  # synced once per burst
-        while len(chain) < min(depth, max_steps - len(out)):
-            plan = _plan_step(packed, act, datasets, None, None, curs=curs, dpack=dpack)
-            chain.append((act, plan, plan.dpack.step_async()))
-            # shadow state after this step commits → the next step's members
-            nact, ncurs = [], {}
-            for h in packed.members:
-                ep, pos, steps = shadow[id(h)]
-                if id(h) in plan.takes:
-                    steps += 1
-                    pos += plan.takes[id(h)][1]
-                shadow[id(h)] = (ep, pos, steps)
-                if steps >= h.target_steps:
-                    continue
-                n = datasets[h.dataset_binding].n
-                if pos >= n:
-                    ep, pos = ep + 1, 0
+    if max_steps <= 0:
+        return out
+    try:
+        act = _active_members(packed, datasets, False)
+    except ReplanNeeded:
+        return out
+    shadow = {id(h): (h.cursor.epoch_index, h.cursor.pos, h.cursor.steps_done)
+              for h in packed.members}
+    dpack = packed._device_pack(_rt.runtime())  # host-side edits synced once
+    inflight = deque()
+    curs, planned, more = None, 0, True
+    try:
+        while len(out) < max_steps:
+            while more and len(inflight) < depth and planned < max_steps:
+                # stream mode: every in-flight step owns a pinned + device
+                # staging slot; a slot is reused only after its step was waited
+                plan = _plan_step(packed, act, datasets, None, None, curs=curs, dpack=dpack,
+                                  buf=2 + planned % depth)
+                inflight.append((act, plan, plan.dpack.step_async()))
+                planned += 1
+                nact, ncurs = [], {}
+                for h in packed.members:  # shadow state after this step commits
+                    ep, pos, steps = shadow[id(h)]
+                    if id(h) in plan.takes:
+                        steps += 1
+                        pos += plan.takes[id(h)][1]
                     shadow[id(h)] = (ep, pos, steps)
-                ncurs[id(h)] = (ep, pos)
-                nact.append(h)
-            if not nact:
+                    if steps >= h.target_steps:
+                        continue
+                    n = datasets[h.dataset_binding].n
+                    if pos >= n:
+                        ep, pos = ep + 1, 0
+                        shadow[id(h)] = (ep, pos, steps)
+                    ncurs[id(h)] = (ep, pos)
+                    nact.append(h)
+                more = bool(nact)
+                act, curs = nact, ncurs
+            if not inflight:
                 break
-            act, curs = nact, ncurs
-        for j, (act, plan, ticket) in enumerate(chain):
+            a, plan, ticket = inflight.popleft()
             code, who, where, _, losses = plan.dpack.wait(ticket)
-            if j:  # the reference rolls epochs at the top of each packed_step
-                for h in act:
+            if out:  # the reference rolls epochs at the top of each packed_step
+                for h in a:
                     _roll_if_needed(h, datasets)
-            out.append(_apply_result(packed, act, plan, code, who, where, losses))
+            out.append(_apply_result(packed, a, plan, code, who, where, losses))
             packed.last_step_stats = {"physical_inputs": plan.physical,
                                       "groups": plan.n_groups, "driver_batch": plan.driver}
-    packed._spec = None
+    finally:
+        # a raised step: the later in-flight steps were skipped on the device;
+        # drain their tickets so no staging slot or ring entry is left busy
+        for _, plan, ticket in inflight:
+            try:
+                plan.dpack.wait(ticket)
+            except _lib.PKError:  # PK_SKIPPED: nothing was committed
+                pass
+        packed._spec = None
     return out
 
 

@@ -196,6 +196,20 @@ class DeviceDataset:
             self._wr_ptrs = ptrs
         self.rt.check(self.rt.lib.pk_dataset_write_rows(self.ptr, 0, int(rows), ptrs[1], ptrs[2]))
 
+    def gather_rows(self, rows: int, x, y, idx, hx, hy):
+        """Rows idx of the host source (x, y) → pinned staging (hx, hy) → H2D
+        into rows [0, rows), in one library call (pointers of the long-lived
+        buffers cached)."""
+        key = (x.ctypes.data, y.ctypes.data, hx.ctypes.data, hy.ctypes.data)
+        ptrs = getattr(self, "_gr_ptrs", None)
+        if ptrs is None or ptrs[0] != key:
+            ptrs = (key, *(C.c_void_p(v) for v in key), x.strides[0] // x.itemsize)
+            self._gr_ptrs = ptrs
+        if idx.dtype != np.int64 or not idx.flags.c_contiguous:
+            idx = np.ascontiguousarray(idx, dtype=np.int64)
+        self.rt.check(self.rt.lib.pk_dataset_gather_rows(
+            self.ptr, int(rows), ptrs[1], ptrs[5], ptrs[2], idx.ctypes.data, ptrs[3], ptrs[4]))
+
     def write_rows(self, row0: int, x, y):
         """Async H2D of rows already in device precision (x) / int32 (y);
         x and y must stay alive until the stream syncs (pinned: true DMA)."""

@@ -517,6 +517,29 @@ def test_streamed_inputs_match_resident_bitwise():
     assert out["resident"][2:] == out["stream"][2:]
 
 
+def test_packed_run_streamed_inputs_match_resident_bitwise():
+    """packed_run with 16 steps in flight in input_mode 'stream': every
+    in-flight step owns its pinned + device staging slot, so the trajectory
+    equals the resident packed_step loop bit for bit (epoch rolls included)."""
+    out = {}
+    for mode in ("resident", "stream"):
+        runtime.set_input_mode(mode)
+        try:
+            datasets = _ds(n=50)
+            hs = [_h("a", seed=1, steps=40), _h("b", seed=2, opt="adam", batch=7, steps=40)]
+            packed = packing.dedup_inputs(packing.pack_models(hs))
+            if mode == "stream":
+                losses = packing.packed_run(packed, datasets, 30, depth=16)
+            else:
+                losses = [packing.packed_step(packed, datasets) for _ in range(30)]
+            out[mode] = (losses, [h._flat_params(h.params) for h in hs])
+        finally:
+            runtime.set_input_mode("resident")
+    assert out["resident"][0] == out["stream"][0]
+    for a, b in zip(out["resident"][1], out["stream"][1]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_costmodel_calibrates_on_device():
     """§8f-4: Eqs. 1-2 fitted to packed steps timed on this GPU; packing K
     same-batch members must be predicted (and measured) cheaper than K

@@ -24,7 +24,23 @@ __global__ void __launch_bounds__(256, 1) k(const float* __restrict__ src, float
   for (int c = 0; c < iters; ++c) {
     if (V >= 1) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
     __syncthreads();
-    if (V >= 2) {
+    if (V == 6 || V == 7) {  // gathered rows (X-like) + strided 64 B segments (W-like)
+      float* st = sm + (c & 3) * 4096;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int e = tid + 256 * j, r = e >> 4, q = e & 15;
+        const size_t row = (size_t)((r * 7919 + blockIdx.x * 31) % 10000);
+        cp16(st + r * 68 + 4 * q, src + row * 784 + c * 64 + 4 * q);
+      }
+      {
+        const int k = tid >> 2, q = tid & 3;
+        const float* w = V == 6 ? src + 8000000 + (size_t)(c * 64 + k) * 256 + blockIdx.x * 16 + 4 * q
+                                : src + 8000000 + (size_t)(c * 64 + k) * 16 + 4 * q;
+        cp16(st + 2176 + k * 20 + 4 * q, w);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    if (V >= 2 && V <= 5) {
       float* st = sm + (c & 3) * 4096;
 #pragma unroll
       for (int j = 0; j < 3; ++j)
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(256, 1) k(const float* __restrict__ src, float
 
 template <int V>
 static void run(const char* name, int cluster, const float* src, float* out, long long* cyc) {
-  const int smem = 200 * 1024, iters = 52;
+  const int smem = 200 * 1024, iters = 12;
   cudaFuncSetAttribute(k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k<V>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
@@ -117,8 +133,8 @@ static void run(const char* name, int cluster, const float* src, float* out, lon
 int main() {
   float *src, *out;
   long long* cyc;
-  cudaMalloc(&src, (size_t)32 * 64 * 4096 * 4 + 65536);
-  cudaMemset(src, 0, (size_t)32 * 64 * 4096 * 4 + 65536);
+  cudaMalloc(&src, (size_t)64 * 1024 * 1024 * 4);
+  cudaMemset(src, 0, (size_t)64 * 1024 * 1024 * 4);
   cudaMalloc(&out, 4096);
   cudaMalloc(&cyc, 32 * 8);
   for (int cl : {1}) {
@@ -128,6 +144,8 @@ int main() {
     run<3>("+ 2 quads (16 LDS.128, 128 FFMA)", cl, src, out, cyc);
     run<4>("+ 2 quads, k-outer FFMA order", cl, src, out, cyc);
     run<5>("+ 2 quads, register operands", cl, src, out, cyc);
+    run<6>("gathered X rows + strided W (1KB)", cl, src, out, cyc);
+    run<7>("gathered X rows + contiguous W", cl, src, out, cyc);
   }
   return 0;
 }
