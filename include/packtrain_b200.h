@@ -163,6 +163,49 @@ int pk_pack_step(pk_pack* p, const pk_feed* feeds, double* losses, pk_status* st
 /* asynchronous form for pipelined drivers: enqueue, then wait by ticket */
 int pk_pack_step_async(pk_pack* p, const pk_feed* feeds, int64_t* ticket);
 int pk_pack_step_wait(pk_pack* p, int64_t ticket, double* losses, pk_status* st);
+
+/* ---- native multi-step driver (reference packing.py:185-264, looped) ------
+ * Up to `max_steps` packed steps with up to `depth` (<= 32) in flight,
+ * planned and applied in C: active members, epoch rolls, input groups sorted
+ * by (dataset, epoch, pos, batch), rows perm[pos : pos + take], label bound
+ * checks, per-step feeds (device-resident order or streamed rows gathered
+ * into pinned slots), and at result time the cursor updates
+ * (steps_done, pos, samples_used[idx] += 1) with the reference's commit rules.
+ * `mem` (K entries, pack order) is updated in place.  Outputs per completed
+ * step i: losses[i*K + k], active[i*K + k] (1 = member k stepped and
+ * committed), stats[3*i .. 3*i+2] = (groups, physical inputs, driver batch).
+ * The loop stops before a step it cannot plan alone (*stop, PK_RUN_*); a
+ * failed step is reported in *st (not counted in *done). */
+typedef struct {
+  int32_t dataset;        /* index into the run's datasets */
+  int32_t batch;          /* batch size */
+  int64_t epoch, pos, steps_done, target_steps; /* cursor (in/out) */
+  int64_t* samples_used;  /* [n] use counts of the current epoch (in/out), or NULL */
+} pk_run_member;
+
+typedef struct {
+  int64_t n;
+  int32_t dim;
+  int32_t max_label;
+  const void* host_x;     /* streamed inputs: host rows in device precision, or NULL */
+  int64_t host_ld;        /* row stride of host_x (elements) */
+  const int32_t* host_y;  /* host labels (always; label bound checks) */
+  const pk_dataset* device;     /* device-resident inputs (host_x == NULL) */
+  int64_t epoch0;               /* permutations / orders given for epochs */
+  int32_t n_epochs;             /*   epoch0 .. epoch0 + n_epochs - 1 */
+  const int64_t* const* perm;   /* host permutations */
+  const pk_order* const* order; /* device orders (device-resident inputs) */
+} pk_run_dataset;
+
+#define PK_RUN_MAX_STEPS 0    /* ran max_steps */
+#define PK_RUN_NO_MEMBER 1    /* every member reached target_steps */
+#define PK_RUN_NEED_PERM 2    /* the next step needs a permutation not given */
+#define PK_RUN_LABEL_BOUNDS 3 /* the next step's labels exceed a member's classes */
+#define PK_RUN_FAILED 4       /* a step failed (non-finite); see *st */
+
+int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset* ds, int32_t n_ds,
+                int32_t share_inputs, int64_t max_steps, int32_t depth, double* losses,
+                uint8_t* active, int32_t* stats, int64_t* done, pk_status* st, int32_t* stop);
 /* forward-only mean softmax-xent of every member on `rows` rows of one
  * dataset (order NULL = rows 0..rows-1); replaces EngineExecutor._val_loss
  * (tuner.py:460-464).  Nothing is updated. */

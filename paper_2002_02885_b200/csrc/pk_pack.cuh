@@ -65,6 +65,16 @@ struct pk_pack {
   std::vector<char> h_feeds;  // host FeedDev<T>[K] of the step being launched
   std::vector<char> h_mems;   // host MemberDev<T>[K] (static)
   bool halt_dirty = false;    // a failed step set the device halt flag
+  struct RunStage {           // pk_pack_run's streamed-input slot (pinned + device)
+    pk_dataset* d = nullptr;
+    void* hx = nullptr;
+    int32_t* hy = nullptr;
+  };
+  std::vector<RunStage> run_stage;
+  // pk_pack_run's streamed inputs travel on their own stream, so step n+1's
+  // H2D overlaps step n's kernels; the pack stream waits on ev_copy[slot]
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[kRing] = {};
 };
 
 template <typename T>
@@ -806,6 +816,14 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
   cudaFree(p->d_tiles);
   cudaFree(p->d_done);
   if (p->d_trace) cudaFree(p->d_trace);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  for (auto& e : p->ev_copy)
+    if (e) cudaEventDestroy(e);
+  for (auto& s : p->run_stage) {
+    if (s.d) pk_dataset_destroy(s.d);
+    if (s.hx) cudaFreeHost(s.hx);
+    if (s.hy) cudaFreeHost(s.hy);
+  }
   cudaFreeHost(p->h_desc);
   cudaFreeHost(p->h_ring);
   delete p;

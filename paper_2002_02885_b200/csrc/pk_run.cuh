@@ -1,0 +1,261 @@
+// pk_run.cuh — native multi-step driver (included by pk_runtime.cu after
+// pk_pack.cuh): `pk_pack_run` is the reference's packed_step loop
+// (packing.py:185-264) planned and applied in C++, with up to `depth` steps in
+// flight.  Per step it does exactly what the Python planner does:
+//
+//   active     members with steps_done < target_steps (shadow cursors)
+//   roll       pos >= n → epoch + 1, pos 0 (packing.py:175-182)
+//   groups     (dataset, epoch, pos, batch) in sorted order (packing.py:121-128)
+//   rows       take = min(batch, n - pos), idx = perm_epoch[pos : pos + take]
+//              (data.py:124-136); labels checked against every member's classes
+//   inputs     device-resident: feed = (dataset, device order, pos, take);
+//              streamed: rows gathered into a pinned slot + async H2D
+//   apply      at result time, in step order: roll, then steps_done += 1,
+//              pos += take, samples_used[idx] += 1 (packing.py:255-257); a
+//              non-finite value commits nothing, a non-finite gradient at
+//              member k commits the members before k (packing.py:246-253)
+//
+// The host's share of a step drops to a few microseconds, so the pipeline is
+// bound by the device.  Anything the loop cannot decide alone (a permutation
+// it was not given, a label out of bounds) stops it cleanly before that step
+// is enqueued; the Python caller resolves it and calls again.
+
+#pragma once
+
+namespace {
+
+struct RunKey {
+  int32_t ds;
+  int64_t epoch, pos;
+  int32_t batch;
+  bool operator<(const RunKey& o) const {
+    if (ds != o.ds) return ds < o.ds;
+    if (epoch != o.epoch) return epoch < o.epoch;
+    if (pos != o.pos) return pos < o.pos;
+    return batch < o.batch;
+  }
+  bool operator==(const RunKey& o) const {
+    return ds == o.ds && epoch == o.epoch && pos == o.pos && batch == o.batch;
+  }
+};
+
+struct RunStep {
+  int64_t ticket;
+  std::vector<int32_t> member;  // active members (pack order)
+  std::vector<int32_t> take;    // rows each took
+  std::vector<const int64_t*> idx;
+  int32_t groups, physical, driver;
+};
+
+}  // namespace
+
+static pk_pack::RunStage* run_stage(pk_pack* p, int slot, int gi, int64_t rows, int32_t dim) {
+  auto& v = p->run_stage;
+  const size_t i = (size_t)slot * p->K + gi;
+  if (v.size() <= i) v.resize(i + 1);
+  pk_pack::RunStage& s = v[i];
+  if (s.d && (s.d->n < rows || s.d->dim != dim)) {
+    pk_dataset_destroy(s.d);
+    cudaFreeHost(s.hx);
+    cudaFreeHost(s.hy);
+    s = pk_pack::RunStage{};
+  }
+  if (!s.d) {
+    if (pk_dataset_create(p->ctx, rows, dim, &s.d) != PK_OK) return nullptr;
+    if (cudaHostAlloc(&s.hx, (size_t)rows * dim * p->ctx->esize(), cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaHostAlloc((void**)&s.hy, (size_t)rows * 4, cudaHostAllocDefault) != cudaSuccess)
+      return nullptr;
+  }
+  return &s;
+}
+
+// rows idx of a host dataset → the slot's pinned staging → H2D on the copy
+// stream; the pack stream waits for that copy before the step's kernels
+static int run_gather(pk_pack* p, int slot, pk_pack::RunStage* g, int64_t take,
+                      const pk_run_dataset& d, const int64_t* idx) {
+  pk_ctx* c = p->ctx;
+  if (!p->copy_stream) CK_CTX(c, cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  if (!p->ev_copy[slot]) CK_CTX(c, cudaEventCreateWithFlags(&p->ev_copy[slot], cudaEventDisableTiming));
+  const size_t es = c->esize(), rb = (size_t)d.dim * es;
+  for (int64_t i = 0; i < take; ++i) {
+    memcpy((char*)g->hx + (size_t)i * rb, (const char*)d.host_x + (size_t)idx[i] * d.host_ld * es, rb);
+    g->hy[i] = d.host_y[idx[i]];
+  }
+  CK_CTX(c, cudaMemcpyAsync(g->d->feat, g->hx, (size_t)take * rb, cudaMemcpyHostToDevice,
+                            p->copy_stream));
+  CK_CTX(c, cudaMemcpyAsync(g->d->labels, g->hy, (size_t)take * 4, cudaMemcpyHostToDevice,
+                            p->copy_stream));
+  CK_CTX(c, cudaEventRecord(p->ev_copy[slot], p->copy_stream));
+  CK_CTX(c, cudaStreamWaitEvent(c->stream, p->ev_copy[slot], 0));
+  return PK_OK;
+}
+
+static void run_roll(pk_run_member& m, const pk_run_dataset& d) {
+  if (m.pos >= d.n) {
+    m.epoch += 1;
+    m.pos = 0;
+    if (m.samples_used) memset(m.samples_used, 0, sizeof(int64_t) * (size_t)d.n);
+  }
+}
+
+extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset* ds, int32_t n_ds,
+                           int32_t share_inputs, int64_t max_steps, int32_t depth, double* losses,
+                           uint8_t* active, int32_t* stats, int64_t* done, pk_status* st,
+                           int32_t* stop) {
+  if (!p || !mem || !ds || n_ds < 1 || !losses || !active || !stats || !done || !st || !stop)
+    return PK_ERR_ARG;
+  pk_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  const int K = p->K;
+  depth = std::max(1, std::min(depth, kRing));
+  *done = 0;
+  *stop = PK_RUN_MAX_STEPS;
+  st->code = PK_OK;
+  st->member = -1;
+  st->index = -1;
+  st->committed = 0;
+  for (int k = 0; k < K; ++k)
+    if (mem[k].dataset < 0 || mem[k].dataset >= n_ds) return arg_err(c, "run: bad dataset index");
+  // shadow cursors: the state after every enqueued step commits
+  std::vector<pk_run_member> sh(mem, mem + K);
+  for (auto& m : sh) m.samples_used = nullptr;  // the shadow never touches bookkeeping
+  std::vector<pk_feed> feeds(K);
+  std::vector<RunStep> fly;  // in flight, oldest first
+  size_t head = 0;
+  int64_t planned = 0, applied = 0;
+  bool more = true;
+  int rc = PK_OK;
+  while (applied < max_steps) {
+    // ---- plan + enqueue while the window has room --------------------------
+    while (more && (int)(fly.size() - head) < depth && planned < max_steps) {
+      std::vector<int32_t> act;
+      for (int k = 0; k < K; ++k)
+        if (sh[k].steps_done < sh[k].target_steps) act.push_back(k);
+      if (act.empty()) {
+        more = false;
+        *stop = PK_RUN_NO_MEMBER;
+        break;
+      }
+      for (int k : act) run_roll(sh[k], ds[sh[k].dataset]);  // shadow roll (no bookkeeping)
+      std::vector<std::pair<RunKey, int32_t>> keyed;
+      int32_t driver = 0;
+      for (int k : act) {
+        keyed.push_back({RunKey{sh[k].dataset, sh[k].epoch, sh[k].pos, sh[k].batch}, k});
+        driver = std::max(driver, sh[k].batch);
+      }
+      std::stable_sort(keyed.begin(), keyed.end(),
+                       [](const auto& a, const auto& b) { return a.first < b.first; });
+      // every group's permutation must be known and its labels in bounds
+      bool ok = true;
+      for (size_t i = 0; i < keyed.size() && ok; ++i) {
+        const RunKey& key = keyed[i].first;
+        const pk_run_dataset& d = ds[key.ds];
+        const int64_t e = key.epoch - d.epoch0;
+        if (e < 0 || e >= d.n_epochs || !d.perm[e]) {
+          *stop = PK_RUN_NEED_PERM;
+          ok = false;
+          break;
+        }
+        const pk_member* m = p->members[keyed[i].second];
+        if (d.max_label >= m->desc.dims[m->desc.n_layers]) {
+          const int64_t take = std::min<int64_t>(key.batch, d.n - key.pos);
+          const int64_t* idx = d.perm[e] + key.pos;
+          for (int64_t r = 0; r < take; ++r)
+            if (d.host_y[idx[r]] >= m->desc.dims[m->desc.n_layers]) {
+              *stop = PK_RUN_LABEL_BOUNDS;
+              ok = false;
+              break;
+            }
+        }
+      }
+      if (!ok) {
+        more = false;
+        break;
+      }
+      RunStep s;
+      s.driver = driver;
+      s.groups = 0;
+      s.physical = 0;
+      for (int k = 0; k < K; ++k) feeds[k] = pk_feed{nullptr, nullptr, 0, 0, 0};
+      const int slot = (int)(planned % depth);
+      for (size_t i = 0; i < keyed.size();) {
+        size_t j = i;
+        while (j < keyed.size() && keyed[j].first == keyed[i].first) ++j;
+        const RunKey& key = keyed[i].first;
+        const pk_run_dataset& d = ds[key.ds];
+        const int64_t* perm = d.perm[key.epoch - d.epoch0];
+        const int32_t take = (int32_t)std::min<int64_t>(key.batch, d.n - key.pos);
+        const int gi = s.groups;
+        pk_feed f{};
+        if (d.host_x) {  // streamed: gather into this slot's pinned staging, H2D
+          pk_pack::RunStage* g = run_stage(p, slot, gi, std::max<int64_t>(take, driver), d.dim);
+          if (!g) return arg_err(c, "run: staging allocation failed");
+          if ((rc = run_gather(p, slot, g, take, d, perm + key.pos))) return rc;
+          f = pk_feed{g->d, nullptr, 0, take, gi};
+        } else {
+          const int64_t e = key.epoch - d.epoch0;
+          if (!d.device || !d.order || !d.order[e]) return arg_err(c, "run: missing device order");
+          f = pk_feed{d.device, d.order[e], key.pos, take, gi};
+        }
+        for (size_t q = i; q < j; ++q) {
+          const int k = keyed[q].second;
+          feeds[k] = f;
+          s.member.push_back(k);
+          s.take.push_back(take);
+          s.idx.push_back(perm + key.pos);
+        }
+        s.physical += share_inputs ? 1 : (int32_t)(j - i);
+        ++s.groups;
+        i = j;
+      }
+      if ((rc = pk_pack_step_async(p, feeds.data(), &s.ticket))) return rc;
+      for (size_t q = 0; q < s.member.size(); ++q) {
+        pk_run_member& m = sh[s.member[q]];
+        m.steps_done += 1;
+        m.pos += s.take[q];
+      }
+      fly.push_back(std::move(s));
+      ++planned;
+    }
+    if (fly.size() == head) break;
+    // ---- oldest step: result → the real cursors ------------------------------
+    RunStep& s = fly[head++];
+    double* L = losses + (size_t)applied * K;
+    pk_status rs{};
+    rc = pk_pack_step_wait(p, s.ticket, L, &rs);
+    if (rc != PK_OK && rc != PK_ERR_NONFINITE_VALUE && rc != PK_ERR_NONFINITE_GRAD) return rc;
+    uint8_t* A = active + (size_t)applied * K;
+    memset(A, 0, K);
+    if (applied > 0)  // the reference rolls at the top of every later step
+      for (int k : s.member) run_roll(mem[k], ds[mem[k].dataset]);
+    const bool fail = rs.code != PK_OK;
+    for (size_t q = 0; q < s.member.size(); ++q) {
+      const int k = s.member[q];
+      if (rs.code == PK_ERR_NONFINITE_VALUE) break;
+      if (rs.code == PK_ERR_NONFINITE_GRAD && k >= rs.member) continue;  // pack order
+      pk_run_member& m = mem[k];
+      m.steps_done += 1;
+      m.pos += s.take[q];
+      if (m.samples_used)
+        for (int32_t r = 0; r < s.take[q]; ++r) m.samples_used[s.idx[q][r]] += 1;
+      A[k] = 1;
+    }
+    stats[3 * applied] = s.groups;
+    stats[3 * applied + 1] = s.physical;
+    stats[3 * applied + 2] = s.driver;
+    if (fail) {
+      *st = rs;
+      *stop = PK_RUN_FAILED;
+      *done = applied;  // the failed step is reported through st, not counted
+      for (size_t i = head; i < fly.size(); ++i) {  // skipped on the device (halt)
+        pk_status sk{};
+        pk_pack_step_wait(p, fly[i].ticket, L, &sk);
+      }
+      return PK_OK;
+    }
+    ++applied;
+  }
+  *done = applied;
+  return PK_OK;
+}

@@ -487,3 +487,4 @@ extern "C" int pk_member_get_state(pk_member* m, double* params, double* slots, 
 
 // ---------------------------------------------------------------- packs --
 #include "pk_pack.cuh"
+#include "pk_run.cuh"

@@ -25,6 +25,8 @@ from . import engine
 from . import runtime as _rt
 from .data import Dataset, account_cache, epoch_permutation, preprocess
 from .engine import ComputationGraph
+import ctypes as C
+
 from . import _lib
 from ._lib import PK_ERR_NONFINITE_GRAD, PK_ERR_NONFINITE_VALUE, PK_SKIPPED
 
@@ -493,7 +495,117 @@ def _speculate(packed, active, plan, datasets, stop_at_epoch_end, buf):
         return None
 
 
-def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16) -> list:
+def _native_run(packed: PackedModel, datasets, max_steps: int, depth: int):
+    """packed_run through the library's native driver (pk_pack_run): the same
+    plan / apply semantics as the Python loop below, host cost per step a few
+    microseconds.  Returns (loss dicts, finished) — finished False means the
+    remaining steps need the Python loop (a label out of bounds)."""
+    rt = _rt.runtime()
+    out = []
+    K = len(packed.members)
+    stream = _rt.input_mode() == "stream"
+    bindings = sorted({h.dataset_binding for h in packed.members})
+    for h in packed.members:
+        if datasets[h.dataset_binding].dim != h.arch.input_dim:
+            return out, False  # the Python planner raises ShapeMismatch
+    while len(out) < max_steps:
+        try:
+            active = _active_members(packed, datasets, False)
+        except ReplanNeeded:
+            return out, True
+        dpack = packed._device_pack(rt)
+        mem = (_lib.RunMember * K)()
+        keep = []
+        for k, h in enumerate(packed.members):
+            c = h.cursor
+            m = mem[k]
+            m.dataset = bindings.index(h.dataset_binding)
+            m.batch = h.batch_size
+            m.epoch, m.pos, m.steps_done = c.epoch_index, c.pos, c.steps_done
+            m.target_steps = h.target_steps
+            su = c.samples_used
+            if su is not None:
+                if su.dtype != np.int64 or not su.flags.c_contiguous:
+                    c.samples_used = su = np.ascontiguousarray(su, dtype=np.int64)
+                m.samples_used = su.ctypes.data
+        dsa = (_lib.RunDataset * len(bindings))()
+        for i, b in enumerate(bindings):
+            ds = datasets[b]
+            epochs = [h.cursor.epoch_index for h in packed.members if h.dataset_binding == b]
+            e0, e1 = min(epochs), max(epochs) + 1  # current epochs and the next one
+            perms = [np.ascontiguousarray(rt.host_order(ds.dataset_id, ds.n, e, _order_fn(ds, e)),
+                                          dtype=np.int64) for e in range(e0, e1 + 1)]
+            pa = (C.c_void_p * len(perms))(*[q.ctypes.data for q in perms])
+            x, y = rt.host_rows_source(ds)
+            d = dsa[i]
+            d.n, d.dim, d.max_label = ds.n, ds.dim, _dataset_max_label(rt, ds)
+            d.host_y = y.ctypes.data
+            d.epoch0, d.n_epochs, d.perm = e0, len(perms), C.cast(pa, C.c_void_p)
+            keep += [perms, pa, x, y]
+            if stream:
+                d.host_x, d.host_ld = x.ctypes.data, x.strides[0] // x.itemsize
+            else:
+                dev = rt.dataset(ds)
+                orders = [rt.order(ds.dataset_id, ds.n, e, _order_fn(ds, e)) for e in range(e0, e1 + 1)]
+                oa = (C.c_void_p * len(orders))(*[o.ptr.value for o in orders])
+                d.device, d.order = dev.ptr.value, C.cast(oa, C.c_void_p)
+                keep += [dev, orders, oa]
+        n = max_steps - len(out)
+        losses = np.empty((n, K), dtype=np.float64)
+        act = np.empty((n, K), dtype=np.uint8)
+        stats = np.empty((n, 3), dtype=np.int32)
+        done, stop, st = C.c_int64(), C.c_int32(), _lib.Status()
+        rt.check(rt.lib.pk_pack_run(dpack.ptr, mem, dsa, len(bindings), int(packed.share_inputs),
+                                    n, int(depth), losses.ctypes.data, act.ctypes.data,
+                                    stats.ctypes.data, C.byref(done), C.byref(st), C.byref(stop)))
+        nd = done.value
+        code = stop.value
+        rows = nd + (1 if code == _lib.PK_RUN_FAILED and nd < n else 0)  # + a partial commit
+        for k, h in enumerate(packed.members):  # cursors → handles
+            c = h.cursor
+            c.epoch_index, c.pos = int(mem[k].epoch), int(mem[k].pos)
+            stepped = int(act[:rows, k].sum())
+            c.steps_done = int(mem[k].steps_done)
+            for _ in range(stepped):
+                h._committed()
+        mids = [h.model_id for h in packed.members]
+        for i in range(nd):
+            out.append({mids[k]: float(losses[i, k]) for k in range(K) if act[i, k]})
+        if nd:
+            g, ph, dr = (int(v) for v in stats[nd - 1])
+            packed.last_step_stats = {"physical_inputs": ph, "groups": g, "driver_batch": dr}
+        if code == _lib.PK_RUN_FAILED:
+            who = packed.members[st.member]
+            # on a gradient error the members before `who` committed inside the
+            # library; the failed step's losses are not returned (as in Python)
+            if st.code == PK_ERR_NONFINITE_VALUE:
+                raise engine.EngineError(f"non-finite value at node {_node_name(who, st.index)!r}")
+            raise engine.NonFiniteGradient(_grad_name(who, st.index))
+        if code == _lib.PK_RUN_LABEL_BOUNDS:
+            return out, False
+        if code == _lib.PK_RUN_NO_MEMBER and len(out) < max_steps:
+            return out, True
+        # PK_RUN_NEED_PERM: loop with the next epochs' permutations
+    return out, True
+
+
+def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16,
+               native: bool = True) -> list:
+    """Up to `max_steps` packed_step calls with up to `depth` in flight.  The
+    native driver (pk_pack_run) plans and applies the steps in the library;
+    the Python sliding window below is the same loop (and the fallback for
+    anything the native loop hands back).  Both produce the reference
+    packed_step loop's state bit for bit."""
+    out = []
+    if native and max_steps > 0 and not _rt.env_flag("PK_PY_RUN"):
+        out, finished = _native_run(packed, datasets, max_steps, depth)
+        packed._spec = None
+        if finished or len(out) >= max_steps:
+            return out
+    return out + _py_run(packed, datasets, max_steps - len(out), depth)
+
+
+def _py_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16) -> list:
     """Up to `max_steps` packed_step calls (reference semantics, packing.py:185-264)
     with up to `depth` steps in flight on the device: a sliding window — the
     host plans step n+depth from shadow cursors (epoch rolls and finished

@@ -34,6 +34,11 @@ def set_input_mode(mode: str):
     _DEFAULT["inputs"] = mode
 
 
+def env_flag(name: str) -> bool:
+    """A set, non-empty environment switch (measurement / A-B toggles)."""
+    return bool(os.environ.get(name))
+
+
 def input_mode() -> str:
     return _DEFAULT["inputs"] or _ENV["inputs"]
 
