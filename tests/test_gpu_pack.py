@@ -748,6 +748,66 @@ def test_packed_run_equals_packed_step_loop():
     assert pa.last_step_stats == pb.last_step_stats
 
 
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+def test_native_run_matches_python_loop_two_datasets(mode, monkeypatch):
+    """pk_pack_run (the library's multi-step driver) against the Python
+    sliding window and the packed_step loop: two datasets, four batch sizes
+    (several input groups), many epoch rolls (the driver returns for the next
+    epochs' permutations), members finishing at different steps; losses,
+    params, cursors, samples_used and last_step_stats bit-identical."""
+    ds = {"a": data.synth_dataset(70, 12, 4, seed=41), "b": data.synth_dataset(45, 8, 3, seed=42)}
+
+    def make():
+        spec = [("n0", 12, 4, "a", "adam", 16, 60), ("n1", 12, 4, "a", "sgd", 16, 45),
+                ("n2", 12, 4, "a", "momentum", 9, 80), ("n3", 8, 3, "b", "adagrad", 7, 70),
+                ("n4", 8, 3, "b", "sgd", 20, 33)]
+        hs = [packing.make_handle(m, packing.MLPArch(d, (8,), c, "tanh"), o, 0.03, b, t, bind, i)
+              for i, (m, d, c, bind, o, b, t) in enumerate(spec)]
+        return hs, packing.dedup_inputs(packing.pack_models(hs))
+
+    runtime.set_input_mode(mode)
+    try:
+        hl, pl = make()
+        ll = []
+        while any(not h.finished for h in hl):
+            ll.append(packing.packed_step(pl, ds))
+        hn, pn = make()
+        ln = packing.packed_run(pn, ds, 1 << 30, depth=8)
+        monkeypatch.setenv("PK_PY_RUN", "1")
+        hp, pp = make()
+        lp = packing.packed_run(pp, ds, 1 << 30, depth=8)
+    finally:
+        runtime.set_input_mode("resident")
+    assert ll == ln == lp
+    for a, b, c in zip(hl, hn, hp):
+        assert _maxdiff(a, b) == 0.0 and _maxdiff(a, c) == 0.0
+        for x in (b, c):
+            assert (a.cursor.steps_done, a.cursor.epoch_index, a.cursor.pos) == \
+                (x.cursor.steps_done, x.cursor.epoch_index, x.cursor.pos)
+            np.testing.assert_array_equal(a.cursor.samples_used, x.cursor.samples_used)
+            assert a.optimizer.step_counter == x.optimizer.step_counter
+    assert pl.last_step_stats == pn.last_step_stats == pp.last_step_stats
+
+
+def test_native_run_hands_label_errors_back():
+    """A batch whose labels exceed a member's classes: the native driver stops
+    before that step and the Python planner raises the reference's IndexError
+    at exactly the same step."""
+    d = data.synth_dataset(60, 6, 5, seed=43)
+    ds = {"d": d}
+    hs = [packing.make_handle("z0", packing.MLPArch(6, (4,), 3, "relu"), "sgd", 0.05, 10, 100, "d", 0)]
+    packed = packing.pack_models(hs)
+    with pytest.raises(IndexError):
+        packing.packed_run(packed, ds, 100)
+    ref = packing.make_handle("z0", packing.MLPArch(6, (4,), 3, "relu"), "sgd", 0.05, 10, 100, "d", 0)
+    pr = packing.pack_models([ref])
+    with pytest.raises(IndexError):
+        for _ in range(100):
+            packing.packed_step(pr, ds)
+    assert hs[0].cursor.steps_done == ref.cursor.steps_done
+    assert _maxdiff(hs[0], ref) == 0.0
+
+
 def test_packed_run_stops_exactly_at_a_failing_step():
     """A non-finite gradient inside a pipelined run raises at that step; the
     device skipped every step enqueued behind it, so the state equals the
