@@ -531,8 +531,17 @@ def _native_run(packed: PackedModel, datasets, max_steps: int, depth: int):
         dsa = (_lib.RunDataset * len(bindings))()
         for i, b in enumerate(bindings):
             ds = datasets[b]
-            epochs = [h.cursor.epoch_index for h in packed.members if h.dataset_binding == b]
-            e0, e1 = min(epochs), max(epochs) + 1  # current epochs and the next one
+            # every epoch the remaining steps can reach (each re-entry drains the
+            # in-flight window, so give the driver the whole horizon at once)
+            mine = [h for h in packed.members if h.dataset_binding == b]
+            e0 = min(h.cursor.epoch_index for h in mine)
+            e1 = e0
+            for h in mine:
+                left = min(h.target_steps - h.cursor.steps_done, max_steps - len(out))
+                if left > 0:
+                    reach = h.cursor.pos + left * h.batch_size
+                    e1 = max(e1, h.cursor.epoch_index + -(-reach // ds.n))
+            e1 = min(e1, e0 + 64)
             perms = [np.ascontiguousarray(rt.host_order(ds.dataset_id, ds.n, e, _order_fn(ds, e)),
                                           dtype=np.int64) for e in range(e0, e1 + 1)]
             pa = (C.c_void_p * len(perms))(*[q.ctypes.data for q in perms])

@@ -10,6 +10,7 @@ timeout 600 python -m pytest tests -m gpu -x -q --timeout 120 > $OUT/pytest_gpu.
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 400 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 400 python bench.py --workload k16 --cpu-seconds 0 --hyperband-r 0 > $OUT/bench_k16.json 2> $OUT/bench_k16.err
+timeout 400 python bench.py --workload wide16 --cpu-seconds 0 --hyperband-r 0 > $OUT/bench_wide16.json 2> $OUT/bench_wide16.err
 timeout 300 python bench.py --impl reference --steps 20 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches.csv python tools/profile_step.py --steps 20 > $OUT/ncu_launch.log 2>&1
