@@ -75,6 +75,8 @@ struct pk_pack {
   // H2D overlaps step n's kernels; the pack stream waits on ev_copy[slot]
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[kRing] = {};
+  // capacities of the recycled context blocks this pack holds
+  size_t cap_members = 0, cap_blob = 0, cap_done = 0, cap_tiles = 0, cap_desc = 0, cap_ring = 0;
 };
 
 template <typename T>
@@ -745,24 +747,26 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
   p->ring_stride = (int32_t)align_up(16 + 8 * (size_t)k, 64);
   auto fail = [&](cudaError_t e) {
     c->err = std::string("pack alloc: ") + cudaGetErrorString(e);
-    if (p->d_members) cudaFree(p->d_members);
-    if (p->d_blob) cudaFree(p->d_blob);
-    if (p->d_tiles) cudaFree(p->d_tiles);
-    if (p->d_done) cudaFree(p->d_done);
-    if (p->h_desc) cudaFreeHost(p->h_desc);
-    if (p->h_ring) cudaFreeHost(p->h_ring);
+    ctx_release(c, 0, p->d_members, p->cap_members);
+    ctx_release(c, 0, p->d_blob, p->cap_blob);
+    ctx_release(c, 0, p->d_tiles, p->cap_tiles);
+    ctx_release(c, 0, p->d_done, p->cap_done);
+    ctx_release(c, 1, p->h_desc, p->cap_desc);
+    ctx_release(c, 2, p->h_ring, p->cap_ring);
     delete p;
     return e == cudaErrorMemoryAllocation ? PK_ERR_OOM : PK_ERR_CUDA;
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&p->d_members, hm.size())) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc((void**)&p->d_blob, p->blob_bytes)) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc((void**)&p->d_done, 16)) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc((void**)&p->d_tiles, std::max<size_t>(1, all.size()) * sizeof(Tile))) != cudaSuccess)
+  if ((e = ctx_alloc(c, 0, hm.size(), &p->d_members, &p->cap_members)) != cudaSuccess) return fail(e);
+  if ((e = ctx_alloc(c, 0, p->blob_bytes, (void**)&p->d_blob, &p->cap_blob)) != cudaSuccess)
     return fail(e);
-  if ((e = cudaHostAlloc((void**)&p->h_desc, p->blob_bytes * kRing, cudaHostAllocDefault)) != cudaSuccess)
+  if ((e = ctx_alloc(c, 0, 16, (void**)&p->d_done, &p->cap_done)) != cudaSuccess) return fail(e);
+  if ((e = ctx_alloc(c, 0, std::max<size_t>(1, all.size()) * sizeof(Tile), (void**)&p->d_tiles,
+                     &p->cap_tiles)) != cudaSuccess)
     return fail(e);
-  if ((e = cudaHostAlloc((void**)&p->h_ring, (size_t)p->ring_stride * kRing, cudaHostAllocMapped)) !=
+  if ((e = ctx_alloc(c, 1, p->blob_bytes * kRing, (void**)&p->h_desc, &p->cap_desc)) != cudaSuccess)
+    return fail(e);
+  if ((e = ctx_alloc(c, 2, (size_t)p->ring_stride * kRing, (void**)&p->h_ring, &p->cap_ring)) !=
       cudaSuccess)
     return fail(e);
   if ((e = cudaHostGetDevicePointer((void**)&p->d_ring, p->h_ring, 0)) != cudaSuccess) return fail(e);
@@ -778,7 +782,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
       off += ph.host.size();
     }
   for (int i = 0; i < kRing; ++i) {
-    cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
+    p->ev[i] = ctx_event(c);
     p->ev_pending[i] = false;
   }
   const char* tr = getenv("PK_TRACE");
@@ -810,11 +814,11 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
   cudaStreamSynchronize(c->stream);
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
-  for (int i = 0; i < kRing; ++i) cudaEventDestroy(p->ev[i]);
-  cudaFree(p->d_members);
-  cudaFree(p->d_blob);
-  cudaFree(p->d_tiles);
-  cudaFree(p->d_done);
+  for (int i = 0; i < kRing; ++i) c->events.push_back(p->ev[i]);
+  ctx_release(c, 0, p->d_members, p->cap_members);
+  ctx_release(c, 0, p->d_blob, p->cap_blob);
+  ctx_release(c, 0, p->d_tiles, p->cap_tiles);
+  ctx_release(c, 0, p->d_done, p->cap_done);
   if (p->d_trace) cudaFree(p->d_trace);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (auto& e : p->ev_copy)
@@ -824,8 +828,8 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
     if (s.hx) cudaFreeHost(s.hx);
     if (s.hy) cudaFreeHost(s.hy);
   }
-  cudaFreeHost(p->h_desc);
-  cudaFreeHost(p->h_ring);
+  ctx_release(c, 1, p->h_desc, p->cap_desc);
+  ctx_release(c, 2, p->h_ring, p->cap_ring);
   delete p;
   return PK_OK;
 }

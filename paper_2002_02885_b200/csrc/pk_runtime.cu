@@ -39,7 +39,66 @@ struct pk_ctx {
   std::string err;
   uint64_t bytes = 0;
   size_t esize() const { return dtype == PK_F64 ? 8 : 4; }
+  // recycled per-pack buffers and events: Hyperband builds and drops a pack
+  // per group evaluation, and cudaFree / cudaFreeHost / cudaHostAlloc cost
+  // milliseconds each (kind 0 device, 1 pinned, 2 pinned + mapped)
+  struct Block {
+    void* p;
+    size_t cap;
+    int kind;
+  };
+  std::vector<Block> blocks;
+  std::vector<cudaEvent_t> events;
 };
+
+static const char* const kAllocKind[] = {"device", "pinned", "mapped"};
+
+// a cached block of `kind` with bytes <= cap <= 4·bytes, else a fresh one
+static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size_t* cap) {
+  bytes = std::max<size_t>(bytes, 256);
+  size_t best = SIZE_MAX, bi = 0;
+  for (size_t i = 0; i < c->blocks.size(); ++i) {
+    const auto& b = c->blocks[i];
+    if (b.kind == kind && b.cap >= bytes && b.cap <= 4 * bytes && b.cap < best) {
+      best = b.cap;
+      bi = i;
+    }
+  }
+  if (best != SIZE_MAX) {
+    *out = c->blocks[bi].p;
+    *cap = best;
+    c->blocks.erase(c->blocks.begin() + bi);
+    return cudaSuccess;
+  }
+  *cap = bytes;
+  if (kind == 0) return cudaMalloc(out, bytes);
+  return cudaHostAlloc(out, bytes, kind == 1 ? cudaHostAllocDefault : cudaHostAllocMapped);
+}
+
+static void ctx_free_block(const pk_ctx::Block& b) {
+  if (b.kind == 0) cudaFree(b.p);
+  else cudaFreeHost(b.p);
+}
+
+static void ctx_release(pk_ctx* c, int kind, void* p, size_t cap) {
+  if (!p) return;
+  c->blocks.push_back({p, cap, kind});
+  if (c->blocks.size() > 512) {  // bounded: drop the oldest
+    ctx_free_block(c->blocks.front());
+    c->blocks.erase(c->blocks.begin());
+  }
+}
+
+static cudaEvent_t ctx_event(pk_ctx* c) {
+  if (!c->events.empty()) {
+    cudaEvent_t e = c->events.back();
+    c->events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
 
 struct pk_dataset {
   pk_ctx* ctx;
@@ -122,6 +181,8 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (!c) return PK_ERR_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (const auto& b : c->blocks) ctx_free_block(b);
+  for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PK_OK;
