@@ -185,6 +185,11 @@ constexpr int kStaticSmemMargin = 16 * 1024;
 
 static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device) {
   if (d.n_layers != 2 || d.dims[2] > pk::M1_MAXC || d.max_rows > pk::M1_MAXR) return false;
+  if (getenv("PK_NO_MLP1")) return false;  // A/B switch for measurements
+  // f64 members: the phase kernels are faster at every Hyperband shape
+  // (784-16-10: 45 vs 78 µs per step at K=1, 74 vs 128 at K=8 — its 8-unit
+  // column blocks leave a narrow member with 2 CTAs walking all 784 inputs)
+  if (dtype == PK_F64) return false;
   int optin = 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
       cudaSuccess)

@@ -10,6 +10,7 @@ interface so `pack_opt_*` and `load_model(device=...)` work unchanged.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 _CTL_BYTES = 80          # sizeof(pk::MemberCtl)
@@ -112,6 +113,8 @@ def uses_fused_mlp1(arch, optimizer: str, batch_size: int, precision="f32") -> b
             uses_m1x(arch, optimizer, batch_size, precision):
         return False
     if len(arch.hidden) != 1 or arch.classes > _M1_MAXC or batch_size > _M1_MAXR:
+        return False
+    if precision == "f64" or os.environ.get("PK_NO_MLP1"):  # phase kernels win in f64
         return False
     es = 8 if precision == "f64" else 4
     vec = 16 // es
