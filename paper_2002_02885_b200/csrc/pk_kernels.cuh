@@ -132,6 +132,8 @@ struct PhaseArgs {
   int32_t K;
   int32_t is_last;     // run FINALIZE in the last CTA
   int32_t prefetch;    // issue L2 prefetch of params/slots (first phase)
+  int32_t first;       // first launch of a step: inside a multi-step graph it waits
+                       // for the previous step (PDL) before touching member state
   unsigned long long* trace;  // profiling: kTraceSlots stamps per CTA, or nullptr
   int32_t cs;          // cluster size of this launch (k_m1t_fwd: input splits)
   int32_t stages;      // k_m1t_bwd: input-tile stages in flight
@@ -201,6 +203,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+// kernel entry: a step's first launch waits for the previous step of a
+// multi-step graph (its parameters, parity and halt flag) before letting its
+// own dependents start; later launches release their dependents at once
+#define pdl_begin(P)        \
+  do {                      \
+    if ((P).first) pdl_wait(); \
+    pdl_launch();           \
+  } while (0)
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred) {
@@ -1072,7 +1082,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if (P.prefetch) prefetch_params(P);
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
@@ -1106,7 +1116,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1134,7 +1144,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1x_step(const __grid_constant__ Phas
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1158,7 +1168,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1185,7 +1195,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1208,7 +1218,7 @@ __global__ void __launch_bounds__(T_BWD_NT, 1) k_m1t_bwd(const __grid_constant__
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1231,7 +1241,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_fwd(const __grid_constant__ Phas
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   if (P.prefetch) prefetch_params(P);
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
@@ -1245,7 +1255,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp1_bwd(const __grid_constant__ Phas
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_launch();
+  pdl_begin(P);
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   if (f.take != 0 && !halted(P)) {

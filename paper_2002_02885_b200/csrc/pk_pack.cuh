@@ -75,6 +75,12 @@ struct pk_pack {
   // H2D overlaps step n's kernels; the pack stream waits on ev_copy[slot]
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[kRing] = {};
+  // pk_pack_run's multi-step graph: `multi_n` whole steps captured back to
+  // back, each step's first launch chained to the previous step by PDL
+  int multi_n = 0;
+  cudaGraph_t graph_multi = nullptr;
+  cudaGraphExec_t exec_multi = nullptr;
+  std::vector<std::vector<Node>> nodes_multi;
   // capacities of the recycled context blocks this pack holds
   size_t cap_members = 0, cap_blob = 0, cap_done = 0, cap_tiles = 0, cap_desc = 0, cap_ring = 0;
 };
@@ -623,6 +629,7 @@ static int launch_phases(pk_pack* p, const std::vector<Phase>& phases, int only 
     a.K = p->K;
     a.is_last = finalize && (int)i == last;
     a.prefetch = (int)i == first;
+    a.first = (int)i == first;
     if (p->d_trace && &phases == &p->train) {  // train phases: [phase][cta][slot]
       size_t off = 0;
       for (size_t j = 0; j < i; ++j) off += (size_t)phases[j].ntiles * pk::kTraceSlots;
@@ -819,6 +826,8 @@ extern "C" int pk_pack_destroy(pk_pack* p) {
   cudaStreamSynchronize(c->stream);
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
+  if (p->exec_multi) cudaGraphExecDestroy(p->exec_multi);
+  if (p->graph_multi) cudaGraphDestroy(p->graph_multi);
   for (int i = 0; i < kRing; ++i) c->events.push_back(p->ev[i]);
   ctx_release(c, 0, p->d_members, p->cap_members);
   ctx_release(c, 0, p->d_blob, p->cap_blob);
