@@ -103,10 +103,10 @@ __device__ __forceinline__ V x_tree(const V* p, int st) {
                add(add(p[4 * st], p[5 * st]), add(p[6 * st], p[7 * st])));
 }
 
-template <int RP, int BPC, int OPT>
+template <int RP, int BPC>
 __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
                                            const FeedDev<float>& f, int q, int Sb) {
-  constexpr int NS = OPT == PK_OPT_SGD ? 0 : (OPT == PK_OPT_ADAM ? 2 : 1);
+  const int OPT = M.opt, NS = M.n_slots;
   constexpr int U = X_UB * BPC, WLD = U + 4, CW = U / 4;
   constexpr int NI = RP * U / 512;           // work items per thread: 1, 2, 4
   constexpr int RQ = RP / 4, CELLS = RP * U / 16, G8 = 8 / NI;
@@ -114,7 +114,7 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
   static_assert(NI == 1 || NI == 2 || NI == 4, "RP * U must be 512, 1024 or 2048");
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take;
-  constexpr int ns = NS;
+  const int ns = NS;
   const int u0 = q * U;
   const int nu = max(0, min(U, H - u0));  // own valid units (H % 4 == 0: whole quads)
   const int nblk = x_nblk(H);
@@ -541,27 +541,15 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
   umma::cluster_wait();  // peers have finished reading this CTA's partials
 }
 
-// one instantiation per (rows pad, blocks per CTA, optimizer): every index and
-// the optimizer are constants, so each hot loop is short straight-line code
-template <int RP, int BPC>
-__device__ __forceinline__ void m1x_opt(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                                        int q, int Sb) {
-  switch (M.opt) {
-    case PK_OPT_SGD: m1x_step_t<RP, BPC, PK_OPT_SGD>(sm, M, f, q, Sb); break;
-    case PK_OPT_MOMENTUM: m1x_step_t<RP, BPC, PK_OPT_MOMENTUM>(sm, M, f, q, Sb); break;
-    case PK_OPT_ADAGRAD: m1x_step_t<RP, BPC, PK_OPT_ADAGRAD>(sm, M, f, q, Sb); break;
-    default: m1x_step_t<RP, BPC, PK_OPT_ADAM>(sm, M, f, q, Sb); break;
-  }
-}
-
+// one instantiation per (rows pad, blocks per CTA): every index is a constant
 __device__ void m1x_step(char* sm, const MemberDev<float>& M, const FeedDev<float>& f, int q,
                          int bpc, int Sb) {
   switch (m1_rows_pad(M.max_rows) * 8 + bpc) {
-    case 32 * 8 + 1: m1x_opt<32, 1>(sm, M, f, q, Sb); break;
-    case 32 * 8 + 2: m1x_opt<32, 2>(sm, M, f, q, Sb); break;
-    case 32 * 8 + 4: m1x_opt<32, 4>(sm, M, f, q, Sb); break;
-    case 64 * 8 + 1: m1x_opt<64, 1>(sm, M, f, q, Sb); break;
-    case 64 * 8 + 2: m1x_opt<64, 2>(sm, M, f, q, Sb); break;
+    case 32 * 8 + 1: m1x_step_t<32, 1>(sm, M, f, q, Sb); break;
+    case 32 * 8 + 2: m1x_step_t<32, 2>(sm, M, f, q, Sb); break;
+    case 32 * 8 + 4: m1x_step_t<32, 4>(sm, M, f, q, Sb); break;
+    case 64 * 8 + 1: m1x_step_t<64, 1>(sm, M, f, q, Sb); break;
+    case 64 * 8 + 2: m1x_step_t<64, 2>(sm, M, f, q, Sb); break;
     default: __trap();
   }
 }
