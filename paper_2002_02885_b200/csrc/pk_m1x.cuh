@@ -457,12 +457,9 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
   }
   if (work) {
     for (int c = 0; c < nch; ++c) {
-      if (c == 4) PK_TRACE(10);
       cp_wait_n(issued_b - c - 1);
       __syncthreads();  // chunk c landed; chunk c-1's optimizer pass is done
-      if (c == 4) PK_TRACE(11);
       if (c >= 1 && c - 1 + Sb < nch) issue_b(c - 1 + Sb);
-      if (c == 4) PK_TRACE(12);
       const float* X = ring + (c % Sb) * SB;
       const float* W = X + RP * X_LD;
       const int k0 = c * X_KC, nk = min(X_KC, D - k0);
@@ -506,9 +503,7 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
         red4[(bgrp * CW + buq) * 64 + 4 * dq + (dd ^ sw)] =
             make_float4(x_fold<NI>(bacc, 4 * dd), x_fold<NI>(bacc, 4 * dd + 1),
                         x_fold<NI>(bacc, 4 * dd + 2), x_fold<NI>(bacc, 4 * dd + 3));
-      if (c == 4) PK_TRACE(13);
       __syncthreads();
-      if (c == 4) PK_TRACE(14);
       // optimizer pass: lane pairs (j even/odd) on 16 consecutive rows d → full
       // 32-byte sectors to HBM, conflict-free shared reads
 #pragma unroll
