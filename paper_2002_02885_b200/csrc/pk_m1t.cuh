@@ -1291,6 +1291,52 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   umma::fence_after();
   if (warp < 8) {
     // -------------------------------------------------------------- epilogue
+    // ---- W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3), element e
+    //      of the unit tile by the tile's group gi ≡ e (mod ngr): done here,
+    //      while the producers stage and the MMA warp multiplies tile 0
+    {
+      const int gi = kt0 / G, ngr = (cdiv_d(D, T_BK) + G - 1) / G;
+      for (int e = gi + ngr * tid; e < nu * C; e += ngr * 256) {
+        const int j = e / C, c = e % C;
+        float g = 0.f;
+        for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * LDL + c], g);
+        if (fault == 0) g = NAN;
+        badW1 |= !finite(g);
+        float w = sW1[e], s0 = ns >= 1 ? sW1[T_BU * C + e] : 0.f,
+              s1 = ns >= 2 ? sW1[2 * T_BU * C + e] : 0.f;
+        opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+        const int64_t i = M.w_off[1] + (int64_t)u0 * C + e;
+        Pn[i] = w;
+        if (ns >= 1) Sn[i] = s0;
+        if (ns >= 2) Sn[NP + i] = s1;
+      }
+      if (utile == 0) {
+        for (int c = gi + ngr * tid; c < C; c += ngr * 256) {
+          float g = 0.f;
+          for (int r = 0; r < R; ++r) g += sL[r * LDL + c];
+          if (fault == 1) g = NAN;
+          badb1 |= !finite(g);
+          const int64_t i = M.b_off[1] + c;
+          float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
+          opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+          Pn[i] = w;
+          if (ns >= 1) Sn[i] = s0;
+          if (ns >= 2) Sn[NP + i] = s1;
+        }
+      }
+      for (int j = gi + ngr * tid; j < nu; j += ngr * 256) {
+        float g = 0.f;
+        for (int r = 0; r < R; ++r) g += sdZ[r * T_BU + j];
+        if (fault == 3) g = NAN;
+        badb0 |= !finite(g);
+        const int64_t i = M.b_off[0] + u0 + j;
+        float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
+        opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
+        Pn[i] = w;
+        if (ns >= 1) Sn[i] = s0;
+        if (ns >= 2) Sn[NP + i] = s1;
+      }
+    }
     // warp w: TMEM lane quarter w % 4 (input rows k), column half w / 4
     const int k = 32 * (warp & 3) + lane, ch16 = (warp >> 2) * 16;
     for (int i = 0; i < ng; ++i) {
@@ -1477,51 +1523,6 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   __syncthreads();
   umma::fence_after();
   PK_TRACE(3);
-  // ---- W1[units, :] (grad 0), b1 (grad 1), b0[units] (grad 3): element e
-  //      of the unit tile is updated by the tile's group gi ≡ e (mod ngr)
-  {
-    const int gi = kt0 / G, ngr = (cdiv_d(D, T_BK) + G - 1) / G;
-    for (int e = gi + ngr * tid; e < nu * C; e += ngr * BT) {
-      const int j = e / C, c = e % C;
-      float g = 0.f;
-      for (int r = 0; r < R; ++r) g = fmaf(sA0[r * T_BU + j], sL[r * LDL + c], g);
-      if (fault == 0) g = NAN;
-      badW1 |= !finite(g);
-      float w = sW1[e], s0 = ns >= 1 ? sW1[T_BU * C + e] : 0.f,
-            s1 = ns >= 2 ? sW1[2 * T_BU * C + e] : 0.f;
-      opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
-      const int64_t i = M.w_off[1] + (int64_t)u0 * C + e;
-      Pn[i] = w;
-      if (ns >= 1) Sn[i] = s0;
-      if (ns >= 2) Sn[NP + i] = s1;
-    }
-    if (utile == 0) {
-      for (int c = gi + ngr * tid; c < C; c += ngr * BT) {
-        float g = 0.f;
-        for (int r = 0; r < R; ++r) g += sL[r * LDL + c];
-        if (fault == 1) g = NAN;
-        badb1 |= !finite(g);
-        const int64_t i = M.b_off[1] + c;
-        float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
-        opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
-        Pn[i] = w;
-        if (ns >= 1) Sn[i] = s0;
-        if (ns >= 2) Sn[NP + i] = s1;
-      }
-    }
-    for (int j = gi + ngr * tid; j < nu; j += ngr * BT) {
-      float g = 0.f;
-      for (int r = 0; r < R; ++r) g += sdZ[r * T_BU + j];
-      if (fault == 3) g = NAN;
-      badb0 |= !finite(g);
-      const int64_t i = M.b_off[0] + u0 + j;
-      float w = Pc[i], s0 = ns >= 1 ? Sc[i] : 0.f, s1 = ns >= 2 ? Sc[NP + i] : 0.f;
-      opt_step1(M.opt, lr, wd, bc1, bc2, w, s0, s1, g);
-      Pn[i] = w;
-      if (ns >= 1) Sn[i] = s0;
-      if (ns >= 2) Sn[NP + i] = s1;
-    }
-  }
   PK_TRACE(4);
   if (badW1) flag_min(&M.ctl->bad_grad, 0);
   if (badb1) flag_min(&M.ctl->bad_grad, 1);
