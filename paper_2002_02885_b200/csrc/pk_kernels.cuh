@@ -227,6 +227,22 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// one line toward L1 (non-blocking): a step's first kernel touches the halt
+// flag, the member's control block and the batch's gather index before any
+// of them is used — prefetched together they cost one round trip, not three
+__device__ __forceinline__ void l1_prefetch(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <typename T>
+__device__ __forceinline__ void first_touch(const PhaseArgs<T>& P, const MemberDev<T>* m,
+                                            const FeedDev<T>& f) {
+  if (threadIdx.x == 0) {
+    if (P.halt) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.halt));  // read volatile: L2
+    l1_prefetch(m->ctl);
+  }
+  if (f.rows && (int)threadIdx.x < f.take && (threadIdx.x & 31) == 0) l1_prefetch(f.rows + threadIdx.x);
+}
+
 // bulk (TMA-engine) prefetch of a global range into L2
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
@@ -1130,6 +1146,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
+    first_touch(P, reinterpret_cast<const MemberDev<T>*>(mem_of(P, t.member)), f);
     // the member's descriptor in shared memory: every field read is an LDS,
     // not a global load on the critical path
     __shared__ MemberDev<float> sM;
@@ -1182,6 +1199,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1s_fwd(const __grid_constant__ Phase
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
+    first_touch(P, reinterpret_cast<const MemberDev<T>*>(mem_of(P, t.member)), f);
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
@@ -1209,6 +1227,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
+    first_touch(P, reinterpret_cast<const MemberDev<T>*>(mem_of(P, t.member)), f);
     __shared__ MemberDev<float> sM;
     if (threadIdx.x < sizeof(MemberDev<float>) / 4)
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
