@@ -1419,11 +1419,11 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
           cp_async<16>(sW + kk * T_BWLD + 4 * c, src + (int64_t)(k0 + kk) * H + 4 * c, true);
         }
         // the epilogue reads this tile's optimizer slots from global: pull
-        // them into L2 now, one bulk prefetch per row segment
+        // them into L2 now, one line prefetch per row segment
         for (int e = pt; e < ns * nk; e += NP3) {
           const int s2 = e / nk, kk = e % nk;
-          l2_prefetch(Sc + (int64_t)s2 * NP + M.w_off[0] + (int64_t)(k0 + kk) * H + u0,
-                      (uint32_t)(nu * 4));
+          l2_prefetch_lines(Sc + (int64_t)s2 * NP + M.w_off[0] + (int64_t)(k0 + kk) * H + u0,
+                            (uint32_t)(nu * 4));
         }
       }
       for (int e = pt; e < R * cx; e += NP3) {

@@ -68,6 +68,15 @@ def main():
             if len(v):
                 print(f"   {name:6s} min {v.min() / 1e3:8.2f}  med {statistics.median(v) / 1e3:8.2f}"
                       f"  max {v.max() / 1e3:8.2f} us   (n={len(v)})")
+        if os.environ.get("PK_TRACE_BY_MEMBER") and i == len(phases) - 1:
+            # last phase: per-member medians of ready→done (tiles are member-major)
+            per = max(1, ctas // len(hs))
+            t0m = blk[:, 1]
+            for k, h in enumerate(hs):
+                seg = blk[k * per:(k + 1) * per]
+                d = (seg[:, 5] - seg[:, 1]) / 1e3
+                print(f"   member {k} {h.optimizer.kind:9s} ready→done med {statistics.median(d):6.2f}"
+                      f"  max {d.max():6.2f} us")
         if int(os.environ.get("PK_M1X_DEBUG", "0")) & 32:  # k_m1x: clock64 at chunks 4 / 8
             cyc = (blk[:, 7] - blk[:, 6]) / 4.0
             ns = (blk[:, 12] - blk[:, 11]) / 4.0
