@@ -1034,6 +1034,19 @@ __device__ __forceinline__ void opt_x(int opt, float lr, float wd, float ib1, fl
   }
 }
 
+// 256-bit global accesses (sm_100): one full 32-byte sector per lane
+__device__ __forceinline__ void ld8g(const float* p, float4& a, float4& b) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st8g(float* p, float4 a, float4 b) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x), "f"(a.y),
+               "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
+
 // the member's optimizer on four elements
 __device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1, float bc2,
                                           float4& w, float4& s0, float4& s1, float4 g) {
@@ -1339,6 +1352,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     }
     // warp w: TMEM lane quarter w % 4 (input rows k), column half w / 4
     const int k = 32 * (warp & 3) + lane, ch16 = (warp >> 2) * 16;
+    // full 16-unit halves on 32-byte boundaries: 256-bit slot / param I/O
+    const bool wide8 = H % 8 == 0 && NP % 8 == 0 && u0 % 8 == 0 && ch16 + 16 <= nu;
     for (int i = 0; i < ng; ++i) {
       const int t = i & 1, st = i % S;
       const int k0 = (kt0 + i) * T_BK, nk = min(T_BK, D - k0);
@@ -1347,13 +1362,23 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       float4 sl0[4], sl1[4];
       {
         const int64_t ib = M.w_off[0] + (int64_t)(k0 + min(k, nk - 1)) * H + u0 + ch16;
+        if (wide8 && k < nk) {  // two 256-bit loads per slot block
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          const bool ok = k < nk && ch16 + 4 * qd < nu;
-          sl0[qd] = ns >= 1 && ok ? *reinterpret_cast<const float4*>(Sc + ib + 4 * qd)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-          sl1[qd] = ns >= 2 && ok ? *reinterpret_cast<const float4*>(Sc + NP + ib + 4 * qd)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int h = 0; h < 2; ++h) {
+            if (ns >= 1) ld8g(Sc + ib + 8 * h, sl0[2 * h], sl0[2 * h + 1]);
+            else sl0[2 * h] = sl0[2 * h + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ns >= 2) ld8g(Sc + NP + ib + 8 * h, sl1[2 * h], sl1[2 * h + 1]);
+            else sl1[2 * h] = sl1[2 * h + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            const bool ok = k < nk && ch16 + 4 * qd < nu;
+            sl0[qd] = ns >= 1 && ok ? *reinterpret_cast<const float4*>(Sc + ib + 4 * qd)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            sl1[qd] = ns >= 2 && ok ? *reinterpret_cast<const float4*>(Sc + NP + ib + 4 * qd)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
       }
       umma::mbar_wait(&bar[6 + t], (uint32_t)((i >> 1) & 1));
@@ -1374,7 +1399,35 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
                      : "memory");
       if (i == min(1, ng - 1)) PK_TRACE(14);
       const float* sW = stg + st * SF;
-      if (k < nk) {
+      if (k < nk && wide8) {
+        // 16 units of one row: two pairs of quads, each written as one
+        // 256-bit store per stream (full sectors, half the transactions)
+        const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + ch16;
+        const float* row = sW + k * T_BWLD + ch16;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          float4 gq[2], w[2], s0[2], s1[2];
+          if (h == 0) {
+            gq[0] = make_float4(g[0], g[1], g[2], g[3]);
+            gq[1] = make_float4(g[4], g[5], g[6], g[7]);
+            s0[0] = sl0[0]; s0[1] = sl0[1]; s1[0] = sl1[0]; s1[1] = sl1[1];
+          } else {
+            gq[0] = make_float4(g[8], g[9], g[10], g[11]);
+            gq[1] = make_float4(g[12], g[13], g[14], g[15]);
+            s0[0] = sl0[2]; s0[1] = sl0[3]; s1[0] = sl1[2]; s1[1] = sl1[3];
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (fault == 2) gq[j] = make_float4(NAN, NAN, NAN, NAN);
+            badW0 |= !finite(gq[j].x) | !finite(gq[j].y) | !finite(gq[j].z) | !finite(gq[j].w);
+            w[j] = *reinterpret_cast<const float4*>(row + 8 * h + 4 * j);
+            opt_step4(M.opt, lr, wd, bc1, bc2, w[j], s0[j], s1[j], gq[j]);
+          }
+          st8g(Pn + i0 + 8 * h, w[0], w[1]);
+          if (ns >= 1) st8g(Sn + i0 + 8 * h, s0[0], s0[1]);
+          if (ns >= 2) st8g(Sn + NP + i0 + 8 * h, s1[0], s1[1]);
+        }
+      } else if (k < nk) {
         const int64_t i0 = M.w_off[0] + (int64_t)(k0 + k) * H + u0 + ch16;
         const float* row = sW + k * T_BWLD + ch16;
         // one rolled quad loop, one optimizer body (nu % 4 == 0)

@@ -377,7 +377,9 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   }
   m->P = P;
   const size_t es = c->esize();
-  m->SS = (int64_t)(align_up((size_t)P * es, 16) / es);
+  // slot blocks 32-byte strided: the tensor path's epilogue moves a thread's
+  // slots with 256-bit loads/stores (one full sector each)
+  m->SS = (int64_t)(align_up((size_t)P * es, 32) / es);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;

@@ -134,7 +134,7 @@ def member_device_bytes(arch, optimizer: str, batch_size: int, precision="f32") 
     es = 8 if precision == "f64" else 4
     dims = (arch.input_dim, *arch.hidden, arch.classes)
     P = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
-    ss = _cdiv(P * es, 16) * 16 // es  # slot blocks are 16-byte strided
+    ss = _cdiv(P * es, 32) * 32 // es  # slot blocks are 32-byte strided
     ns = _SLOTS[optimizer.lower()]
     total = 2 * _al(P * es) + 2 * _al(ns * ss * es)
     n = len(dims) - 1
