@@ -1151,7 +1151,8 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_begin(P);
+  if (!P.first) pdl_launch();  // a step's first launch waits inside the tile (after its
+                               // independent prologue) and releases its dependents then
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1163,7 +1164,12 @@ __global__ void __launch_bounds__(NT, 1) k_m1t_fwd(const __grid_constant__ Phase
       reinterpret_cast<int32_t*>(&sM)[threadIdx.x] =
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
-    if (f.take != 0 && !halted(P)) m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+    if (f.take != 0) {
+      m1t_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs, P);
+    } else if (P.first) {
+      pdl_wait();
+      pdl_launch();
+    }
   } else {
     __trap();
   }

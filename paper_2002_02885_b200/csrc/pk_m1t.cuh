@@ -123,7 +123,7 @@ __device__ __forceinline__ void xent_row8(float* z, int C, int y, int R, bool li
 // deterministic), adds b0, applies the activation and writes Z0/A0 and the
 // block's partial logits.
 __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                             int tile, int split, int CS) {
+                             int tile, int split, int CS, const PhaseArgs<float>& P) {
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows);
   const int u0 = tile * T_UM, nu = min(T_UM, H - u0);
@@ -141,29 +141,14 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   uint64_t* bar = reinterpret_cast<uint64_t*>(srow + RP);  // [2] (RP even)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
   float* sP = Ah;                                 // after the MMA: partial [RP][T_UM]
-  const float* Pc = M.params[M.ctl->parity];
-  const float* W0 = Pc + M.w_off[0];
   const uint32_t tcols = umma::tmem_cols_pow2(RP);
   const int nu4 = (nu + 3) & ~3;
   const bool reducer = true;  // every rank reduces a row subset of the tile
 
-  // the batch's gather index: issue its load first so it flies together with
-  // the parity load below (two cold round trips overlap instead of chaining)
+  // ---- everything that does not depend on the previous step: the batch's
+  //      gather index, barriers, TMEM and the X rows (inside a multi-step
+  //      graph this overlaps the previous step's tail)
   const int myrow = tid < R ? (int32_t)feed_row(f, tid) : 0;
-  // 16-byte cp.async (LDGSTS) from every thread: W0 rows first (they do not
-  // depend on the batch rows), then W1 / b0 of the tile, then the X rows
-  {
-    const int cpr = nu4 / 4;
-    for (int e = tid; e < nk * cpr; e += NT) {
-      const int k = e / cpr, c = e % cpr;
-      cp_async<16>(rawA + k * T_UM + 4 * c, W0 + (int64_t)(ks + k) * H + u0 + 4 * c, true);
-    }
-    if (reducer) {
-      for (int e = tid; e < nu4 * C / 4; e += NT)
-        cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
-      for (int e = tid; e < cpr; e += NT) cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
-    }
-  }
   if (tid < RP) srow[tid] = myrow;  // RP <= 128 < NT
   if (tid == 32) {
     umma::mbar_init(&bar[1], 1);
@@ -180,8 +165,34 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       cp_async<16>(rawX + r * T_XLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + ks + 4 * c, true);
     }
   }
-  cp_commit();
   const uint32_t tmem = *tslot;
+  // ---- the member's state: after the previous step (parity, halt flag)
+  if (P.first) {
+    pdl_wait();
+    pdl_launch();
+  }
+  if (halted(P)) {  // uniform over the grid: no cluster barrier is left waiting
+    cp_wait<0>();
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+    return;
+  }
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
+  {
+    const int cpr = nu4 / 4;
+    for (int e = tid; e < nk * cpr; e += NT) {
+      const int k = e / cpr, c = e % cpr;
+      cp_async<16>(rawA + k * T_UM + 4 * c, W0 + (int64_t)(ks + k) * H + u0 + 4 * c, true);
+    }
+    if (reducer) {
+      for (int e = tid; e < nu4 * C / 4; e += NT)
+        cp_async<16>(sW1 + 4 * e, Pc + M.w_off[1] + (int64_t)u0 * C + 4 * e, true);
+      for (int e = tid; e < cpr; e += NT) cp_async<16>(sb0 + 4 * e, Pc + M.b_off[0] + u0 + 4 * e, true);
+    }
+  }
+  cp_commit();
   PK_TRACE(1);
   cp_wait<0>();
   __syncthreads();
