@@ -1238,7 +1238,7 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_begin(P);
+  if (!P.first) pdl_launch();  // a first launch waits inside the tile, after its prologue
   if constexpr (sizeof(T) == 4) {
     const Tile t = tile_of(P);
     const FeedDev<T> f = feed_of(P, t.member);
@@ -1249,7 +1249,12 @@ __global__ void __launch_bounds__(NT, 1) k_m1c_fwd(const __grid_constant__ Phase
           reinterpret_cast<const int32_t*>(mem_of(P, t.member))[threadIdx.x];
     __syncthreads();
     // m0 = unit tile, n0 = cluster rank (input-split range)
-    if (f.take != 0 && !halted(P)) m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs);
+    if (f.take != 0) {
+      m1c_fwd_tile(smem_raw, sM, f, t.m0, t.n0, P.cs, P);
+    } else if (P.first) {
+      pdl_wait();
+      pdl_launch();
+    }
   } else {
     __trap();
   }

@@ -784,7 +784,7 @@ __host__ __device__ inline void m1c_range(int nsplit, int CS, int r, int* s0, in
 }
 
 __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<float>& f,
-                             int tile, int rank, int CS) {
+                             int tile, int rank, int CS, const PhaseArgs<float>& P) {
   const int D = M.dims[0], H = M.dims[1], C = M.dims[2];
   const int R = f.take, RP = m1_rows_pad(M.max_rows), S = m1c_raw_stages(RP);
   const int u0 = tile * T_UM, nu = min(T_UM, H - u0), nu4 = (nu + 3) & ~3;
@@ -807,8 +807,6 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
   float* sP = raw;                      // after the loop: [nloc][RP][T_UM] partials
   float* sA = raw + nloc * RP * T_UM;   // then my rows' activations [nr][T_UM]
-  const float* Pc = M.params[M.ctl->parity];
-  const float* W0 = Pc + M.w_off[0];
   const uint32_t tcols = umma::tmem_cols_pow2(max(nloc, 1) * RP);
 
   for (int r = tid; r < RP; r += NT) srow[r] = r < R ? (int32_t)feed_row(f, r) : 0;
@@ -833,6 +831,19 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tslot;
+  // the member's state only after the previous step of a multi-step graph
+  if (P.first) {
+    pdl_wait();
+    pdl_launch();
+  }
+  if (halted(P)) {  // uniform over the grid: no cluster barrier is left waiting
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 1) umma::tmem_dealloc(tmem, tcols);
+    return;
+  }
+  const float* Pc = M.params[M.ctl->parity];
+  const float* W0 = Pc + M.w_off[0];
   bool badx = false;
   if (warp < 7) {
     // ------------------------------------------------------------ producers
