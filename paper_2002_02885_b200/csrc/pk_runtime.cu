@@ -53,13 +53,14 @@ struct pk_ctx {
 
 static const char* const kAllocKind[] = {"device", "pinned", "mapped"};
 
-// a cached block of `kind` with bytes <= cap <= 4·bytes, else a fresh one
-static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size_t* cap) {
+// a cached block of `kind` with bytes <= cap <= slack·bytes, else a fresh one
+static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size_t* cap,
+                             double slack = 4.0) {
   bytes = std::max<size_t>(bytes, 256);
   size_t best = SIZE_MAX, bi = 0;
   for (size_t i = 0; i < c->blocks.size(); ++i) {
     const auto& b = c->blocks[i];
-    if (b.kind == kind && b.cap >= bytes && b.cap <= 4 * bytes && b.cap < best) {
+    if (b.kind == kind && b.cap >= bytes && (double)b.cap <= slack * (double)bytes && b.cap < best) {
       best = b.cap;
       bi = i;
     }
@@ -83,7 +84,11 @@ static void ctx_free_block(const pk_ctx::Block& b) {
 static void ctx_release(pk_ctx* c, int kind, void* p, size_t cap) {
   if (!p) return;
   c->blocks.push_back({p, cap, kind});
-  if (c->blocks.size() > 512) {  // bounded: drop the oldest
+  size_t held = 0;
+  for (const auto& b : c->blocks) held += b.cap;
+  // bounded (entries and bytes): drop the oldest
+  while (!c->blocks.empty() && (c->blocks.size() > 512 || held > (size_t(2) << 30))) {
+    held -= c->blocks.front().cap;
     ctx_free_block(c->blocks.front());
     c->blocks.erase(c->blocks.begin());
   }
@@ -123,6 +128,7 @@ struct pk_member {
   int64_t w_off[PK_MAX_LAYERS], b_off[PK_MAX_LAYERS];
   char* slab;
   size_t slab_bytes;
+  size_t slab_cap;  // capacity of the (possibly recycled) block
   void* params[2];
   void* slots[2];
   void* Z[PK_MAX_LAYERS];
@@ -401,7 +407,10 @@ extern "C" int pk_member_create(pk_ctx* c, const pk_member_desc* d, pk_member** 
   const size_t o_loss = take((size_t)d->max_rows * sizeof(double));
   const size_t o_ctl = take(sizeof(MemberCtl));
   m->slab_bytes = off;
-  cudaError_t e = cudaMalloc((void**)&m->slab, off);
+  // recycled from the context when a slab of about this size was freed
+  // (Hyperband creates and drops members per configuration; cudaMalloc /
+  // cudaFree cost milliseconds at times)
+  cudaError_t e = ctx_alloc(c, 0, off, (void**)&m->slab, &m->slab_cap, 1.25);
   if (e != cudaSuccess) {
     delete m;
     c->err = std::string("member alloc: ") + cudaGetErrorString(e);
@@ -439,7 +448,7 @@ extern "C" int pk_member_destroy(pk_member* m) {
   if (!m) return PK_ERR_ARG;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
-  cudaFree(m->slab);
+  ctx_release(m->ctx, 0, m->slab, m->slab_cap);
   m->ctx->bytes -= m->slab_bytes;
   delete m;
   return PK_OK;
