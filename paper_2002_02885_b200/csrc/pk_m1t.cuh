@@ -1111,6 +1111,19 @@ __device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
   return T_BK * T_BWLD + RP * T_BXLD;  // W0 tile + X columns
 }
 
+// e / d and e % d for a runtime d that is a power of two on full tiles
+// (8 unit quads, 32 input quads): a shift on that path, a division otherwise
+__device__ __forceinline__ void divmod_p2(int e, int d, int& q, int& r) {
+  if ((d & (d - 1)) == 0) {
+    const int s = __ffs(d) - 1;
+    q = e >> s;
+    r = e & (d - 1);
+  } else {
+    q = e / d;
+    r = e - q * d;
+  }
+}
+
 __device__ __forceinline__ void cp_wait_n(int n) {  // pending commit groups allowed (<= 4)
   // predicated waits, no branch: a switch here compiles to a jump table
   // (LDC + BRX) whose indirect fetch costs hundreds of cycles per call
@@ -1189,12 +1202,14 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     {
       const float* src = Pc + M.w_off[0] + u0;
       for (int e = tid; e < nk * cw; e += BT) {
-        const int k = e / cw, c = e % cw;
+        int k, c;
+        divmod_p2(e, cw, k, c);
         cp_async<16>(sW + k * T_BWLD + 4 * c, src + (int64_t)(k0 + k) * H + 4 * c, true);
       }
     }
     for (int e = tid; e < R * cx; e += BT) {
-      const int r = e / cx, c = e % cx;
+      int r, c;
+      divmod_p2(e, cx, r, c);
       cp_async<16>(sX + r * T_BXLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * c, true);
     }
     cp_commit();
@@ -1490,7 +1505,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       {
         const float* src = Pc + M.w_off[0] + u0;
         for (int e = pt; e < nk * cw; e += NP3) {
-          const int kk = e / cw, c = e % cw;
+          int kk, c;
+          divmod_p2(e, cw, kk, c);
           cp_async<16>(sW + kk * T_BWLD + 4 * c, src + (int64_t)(k0 + kk) * H + 4 * c, true);
         }
         // the epilogue reads this tile's optimizer slots from global: pull
@@ -1502,7 +1518,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
         }
       }
       for (int e = pt; e < R * cx; e += NP3) {
-        const int r = e / cx, c = e % cx;
+        int r, c;
+      divmod_p2(e, cx, r, c);
         cp_async<16>(sX + r * T_BXLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * c, true);
       }
       cp_commit();
