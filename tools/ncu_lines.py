@@ -70,6 +70,9 @@ def main():
             if v and float(v) > 0:
                 why[src][name] += float(v)
     print(f"{len(data)} SASS rows, {len(lines)} disassembled, {tot} samples")
+    if len(data) != len(lines):
+        print("WARNING: the report and the library's SASS differ (the .ncu-rep was captured "
+              "with another build): source lines below are not reliable")
     for src, s in agg.most_common(int(os.environ.get("TOP", "30"))):
         top = ", ".join(f"{n} {int(v)}" for n, v in why[src].most_common(3))
         print(f"{s:5d} {100 * s / tot:5.1f}%  {src:24s} inst {execd[src]:9d}  [{top}]")
