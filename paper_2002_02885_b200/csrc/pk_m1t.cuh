@@ -77,6 +77,19 @@ struct M1T {
   }
 };
 
+// e / d and e % d for a runtime d that is a power of two on full tiles
+// (8 unit quads, 32 input quads): a shift on that path, a division otherwise
+__device__ __forceinline__ void divmod_p2(int e, int d, int& q, int& r) {
+  if ((d & (d - 1)) == 0) {
+    const int s = __ffs(d) - 1;
+    q = e >> s;
+    r = e & (d - 1);
+  } else {
+    q = e / d;
+    r = e - q * d;
+  }
+}
+
 // softmax-xent of one row by an aligned group of 8 lanes (classes c ≡ lane
 // mod 8, C <= 32; engine.py:211-230, :252-264): z ← dlogits in place,
 // −logp[y] into *rowloss.  `live` = false lanes join the shuffles only.
@@ -161,7 +174,8 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   {
     const int cpr = nk / 4;
     for (int e = tid; e < R * cpr; e += NT) {
-      const int r = e / cpr, c = e % cpr;
+      int r, c;
+      divmod_p2(e, cpr, r, c);
       cp_async<16>(rawX + r * T_XLD + 4 * c, f.feat + (int64_t)srow[r] * f.ld + ks + 4 * c, true);
     }
   }
@@ -183,7 +197,8 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   {
     const int cpr = nu4 / 4;
     for (int e = tid; e < nk * cpr; e += NT) {
-      const int k = e / cpr, c = e % cpr;
+      int k, c;
+      divmod_p2(e, cpr, k, c);
       cp_async<16>(rawA + k * T_UM + 4 * c, W0 + (int64_t)(ks + k) * H + u0 + 4 * c, true);
     }
     if (reducer) {
@@ -376,12 +391,14 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
     float* rX = rA + T_SC * T_UM;
     const int k0 = c * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
     for (int e = tid; e < nk * cpr; e += NT) {
-      const int k = e / cpr, q = e % cpr;
+      int k, q;
+      divmod_p2(e, cpr, k, q);
       cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
     }
     const int cx = nk / 4;
     for (int e = tid; e < R * cx; e += NT) {
-      const int r = e / cx, q = e % cx;
+      int r, q;
+      divmod_p2(e, cx, r, q);
       cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
     }
     cp_commit();
@@ -594,12 +611,14 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
       float* rX = rA + T_SC * T_UM;
       const int k0 = c * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
       for (int e = pt; e < nk * cpr; e += T_WS_PRODUCERS) {
-        const int k = e / cpr, q = e % cpr;
+        int k, q;
+      divmod_p2(e, cpr, k, q);
         cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
       }
       const int cx = nk / 4;
       for (int e = pt; e < R * cx; e += T_WS_PRODUCERS) {
-        const int r = e / cx, q = e % cx;
+        int r, q;
+      divmod_p2(e, cx, r, q);
         cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
       }
       cp_commit();
@@ -853,12 +872,14 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
       float* rX = rA + T_SC * T_UM;
       const int k0 = (c_beg + i) * T_SC, nk = min(T_SC, D - k0), cpr = nu4 / 4;
       for (int e = pt; e < nk * cpr; e += T_WS_PRODUCERS) {
-        const int k = e / cpr, q = e % cpr;
+        int k, q;
+      divmod_p2(e, cpr, k, q);
         cp_async<16>(rA + k * T_UM + 4 * q, W0 + (int64_t)(k0 + k) * H + u0 + 4 * q, true);
       }
       const int cx = nk / 4;
       for (int e = pt; e < R * cx; e += T_WS_PRODUCERS) {
-        const int r = e / cx, q = e % cx;
+        int r, q;
+      divmod_p2(e, cx, r, q);
         cp_async<16>(rX + r * T_SXLD + 4 * q, f.feat + (int64_t)srow[r] * f.ld + k0 + 4 * q, true);
       }
       cp_commit();
@@ -1109,19 +1130,6 @@ __device__ __forceinline__ void m1t_stage_xT(float* Ah, float* Al, const float* 
 
 __device__ __forceinline__ int m1t_bwd_stage_floats(int RP, int ns) {
   return T_BK * T_BWLD + RP * T_BXLD;  // W0 tile + X columns
-}
-
-// e / d and e % d for a runtime d that is a power of two on full tiles
-// (8 unit quads, 32 input quads): a shift on that path, a division otherwise
-__device__ __forceinline__ void divmod_p2(int e, int d, int& q, int& r) {
-  if ((d & (d - 1)) == 0) {
-    const int s = __ffs(d) - 1;
-    q = e >> s;
-    r = e & (d - 1);
-  } else {
-    q = e / d;
-    r = e - q * d;
-  }
 }
 
 __device__ __forceinline__ void cp_wait_n(int n) {  // pending commit groups allowed (<= 4)
