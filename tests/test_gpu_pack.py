@@ -808,6 +808,58 @@ def test_native_run_hands_label_errors_back():
     assert _maxdiff(hs[0], ref) == 0.0
 
 
+def test_native_run_failure_inside_a_multi_step_graph():
+    """A non-finite input row reached at the 4th step of a run: the native
+    driver launches 8 steps per graph, the failing step's finalize sets the
+    halt flag and steps 5..8 of the same graph skip; the exception, the step
+    it happens at and every member's state equal the packed_step loop's."""
+    from paper_2002_02885_b200.data import epoch_permutation
+
+    def make():
+        d = data.synth_dataset(200, 12, 4, seed=44)
+        perm = epoch_permutation(d.dataset_id, d.n, 0)
+        d.features[perm[3 * 10 + 2]] = np.inf  # a row of step 3's batch (b = 10)
+        hs = [packing.make_handle(f"q{i}", packing.MLPArch(12, (8,), 4, "tanh"), o, 0.05, 10,
+                                  100, "d", i) for i, o in enumerate(("sgd", "adam", "momentum"))]
+        return {"d": d}, hs, packing.dedup_inputs(packing.pack_models(hs))
+
+    out = []
+    for mode in ("loop", "run"):
+        ds, hs, pk = make()
+        done = []
+        with pytest.raises(engine.EngineError):
+            if mode == "loop":
+                for _ in range(20):
+                    done.append(packing.packed_step(pk, ds))
+            else:
+                done = packing.packed_run(pk, ds, 20, depth=16)
+        steps = [h.cursor.steps_done for h in hs]
+        out.append((steps, [h._flat_params(h.params) for h in hs]))
+    assert out[0][0] == out[1][0] == [3, 3, 3]
+    for a, b in zip(out[0][1], out[1][1]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_native_run_without_inline_descriptors():
+    """K = 36 > 32 members: step descriptors travel by H2D copy and the driver
+    launches one step per graph; packed_run still equals the packed_step loop."""
+    ds = {"t": data.synth_dataset(300, 12, 4, seed=45)}
+
+    def make():
+        hs = [packing.make_handle(f"w{i}", packing.MLPArch(12, (8,), 4, "relu"),
+                                  ("sgd", "adam")[i % 2], 0.02, 16, 12, "t", i) for i in range(36)]
+        return hs, packing.dedup_inputs(packing.pack_models(hs))
+
+    ha, pa = make()
+    la = [packing.packed_step(pa, ds) for _ in range(12)]
+    hb, pb = make()
+    lb = packing.packed_run(pb, ds, 12)
+    assert la == lb
+    for a, b in zip(ha, hb):
+        assert _maxdiff(a, b) == 0.0
+        assert a.cursor.pos == b.cursor.pos and a.cursor.steps_done == b.cursor.steps_done
+
+
 def test_packed_run_stops_exactly_at_a_failing_step():
     """A non-finite gradient inside a pipelined run raises at that step; the
     device skipped every step enqueued behind it, so the state equals the
