@@ -347,6 +347,26 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 constexpr int T_SC = 32;              // input dims per streamed chunk
 constexpr int T_SXLD = T_SC + 4;      // raw X chunk row stride (16B rows, conflict-free)
 
+// sA[r][u] holds z = Σ partials + b0 for the tile's rows × units: activation,
+// Z0 / A0 to global (coalesced along u), sA ← A0 (0 outside the valid box)
+__device__ __forceinline__ void m1_act_epilogue(const MemberDev<float>& M, float* sA, int R, int RP,
+                                                int nu, int u0, int H, int* bad) {
+#pragma unroll 1
+  for (int e = threadIdx.x; e < RP * T_UM; e += blockDim.x) {
+    const int r = e / T_UM, u = e % T_UM;
+    float a = 0.f;
+    if (r < R && u < nu) {
+      const float zz = sA[e];
+      a = act_fwd(M.act, zz);
+      M.Z[0][(int64_t)r * H + u0 + u] = zz;
+      M.A[0][(int64_t)r * H + u0 + u] = a;
+      if (!finite(zz)) *bad = min(*bad, 1);
+      if (!finite(a)) *bad = min(*bad, 2);
+    }
+    sA[e] = a;
+  }
+}
+
 __host__ __device__ inline int m1s_raw_stages(int RP) { return RP >= 128 ? 2 : 4; }
 __host__ __device__ inline int m1s_fwd_smem(int RP, int C) {
   const int S = m1s_raw_stages(RP);
@@ -521,22 +541,17 @@ __device__ void m1s_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   PK_TRACE(2);
   // ---- epilogue: b0, activation, Z0/A0; sA[r][u] for the logits
   float* sA = raw;  // [RP][T_UM] (raw stages are free)
-  int bad = INT_MAX;
+  // z + b0 through shared memory: the unrolled part is plain stores, the
+  // activation and the Z0/A0 stores one rolled loop (compact code: this runs
+  // once per step, every line of it an instruction-cache miss otherwise)
 #pragma unroll
   for (int i = 0; i < 64; ++i) {
     if (i >= RP / 2) break;
-    const int r = rlo + i;
-    float a = 0.f;
-    if (r < R && uu < nu) {
-      const float zz = z[i] + sb0[uu];
-      a = act_fwd(M.act, zz);
-      M.Z[0][(int64_t)r * H + u0 + uu] = zz;
-      M.A[0][(int64_t)r * H + u0 + uu] = a;
-      if (!finite(zz)) bad = min(bad, 1);
-      if (!finite(a)) bad = min(bad, 2);
-    }
-    sA[r * T_UM + uu] = a;
+    sA[(rlo + i) * T_UM + uu] = z[i] + sb0[uu];
   }
+  __syncthreads();
+  int bad = INT_MAX;
+  m1_act_epilogue(M, sA, R, RP, nu, u0, H, &bad);
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   umma::fence_before();
   __syncthreads();
@@ -738,21 +753,11 @@ __device__ void m1s_fwd_tile_ws(char* sm, const MemberDev<float>& M, const FeedD
     }
   }
   float* sA = raw;  // [RP][T_UM]
-  int bad = INT_MAX;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int r = rlo + i;
-    float a = 0.f;
-    if (r < R && uu < nu) {
-      const float zz = z[i] + sb0[uu];
-      a = act_fwd(M.act, zz);
-      M.Z[0][(int64_t)r * H + u0 + uu] = zz;
-      M.A[0][(int64_t)r * H + u0 + uu] = a;
-      if (!finite(zz)) bad = min(bad, 1);
-      if (!finite(a)) bad = min(bad, 2);
-    }
-    sA[r * T_UM + uu] = a;
-  }
+  for (int i = 0; i < 16; ++i) sA[(rlo + i) * T_UM + uu] = z[i] + sb0[uu];
+  __syncthreads();
+  int bad = INT_MAX;
+  m1_act_epilogue(M, sA, R, RP, nu, u0, H, &bad);
   if (bad != INT_MAX) flag_min(&M.ctl->bad_node, bad);
   umma::fence_before();
   __syncthreads();
