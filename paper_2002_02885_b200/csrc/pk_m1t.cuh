@@ -1058,6 +1058,20 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 // instantiation that applies it (packed == standalone does not depend on how
 // the compiler scheduled a particular copy).  ib1 / ib2 = 1 / Adam's bias
 // corrections (≤ 1 ulp from the divisions; the fp32 contract is rel 1e-4).
+// the MUFU square root and reciprocal (≤ 2 ulp): one instruction each
+// instead of the IEEE-exact sequences, deterministic in every kernel copy;
+// the fp32 contract is rel 1e-4
+__device__ __forceinline__ float sqrt_mufu(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_mufu(float x) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ void opt_x(int opt, float lr, float wd, float ib1, float ib2, float& w,
                                       float& s0, float& s1, float g) {
   if (wd != 0.f) g = __fadd_rn(g, __fmul_rn(wd, w));
@@ -1071,13 +1085,13 @@ __device__ __forceinline__ void opt_x(int opt, float lr, float wd, float ib1, fl
       break;
     case PK_OPT_ADAGRAD:
       s0 = __fadd_rn(s0, __fmul_rn(g, g));
-      w = __fsub_rn(w, __fmul_rn(__fmul_rn(lr, g), __frcp_rn(__fadd_rn(sqrtf(s0), 1e-10f))));
+      w = __fsub_rn(w, __fmul_rn(__fmul_rn(lr, g), rcp_mufu(__fadd_rn(sqrt_mufu(s0), 1e-10f))));
       break;
     default:
       s0 = __fadd_rn(__fmul_rn(s0, 0.9f), __fmul_rn(1.f - 0.9f, g));
       s1 = __fadd_rn(__fmul_rn(s1, 0.999f), __fmul_rn(__fmul_rn(1.f - 0.999f, g), g));
       w = __fsub_rn(w, __fmul_rn(__fmul_rn(lr, __fmul_rn(s0, ib1)),
-                                 __frcp_rn(__fadd_rn(sqrtf(__fmul_rn(s1, ib2)), 1e-8f))));
+                                 rcp_mufu(__fadd_rn(sqrt_mufu(__fmul_rn(s1, ib2)), 1e-8f))));
       break;
   }
 }
