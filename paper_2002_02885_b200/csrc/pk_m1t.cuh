@@ -1109,10 +1109,10 @@ __device__ __forceinline__ void st8g(float* p, float4 a, float4 b) {
                : "memory");
 }
 
-// the member's optimizer on four elements
-__device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1, float bc2,
+// the member's optimizer on four elements; ib1 / ib2 = 1 / Adam's bias
+// corrections, computed once per tile by the caller (opt_recips)
+__device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float ib1, float ib2,
                                           float4& w, float4& s0, float4& s1, float4 g) {
-  const float ib1 = opt == PK_OPT_ADAM ? 1.f / bc1 : 1.f, ib2 = opt == PK_OPT_ADAM ? 1.f / bc2 : 1.f;
   opt_x(opt, lr, wd, ib1, ib2, w.x, s0.x, s1.x, g.x);
   opt_x(opt, lr, wd, ib1, ib2, w.y, s0.y, s1.y, g.y);
   opt_x(opt, lr, wd, ib1, ib2, w.z, s0.z, s1.z, g.z);
@@ -1120,10 +1120,16 @@ __device__ __forceinline__ void opt_step4(int opt, float lr, float wd, float bc1
 }
 
 // scalar form for the small W1 / b0 / b1 updates
-__device__ __forceinline__ void opt_step1(int opt, float lr, float wd, float bc1, float bc2,
+__device__ __forceinline__ void opt_step1(int opt, float lr, float wd, float ib1, float ib2,
                                           float& w, float& s0, float& s1, float g) {
-  const float ib1 = opt == PK_OPT_ADAM ? 1.f / bc1 : 1.f, ib2 = opt == PK_OPT_ADAM ? 1.f / bc2 : 1.f;
   opt_x(opt, lr, wd, ib1, ib2, w, s0, s1, g);
+}
+
+// Adam's bias-correction reciprocals 1/(1-β^t) of the member's control block
+// (1 for the other optimizers)
+__device__ __forceinline__ void opt_recips(int opt, const MemberCtl* ctl, float* ib1, float* ib2) {
+  *ib1 = opt == PK_OPT_ADAM ? 1.f / float(ctl->bc1) : 1.f;
+  *ib2 = opt == PK_OPT_ADAM ? 1.f / float(ctl->bc2) : 1.f;
 }
 
 // A operand of the weight-gradient MMA: Xᵀ rows k (128) × K = batch rows
@@ -1341,8 +1347,8 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   __syncthreads();
   PK_TRACE(11);
   const float lr = float(ctl->lr), wd = float(M.wd);
-  const float bc1 = M.opt == PK_OPT_ADAM ? float(ctl->bc1) : 1.f;
-  const float bc2 = M.opt == PK_OPT_ADAM ? float(ctl->bc2) : 1.f;
+  float bc1, bc2;  // (reciprocals)
+  opt_recips(M.opt, ctl, &bc1, &bc2);
   const int fault = ctl->fault_grad;
   bool badW0 = false, badW1 = false, badb1 = false, badb0 = false;
   // ---- stream the group's input tiles, warp-specialised -------------------

@@ -391,8 +391,8 @@ __device__ __forceinline__ void m1x_step_t(char* sm, const MemberDev<float>& M,
   __syncthreads();
   PK_TRACE(9);
   const float lr = float(ctl->lr), wd = float(M.wd);
-  const float bc1 = OPT == PK_OPT_ADAM ? float(ctl->bc1) : 1.f;
-  const float bc2 = OPT == PK_OPT_ADAM ? float(ctl->bc2) : 1.f;
+  float bc1, bc2;  // (reciprocals)
+  opt_recips(OPT, ctl, &bc1, &bc2);
   const int fault = ctl->fault_grad;
   bool badW1 = false, badb1 = false, badW0 = false, badb0 = false;
   // ---- W1[units, :] (grad 0), b1 (grad 1, rank 0), b0[units] (grad 3) --------
