@@ -90,6 +90,27 @@ __device__ __forceinline__ void divmod_p2(int e, int d, int& q, int& r) {
   }
 }
 
+// four consecutive units u..u+3 of row r with their split sums z: + b0, the
+// activation, Z0/A0 (one 16-byte store each), A0 into sA4 (0 outside the box)
+__device__ __forceinline__ void m1_finish4(const MemberDev<float>& M, float4 z, const float* sb0,
+                                           int r, int u, int R, int nu, int u0, int H,
+                                           float* sA4, int* bad) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (r < R && u < nu) {  // H % 4 == 0: a quad is valid or not as a whole
+    z.x += sb0[u];
+    z.y += sb0[u + 1];
+    z.z += sb0[u + 2];
+    z.w += sb0[u + 3];
+    a = make_float4(act_fwd(M.act, z.x), act_fwd(M.act, z.y), act_fwd(M.act, z.z),
+                    act_fwd(M.act, z.w));
+    *reinterpret_cast<float4*>(M.Z[0] + (int64_t)r * H + u0 + u) = z;
+    *reinterpret_cast<float4*>(M.A[0] + (int64_t)r * H + u0 + u) = a;
+    if (!finite(z.x) || !finite(z.y) || !finite(z.z) || !finite(z.w)) *bad = min(*bad, 1);
+    if (!finite(a.x) || !finite(a.y) || !finite(a.z) || !finite(a.w)) *bad = min(*bad, 2);
+  }
+  *reinterpret_cast<float4*>(sA4) = a;
+}
+
 // softmax-xent of one row by an aligned group of 8 lanes (classes c ≡ lane
 // mod 8, C <= 32; engine.py:211-230, :252-264): z ← dlogits in place,
 // −logp[y] into *rowloss.  `live` = false lanes join the shuffles only.
@@ -293,26 +314,27 @@ __device__ void m1t_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   float* sA = rawA;  // [my rows][T_UM] activations (rawA + rawX are free now)
   const int nr = R > split ? (R - split + CS - 1) / CS : 0;
   int bad = INT_MAX;
-  for (int e = tid; e < nr * T_UM; e += NT) {
-    const int rl = e / T_UM, u = e % T_UM, r = split + rl * CS;
-    float a = 0.f;
+  // four consecutive units per thread: one 16-byte DSMEM load per rank
+  for (int e4 = tid; e4 < nr * T_UM / 4; e4 += NT) {
+    const int rl = e4 / (T_UM / 4), u = 4 * (e4 % (T_UM / 4)), r = split + rl * CS;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     if (u < nu) {
-      float v[T_MAXCS];
+      float4 v[T_MAXCS];
       const uint32_t la = umma::smem_u32(sP + r * T_UM + u);
 #pragma unroll
-      for (int s = 0; s < T_MAXCS; ++s) v[s] = s < CS ? umma::dsmem_ld(la, (uint32_t)s) : 0.f;
-      float z = v[0];
+      for (int s = 0; s < T_MAXCS; ++s)
+        v[s] = s < CS ? umma::dsmem_ld4(la, (uint32_t)s) : make_float4(0.f, 0.f, 0.f, 0.f);
+      z = v[0];
 #pragma unroll
       for (int s = 1; s < T_MAXCS; ++s)
-        if (s < CS) z += v[s];
-      z += sb0[u];
-      a = act_fwd(M.act, z);
-      M.Z[0][(int64_t)r * H + u0 + u] = z;
-      M.A[0][(int64_t)r * H + u0 + u] = a;
-      if (!finite(z)) bad = min(bad, 1);
-      if (!finite(a)) bad = min(bad, 2);
+        if (s < CS) {
+          z.x += v[s].x;
+          z.y += v[s].y;
+          z.z += v[s].z;
+          z.w += v[s].w;
+        }
     }
-    sA[e] = a;
+    m1_finish4(M, z, sb0, r, u, R, nu, u0, H, sA + rl * T_UM + u, &bad);
   }
   __syncthreads();
   // P[blk][r][c] = Σ_{j<32} A0[r][32·blk + j] · W1[32·blk + j][c] for my rows
@@ -1003,29 +1025,29 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   // ---- rank r reduces rows r, r + CS, ...: z = Σ_s p_s in split order ------
   const int nr = R > rank ? (R - rank + CS - 1) / CS : 0;
   int bad = INT_MAX;
-  for (int e = tid; e < nr * T_UM; e += NT) {
-    const int rl = e / T_UM, u = e % T_UM, r = rank + rl * CS;
-    float a = 0.f;
+  // four consecutive units per thread: one 16-byte DSMEM load per split
+  for (int e4 = tid; e4 < nr * T_UM / 4; e4 += NT) {
+    const int rl = e4 / (T_UM / 4), u = 4 * (e4 % (T_UM / 4)), r = rank + rl * CS;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     if (u < nu) {
-      float v[T_MAXCS];
+      float4 v[T_MAXCS];
 #pragma unroll
       for (int sp = 0; sp < T_MAXCS; ++sp)
         v[sp] = sp < nsplit
-                    ? umma::dsmem_ld(umma::smem_u32(sP + (s_loc[sp] * RP + r) * T_UM + u),
-                                     (uint32_t)s_own[sp])
-                    : 0.f;
-      float z = v[0];
+                    ? umma::dsmem_ld4(umma::smem_u32(sP + (s_loc[sp] * RP + r) * T_UM + u),
+                                      (uint32_t)s_own[sp])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      z = v[0];
 #pragma unroll
       for (int sp = 1; sp < T_MAXCS; ++sp)
-        if (sp < nsplit) z += v[sp];
-      z += sb0[u];
-      a = act_fwd(M.act, z);
-      M.Z[0][(int64_t)r * H + u0 + u] = z;
-      M.A[0][(int64_t)r * H + u0 + u] = a;
-      if (!finite(z)) bad = min(bad, 1);
-      if (!finite(a)) bad = min(bad, 2);
+        if (sp < nsplit) {
+          z.x += v[sp].x;
+          z.y += v[sp].y;
+          z.z += v[sp].z;
+          z.w += v[sp].w;
+        }
     }
-    sA[e] = a;
+    m1_finish4(M, z, sb0, r, u, R, nu, u0, H, sA + rl * T_UM + u, &bad);
   }
   __syncthreads();
   const int nbt = (nu + T_LB - 1) / T_LB;

@@ -139,6 +139,18 @@ __device__ __forceinline__ float dsmem_ld(uint32_t la, uint32_t rank) {
   return v;
 }
 
+// the 16-byte vector at local shared address `la` (16-B aligned) of cluster CTA
+// `rank`: one DSMEM transaction for four consecutive floats
+__device__ __forceinline__ float4 dsmem_ld4(uint32_t la, uint32_t rank) {
+  uint32_t ra;
+  float4 v;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ra));
+  return v;
+}
+
 // ---- bulk copies (TMA engine, no tensor map) ---------------------------------
 // dst/src 16-byte aligned, bytes a multiple of 16; completes tx on `mbar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
