@@ -525,7 +525,9 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     // wave); never below what TMEM / smem per CTA allow
     int CS = cs_lo;
     bool one_wave = false;
-    for (int cs = std::min(ns_max, pk::T_MAXCS); cs >= cs_lo; --cs) {
+    int cs_hi = std::min(ns_max, pk::T_MAXCS);
+    if (const char* e = getenv("PK_FWD_CS")) cs_hi = std::max(cs_lo, std::min(cs_hi, atoi(e)));
+    for (int cs = cs_hi; cs >= cs_lo; --cs) {
       if (dt != PK_F32) break;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cs * n_tiles);
