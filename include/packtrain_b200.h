@@ -131,6 +131,13 @@ int pk_dataset_write_rows(pk_dataset* ds, int64_t row0, int64_t rows, const void
 int pk_dataset_gather_rows(pk_dataset* ds, int64_t rows, const void* src_features, int64_t src_ld,
                            const int32_t* src_labels, const int64_t* idx, void* stage_features,
                            int32_t* stage_labels);
+
+/* Page-lock a host buffer and map it into the device address space
+ * (cudaHostRegister, mapped); *dev receives the device view.  Streamed inputs
+ * whose rows the GPU gathers itself over PCIe (pk_pack_run) avoid the host-side
+ * memcpy + copy calls of pk_dataset_gather_rows.  pk_host_unmap undoes it. */
+int pk_host_map(pk_ctx* ctx, void* host, int64_t bytes, void** dev);
+int pk_host_unmap(pk_ctx* ctx, void* host);
 int pk_dataset_destroy(pk_dataset* ds);
 int pk_order_create(pk_ctx* ctx, const int64_t* perm, int64_t n, pk_order** out);
 int pk_order_destroy(pk_order* order);
@@ -194,7 +201,10 @@ typedef struct {
   int64_t epoch0;               /* permutations / orders given for epochs */
   int32_t n_epochs;             /*   epoch0 .. epoch0 + n_epochs - 1 */
   const int64_t* const* perm;   /* host permutations */
-  const pk_order* const* order; /* device orders (device-resident inputs) */
+  const pk_order* const* order; /* device orders (device-resident inputs; streamed inputs
+                                   with mapped_x use them for the on-device gather) */
+  const void* mapped_x;         /* streamed inputs: device view of host_x (pk_host_map), or NULL */
+  const int32_t* mapped_y;      /* device view of host_y */
 } pk_run_dataset;
 
 #define PK_RUN_MAX_STEPS 0    /* ran max_steps */

@@ -25,7 +25,7 @@ EXPORTS = (
     "pk_abi_version", "pk_ctx_create", "pk_ctx_destroy", "pk_ctx_last_error",
     "pk_ctx_set_stream", "pk_ctx_synchronize", "pk_ctx_mem_info",
     "pk_dataset_create", "pk_dataset_write", "pk_dataset_write_rows", "pk_dataset_gather_rows",
-    "pk_pack_run",
+    "pk_pack_run", "pk_host_map", "pk_host_unmap",
     "pk_dataset_destroy",
     "pk_order_create", "pk_order_destroy",
     "pk_member_create", "pk_member_destroy", "pk_member_param_count",
@@ -71,7 +71,8 @@ class RunDataset(C.Structure):
     _fields_ = [("n", C.c_int64), ("dim", C.c_int32), ("max_label", C.c_int32),
                 ("host_x", C.c_void_p), ("host_ld", C.c_int64), ("host_y", C.c_void_p),
                 ("device", C.c_void_p), ("epoch0", C.c_int64), ("n_epochs", C.c_int32),
-                ("perm", C.c_void_p), ("order", C.c_void_p)]
+                ("perm", C.c_void_p), ("order", C.c_void_p),
+                ("mapped_x", C.c_void_p), ("mapped_y", C.c_void_p)]
 
 
 PK_RUN_MAX_STEPS, PK_RUN_NO_MEMBER, PK_RUN_NEED_PERM, PK_RUN_LABEL_BOUNDS, PK_RUN_FAILED = range(5)
@@ -108,6 +109,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pk_dataset_write": (C.c_int, [vp, i64, i64, vp, vp]),
         "pk_dataset_write_rows": (C.c_int, [vp, i64, i64, vp, vp]),
         "pk_dataset_gather_rows": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, vp]),
+        "pk_host_map": (C.c_int, [vp, vp, i64, vp]),
+        "pk_host_unmap": (C.c_int, [vp, vp]),
         "pk_pack_run": (C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, i64, C.c_int32, vp, vp, vp,
                                   vp, vp, vp]),
         "pk_dataset_destroy": (C.c_int, [vp]),

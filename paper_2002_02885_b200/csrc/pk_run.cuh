@@ -72,20 +72,63 @@ static pk_pack::RunStage* run_stage(pk_pack* p, int slot, int gi, int64_t rows, 
 
 // rows idx of a host dataset → the slot's pinned staging → H2D on the copy
 // stream; the pack stream waits for that copy before the step's kernels
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ src, int64_t ld,
+                              const int32_t* __restrict__ src_y, const int32_t* __restrict__ perm,
+                              int64_t pos, int dim, T* __restrict__ dst, int32_t* __restrict__ dst_y);
+
+template <typename T>
+static void pk_k_gather_launch(pk_pack* p, const pk_run_dataset& d, int64_t take, int64_t pos,
+                               int64_t e, pk_pack::RunStage* g) {
+  k_gather_rows<T><<<(unsigned)take, 128, 0, p->copy_stream>>>(
+      static_cast<const T*>(d.mapped_x), d.host_ld, d.mapped_y, d.order[e]->perm, pos, d.dim,
+      static_cast<T*>(g->d->feat), g->d->labels);
+}
+
+// streamed rows gathered by the GPU itself: row perm[pos + r] of the
+// host-mapped dataset (read over PCIe) → staging row r; one CTA per row,
+// 16-byte reads (zero-copy H2D of exactly the batch's bytes)
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ src, int64_t ld,
+                              const int32_t* __restrict__ src_y, const int32_t* __restrict__ perm,
+                              int64_t pos, int dim, T* __restrict__ dst, int32_t* __restrict__ dst_y) {
+  const int r = blockIdx.x;
+  const int64_t row = perm[pos + r];
+  const T* s = src + row * ld;
+  T* d = dst + (int64_t)r * dim;
+  constexpr int V = 16 / (int)sizeof(T);
+  if ((ld % V) == 0 && (dim % V) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    for (int i = threadIdx.x; i < dim / V; i += blockDim.x)
+      reinterpret_cast<float4*>(d)[i] = reinterpret_cast<const float4*>(s)[i];
+  } else {
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) d[i] = s[i];
+  }
+  if (threadIdx.x == 0) dst_y[r] = src_y[row];
+}
+
 static int run_gather(pk_pack* p, int slot, pk_pack::RunStage* g, int64_t take,
-                      const pk_run_dataset& d, const int64_t* idx) {
+                      const pk_run_dataset& d, const int64_t* idx, int64_t pos, int64_t e) {
   pk_ctx* c = p->ctx;
   if (!p->copy_stream) CK_CTX(c, cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
   if (!p->ev_copy[slot]) CK_CTX(c, cudaEventCreateWithFlags(&p->ev_copy[slot], cudaEventDisableTiming));
   const size_t es = c->esize(), rb = (size_t)d.dim * es;
-  for (int64_t i = 0; i < take; ++i) {
-    memcpy((char*)g->hx + (size_t)i * rb, (const char*)d.host_x + (size_t)idx[i] * d.host_ld * es, rb);
-    g->hy[i] = d.host_y[idx[i]];
+  if (d.mapped_x && d.mapped_y && d.order && d.order[e]) {
+    // zero-copy: the GPU pulls the batch's rows from page-locked host memory
+    if (c->dtype == PK_F64)
+      pk_k_gather_launch<double>(p, d, take, pos, e, g);
+    else
+      pk_k_gather_launch<float>(p, d, take, pos, e, g);
+    CK_CTX(c, cudaGetLastError());
+  } else {
+    for (int64_t i = 0; i < take; ++i) {
+      memcpy((char*)g->hx + (size_t)i * rb, (const char*)d.host_x + (size_t)idx[i] * d.host_ld * es, rb);
+      g->hy[i] = d.host_y[idx[i]];
+    }
+    CK_CTX(c, cudaMemcpyAsync(g->d->feat, g->hx, (size_t)take * rb, cudaMemcpyHostToDevice,
+                              p->copy_stream));
+    CK_CTX(c, cudaMemcpyAsync(g->d->labels, g->hy, (size_t)take * 4, cudaMemcpyHostToDevice,
+                              p->copy_stream));
   }
-  CK_CTX(c, cudaMemcpyAsync(g->d->feat, g->hx, (size_t)take * rb, cudaMemcpyHostToDevice,
-                            p->copy_stream));
-  CK_CTX(c, cudaMemcpyAsync(g->d->labels, g->hy, (size_t)take * 4, cudaMemcpyHostToDevice,
-                            p->copy_stream));
   CK_CTX(c, cudaEventRecord(p->ev_copy[slot], p->copy_stream));
   CK_CTX(c, cudaStreamWaitEvent(c->stream, p->ev_copy[slot], 0));
   return PK_OK;
@@ -285,7 +328,9 @@ extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset*
         if (d.host_x) {  // streamed: gather into this slot's pinned staging, H2D
           pk_pack::RunStage* g = run_stage(p, slot, gi, std::max<int64_t>(take, driver), d.dim);
           if (!g) return arg_err(c, "run: staging allocation failed");
-          if ((rc = run_gather(p, slot, g, take, d, perm + key.pos))) return rc;
+          if ((rc = run_gather(p, slot, g, take, d, perm + key.pos, key.pos,
+                               key.epoch - d.epoch0)))
+            return rc;
           f = pk_feed{g->d, nullptr, 0, take, gi};
         } else {
           const int64_t e = key.epoch - d.epoch0;

@@ -309,6 +309,23 @@ extern "C" int pk_dataset_gather_rows(pk_dataset* d, int64_t rows, const void* s
   return pk_dataset_write_rows(d, 0, rows, stage_x, stage_y);
 }
 
+extern "C" int pk_host_map(pk_ctx* c, void* host, int64_t bytes, void** dev) {
+  if (!c || !host || bytes <= 0 || !dev) return arg_err(c, "host_map: bad args");
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterMapped);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();  // shared buffer: fine
+  else CK_CTX(c, e);
+  CK_CTX(c, cudaHostGetDevicePointer(dev, host, 0));
+  return PK_OK;
+}
+
+extern "C" int pk_host_unmap(pk_ctx* c, void* host) {
+  if (!c || !host) return PK_ERR_ARG;
+  cudaSetDevice(c->device);
+  CK_CTX(c, cudaHostUnregister(host));
+  return PK_OK;
+}
+
 extern "C" int pk_dataset_destroy(pk_dataset* d) {
   if (!d) return PK_ERR_ARG;
   cudaSetDevice(d->ctx->device);

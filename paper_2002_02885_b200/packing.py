@@ -551,14 +551,20 @@ def _native_run(packed: PackedModel, datasets, max_steps: int, depth: int):
             d.host_y = y.ctypes.data
             d.epoch0, d.n_epochs, d.perm = e0, len(perms), C.cast(pa, C.c_void_p)
             keep += [perms, pa, x, y]
+            # device orders: the resident gather, and the GPU's own gather of
+            # streamed rows from page-locked host memory
+            orders = [rt.order(ds.dataset_id, ds.n, e, _order_fn(ds, e)) for e in range(e0, e1 + 1)]
+            oa = (C.c_void_p * len(orders))(*[o.ptr.value for o in orders])
+            d.order = C.cast(oa, C.c_void_p)
+            keep += [orders, oa]
             if stream:
                 d.host_x, d.host_ld = x.ctypes.data, x.strides[0] // x.itemsize
+                if not _rt.env_flag("PK_HOST_GATHER"):
+                    d.mapped_x, d.mapped_y = rt.host_rows_mapped(ds)
             else:
                 dev = rt.dataset(ds)
-                orders = [rt.order(ds.dataset_id, ds.n, e, _order_fn(ds, e)) for e in range(e0, e1 + 1)]
-                oa = (C.c_void_p * len(orders))(*[o.ptr.value for o in orders])
-                d.device, d.order = dev.ptr.value, C.cast(oa, C.c_void_p)
-                keep += [dev, orders, oa]
+                d.device = dev.ptr.value
+                keep.append(dev)
         n = max_steps - len(out)
         losses = np.empty((n, K), dtype=np.float64)
         act = np.empty((n, K), dtype=np.uint8)

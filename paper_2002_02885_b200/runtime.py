@@ -95,6 +95,7 @@ class Runtime:
         self._datasets: dict = {}
         self._orders: OrderedDict = OrderedDict()
         self._host_orders: OrderedDict = OrderedDict()
+        self._mapped: list = []
 
     def check(self, rc):
         return L.check(self.ptr, rc)
@@ -149,6 +150,22 @@ class Runtime:
                                         dtype=np.float64 if self.dtype == "f64" else np.float32),
                    np.ascontiguousarray(ds.labels, dtype=np.int32))
             self._datasets[key] = got
+        return got
+
+    def host_rows_mapped(self, ds):
+        """Device views (x, y) of host_rows_source(ds), page-locked and mapped
+        once per dataset: pk_pack_run's streamed steps let the GPU pull the
+        batch rows over PCIe itself (no host memcpy per step)."""
+        key = ("mapped", ds.dataset_id, id(ds.features), ds.features.shape)
+        got = self._datasets.get(key)
+        if got is None:
+            x, y = self.host_rows_source(ds)
+            dx, dy = C.c_void_p(), C.c_void_p()
+            self.check(self.lib.pk_host_map(self.ptr, x.ctypes.data, x.nbytes, C.byref(dx)))
+            self.check(self.lib.pk_host_map(self.ptr, y.ctypes.data, y.nbytes, C.byref(dy)))
+            got = (dx.value, dy.value)
+            self._datasets[key] = got
+            self._mapped.append((x, y))  # page-locked for the runtime's lifetime
         return got
 
     def host_order(self, dataset_id: str, n: int, epoch: int, make) -> np.ndarray:
