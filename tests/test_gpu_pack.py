@@ -403,6 +403,29 @@ def test_f64_context_reproduces_reference_golden_to_1e10():
         runtime.set_precision("f32")
 
 
+def test_f64_packed_run_reproduces_reference_golden():
+    """The native multi-step driver in the float64 context (the Hyperband
+    executor's mode): the reference's own 5-step trajectories, streamed and
+    resident inputs."""
+    z = np.load(os.path.join(G, "small_pairs.npz"))
+    runtime.set_precision("f64")
+    try:
+        for mode in ("resident", "stream"):
+            runtime.set_input_mode(mode)
+            for opt in engine.OPTIMIZERS:
+                arch = packing.MLPArch(6, (8,), 3, "tanh")
+                a = _h("a", opt=opt, seed=1, arch=arch)
+                b = _h("b", opt=opt, lr=0.01, seed=2, arch=arch)
+                packed = packing.dedup_inputs(packing.pack_models([a, b]))
+                ls = [list(d.values()) for d in packing.packed_run(packed, _ds(), 5)]
+                np.testing.assert_allclose(ls, z[f"{opt}_tanh_losses"], rtol=1e-10, atol=1e-13)
+                np.testing.assert_allclose(b._flat_params(b.params), z[f"{opt}_tanh_b_p5"],
+                                           rtol=1e-10, atol=1e-13)
+    finally:
+        runtime.set_input_mode("resident")
+        runtime.set_precision("f32")
+
+
 # ------------------------------------------------------ device memory --
 
 def test_member_device_bytes_matches_allocation():
