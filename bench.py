@@ -385,9 +385,11 @@ def _b200(args):
         "e2e": {"value": world * K * b * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
                 "d2h_bytes_per_step": 16 + 8 * K,
-                "api": "packing.packed_run (16 steps in flight), input_mode=stream: host "
-                       "gather → pinned → H2D per step, losses D2H per step; inputs are "
-                       "fresh host data every step (not L2-resident)"},
+                "api": "packing.packed_run (native pk_pack_run, up to 16 steps in flight, "
+                       "8-step graphs), input_mode=stream: each step's batch rows are read "
+                       "from page-locked mapped host memory by a device gather over PCIe "
+                       "(h2d bytes = the batch), losses D2H per step; inputs are fresh "
+                       "host data every step (not L2-resident)"},
         "e2e_sync": {"value": world * K * b * args.steps / (sync_ms / 1e3), "unit": UNIT,
                      "h2d_bytes_per_step": desc_bytes + b * (wl["dim"] + 1) * 4,
                      "d2h_bytes_per_step": 16 + 8 * K,
