@@ -422,6 +422,16 @@ HB = dict(n=2000, dim=784, classes=10, hidden=(16,), eta=3, seed=0,
           strategies=("original", "knn"))
 
 
+# Hyperband executor shapes (HB: 784-16-10, Table-4 batch sizes)
+HB_SHAPES = {
+    "hb1": dict(n=2000, dim=784, classes=10, hidden=(16,), act="relu", batch=40,
+                members=[("sgd", 0.1)]),
+    "hb8": dict(n=2000, dim=784, classes=10, hidden=(16,), act="relu", batch=40,
+                members=[(("sgd", "adam", "momentum", "adagrad")[i % 4], 10.0 ** -(1 + i % 4))
+                         for i in range(8)]),
+}
+
+
 def _hyperband_b200(R, world, group, precision="f64"):
     """Pack-aware Hyperband (BASELINE configs[4] shape, MLP executor): wall
     time of `original` (one config per group) and `knn` packing, rungs sharded

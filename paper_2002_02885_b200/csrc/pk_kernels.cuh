@@ -454,7 +454,8 @@ struct Gemm {
   // accumulate Σ_k B(k, n0+t) into *colsum, k ascending (the bias gradient).
   __device__ __forceinline__ static int run(T* smem, const Mat<T>& a, const Mat<T>& b,
                                             const int32_t* srow, int m0, int n0, int M, int N,
-                                            int Kr, bool CHECK_A = false, T* colsum = nullptr) {
+                                            int Kr, bool CHECK_A = false, T* colsum = nullptr,
+                                            int c_lo = 0, int c_hi = -1) {
     const bool COLSUM = colsum != nullptr;
     const bool va = vec_ok(a, AK ? Kr : M);
     const bool vb = vec_ok(b, BK ? Kr : N);
@@ -467,15 +468,19 @@ struct Gemm {
       for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
     bool bad = false;
     T csum = T(0);
-    const int nch = (Kr + KC - 1) / KC;
+    // chunks [c_lo, c_hi) of the k range (all of it by default); stage slots
+    // follow the absolute chunk index
+    const int nch = c_hi >= 0 ? c_hi : (Kr + KC - 1) / KC;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nch)
-        load_chunk(smem + s * (A_STAGE + B_STAGE), smem + s * (A_STAGE + B_STAGE) + A_STAGE, a,
-                   b, srow, s, m0, n0, M, N, Kr, va, vb);
+      const int c = c_lo + s;
+      if (c < nch)
+        load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
+                   smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0, M,
+                   N, Kr, va, vb);
       cp_commit();
     }
-    for (int c = 0; c < nch; ++c) {
+    for (int c = c_lo; c < nch; ++c) {
       const int pre = c + STAGES - 1;
       if (pre < nch) {
         T* st = smem + (pre % STAGES) * (A_STAGE + B_STAGE);
@@ -520,6 +525,90 @@ struct Gemm {
     return __syncthreads_or(bad);
   }
 
+  // Input-range segmented variant (FWD split, fwd_tile): chunks [c_lo, c_hi)
+  // in ranges of `cps` chunks aligned at multiples of cps.  At every range end
+  // the slice partials go through `seg` (SK*BM*BN elements outside the
+  // pipeline) and are reduced in value()'s order; thread t < BM*BN owns tile
+  // element t.  part != nullptr: range r's tile is stored at part + r*BM*BN;
+  // else the ranges are left-folded and the fold is left in seg[0, BM*BN).
+  static constexpr int SEG = SK * BM * BN;
+  __device__ static int run_seg(T* smem, T* seg, const Mat<T>& a, const Mat<T>& b,
+                                const int32_t* srow, int m0, int n0, int M, int N, int Kr,
+                                bool CHECK_A, int c_lo, int c_hi, int cps, T* part) {
+    static_assert(BM * BN <= NT, "one tile element per thread");
+    const bool va = vec_ok(a, AK ? Kr : M);
+    const bool vb = vec_ok(b, BK ? Kr : N);
+    const int slice = threadIdx.x / TPS, lt = threadIdx.x % TPS;
+    const int tc = lt % CS, tr = lt / CS;
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    bool bad = false;
+    T fold = T(0);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      const int c = c_lo + s;
+      if (c < c_hi)
+        load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
+                   smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0, M,
+                   N, Kr, va, vb);
+      cp_commit();
+    }
+    for (int c = c_lo; c < c_hi; ++c) {
+      const int pre = c + STAGES - 1;
+      if (pre < c_hi) {
+        T* st = smem + (pre % STAGES) * (A_STAGE + B_STAGE);
+        load_chunk(st, st + A_STAGE, a, b, srow, pre, m0, n0, M, N, Kr, va, vb);
+      }
+      cp_commit();
+      cp_wait<STAGES - 1>();
+      __syncthreads();
+      const T* sA = smem + (c % STAGES) * (A_STAGE + B_STAGE);
+      const T* sB = sA + A_STAGE;
+#pragma unroll 4
+      for (int q = 0; q < KS; ++q) {
+        const int kk = slice * KS + q;
+        T av[TM], bv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          av[i] = AK ? sA[(tr + i * RS) * A_LD + kk] : sA[kk * A_LD + tr + i * RS];
+          if (CHECK_A) bad |= !finite(av[i]);
+        }
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          bv[j] = BK ? sB[(tc + j * CS) * B_LD + kk] : sB[kk * B_LD + tc + j * CS];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      if (c + 1 == c_hi || (c + 1) % cps == 0) {  // range end
+        T* red = seg + slice * (BM * BN);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            red[(tr + i * RS) * BN + tc + j * CS] = acc[i][j];
+            acc[i][j] = T(0);
+          }
+        __syncthreads();
+        if (threadIdx.x < BM * BN) {
+          T v = seg[threadIdx.x];
+#pragma unroll
+          for (int s = 1; s < SK; ++s) v += seg[s * BM * BN + threadIdx.x];
+          if (part) __stcg(part + (size_t)(c / cps) * (BM * BN) + threadIdx.x, v);
+          else fold = (c / cps == c_lo / cps) ? v : fold + v;
+        }
+      }
+      __syncthreads();
+    }
+    cp_wait<0>();
+    if (!part && threadIdx.x < BM * BN) seg[threadIdx.x] = fold;
+    return __syncthreads_or(bad);
+  }
+
   __device__ __forceinline__ static T value(const T* smem, int mm, int nn) {
     T v = smem[mm * BN + nn];
 #pragma unroll
@@ -530,6 +619,7 @@ struct Gemm {
 
 // tile shapes: fixed per tile kind (never per pack) → K-invariant
 template <typename T> using FwdG = Gemm<T, 32, 8, 64, 4, 4, 16, 6, true, false>;
+constexpr int FWD_KC = 64;  // FwdG's chunk
 template <typename T> using TailG = Gemm<T, 32, 32, 64, 4, 4, 4, 4, true, false>;
 template <typename T> using DgradG = Gemm<T, 32, 16, 64, 4, 4, 8, 4, true, true>;
 template <typename T> using WgradG = Gemm<T, 32, 32, 32, 4, 4, 4, 4, false, false>;
@@ -543,7 +633,7 @@ constexpr int WG_BM = 32, WG_BN = 32;
 template <typename T>
 struct Smem {
   static constexpr int ROWS = ROWCAP * 4;
-  static constexpr int FWD = FwdG<T>::SMEM_T * (int)sizeof(T) + ROWS;
+  static constexpr int FWD = (FwdG<T>::SMEM_T + FwdG<T>::SEG) * (int)sizeof(T) + ROWS;
   static constexpr int WGRAD = WgradG<T>::SMEM_T * (int)sizeof(T) + ROWS;
   static constexpr int DGRAD = DgradG<T>::SMEM_T * (int)sizeof(T);
   static constexpr int HEAD = ROWS;
@@ -575,13 +665,38 @@ __device__ __forceinline__ Mat<T> input_mat(const MemberDev<T>& M, const FeedDev
 }
 
 // ---------------------------------------------------------------- FWD --
+// Input-range split (pk_pack.cuh emit): a member whose layer input spans
+// more than two chunks reduces it in fixed ranges of `cps` chunks (from its
+// shape alone), each range's partial tile reduced separately and the ranges
+// left-folded in order — so its arithmetic is the same however many CTAs
+// share a tile (packed == standalone bitwise).  When the phase leaves SMs
+// idle (small batch / narrow layer: the per-chunk latency chain of one CTA
+// dominates) a tile gets ng CTAs, CTA g owning ranges [g*R/ng, (g+1)*R/ng);
+// they store their range tiles in the pack workspace and the last to arrive
+// folds them and runs the epilogue.  Tile bits: n0 [0,20) column, [20,27)
+// cps (0 = unsplit); m0 [0,20) row, [20,24) g, [24,28) ng - 1.
+constexpr int kFwdMaxRanges = 8;
+__host__ __device__ inline int fwd_tile_n0(int32_t v) { return v & 0xFFFFF; }
+__host__ __device__ inline int fwd_tile_m0(int32_t v) { return v & 0xFFFFF; }
+__host__ __device__ inline int32_t fwd_pack_n0(int n0, int cps) { return n0 | (cps << 20); }
+__host__ __device__ inline int32_t fwd_pack_m0(int m0, int g, int ng) {
+  return m0 | (g << 20) | ((ng - 1) << 24);
+}
+
 template <typename T>
-__device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t) {
+__device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t,
+                         int32_t* ws) {
   using G = FwdG<T>;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
+  const int n0 = fwd_tile_n0(t.n0), m0 = fwd_tile_m0(t.m0), cps = (t.n0 >> 20) & 127;
+  const int g = (t.m0 >> 20) & 15, ng = ((t.m0 >> 24) & 15) + 1;
+  const int nch = (in + FWD_KC - 1) / FWD_KC;
+  const int NR = cps ? (nch + cps - 1) / cps : 1;
+  const int r_lo = g * NR / ng, r_hi = (g + 1) * NR / ng;
   const int R = f.take;
   T* smem = reinterpret_cast<T*>(sm);
-  int32_t* srow = reinterpret_cast<int32_t*>(sm + G::SMEM_T * sizeof(T));
+  T* seg = smem + G::SMEM_T;
+  int32_t* srow = reinterpret_cast<int32_t*>(sm + (G::SMEM_T + G::SEG) * sizeof(T));
   const int par = M.ctl->parity;
   const T* W = M.params[par] + M.w_off[l];
   const T* bias = M.params[par] + M.b_off[l];
@@ -590,19 +705,51 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   __syncthreads();
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{W, nullptr, 0, out};
+  constexpr int TS = FWD_BM * FWD_BN;
+  // workspace (pk_pack: d_done): [4 ints][one counter per CTA][8 range tiles per CTA]
+  const int b0 = blockIdx.x - g;
+  T* part = ng > 1 ? reinterpret_cast<T*>(ws + 4 + ((gridDim.x + 3) & ~3u)) +
+                         (size_t)b0 * kFwdMaxRanges * TS
+                   : nullptr;
   // layer 0: the input node's finite check (engine.py:233-235) rides on the
   // A operand already staged in shared memory
   PK_TRACE(1);
-  const int badx = (l == 0) ? G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, true)
-                            : G::run(smem, a, b, srow, t.m0, t.n0, R, out, in, false);
+  int badx;
+  if (cps)
+    badx = G::run_seg(smem, seg, a, b, srow, m0, n0, R, out, in, l == 0, r_lo * cps,
+                      min(nch, r_hi * cps), cps, part);
+  else
+    badx = (l == 0) ? G::run(smem, a, b, srow, m0, n0, R, out, in, true)
+                    : G::run(smem, a, b, srow, m0, n0, R, out, in, false);
   PK_TRACE(2);
   const bool last = (l == M.n_layers - 1);
   int bad = badx ? 0 : INT_MAX;
+  if (part) {
+    __threadfence();
+    __shared__ int arrived_last;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      arrived_last = (atomicAdd(ws + 4 + b0, r_hi - r_lo) + (r_hi - r_lo) == NR);
+    __syncthreads();
+    if (!arrived_last) {
+      if (badx && threadIdx.x == 0) flag_min(&M.ctl->bad_node, 0);
+      return;
+    }
+    __threadfence();
+    if (threadIdx.x == 0) ws[4 + b0] = 0;  // ready for the next launch
+    if (threadIdx.x < TS) {
+      T v = __ldcg(part + threadIdx.x);
+      for (int r = 1; r < NR; ++r) v += __ldcg(part + (size_t)r * TS + threadIdx.x);
+      seg[threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < FWD_BM * FWD_BN; e += NT) {
     const int mm = e / FWD_BN, nn = e % FWD_BN;
-    const int m = t.m0 + mm, n = t.n0 + nn;
+    const int m = m0 + mm, n = n0 + nn;
     if (m >= R || n >= out) continue;
-    const T z = G::value(smem, mm, nn) + bias[n];
+    const T acc = cps ? seg[e] : G::value(smem, mm, nn);
+    const T z = acc + bias[n];
     M.Z[l][(int64_t)m * out + n] = z;
     if (!finite(z)) bad = min(bad, 1 + 2 * l);
     if (!last) {
@@ -1125,7 +1272,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
   if (f.take != 0 && !halted(P)) {
     const MemberDev<T>& M = P.mems[t.member];
     if ((MASK & KM_FWD) && t.kind == TK_FWD) {
-      if (t.m0 < f.take) fwd_tile<T>(smem_raw, M, f, t);
+      if (fwd_tile_m0(t.m0) < f.take) fwd_tile<T>(smem_raw, M, f, t, P.done);
     } else if ((MASK & KM_TAIL) && t.kind == TK_TAIL) {
       if (t.m0 < f.take) tail_tile<T>(smem_raw, M, f, t, train);
     } else if ((MASK & KM_HEAD) && t.kind == TK_HEAD) {

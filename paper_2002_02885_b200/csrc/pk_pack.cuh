@@ -38,7 +38,8 @@ struct pk_pack {
   void* d_members = nullptr;  // MemberDev<T>[K]
   char* d_blob = nullptr;     // StepHdr + FeedDev<T>[K]
   size_t blob_bytes = 0;
-  int32_t* d_done = nullptr;  // CTA-completion counter for FINALIZE
+  int32_t* d_done = nullptr;  // CTA-completion counter for FINALIZE (+ FWD split workspace)
+  size_t done_bytes = 16;
   unsigned long long* d_trace = nullptr;  // PK_TRACE=1: stage stamps per CTA
   size_t trace_len = 0;
   Tile* d_tiles = nullptr;
@@ -278,14 +279,29 @@ static int kind_smem(int kind, const pk_member* m, int dtype) {
 
 
 // tiles of one (member, kind, layer) work item
-static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, int l) {
+static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, int l,
+                 int fwd_ctas = 1) {
   const auto& d = m->desc;
   switch (kind) {
-    case pk::TK_FWD:
+    case pk::TK_FWD: {
+      // input ranges from the member's shape alone (pk_kernels.cuh fwd_tile);
+      // CTAs per tile (ng) from the phase's room, which never changes the sums
+      const int nch = cdiv(d.dims[l], pk::FWD_KC);
+      int cps = 0, nr = 1;
+      if (nch >= 3 && !getenv("PK_NO_FWD_SPLIT")) {
+        cps = std::max(2, cdiv(nch, pk::kFwdMaxRanges));
+        nr = cdiv(nch, cps);
+        if (cps > 127) cps = 0, nr = 1;
+      }
+      const int ng = std::max(1, std::min({nr, fwd_ctas, 16}));
       for (int mb = 0; mb < cdiv(d.max_rows, pk::FWD_BM); ++mb)
         for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::FWD_BN); ++nb)
-          out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::FWD_BM, nb * pk::FWD_BN});
+          for (int g = 0; g < ng; ++g)
+            out.push_back(Tile{k, (int16_t)l, (int16_t)kind,
+                               pk::fwd_pack_m0(mb * pk::FWD_BM, g, ng),
+                               pk::fwd_pack_n0(nb * pk::FWD_BN, cps)});
       break;
+    }
     case pk::TK_TAIL:
       for (int mb = 0; mb < cdiv(d.max_rows, pk::TAIL_BM); ++mb)
         out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::TAIL_BM, 0});
@@ -490,11 +506,17 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   for (size_t ph = 0; ph < nph; ++ph) {
     Phase& P = phases[ph];
     double best = -1;
+    // FWD tiles share a tile among up to (SMs / tiles of the phase) CTAs
+    std::vector<Tile> probe;
+    for (int k = 0; k < p->K; ++k)
+      if (ph < seq[k].size())
+        for (auto [kind, layer] : seq[k][ph]) emit(probe, k, p->members[k], kind, layer);
+    const int fwd_ctas = std::max(1, 148 / std::max<int>(1, (int)probe.size()));
     for (int k = 0; k < p->K; ++k) {
       if (ph >= seq[k].size()) continue;
       for (auto [kind, layer] : seq[k][ph]) {
         const size_t before = P.host.size();
-        emit(P.host, k, p->members[k], kind, layer);
+        emit(P.host, k, p->members[k], kind, layer, fwd_ctas);
         P.smem = std::max(P.smem, kind_smem(kind, p->members[k], dt));
         const double w = double(P.host.size() - before);
         if (w > best) { best = w; P.kind = kind; P.layer = layer; }
@@ -774,7 +796,25 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
   if ((e = ctx_alloc(c, 0, hm.size(), &p->d_members, &p->cap_members)) != cudaSuccess) return fail(e);
   if ((e = ctx_alloc(c, 0, p->blob_bytes, (void**)&p->d_blob, &p->cap_blob)) != cudaSuccess)
     return fail(e);
-  if ((e = ctx_alloc(c, 0, 16, (void**)&p->d_done, &p->cap_done)) != cudaSuccess) return fail(e);
+  // d_done: [done, halt, -, -] + the FWD split workspace (one arrival counter
+  // per CTA, then kFwdMaxRanges range tiles per CTA) for the largest phase in
+  // which FWD tiles are shared by several CTAs
+  size_t ws_ctas = 0;
+  for (auto* v : {&p->train, &p->eval})
+    for (auto& ph : *v) {
+      if (ph.special) continue;
+      for (const Tile& t : ph.host)
+        if (t.kind == pk::TK_FWD && (t.m0 >> 24)) {
+          ws_ctas = std::max(ws_ctas, (size_t)ph.ntiles);
+          break;
+        }
+    }
+  const size_t es = c->dtype == PK_F64 ? 8 : 4;
+  p->done_bytes = 16 + (ws_ctas ? 4 * ((ws_ctas + 3) & ~(size_t)3) +
+                                      ws_ctas * pk::kFwdMaxRanges * pk::FWD_BM * pk::FWD_BN * es
+                                : 0);
+  if ((e = ctx_alloc(c, 0, p->done_bytes, (void**)&p->d_done, &p->cap_done)) != cudaSuccess)
+    return fail(e);
   if ((e = ctx_alloc(c, 0, std::max<size_t>(1, all.size()) * sizeof(Tile), (void**)&p->d_tiles,
                      &p->cap_tiles)) != cudaSuccess)
     return fail(e);
@@ -785,7 +825,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
     return fail(e);
   if ((e = cudaHostGetDevicePointer((void**)&p->d_ring, p->h_ring, 0)) != cudaSuccess) return fail(e);
   memset(p->h_ring, 0, (size_t)p->ring_stride * kRing);
-  cudaMemsetAsync(p->d_done, 0, 16, c->stream);
+  cudaMemsetAsync(p->d_done, 0, p->done_bytes, c->stream);
   cudaMemcpyAsync(p->d_members, hm.data(), hm.size(), cudaMemcpyHostToDevice, c->stream);
   if (!all.empty())
     cudaMemcpyAsync(p->d_tiles, all.data(), all.size() * sizeof(Tile), cudaMemcpyHostToDevice, c->stream);

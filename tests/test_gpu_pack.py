@@ -426,6 +426,42 @@ def test_f64_packed_run_reproduces_reference_golden():
         runtime.set_precision("f32")
 
 
+def test_fwd_input_ranges_lockstep_parity():
+    """Generic forward with input ranges (in=300: 3 ranges of 2 chunks) and
+    tiles shared by several CTAs: per-step parity with the f64 oracle."""
+    datasets = _ds(n=400, d=300, c=10, seed=11)
+    hs = [packing.make_handle(f"r{i}", packing.MLPArch(300, (40, 24), 10, "relu"), opt, lr,
+                              b, 20, "d", i)
+          for i, (opt, lr, b) in enumerate((("sgd", 0.05, 40), ("adam", 0.002, 33),
+                                            ("momentum", 0.02, 64)))]
+    lockstep(packing.dedup_inputs(packing.pack_models(hs)), datasets, 5, packing=packing)
+
+
+def test_f64_fwd_input_ranges_k_invariant():
+    """Hyperband shape (784-16-10, float64): a member alone shares each forward
+    tile among 7 CTAs, inside an 8-member pack among 4; the input-range sums
+    are the same, so the trajectories are bit-identical."""
+    runtime.set_precision("f64")
+    try:
+        ds = {"t": data.synth_dataset(600, 784, 10, seed=7)}
+        arch = packing.MLPArch(784, (16,), 10, "relu")
+
+        def mk(i):
+            return packing.make_handle(f"h{i}", arch, ("sgd", "adam", "momentum", "adagrad")[i % 4],
+                                       0.01 * (1 + i % 3), 40, 30, "t", i)
+        hs, solo = [mk(i) for i in range(8)], [mk(i) for i in range(8)]
+        packed = packing.dedup_inputs(packing.pack_models(hs))
+        for _ in range(6):
+            packing.packed_step(packed, ds)
+        for h in solo:
+            for _ in range(6):
+                packing.standalone_step(h, ds)
+        for a, b in zip(hs, solo):
+            assert _maxdiff(a, b) == 0.0
+    finally:
+        runtime.set_precision("f32")
+
+
 # ------------------------------------------------------ device memory --
 
 def test_member_device_bytes_matches_allocation():

@@ -12,15 +12,17 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import bench  # noqa: E402
-from paper_2002_02885_b200 import data, packing  # noqa: E402
+from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="config0", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--workload", default="config0", choices=sorted(bench.WORKLOADS) + sorted(bench.HB_SHAPES))
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--steps", type=int, default=20)
     a = ap.parse_args()
-    wl = bench.WORKLOADS[a.workload]
+    wl = bench.WORKLOADS.get(a.workload) or bench.HB_SHAPES[a.workload]
+    runtime.set_precision(a.precision)
     datasets, hs = bench._make(wl, data, packing)
     packed = packing.dedup_inputs(packing.pack_models(hs))
     for _ in range(a.steps):

@@ -24,18 +24,19 @@ from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
 STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1",
           "s8", "s9", "s10", "s11", "s12", "s13", "s14", "s15")
 
-
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="config0", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--workload", default="config0", choices=sorted(bench.WORKLOADS) + sorted(bench.HB_SHAPES))
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--warm", action="store_true", help="no L2 flush before the traced step")
     ap.add_argument("--steps", type=int, default=3, help="traced steps (last one printed)")
     a = ap.parse_args()
     import torch
+    runtime.set_precision(a.precision)
     rt = runtime.runtime()
     stream = torch.cuda.Stream()
     rt.set_stream(stream.cuda_stream)
-    wl = bench.WORKLOADS[a.workload]
+    wl = bench.WORKLOADS.get(a.workload) or bench.HB_SHAPES[a.workload]
     datasets, hs = bench._make(wl, data, packing)
     packed = packing.dedup_inputs(packing.pack_models(hs))
     for _ in range(5):
@@ -56,7 +57,7 @@ def main():
     code, phases, _ = dp.profile()  # only for per-phase CTA counts
     t0 = arr[arr[:, 0] > 0, 0].min()
     off = 0
-    plan = bench._phase_plan(wl)
+    plan = bench._phase_plan(wl, 8 if a.precision == "f64" else 4)
     for i, (kind, layer, ctas, _) in enumerate(phases):
         blk = arr[off:off + ctas]
         off += ctas
