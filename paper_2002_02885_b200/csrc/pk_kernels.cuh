@@ -620,11 +620,13 @@ struct Gemm {
 // tile shapes: fixed per tile kind (never per pack) → K-invariant
 template <typename T> using FwdG = Gemm<T, 32, 8, 64, 4, 4, 16, 6, true, false>;
 constexpr int FWD_KC = 64;  // FwdG's chunk
-template <typename T> using TailG = Gemm<T, 32, 32, 64, 4, 4, 4, 4, true, false>;
+template <typename T> using TailG = Gemm<T, 16, 32, 64, 2, 4, 4, 4, true, false>;
 template <typename T> using DgradG = Gemm<T, 32, 16, 64, 4, 4, 8, 4, true, true>;
 template <typename T> using WgradG = Gemm<T, 32, 32, 32, 4, 4, 4, 4, false, false>;
 constexpr int FWD_BM = 32, FWD_BN = 8;
-constexpr int TAIL_BM = 32, TAIL_MAXC = 32;
+// TAIL: 16-row tiles — its serial softmax-xent + dgrad chain is per row, so
+// small batches spread over more CTAs (the per-element sums are unchanged)
+constexpr int TAIL_BM = 16, TAIL_MAXC = 32;
 constexpr int HEAD_BM = 32;
 constexpr int DG_BM = 32, DG_BN = 16;
 constexpr int WG_BM = 32, WG_BN = 32;
@@ -789,6 +791,34 @@ __device__ __forceinline__ void xent_row(const T* z, T* dz, int C, int y, int R,
   if (lane == 0 && rowloss) *rowloss = -(double)((zy - mx) - lg(s));
 }
 
+// xent_row for C <= 16 on a half warp (lanes [16h, 16h+16)): the same
+// butterfly minus its first step, which only folds in the idle lanes' -inf /
+// 0 — identical results.  Both halves run the shuffles; `active` gates the
+// row's reads and writes.
+template <typename T>
+__device__ __forceinline__ void xent_row16(const T* z, T* dz, int C, int y, int R, bool train,
+                                           double* rowloss, bool active) {
+  const int lane = threadIdx.x & 15;
+  T mx = -INFINITY;
+  if (active && lane < C) mx = z[lane];
+#pragma unroll
+  for (int o = 8; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o, 16));
+  T s = T(0);
+  if (active && lane < C) s = ex(z[lane] - mx);
+#pragma unroll
+  for (int o = 8; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 16);
+  const T zy = active ? z[y] : T(0);  // before dz (which may alias z) is written
+  __syncwarp();
+  if (!active) return;
+  if (train && lane < C) {
+    const T inv = T(1) / s, nv = T(R);
+    T p = ex(z[lane] - mx) * inv;
+    if (lane == y) p -= T(1);
+    dz[lane] = p / nv;
+  }
+  if (lane == 0 && rowloss) *rowloss = -(double)((zy - mx) - lg(s));
+}
+
 template <typename T>
 __device__ void head_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t,
                           bool train) {
@@ -854,9 +884,18 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   __syncthreads();
   // softmax-xent per row, in place in sD (logits → dlogits)
   const int warp = threadIdx.x >> 5;
-  for (int mm = warp; mm < TAIL_BM && t.m0 + mm < R; mm += NT / 32) {
-    T* row = sD + mm * (TAIL_MAXC + 1);
-    xent_row(row, row, C, ylab[mm], R, train, M.rowloss + t.m0 + mm);
+  if (C <= 16) {  // two rows per warp
+    for (int m2 = 2 * warp; m2 < TAIL_BM && t.m0 + m2 < R; m2 += NT / 16) {
+      const int mm = m2 + ((threadIdx.x >> 4) & 1);
+      const bool act = mm < TAIL_BM && t.m0 + mm < R;
+      T* row = sD + (act ? mm : m2) * (TAIL_MAXC + 1);
+      xent_row16(row, row, C, act ? ylab[mm] : 0, R, train, M.rowloss + t.m0 + mm, act);
+    }
+  } else {
+    for (int mm = warp; mm < TAIL_BM && t.m0 + mm < R; mm += NT / 32) {
+      T* row = sD + mm * (TAIL_MAXC + 1);
+      xent_row(row, row, C, ylab[mm], R, train, M.rowloss + t.m0 + mm);
+    }
   }
   PK_TRACE(3);
   if (!train) return;
