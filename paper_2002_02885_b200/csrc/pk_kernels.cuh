@@ -1211,7 +1211,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
         if (P.mems[k].tensor) {
           c->bc1 = c->bcn1;
           c->bc2 = c->bcn2;
-        } else {
+        } else if (P.mems[k].opt == PK_OPT_ADAM) {  // the only reader (wgrad_tile)
           adam_bias_corrections(c->step_counter, &c->bc1, &c->bc2);
         }
         ++committed;
