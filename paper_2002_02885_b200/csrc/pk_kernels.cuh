@@ -36,6 +36,7 @@
 
 #include <cstdint>
 #include <climits>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -623,6 +624,10 @@ constexpr int FWD_KC = 64;  // FwdG's chunk
 template <typename T> using TailG = Gemm<T, 16, 32, 64, 2, 4, 4, 4, true, false>;
 template <typename T> using DgradG = Gemm<T, 32, 16, 64, 4, 4, 8, 4, true, true>;
 template <typename T> using WgradG = Gemm<T, 32, 32, 32, 4, 4, 4, 4, false, false>;
+// narrow layers (out <= 16): 64 x 16 tiles, the same 1024 elements per CTA
+// and the same per-element sums (chunk / slice order), half the CTAs
+template <typename T> using WgradNG = Gemm<T, 64, 16, 32, 8, 2, 4, 4, false, false>;
+constexpr int WGN_BM = 64, WGN_BN = 16;
 constexpr int FWD_BM = 32, FWD_BN = 8;
 // TAIL: 16-row tiles — its serial softmax-xent + dgrad chain is per row, so
 // small batches spread over more CTAs (the per-element sums are unchanged)
@@ -636,7 +641,9 @@ template <typename T>
 struct Smem {
   static constexpr int ROWS = ROWCAP * 4;
   static constexpr int FWD = (FwdG<T>::SMEM_T + FwdG<T>::SEG) * (int)sizeof(T) + ROWS;
-  static constexpr int WGRAD = WgradG<T>::SMEM_T * (int)sizeof(T) + ROWS;
+  static constexpr int WGRAD = (WgradG<T>::SMEM_T > WgradNG<T>::SMEM_T ? WgradG<T>::SMEM_T
+                                                                       : WgradNG<T>::SMEM_T) *
+                                   (int)sizeof(T) + ROWS;
   static constexpr int DGRAD = DgradG<T>::SMEM_T * (int)sizeof(T);
   static constexpr int HEAD = ROWS;
   // TAIL: pipeline + resident W_L [in x C] + dZ block [32 x 33] + rows
@@ -976,9 +983,10 @@ __device__ void dgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
 }
 
 // -------------------------------------------------------------- WGRAD --
-template <typename T>
+template <typename T, int WB>
 __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t) {
-  using G = WgradG<T>;
+  using G = typename std::conditional<WB == WGN_BM, WgradNG<T>, WgradG<T>>::type;
+  constexpr int WG_BM = WB, WG_BN = WB == WGN_BM ? WGN_BN : 32;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
   const int R = f.take;
   T* smem = reinterpret_cast<T*>(sm);
@@ -1235,6 +1243,12 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
 
 // ------------------------------------------------------------- kernels --
 
+// WGRAD tiles of narrow layers carry bit 20 of n0 (pk_pack.cuh emit)
+__device__ __forceinline__ Tile wg_tile(Tile t) {
+  t.n0 &= 0xFFFFF;
+  return t;
+}
+
 // L2 prefetch of every active member's committed params + slots (first
 // phase): the step's dominant HBM stream overlaps the forward pass.
 template <typename T>
@@ -1319,7 +1333,8 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
     } else if ((MASK & KM_DGRAD) && t.kind == TK_DGRAD) {
       if (t.m0 < f.take) dgrad_tile<T>(smem_raw, M, f, t);
     } else if ((MASK & KM_WGRAD) && t.kind == TK_WGRAD) {
-      wgrad_tile<T>(smem_raw, M, f, t);
+      if (t.n0 >> 20) wgrad_tile<T, WGN_BM>(smem_raw, M, f, wg_tile(t));
+      else wgrad_tile<T, WG_BM>(smem_raw, M, f, t);
     }
   }
   kernel_end(P, train);

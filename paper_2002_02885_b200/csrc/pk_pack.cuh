@@ -316,6 +316,12 @@ static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, in
           out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::DG_BM, nb * pk::DG_BN});
       break;
     default:  // WGRAD over W_l [in x out]
+      if (d.dims[l + 1] <= pk::WGN_BN && !getenv("PK_NO_WGRAD_NARROW")) {
+        // narrow layer: 64 x 16 tiles (pk_kernels.cuh WgradNG), flagged by n0 bit 20
+        for (int mb = 0; mb < cdiv(d.dims[l], pk::WGN_BM); ++mb)
+          out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::WGN_BM, 1 << 20});
+        break;
+      }
       for (int mb = 0; mb < cdiv(d.dims[l], pk::WG_BM); ++mb)
         for (int nb = 0; nb < cdiv(d.dims[l + 1], pk::WG_BN); ++nb)
           out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::WG_BM, nb * pk::WG_BN});

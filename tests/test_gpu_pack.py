@@ -437,6 +437,28 @@ def test_fwd_input_ranges_lockstep_parity():
     lockstep(packing.dedup_inputs(packing.pack_models(hs)), datasets, 5, packing=packing)
 
 
+def test_narrow_wgrad_tiles_match_square_tiles_bitwise(monkeypatch):
+    """Weight-gradient tiles of narrow layers (out <= 16) are 64x16 instead of
+    32x32: the per-element sums keep their order, so the trajectories are
+    bit-identical to the 32x32 tiles (PK_NO_WGRAD_NARROW=1)."""
+    datasets = _ds(n=300, d=100, c=10, seed=4)
+    arch = packing.MLPArch(100, (16, 12), 10, "tanh")
+    runs = []
+    for narrow in (True, False):
+        if narrow:
+            monkeypatch.delenv("PK_NO_WGRAD_NARROW", raising=False)
+        else:
+            monkeypatch.setenv("PK_NO_WGRAD_NARROW", "1")
+        hs = [packing.make_handle(f"w{i}", arch, opt, 0.01, 24, 20, "d", i)
+              for i, opt in enumerate(("adam", "momentum"))]
+        packed = packing.pack_models(hs)
+        for _ in range(5):
+            packing.packed_step(packed, datasets)
+        runs.append(hs)
+    for a, b in zip(*runs):
+        assert _maxdiff(a, b) == 0.0
+
+
 def test_f64_fwd_input_ranges_k_invariant():
     """Hyperband shape (784-16-10, float64): a member alone shares each forward
     tile among 7 CTAs, inside an 8-member pack among 4; the input-range sums
