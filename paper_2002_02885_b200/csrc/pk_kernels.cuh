@@ -1166,6 +1166,27 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
   __shared__ int s_code, s_who, s_idx, s_stop;
   const int K = P.K, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;  // kernels run 8 or 12 warps
+  // K <= 32: the commit's operands (parity, step counter, Adam's next bias
+  // corrections, the loss) are fetched / computed while the losses reduce —
+  // by the last warp when it has no member to reduce, else by warp 0 — and
+  // handed over in shared memory (no second round trip on the serial tail)
+  __shared__ double f_loss[32], f_bc1[32], f_bc2[32];
+  __shared__ long long f_step[32];
+  __shared__ int f_par[32];
+  const bool fast = train && K <= 32;
+  if (fast && warp == (K < nw ? nw - 1 : 0) && lane < K && feed_of(P, lane).take) {
+    const MemberDev<T>& M = P.mems[lane];
+    const MemberCtl* c = M.ctl;
+    const long long step = c->step_counter;
+    f_par[lane] = c->parity;
+    f_step[lane] = step;
+    if (M.tensor) {
+      f_bc1[lane] = c->bcn1;
+      f_bc2[lane] = c->bcn2;
+    } else if (M.opt == PK_OPT_ADAM) {
+      adam_bias_corrections(step + 1, &f_bc1[lane], &f_bc2[lane]);
+    }
+  }
   // warp w reduces the loss terms of members w, w+8, ...: lane-strided
   // partial sums then a fixed butterfly (deterministic, K-invariant)
   for (int k = warp; k < K; k += nw) {
@@ -1174,17 +1195,21 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
     if (take) {
       const MemberDev<T>& M = P.mems[k];
       MemberCtl* c = M.ctl;
+      bn = c->bad_node;  // issued ahead of the row-loss loads
+      bg = c->bad_grad;
+      const double tl = (train && M.tensor) ? c->loss : 0.0;
       double s = 0.0;
       if (!(train && M.tensor)) {
         for (int r = lane; r < take; r += 32) s += M.rowloss[r];
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       }
-      bn = c->bad_node;
-      bg = c->bad_grad;
       if (train) {
-        const double loss = M.tensor ? c->loss : s / double(take);
-        if (lane == 0) c->loss = loss;
+        const double loss = M.tensor ? tl : s / double(take);
+        if (lane == 0) {
+          c->loss = loss;
+          if (fast) f_loss[k] = loss;
+        }
         if (!isfinite(loss)) bn = min(bn, 2 * M.n_layers);
       } else if (lane == 0) {
         c->eval_acc += s;
@@ -1195,6 +1220,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
       s_bg[k] = bg;
     }
   }
+  PK_TRACE(8);
   __syncthreads();
   if (threadIdx.x == 0) {
     int code = PK_OK, who = -1, idx = -1, stop = K;
@@ -1205,13 +1231,26 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
     s_code = code; s_who = who; s_idx = idx; s_stop = stop;
   }
   __syncthreads();
+  PK_TRACE(9);
   int32_t* st = reinterpret_cast<int32_t*>(P.ring + (int64_t)hdr_of(P).slot * P.ring_stride);
   double* losses = reinterpret_cast<double*>(st + 4);
   int committed = 0;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     MemberCtl* c = P.mems[k].ctl;
     const bool act = feed_of(P, k).take != 0;
-    if (train) {
+    if (train && fast) {
+      losses[k] = act ? f_loss[k] : 0.0;
+      if (act && k < s_stop) {
+        c->parity = f_par[k] ^ 1;
+        c->step_counter = f_step[k] + 1;
+        if (P.mems[k].tensor || P.mems[k].opt == PK_OPT_ADAM) {  // the only reader: wgrad_tile
+          c->bc1 = f_bc1[k];
+          c->bc2 = f_bc2[k];
+        }
+        ++committed;
+      }
+      if (act) c->fault_grad = -1;  // one-shot
+    } else if (train) {
       losses[k] = act ? c->loss : 0.0;
       if (act && k < s_stop) {
         c->parity ^= 1;
@@ -1229,6 +1268,7 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
     c->bad_node = INT_MAX;
     c->bad_grad = INT_MAX;
   }
+  PK_TRACE(10);
   committed = __syncthreads_count(committed > 0) ? committed : committed;
   __shared__ int s_comm;
   if (threadIdx.x == 0) s_comm = 0;
