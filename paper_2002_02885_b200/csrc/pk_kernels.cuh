@@ -1328,17 +1328,25 @@ __device__ __forceinline__ void kernel_end(const PhaseArgs<T>& P, bool train) {
   PK_TRACE(5);
   pdl_wait();
   if (!P.is_last) return;
-  __shared__ int last;
+  __shared__ int last, was_halted;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    last = (atomicAdd(P.done, 1) == (int)gridDim.x - 1);
+    // the halt flag only changes in a FINALIZE (of an earlier step, complete
+    // before this step's first launch passed its PDL wait): its load is
+    // issued while the arrival atomic is in flight, not after it
+    int prev, hv = 0;
+    asm volatile("atom.add.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.done) : "memory");
+    if (train && P.halt)
+      asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(hv) : "l"(P.halt) : "memory");
+    was_halted = hv != 0;
+    last = (prev == (int)gridDim.x - 1);
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   PK_TRACE(6);
-  if (train && halted(P)) finalize_skipped<T>(P);
+  if (train && was_halted) finalize_skipped<T>(P);
   else if (train && P.all_tensor) finalize_fast<T>(P);
   else finalize<T>(P, train);
   PK_TRACE(7);
