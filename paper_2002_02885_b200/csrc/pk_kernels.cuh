@@ -715,6 +715,9 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{W, nullptr, 0, out};
   constexpr int TS = FWD_BM * FWD_BN;
+  static_assert(TS == NT, "one tile element per thread in the epilogue");
+  // the thread's bias element, fetched under the GEMM
+  const T bias_e = (n0 + (int)threadIdx.x % FWD_BN < out) ? bias[n0 + threadIdx.x % FWD_BN] : T(0);
   // workspace (pk_pack: d_done): [4 ints][one counter per CTA][8 range tiles per CTA]
   const int b0 = blockIdx.x - g;
   T* part = ng > 1 ? reinterpret_cast<T*>(ws + 4 + ((gridDim.x + 3) & ~3u)) +
@@ -746,9 +749,15 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
     }
     __threadfence();
     if (threadIdx.x == 0) ws[4 + b0] = 0;  // ready for the next launch
-    if (threadIdx.x < TS) {
-      T v = __ldcg(part + threadIdx.x);
-      for (int r = 1; r < NR; ++r) v += __ldcg(part + (size_t)r * TS + threadIdx.x);
+    if (threadIdx.x < TS) {  // all range tiles in flight at once, then the fold
+      T pv[kFwdMaxRanges];
+#pragma unroll
+      for (int r = 0; r < kFwdMaxRanges; ++r)
+        pv[r] = r < NR ? __ldcg(part + (size_t)r * TS + threadIdx.x) : T(0);
+      T v = pv[0];
+#pragma unroll
+      for (int r = 1; r < kFwdMaxRanges; ++r)
+        if (r < NR) v += pv[r];
       seg[threadIdx.x] = v;
     }
     __syncthreads();
@@ -758,7 +767,7 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
     const int m = m0 + mm, n = n0 + nn;
     if (m >= R || n >= out) continue;
     const T acc = cps ? seg[e] : G::value(smem, mm, nn);
-    const T z = acc + bias[n];
+    const T z = acc + bias_e;
     M.Z[l][(int64_t)m * out + n] = z;
     if (!finite(z)) bad = min(bad, 1 + 2 * l);
     if (!last) {
@@ -1200,7 +1209,15 @@ __device__ __noinline__ void finalize(const PhaseArgs<T>& P, bool train) {
       const double tl = (train && M.tensor) ? c->loss : 0.0;
       double s = 0.0;
       if (!(train && M.tensor)) {
-        for (int r = lane; r < take; r += 32) s += M.rowloss[r];
+        // four rows per lane in flight at once, summed in row order
+        for (int r0 = lane; r0 < take; r0 += 128) {
+          double x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = r0 + 32 * u < take ? M.rowloss[r0 + 32 * u] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + 32 * u < take) s += x[u];
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       }
