@@ -877,6 +877,10 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
   }
   if (threadIdx.x < TAIL_BM && t.m0 + (int)threadIdx.x < R)
     ylab[threadIdx.x] = f.labels[feed_row(f, t.m0 + threadIdx.x)];
+  // the thread's bias element (its column is fixed: NT is a multiple of TAIL_MAXC)
+  static_assert(NT % TAIL_MAXC == 0, "fixed epilogue column per thread");
+  const int ce = threadIdx.x % TAIL_MAXC;
+  const T bias_e = ce < C ? bias[ce] : T(0);
   if (L == 0) stage_rows(srow, f, R);
   if (L > 0) pdl_wait();
   __syncthreads();
@@ -891,7 +895,7 @@ __device__ void tail_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, 
     const int mm = e / TAIL_MAXC, c = e % TAIL_MAXC;
     const int m = t.m0 + mm;
     if (m >= R || c >= C) continue;
-    const T z = G::value(smem, mm, c) + bias[c];
+    const T z = G::value(smem, mm, c) + bias_e;
     M.Z[L][(int64_t)m * C + c] = z;
     sD[mm * (TAIL_MAXC + 1) + c] = z;
     if (!finite(z)) bad = min(bad, 1 + 2 * L);
@@ -1018,31 +1022,13 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
       l2_prefetch_lines(reinterpret_cast<const void*>(p0), (uint32_t)(p1 - p0));
     }
   }
-  if (l == 0) stage_rows(srow, f, R);
-  pdl_wait();
-  __syncthreads();
-  // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]; tiles on the first
-  // row block also sum dZ_l's columns (the bias gradient) from the staged B
-  const Mat<T> a = input_mat(M, f, l);
-  const Mat<T> b{M.dZ[l], nullptr, 0, out};
-  T gb = T(0);
-  PK_TRACE(1);
-  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr);
-  PK_TRACE(2);
-  const T lr = T(ctl->lr), wd = T(M.wd);
-  T bc1 = T(1), bc2 = T(1);
-  if (M.opt == PK_OPT_ADAM) {
-    bc1 = T(ctl->bc1);
-    bc2 = T(ctl->bc2);
-  }
   const T* __restrict__ s0c = sc;
   T* __restrict__ s0n = sn;
   const T* __restrict__ s1c = sc ? sc + P : nullptr;
   T* __restrict__ s1n = sn ? sn + P : nullptr;
-  const int gpos = 2 * (M.n_layers - 1 - l);
-  const int fault = ctl->fault_grad;
-  // optimizer epilogue: gather every operand of the thread's elements first,
-  // then update — one memory round trip per tensor, not per element
+  // optimizer operands: every element's weight and slots are gathered before
+  // the GEMM (they do not depend on earlier phases; one round trip per
+  // tensor, hidden under the GEMM — the L2 prefetch above warmed them)
   constexpr int PER = WG_BM * WG_BN / NT;
   int64_t idx[PER];
   bool ok[PER];
@@ -1059,6 +1045,25 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
       if (M.n_slots >= 2) s1[u] = s1c[idx[u]];
     }
   }
+  const T lr = T(ctl->lr), wd = T(M.wd);
+  T bc1 = T(1), bc2 = T(1);
+  if (M.opt == PK_OPT_ADAM) {
+    bc1 = T(ctl->bc1);
+    bc2 = T(ctl->bc2);
+  }
+  const int gpos = 2 * (M.n_layers - 1 - l);
+  const int fault = ctl->fault_grad;
+  if (l == 0) stage_rows(srow, f, R);
+  pdl_wait();
+  __syncthreads();
+  // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]; tiles on the first
+  // row block also sum dZ_l's columns (the bias gradient) from the staged B
+  const Mat<T> a = input_mat(M, f, l);
+  const Mat<T> b{M.dZ[l], nullptr, 0, out};
+  T gb = T(0);
+  PK_TRACE(1);
+  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr);
+  PK_TRACE(2);
   bool badW = false;
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
