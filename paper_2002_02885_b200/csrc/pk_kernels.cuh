@@ -382,8 +382,9 @@ struct Gemm {
   __device__ __forceinline__ static void load_chunk_vec(T* sA, T* sB, const Mat<T>& a,
                                                         const Mat<T>& b, const int32_t* srow,
                                                         int k0, int m0, int n0, int M, int N,
-                                                        int Kr, bool va, bool vb) {
-    if (va) {
+                                                        int Kr, bool va, bool vb, bool do_a = true,
+                                                        bool do_b = true) {
+    if (va && do_a) {
       for (int e = threadIdx.x; e < A_ELEMS / VEC; e += NT) {
         int kk, mm;
         if (AK) { kk = (e % (KC / VEC)) * VEC; mm = e / (KC / VEC); }
@@ -396,7 +397,7 @@ struct Gemm {
         cp_async<16>(s, g, ok);
       }
     }
-    if (vb) {
+    if (vb && do_b) {
       for (int e = threadIdx.x; e < B_ELEMS / VEC; e += NT) {
         int kk, nn;
         if (BK) { kk = (e % (KC / VEC)) * VEC; nn = e / (KC / VEC); }
@@ -413,10 +414,11 @@ struct Gemm {
 
   __device__ __forceinline__ static void load_chunk(T* sA, T* sB, const Mat<T>& a, const Mat<T>& b,
                                                     const int32_t* srow, int chunk, int m0, int n0,
-                                                    int M, int N, int Kr, bool va, bool vb) {
+                                                    int M, int N, int Kr, bool va, bool vb,
+                                                    bool do_a = true, bool do_b = true) {
     const int k0 = chunk * KC;
-    load_chunk_vec(sA, sB, a, b, srow, k0, m0, n0, M, N, Kr, va, vb);
-    if (!va)
+    load_chunk_vec(sA, sB, a, b, srow, k0, m0, n0, M, N, Kr, va, vb, do_a, do_b);
+    if (!va && do_a)
 #pragma unroll 2
     for (int e = threadIdx.x; e < A_ELEMS; e += NT) {
       int kk, mm;
@@ -428,7 +430,7 @@ struct Gemm {
       T* s = AK ? sA + mm * A_LD + kk : sA + kk * A_LD + mm;
       cp_async<sizeof(T)>(s, g, ok);
     }
-    if (!vb)
+    if (!vb && do_b)
 #pragma unroll 2
     for (int e = threadIdx.x; e < B_ELEMS; e += NT) {
       int kk, nn;
@@ -456,7 +458,7 @@ struct Gemm {
   __device__ __forceinline__ static int run(T* smem, const Mat<T>& a, const Mat<T>& b,
                                             const int32_t* srow, int m0, int n0, int M, int N,
                                             int Kr, bool CHECK_A = false, T* colsum = nullptr,
-                                            int c_lo = 0, int c_hi = -1) {
+                                            int c_lo = 0, int c_hi = -1, bool a_early = false) {
     const bool COLSUM = colsum != nullptr;
     const bool va = vec_ok(a, AK ? Kr : M);
     const bool vb = vec_ok(b, BK ? Kr : N);
@@ -472,13 +474,27 @@ struct Gemm {
     // chunks [c_lo, c_hi) of the k range (all of it by default); stage slots
     // follow the absolute chunk index
     const int nch = c_hi >= 0 ? c_hi : (Kr + KC - 1) / KC;
+    // a_early: A does not depend on the previous launch — the prologue's A
+    // chunks are issued before the PDL wait (uncommitted, so they join the
+    // first group), the B chunks after it
+    if (a_early) {
+#pragma unroll
+      for (int s = 0; s < STAGES - 1; ++s) {
+        const int c = c_lo + s;
+        if (c < nch)
+          load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
+                     smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0,
+                     M, N, Kr, va, vb, true, false);
+      }
+      pdl_wait();
+    }
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       const int c = c_lo + s;
       if (c < nch)
         load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
                    smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0, M,
-                   N, Kr, va, vb);
+                   N, Kr, va, vb, !a_early, true);
       cp_commit();
     }
     for (int c = c_lo; c < nch; ++c) {
@@ -1053,8 +1069,10 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   }
   const int gpos = 2 * (M.n_layers - 1 - l);
   const int fault = ctl->fault_grad;
+  // layer 0: the input rows do not come from this step's launches — their
+  // first chunks load before the PDL wait (inside G::run), dZ_0's after it
   if (l == 0) stage_rows(srow, f, R);
-  pdl_wait();
+  else pdl_wait();
   __syncthreads();
   // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]; tiles on the first
   // row block also sum dZ_l's columns (the bias gradient) from the staged B
@@ -1062,7 +1080,8 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const Mat<T> b{M.dZ[l], nullptr, 0, out};
   T gb = T(0);
   PK_TRACE(1);
-  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr);
+  G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr, 0, -1,
+         l == 0);
   PK_TRACE(2);
   bool badW = false;
 #pragma unroll
