@@ -354,6 +354,7 @@ struct Mat {
 template <typename T, int BM, int BN, int KC, int TM, int TN, int SK, int STAGES, bool AK, bool BK>
 struct Gemm {
   static constexpr int TPS = NT / SK;
+  static constexpr int KCH = KC;
   static constexpr int RS = BM / TM;
   static constexpr int CS = BN / TN;
   static_assert(RS * CS == TPS, "micro-tile does not cover the tile");
@@ -458,7 +459,7 @@ struct Gemm {
   __device__ __forceinline__ static int run(T* smem, const Mat<T>& a, const Mat<T>& b,
                                             const int32_t* srow, int m0, int n0, int M, int N,
                                             int Kr, bool CHECK_A = false, T* colsum = nullptr,
-                                            int c_lo = 0, int c_hi = -1, bool a_early = false) {
+                                            int c_lo = 0, int c_hi = -1, bool a_issued = false) {
     const bool COLSUM = colsum != nullptr;
     const bool va = vec_ok(a, AK ? Kr : M);
     const bool vb = vec_ok(b, BK ? Kr : N);
@@ -474,27 +475,13 @@ struct Gemm {
     // chunks [c_lo, c_hi) of the k range (all of it by default); stage slots
     // follow the absolute chunk index
     const int nch = c_hi >= 0 ? c_hi : (Kr + KC - 1) / KC;
-    // a_early: A does not depend on the previous launch — the prologue's A
-    // chunks are issued before the PDL wait (uncommitted, so they join the
-    // first group), the B chunks after it
-    if (a_early) {
-#pragma unroll
-      for (int s = 0; s < STAGES - 1; ++s) {
-        const int c = c_lo + s;
-        if (c < nch)
-          load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
-                     smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0,
-                     M, N, Kr, va, vb, true, false);
-      }
-      pdl_wait();
-    }
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       const int c = c_lo + s;
       if (c < nch)
         load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
                    smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0, M,
-                   N, Kr, va, vb, !a_early, true);
+                   N, Kr, va, vb, !a_issued, true);
       cp_commit();
     }
     for (int c = c_lo; c < nch; ++c) {
@@ -542,6 +529,22 @@ struct Gemm {
     return __syncthreads_or(bad);
   }
 
+  // The prologue's A chunks alone (uncommitted: they join the first cp.async
+  // group of run / run_seg called with a_issued).  For an A that does not
+  // depend on the previous launch: issued before the PDL wait, B after it.
+  __device__ static void prologue_a(T* smem, const Mat<T>& a, const int32_t* srow, int m0, int M,
+                                    int Kr, int c_lo, int c_hi) {
+    const bool va = vec_ok(a, AK ? Kr : M);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      const int c = c_lo + s;
+      if (c < c_hi)
+        load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
+                   smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, a, srow, c, m0, 0, M,
+                   0, Kr, va, false, true, false);
+    }
+  }
+
   // Input-range segmented variant (FWD split, fwd_tile): chunks [c_lo, c_hi)
   // in ranges of `cps` chunks aligned at multiples of cps.  At every range end
   // the slice partials go through `seg` (SK*BM*BN elements outside the
@@ -551,7 +554,8 @@ struct Gemm {
   static constexpr int SEG = SK * BM * BN;
   __device__ static int run_seg(T* smem, T* seg, const Mat<T>& a, const Mat<T>& b,
                                 const int32_t* srow, int m0, int n0, int M, int N, int Kr,
-                                bool CHECK_A, int c_lo, int c_hi, int cps, T* part) {
+                                bool CHECK_A, int c_lo, int c_hi, int cps, T* part,
+                                bool a_issued = false) {
     static_assert(BM * BN <= NT, "one tile element per thread");
     const bool va = vec_ok(a, AK ? Kr : M);
     const bool vb = vec_ok(b, BK ? Kr : N);
@@ -570,7 +574,7 @@ struct Gemm {
       if (c < c_hi)
         load_chunk(smem + (c % STAGES) * (A_STAGE + B_STAGE),
                    smem + (c % STAGES) * (A_STAGE + B_STAGE) + A_STAGE, a, b, srow, c, m0, n0, M,
-                   N, Kr, va, vb);
+                   N, Kr, va, vb, !a_issued, true);
       cp_commit();
     }
     for (int c = c_lo; c < c_hi; ++c) {
@@ -709,8 +713,11 @@ __host__ __device__ inline int32_t fwd_pack_m0(int m0, int g, int ng) {
 }
 
 template <typename T>
+__device__ __noinline__ void prefetch_params(const PhaseArgs<T>& P);
+
+template <typename T>
 __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, const Tile& t,
-                         int32_t* ws) {
+                         int32_t* ws, const PhaseArgs<T>* first = nullptr) {
   using G = FwdG<T>;
   const int l = t.layer, in = M.dims[l], out = M.dims[l + 1];
   const int n0 = fwd_tile_n0(t.n0), m0 = fwd_tile_m0(t.m0), cps = (t.n0 >> 20) & 127;
@@ -722,13 +729,28 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   T* smem = reinterpret_cast<T*>(sm);
   T* seg = smem + G::SMEM_T;
   int32_t* srow = reinterpret_cast<int32_t*>(sm + (G::SMEM_T + G::SEG) * sizeof(T));
-  const int par = M.ctl->parity;
-  const T* W = M.params[par] + M.w_off[l];
-  const T* bias = M.params[par] + M.b_off[l];
+  const Mat<T> a = input_mat(M, f, l);
   if (l == 0) stage_rows(srow, f, R);
   if (l > 0) pdl_wait();  // A_{l-1} comes from the previous phase
   __syncthreads();
-  const Mat<T> a = input_mat(M, f, l);
+  if (first) {
+    // the step's first launch (k_phase): the batch rows do not depend on the
+    // previous step, so their first chunks load before the PDL wait; the
+    // parity, halt flag and parameters are read after it
+    G::prologue_a(smem, a, srow, m0, R, in, cps ? r_lo * cps : 0,
+                  cps ? min(nch, r_hi * cps) : nch);
+    pdl_wait();
+    pdl_launch();
+    if (halted(*first)) {
+      cp_commit();
+      cp_wait<0>();
+      return;
+    }
+    if (first->prefetch) prefetch_params(*first);
+  }
+  const int par = M.ctl->parity;
+  const T* W = M.params[par] + M.w_off[l];
+  const T* bias = M.params[par] + M.b_off[l];
   const Mat<T> b{W, nullptr, 0, out};
   constexpr int TS = FWD_BM * FWD_BN;
   static_assert(TS == NT, "one tile element per thread in the epilogue");
@@ -743,12 +765,13 @@ __device__ void fwd_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f, c
   // A operand already staged in shared memory
   PK_TRACE(1);
   int badx;
+  const bool ai = first != nullptr;
   if (cps)
     badx = G::run_seg(smem, seg, a, b, srow, m0, n0, R, out, in, l == 0, r_lo * cps,
-                      min(nch, r_hi * cps), cps, part);
+                      min(nch, r_hi * cps), cps, part, ai);
   else
-    badx = (l == 0) ? G::run(smem, a, b, srow, m0, n0, R, out, in, true)
-                    : G::run(smem, a, b, srow, m0, n0, R, out, in, false);
+    badx = (l == 0) ? G::run(smem, a, b, srow, m0, n0, R, out, in, true, nullptr, 0, -1, ai)
+                    : G::run(smem, a, b, srow, m0, n0, R, out, in, false, nullptr, 0, -1, ai);
   PK_TRACE(2);
   const bool last = (l == M.n_layers - 1);
   int bad = badx ? 0 : INT_MAX;
@@ -1071,13 +1094,17 @@ __device__ void wgrad_tile(char* sm, const MemberDev<T>& M, const FeedDev<T>& f,
   const int fault = ctl->fault_grad;
   // layer 0: the input rows do not come from this step's launches — their
   // first chunks load before the PDL wait (inside G::run), dZ_0's after it
-  if (l == 0) stage_rows(srow, f, R);
-  else pdl_wait();
-  __syncthreads();
   // A(m=i, k=r) = input[r][i]; B(k=r, n=j) = dZ_l[r][j]; tiles on the first
   // row block also sum dZ_l's columns (the bias gradient) from the staged B
   const Mat<T> a = input_mat(M, f, l);
   const Mat<T> b{M.dZ[l], nullptr, 0, out};
+  if (l == 0) {
+    stage_rows(srow, f, R);
+    __syncthreads();
+    G::prologue_a(smem, a, srow, t.m0, in, R, 0, (R + G::KCH - 1) / G::KCH);
+  }
+  pdl_wait();
+  __syncthreads();
   T gb = T(0);
   PK_TRACE(1);
   G::run(smem, a, b, srow, t.m0, t.n0, in, out, R, false, t.m0 == 0 ? &gb : nullptr, 0, -1,
@@ -1406,11 +1433,22 @@ __global__ void __launch_bounds__(NT, 1) k_phase(const __grid_constant__ PhaseAr
   if (threadIdx.x == 0)
     pk_trace_slots = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   PK_TRACE(0);
-  pdl_begin(P);
-  if (P.prefetch) prefetch_params(P);
+  // tiles, feeds and the step header are static or step-inline: readable
+  // before the PDL wait
   const Tile t = tile_of(P);
   const FeedDev<T> f = feed_of(P, t.member);
   const bool train = (hdr_of(P).mode == 0);
+  // a first-launch layer-0 FWD tile waits inside fwd_tile, after its batch
+  // rows are in flight
+  const bool early = (MASK & KM_FWD) && P.first && t.kind == TK_FWD && t.layer == 0 &&
+                     f.take != 0 && fwd_tile_m0(t.m0) < f.take;
+  if (early) {
+    fwd_tile<T>(smem_raw, P.mems[t.member], f, t, P.done, &P);
+    kernel_end(P, train);
+    return;
+  }
+  pdl_begin(P);
+  if (P.prefetch) prefetch_params(P);
   if (f.take != 0 && !halted(P)) {
     const MemberDev<T>& M = P.mems[t.member];
     if ((MASK & KM_FWD) && t.kind == TK_FWD) {
