@@ -48,10 +48,17 @@ struct pk_ctx {
     int kind;
   };
   std::vector<Block> blocks;
+  // device blocks up to kArenaBlock are carved from 64 MiB arenas: a cache
+  // miss costs no cudaMalloc (Hyperband creates a member slab per new
+  // configuration); arena blocks stay cached until the context is destroyed
+  std::vector<std::pair<char*, size_t>> arenas;
+  char* arena_cur = nullptr;
+  size_t arena_left = 0;
   std::vector<cudaEvent_t> events;
 };
 
 static const char* const kAllocKind[] = {"device", "pinned", "mapped"};
+constexpr size_t kArenaBlock = size_t(8) << 20, kArenaBytes = size_t(64) << 20;
 
 // a cached block of `kind` with bytes <= cap <= slack·bytes, else a fresh one
 static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size_t* cap,
@@ -72,25 +79,59 @@ static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size
     return cudaSuccess;
   }
   *cap = bytes;
+  if (kind == 0 && bytes <= kArenaBlock) {
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (c->arena_left < need) {
+      char* a = nullptr;
+      cudaError_t e = cudaMalloc(&a, kArenaBytes);
+      if (e != cudaSuccess) return e;
+      c->arenas.push_back({a, kArenaBytes});
+      c->arena_cur = a;
+      c->arena_left = kArenaBytes;
+    }
+    *out = c->arena_cur;
+    *cap = need;
+    c->arena_cur += need;
+    c->arena_left -= need;
+    return cudaSuccess;
+  }
   if (kind == 0) return cudaMalloc(out, bytes);
   return cudaHostAlloc(out, bytes, kind == 1 ? cudaHostAllocDefault : cudaHostAllocMapped);
 }
 
-static void ctx_free_block(const pk_ctx::Block& b) {
-  if (b.kind == 0) cudaFree(b.p);
-  else cudaFreeHost(b.p);
+static bool ctx_in_arena(const pk_ctx* c, const void* p) {
+  const char* q = static_cast<const char*>(p);
+  for (const auto& a : c->arenas)
+    if (q >= a.first && q < a.first + a.second) return true;
+  return false;
+}
+
+static void ctx_free_block(const pk_ctx* c, const pk_ctx::Block& b) {
+  if (b.kind == 0) {
+    if (!ctx_in_arena(c, b.p)) cudaFree(b.p);
+  } else {
+    cudaFreeHost(b.p);
+  }
 }
 
 static void ctx_release(pk_ctx* c, int kind, void* p, size_t cap) {
   if (!p) return;
   c->blocks.push_back({p, cap, kind});
-  size_t held = 0;
-  for (const auto& b : c->blocks) held += b.cap;
-  // bounded (entries and bytes): drop the oldest
-  while (!c->blocks.empty() && (c->blocks.size() > 512 || held > (size_t(2) << 30))) {
-    held -= c->blocks.front().cap;
-    ctx_free_block(c->blocks.front());
-    c->blocks.erase(c->blocks.begin());
+  // bounded (entries and bytes) over the blocks that own their memory: drop
+  // the oldest of those; arena blocks stay until the context goes
+  size_t held = 0, owned = 0;
+  for (const auto& b : c->blocks)
+    if (b.kind != 0 || !ctx_in_arena(c, b.p)) held += b.cap, ++owned;
+  for (size_t i = 0; i < c->blocks.size() && (owned > 512 || held > (size_t(2) << 30));) {
+    const auto& b = c->blocks[i];
+    if (b.kind == 0 && ctx_in_arena(c, b.p)) {
+      ++i;
+      continue;
+    }
+    held -= b.cap;
+    --owned;
+    ctx_free_block(c, b);
+    c->blocks.erase(c->blocks.begin() + i);
   }
 }
 
@@ -187,7 +228,8 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (!c) return PK_ERR_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (const auto& b : c->blocks) ctx_free_block(b);
+  for (const auto& b : c->blocks) ctx_free_block(c, b);
+  for (const auto& a : c->arenas) cudaFree(a.first);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
