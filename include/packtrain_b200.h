@@ -239,6 +239,33 @@ int64_t pk_pack_trace(pk_pack* p, uint64_t* out, int64_t cap);
 /* number of kernel launches one pk_pack_step enqueues */
 int32_t pk_pack_launches_per_step(const pk_pack* p);
 
+/* ======================================================================
+ * Conv pack path (BASELINE configs 1-4: LeNet / MobileNetV2 / ResNet /
+ * DenseNet members).  The reference engine has no conv layers
+ * (SPEC.md:15, :90); these entry points extend its pack primitive
+ * (packing.py:185-264 packed_step semantics: shared input groups, per-member
+ * valid rows, one optimizer step per member) to conv members.  Activations
+ * are NHWC bf16, GEMMs run on tcgen05 (bf16 operands, fp32 accumulate),
+ * master weights and optimizer slots are fp32.
+ * ====================================================================== */
+typedef struct pk_conv_geom {
+  int32_t n, h, w, c;            /* input NHWC (c a multiple of 8) */
+  int32_t k, r, s, stride, pad;  /* output channels, filter, stride (1|2), pad */
+  int32_t p, q;                  /* output spatial dims */
+} pk_conv_geom;
+
+/* One implicit-GEMM conv on caller-owned device buffers (unit-test and
+ * microbenchmark hook of the kernel every conv layer uses).
+ *   mode 0 FPROP: out bf16 [n*p*q][k]  = conv(x bf16 [n,h,w,c], w bf16 [k][kpad]),
+ *                 kpad = roundup(r*s*c, 64), w[k][(r*s_+s)*c + ci]
+ *   mode 1 DGRAD: out bf16 [n*h*w][c]  from dy bf16 [n*p*q][k] and the transposed
+ *                 weights w = wt bf16 [c][roundup(r*s*k, 64)], wt[ci][(r*s_+s)*k + co]
+ *   mode 2 WGRAD: out f32 [splits][k][kpad] partial sums over pixel splits
+ * ntile: GEMM N tile (16..256, multiple of 16; of 64 for WGRAD); stages 2..6. */
+int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void* x, const void* w,
+                      const void* dy, void* out, int32_t ntile, int32_t splits,
+                      int32_t stages, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

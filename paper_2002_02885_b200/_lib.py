@@ -34,6 +34,7 @@ EXPORTS = (
     "pk_pack_create", "pk_pack_destroy", "pk_pack_step", "pk_pack_step_async",
     "pk_pack_step_wait", "pk_pack_eval", "pk_pack_profile_step", "pk_pack_trace",
     "pk_pack_launches_per_step",
+    "pk_conv_gemm_test",
 )
 
 
@@ -76,6 +77,11 @@ class RunDataset(C.Structure):
 
 
 PK_RUN_MAX_STEPS, PK_RUN_NO_MEMBER, PK_RUN_NEED_PERM, PK_RUN_LABEL_BOUNDS, PK_RUN_FAILED = range(5)
+
+
+class ConvGeom(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in ("n", "h", "w", "c", "k", "r", "s", "stride", "pad",
+                                         "p", "q")]
 
 
 class PKError(RuntimeError):
@@ -135,6 +141,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            P(i32), P(dbl), P(Status)]),
         "pk_pack_trace": (i64, [vp, vp, i64]),
         "pk_pack_launches_per_step": (i32, [vp]),
+        "pk_conv_gemm_test": (C.c_int, [i32, P(ConvGeom), vp, vp, vp, vp, i32, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1,0 +1,350 @@
+// pk_convgemm.cuh — grouped implicit-GEMM convolution on tcgen05 (bf16 → fp32 TMEM).
+//
+// The dense conv and linear layers of the conv pack path
+// are three GEMM shapes over NHWC bf16 activations:
+//   FPROP  Y[m = (n,p,q), co]  = Σ_k  X[n, p·st−pad+r, q·st−pad+s, ci] · W[co, k]
+//          k = (r, s, ci), ci fastest; A gathered (im2col) by cp.async, B = W by TMA.
+//   DGRAD  dX[m = (n,h,w), ci] = Σ_k dY[n, (h+pad−r)/st, (w+pad−s)/st, co] · Wt[ci, k]
+//          k = (r, s, co); taps whose quotient is not exact are zero; B = Wt by TMA
+//          (a transposed bf16 copy the optimizer writes next to W).
+//   WGRAD  dW[co, n = (r,s,ci)] = Σ_pix dY[pix, co] · X[im2col(pix), n]
+//          both operands MN-major (pixel rows), gathered by cp.async; the pixel
+//          reduction may be split (fixed split boundaries; the optimizer sums the
+//          split partials in split order, so the result never depends on timing).
+// One launch covers up to kMaxProblems problems — the K members of a pack at
+// one layer (ragged rows / shapes allowed).  A CTA owns one 128 x NT output
+// tile of one problem; problems never share a tile, and every output element's
+// reduction order (64-deep K blocks in order, UMMA K=16 steps in order) is fixed
+// by the problem's own shape, so a member's result is independent of the pack
+// it trains in (packed == standalone bit for bit).
+//
+// Warp roles (192 threads): warps 0-3 gather operands with cp.async (16-B
+// chunks, zero fill for padding / out-of-image taps) and then run the
+// epilogue (TMEM lane quarter = warp); warp 4 owns TMEM and one lane issues the
+// tcgen05.mma chain; warp 5 lane 0 issues the TMA loads of the weight operand.
+// Stages ring through full/empty mbarriers; the producers' arrival on a
+// stage lags one stage behind its issue (cp.async.wait_group 1 → proxy fence →
+// arrive), so copies of consecutive stages overlap.
+#pragma once
+#include "pk_tc.cuh"
+
+namespace cg {
+
+enum Mode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
+constexpr int BM = 128, BK = 64;
+constexpr int kMaxProblems = 16;
+constexpr int kThreads = 192;
+
+struct Problem {
+  const __nv_bfloat16* src;   // gather source: X (FPROP/WGRAD) or dY (DGRAD)
+  const __nv_bfloat16* src2;  // WGRAD: dY (the A operand)
+  void* dst;                  // bf16 Y / dX, or fp32 dW partials
+  int M, N, K;                // GEMM extents (K = true reduction extent, unpadded)
+  int kper;                   // WGRAD: pixels per split (multiple of 64); else 0
+  int tiles_m, tiles_n, splits, tile0;
+  int brow0;                  // FPROP/DGRAD: first row of this problem's B in the map
+  int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
+  int OH, OW;                 // spatial dims of the GEMM's pixel space
+  int R, S, stride, pad;
+  int dld;                    // dst row stride (elements)
+  int ald;                    // WGRAD: dY pixel stride
+  int nseg;                   // FPROP: columns per dst segment (concat-N), 0 = one
+  int accumulate;             // DGRAD: dst += result
+  long long dseg;             // elements between dst segments
+  long long split_stride;     // WGRAD: elements between split partials
+};
+
+struct Launch {
+  Problem p[kMaxProblems];
+  int nprob;
+  int ntile;   // N tile: multiple of 16 in [16, 256] (multiple of 64 for WGRAD)
+  int stages;  // 2..6
+  int total_tiles;
+};
+
+__host__ __device__ inline uint32_t stage_bytes(int ntile) { return 16384u + (uint32_t)ntile * 128u; }
+__host__ inline size_t smem_bytes(int ntile, int stages) {
+  return 1024 + (size_t)stages * stage_bytes(ntile) + 8 * (2 * stages + 1) + 16;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile, ST = L.stages;
+  const uint32_t SB = stage_bytes(NT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * SB);
+  uint64_t* empty = full + ST;
+  uint64_t* done = empty + ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- tile → (problem, split, m tile, n tile) ----
+  int pi = 0;
+  const int t = blockIdx.x;
+  while (pi + 1 < L.nprob && t >= L.p[pi + 1].tile0) ++pi;
+  const Problem& P = L.p[pi];
+  int lt = t - P.tile0;
+  const int per_split = P.tiles_m * P.tiles_n;
+  const int split = lt / per_split;
+  lt -= split * per_split;
+  const int tm = lt % P.tiles_m, tn = lt / P.tiles_m;
+  int k0 = 0, kend = P.K;
+  if (MODE == WGRAD) {
+    k0 = split * P.kper;
+    kend = min(P.K, k0 + P.kper);
+  }
+  const int nkb = (kend - k0 + BK - 1) / BK;
+  constexpr bool kTma = MODE != WGRAD;
+
+  if (tid == 160) {
+    for (int s = 0; s < ST; ++s) {
+      umma::mbar_init(&full[s], 128 + (kTma ? 1 : 0));
+      umma::mbar_init(&empty[s], 1);
+    }
+    umma::mbar_init(done, 1);
+    umma::mbar_fence_init();
+    if (kTma) tc::tma_prefetch(&tmB);
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)NT);
+  if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // =========================== producers ===========================
+    const uint32_t sbase = tc::smem_u32(smem);
+    if (MODE != WGRAD) {
+      const int j = tid & 7, r0 = tid >> 3;
+      int rimg[8], ry[8], rx[8];
+      const int ohw = P.OH * P.OW;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = tm * BM + r0 + 16 * i;
+        if (m < P.M) {
+          const int n = m / ohw, rem = m - n * ohw, y = rem / P.OW, x = rem - y * P.OW;
+          rimg[i] = n * P.SH * P.SW;
+          if (MODE == FPROP) {
+            ry[i] = y * P.stride - P.pad;
+            rx[i] = x * P.stride - P.pad;
+          } else {
+            ry[i] = y + P.pad;
+            rx[i] = x + P.pad;
+          }
+        } else {
+          rimg[i] = -1;
+          ry[i] = rx[i] = 0;
+        }
+      }
+      const int sh = P.stride - 1;  // stride in {1, 2}
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % ST;
+        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+        const uint32_t a_s = sbase + s * SB;
+        const int k = k0 + kb * BK + 8 * j;
+        const int tap = k / P.SC, c = k - tap * P.SC;
+        const int r = tap / P.S, sx = tap - r * P.S;
+        const bool kok = k < kend;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          int iy, ix;
+          bool ok = kok && rimg[i] >= 0;
+          if (MODE == FPROP) {
+            iy = ry[i] + r;
+            ix = rx[i] + sx;
+          } else {
+            const int ny = ry[i] - r, nx = rx[i] - sx;
+            ok = ok && ny >= 0 && nx >= 0 && ((ny | nx) & sh) == 0;
+            iy = ny >> sh;
+            ix = nx >> sh;
+          }
+          ok = ok && (unsigned)iy < (unsigned)P.SH && (unsigned)ix < (unsigned)P.SW;
+          const __nv_bfloat16* g =
+              ok ? P.src + ((long long)(rimg[i] + iy * P.SW + ix) * P.sld + c) : P.src;
+          tc::cp16(a_s + tc::kmaj_sw128(r0 + 16 * i, j), g, ok);
+        }
+        tc::cp_commit();
+        if (kb >= 1) {
+          tc::cp_wait<1>();
+          umma::fence_async_smem();
+          tc::mbar_arrive(&full[(kb - 1) % ST]);
+        }
+      }
+    } else {
+      // A: dY [64 pixel rows][128 co], MN-major
+      const int acj = tid & 15, arr = tid >> 4;
+      const int co = tm * BM + acj * 8;
+      const bool co_ok = co < P.M;
+      // B: X im2col [64 pixel rows][NT cols], MN-major
+      const int cpr = NT >> 3, rpp = 128 / cpr, passes = BK / rpp;
+      const int bcj = tid % cpr, brr = tid / cpr;
+      const int col = tn * NT + bcj * 8;
+      const int tap = col / P.SC, cc = col - tap * P.SC;
+      const int fr = tap / P.S, fs = tap - fr * P.S;
+      const bool col_ok = col < P.N;
+      const int ohw = P.OH * P.OW;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % ST;
+        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+        const uint32_t a_s = sbase + s * SB, b_s = a_s + 16384;
+        const int kbase = k0 + kb * BK;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = arr + 8 * i, pix = kbase + row;
+          const bool ok = co_ok && pix < kend;
+          const __nv_bfloat16* g = ok ? P.src2 + ((long long)pix * P.ald + co) : P.src2;
+          tc::cp16(a_s + tc::mnmaj_sw128(row, acj), g, ok);
+        }
+        for (int ps = 0; ps < passes; ++ps) {
+          const int row = brr + ps * rpp, pix = kbase + row;
+          bool ok = col_ok && pix < kend;
+          int off = 0;
+          if (ok) {
+            const int n = pix / ohw, rem = pix - n * ohw, y = rem / P.OW, x = rem - y * P.OW;
+            const int iy = y * P.stride - P.pad + fr, ix = x * P.stride - P.pad + fs;
+            ok = (unsigned)iy < (unsigned)P.SH && (unsigned)ix < (unsigned)P.SW;
+            off = ((n * P.SH + iy) * P.SW + ix) * P.sld + cc;
+          }
+          tc::cp16(b_s + tc::mnmaj_sw128(row, bcj), ok ? P.src + off : P.src, ok);
+        }
+        tc::cp_commit();
+        if (kb >= 1) {
+          tc::cp_wait<1>();
+          umma::fence_async_smem();
+          tc::mbar_arrive(&full[(kb - 1) % ST]);
+        }
+      }
+    }
+    if (nkb > 0) {
+      tc::cp_wait<0>();
+      umma::fence_async_smem();
+      tc::mbar_arrive(&full[(nkb - 1) % ST]);
+    }
+
+    // =========================== epilogue ===========================
+    umma::mbar_wait(done, 0);
+    umma::fence_after();
+    const int row = warp * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const int m = tm * BM + row;
+    for (int c0 = 0; c0 < NT; c0 += 16) {
+      float v[16];
+      if (nkb > 0) {
+        tc::tmem_ld16(trow + c0, v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+      }
+      const int n0 = tn * NT + c0;
+      if (m >= P.M || n0 >= P.N) continue;
+      if (MODE == WGRAD) {
+        float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride +
+                   (long long)m * P.dld + n0;
+        if (n0 + 16 <= P.N) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        } else {
+          for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
+        }
+      } else {
+        int seg = 0, nn = n0;
+        if (P.nseg > 0) {
+          seg = n0 / P.nseg;
+          nn = n0 - seg * P.nseg;
+        }
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(P.dst) + (long long)seg * P.dseg +
+                           (long long)m * P.dld + nn;
+        const bool vec = n0 + 16 <= P.N && (P.nseg == 0 || nn + 16 <= P.nseg);
+        if (vec) {
+          if (P.accumulate) {
+            const uint4 o0 = reinterpret_cast<const uint4*>(d)[0];
+            const uint4 o1 = reinterpret_cast<const uint4*>(d)[1];
+            const __nv_bfloat16* ob0 = reinterpret_cast<const __nv_bfloat16*>(&o0);
+            const __nv_bfloat16* ob1 = reinterpret_cast<const __nv_bfloat16*>(&o1);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              v[e] += __bfloat162float(ob0[e]);
+              v[e + 8] += __bfloat162float(ob1[e]);
+            }
+          }
+          uint4 w0, w1;
+          w0.x = tc::pack_bf16(v[0], v[1]);
+          w0.y = tc::pack_bf16(v[2], v[3]);
+          w0.z = tc::pack_bf16(v[4], v[5]);
+          w0.w = tc::pack_bf16(v[6], v[7]);
+          w1.x = tc::pack_bf16(v[8], v[9]);
+          w1.y = tc::pack_bf16(v[10], v[11]);
+          w1.z = tc::pack_bf16(v[12], v[13]);
+          w1.w = tc::pack_bf16(v[14], v[15]);
+          reinterpret_cast<uint4*>(d)[0] = w0;
+          reinterpret_cast<uint4*>(d)[1] = w1;
+        } else {
+          for (int e = 0; e < 16 && n0 + e < P.N; ++e) {
+            int sg = seg, cn = nn + e;
+            if (P.nseg > 0 && cn >= P.nseg) {
+              sg += cn / P.nseg;
+              cn -= (cn / P.nseg) * P.nseg;
+            }
+            __nv_bfloat16* de = static_cast<__nv_bfloat16*>(P.dst) + (long long)sg * P.dseg +
+                                (long long)m * P.dld + cn;
+            float x = v[e];
+            if (P.accumulate) x += __bfloat162float(*de);
+            *de = __float2bfloat16_rn(x);
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // =========================== MMA issuer ===========================
+    if (lane == 0) {
+      constexpr bool mn = MODE == WGRAD;
+      const uint32_t idesc = tc::idesc_bf16(BM, NT, mn, mn);
+      const uint32_t sbase = tc::smem_u32(smem);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % ST;
+        umma::mbar_wait(&full[s], (kb / ST) & 1);
+        umma::fence_after();
+        const uint32_t a_s = sbase + s * SB, b_s = a_s + 16384;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          uint64_t ad, bd;
+          if (mn) {
+            ad = tc::sdesc_sw128(a_s + ks * 2048, 8192, 1024);
+            bd = tc::sdesc_sw128(b_s + ks * 2048, 8192, 1024);
+          } else {
+            ad = tc::sdesc_sw128(a_s + ks * 32, 16, 1024);
+            bd = tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
+          }
+          tc::mma_bf16(tmem, ad, bd, idesc, (kb | ks) != 0);
+        }
+        umma::commit(&empty[s]);
+      }
+      umma::commit(done);
+    }
+    __syncwarp();
+  } else if (kTma && warp == 5 && lane == 0) {
+    // =========================== TMA (weights) ===========================
+    const uint32_t bbytes = (uint32_t)NT * 128u;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % ST;
+      if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+      umma::mbar_arrive_expect_tx(&full[s], bbytes);
+      tc::tma_load_2d(smem + s * SB + 16384, &tmB, k0 + kb * BK, P.brow0 + tn * NT, &full[s]);
+    }
+  }
+
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, tcols);
+  }
+}
+
+}  // namespace cg

@@ -1,0 +1,125 @@
+// pk_tc.cuh — bf16 tcgen05 / TMA / cp.async layer for the conv pack path.
+//
+// Complements pk_umma.cuh (kind::tf32, SWIZZLE_NONE) with what the implicit-
+// GEMM conv kernels need:
+//   * kind::f16 (bf16 operands, fp32 accumulators in TMEM), cta_group::1;
+//   * 128-byte-swizzled shared-memory operands, both majors:
+//       K-major  : row r (an M or N index) holds 64 bf16 of K in 128 B; rows
+//                  at 128 B, 8-row groups at SBO = 1024 B.  The 16-B chunk j
+//                  of row r sits at chunk (j ^ (r & 7)) — the layout TMA
+//                  writes with CU_TENSOR_MAP_SWIZZLE_128B for a {64, rows}
+//                  box.  One UMMA K-step (16 bf16) advances the start address
+//                  by 32 B inside the swizzle atom.
+//       MN-major : row k (a K index) holds 64 bf16 of M (or N) in 128 B;
+//                  8-k groups at SBO = 1024 B, 64-wide MN atoms at
+//                  LBO = 64 rows · 128 B = 8192 B.  One K-step = 2 groups
+//                  = +2048 B.
+//   * TMA 2-D tile loads (cp.async.bulk.tensor) completing on an mbarrier;
+//   * cp.async 16-B copies with zero fill (the im2col gathers).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "pk_umma.cuh"
+
+namespace tc {
+
+using umma::smem_u32;
+
+// sm_100 shared-memory descriptor, SWIZZLE_128B (layout_type 2), version 1
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes,
+                                                uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::f16 with bf16 A/B, fp32 accumulate, dense
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                     // c_format = F32
+         | (1u << 7)                   // a_format = BF16
+         | (1u << 10)                  // b_format = BF16
+         | ((a_mn ? 1u : 0u) << 15)    // a_major
+         | ((b_mn ? 1u : 0u) << 16)    // b_major
+         | ((uint32_t)(N >> 3) << 17)  // n_dim
+         | ((uint32_t)(M >> 4) << 24); // m_dim
+}
+
+// byte offset of (row, 16-B chunk) in a K-major SW128 operand (64 bf16 / row)
+__device__ __forceinline__ uint32_t kmaj_sw128(int row, int chunk) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
+}
+// byte offset of (k row, 16-B chunk along MN) in an MN-major SW128 operand
+// with 64 k rows per stage: 64-wide MN atoms are 8 KB apart
+__device__ __forceinline__ uint32_t mnmaj_sw128(int k, int mn_chunk) {
+  return (uint32_t)((mn_chunk >> 3) * 8192 + (k >> 3) * 1024 + (k & 7) * 128 +
+                    (((mn_chunk & 7) ^ (k & 7)) << 4));
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+      :
+      : "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// ---- mbarrier extras ------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+// ---- TMA ------------------------------------------------------------------------
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+// 2-D tile {x (inner), y} of tensor map `m` → shared `dst`, tx bytes on `mbar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int x, int y,
+                                            uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(mbar))
+      : "memory");
+}
+
+// ---- cp.async (16 B, zero fill when !ok) ------------------------------------------
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---- TMEM loads: 32 lanes x 16 columns (32x32b.x16) ---------------------------------
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+}  // namespace tc
