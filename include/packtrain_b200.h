@@ -266,6 +266,206 @@ int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void* x, const 
                       const void* dy, void* out, int32_t ntile, int32_t splits,
                       int32_t stages, void* stream);
 
+/* ----------------------------------------------------------------------
+ * Conv pack program.  A packed conv train step is a fixed sequence of
+ * grouped kernel launches ("ops"); each op covers one layer of every member
+ * of the pack (nprob problems, one per member / input group), so a K-member
+ * pack of identical nets costs the launches of one net.  The host planner
+ * (paper_2002_02885_b200/cnn.py) owns the device buffers (HBM layout in
+ * DESIGN.md §3b) and describes every launch with the structs below; the
+ * program copies the descriptors to the device once and replays them
+ * (optionally as one CUDA graph) every step.  All tensors are NHWC with a
+ * pixel-row stride (ld*) in elements; channel counts are multiples of 8.
+ * Activations / GEMM operands are bf16, master weights, optimizer slots,
+ * BN statistics and gradients fp32.
+ * ---------------------------------------------------------------------- */
+#define PK_CNN_CONV_FPROP 0     /* implicit-GEMM conv forward (tcgen05)          */
+#define PK_CNN_CONV_DGRAD 1     /* implicit-GEMM conv data gradient (tcgen05)    */
+#define PK_CNN_CONV_WGRAD 2     /* implicit-GEMM conv weight gradient (tcgen05)  */
+#define PK_CNN_BN_STATS 3       /* batch mean / rstd over valid rows             */
+#define PK_CNN_BN_APPLY 4       /* y -> act(bn(y) [+ residual])                  */
+#define PK_CNN_BN_BWD_REDUCE 5  /* dgamma, dbeta, Σg / Σg·xhat                   */
+#define PK_CNN_BN_BWD_APPLY 6   /* dx (and the residual gradient)                */
+#define PK_CNN_DW_FPROP 7       /* depthwise conv forward                        */
+#define PK_CNN_DW_DGRAD 8
+#define PK_CNN_DW_WGRAD 9
+#define PK_CNN_MAXPOOL_FWD 10
+#define PK_CNN_MAXPOOL_BWD 11
+#define PK_CNN_AVGPOOL_FWD 12
+#define PK_CNN_AVGPOOL_BWD 13
+#define PK_CNN_XENT 14          /* softmax cross-entropy head (+ last bias grad) */
+#define PK_CNN_BIAS_ACT_BWD 15  /* g = dy·act'(out), dbias = Σ_rows g            */
+#define PK_CNN_SPLIT_REDUCE 16  /* dW = Σ_split partials (fixed order)           */
+#define PK_CNN_OPT 17           /* fused multi-member optimizer + bf16 publish   */
+#define PK_CNN_PUBLISH_T 18     /* transposed bf16 weights for DGRAD             */
+#define PK_CNN_COMMIT 19        /* per-member step counter / non-finite verdict  */
+#define PK_CNN_NUM_KINDS 20
+
+#define PK_CNN_ACT_NONE 0
+#define PK_CNN_ACT_RELU 1
+#define PK_CNN_ACT_RELU6 2
+
+/* conv geometry of the forward conv: x [n,h,w,c] * W [k][r][s][c] -> y [n,p,q,k] */
+typedef struct pk_cnn_conv {
+  const void* src;        /* FPROP/WGRAD: x (pixel stride ldx); DGRAD: dy (stride ldy) */
+  const void* dy;         /* WGRAD: dy (stride ldy) */
+  const void* wt;         /* FPROP: W16 bf16 [k][kpad]; DGRAD: Wt16 bf16 [c][kpadt] */
+  void* dst;              /* FPROP: y (bf16, or fp32 if out_f32), stride ldo;
+                             DGRAD: dx bf16 stride ldo; WGRAD: fp32 [splits][k][kpad] */
+  const int64_t* idx;     /* FPROP/WGRAD: batch image i reads source image idx[i] */
+  const float* bias;      /* FPROP: per output channel (NULL = none) */
+  int32_t* flag;          /* WGRAD (splits == 1): member's non-finite flag */
+  int64_t dseg;           /* FPROP concat-N: elements between member segments of dst */
+  int32_t n, h, w, c, k, r, s, stride, pad, p, q;
+  int32_t ldx, ldy, ldo;
+  int32_t act;            /* FPROP: PK_CNN_ACT_* after bias */
+  int32_t out_f32;        /* FPROP: dst fp32 */
+  int32_t accumulate;     /* DGRAD: dst += result */
+  int32_t splits;         /* WGRAD: pixel splits */
+  int32_t nseg;           /* FPROP concat-N: output channels per member segment (0 = one) */
+} pk_cnn_conv;
+
+/* batch norm over the `rows` valid rows of one member (BN_* kinds) */
+typedef struct pk_cnn_bn {
+  const void* x;          /* pre-norm y (bf16, stride ldx) */
+  const void* res;        /* APPLY: residual added before act (bf16, stride ldr) or NULL */
+  void* out;              /* APPLY: act(bn(x) + res) (bf16, stride ldo) */
+  const void* dout;       /* BWD: dL/d out (bf16, stride ldd) */
+  const void* fout;       /* BWD: forward out, for act' (bf16, stride ldo) */
+  void* dx;               /* BWD_APPLY: dL/dx (bf16, stride ldx2) */
+  void* dres;             /* BWD_APPLY: dL/d res = g (bf16, stride ldr) or NULL */
+  const float* gamma;
+  const float* beta;
+  float* dgamma;          /* BWD_REDUCE: gradient slab entries */
+  float* dbeta;
+  float* stats;           /* [4][c]: mean, rstd, mean(g), mean(g·xhat) */
+  float* run_mean;        /* STATS: running statistics (torch momentum rule) or NULL */
+  float* run_var;
+  float* ws;              /* partials workspace, >= 2*c*ceil(rows/PK_CNN_BN_ROWS) floats */
+  int32_t* counter;       /* zero-initialised; reset by the kernel */
+  int32_t* flag;          /* member's non-finite flag */
+  int32_t rows, c, ldx, ldo, ldr, ldd, ldx2;
+  int32_t act;            /* PK_CNN_ACT_* */
+  int32_t accumulate;     /* BWD_APPLY: dx += */
+  int32_t res_accumulate; /* BWD_APPLY: dres += */
+  int32_t use_running;    /* APPLY: normalise with running stats (eval) */
+  float eps, momentum;
+} pk_cnn_bn;
+#define PK_CNN_BN_ROWS 256
+
+/* depthwise r x s conv (groups = c), weights bf16 [r*s][c] / gradient fp32 [r*s][c] */
+typedef struct pk_cnn_dw {
+  const void* x;          /* FPROP/WGRAD input (stride ldx) */
+  const void* wt;         /* FPROP/DGRAD: W16 bf16 [r*s][c] */
+  const void* dy;         /* DGRAD/WGRAD (stride ldy) */
+  void* y;                /* FPROP output (stride ldy) / DGRAD dx (stride ldx) */
+  float* dw;              /* WGRAD gradient [r*s][c] */
+  float* ws;              /* WGRAD partials */
+  int32_t* counter;
+  int32_t* flag;
+  int32_t n, h, w, c, r, s, stride, pad, p, q, ldx, ldy;
+} pk_cnn_dw;
+#define PK_CNN_DW_PIX 256  /* output pixels per WGRAD partial */
+
+/* pooling: max (window r x s, stride, pad; argmax kept as uint8) or average */
+typedef struct pk_cnn_pool {
+  const void* x;          /* FWD input (stride ldx) */
+  void* y;                /* FWD output (stride ldy) */
+  const void* dy;         /* BWD (stride ldy) */
+  void* dx;               /* BWD (stride ldx) */
+  uint8_t* arg;           /* MAXPOOL: argmax tap per output element [n*p*q][c] */
+  int32_t n, h, w, c, r, s, stride, pad, p, q, ldx, ldy;
+  int32_t accumulate;     /* BWD: dx += */
+} pk_cnn_pool;
+
+/* softmax cross-entropy over the member's `rows` rows (mean), reference
+ * engine.py:211-230 / :252-264 */
+typedef struct pk_cnn_head {
+  const float* logits;    /* fp32 [rows][ldl] (bias already added) */
+  const int64_t* labels;  /* dataset labels */
+  const int64_t* idx;     /* batch row i has label labels[idx[i]] */
+  void* dlogits;          /* bf16 [rows][ldl] (NULL = loss only, eval) */
+  float* dbias;           /* last-layer bias gradient [classes] or NULL */
+  float* loss;            /* member's loss (mean over rows) */
+  int32_t* flag;
+  int32_t rows, classes, ldl;
+} pk_cnn_head;
+
+/* g = dy · act'(fout), written bf16; dbias = Σ_rows g */
+typedef struct pk_cnn_bias {
+  const void* dy;         /* stride ld */
+  const void* fout;       /* stride ld */
+  void* g;                /* stride ld (may alias dy) */
+  float* dbias;
+  float* ws;
+  int32_t* counter;
+  int32_t* flag;
+  int32_t rows, c, ld, act;
+} pk_cnn_bias;
+
+/* dst[i] = Σ_{j<splits} src[j*len + i] (j in order) */
+typedef struct pk_cnn_reduce {
+  const float* src;
+  float* dst;
+  int32_t* flag;
+  int64_t len;
+  int32_t splits, pad0;
+} pk_cnn_reduce;
+
+/* one contiguous parameter segment of one member for the fused optimizer */
+typedef struct pk_cnn_opt_seg {
+  float* w;               /* fp32 master */
+  const float* g;         /* gradient */
+  float* s1;              /* slot 1 (velocity / accum / adam m) or NULL */
+  float* s2;              /* slot 2 (adam v) or NULL */
+  void* w16;              /* bf16 mirror (GEMM operand) or NULL */
+  const int32_t* step;    /* member step counter (t-1) */
+  const int32_t* flag;    /* member's commit verdict (COMMIT mode 0): skip if set */
+  int64_t len;
+  int32_t kind;           /* PK_OPT_* */
+  float lr, wd;
+} pk_cnn_opt_seg;
+
+/* Wt16[ci][(r*s_+s)*kp + co] = W16[co][(r*s_+s)*cp + ci] */
+typedef struct pk_cnn_tpose {
+  const void* src;
+  void* dst;
+  int32_t k, c, taps, kpad, kpadt, pad0;
+} pk_cnn_tpose;
+
+/* per-member commit (op cfg0 = mode).  mode 0, before PK_CNN_OPT: verdict =
+ * OR of the flags of this and every earlier problem (the reference's update
+ * loop stops at the first non-finite member, packing.py:250-253); mode 1,
+ * after it: if (!verdict) ++step; verdict |= (flag != 0) << 1; flag = 0. */
+typedef struct pk_cnn_commit {
+  int32_t* step;
+  int32_t* flag;
+  int32_t* verdict;
+} pk_cnn_commit;
+
+typedef struct pk_cnn_op {
+  int32_t kind;           /* PK_CNN_* */
+  int32_t nprob;
+  int32_t cfg0;           /* CONV: GEMM N tile */
+  int32_t cfg1;           /* CONV: pipeline stages */
+  const void* probs;      /* nprob structs of the kind's type (host, copied) */
+} pk_cnn_op;
+
+typedef struct pk_cnn_prog pk_cnn_prog;
+
+/* Build a program on `device` from nops op descriptors (host memory, copied). */
+int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t device, pk_cnn_prog** out);
+void pk_cnn_prog_destroy(pk_cnn_prog* p);
+/* Enqueue the whole program on `stream`; use_graph != 0 captures it once into
+ * a CUDA graph and replays that graph on later calls. */
+int pk_cnn_prog_run(pk_cnn_prog* p, void* stream, int32_t use_graph);
+/* Run op by op, bracketing each op with CUDA events; op_ms[i] = duration. */
+int pk_cnn_prog_profile(pk_cnn_prog* p, void* stream, float* op_ms);
+/* kernel launches one run enqueues */
+int32_t pk_cnn_prog_launches(const pk_cnn_prog* p);
+/* last error of the conv pack path on this thread */
+const char* pk_cnn_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,8 @@ EXPORTS = (
     "pk_pack_step_wait", "pk_pack_eval", "pk_pack_profile_step", "pk_pack_trace",
     "pk_pack_launches_per_step",
     "pk_conv_gemm_test",
+    "pk_cnn_prog_create", "pk_cnn_prog_destroy", "pk_cnn_prog_run", "pk_cnn_prog_profile",
+    "pk_cnn_prog_launches", "pk_cnn_last_error",
 )
 
 
@@ -82,6 +84,100 @@ PK_RUN_MAX_STEPS, PK_RUN_NO_MEMBER, PK_RUN_NEED_PERM, PK_RUN_LABEL_BOUNDS, PK_RU
 class ConvGeom(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("n", "h", "w", "c", "k", "r", "s", "stride", "pad",
                                          "p", "q")]
+
+
+# ---- conv pack program (packtrain_b200.h pk_cnn_*) ----------------------------------
+CNN_KINDS = ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD", "BN_STATS", "BN_APPLY", "BN_BWD_REDUCE",
+             "BN_BWD_APPLY", "DW_FPROP", "DW_DGRAD", "DW_WGRAD", "MAXPOOL_FWD", "MAXPOOL_BWD",
+             "AVGPOOL_FWD", "AVGPOOL_BWD", "XENT", "BIAS_ACT_BWD", "SPLIT_REDUCE", "OPT",
+             "PUBLISH_T", "COMMIT")
+CNN = {k: i for i, k in enumerate(CNN_KINDS)}
+CNN_ACT = {"none": 0, "relu": 1, "relu6": 2}
+PK_CNN_BN_ROWS = 256
+PK_CNN_DW_PIX = 256
+_vp, _i32, _i64, _f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+
+
+def _ints(*names):
+    return [(n, _i32) for n in names]
+
+
+class CnnConv(C.Structure):
+    _fields_ = ([("src", _vp), ("dy", _vp), ("wt", _vp), ("dst", _vp), ("idx", _vp),
+                 ("bias", _vp), ("flag", _vp), ("dseg", _i64)]
+                + _ints("n", "h", "w", "c", "k", "r", "s", "stride", "pad", "p", "q",
+                        "ldx", "ldy", "ldo", "act", "out_f32", "accumulate", "splits", "nseg"))
+
+
+class CnnBn(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("x", "res", "out", "dout", "fout", "dx", "dres", "gamma",
+                                    "beta", "dgamma", "dbeta", "stats", "run_mean", "run_var",
+                                    "ws", "counter", "flag")]
+                + _ints("rows", "c", "ldx", "ldo", "ldr", "ldd", "ldx2", "act", "accumulate",
+                        "res_accumulate", "use_running")
+                + [("eps", _f32), ("momentum", _f32)])
+
+
+class CnnDw(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("x", "wt", "dy", "y", "dw", "ws", "counter", "flag")]
+                + _ints("n", "h", "w", "c", "r", "s", "stride", "pad", "p", "q", "ldx", "ldy"))
+
+
+class CnnPool(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("x", "y", "dy", "dx", "arg")]
+                + _ints("n", "h", "w", "c", "r", "s", "stride", "pad", "p", "q", "ldx", "ldy",
+                        "accumulate"))
+
+
+class CnnHead(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("logits", "labels", "idx", "dlogits", "dbias", "loss",
+                                    "flag")]
+                + _ints("rows", "classes", "ldl"))
+
+
+class CnnBias(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("dy", "fout", "g", "dbias", "ws", "counter", "flag")]
+                + _ints("rows", "c", "ld", "act"))
+
+
+class CnnReduce(C.Structure):
+    _fields_ = [("src", _vp), ("dst", _vp), ("flag", _vp), ("len", _i64), ("splits", _i32),
+                ("pad0", _i32)]
+
+
+class CnnOptSeg(C.Structure):
+    _fields_ = ([(n, _vp) for n in ("w", "g", "s1", "s2", "w16", "step", "flag")]
+                + [("len", _i64), ("kind", _i32), ("lr", _f32), ("wd", _f32)])
+
+
+class CnnTpose(C.Structure):
+    _fields_ = [("src", _vp), ("dst", _vp)] + _ints("k", "c", "taps", "kpad", "kpadt", "pad0")
+
+
+class CnnCommit(C.Structure):
+    _fields_ = [("step", _vp), ("flag", _vp), ("verdict", _vp)]
+
+
+class CnnOp(C.Structure):
+    _fields_ = [("kind", _i32), ("nprob", _i32), ("cfg0", _i32), ("cfg1", _i32),
+                ("probs", _vp)]
+
+
+CNN_STRUCT = {}
+for _k in ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD"):
+    CNN_STRUCT[CNN[_k]] = CnnConv
+for _k in ("BN_STATS", "BN_APPLY", "BN_BWD_REDUCE", "BN_BWD_APPLY"):
+    CNN_STRUCT[CNN[_k]] = CnnBn
+for _k in ("DW_FPROP", "DW_DGRAD", "DW_WGRAD"):
+    CNN_STRUCT[CNN[_k]] = CnnDw
+for _k in ("MAXPOOL_FWD", "MAXPOOL_BWD", "AVGPOOL_FWD", "AVGPOOL_BWD"):
+    CNN_STRUCT[CNN[_k]] = CnnPool
+CNN_STRUCT[CNN["XENT"]] = CnnHead
+CNN_STRUCT[CNN["BIAS_ACT_BWD"]] = CnnBias
+CNN_STRUCT[CNN["SPLIT_REDUCE"]] = CnnReduce
+CNN_STRUCT[CNN["OPT"]] = CnnOptSeg
+CNN_STRUCT[CNN["PUBLISH_T"]] = CnnTpose
+CNN_STRUCT[CNN["COMMIT"]] = CnnCommit
 
 
 class PKError(RuntimeError):
@@ -142,6 +238,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pk_pack_trace": (i64, [vp, vp, i64]),
         "pk_pack_launches_per_step": (i32, [vp]),
         "pk_conv_gemm_test": (C.c_int, [i32, P(ConvGeom), vp, vp, vp, vp, i32, i32, i32, vp]),
+        "pk_cnn_prog_create": (C.c_int, [P(CnnOp), i32, i32, P(vp)]),
+        "pk_cnn_prog_destroy": (None, [vp]),
+        "pk_cnn_prog_run": (C.c_int, [vp, vp, i32]),
+        "pk_cnn_prog_profile": (C.c_int, [vp, vp, P(C.c_float)]),
+        "pk_cnn_prog_launches": (i32, [vp]),
+        "pk_cnn_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -50,7 +50,7 @@ inline int rup(int a, int b) { return (a + b - 1) / b * b; }
 
 // fill tile counts / prefix and launch one grouped implicit-GEMM conv
 template <int MODE>
-cudaError_t launch_gemm(cg::Launch& L, const CUtensorMap& tm, cudaStream_t st) {
+cudaError_t launch_gemm(cg::Launch& L, cudaStream_t st) {
   static bool attr_set = false;
   int tiles = 0;
   for (int i = 0; i < L.nprob; ++i) {
@@ -70,11 +70,468 @@ cudaError_t launch_gemm(cg::Launch& L, const CUtensorMap& tm, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  cg::k_conv_gemm<MODE><<<tiles, cg::kThreads, smem, st>>>(L, tm);
+  cg::k_conv_gemm<MODE><<<tiles, cg::kThreads, smem, st>>>(L);
   return cudaGetLastError();
 }
 
+
+thread_local std::string g_err;
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+size_t prob_size(int kind) {
+  switch (kind) {
+    case PK_CNN_CONV_FPROP:
+    case PK_CNN_CONV_DGRAD:
+    case PK_CNN_CONV_WGRAD: return sizeof(pk_cnn_conv);
+    case PK_CNN_BN_STATS:
+    case PK_CNN_BN_APPLY:
+    case PK_CNN_BN_BWD_REDUCE:
+    case PK_CNN_BN_BWD_APPLY: return sizeof(pk_cnn_bn);
+    case PK_CNN_DW_FPROP:
+    case PK_CNN_DW_DGRAD:
+    case PK_CNN_DW_WGRAD: return sizeof(pk_cnn_dw);
+    case PK_CNN_MAXPOOL_FWD:
+    case PK_CNN_MAXPOOL_BWD:
+    case PK_CNN_AVGPOOL_FWD:
+    case PK_CNN_AVGPOOL_BWD: return sizeof(pk_cnn_pool);
+    case PK_CNN_XENT: return sizeof(pk_cnn_head);
+    case PK_CNN_BIAS_ACT_BWD: return sizeof(pk_cnn_bias);
+    case PK_CNN_SPLIT_REDUCE: return sizeof(pk_cnn_reduce);
+    case PK_CNN_OPT: return sizeof(pk_cnn_opt_seg);
+    case PK_CNN_PUBLISH_T: return sizeof(pk_cnn_tpose);
+    case PK_CNN_COMMIT: return sizeof(pk_cnn_commit);
+  }
+  return 0;
+}
+
+long long items(long long rows, int c) { return rows * (c / 8); }
+int blocks_of(long long n) { return (int)((n + cnn::kBlock - 1) / cnn::kBlock); }
+
+// blocks one problem of a non-conv kind needs
+int prob_blocks(int kind, const void* pr) {
+  switch (kind) {
+    case PK_CNN_BN_STATS:
+    case PK_CNN_BN_BWD_REDUCE: {
+      const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
+      return cdiv(P.rows, PK_CNN_BN_ROWS);
+    }
+    case PK_CNN_BN_APPLY:
+    case PK_CNN_BN_BWD_APPLY: {
+      const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
+      return blocks_of(items(P.rows, P.c));
+    }
+    case PK_CNN_DW_FPROP: {
+      const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
+      return blocks_of(items((long long)P.n * P.p * P.q, P.c));
+    }
+    case PK_CNN_DW_DGRAD: {
+      const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
+      return blocks_of(items((long long)P.n * P.h * P.w, P.c));
+    }
+    case PK_CNN_DW_WGRAD: {
+      const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
+      return cdiv((long long)P.n * P.p * P.q, PK_CNN_DW_PIX);
+    }
+    case PK_CNN_MAXPOOL_FWD:
+    case PK_CNN_AVGPOOL_FWD: {
+      const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
+      return blocks_of(items((long long)P.n * P.p * P.q, P.c));
+    }
+    case PK_CNN_MAXPOOL_BWD:
+    case PK_CNN_AVGPOOL_BWD: {
+      const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
+      return blocks_of(items((long long)P.n * P.h * P.w, P.c));
+    }
+    case PK_CNN_BIAS_ACT_BWD: {
+      const pk_cnn_bias& P = *static_cast<const pk_cnn_bias*>(pr);
+      return cdiv(P.rows, PK_CNN_BN_ROWS);
+    }
+    case PK_CNN_SPLIT_REDUCE: {
+      const pk_cnn_reduce& P = *static_cast<const pk_cnn_reduce*>(pr);
+      return blocks_of((P.len + 3) / 4);
+    }
+    case PK_CNN_OPT: {
+      const pk_cnn_opt_seg& P = *static_cast<const pk_cnn_opt_seg*>(pr);
+      return (int)((P.len + cnn::kOptChunk - 1) / cnn::kOptChunk);
+    }
+    case PK_CNN_PUBLISH_T: {
+      const pk_cnn_tpose& P = *static_cast<const pk_cnn_tpose*>(pr);
+      return P.taps * cdiv(P.k, 32) * cdiv(P.c, 32);
+    }
+  }
+  return 0;
+}
+
+std::string check_prob(int kind, const void* pr) {
+  auto c8 = [](int c) { return c > 0 && c % 8 == 0 && c <= 2048; };
+  switch (kind) {
+    case PK_CNN_BN_STATS:
+    case PK_CNN_BN_APPLY:
+    case PK_CNN_BN_BWD_REDUCE:
+    case PK_CNN_BN_BWD_APPLY: {
+      const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
+      if (!c8(P.c) || P.rows <= 0) return "bn: channels must be a multiple of 8 in [8, 2048]";
+      break;
+    }
+    case PK_CNN_DW_FPROP:
+    case PK_CNN_DW_DGRAD:
+    case PK_CNN_DW_WGRAD: {
+      const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
+      if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
+      break;
+    }
+    case PK_CNN_MAXPOOL_FWD:
+    case PK_CNN_MAXPOOL_BWD:
+    case PK_CNN_AVGPOOL_FWD:
+    case PK_CNN_AVGPOOL_BWD: {
+      const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
+      if (P.c % 8 || P.r * P.s > 255 || P.stride < 1) return "pool: c % 8, window <= 255";
+      break;
+    }
+    case PK_CNN_BIAS_ACT_BWD: {
+      const pk_cnn_bias& P = *static_cast<const pk_cnn_bias*>(pr);
+      if (!c8(P.c)) return "bias: channels must be a multiple of 8 in [8, 2048]";
+      break;
+    }
+    case PK_CNN_XENT: {
+      const pk_cnn_head& P = *static_cast<const pk_cnn_head*>(pr);
+      if (P.rows <= 0 || P.rows > 4096 || P.classes <= 0 || P.ldl < P.classes)
+        return "xent: 0 < rows <= 4096, classes <= ldl";
+      break;
+    }
+    case PK_CNN_SPLIT_REDUCE: {
+      const pk_cnn_reduce& P = *static_cast<const pk_cnn_reduce*>(pr);
+      if (P.len % 4 || P.splits < 1) return "split_reduce: len % 4";
+      break;
+    }
+  }
+  return std::string();
+}
+
+struct OpRec {
+  int kind = 0, nprob = 0, nblocks = 0;
+  int ntile = 0, stages = 0;
+  size_t probs_off = 0, blk_off = 0;  // offsets into the device descriptor block
+  std::vector<cg::Launch> conv;       // conv ops: launches of <= kMaxProblems problems
+};
+
 }  // namespace
+
+struct pk_cnn_prog {
+  int device = 0;
+  std::vector<OpRec> ops;
+  uint8_t* dmem = nullptr;
+  int launches = 0;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;
+};
+
+namespace {
+
+int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stages,
+                     std::vector<cg::Launch>& out) {
+  for (int i0 = 0; i0 < n; i0 += cg::kMaxProblems) {
+    cg::Launch L;
+    memset(&L, 0, sizeof(L));
+    L.nprob = std::min(cg::kMaxProblems, n - i0);
+    L.ntile = ntile;
+    L.stages = stages;
+    int tiles = 0;
+    for (int j = 0; j < L.nprob; ++j) {
+      const pk_cnn_conv& g = pr[i0 + j];
+      cg::Problem& p = L.p[j];
+      if (g.c % 8 || g.k % 8 || (g.stride != 1 && g.stride != 2))
+        return fail(PK_ERR_ARG, "conv: c, k multiples of 8; stride 1 or 2");
+      p.R = g.r; p.S = g.s; p.stride = g.stride; p.pad = g.pad;
+      p.dst = g.dst;
+      if (kind == PK_CNN_CONV_FPROP) {
+        const int kpad = rup(g.r * g.s * g.c, 64);
+        p.src = static_cast<const __nv_bfloat16*>(g.src);
+        p.idx = reinterpret_cast<const long long*>(g.idx);
+        p.bias = g.bias; p.act = g.act; p.out_f32 = g.out_f32;
+        p.nseg = g.nseg; p.dseg = g.dseg;
+        p.M = g.n * g.p * g.q; p.N = g.k; p.K = g.r * g.s * g.c;
+        p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
+        p.OH = g.p; p.OW = g.q; p.dld = g.ldo;
+        if (!make_map_2d(&L.tm[j], g.wt, g.k, kpad, kpad, ntile))
+          return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (FPROP weights)");
+        p.splits = 1;
+      } else if (kind == PK_CNN_CONV_DGRAD) {
+        const int kpadt = rup(g.r * g.s * g.k, 64);
+        p.src = static_cast<const __nv_bfloat16*>(g.src);
+        p.accumulate = g.accumulate;
+        p.M = g.n * g.h * g.w; p.N = g.c; p.K = g.r * g.s * g.k;
+        p.SH = g.p; p.SW = g.q; p.SC = g.k; p.sld = g.ldy;
+        p.OH = g.h; p.OW = g.w; p.dld = g.ldo;
+        if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile))
+          return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (DGRAD weights)");
+        p.splits = 1;
+      } else {
+        if (ntile % 64) return fail(PK_ERR_ARG, "conv: WGRAD N tile must be a multiple of 64");
+        const int kpad = rup(g.r * g.s * g.c, 64);
+        const int pix = g.n * g.p * g.q;
+        p.src = static_cast<const __nv_bfloat16*>(g.src);
+        p.src2 = static_cast<const __nv_bfloat16*>(g.dy);
+        p.idx = reinterpret_cast<const long long*>(g.idx);
+        p.M = g.k; p.N = g.r * g.s * g.c; p.K = pix;
+        const int sp = std::max(1, g.splits);
+        p.kper = rup(cdiv(pix, sp), 64);
+        p.splits = cdiv(pix, p.kper);
+        if (p.splits != sp) return fail(PK_ERR_ARG, "conv: WGRAD splits leave an empty split");
+        p.flag = p.splits == 1 ? g.flag : nullptr;
+        p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
+        p.OH = g.p; p.OW = g.q; p.ald = g.ldy;
+        p.dld = kpad;
+        p.split_stride = (long long)g.k * kpad;
+      }
+      p.tiles_m = cdiv(p.M, cg::BM);
+      p.tiles_n = cdiv(p.N, ntile);
+      p.tile0 = tiles;
+      tiles += p.tiles_m * p.tiles_n * p.splits;
+    }
+    L.total_tiles = tiles;
+    out.push_back(L);
+  }
+  return PK_OK;
+}
+
+template <int MODE>
+cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
+  static bool attr_set = false;
+  if (L.total_tiles == 0) return cudaSuccess;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cg::k_conv_gemm<MODE><<<L.total_tiles, cg::kThreads, cg::smem_bytes(L.ntile, L.stages), st>>>(L);
+  return cudaGetLastError();
+}
+
+template <class P>
+const P* dp(const pk_cnn_prog* g, const OpRec& o) {
+  return reinterpret_cast<const P*>(g->dmem + o.probs_off);
+}
+const int* db(const pk_cnn_prog* g, const OpRec& o) {
+  return reinterpret_cast<const int*>(g->dmem + o.blk_off);
+}
+
+cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
+  using namespace cnn;
+  const int nb = o.nblocks, np = o.nprob;
+  switch (o.kind) {
+    case PK_CNN_CONV_FPROP:
+      for (auto& L : o.conv) {
+        cudaError_t e = launch_conv<cg::FPROP>(L, st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    case PK_CNN_CONV_DGRAD:
+      for (auto& L : o.conv) {
+        cudaError_t e = launch_conv<cg::DGRAD>(L, st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    case PK_CNN_CONV_WGRAD:
+      for (auto& L : o.conv) {
+        cudaError_t e = launch_conv<cg::WGRAD>(L, st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    case PK_CNN_BN_STATS: k_bn_stats<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np); break;
+    case PK_CNN_BN_APPLY: k_bn_apply<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np); break;
+    case PK_CNN_BN_BWD_REDUCE:
+      k_bn_bwd_reduce<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_BN_BWD_APPLY:
+      k_bn_bwd_apply<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_DW_FPROP: k_dw_fprop<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
+    case PK_CNN_DW_DGRAD: k_dw_dgrad<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
+    case PK_CNN_DW_WGRAD: k_dw_wgrad<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
+    case PK_CNN_MAXPOOL_FWD:
+      k_maxpool_fwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_MAXPOOL_BWD:
+      k_maxpool_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_AVGPOOL_FWD:
+      k_avgpool_fwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_AVGPOOL_BWD:
+      k_avgpool_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_XENT: k_xent<<<np, kBlock, o.ntile, st>>>(dp<pk_cnn_head>(g, o), np); break;
+    case PK_CNN_BIAS_ACT_BWD:
+      k_bias_act_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bias>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_SPLIT_REDUCE:
+      k_split_reduce<<<nb, kBlock, 0, st>>>(dp<pk_cnn_reduce>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_OPT: k_opt<<<nb, kBlock, 0, st>>>(dp<pk_cnn_opt_seg>(g, o), db(g, o), np); break;
+    case PK_CNN_PUBLISH_T:
+      k_publish_t<<<nb, kBlock, 0, st>>>(dp<pk_cnn_tpose>(g, o), db(g, o), np);
+      break;
+    case PK_CNN_COMMIT:
+      k_commit<<<cdiv(np, 128), 128, 0, st>>>(dp<pk_cnn_commit>(g, o), np, o.ntile);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+int run_all(pk_cnn_prog* g, cudaStream_t st) {
+  for (size_t i = 0; i < g->ops.size(); ++i) {
+    cudaError_t e = run_op(g, g->ops[i], st);
+    if (e != cudaSuccess)
+      return fail(PK_ERR_CUDA, "op " + std::to_string(i) + " (kind " +
+                                   std::to_string(g->ops[i].kind) + "): " + cudaGetErrorString(e));
+  }
+  return PK_OK;
+}
+
+}  // namespace
+
+extern "C" const char* pk_cnn_last_error(void) { return g_err.c_str(); }
+
+extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t device,
+                                  pk_cnn_prog** out) {
+  if (!ops || nops <= 0 || !out) return fail(PK_ERR_ARG, "pk_cnn_prog_create: no ops");
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return fail(PK_ERR_CUDA, "cudaSetDevice failed");
+  auto* g = new pk_cnn_prog();
+  g->device = device;
+  std::vector<uint8_t> host;
+  auto align = [&](size_t a) { host.resize((host.size() + a - 1) / a * a); };
+  for (int i = 0; i < nops; ++i) {
+    const pk_cnn_op& op = ops[i];
+    OpRec r;
+    r.kind = op.kind;
+    r.nprob = op.nprob;
+    const size_t ps = prob_size(op.kind);
+    if (!ps || op.nprob <= 0 || !op.probs) {
+      delete g;
+      return fail(PK_ERR_ARG, "op " + std::to_string(i) + ": bad kind or no problems");
+    }
+    if (op.kind <= PK_CNN_CONV_WGRAD) {
+      r.ntile = op.cfg0;
+      r.stages = op.cfg1;
+      if (r.ntile < 16 || r.ntile > 256 || r.ntile % 16 || r.stages < 2 ||
+          cg::smem_bytes(r.ntile, r.stages) > 227 * 1024) {
+        delete g;
+        return fail(PK_ERR_ARG, "op " + std::to_string(i) + ": bad conv tile / stages");
+      }
+      int rc = conv_to_launches(op.kind, static_cast<const pk_cnn_conv*>(op.probs), op.nprob,
+                                r.ntile, r.stages, r.conv);
+      if (rc != PK_OK) {
+        delete g;
+        return rc;
+      }
+      g->launches += (int)r.conv.size();
+      g->ops.push_back(std::move(r));
+      continue;
+    }
+    std::vector<int> blk(op.nprob + 1, 0);
+    const uint8_t* src = static_cast<const uint8_t*>(op.probs);
+    for (int j = 0; j < op.nprob; ++j) {
+      std::string why = check_prob(op.kind, src + j * ps);
+      if (!why.empty()) {
+        delete g;
+        return fail(PK_ERR_ARG, "op " + std::to_string(i) + ": " + why);
+      }
+      blk[j + 1] = blk[j] + prob_blocks(op.kind, src + j * ps);
+    }
+    r.nblocks = blk[op.nprob];
+    if (op.kind == PK_CNN_COMMIT) r.ntile = op.cfg0;  // mode
+    if (op.kind == PK_CNN_XENT) {
+      int mx = 0;
+      for (int j = 0; j < op.nprob; ++j)
+        mx = std::max(mx, reinterpret_cast<const pk_cnn_head*>(src)[j].rows);
+      r.ntile = mx * 16;  // dynamic smem bytes
+    }
+    align(64);
+    r.probs_off = host.size();
+    host.insert(host.end(), src, src + ps * op.nprob);
+    align(16);
+    r.blk_off = host.size();
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(blk.data());
+    host.insert(host.end(), b, b + sizeof(int) * blk.size());
+    g->launches += 1;
+    g->ops.push_back(std::move(r));
+  }
+  if (!host.empty()) {
+    if (cudaMalloc(&g->dmem, host.size()) != cudaSuccess) {
+      delete g;
+      return fail(PK_ERR_OOM, "pk_cnn_prog_create: descriptor allocation failed");
+    }
+    if (cudaMemcpy(g->dmem, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(g->dmem);
+      delete g;
+      return fail(PK_ERR_CUDA, "pk_cnn_prog_create: descriptor upload failed");
+    }
+  }
+  *out = g;
+  return PK_OK;
+}
+
+extern "C" void pk_cnn_prog_destroy(pk_cnn_prog* g) {
+  if (!g) return;
+  if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  if (g->dmem) cudaFree(g->dmem);
+  delete g;
+}
+
+extern "C" int32_t pk_cnn_prog_launches(const pk_cnn_prog* g) { return g ? g->launches : 0; }
+
+extern "C" int pk_cnn_prog_run(pk_cnn_prog* g, void* stream, int32_t use_graph) {
+  if (!g) return fail(PK_ERR_ARG, "pk_cnn_prog_run: null program");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!use_graph) return run_all(g, st);
+  if (!g->gexec) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return fail(PK_ERR_CUDA, "pk_cnn_prog_run: cannot capture on this stream (legacy default "
+                               "stream?)");
+    int rc = run_all(g, st);
+    cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (rc != PK_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&g->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      g->gexec = nullptr;
+      return fail(PK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+  }
+  cudaError_t e = cudaGraphLaunch(g->gexec, st);
+  return e == cudaSuccess ? PK_OK : fail(PK_ERR_CUDA, cudaGetErrorString(e));
+}
+
+extern "C" int pk_cnn_prog_profile(pk_cnn_prog* g, void* stream, float* op_ms) {
+  if (!g || !op_ms) return fail(PK_ERR_ARG, "pk_cnn_prog_profile: null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t n = g->ops.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) cudaEventCreate(&e);
+  int rc = PK_OK;
+  cudaEventRecord(ev[0], st);
+  for (size_t i = 0; i < n && rc == PK_OK; ++i) {
+    cudaError_t e = run_op(g, g->ops[i], st);
+    if (e != cudaSuccess) rc = fail(PK_ERR_CUDA, cudaGetErrorString(e));
+    cudaEventRecord(ev[i + 1], st);
+  }
+  if (cudaEventSynchronize(ev[n]) != cudaSuccess && rc == PK_OK)
+    rc = fail(PK_ERR_CUDA, "pk_cnn_prog_profile: synchronize failed");
+  for (size_t i = 0; i < n && rc == PK_OK; ++i) cudaEventElapsedTime(&op_ms[i], ev[i], ev[i + 1]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
 
 extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void* x,
                                  const void* w, const void* dy, void* out, int32_t ntile,
@@ -83,7 +540,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
       stages > 6 || g->c % 8 || g->k % 8 || (g->stride != 1 && g->stride != 2))
     return PK_ERR_ARG;
   if (mode == 2 && ntile % 64) return PK_ERR_ARG;
-  cg::Launch L;
+  static cg::Launch L;
   memset(&L, 0, sizeof(L));
   L.nprob = 1;
   L.ntile = ntile;
@@ -93,8 +550,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
   p.S = g->s;
   p.stride = g->stride;
   p.pad = g->pad;
-  CUtensorMap tm;
-  memset(&tm, 0, sizeof(tm));
+  CUtensorMap& tm = L.tm[0];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (mode == 0) {
@@ -108,7 +564,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
     p.OH = g->p; p.OW = g->q;
     p.dld = g->k;
     if (!make_map_2d(&tm, w, g->k, kpad, kpad, ntile)) return PK_ERR_CUDA;
-    e = launch_gemm<cg::FPROP>(L, tm, st);
+    e = launch_gemm<cg::FPROP>(L, st);
   } else if (mode == 1) {
     const int kpad = rup(g->r * g->s * g->k, 64);
     p.src = static_cast<const __nv_bfloat16*>(dy);
@@ -120,7 +576,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
     p.OH = g->h; p.OW = g->w;
     p.dld = g->c;
     if (!make_map_2d(&tm, w, g->c, kpad, kpad, ntile)) return PK_ERR_CUDA;
-    e = launch_gemm<cg::DGRAD>(L, tm, st);
+    e = launch_gemm<cg::DGRAD>(L, st);
   } else {
     const int kpad = rup(g->r * g->s * g->c, 64);
     const int pix = g->n * g->p * g->q;
@@ -138,7 +594,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
     p.ald = g->k;
     p.dld = kpad;
     p.split_stride = (long long)g->k * kpad;
-    e = launch_gemm<cg::WGRAD>(L, tm, st);
+    e = launch_gemm<cg::WGRAD>(L, st);
   }
   return e == cudaSuccess ? PK_OK : PK_ERR_CUDA;
 }

@@ -1,2 +1,825 @@
-// pk_cnn_ops.cuh — HBM-bound kernels of the conv pack path (filled in below).
+// pk_cnn_ops.cuh — HBM-bound kernels of the conv pack path.
+//
+// Every kernel is grouped: one launch covers one layer of all members of the
+// pack.  Problem descriptors (packtrain_b200.h pk_cnn_*) live in device memory;
+// blk0[i] is the first block of problem i (prefix over problems, blk0[nprob] =
+// grid size), so a block finds its problem by binary search and never mixes
+// two members.  Tensors are NHWC bf16 with C a multiple of 8: a thread moves
+// one 16-byte vector of 8 channels of one pixel row ("item").
+//
+// Determinism / K-invariance: every reduction (BN statistics, BN backward,
+// bias and depthwise weight gradients, the softmax head) sums a fixed row
+// partition of the member's own rows in a fixed order: per-block fp32 partial
+// sums over PK_CNN_BN_ROWS rows → workspace → the last block to finish (atomic
+// ticket) adds the partials in block order in fp64.  Results depend only on
+// the member's shape, never on which members share the launch, so packed ==
+// standalone bit for bit.
 #pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "packtrain_b200.h"
+
+namespace cnn {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ int find_prob(const int* blk0, int nprob, int b) {
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(blk0 + mid) <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void ld8(const void* p, float (&v)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void st8(void* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void ld8f(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ const uint8_t* bptr(const void* base, long long row, int ld, int ch) {
+  return static_cast<const uint8_t*>(base) + (row * ld + ch) * 2;
+}
+__device__ __forceinline__ uint8_t* bptr(void* base, long long row, int ld, int ch) {
+  return static_cast<uint8_t*>(base) + (row * ld + ch) * 2;
+}
+
+__device__ __forceinline__ float act_fwd(float x, int act) {
+  if (act == PK_CNN_ACT_RELU) return fmaxf(x, 0.f);
+  if (act == PK_CNN_ACT_RELU6) return fminf(fmaxf(x, 0.f), 6.f);
+  return x;
+}
+// derivative of the activation, from its OUTPUT (relu: out > 0 ⇔ in > 0;
+// relu6: 0 < out < 6 ⇔ 0 < in < 6 — torch's hardtanh_backward rule)
+__device__ __forceinline__ float act_bwd(float out, int act) {
+  if (act == PK_CNN_ACT_RELU) return out > 0.f ? 1.f : 0.f;
+  if (act == PK_CNN_ACT_RELU6) return (out > 0.f && out < 6.f) ? 1.f : 0.f;
+  return 1.f;
+}
+
+// last-block ticket: true in exactly one block, after all blocks' partials are visible
+__device__ __forceinline__ bool last_block(int* counter, int nblk) {
+  __shared__ int s_last;
+  __threadfence();  // every thread's partial-sum stores before the block's ticket
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(counter, 1);
+    s_last = (prev == nblk - 1);
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+// ------------------------------------------------------------------------------
+// Column (channel) partial sums of up to two per-element quantities over one
+// PK_CNN_BN_ROWS-row block.  F(row, ch0, a[8], b[8]) fills the two values of
+// the 8 channels ch0.. of `row`.  Writes ws[blk][2][c].
+// ------------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ void col_partials(int rows, int c, int blk, float* ws, F f) {
+  __shared__ float sh[2][2048];
+  const int cgs = c >> 3;
+  const int nr = kBlock / cgs;  // row lanes (cgs <= 256)
+  const int t = threadIdx.x;
+  const int rl = t / cgs, j = t - rl * cgs;
+  float s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
+  const int r0 = blk * PK_CNN_BN_ROWS, r1 = min(rows, r0 + PK_CNN_BN_ROWS);
+  if (rl < nr) {
+    for (int r = r0 + rl; r < r1; r += nr) {
+      float a[8], b[8];
+      f(r, 8 * j, a, b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        s1[e] += a[e];
+        s2[e] += b[e];
+      }
+    }
+  }
+  // fixed-order combine over the row lanes, 2048/c lanes per pass; thread t
+  // owns channels t, t+256, ... (c <= 2048)
+  const int lanes_per_pass = 2048 / c;
+  float acc1[8], acc2[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc1[q] = acc2[q] = 0.f;
+  for (int base = 0; base < nr; base += lanes_per_pass) {
+    __syncthreads();
+    if (rl < nr && rl >= base && rl < base + lanes_per_pass) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        sh[0][(rl - base) * c + 8 * j + e] = s1[e];
+        sh[1][(rl - base) * c + 8 * j + e] = s2[e];
+      }
+    }
+    __syncthreads();
+    const int nl = min(lanes_per_pass, nr - base);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ch = q * kBlock + t;
+      if (ch < c)
+        for (int l = 0; l < nl; ++l) {
+          acc1[q] += sh[0][l * c + ch];
+          acc2[q] += sh[1][l * c + ch];
+        }
+    }
+  }
+  float* out1 = ws + (long long)blk * 2 * c;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int ch = q * kBlock + t;
+    if (ch < c) {
+      out1[ch] = acc1[q];
+      out1[c + ch] = acc2[q];
+    }
+  }
+}
+
+// ============================== batch norm =====================================
+__global__ void __launch_bounds__(kBlock) k_bn_stats(const pk_cnn_bn* probs, const int* blk0,
+                                                     int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_bn& P = probs[pi];
+  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+    ld8(bptr(P.x, r, P.ldx, ch), a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) b[e] = a[e] * a[e];
+  });
+  if (!last_block(P.counter, nblk)) return;
+  for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+      s1 += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
+      s2 += __ldcg(P.ws + (long long)b * 2 * P.c + P.c + ch);
+    }
+    const double mean = s1 / P.rows;
+    const double var = fmax(s2 / P.rows - mean * mean, 0.0);
+    P.stats[ch] = (float)mean;
+    P.stats[P.c + ch] = (float)(1.0 / sqrt(var + (double)P.eps));
+    if (P.run_mean) {
+      const double unb = P.rows > 1 ? var * P.rows / (P.rows - 1) : var;
+      P.run_mean[ch] = (float)((1.0 - P.momentum) * P.run_mean[ch] + P.momentum * mean);
+      P.run_var[ch] = (float)((1.0 - P.momentum) * P.run_var[ch] + P.momentum * unb);
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0;
+}
+
+__device__ __forceinline__ void bn_coef(const pk_cnn_bn& P, int ch, float (&mean)[8],
+                                        float (&rs)[8]) {
+  if (P.use_running) {
+    float v[8];
+    ld8f(P.run_mean + ch, mean);
+    ld8f(P.run_var + ch, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) rs[e] = (float)(1.0 / sqrt((double)v[e] + (double)P.eps));
+  } else {
+    ld8f(P.stats + ch, mean);
+    ld8f(P.stats + P.c + ch, rs);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_bn_apply(const pk_cnn_bn* probs, const int* blk0,
+                                                     int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_bn& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  if (item >= (long long)P.rows * cgs) return;
+  const long long r = item / cgs;
+  const int ch = 8 * (int)(item - r * cgs);
+  float x[8], mean[8], rs[8], g[8], b[8];
+  ld8(bptr(P.x, r, P.ldx, ch), x);
+  bn_coef(P, ch, mean, rs);
+  ld8f(P.gamma + ch, g);
+  ld8f(P.beta + ch, b);
+  float res[8];
+  if (P.res) ld8(bptr(P.res, r, P.ldr, ch), res);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float y = (x[e] - mean[e]) * rs[e] * g[e] + b[e];
+    if (P.res) y += res[e];
+    x[e] = act_fwd(y, P.act);
+  }
+  st8(bptr(P.out, r, P.ldo, ch), x);
+}
+
+// g = dout · act'(fout); xhat = (x - mean)·rstd
+__device__ __forceinline__ void bn_g_xhat(const pk_cnn_bn& P, long long r, int ch, float (&g)[8],
+                                          float (&xh)[8]) {
+  float d[8], fo[8], x[8], mean[8], rs[8];
+  ld8(bptr(P.dout, r, P.ldd, ch), d);
+  ld8(bptr(P.x, r, P.ldx, ch), x);
+  ld8f(P.stats + ch, mean);
+  ld8f(P.stats + P.c + ch, rs);
+  if (P.act != PK_CNN_ACT_NONE) ld8(bptr(P.fout, r, P.ldo, ch), fo);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    g[e] = P.act != PK_CNN_ACT_NONE ? d[e] * act_bwd(fo[e], P.act) : d[e];
+    xh[e] = (x[e] - mean[e]) * rs[e];
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_bn_bwd_reduce(const pk_cnn_bn* probs,
+                                                          const int* blk0, int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_bn& P = probs[pi];
+  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+    float xh[8];
+    bn_g_xhat(P, r, ch, a, xh);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) b[e] = a[e] * xh[e];
+  });
+  if (!last_block(P.counter, nblk)) return;
+  bool bad = false;
+  for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+      s1 += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
+      s2 += __ldcg(P.ws + (long long)b * 2 * P.c + P.c + ch);
+    }
+    P.dbeta[ch] = (float)s1;
+    P.dgamma[ch] = (float)s2;
+    P.stats[2 * P.c + ch] = (float)(s1 / P.rows);
+    P.stats[3 * P.c + ch] = (float)(s2 / P.rows);
+    bad |= !isfinite(s1) || !isfinite(s2);
+  }
+  if (bad) *P.flag = 1;
+  if (threadIdx.x == 0) *P.counter = 0;
+}
+
+__global__ void __launch_bounds__(kBlock) k_bn_bwd_apply(const pk_cnn_bn* probs,
+                                                         const int* blk0, int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_bn& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  if (item >= (long long)P.rows * cgs) return;
+  const long long r = item / cgs;
+  const int ch = 8 * (int)(item - r * cgs);
+  float g[8], xh[8], ga[8], mg[8], mgx[8], rs[8];
+  bn_g_xhat(P, r, ch, g, xh);
+  ld8f(P.gamma + ch, ga);
+  ld8f(P.stats + P.c + ch, rs);
+  ld8f(P.stats + 2 * P.c + ch, mg);
+  ld8f(P.stats + 3 * P.c + ch, mgx);
+  float dx[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) dx[e] = ga[e] * rs[e] * (g[e] - mg[e] - xh[e] * mgx[e]);
+  if (P.accumulate) {
+    float o[8];
+    ld8(bptr(P.dx, r, P.ldx2, ch), o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dx[e] += o[e];
+  }
+  st8(bptr(P.dx, r, P.ldx2, ch), dx);
+  if (P.dres) {
+    if (P.res_accumulate) {
+      float o[8];
+      ld8(bptr(P.dres, r, P.ldr, ch), o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] += o[e];
+    }
+    st8(bptr(P.dres, r, P.ldr, ch), g);
+  }
+}
+
+// ============================ depthwise conv =====================================
+__global__ void __launch_bounds__(kBlock) k_dw_fprop(const pk_cnn_dw* probs, const int* blk0,
+                                                     int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_dw& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.p * P.q;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
+  const int oy = rem / P.q, ox = rem - oy * P.q;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = 0; r < P.r; ++r) {
+    const int iy = oy * P.stride - P.pad + r;
+    if ((unsigned)iy >= (unsigned)P.h) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int ix = ox * P.stride - P.pad + s;
+      if ((unsigned)ix >= (unsigned)P.w) continue;
+      float x[8], w[8];
+      ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+      ld8(bptr(P.wt, r * P.s + s, P.c, ch), w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(x[e], w[e], acc[e]);
+    }
+  }
+  st8(bptr(P.y, m, P.ldy, ch), acc);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dw_dgrad(const pk_cnn_dw* probs, const int* blk0,
+                                                     int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_dw& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.h * P.w;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
+  const int iy = rem / P.w, ix = rem - iy * P.w;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = 0; r < P.r; ++r) {
+    const int ty = iy + P.pad - r;
+    if (ty < 0 || ty % P.stride) continue;
+    const int oy = ty / P.stride;
+    if (oy >= P.p) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int tx = ix + P.pad - s;
+      if (tx < 0 || tx % P.stride) continue;
+      const int ox = tx / P.stride;
+      if (ox >= P.q) continue;
+      float d[8], w[8];
+      ld8(bptr(P.dy, ((long long)n * P.p + oy) * P.q + ox, P.ldy, ch), d);
+      ld8(bptr(P.wt, r * P.s + s, P.c, ch), w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(d[e], w[e], acc[e]);
+    }
+  }
+  st8(bptr(P.y, m, P.ldx, ch), acc);
+}
+
+// dw[tap][c] = Σ_pix dy[pix][c] · x[im2col(pix, tap)][c]
+__global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, const int* blk0,
+                                                     int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_dw& P = probs[pi];
+  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+  const int taps = P.r * P.s;  // <= 9
+  const int cgs = P.c >> 3, nr = kBlock / cgs;
+  const int t = threadIdx.x, rl = t / cgs, j = t - rl * cgs, ch = 8 * j;
+  const int pq = P.p * P.q;
+  const long long M = (long long)P.n * pq;
+  const long long m0 = (long long)blk * PK_CNN_DW_PIX, m1 = min(M, m0 + PK_CNN_DW_PIX);
+  float acc[9][8];
+#pragma unroll
+  for (int k = 0; k < 9; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+  if (rl < nr) {
+    for (long long m = m0 + rl; m < m1; m += nr) {
+      const int n = (int)(m / pq), rem = (int)(m - (long long)n * pq);
+      const int oy = rem / P.q, ox = rem - oy * P.q;
+      float d[8];
+      ld8(bptr(P.dy, m, P.ldy, ch), d);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        if (k >= taps) break;
+        const int r = k / P.s, s = k - r * P.s;
+        const int iy = oy * P.stride - P.pad + r, ix = ox * P.stride - P.pad + s;
+        if ((unsigned)iy >= (unsigned)P.h || (unsigned)ix >= (unsigned)P.w) continue;
+        float x[8];
+        ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[k][e] = fmaf(d[e], x[e], acc[k][e]);
+      }
+    }
+  }
+  __shared__ float sh[2048];
+  const int lanes_per_pass = 2048 / P.c;
+  float* out = P.ws + (long long)blk * taps * P.c;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    if (k >= taps) break;
+    float tot[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot[q] = 0.f;
+    for (int base = 0; base < nr; base += lanes_per_pass) {
+      __syncthreads();
+      if (rl < nr && rl >= base && rl < base + lanes_per_pass) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sh[(rl - base) * P.c + ch + e] = acc[k][e];
+      }
+      __syncthreads();
+      const int nl = min(lanes_per_pass, nr - base);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q * kBlock + t < P.c)
+          for (int l = 0; l < nl; ++l) tot[q] += sh[l * P.c + q * kBlock + t];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q * kBlock + t < P.c) out[k * P.c + q * kBlock + t] = tot[q];
+  }
+  if (!last_block(P.counter, nblk)) return;
+  bool bad = false;
+  for (int i = threadIdx.x; i < taps * P.c; i += kBlock) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += __ldcg(P.ws + (long long)b * taps * P.c + i);
+    P.dw[i] = (float)s;
+    bad |= !isfinite(s);
+  }
+  if (bad) *P.flag = 1;
+  if (threadIdx.x == 0) *P.counter = 0;
+}
+
+// ================================ pooling ========================================
+__global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const pk_cnn_pool* probs, const int* blk0,
+                                                        int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_pool& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.p * P.q;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
+  const int oy = rem / P.q, ox = rem - oy * P.q;
+  float best[8];
+  uint8_t arg[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    best[e] = -INFINITY;
+    arg[e] = 0;
+  }
+  for (int r = 0; r < P.r; ++r) {
+    const int iy = oy * P.stride - P.pad + r;
+    if ((unsigned)iy >= (unsigned)P.h) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int ix = ox * P.stride - P.pad + s;
+      if ((unsigned)ix >= (unsigned)P.w) continue;
+      float x[8];
+      ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (x[e] > best[e]) {
+          best[e] = x[e];
+          arg[e] = (uint8_t)(r * P.s + s);
+        }
+    }
+  }
+  st8(bptr(P.y, m, P.ldy, ch), best);
+  uint2 a;
+  a.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | ((uint32_t)arg[3] << 24);
+  a.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | ((uint32_t)arg[7] << 24);
+  *reinterpret_cast<uint2*>(P.arg + m * P.c + ch) = a;
+}
+
+__global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const pk_cnn_pool* probs, const int* blk0,
+                                                        int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_pool& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.h * P.w;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
+  const int iy = rem / P.w, ix = rem - iy * P.w;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = 0; r < P.r; ++r) {
+    const int ty = iy + P.pad - r;
+    if (ty < 0 || ty % P.stride) continue;
+    const int oy = ty / P.stride;
+    if (oy >= P.p) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int tx = ix + P.pad - s;
+      if (tx < 0 || tx % P.stride) continue;
+      const int ox = tx / P.stride;
+      if (ox >= P.q) continue;
+      const long long o = ((long long)n * P.p + oy) * P.q + ox;
+      const uint2 a = *reinterpret_cast<const uint2*>(P.arg + o * P.c + ch);
+      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
+      const int tap = r * P.s + s;
+      float d[8];
+      ld8(bptr(P.dy, o, P.ldy, ch), d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (ab[e] == tap) acc[e] += d[e];
+    }
+  }
+  if (P.accumulate) {
+    float o[8];
+    ld8(bptr(P.dx, m, P.ldx, ch), o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += o[e];
+  }
+  st8(bptr(P.dx, m, P.ldx, ch), acc);
+}
+
+__global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const pk_cnn_pool* probs, const int* blk0,
+                                                        int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_pool& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.p * P.q;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
+  const int oy = rem / P.q, ox = rem - oy * P.q;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = 0; r < P.r; ++r) {
+    const int iy = oy * P.stride - P.pad + r;
+    if ((unsigned)iy >= (unsigned)P.h) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int ix = ox * P.stride - P.pad + s;
+      if ((unsigned)ix >= (unsigned)P.w) continue;
+      float x[8];
+      ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += x[e];
+    }
+  }
+  const float inv = 1.f / (float)(P.r * P.s);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] *= inv;
+  st8(bptr(P.y, m, P.ldy, ch), acc);
+}
+
+__global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const pk_cnn_pool* probs, const int* blk0,
+                                                        int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_pool& P = probs[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long M = (long long)P.n * P.h * P.w;
+  if (item >= M * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
+  const int iy = rem / P.w, ix = rem - iy * P.w;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = 0; r < P.r; ++r) {
+    const int ty = iy + P.pad - r;
+    if (ty < 0 || ty % P.stride) continue;
+    const int oy = ty / P.stride;
+    if (oy >= P.p) continue;
+    for (int s = 0; s < P.s; ++s) {
+      const int tx = ix + P.pad - s;
+      if (tx < 0 || tx % P.stride) continue;
+      const int ox = tx / P.stride;
+      if (ox >= P.q) continue;
+      float d[8];
+      ld8(bptr(P.dy, ((long long)n * P.p + oy) * P.q + ox, P.ldy, ch), d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += d[e];
+    }
+  }
+  const float inv = 1.f / (float)(P.r * P.s);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] *= inv;
+  if (P.accumulate) {
+    float o[8];
+    ld8(bptr(P.dx, m, P.ldx, ch), o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += o[e];
+  }
+  st8(bptr(P.dx, m, P.ldx, ch), acc);
+}
+
+// ======================== softmax cross-entropy head ============================
+// one block per member; reference engine.py:211-230 (loss) and :252-264 (dlogits)
+__global__ void __launch_bounds__(kBlock) k_xent(const pk_cnn_head* probs, int nprob) {
+  const pk_cnn_head& P = probs[blockIdx.x];
+  extern __shared__ float xs[];
+  float* rmax = xs;
+  float* rsum = xs + P.rows;
+  float* rloss = xs + 2 * P.rows;
+  int* rlab = reinterpret_cast<int*>(xs + 3 * P.rows);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float inv = 1.f / (float)P.rows;
+  for (int r = warp; r < P.rows; r += kBlock / 32) {
+    const float* z = P.logits + (long long)r * P.ldl;
+    float mx = -INFINITY;
+    for (int j = lane; j < P.classes; j += 32) mx = fmaxf(mx, z[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f;
+    for (int j = lane; j < P.classes; j += 32) se += expf(z[j] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const long long lab = P.labels[P.idx ? P.idx[r] : r];
+    if (lane == 0) {
+      rmax[r] = mx;
+      rsum[r] = se;
+      rlab[r] = (int)lab;
+      rloss[r] = logf(se) - (z[lab] - mx);
+    }
+    if (P.dlogits) {
+      const float is = 1.f / se;
+      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(P.dlogits) + (long long)r * P.ldl;
+      for (int j = lane; j < P.ldl; j += 32) {
+        float v = 0.f;
+        if (j < P.classes) v = (expf(z[j] - mx) * is - (j == lab ? 1.f : 0.f)) * inv;
+        d[j] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  if (P.dbias) {
+    for (int j = threadIdx.x; j < P.classes; j += kBlock) {
+      float s = 0.f;
+      for (int r = 0; r < P.rows; ++r) {
+        const float z = P.logits[(long long)r * P.ldl + j];
+        s += (expf(z - rmax[r]) / rsum[r] - (j == rlab[r] ? 1.f : 0.f)) * inv;
+      }
+      P.dbias[j] = s;
+      bad |= !isfinite(s);
+    }
+  }
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int r = 0; r < P.rows; ++r) l += rloss[r];
+    l /= P.rows;
+    *P.loss = (float)l;
+    bad |= !isfinite(l);
+  }
+  if (bad && P.flag) *P.flag = 1;
+}
+
+// =================== bias + activation backward (LeNet layers) =====================
+__global__ void __launch_bounds__(kBlock) k_bias_act_bwd(const pk_cnn_bias* probs, const int* blk0,
+                                                         int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_bias& P = probs[pi];
+  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+    ld8(bptr(P.dy, r, P.ld, ch), a);
+    if (P.act != PK_CNN_ACT_NONE) {
+      float fo[8];
+      ld8(bptr(P.fout, r, P.ld, ch), fo);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] *= act_bwd(fo[e], P.act);
+    }
+    if (P.act != PK_CNN_ACT_NONE || P.g != P.dy) st8(bptr(P.g, r, P.ld, ch), a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) b[e] = 0.f;
+  });
+  if (!last_block(P.counter, nblk)) return;
+  bool bad = false;
+  for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
+    P.dbias[ch] = (float)s;
+    bad |= !isfinite(s);
+  }
+  if (bad) *P.flag = 1;
+  if (threadIdx.x == 0) *P.counter = 0;
+}
+
+// ========================== WGRAD split reduction ================================
+__global__ void __launch_bounds__(kBlock) k_split_reduce(const pk_cnn_reduce* probs,
+                                                         const int* blk0, int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_reduce& P = probs[pi];
+  const long long i4 = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  if (i4 * 4 >= P.len) return;
+  float4 s = __ldcg(reinterpret_cast<const float4*>(P.src) + i4);
+  for (int j = 1; j < P.splits; ++j) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(P.src + (long long)j * P.len) + i4);
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  reinterpret_cast<float4*>(P.dst)[i4] = s;
+  if (!isfinite(s.x) || !isfinite(s.y) || !isfinite(s.z) || !isfinite(s.w)) *P.flag = 1;
+}
+
+// ====================== fused multi-member optimizer (K7) ==========================
+// reference engine.py:295-326 (+ coupled weight decay g += wd·w, the torch.optim
+// rule, as the north_star's per-member extension).  A flagged member (non-finite
+// gradient anywhere) is left untouched, engine.py:297-299.
+constexpr int kOptChunk = 4096;  // elements per block
+__global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, const int* blk0,
+                                                int nseg) {
+  const int si = find_prob(blk0, nseg, blockIdx.x);
+  const pk_cnn_opt_seg& S = segs[si];
+  if (*S.flag) return;  // the member's commit verdict (k_commit mode 0)
+  const long long base = (long long)(blockIdx.x - blk0[si]) * kOptChunk;
+  const int t = *S.step + 1;
+  float c1 = 1.f, c2 = 1.f;
+  if (S.kind == PK_OPT_ADAM) {
+    c1 = (float)(1.0 - pow(0.9, (double)t));
+    c2 = (float)(1.0 - pow(0.999, (double)t));
+  }
+  const float lr = S.lr, wd = S.wd;
+  for (int k = threadIdx.x; k < kOptChunk; k += kBlock) {
+    const long long i = base + k;
+    if (i >= S.len) break;
+    float w = S.w[i];
+    float g = S.g[i];
+    if (wd != 0.f) g = fmaf(wd, w, g);
+    switch (S.kind) {
+      case PK_OPT_SGD:
+        w -= lr * g;
+        break;
+      case PK_OPT_MOMENTUM: {
+        const float v = 0.9f * S.s1[i] + g;
+        S.s1[i] = v;
+        w -= lr * v;
+        break;
+      }
+      case PK_OPT_ADAGRAD: {
+        const float a = S.s1[i] + g * g;
+        S.s1[i] = a;
+        w -= lr * g / (sqrtf(a) + 1e-10f);
+        break;
+      }
+      default: {  // adam
+        const float m = 0.9f * S.s1[i] + 0.1f * g;
+        const float v = 0.999f * S.s2[i] + 0.001f * (g * g);
+        S.s1[i] = m;
+        S.s2[i] = v;
+        w -= lr * (m / c1) / (sqrtf(v / c2) + 1e-8f);
+      }
+    }
+    S.w[i] = w;
+    if (S.w16) static_cast<__nv_bfloat16*>(S.w16)[i] = __float2bfloat16_rn(w);
+  }
+}
+
+// ================= transposed bf16 weights for DGRAD (B operand) ===================
+__global__ void __launch_bounds__(kBlock) k_publish_t(const pk_cnn_tpose* probs, const int* blk0,
+                                                      int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_tpose& P = probs[pi];
+  const int tk = (P.k + 31) / 32, tc = (P.c + 31) / 32;
+  int b = blockIdx.x - blk0[pi];
+  const int tap = b / (tk * tc);
+  b -= tap * tk * tc;
+  const int kt = b / tc, ct = b - kt * tc;
+  __shared__ uint16_t tile[32][33];
+  const uint16_t* src = static_cast<const uint16_t*>(P.src);
+  uint16_t* dst = static_cast<uint16_t*>(P.dst);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int co = kt * 32 + i, ci = ct * 32 + tx;
+    tile[i][tx] = (co < P.k && ci < P.c) ? src[(long long)co * P.kpad + tap * P.c + ci] : 0;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int ci = ct * 32 + i, co = kt * 32 + tx;
+    if (ci < P.c && co < P.k) dst[(long long)ci * P.kpadt + tap * P.k + co] = tile[tx][i];
+  }
+}
+
+// Commit, reference packing.py:250-257 + engine.py:297-299: members are
+// updated in pack order and the first non-finite gradient aborts the loop, so a
+// member commits only if no member at or before it (in the problem order) is
+// flagged.  mode 0 (before the optimizer, one thread): verdict = prefix-OR of
+// the flags; mode 1 (after it): step += !verdict, verdict |= flag << 1, flag = 0.
+__global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
+  if (mode == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int run = 0;
+      for (int i = 0; i < nprob; ++i) {
+        run |= *probs[i].flag;
+        *probs[i].verdict = run ? 1 : 0;
+      }
+    }
+    return;
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nprob) return;
+  const pk_cnn_commit& P = probs[i];
+  const int eff = *P.verdict;
+  if (!eff) *P.step += 1;
+  *P.verdict = eff | ((*P.flag ? 1 : 0) << 1);
+  *P.flag = 0;
+}
+
+}  // namespace cnn

@@ -38,11 +38,14 @@ constexpr int kThreads = 192;
 struct Problem {
   const __nv_bfloat16* src;   // gather source: X (FPROP/WGRAD) or dY (DGRAD)
   const __nv_bfloat16* src2;  // WGRAD: dY (the A operand)
-  void* dst;                  // bf16 Y / dX, or fp32 dW partials
+  void* dst;                  // bf16 Y / dX, fp32 Y (out_f32), or fp32 dW partials
+  const long long* idx;       // FPROP/WGRAD: image n of the batch is source image idx[n]
+  const float* bias;          // FPROP epilogue: + bias[n] (NULL = none)
+  int* flag;                  // WGRAD: set to 1 when a written gradient is non-finite
   int M, N, K;                // GEMM extents (K = true reduction extent, unpadded)
   int kper;                   // WGRAD: pixels per split (multiple of 64); else 0
   int tiles_m, tiles_n, splits, tile0;
-  int brow0;                  // FPROP/DGRAD: first row of this problem's B in the map
+  int brow0;                  // FPROP/DGRAD: first row of this problem's B in its map
   int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
   int OH, OW;                 // spatial dims of the GEMM's pixel space
   int R, S, stride, pad;
@@ -50,11 +53,14 @@ struct Problem {
   int ald;                    // WGRAD: dY pixel stride
   int nseg;                   // FPROP: columns per dst segment (concat-N), 0 = one
   int accumulate;             // DGRAD: dst += result
+  int act;                    // FPROP epilogue activation after bias: 0 none, 1 relu, 2 relu6
+  int out_f32;                // FPROP: dst is fp32
   long long dseg;             // elements between dst segments
   long long split_stride;     // WGRAD: elements between split partials
 };
 
 struct Launch {
+  CUtensorMap tm[kMaxProblems];  // weight operand map of each problem (FPROP/DGRAD)
   Problem p[kMaxProblems];
   int nprob;
   int ntile;   // N tile: multiple of 16 in [16, 256] (multiple of 64 for WGRAD)
@@ -69,7 +75,7 @@ __host__ inline size_t smem_bytes(int ntile, int stages) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMap tmB) {
+k_conv_gemm(const __grid_constant__ Launch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -107,7 +113,7 @@ k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMa
     }
     umma::mbar_init(done, 1);
     umma::mbar_fence_init();
-    if (kTma) tc::tma_prefetch(&tmB);
+    if (kTma) tc::tma_prefetch(&L.tm[pi]);
   }
   const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)NT);
   if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
@@ -128,7 +134,7 @@ k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMa
         const int m = tm * BM + r0 + 16 * i;
         if (m < P.M) {
           const int n = m / ohw, rem = m - n * ohw, y = rem / P.OW, x = rem - y * P.OW;
-          rimg[i] = n * P.SH * P.SW;
+          rimg[i] = (MODE == FPROP && P.idx ? (int)P.idx[n] : n) * P.SH * P.SW;
           if (MODE == FPROP) {
             ry[i] = y * P.stride - P.pad;
             rx[i] = x * P.stride - P.pad;
@@ -203,12 +209,13 @@ k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMa
         for (int ps = 0; ps < passes; ++ps) {
           const int row = brr + ps * rpp, pix = kbase + row;
           bool ok = col_ok && pix < kend;
-          int off = 0;
+          long long off = 0;
           if (ok) {
             const int n = pix / ohw, rem = pix - n * ohw, y = rem / P.OW, x = rem - y * P.OW;
             const int iy = y * P.stride - P.pad + fr, ix = x * P.stride - P.pad + fs;
             ok = (unsigned)iy < (unsigned)P.SH && (unsigned)ix < (unsigned)P.SW;
-            off = ((n * P.SH + iy) * P.SW + ix) * P.sld + cc;
+            const long long img = P.idx ? P.idx[n] : n;
+            off = ((img * P.SH + iy) * P.SW + ix) * P.sld + cc;
           }
           tc::cp16(b_s + tc::mnmaj_sw128(row, bcj), ok ? P.src + off : P.src, ok);
         }
@@ -242,7 +249,32 @@ k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMa
       }
       const int n0 = tn * NT + c0;
       if (m >= P.M || n0 >= P.N) continue;
-      if (MODE == WGRAD) {
+      if (MODE == FPROP && (P.bias || P.act)) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float x = v[e];
+          if (P.bias) x += (n0 + e < P.N) ? __ldg(P.bias + n0 + e) : 0.f;
+          if (P.act == 1) x = fmaxf(x, 0.f);
+          else if (P.act == 2) x = fminf(fmaxf(x, 0.f), 6.f);
+          v[e] = x;
+        }
+      }
+      if (MODE == WGRAD && P.flag) {
+        bool bad = false;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) bad |= (n0 + e < P.N) && !isfinite(v[e]);
+        if (bad) *P.flag = 1;
+      }
+      if (MODE == FPROP && P.out_f32) {
+        float* d = static_cast<float*>(P.dst) + (long long)m * P.dld + n0;
+        if (n0 + 16 <= P.N && (P.dld & 3) == 0) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        } else {
+          for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
+        }
+      } else if (MODE == WGRAD) {
         float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride +
                    (long long)m * P.dld + n0;
         if (n0 + 16 <= P.N) {
@@ -335,7 +367,7 @@ k_conv_gemm(const __grid_constant__ Launch L, const __grid_constant__ CUtensorMa
       const int s = kb % ST;
       if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
       umma::mbar_arrive_expect_tx(&full[s], bbytes);
-      tc::tma_load_2d(smem + s * SB + 16384, &tmB, k0 + kb * BK, P.brow0 + tn * NT, &full[s]);
+      tc::tma_load_2d(smem + s * SB + 16384, &L.tm[pi], k0 + kb * BK, P.brow0 + tn * NT, &full[s]);
     }
   }
 

@@ -199,7 +199,13 @@ class ModelHandle:
 
 def make_handle(model_id, arch: MLPArch, optimizer, learning_rate, batch_size,
                 target_steps, dataset_binding, seed, weight_decay=0.0) -> ModelHandle:
-    """packing.py:69-81; `weight_decay` is the coupled-L2 extension."""
+    """packing.py:69-81; `weight_decay` is the coupled-L2 extension.  A
+    ConvArch member (BASELINE configs 1-4) gets a convpack.ConvModelHandle."""
+    from .cnn import ConvArch
+    if isinstance(arch, ConvArch):
+        from .convpack import make_conv_handle
+        return make_conv_handle(model_id, arch, optimizer, learning_rate, batch_size,
+                                target_steps, dataset_binding, seed, weight_decay)
     if batch_size < 1 or target_steps < 1:
         raise PackError("batch_size and target_steps must be >= 1")
     graph = engine.build_mlp(model_id, arch.input_dim, arch.hidden, arch.classes,
@@ -315,6 +321,12 @@ def pack_models(handles) -> PackedModel:
     ids = [h.model_id for h in handles]
     if len(set(ids)) != len(ids):
         raise PackError(f"duplicate model_id in pack: {sorted(ids)}")
+    from .convpack import ConvModelHandle, conv_pack_models
+    conv = [isinstance(h, ConvModelHandle) for h in handles]
+    if any(conv):
+        if not all(conv):
+            raise PackError("a pack holds either MLP or conv members, not both")
+        return conv_pack_models(handles)
     return PackedModel(members=list(handles), fused_graph=_fuse(handles))
 
 
@@ -732,6 +744,9 @@ def packed_step(packed: PackedModel, datasets, preprocess_spec=None, cache=None,
                 stop_at_epoch_end=False):
     """Train every active member for exactly one synchronized step
     (packing.py:185-264).  Returns {model_id: loss}."""
+    from .convpack import ConvPackedModel, conv_packed_step
+    if isinstance(packed, ConvPackedModel):
+        return conv_packed_step(packed, datasets, preprocess_spec, cache, stop_at_epoch_end)
     active = _active_members(packed, datasets, stop_at_epoch_end)
     losses, n_groups, physical, driver = _device_step(packed, active, datasets,
                                                       preprocess_spec, cache,
@@ -745,6 +760,9 @@ def standalone_step(handle: ModelHandle, datasets, preprocess_spec=None, cache=N
     """One unpacked step (packing.py:267-282): the same device kernels on a
     one-member pack, so a packed member's trajectory equals its standalone
     one bit for bit."""
+    from .convpack import ConvModelHandle, conv_standalone_step
+    if isinstance(handle, ConvModelHandle):
+        return conv_standalone_step(handle, datasets, preprocess_spec, cache)
     if handle.finished:
         raise PackError(f"{handle.model_id}: no remaining steps")
     _roll_if_needed(handle, datasets)

@@ -1,0 +1,164 @@
+"""GPU parity of the conv pack path (BASELINE configs 1-3) through the
+reference's pack API (packing.make_handle / pack_models / dedup_inputs /
+packed_step / standalone_step) and the pk_cnn_* C-ABI behind it.
+
+* every kernel teacher-forced against oracle/cnn64.py (tests/_cnn.py states the
+  bf16 tolerances), for LeNet-5, MobileNetV2-w0.5 and ResNet-18 members with
+  mixed optimizers, shared-input (concatenated-N) first layer included;
+* the fused optimizer against engine.py:295-326 in fp32 on the device's grads;
+* packed == standalone bit for bit (K-invariant kernels);
+* the reference's step semantics: non-finite gradient stops the update loop at
+  that member, misaligned batches form separate input groups, the last batch
+  of an epoch is short, cursors and samples_used advance exactly.
+"""
+import numpy as np
+import pytest
+
+from _helpers import has_gpu
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+import torch  # noqa: E402
+
+from oracle import cnn64 as O  # noqa: E402
+from paper_2002_02885_b200 import cnn, data, engine, packing  # noqa: E402
+import _cnn  # noqa: E402
+
+OPTS = ("sgd", "momentum", "adam", "adagrad")
+
+
+def _arch(fam, img=32):
+    return cnn.ConvArch(fam, 10, (3, img, img), 0.5 if fam == "mobilenetv2" else 1.0)
+
+
+def _ds(n=256, img=32, seed=1):
+    return data.synth_dataset(n, 3 * img * img, 10, seed=seed, spread=0.5)
+
+
+def _handles(arch, K, b, opts=OPTS, lr0=0.05, target=50, wd=0.0, prefix="m"):
+    return [packing.make_handle(f"{prefix}{i}", arch, opts[i % len(opts)], lr0 / (i + 1), b,
+                                target, "train", 0, weight_decay=wd) for i in range(K)]
+
+
+def _batch(ds, arch, epoch, pos, take):
+    perm = data.epoch_permutation(ds.dataset_id, ds.n, epoch)
+    rows = perm[pos:pos + take]
+    return O.batch_images(ds.features, arch.image, rows), torch.from_numpy(
+        ds.labels[rows].astype(np.int64))
+
+
+@pytest.mark.parametrize("fam,K,b", [("lenet5", 2, 32), ("mobilenetv2", 2, 32),
+                                     ("resnet18", 2, 16), ("lenet5", 5, 20)])
+def test_teacher_forced_step(fam, K, b):
+    arch = _arch(fam)
+    ds = _ds()
+    hs = _handles(arch, K, b, wd=1e-3)
+    before = [{n.split("/", 1)[1]: v.copy() for n, v in h.params.items()} for h in hs]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    losses = packing.packed_step(packed, {"train": ds})
+    assert packed.last_step_stats == {"physical_inputs": 1, "groups": 1, "driver_batch": b}
+    cp = packed._cp
+    x, y = _batch(ds, arch, 0, 0, b)
+    for k, h in enumerate(hs):
+        _cnn.teacher_forced(cp, k, before[k], x, y, b, losses[h.model_id])
+        _cnn.check_update(cp, k, h.optimizer.kind, h.optimizer.learning_rate, 1e-3, 0,
+                          before[k], {})
+        assert h.optimizer.step_counter == 1 and h.cursor.steps_done == 1 and h.cursor.pos == b
+
+
+def test_end_to_end_loss_vs_oracle():
+    """Whole-net forward from identical state: LeNet (no BN) matches the
+    mirrored oracle to fp32 precision; BN nets within 1 % (bf16 chaos)."""
+    ds = _ds()
+    for fam, b, tol in (("lenet5", 32, 1e-4), ("resnet18", 16, 1e-2)):
+        arch = _arch(fam)
+        hs = _handles(arch, 2, b)
+        init = [{n.split("/", 1)[1]: v.copy() for n, v in h.params.items()} for h in hs]
+        losses = packing.packed_step(packing.dedup_inputs(packing.pack_models(hs)),
+                                     {"train": ds})
+        x, y = _batch(ds, arch, 0, 0, b)
+        spec = _cnn.spec_of(arch)
+        for k, h in enumerate(hs):
+            ref, _, _ = O.forward_backward(spec, init[k], x, y)
+            assert abs(losses[h.model_id] - ref) <= tol * ref, (fam, losses, ref)
+
+
+@pytest.mark.parametrize("fam,b", [("lenet5", 32), ("mobilenetv2", 16), ("resnet18", 8)])
+def test_packed_equals_standalone_bitwise(fam, b):
+    arch = _arch(fam)
+    ds = _ds()
+    K = 3
+    hs = _handles(arch, K, b)
+    solo = _handles(arch, K, b)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    for _ in range(3):
+        lp = packing.packed_step(packed, {"train": ds})
+        for h in solo:
+            ls = packing.standalone_step(h, {"train": ds})
+            assert ls == lp[h.model_id]
+    for a, s in zip(hs, solo):
+        pa, ps = a.params, s.params
+        for n in pa:
+            assert np.array_equal(pa[n], ps[n]), n
+        assert a.optimizer.step_counter == s.optimizer.step_counter == 3
+
+
+def test_nonfinite_stops_update_loop_at_member():
+    """engine.py:297-299 + packing.py:250-253: members before the bad one are
+    updated, the bad one and every later member are not; NonFiniteGradient."""
+    arch = _arch("lenet5")
+    ds = _ds()
+    hs = _handles(arch, 3, 16, opts=("sgd",))
+    packed = packing.pack_models(hs)
+    packing.packed_step(packed, {"train": ds})
+    before = [{n: v.copy() for n, v in h.params.items()} for h in hs]
+    p = hs[1].params
+    p["m1/L2/W"][0, 0, 0, 0] = np.nan
+    before[1]["m1/L2/W"][0, 0, 0, 0] = np.nan
+    with pytest.raises(engine.NonFiniteGradient):
+        packing.packed_step(packed, {"train": ds})
+    assert [h.optimizer.step_counter for h in hs] == [2, 1, 1]
+    assert [h.cursor.steps_done for h in hs] == [2, 1, 1]
+    for k in (1, 2):
+        after = hs[k].params
+        for n in after:
+            np.testing.assert_array_equal(after[n], np.asarray(before[k][n], np.float32))
+    assert not np.array_equal(hs[0].params["m0/L0/W"], before[0]["m0/L0/W"])
+
+
+def test_misaligned_and_partial_batches_match_standalone():
+    """Batches 20 / 32 on n = 84: separate input groups, short last batches
+    (packing.py:167), each member's trajectory == its standalone one."""
+    arch = _arch("lenet5")
+    ds = _ds(n=84)
+    hs = [packing.make_handle(f"m{i}", arch, o, 0.05, b, 30, "train", 0)
+          for i, (o, b) in enumerate((("sgd", 20), ("adam", 32), ("momentum", 20)))]
+    solo = [packing.make_handle(f"m{i}", arch, o, 0.05, b, 30, "train", 0)
+            for i, (o, b) in enumerate((("sgd", 20), ("adam", 32), ("momentum", 20)))]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    for step in range(7):
+        lp = packing.packed_step(packed, {"train": ds})
+        assert packed.last_step_stats["groups"] == 2
+        assert packed.last_step_stats["physical_inputs"] == 2
+        for h in solo:
+            assert packing.standalone_step(h, {"train": ds}) == lp[h.model_id]
+    for a, s in zip(hs, solo):
+        assert (a.cursor.epoch_index, a.cursor.pos) == (s.cursor.epoch_index, s.cursor.pos)
+        np.testing.assert_array_equal(a.cursor.samples_used, s.cursor.samples_used)
+        for n in a.params:
+            assert np.array_equal(a.params[n], s.params[n]), n
+    # b=32 over n=84: 32, 32, 20 | 32, 32, 20 | 32 → epoch 2, pos 32
+    assert (hs[1].cursor.epoch_index, hs[1].cursor.pos) == (2, 32)
+
+
+def test_training_reduces_loss():
+    arch = _arch("lenet5")
+    ds = data.synth_dataset(512, 3 * 32 * 32, 10, seed=3, spread=1.0)
+    hs = _handles(arch, 4, 32, opts=("sgd", "momentum", "adam", "adagrad"), lr0=0.02)
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    first = packing.packed_step(packed, {"train": ds})
+    for _ in range(40):
+        last = packing.packed_step(packed, {"train": ds})
+    for h in hs:
+        assert last[h.model_id] < first[h.model_id], (first, last)
