@@ -418,6 +418,11 @@ def _b200(args):
     return line
 
 
+def _cnn_workloads():
+    from tools import bench_cnn
+    return bench_cnn.WORKLOADS
+
+
 HB = dict(n=2000, dim=784, classes=10, hidden=(16,), eta=3, seed=0,
           strategies=("original", "knn"))
 
@@ -572,13 +577,55 @@ def _reference(args):
                           if args.hyperband_ref_r > 0 else None)}
 
 
+def _cnn_line(args):
+    """bench line of a conv workload (tools/bench_cnn.py; BASELINE configs 1-3)."""
+    import torch
+    import torch.distributed as dist
+
+    from tools import bench_cnn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return None
+        bench_cnn.cpu_baseline(args.workload, steps=1)
+        r = bench_cnn.cpu_baseline(args.workload, seconds=max(args.cpu_seconds, 5.0))
+        wl = bench_cnn.WORKLOADS[args.workload]
+        return {"metric": METRIC, "value": r["value"], "unit": UNIT, "impl": "reference",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["ms_per_member_step"] * wl["K"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.workload, "family": wl["family"],
+                           "members": wl["K"], "batch": wl["batch"]},
+                "cpu_baseline": r,
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    line = bench_cnn.run_b200(args, world, rank, local, Clocks, L2_FLUSH_BYTES)
+    if world > 1:
+        dist.destroy_process_group()
+    if line is None:
+        return None
+    out = {"metric": METRIC, "unit": UNIT}
+    out.update(line)
+    out["e2e"]["unit"] = UNIT
+    out["cpu_baseline"] = (bench_cnn.cpu_baseline(args.workload, seconds=args.cpu_seconds)
+                           if args.cpu_seconds > 0 and world == 1 else None)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="config0", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="config0",
+                    choices=sorted(WORKLOADS) + sorted(_cnn_workloads()))
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--hyperband-r", type=int, default=81,
@@ -588,7 +635,10 @@ def main():
                     help="the same Hyperband on the CPU reference (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    line = _reference(args) if args.impl == "reference" else _b200(args)
+    if args.workload in _cnn_workloads():
+        line = _cnn_line(args)
+    else:
+        line = _reference(args) if args.impl == "reference" else _b200(args)
     if line is not None:
         print(json.dumps(line), flush=True)
 

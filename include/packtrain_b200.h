@@ -299,7 +299,8 @@ int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void* x, const 
 #define PK_CNN_OPT 17           /* fused multi-member optimizer + bf16 publish   */
 #define PK_CNN_PUBLISH_T 18     /* transposed bf16 weights for DGRAD             */
 #define PK_CNN_COMMIT 19        /* per-member step counter / non-finite verdict  */
-#define PK_CNN_NUM_KINDS 20
+#define PK_CNN_GATHER 20        /* batch rows src[idx[i]] -> dst[i] (e.g. over PCIe) */
+#define PK_CNN_NUM_KINDS 21
 
 #define PK_CNN_ACT_NONE 0
 #define PK_CNN_ACT_RELU 1
@@ -442,6 +443,16 @@ typedef struct pk_cnn_commit {
   int32_t* flag;
   int32_t* verdict;
 } pk_cnn_commit;
+
+/* dst row i = src row idx[i] (row_bytes a multiple of 16); src may be
+ * page-locked host memory (read by the GPU over PCIe) */
+typedef struct pk_cnn_gather {
+  const void* src;
+  void* dst;
+  const int64_t* idx;
+  int64_t row_bytes;
+  int32_t rows, pad0;
+} pk_cnn_gather;
 
 typedef struct pk_cnn_op {
   int32_t kind;           /* PK_CNN_* */

@@ -90,7 +90,7 @@ class ConvGeom(C.Structure):
 CNN_KINDS = ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD", "BN_STATS", "BN_APPLY", "BN_BWD_REDUCE",
              "BN_BWD_APPLY", "DW_FPROP", "DW_DGRAD", "DW_WGRAD", "MAXPOOL_FWD", "MAXPOOL_BWD",
              "AVGPOOL_FWD", "AVGPOOL_BWD", "XENT", "BIAS_ACT_BWD", "SPLIT_REDUCE", "OPT",
-             "PUBLISH_T", "COMMIT")
+             "PUBLISH_T", "COMMIT", "GATHER")
 CNN = {k: i for i, k in enumerate(CNN_KINDS)}
 CNN_ACT = {"none": 0, "relu": 1, "relu6": 2}
 PK_CNN_BN_ROWS = 256
@@ -158,6 +158,11 @@ class CnnCommit(C.Structure):
     _fields_ = [("step", _vp), ("flag", _vp), ("verdict", _vp)]
 
 
+class CnnGather(C.Structure):
+    _fields_ = [("src", _vp), ("dst", _vp), ("idx", _vp), ("row_bytes", _i64), ("rows", _i32),
+                ("pad0", _i32)]
+
+
 class CnnOp(C.Structure):
     _fields_ = [("kind", _i32), ("nprob", _i32), ("cfg0", _i32), ("cfg1", _i32),
                 ("probs", _vp)]
@@ -178,6 +183,7 @@ CNN_STRUCT[CNN["SPLIT_REDUCE"]] = CnnReduce
 CNN_STRUCT[CNN["OPT"]] = CnnOptSeg
 CNN_STRUCT[CNN["PUBLISH_T"]] = CnnTpose
 CNN_STRUCT[CNN["COMMIT"]] = CnnCommit
+CNN_STRUCT[CNN["GATHER"]] = CnnGather
 
 
 class PKError(RuntimeError):

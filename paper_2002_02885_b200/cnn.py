@@ -378,10 +378,12 @@ def _ptr(t):
 
 
 class DeviceConvDataset:
-    """A dataset resident in HBM as NHWC bf16 [n][H][W][Cp] (rows are the
-    reference's NCHW feature rows, data.py:18-39) plus int64 labels."""
+    """A dataset as NHWC bf16 [n][H][W][Cp] (rows are the reference's NCHW
+    feature rows, data.py:18-39) plus int64 labels: resident in HBM, or
+    (host=True, the streamed e2e mode) in page-locked host memory that the
+    step's GATHER op reads over PCIe."""
 
-    def __init__(self, ds, image, device):
+    def __init__(self, ds, image, device, host=False):
         torch = _torch()
         c, h, w = image
         n = ds.features.shape[0]
@@ -393,9 +395,16 @@ class DeviceConvDataset:
         x = np.zeros((n, h, w, cp), dtype=np.float32)
         x[..., :c] = np.asarray(ds.features, dtype=np.float32).reshape(n, c, h, w).transpose(
             0, 2, 3, 1)
-        bits = bf16_bits(x)
-        self.x = torch.from_numpy(bits.view(np.int16)).to(device).view(torch.bfloat16)
-        self.y = torch.from_numpy(np.asarray(ds.labels, dtype=np.int64)).to(device)
+        bits = torch.from_numpy(bf16_bits(x).view(np.int16))
+        labels = torch.from_numpy(np.asarray(ds.labels, dtype=np.int64))
+        self.host = bool(host)
+        if self.host:
+            self.x = bits.pin_memory().view(torch.bfloat16)
+            self.y = labels.pin_memory()
+        else:
+            self.x = bits.to(device).view(torch.bfloat16)
+            self.y = labels.to(device)
+        self.row_bytes = h * w * cp * 2
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
@@ -461,6 +470,7 @@ class ConvPack:
         for m in members:
             self.acts.append(self._alloc_acts(m))
         self._progs = {}
+        self.staging = {}   # leader -> device batch buffer (streamed inputs)
         # programs are captured / replayed on this stream (graph capture cannot use the
         # legacy default stream); it is ordered after the caller's stream on entry
         self.stream = torch.cuda.Stream(device=self.dev)
@@ -687,10 +697,10 @@ class ConvPack:
             if op.kind == "conv":
                 ty = net.tensors[op.y]
                 first = op.x == "input"
-                src = data.x.data_ptr() if first else A["val"][op.x].data_ptr()
+                src, fidx = self._input(lead, data) if first else (A["val"][op.x].data_ptr(), 0)
                 cs = _lib.CnnConv()
                 cs.src = src
-                cs.idx = idx if first else 0
+                cs.idx = fidx
                 cs.wt = self.w16[k][op.params[0]].data_ptr()
                 cs.dst = A["val"][op.y].data_ptr()
                 cs.bias = self.params[k][op.params[1]].data_ptr() if op.a["bias"] else 0
@@ -733,6 +743,19 @@ class ConvPack:
                 h.rows, h.classes, h.ldl = take, op.a["classes"], t.c
                 steps.append((CNN["XENT"], None, h, None))
         return steps
+
+    def _input(self, lead, data):
+        """(source, index list) the first conv of a member led by `lead` reads:
+        the resident dataset through the batch indices, or the leader's
+        staging buffer that the step's GATHER filled (streamed inputs)."""
+        if not data.host:
+            return data.x.data_ptr(), self.idx[lead].data_ptr()
+        st = self.staging.get(lead)
+        if st is None:
+            _, h, w = self.members[lead].net.arch.image
+            st = self._z(self.members[lead].batch, h, w, data.cp, dt=self.torch.bfloat16)
+            self.staging[lead] = st
+        return st.data_ptr(), 0
 
     def _bn_struct(self, k, op, rows):
         m = self.members[k]
@@ -834,8 +857,8 @@ class ConvPack:
                 bsplits = _wgrad_cfg(ty.c, rsc, m.batch * ty.h * ty.w)[1]
                 splits = min(splits, bsplits) if op.name in A["split"] else 1
                 cs = _lib.CnnConv()
-                cs.src = data.x.data_ptr() if first else A["val"][op.x].data_ptr()
-                cs.idx = idx if first else 0
+                cs.src, cs.idx = self._input(lead, data) if first else (
+                    A["val"][op.x].data_ptr(), 0)
                 cs.dy = A["grad"][op.y].data_ptr()
                 cs.n, cs.h, cs.w, cs.c = take, tx.h, tx.w, tx.c
                 cs.k, cs.r, cs.s = ty.c, op.a["r"], op.a["s"]
@@ -1007,7 +1030,18 @@ class ConvPack:
     def _build_ops(self, takes, leads, data, with_update=True):
         K = len(self.members)
         act = [k for k in range(K) if takes[k] > 0]
-        ops = self._group([self._fwd_steps(k, takes[k], leads[k], data) for k in act])
+        ops = []
+        if data.host:  # streamed inputs: each group's batch rows over PCIe, once
+            gs = []
+            for lead in sorted({leads[k] for k in act}):
+                g = _lib.CnnGather()
+                g.src = data.x.data_ptr()
+                g.dst = self._input(lead, data)[0]
+                g.idx = self.idx[lead].data_ptr()
+                g.row_bytes, g.rows = data.row_bytes, takes[lead]
+                gs.append(g)
+            ops.append((CNN["GATHER"], None, gs))
+        ops += self._group([self._fwd_steps(k, takes[k], leads[k], data) for k in act])
         ops += self._group([self._bwd_steps(k, takes[k], leads[k], data) for k in act])
         if with_update:
             cm = []

@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import cnn, engine
+from . import runtime as _rt
 from .cnn import ConvArch
 from .data import epoch_permutation
 
@@ -180,17 +181,19 @@ def conv_pack_models(handles) -> ConvPackedModel:
 _DATA: dict = {}   # id(dataset) -> {(image, device): DeviceConvDataset}
 
 
-def device_dataset(ds, image, device):
-    """The HBM copy of `ds` (uploaded once per dataset object and device)."""
+def device_dataset(ds, image, device, host=False):
+    """The NHWC bf16 copy of `ds` the step reads (made once per dataset object,
+    device and placement): HBM-resident, or page-locked host memory for the
+    streamed input mode (runtime.set_input_mode("stream"))."""
     per = _DATA.get(id(ds))
     if per is None:
         per = {}
         _DATA[id(ds)] = per
         weakref.finalize(ds, _DATA.pop, id(ds), None)
-    key = (tuple(image), device)
+    key = (tuple(image), device, host)
     d = per.get(key)
     if d is None:
-        d = cnn.DeviceConvDataset(ds, image, device)
+        d = cnn.DeviceConvDataset(ds, image, device, host)
         per[key] = d
     return d
 
@@ -248,7 +251,7 @@ def _plan(packed: ConvPackedModel, active, datasets, cp):
             if h.arch.image != image or ds.dim != h.arch.input_dim:
                 raise engine.ShapeMismatch(f"{h.model_id}/x", ("batch", h.arch.input_dim),
                                            (b, ds.dim))
-        d = device_dataset(ds, image, cp.device)
+        d = device_dataset(ds, image, cp.device, host=_rt.input_mode() == "stream")
         if data is None:
             data = d
         elif d is not data:

@@ -103,6 +103,7 @@ size_t prob_size(int kind) {
     case PK_CNN_OPT: return sizeof(pk_cnn_opt_seg);
     case PK_CNN_PUBLISH_T: return sizeof(pk_cnn_tpose);
     case PK_CNN_COMMIT: return sizeof(pk_cnn_commit);
+    case PK_CNN_GATHER: return sizeof(pk_cnn_gather);
   }
   return 0;
 }
@@ -161,6 +162,10 @@ int prob_blocks(int kind, const void* pr) {
       const pk_cnn_tpose& P = *static_cast<const pk_cnn_tpose*>(pr);
       return P.taps * cdiv(P.k, 32) * cdiv(P.c, 32);
     }
+    case PK_CNN_GATHER: {
+      const pk_cnn_gather& P = *static_cast<const pk_cnn_gather*>(pr);
+      return (int)((P.row_bytes * P.rows + cnn::kGatherChunk - 1) / cnn::kGatherChunk);
+    }
   }
   return 0;
 }
@@ -205,6 +210,11 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_SPLIT_REDUCE: {
       const pk_cnn_reduce& P = *static_cast<const pk_cnn_reduce*>(pr);
       if (P.len % 4 || P.splits < 1) return "split_reduce: len % 4";
+      break;
+    }
+    case PK_CNN_GATHER: {
+      const pk_cnn_gather& P = *static_cast<const pk_cnn_gather*>(pr);
+      if (P.row_bytes % 16 || P.rows < 0) return "gather: row_bytes % 16";
       break;
     }
   }
@@ -376,6 +386,7 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
     case PK_CNN_PUBLISH_T:
       k_publish_t<<<nb, kBlock, 0, st>>>(dp<pk_cnn_tpose>(g, o), db(g, o), np);
       break;
+    case PK_CNN_GATHER: k_gather<<<nb, kBlock, 0, st>>>(dp<pk_cnn_gather>(g, o), db(g, o), np); break;
     case PK_CNN_COMMIT:
       k_commit<<<cdiv(np, 128), 128, 0, st>>>(dp<pk_cnn_commit>(g, o), np, o.ntile);
       break;

@@ -822,4 +822,20 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
   *P.flag = 0;
 }
 
+// batch gather: one block per 4 KB of rows, 16-byte vectors
+constexpr int kGatherChunk = 4096;
+__global__ void __launch_bounds__(kBlock) k_gather(const pk_cnn_gather* probs, const int* blk0,
+                                                   int nprob) {
+  const int pi = find_prob(blk0, nprob, blockIdx.x);
+  const pk_cnn_gather& P = probs[pi];
+  const long long v0 = (long long)(blockIdx.x - blk0[pi]) * (kGatherChunk / 16);
+  const long long vrow = P.row_bytes / 16, total = vrow * P.rows;
+  for (long long v = v0 + threadIdx.x; v < min(total, v0 + kGatherChunk / 16); v += kBlock) {
+    const long long r = v / vrow, c = v - r * vrow;
+    const uint4* s = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(P.src) +
+                                                    P.idx[r] * P.row_bytes) + c;
+    reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + r * P.row_bytes)[c] = *s;
+  }
+}
+
 }  // namespace cnn

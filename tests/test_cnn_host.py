@@ -106,6 +106,7 @@ _PROBE = r'''
 int main(void) {
   S(pk_cnn_conv) S(pk_cnn_bn) S(pk_cnn_dw) S(pk_cnn_pool) S(pk_cnn_head) S(pk_cnn_bias)
   S(pk_cnn_reduce) S(pk_cnn_opt_seg) S(pk_cnn_tpose) S(pk_cnn_commit) S(pk_cnn_op)
+  S(pk_cnn_gather)
   O(pk_cnn_conv, n) O(pk_cnn_conv, nseg) O(pk_cnn_bn, rows) O(pk_cnn_bn, eps)
   O(pk_cnn_opt_seg, len) O(pk_cnn_opt_seg, wd) O(pk_cnn_head, ldl) O(pk_cnn_op, probs)
   printf("PK_CNN_NUM_KINDS %d\n", PK_CNN_NUM_KINDS);
@@ -116,7 +117,8 @@ int main(void) {
 _PY = {"pk_cnn_conv": _lib.CnnConv, "pk_cnn_bn": _lib.CnnBn, "pk_cnn_dw": _lib.CnnDw,
        "pk_cnn_pool": _lib.CnnPool, "pk_cnn_head": _lib.CnnHead, "pk_cnn_bias": _lib.CnnBias,
        "pk_cnn_reduce": _lib.CnnReduce, "pk_cnn_opt_seg": _lib.CnnOptSeg,
-       "pk_cnn_tpose": _lib.CnnTpose, "pk_cnn_commit": _lib.CnnCommit, "pk_cnn_op": _lib.CnnOp}
+       "pk_cnn_tpose": _lib.CnnTpose, "pk_cnn_commit": _lib.CnnCommit, "pk_cnn_op": _lib.CnnOp,
+       "pk_cnn_gather": _lib.CnnGather}
 
 
 def test_ctypes_structs_match_c_header(tmp_path):
