@@ -618,6 +618,21 @@ def _cnn_line(args):
     return out
 
 
+def _self_launch(n):
+    """`python bench.py --gpus N` without torchrun: re-launch this command as N
+    ranks (one per GPU) through torch.distributed.run on 127.0.0.1; rank 0's
+    JSON line reaches our stdout."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -635,6 +650,15 @@ def main():
                     help="the same Hyperband on the CPU reference (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_self_launch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if os.environ.get("PK_BENCH_DRYRUN"):  # launcher test hook (tests/test_bench_contract.py)
+        print(json.dumps({"dryrun": True, "rank": int(os.environ.get("RANK", "0")),
+                          "world": world}), flush=True)
+        return
     if args.workload in _cnn_workloads():
         line = _cnn_line(args)
     else:

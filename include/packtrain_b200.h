@@ -342,7 +342,7 @@ typedef struct pk_cnn_bn {
   float* stats;           /* [4][c]: mean, rstd, mean(g), mean(g·xhat) */
   float* run_mean;        /* STATS: running statistics (torch momentum rule) or NULL */
   float* run_var;
-  float* ws;              /* partials workspace, >= 2*c*ceil(rows/PK_CNN_BN_ROWS) floats */
+  float* ws;              /* partials workspace (see rpb) */
   int32_t* counter;       /* zero-initialised; reset by the kernel */
   int32_t* flag;          /* member's non-finite flag */
   int32_t rows, c, ldx, ldo, ldr, ldd, ldx2;
@@ -351,8 +351,10 @@ typedef struct pk_cnn_bn {
   int32_t res_accumulate; /* BWD_APPLY: dres += */
   int32_t use_running;    /* APPLY: normalise with running stats (eval) */
   float eps, momentum;
+  int32_t rpb;            /* STATS / BWD_REDUCE: rows per partial block (multiple of 32);
+                             ws >= 2*c*ceil(rows/rpb) floats + 2*c doubles */
+  int32_t pad0;
 } pk_cnn_bn;
-#define PK_CNN_BN_ROWS 256
 
 /* depthwise r x s conv (groups = c), weights bf16 [r*s][c] / gradient fp32 [r*s][c] */
 typedef struct pk_cnn_dw {
@@ -365,8 +367,10 @@ typedef struct pk_cnn_dw {
   int32_t* counter;
   int32_t* flag;
   int32_t n, h, w, c, r, s, stride, pad, p, q, ldx, ldy;
+  int32_t ppb;            /* WGRAD: output pixels per partial block; ws >= r*s*c *
+                             ceil(n*p*q/ppb) floats + r*s*c doubles */
+  int32_t pad0;
 } pk_cnn_dw;
-#define PK_CNN_DW_PIX 256  /* output pixels per WGRAD partial */
 
 /* pooling: max (window r x s, stride, pad; argmax kept as uint8) or average */
 typedef struct pk_cnn_pool {
@@ -402,6 +406,8 @@ typedef struct pk_cnn_bias {
   int32_t* counter;
   int32_t* flag;
   int32_t rows, c, ld, act;
+  int32_t rpb;            /* rows per partial block; ws as pk_cnn_bn */
+  int32_t pad0;
 } pk_cnn_bias;
 
 /* dst[i] = Σ_{j<splits} src[j*len + i] (j in order) */

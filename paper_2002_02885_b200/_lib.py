@@ -93,8 +93,6 @@ CNN_KINDS = ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD", "BN_STATS", "BN_APPLY", "
              "PUBLISH_T", "COMMIT", "GATHER")
 CNN = {k: i for i, k in enumerate(CNN_KINDS)}
 CNN_ACT = {"none": 0, "relu": 1, "relu6": 2}
-PK_CNN_BN_ROWS = 256
-PK_CNN_DW_PIX = 256
 _vp, _i32, _i64, _f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
 
 
@@ -115,12 +113,13 @@ class CnnBn(C.Structure):
                                     "ws", "counter", "flag")]
                 + _ints("rows", "c", "ldx", "ldo", "ldr", "ldd", "ldx2", "act", "accumulate",
                         "res_accumulate", "use_running")
-                + [("eps", _f32), ("momentum", _f32)])
+                + [("eps", _f32), ("momentum", _f32), ("rpb", _i32), ("pad0", _i32)])
 
 
 class CnnDw(C.Structure):
     _fields_ = ([(n, _vp) for n in ("x", "wt", "dy", "y", "dw", "ws", "counter", "flag")]
-                + _ints("n", "h", "w", "c", "r", "s", "stride", "pad", "p", "q", "ldx", "ldy"))
+                + _ints("n", "h", "w", "c", "r", "s", "stride", "pad", "p", "q", "ldx", "ldy",
+                        "ppb", "pad0"))
 
 
 class CnnPool(C.Structure):
@@ -137,7 +136,7 @@ class CnnHead(C.Structure):
 
 class CnnBias(C.Structure):
     _fields_ = ([(n, _vp) for n in ("dy", "fout", "g", "dbias", "ws", "counter", "flag")]
-                + _ints("rows", "c", "ld", "act"))
+                + _ints("rows", "c", "ld", "act", "rpb", "pad0"))
 
 
 class CnnReduce(C.Structure):

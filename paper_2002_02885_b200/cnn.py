@@ -408,6 +408,25 @@ class DeviceConvDataset:
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
+def rows_per_block(rows, nout=0):
+    """Rows per partial block of a column reduction with `nout` outputs per
+    block: a function of the member's own shape only (K-invariant).  The last
+    block sums nblk x nout partials alone, so nblk is capped at ~8192 / nout
+    (and at 128), at least 32 rows per block."""
+    target = max(4, min(128, 8192 // max(nout, 1)))
+    return max(32, rup(cdiv(rows, target), 32))
+
+
+def red_blocks_max(rows, nout):
+    """upper bound of cdiv(r, rows_per_block(r, nout)) over r <= rows (ws sizing)"""
+    return min(max(4, min(128, 8192 // max(nout, 1))), cdiv(rows, 32))
+
+
+def _red_ws(nout_per_blk, nblk, nout):
+    """floats for nblk partial records + an fp64 total area of nout doubles."""
+    return rup(nout_per_blk * nblk, 2) + 2 * nout + 2
+
+
 def _pick_ntile(n, cap=256):
     if n <= cap:
         return rup(n, 16)
@@ -581,16 +600,19 @@ class ConvPack:
             tx = net.tensors[op.x]
             if op.kind in ("bn",):
                 rows = b * tx.h * tx.w
-                A["ws"][op.name] = z(2 * tx.c * cdiv(rows, _lib.PK_CNN_BN_ROWS))
+                nb = red_blocks_max(rows, 2 * tx.c)
+                A["ws"][op.name] = z(_red_ws(2 * tx.c, nb, 2 * tx.c))
                 A["stats"][op.name] = z(4 * tx.c)
             elif op.kind == "conv" and op.a["bias"] and not op.a["out_f32"]:
                 ty = net.tensors[op.y]
                 rows = b * ty.h * ty.w
-                A["ws"][op.name] = z(2 * ty.c * cdiv(rows, _lib.PK_CNN_BN_ROWS))
+                nb = red_blocks_max(rows, ty.c)
+                A["ws"][op.name] = z(_red_ws(2 * ty.c, nb, 2 * ty.c))
             elif op.kind == "dw":
                 ty = net.tensors[op.y]
                 pix = b * ty.h * ty.w
-                A["ws"][op.name] = z(op.a["r"] * op.a["s"] * tx.c * cdiv(pix, _lib.PK_CNN_DW_PIX))
+                nout = op.a["r"] * op.a["s"] * tx.c
+                A["ws"][op.name] = z(_red_ws(nout, red_blocks_max(pix, nout), nout))
             elif op.kind == "maxpool":
                 ty = net.tensors[op.y]
                 A["arg"][op.name] = z(b * ty.h * ty.w * ty.c, dt=torch.uint8)
@@ -779,6 +801,7 @@ class ConvPack:
         b.counter = self._counter(k, 4 * net.ops.index(op))
         b.flag = self._flag(k)
         b.rows, b.c = rows, tx.c
+        b.rpb = rows_per_block(rows, 2 * tx.c)
         b.ldx = b.ldo = b.ldr = b.ldd = b.ldx2 = tx.c
         b.act = CNN_ACT[op.a["act"]]
         b.eps, b.momentum = _BN_EPS, _BN_MOMENTUM
@@ -801,6 +824,7 @@ class ConvPack:
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
         d.ldx, d.ldy = tx.c, ty.c
+        d.ppb = rows_per_block(take * ty.h * ty.w, op.a["r"] * op.a["s"] * tx.c)
         return d
 
     def _pool_struct(self, k, op, take):
@@ -848,6 +872,7 @@ class ConvPack:
                     bs.counter = self._counter(k, 4 * net.ops.index(op) + 1)
                     bs.flag = self._flag(k)
                     bs.rows, bs.c, bs.ld = rows, ty.c, ty.c
+                    bs.rpb = rows_per_block(rows, ty.c)
                     bs.act = CNN_ACT[op.a["act"]]
                     steps.append((CNN["BIAS_ACT_BWD"], None, bs, None))
                 W = net.param(op.params[0])

@@ -117,12 +117,12 @@ int prob_blocks(int kind, const void* pr) {
     case PK_CNN_BN_STATS:
     case PK_CNN_BN_BWD_REDUCE: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
-      return cdiv(P.rows, PK_CNN_BN_ROWS);
+      return cdiv(P.rows, P.rpb);
     }
     case PK_CNN_BN_APPLY:
     case PK_CNN_BN_BWD_APPLY: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
-      return blocks_of(items(P.rows, P.c));
+      return blocks_of(items(cdiv(P.rows, cnn::kApplyRows), P.c));
     }
     case PK_CNN_DW_FPROP: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
@@ -134,7 +134,7 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
-      return cdiv((long long)P.n * P.p * P.q, PK_CNN_DW_PIX);
+      return cdiv((long long)P.n * P.p * P.q, P.ppb);
     }
     case PK_CNN_MAXPOOL_FWD:
     case PK_CNN_AVGPOOL_FWD: {
@@ -148,7 +148,7 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_BIAS_ACT_BWD: {
       const pk_cnn_bias& P = *static_cast<const pk_cnn_bias*>(pr);
-      return cdiv(P.rows, PK_CNN_BN_ROWS);
+      return cdiv(P.rows, P.rpb);
     }
     case PK_CNN_SPLIT_REDUCE: {
       const pk_cnn_reduce& P = *static_cast<const pk_cnn_reduce*>(pr);
@@ -179,6 +179,8 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_BN_BWD_APPLY: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
       if (!c8(P.c) || P.rows <= 0) return "bn: channels must be a multiple of 8 in [8, 2048]";
+      if ((kind == PK_CNN_BN_STATS || kind == PK_CNN_BN_BWD_REDUCE) && (P.rpb < 1 || P.rpb % 32))
+        return "bn: rows per block must be a positive multiple of 32";
       break;
     }
     case PK_CNN_DW_FPROP:
@@ -186,6 +188,7 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
+      if (kind == PK_CNN_DW_WGRAD && P.ppb < 1) return "dw: pixels per block >= 1";
       break;
     }
     case PK_CNN_MAXPOOL_FWD:
@@ -198,7 +201,7 @@ std::string check_prob(int kind, const void* pr) {
     }
     case PK_CNN_BIAS_ACT_BWD: {
       const pk_cnn_bias& P = *static_cast<const pk_cnn_bias*>(pr);
-      if (!c8(P.c)) return "bias: channels must be a multiple of 8 in [8, 2048]";
+      if (!c8(P.c) || P.rpb < 1) return "bias: channels % 8 in [8, 2048], rows per block >= 1";
       break;
     }
     case PK_CNN_XENT: {

@@ -10,10 +10,10 @@
 // Determinism / K-invariance: every reduction (BN statistics, BN backward,
 // bias and depthwise weight gradients, the softmax head) sums a fixed row
 // partition of the member's own rows in a fixed order: per-block fp32 partial
-// sums over PK_CNN_BN_ROWS rows → workspace → the last block to finish (atomic
-// ticket) adds the partials in block order in fp64.  Results depend only on
-// the member's shape, never on which members share the launch, so packed ==
-// standalone bit for bit.
+// sums over `rpb` rows (chosen by the planner from the member's own row count)
+// → workspace → the last block to finish (atomic ticket) adds the partials in
+// fp64 along a fixed lane split.  Results depend only on the member's shape,
+// never on which members share the launch, so packed == standalone bit for bit.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -92,12 +92,12 @@ __device__ __forceinline__ bool last_block(int* counter, int nblk) {
 }
 
 // ------------------------------------------------------------------------------
-// Column (channel) partial sums of up to two per-element quantities over one
-// PK_CNN_BN_ROWS-row block.  F(row, ch0, a[8], b[8]) fills the two values of
-// the 8 channels ch0.. of `row`.  Writes ws[blk][2][c].
+// Column (channel) partial sums of up to two per-element quantities over rows
+// [r0, r1) of one block.  F(row, ch0, a[8], b[8]) fills the two values of the 8
+// channels ch0.. of `row`.  Writes ws[blk][2][c].
 // ------------------------------------------------------------------------------
 template <class F>
-__device__ __forceinline__ void col_partials(int rows, int c, int blk, float* ws, F f) {
+__device__ __forceinline__ void col_partials(int r0, int r1, int c, int blk, float* ws, F f) {
   __shared__ float sh[2][2048];
   const int cgs = c >> 3;
   const int nr = kBlock / cgs;  // row lanes (cgs <= 256)
@@ -106,8 +106,8 @@ __device__ __forceinline__ void col_partials(int rows, int c, int blk, float* ws
   float s1[8], s2[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
-  const int r0 = blk * PK_CNN_BN_ROWS, r1 = min(rows, r0 + PK_CNN_BN_ROWS);
   if (rl < nr) {
+#pragma unroll 4
     for (int r = r0 + rl; r < r1; r += nr) {
       float a[8], b[8];
       f(r, 8 * j, a, b);
@@ -156,26 +156,63 @@ __device__ __forceinline__ void col_partials(int rows, int c, int blk, float* ws
   }
 }
 
+// Last block: tot[i] = Σ_b ws[b*stride + i] for i < nout, in fp64, along a
+// fixed split of the blocks over lanes (thread t: item t % nout, lane t / nout),
+// lanes combined in order.  tot (nout doubles) may live in global memory; it is
+// visible to the whole block on return.
+__device__ __forceinline__ void final_reduce(const float* ws, int nblk, int nout, int stride,
+                                             double* tot) {
+  __shared__ double part[kBlock];
+  const int t = threadIdx.x;
+  if (nout >= kBlock / 2) {
+    for (int i = t; i < nout; i += kBlock) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int b = 0; b < nblk; ++b) s += __ldcg(ws + (long long)b * stride + i);
+      tot[i] = s;
+    }
+    __syncthreads();
+    return;
+  }
+  const int lanes = min(kBlock / nout, nblk);
+  const int item = t % nout, lane = t / nout;
+  double s = 0.0;
+  if (lane < lanes) {
+#pragma unroll 8
+    for (int b = lane; b < nblk; b += lanes) s += __ldcg(ws + (long long)b * stride + item);
+    part[lane * nout + item] = s;
+  }
+  __syncthreads();
+  if (t < nout) {
+    double v = 0.0;
+    for (int l = 0; l < lanes; ++l) v += part[l * nout + t];
+    tot[t] = v;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double* tot_area(float* ws, long long floats) {
+  return reinterpret_cast<double*>(ws + ((floats + 1) & ~1LL));
+}
+
 // ============================== batch norm =====================================
 __global__ void __launch_bounds__(kBlock) k_bn_stats(const pk_cnn_bn* probs, const int* blk0,
                                                      int nprob) {
   const int pi = find_prob(blk0, nprob, blockIdx.x);
   const pk_cnn_bn& P = probs[pi];
   const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
-  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+  const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
+  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     ld8(bptr(P.x, r, P.ldx, ch), a);
 #pragma unroll
     for (int e = 0; e < 8; ++e) b[e] = a[e] * a[e];
   });
   if (!last_block(P.counter, nblk)) return;
+  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
+  final_reduce(P.ws, nblk, 2 * P.c, 2 * P.c, tot);
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      s1 += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
-      s2 += __ldcg(P.ws + (long long)b * 2 * P.c + P.c + ch);
-    }
-    const double mean = s1 / P.rows;
-    const double var = fmax(s2 / P.rows - mean * mean, 0.0);
+    const double mean = tot[ch] / P.rows;
+    const double var = fmax(tot[P.c + ch] / P.rows - mean * mean, 0.0);
     P.stats[ch] = (float)mean;
     P.stats[P.c + ch] = (float)(1.0 / sqrt(var + (double)P.eps));
     if (P.run_mean) {
@@ -201,29 +238,46 @@ __device__ __forceinline__ void bn_coef(const pk_cnn_bn& P, int ch, float (&mean
   }
 }
 
+constexpr int kApplyRows = 4;  // rows per thread in the BN apply kernels
+
 __global__ void __launch_bounds__(kBlock) k_bn_apply(const pk_cnn_bn* probs, const int* blk0,
                                                      int nprob) {
   const int pi = find_prob(blk0, nprob, blockIdx.x);
   const pk_cnn_bn& P = probs[pi];
   const int cgs = P.c >> 3;
   const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
-  if (item >= (long long)P.rows * cgs) return;
-  const long long r = item / cgs;
-  const int ch = 8 * (int)(item - r * cgs);
-  float x[8], mean[8], rs[8], g[8], b[8];
-  ld8(bptr(P.x, r, P.ldx, ch), x);
+  const long long rg = item / cgs;  // group of kApplyRows rows
+  if (rg * kApplyRows >= P.rows) return;
+  const int ch = 8 * (int)(item - rg * cgs);
+  float mean[8], rs[8], g[8], b[8];
   bn_coef(P, ch, mean, rs);
   ld8f(P.gamma + ch, g);
   ld8f(P.beta + ch, b);
-  float res[8];
-  if (P.res) ld8(bptr(P.res, r, P.ldr, ch), res);
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    float y = (x[e] - mean[e]) * rs[e] * g[e] + b[e];
-    if (P.res) y += res[e];
-    x[e] = act_fwd(y, P.act);
+    g[e] *= rs[e];
+    b[e] -= mean[e] * g[e];  // y = x·(γ·rstd) + (β − mean·γ·rstd)
   }
-  st8(bptr(P.out, r, P.ldo, ch), x);
+  const long long r0 = rg * kApplyRows;
+  const int nr = (int)min((long long)kApplyRows, P.rows - r0);
+  float x[kApplyRows][8], res[kApplyRows][8];
+#pragma unroll
+  for (int i = 0; i < kApplyRows; ++i)
+    if (i < nr) {
+      ld8(bptr(P.x, r0 + i, P.ldx, ch), x[i]);
+      if (P.res) ld8(bptr(P.res, r0 + i, P.ldr, ch), res[i]);
+    }
+#pragma unroll
+  for (int i = 0; i < kApplyRows; ++i)
+    if (i < nr) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float y = fmaf(x[i][e], g[e], b[e]);
+        if (P.res) y += res[i][e];
+        x[i][e] = act_fwd(y, P.act);
+      }
+      st8(bptr(P.out, r0 + i, P.ldo, ch), x[i]);
+    }
 }
 
 // g = dout · act'(fout); xhat = (x - mean)·rstd
@@ -247,20 +301,19 @@ __global__ void __launch_bounds__(kBlock) k_bn_bwd_reduce(const pk_cnn_bn* probs
   const int pi = find_prob(blk0, nprob, blockIdx.x);
   const pk_cnn_bn& P = probs[pi];
   const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
-  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+  const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
+  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     float xh[8];
     bn_g_xhat(P, r, ch, a, xh);
 #pragma unroll
     for (int e = 0; e < 8; ++e) b[e] = a[e] * xh[e];
   });
   if (!last_block(P.counter, nblk)) return;
+  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
+  final_reduce(P.ws, nblk, 2 * P.c, 2 * P.c, tot);
   bool bad = false;
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      s1 += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
-      s2 += __ldcg(P.ws + (long long)b * 2 * P.c + P.c + ch);
-    }
+    const double s1 = tot[ch], s2 = tot[P.c + ch];
     P.dbeta[ch] = (float)s1;
     P.dgamma[ch] = (float)s2;
     P.stats[2 * P.c + ch] = (float)(s1 / P.rows);
@@ -277,33 +330,46 @@ __global__ void __launch_bounds__(kBlock) k_bn_bwd_apply(const pk_cnn_bn* probs,
   const pk_cnn_bn& P = probs[pi];
   const int cgs = P.c >> 3;
   const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
-  if (item >= (long long)P.rows * cgs) return;
-  const long long r = item / cgs;
-  const int ch = 8 * (int)(item - r * cgs);
-  float g[8], xh[8], ga[8], mg[8], mgx[8], rs[8];
-  bn_g_xhat(P, r, ch, g, xh);
+  const long long rg = item / cgs;
+  if (rg * kApplyRows >= P.rows) return;
+  const int ch = 8 * (int)(item - rg * cgs);
+  float ga[8], mg[8], mgx[8], rs[8], mean[8];
   ld8f(P.gamma + ch, ga);
+  ld8f(P.stats + ch, mean);
   ld8f(P.stats + P.c + ch, rs);
   ld8f(P.stats + 2 * P.c + ch, mg);
   ld8f(P.stats + 3 * P.c + ch, mgx);
-  float dx[8];
+  const long long r0 = rg * kApplyRows;
+  const int nr = (int)min((long long)kApplyRows, P.rows - r0);
+  for (int i = 0; i < nr; ++i) {
+    const long long r = r0 + i;
+    float d[8], fo[8], x[8], dx[8];
+    ld8(bptr(P.dout, r, P.ldd, ch), d);
+    ld8(bptr(P.x, r, P.ldx, ch), x);
+    if (P.act != PK_CNN_ACT_NONE) ld8(bptr(P.fout, r, P.ldo, ch), fo);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) dx[e] = ga[e] * rs[e] * (g[e] - mg[e] - xh[e] * mgx[e]);
-  if (P.accumulate) {
-    float o[8];
-    ld8(bptr(P.dx, r, P.ldx2, ch), o);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) dx[e] += o[e];
-  }
-  st8(bptr(P.dx, r, P.ldx2, ch), dx);
-  if (P.dres) {
-    if (P.res_accumulate) {
-      float o[8];
-      ld8(bptr(P.dres, r, P.ldr, ch), o);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) g[e] += o[e];
+    for (int e = 0; e < 8; ++e) {
+      const float g = P.act != PK_CNN_ACT_NONE ? d[e] * act_bwd(fo[e], P.act) : d[e];
+      const float xh = (x[e] - mean[e]) * rs[e];
+      dx[e] = ga[e] * rs[e] * (g - mg[e] - xh * mgx[e]);
+      d[e] = g;
     }
-    st8(bptr(P.dres, r, P.ldr, ch), g);
+    if (P.accumulate) {
+      float o[8];
+      ld8(bptr(P.dx, r, P.ldx2, ch), o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dx[e] += o[e];
+    }
+    st8(bptr(P.dx, r, P.ldx2, ch), dx);
+    if (P.dres) {
+      if (P.res_accumulate) {
+        float o[8];
+        ld8(bptr(P.dres, r, P.ldr, ch), o);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[e] += o[e];
+      }
+      st8(bptr(P.dres, r, P.ldr, ch), d);
+    }
   }
 }
 
@@ -385,7 +451,7 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, con
   const int t = threadIdx.x, rl = t / cgs, j = t - rl * cgs, ch = 8 * j;
   const int pq = P.p * P.q;
   const long long M = (long long)P.n * pq;
-  const long long m0 = (long long)blk * PK_CNN_DW_PIX, m1 = min(M, m0 + PK_CNN_DW_PIX);
+  const long long m0 = (long long)blk * P.ppb, m1 = min(M, m0 + P.ppb);
   float acc[9][8];
 #pragma unroll
   for (int k = 0; k < 9; ++k)
@@ -437,12 +503,13 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, con
       if (q * kBlock + t < P.c) out[k * P.c + q * kBlock + t] = tot[q];
   }
   if (!last_block(P.counter, nblk)) return;
+  const int nout = taps * P.c;
+  double* tot = tot_area(P.ws, (long long)nblk * nout);
+  final_reduce(P.ws, nblk, nout, nout, tot);
   bool bad = false;
-  for (int i = threadIdx.x; i < taps * P.c; i += kBlock) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += __ldcg(P.ws + (long long)b * taps * P.c + i);
-    P.dw[i] = (float)s;
-    bad |= !isfinite(s);
+  for (int i = threadIdx.x; i < nout; i += kBlock) {
+    P.dw[i] = (float)tot[i];
+    bad |= !isfinite(tot[i]);
   }
   if (bad) *P.flag = 1;
   if (threadIdx.x == 0) *P.counter = 0;
@@ -679,7 +746,8 @@ __global__ void __launch_bounds__(kBlock) k_bias_act_bwd(const pk_cnn_bias* prob
   const int pi = find_prob(blk0, nprob, blockIdx.x);
   const pk_cnn_bias& P = probs[pi];
   const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
-  col_partials(P.rows, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
+  const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
+  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     ld8(bptr(P.dy, r, P.ld, ch), a);
     if (P.act != PK_CNN_ACT_NONE) {
       float fo[8];
@@ -692,12 +760,12 @@ __global__ void __launch_bounds__(kBlock) k_bias_act_bwd(const pk_cnn_bias* prob
     for (int e = 0; e < 8; ++e) b[e] = 0.f;
   });
   if (!last_block(P.counter, nblk)) return;
+  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
+  final_reduce(P.ws, nblk, P.c, 2 * P.c, tot);
   bool bad = false;
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += __ldcg(P.ws + (long long)b * 2 * P.c + ch);
-    P.dbias[ch] = (float)s;
-    bad |= !isfinite(s);
+    P.dbias[ch] = (float)tot[ch];
+    bad |= !isfinite(tot[ch]);
   }
   if (bad) *P.flag = 1;
   if (threadIdx.x == 0) *P.counter = 0;

@@ -23,8 +23,12 @@ class OOMError(Exception):
         self.demand = int(demand)
         self.capacity = int(capacity)
         self.deficit = int(demand - capacity)
+        self.what = what
         super().__init__(f"{what}: demand {self.demand} B exceeds capacity "
                          f"{self.capacity} B by {self.deficit} B")
+
+    def __reduce__(self):  # pickles across the Hyperband pool's gather
+        return (type(self), (self.demand, self.capacity, self.what))
 
 
 def _al(v):

@@ -36,11 +36,17 @@ class ShapeMismatch(EngineError):
         self.port, self.expected, self.got = port, expected, got
         super().__init__(f"port {port!r}: expected shape {expected}, got {got}")
 
+    def __reduce__(self):  # pickles across the Hyperband pool's gather
+        return (type(self), (self.port, self.expected, self.got))
+
 
 class NonFiniteGradient(EngineError):
     def __init__(self, param: str):
         self.param = param
         super().__init__(f"non-finite gradient for parameter {param!r}")
+
+    def __reduce__(self):
+        return (type(self), (self.param,))
 
 
 @dataclass(frozen=True)

@@ -23,9 +23,14 @@ its `rung_runner`:
   tensor of the training path crosses GPUs.  Results merge in group order,
   so records, selection and best config are identical to a 1-GPU run.
 * Failures: OOM degrades a group to singletons on the rank that owns it
-  (tuner.py:309-314); an ExecutorError on any rank is re-raised on every
-  rank after the gather, so all ranks abort the same bracket
-  (tuner.py:332-334).
+  (tuner.py:309-314).  Any other exception a group raises on its rank
+  (ExecutorError, EngineError / NonFiniteGradient from a diverging config,
+  an OOMError from the singleton fallback, ...) is caught, shipped through
+  the rung's gather as (type, message, pickled exception) and re-raised on
+  EVERY rank after the merge, first failing group in group order — so all
+  ranks fail together exactly as the 1-GPU run does (ExecutorError aborts
+  the bracket, tuner.py:332-334; anything else propagates) instead of the
+  healthy ranks blocking in the gather.
 
 Executors used with the pool expose, besides the reference protocol
 (`device`, `memory_bytes(cfg)`, `evaluate(cfgs, epochs)`):
@@ -35,6 +40,7 @@ and `drop_state(config_id)`; optional `group_cost(cfgs, epochs)`.
 from __future__ import annotations
 
 import math
+import pickle
 import time
 
 from . import tuner
@@ -133,8 +139,8 @@ class PackPool:
             try:
                 got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
                 mine[gi] = ("ok", got, t_ms)
-            except tuner.ExecutorError as exc:
-                mine[gi] = ("executor_error", str(exc), 0.0)
+            except Exception as exc:  # noqa: BLE001 - re-raised on every rank below
+                mine[gi] = ("error", _pack_exc(exc), 0.0)
         self.busy_ms += (time.perf_counter() - t0) * 1000.0
         merged = {}
         for part in self._all_gather(mine):
@@ -145,9 +151,27 @@ class PackPool:
         self.rungs += 1
         for gi in range(len(groups)):
             kind, a, _ = merged[gi]
-            if kind == "executor_error":
-                raise tuner.ExecutorError(a)
+            if kind == "error":
+                raise _unpack_exc(a)
         return [(merged[gi][1], merged[gi][2]) for gi in range(len(groups))]
+
+
+def _pack_exc(exc):
+    try:
+        blob = pickle.dumps(exc)
+        pickle.loads(blob)
+    except Exception:  # noqa: BLE001 - unpicklable: keep type name + message
+        blob = None
+    return (type(exc).__name__, str(exc), blob)
+
+
+def _unpack_exc(packed):
+    name, msg, blob = packed
+    if blob is not None:
+        return pickle.loads(blob)
+    if name == "ExecutorError":
+        return tuner.ExecutorError(msg)
+    return RuntimeError(f"{name}: {msg}")
 
 
 def sharded_hyperband(R, eta, executor, seed, strategy="knn", group=None, **kw):

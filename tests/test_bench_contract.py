@@ -57,3 +57,19 @@ def test_reference_arm_line():
     assert (d["metric"], d["unit"], d["higher_is_better"]) == (
         own["metric"], own["unit"], own["higher_is_better"])
     assert d["config"]["workload"] == own["config"]["workload"]
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """`python bench.py --gpus 2` (no torchrun) must run 2 ranks, one per GPU:
+    the launcher re-executes itself under torch.distributed.run (dry-run hook,
+    no device work)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, PK_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 for d in lines)

@@ -12,7 +12,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2002_02885_b200 import hyperband_pool, tuner
+from paper_2002_02885_b200 import engine, hyperband_pool, tuner
 
 
 class StatefulStub:
@@ -21,9 +21,10 @@ class StatefulStub:
 
     device = None
 
-    def __init__(self, fail_on=None):
+    def __init__(self, fail_on=None, diverge_on=None):
         self.state = {}
         self.fail_on = fail_on
+        self.diverge_on = diverge_on
 
     def memory_bytes(self, cfg):
         return 0
@@ -36,6 +37,8 @@ class StatefulStub:
         for c in cfgs:
             if self.fail_on is not None and c.config_id == self.fail_on:
                 raise tuner.ExecutorError(f"injected failure at {c.config_id}")
+            if self.diverge_on is not None and c.config_id == self.diverge_on:
+                raise engine.NonFiniteGradient(f"cfg{c.config_id:04d}/L0/W")
             e = self.state.get(c.config_id, 0) + epochs
             self.state[c.config_id] = e
             out[c.config_id] = ((c.config_id * 7919) % 101) / (1.0 + math.log1p(e)) \
@@ -66,22 +69,24 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, strategy, fail_on, q):
+def _worker(rank, world, port, strategy, fail_on, q, diverge_on=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        res, pool = hyperband_pool.sharded_hyperband(27, 3, StatefulStub(fail_on), seed=3,
-                                                     strategy=strategy)
+        res, pool = hyperband_pool.sharded_hyperband(27, 3, StatefulStub(fail_on, diverge_on),
+                                                     seed=3, strategy=strategy)
         q.put((rank, _summary(res), pool.migrations, pool.rungs))
+    except Exception as exc:  # noqa: BLE001 - reported to the test
+        q.put((rank, ("raised", type(exc).__name__, str(exc)), -1, -1))
     finally:
         dist.destroy_process_group()
 
 
-def _run_world(world, strategy, fail_on=None):
+def _run_world(world, strategy, fail_on=None, diverge_on=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, strategy, fail_on, q))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, strategy, fail_on, q, diverge_on))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -131,3 +136,16 @@ def test_lpt_assignment_balances_and_prefers_owner():
     pool.owner = {c.config_id: 2 for c in groups[0].members}
     same = [tuner.PackGroup(groups[0].members, 0, 0)]
     assert pool.assign(ex, same, 3) == [2]
+
+
+def test_sharded_engine_error_raises_on_every_rank():
+    """A diverging config (NonFiniteGradient, not an ExecutorError) propagates
+    out of the serial run; sharded, every rank raises it together instead of
+    the healthy rank blocking in the rung gather."""
+    serial = tuner.packed_hyperband(27, 3, StatefulStub(), seed=3, strategy="knn")
+    victim = serial.records[7].config_id
+    with pytest.raises(engine.NonFiniteGradient) as ref:
+        tuner.packed_hyperband(27, 3, StatefulStub(diverge_on=victim), seed=3, strategy="knn")
+    out = _run_world(2, "knn", diverge_on=victim)
+    for _, summ, _, _ in out:
+        assert summ == ("raised", "NonFiniteGradient", str(ref.value))
