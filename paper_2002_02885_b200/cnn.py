@@ -433,8 +433,11 @@ def _pick_ntile(n, cap=256):
     return 128 if rup(n, 128) - n <= rup(n, 256) - n else 256
 
 
-def _stages(ntile):
-    return 4 if ntile > 128 else 6
+def _stages(ntile, budget=110 * 1024):
+    """Pipeline depth for an N tile: the deepest ring within ~110 KB of shared
+    memory, so two CTAs share an SM (one's epilogue overlaps the other's
+    mainloop)."""
+    return max(2, min(6, budget // (16384 + ntile * 128)))
 
 
 def _wgrad_cfg(k, rsc, pix):

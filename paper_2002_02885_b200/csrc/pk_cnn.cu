@@ -31,6 +31,44 @@ bool encode_fn() {
   return g_encode != nullptr;
 }
 
+PFN_cuTensorMapEncodeIm2col_v12000 g_encode_i2c = nullptr;
+std::once_flag g_i2c_once;
+int g_driver_version = 0;
+
+// 4-D NHWC bf16 im2col map (dims {c, w, h, n}, pixel pitch `ld` elements):
+// boxes of `pixels` GEMM rows x 64 channels, SW128, zero fill outside the image.
+// lower/upper: the pixel box corners {w, h} (CUTLASS sm100 conv conventions).
+bool make_map_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c, int ld,
+                     int lower_w, int lower_h, int upper_w, int upper_h, int stride,
+                     int pixels) {
+  std::call_once(g_i2c_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_i2c = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
+    cudaDriverGetVersion(&g_driver_version);
+  });
+  if (!g_encode_i2c) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)w * ld * 2,
+                           (cuuint64_t)h * w * ld * 2};
+  int lower[2] = {lower_w, lower_h}, upper[2] = {upper_w, upper_h};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  if (g_encode_i2c(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                   lower, upper, 64, (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  // the driver workaround CUTLASS applies to im2col maps of tensors < 128 KiB on
+  // drivers <= 13.1 (cute/atom/copy_traits_sm90_im2col.hpp)
+  const double bytes = (double)n * h * w * ld * 2;
+  if (g_driver_version <= 13010 && bytes < 131072.0)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return true;
+}
+
 // 2-D bf16 tensor map [rows][cols] (row pitch `ld` elements), box {64, box_rows}, SW128
 bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                  uint32_t box_rows) {
@@ -260,8 +298,19 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         return fail(PK_ERR_ARG, "conv: c, k multiples of 8; stride 1 or 2");
       p.R = g.r; p.S = g.s; p.stride = g.stride; p.pad = g.pad;
       p.dst = g.dst;
+      const bool one = g.r == 1 && g.s == 1 && g.stride == 1 && g.pad == 0;
       if (kind == PK_CNN_CONV_FPROP) {
         const int kpad = rup(g.r * g.s * g.c, 64);
+        if (!g.idx && one) {
+          p.a_mode = 1;
+          if (!make_map_2d(&L.tmA[j], g.src, (uint64_t)g.n * g.h * g.w, g.c, g.ldx, cg::BM))
+            return fail(PK_ERR_CUDA, "conv: FPROP activation map");
+        } else if (!g.idx && g.c % 64 == 0) {
+          p.a_mode = 2;
+          if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.h, g.w, g.c, g.ldx, -g.pad, -g.pad,
+                               g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, cg::BM))
+            return fail(PK_ERR_CUDA, "conv: FPROP im2col map");
+        }
         p.src = static_cast<const __nv_bfloat16*>(g.src);
         p.idx = reinterpret_cast<const long long*>(g.idx);
         p.bias = g.bias; p.act = g.act; p.out_f32 = g.out_f32;
@@ -274,6 +323,17 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         p.splits = 1;
       } else if (kind == PK_CNN_CONV_DGRAD) {
         const int kpadt = rup(g.r * g.s * g.k, 64);
+        if (one) {
+          p.a_mode = 1;
+          if (!make_map_2d(&L.tmA[j], g.src, (uint64_t)g.n * g.p * g.q, g.k, g.ldy, cg::BM))
+            return fail(PK_ERR_CUDA, "conv: DGRAD activation map");
+        } else if (g.stride == 1 && g.k % 64 == 0) {
+          p.a_mode = 2;
+          if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.p, g.q, g.k, g.ldy, g.pad - (g.s - 1),
+                               g.pad - (g.r - 1), g.pad - (g.s - 1) + g.w - g.q,
+                               g.pad - (g.r - 1) + g.h - g.p, 1, cg::BM))
+            return fail(PK_ERR_CUDA, "conv: DGRAD im2col map");
+        }
         p.src = static_cast<const __nv_bfloat16*>(g.src);
         p.accumulate = g.accumulate;
         p.M = g.n * g.h * g.w; p.N = g.c; p.K = g.r * g.s * g.k;
@@ -295,6 +355,15 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         p.splits = cdiv(pix, p.kper);
         if (p.splits != sp) return fail(PK_ERR_ARG, "conv: WGRAD splits leave an empty split");
         p.flag = p.splits == 1 ? g.flag : nullptr;
+        if (!g.idx && (one || g.c % 64 == 0)) {
+          p.b_mode = one ? 1 : 2;
+          const bool ok =
+              one ? make_map_2d(&L.tm[j], g.src, (uint64_t)g.n * g.h * g.w, g.c, g.ldx, 64)
+                  : make_map_im2col(&L.tm[j], g.src, g.n, g.h, g.w, g.c, g.ldx, -g.pad, -g.pad,
+                                    g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, 64);
+          if (!ok || !make_map_2d(&L.tmA[j], g.dy, (uint64_t)pix, g.k, g.ldy, 64))
+            return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
+        }
         p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
         p.OH = g.p; p.OW = g.q; p.ald = g.ldy;
         p.dld = kpad;

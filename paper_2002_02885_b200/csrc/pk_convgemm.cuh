@@ -55,12 +55,17 @@ struct Problem {
   int accumulate;             // DGRAD: dst += result
   int act;                    // FPROP epilogue activation after bias: 0 none, 1 relu, 2 relu6
   int out_f32;                // FPROP: dst is fp32
+  int a_mode;                 // activation operand: 0 cp.async gather, 1 TMA 2-D tile,
+                              //   2 TMA im2col (FPROP/DGRAD: A; WGRAD: A=dY is TMA 2-D
+                              //   whenever b_mode != 0)
+  int b_mode;                 // WGRAD X operand: 0 gather, 1 TMA 2-D tile, 2 TMA im2col
   long long dseg;             // elements between dst segments
   long long split_stride;     // WGRAD: elements between split partials
 };
 
 struct Launch {
-  CUtensorMap tm[kMaxProblems];  // weight operand map of each problem (FPROP/DGRAD)
+  CUtensorMap tm[kMaxProblems];   // FPROP/DGRAD: weights; WGRAD: X (b_mode != 0)
+  CUtensorMap tmA[kMaxProblems];  // activation operand map (a_mode / WGRAD dY)
   Problem p[kMaxProblems];
   int nprob;
   int ntile;   // N tile: multiple of 16 in [16, 256] (multiple of 64 for WGRAD)
@@ -74,7 +79,7 @@ __host__ inline size_t smem_bytes(int ntile, int stages) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 k_conv_gemm(const __grid_constant__ Launch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -104,16 +109,19 @@ k_conv_gemm(const __grid_constant__ Launch L) {
     kend = min(P.K, k0 + P.kper);
   }
   const int nkb = (kend - k0 + BK - 1) / BK;
-  constexpr bool kTma = MODE != WGRAD;
+  // which operands the TMA warp loads: all (tma_all) or only the FPROP/DGRAD weights
+  const bool tma_all = MODE == WGRAD ? P.b_mode != 0 : P.a_mode != 0;
+  const bool kTma = MODE != WGRAD || tma_all;
 
   if (tid == 160) {
     for (int s = 0; s < ST; ++s) {
-      umma::mbar_init(&full[s], 128 + (kTma ? 1 : 0));
+      umma::mbar_init(&full[s], tma_all ? 1 : 128 + (kTma ? 1 : 0));
       umma::mbar_init(&empty[s], 1);
     }
     umma::mbar_init(done, 1);
     umma::mbar_fence_init();
     if (kTma) tc::tma_prefetch(&L.tm[pi]);
+    if (tma_all) tc::tma_prefetch(&L.tmA[pi]);
   }
   const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)NT);
   if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
@@ -125,7 +133,9 @@ k_conv_gemm(const __grid_constant__ Launch L) {
   if (warp < 4) {
     // =========================== producers ===========================
     const uint32_t sbase = tc::smem_u32(smem);
-    if (MODE != WGRAD) {
+    if (tma_all) {
+      // operands arrive by TMA (warp 5): these warps only run the epilogue
+    } else if (MODE != WGRAD) {
       const int j = tid & 7, r0 = tid >> 3;
       int rimg[8], ry[8], rx[8];
       const int ohw = P.OH * P.OW;
@@ -227,7 +237,7 @@ k_conv_gemm(const __grid_constant__ Launch L) {
         }
       }
     }
-    if (nkb > 0) {
+    if (nkb > 0 && !tma_all) {
       tc::cp_wait<0>();
       umma::fence_async_smem();
       tc::mbar_arrive(&full[(nkb - 1) % ST]);
@@ -361,13 +371,61 @@ k_conv_gemm(const __grid_constant__ Launch L) {
     }
     __syncwarp();
   } else if (kTma && warp == 5 && lane == 0) {
-    // =========================== TMA (weights) ===========================
-    const uint32_t bbytes = (uint32_t)NT * 128u;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % ST;
-      if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
-      umma::mbar_arrive_expect_tx(&full[s], bbytes);
-      tc::tma_load_2d(smem + s * SB + 16384, &L.tm[pi], k0 + kb * BK, P.brow0 + tn * NT, &full[s]);
+    // =========================== TMA ===========================
+    const int ohw = P.OH * P.OW;
+    if (MODE == WGRAD) {
+      // A = dY [pix][co] (2-D box {64 co, 64 pix}, two 64-wide M atoms);
+      // B = X im2col / 2-D [pix][c] (box {64 c, 64 pix}, NT/64 N atoms)
+      const uint32_t bytes = 16384u + (uint32_t)NT * 128u;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % ST;
+        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+        umma::mbar_arrive_expect_tx(&full[s], bytes);
+        uint8_t* a_s = smem + s * SB;
+        uint8_t* b_s = a_s + 16384;
+        const int pix0 = k0 + kb * BK;
+        tc::tma_load_2d(a_s, &L.tmA[pi], tm * BM, pix0, &full[s]);
+        tc::tma_load_2d(a_s + 8192, &L.tmA[pi], tm * BM + 64, pix0, &full[s]);
+        const int img = pix0 / ohw, rem = pix0 - img * ohw;
+        const int py = rem / P.OW, px = rem - py * P.OW;
+        for (int j = 0; j < NT / 64; ++j) {
+          const int n = tn * NT + j * 64;
+          if (P.b_mode == 1) {
+            tc::tma_load_2d(b_s + j * 8192, &L.tm[pi], n, pix0, &full[s]);
+          } else {
+            const int tap = n / P.SC, c0 = n - tap * P.SC;
+            const int fr = tap / P.S, fs = tap - fr * P.S;
+            tc::tma_im2col_4d(b_s + j * 8192, &L.tm[pi], c0, px * P.stride - P.pad,
+                              py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, &full[s]);
+          }
+        }
+      }
+    } else {
+      const uint32_t bbytes = (uint32_t)NT * 128u;
+      const uint32_t bytes = bbytes + (tma_all ? 16384u : 0u);
+      const int m0 = tm * BM;
+      const int img = m0 / ohw, rem = m0 - img * ohw;
+      const int py = rem / P.OW, px = rem - py * P.OW;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % ST;
+        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+        umma::mbar_arrive_expect_tx(&full[s], bytes);
+        const int kk = k0 + kb * BK;
+        if (P.a_mode == 1) {
+          tc::tma_load_2d(smem + s * SB, &L.tmA[pi], kk, m0, &full[s]);
+        } else if (P.a_mode == 2) {
+          const int tap = kk / P.SC, c0 = kk - tap * P.SC;
+          const int fr = tap / P.S, fs = tap - fr * P.S;
+          if (MODE == FPROP)
+            tc::tma_im2col_4d(smem + s * SB, &L.tmA[pi], c0, px * P.stride - P.pad,
+                              py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, &full[s]);
+          else  // stride-1 data gradient: dY window of dX pixel (y, x), taps reversed
+            tc::tma_im2col_4d(smem + s * SB, &L.tmA[pi], c0, px + P.pad - (P.S - 1),
+                              py + P.pad - (P.R - 1), img, (uint16_t)(P.S - 1 - fs),
+                              (uint16_t)(P.R - 1 - fr), &full[s]);
+        }
+        tc::tma_load_2d(smem + s * SB + 16384, &L.tm[pi], kk, P.brow0 + tn * NT, &full[s]);
+      }
     }
   }
 

@@ -90,6 +90,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int
       : "memory");
 }
 
+// 4-D im2col box of tensor map `m` (NHWC: {c, w, h, n} base coordinates of the box's
+// first pixel, filter offsets {ow, oh} added per pixel) → shared `dst`
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* m, int c, int w,
+                                              int h, int n, uint16_t ow, uint16_t oh,
+                                              uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(mbar)),
+      "h"(ow), "h"(oh)
+      : "memory");
+}
+
 // ---- cp.async (16 B, zero fill when !ok) ------------------------------------------
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),

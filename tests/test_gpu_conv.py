@@ -20,7 +20,7 @@ pytestmark = [pytest.mark.gpu,
 import torch  # noqa: E402
 import torch.nn.functional as F  # noqa: E402
 
-from paper_2002_02885_b200 import _lib  # noqa: E402
+from paper_2002_02885_b200 import _lib, cnn  # noqa: E402
 
 SHAPES = [
     # n, h, w, c, k, r, s, stride, pad
@@ -134,3 +134,71 @@ def test_wgrad(shape, ntile, splits):
     _run(2, g, _nhwc(x).bfloat16(), None, _nhwc(dy).bfloat16(), out, ntile, splits)
     got = out.double().sum(0)[:, :r * s * c]
     _close(got, ref, 1e-5, bf16_out=False)
+
+
+# ---- the same GEMMs through the program path (pk_cnn_prog), which feeds the
+# activation operands by TMA: 2-D tiles for 1x1 stride-1 layers, im2col boxes
+# for C % 64 == 0 (FPROP, WGRAD; DGRAD at stride 1), cp.async otherwise --------
+PROG_SHAPES = [
+    # n, h, w, c, k, r, s, stride, pad           modes (fprop a, dgrad a, wgrad b)
+    (3, 10, 10, 96, 24, 1, 1, 1, 0),            # 1, 1, 1 (c % 64 != 0)
+    (2, 9, 11, 64, 64, 3, 3, 1, 1),             # 2, 2, 2
+    (2, 15, 15, 128, 256, 3, 3, 2, 1),          # 2, 0, 2 (stride-2 dgrad gathers)
+    (3, 14, 14, 64, 128, 1, 1, 2, 0),           # 2, 0, 2
+    (2, 16, 16, 64, 64, 7, 7, 2, 3),            # 2, 0, 2
+    (2, 7, 7, 512, 512, 3, 3, 1, 1),            # 2, 2, 2 (deep K)
+    (2, 12, 12, 8, 64, 7, 7, 2, 3),             # 0, 0, 0 (first-layer shape)
+]
+
+
+def _prog_conv(kind, g, x, w, dy, out, ntile, splits=1, stages=4):
+    from paper_2002_02885_b200 import cnn
+    cs = _lib.CnnConv()
+    cs.n, cs.h, cs.w, cs.c, cs.k = g.n, g.h, g.w, g.c, g.k
+    cs.r, cs.s, cs.stride, cs.pad, cs.p, cs.q = g.r, g.s, g.stride, g.pad, g.p, g.q
+    cs.ldx, cs.ldy = g.c, g.k
+    if kind == "CONV_FPROP":
+        cs.src, cs.wt, cs.dst, cs.ldo = x.data_ptr(), w.data_ptr(), out.data_ptr(), g.k
+    elif kind == "CONV_DGRAD":
+        cs.src, cs.wt, cs.dst, cs.ldo = dy.data_ptr(), w.data_ptr(), out.data_ptr(), g.c
+    else:
+        cs.src, cs.dy, cs.dst, cs.splits = x.data_ptr(), dy.data_ptr(), out.data_ptr(), splits
+    prog = cnn.CnnProgram([(_lib.CNN[kind], (ntile, stages), [cs])], 0)
+    prog.run(torch.cuda.current_stream().cuda_stream, graph=False)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape", PROG_SHAPES)
+def test_prog_fprop_dgrad_wgrad(shape):
+    n, h, w, c, k, r, s, st, pad = shape
+    g, p, q = _geom(*shape)
+    x, wt = _data(n, h, w, c, k, r, s)
+    dy = torch.randn(n, k, p, q, generator=torch.Generator().manual_seed(1)).bfloat16() \
+        .double().cuda()
+    # FPROP
+    ref = _nhwc(F.conv2d(x, wt, stride=st, padding=pad)).reshape(n * p * q, k)
+    out = torch.empty(n * p * q, k, dtype=torch.bfloat16, device="cuda")
+    _prog_conv("CONV_FPROP", g, _nhwc(x).bfloat16(), _w_dev(wt), None, out,
+               min(256, -(-k // 16) * 16))
+    _close(out, ref, 1e-4)
+    # DGRAD
+    ref = _nhwc(torch.nn.grad.conv2d_input(x.shape, wt, dy, stride=st, padding=pad))
+    ref = ref.reshape(n * h * w, c)
+    out = torch.empty(n * h * w, c, dtype=torch.bfloat16, device="cuda")
+    _prog_conv("CONV_DGRAD", g, None, _wt_dev(wt), _nhwc(dy).bfloat16(), out,
+               min(256, -(-c // 16) * 16))
+    _close(out, ref, 1e-4)
+    # WGRAD (split over pixels: splits chosen so every split is non-empty)
+    ref = torch.nn.grad.conv2d_weight(x, wt.shape, dy, stride=st, padding=pad)
+    ref = ref.permute(0, 2, 3, 1).reshape(k, r * s * c)
+    kpad = _rup(r * s * c, 64)
+    pix = n * p * q
+    for splits in (1, 2):
+        kper = _rup(-(-pix // splits), 64)
+        if -(-pix // kper) != splits:
+            continue
+        outw = torch.zeros(splits, k, kpad, device="cuda")
+        _prog_conv("CONV_WGRAD", g, _nhwc(x).bfloat16(), None, _nhwc(dy).bfloat16(), outw,
+                   128, splits)
+        got = outw.double().sum(0)[:, :r * s * c]
+        _close(got, ref, 1e-5, bf16_out=False)
