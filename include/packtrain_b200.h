@@ -343,7 +343,7 @@ typedef struct pk_cnn_bn {
   float* run_mean;        /* STATS: running statistics (torch momentum rule) or NULL */
   float* run_var;
   float* ws;              /* partials workspace (see rpb) */
-  int32_t* counter;       /* zero-initialised; reset by the kernel */
+  int32_t* counter;       /* int32[17], zero-initialised; the kernels reset it */
   int32_t* flag;          /* member's non-finite flag */
   int32_t rows, c, ldx, ldo, ldr, ldd, ldx2;
   int32_t act;            /* PK_CNN_ACT_* */
@@ -351,8 +351,9 @@ typedef struct pk_cnn_bn {
   int32_t res_accumulate; /* BWD_APPLY: dres += */
   int32_t use_running;    /* APPLY: normalise with running stats (eval) */
   float eps, momentum;
-  int32_t rpb;            /* STATS / BWD_REDUCE: rows per partial block (multiple of 32);
-                             ws >= 2*c*ceil(rows/rpb) floats + 2*c doubles */
+  int32_t rpb;            /* STATS / BWD_REDUCE: rows per partial block (multiple of 32),
+                             ceil(rows/rpb) <= 256; ws >= nblk*2c floats + (ceil(nblk/16)
+                             + 1)*2c doubles (+1 float of alignment) */
   int32_t pad0;
 } pk_cnn_bn;
 
@@ -367,8 +368,8 @@ typedef struct pk_cnn_dw {
   int32_t* counter;
   int32_t* flag;
   int32_t n, h, w, c, r, s, stride, pad, p, q, ldx, ldy;
-  int32_t ppb;            /* WGRAD: output pixels per partial block; ws >= r*s*c *
-                             ceil(n*p*q/ppb) floats + r*s*c doubles */
+  int32_t ppb;            /* WGRAD: output pixels per partial block (<= 256 blocks);
+                             ws as pk_cnn_bn with r*s*c outputs; counter int32[17] */
   int32_t pad0;
 } pk_cnn_dw;
 

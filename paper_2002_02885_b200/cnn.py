@@ -408,23 +408,27 @@ class DeviceConvDataset:
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
-def rows_per_block(rows, nout=0):
-    """Rows per partial block of a column reduction with `nout` outputs per
-    block: a function of the member's own shape only (K-invariant).  The last
-    block sums nblk x nout partials alone, so nblk is capped at ~8192 / nout
-    (and at 128), at least 32 rows per block."""
-    target = max(4, min(128, 8192 // max(nout, 1)))
-    return max(32, rup(cdiv(rows, target), 32))
+def rows_per_block(rows, c=8, per_thread=4):
+    """Rows per partial block of a column reduction over `c` channels: a
+    function of the member's own shape only (K-invariant).  Each of a block's
+    256/pow2(c/8) row lanes sums ~`per_thread` rows; at most 256 blocks (the
+    kernels' two-level ticket tree); a multiple of 32."""
+    cgp = 1
+    while cgp < max(1, c // 8):
+        cgp *= 2
+    lanes = max(1, 256 // cgp)
+    return rup(max(32, lanes * per_thread, cdiv(rows, 256)), 32)
 
 
 def red_blocks_max(rows, nout):
-    """upper bound of cdiv(r, rows_per_block(r, nout)) over r <= rows (ws sizing)"""
-    return min(max(4, min(128, 8192 // max(nout, 1))), cdiv(rows, 32))
+    """upper bound of cdiv(r, rows_per_block(r)) over r <= rows (ws sizing)"""
+    return min(256, cdiv(rows, 32))
 
 
 def _red_ws(nout_per_blk, nblk, nout):
-    """floats for nblk partial records + an fp64 total area of nout doubles."""
-    return rup(nout_per_blk * nblk, 2) + 2 * nout + 2
+    """floats for nblk partial records + fp64 group records and totals
+    (tree_reduce in csrc/pk_cnn_ops.cuh)."""
+    return rup(nout_per_blk * nblk, 2) + 2 * nout * (cdiv(nblk, 16) + 1) + 2
 
 
 def _pick_ntile(n, cap=256):
@@ -625,7 +629,7 @@ class ConvPack:
                 _, splits = _wgrad_cfg(ty.c, op.a["r"] * op.a["s"] * tx.c, b * ty.h * ty.w)
                 if splits > 1:
                     A["split"][op.name] = z(splits * W.numel)
-        A["counters"] = z(4 * len(net.ops) + 4, dt=torch.int32)
+        A["counters"] = z(17 * (4 * len(net.ops) + 4), dt=torch.int32)
         return A
 
     # -- state transfer ------------------------------------------------------------
@@ -705,8 +709,9 @@ class ConvPack:
 
     # -- program construction -------------------------------------------------------
     def _counter(self, k, slot):
+        """int32[17] ticket counters of (op, slot) of member k (tree_reduce)"""
         c = self.acts[k]["counters"]
-        return c.data_ptr() + 4 * slot
+        return c.data_ptr() + 4 * 17 * slot
 
     def _flag(self, k):
         return self.state.data_ptr() + 16 * k + 4
@@ -804,7 +809,7 @@ class ConvPack:
         b.counter = self._counter(k, 4 * net.ops.index(op))
         b.flag = self._flag(k)
         b.rows, b.c = rows, tx.c
-        b.rpb = rows_per_block(rows, 2 * tx.c)
+        b.rpb = rows_per_block(rows, tx.c)
         b.ldx = b.ldo = b.ldr = b.ldd = b.ldx2 = tx.c
         b.act = CNN_ACT[op.a["act"]]
         b.eps, b.momentum = _BN_EPS, _BN_MOMENTUM
@@ -827,7 +832,7 @@ class ConvPack:
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
         d.ldx, d.ldy = tx.c, ty.c
-        d.ppb = rows_per_block(take * ty.h * ty.w, op.a["r"] * op.a["s"] * tx.c)
+        d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
         return d
 
     def _pool_struct(self, k, op, take):

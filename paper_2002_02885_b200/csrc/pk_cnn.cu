@@ -208,6 +208,8 @@ int prob_blocks(int kind, const void* pr) {
   return 0;
 }
 
+int head_blocks(int, const void*) { return 1; }  // XENT: one block per member
+
 std::string check_prob(int kind, const void* pr) {
   auto c8 = [](int c) { return c > 0 && c % 8 == 0 && c <= 2048; };
   switch (kind) {
@@ -217,8 +219,9 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_BN_BWD_APPLY: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
       if (!c8(P.c) || P.rows <= 0) return "bn: channels must be a multiple of 8 in [8, 2048]";
-      if ((kind == PK_CNN_BN_STATS || kind == PK_CNN_BN_BWD_REDUCE) && (P.rpb < 1 || P.rpb % 32))
-        return "bn: rows per block must be a positive multiple of 32";
+      if ((kind == PK_CNN_BN_STATS || kind == PK_CNN_BN_BWD_REDUCE) &&
+          (P.rpb < 1 || P.rpb % 32 || cdiv(P.rows, P.rpb) > cnn::kRedMaxBlocks))
+        return "bn: rows per block must be a positive multiple of 32, <= 256 blocks";
       break;
     }
     case PK_CNN_DW_FPROP:
@@ -226,7 +229,9 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
-      if (kind == PK_CNN_DW_WGRAD && P.ppb < 1) return "dw: pixels per block >= 1";
+      if (kind == PK_CNN_DW_WGRAD &&
+          (P.ppb < 1 || cdiv((long long)P.n * P.p * P.q, P.ppb) > cnn::kRedMaxBlocks))
+        return "dw: pixels per block >= 1, <= 256 blocks";
       break;
     }
     case PK_CNN_MAXPOOL_FWD:
@@ -239,7 +244,8 @@ std::string check_prob(int kind, const void* pr) {
     }
     case PK_CNN_BIAS_ACT_BWD: {
       const pk_cnn_bias& P = *static_cast<const pk_cnn_bias*>(pr);
-      if (!c8(P.c) || P.rpb < 1) return "bias: channels % 8 in [8, 2048], rows per block >= 1";
+      if (!c8(P.c) || P.rpb < 1 || cdiv(P.rows, P.rpb) > cnn::kRedMaxBlocks)
+        return "bias: channels % 8 in [8, 2048], <= 256 row blocks";
       break;
     }
     case PK_CNN_XENT: {
@@ -265,9 +271,30 @@ std::string check_prob(int kind, const void* pr) {
 struct OpRec {
   int kind = 0, nprob = 0, nblocks = 0;
   int ntile = 0, stages = 0;
-  size_t probs_off = 0, blk_off = 0;  // offsets into the device descriptor block
+  size_t probs_off = 0, blk_off = 0;  // offsets into the device descriptor block (OPT, COMMIT)
   std::vector<cg::Launch> conv;       // conv ops: launches of <= kMaxProblems problems
+  // other kinds: parameter packs of <= cnn::kPack problems (raw cnn::Pack<T> bytes)
+  std::vector<std::vector<uint8_t>> packs;
+  std::vector<int> pack_blocks;
 };
+
+// split one op's problems into kernel-parameter packs of <= kPack problems
+template <class T>
+void make_packs(OpRec& r, const T* pr, int n, int (*blocks)(int, const void*)) {
+  for (int i0 = 0; i0 < n; i0 += cnn::kPack) {
+    cnn::Pack<T> P;
+    memset(&P, 0, sizeof(P));
+    P.nprob = std::min(cnn::kPack, n - i0);
+    for (int j = 0; j < P.nprob; ++j) {
+      P.p[j] = pr[i0 + j];
+      P.blk0[j + 1] = P.blk0[j] + blocks(r.kind, &pr[i0 + j]);
+    }
+    std::vector<uint8_t> raw(sizeof(P));
+    memcpy(raw.data(), &P, sizeof(P));
+    r.packs.push_back(std::move(raw));
+    r.pack_blocks.push_back(P.blk0[P.nprob]);
+  }
+}
 
 }  // namespace
 
@@ -402,6 +429,19 @@ const int* db(const pk_cnn_prog* g, const OpRec& o) {
   return reinterpret_cast<const int*>(g->dmem + o.blk_off);
 }
 
+template <class T>
+cudaError_t launch_packs(const OpRec& o, void (*kern)(cnn::Pack<T>), cudaStream_t st,
+                         int smem = 0) {
+  for (size_t i = 0; i < o.packs.size(); ++i) {
+    if (o.pack_blocks[i] == 0) continue;
+    kern<<<o.pack_blocks[i], cnn::kBlock, smem, st>>>(
+        *reinterpret_cast<const cnn::Pack<T>*>(o.packs[i].data()));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
   using namespace cnn;
   const int nb = o.nblocks, np = o.nprob;
@@ -424,41 +464,23 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
         if (e != cudaSuccess) return e;
       }
       return cudaSuccess;
-    case PK_CNN_BN_STATS: k_bn_stats<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np); break;
-    case PK_CNN_BN_APPLY: k_bn_apply<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np); break;
-    case PK_CNN_BN_BWD_REDUCE:
-      k_bn_bwd_reduce<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_BN_BWD_APPLY:
-      k_bn_bwd_apply<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bn>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_DW_FPROP: k_dw_fprop<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
-    case PK_CNN_DW_DGRAD: k_dw_dgrad<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
-    case PK_CNN_DW_WGRAD: k_dw_wgrad<<<nb, kBlock, 0, st>>>(dp<pk_cnn_dw>(g, o), db(g, o), np); break;
-    case PK_CNN_MAXPOOL_FWD:
-      k_maxpool_fwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_MAXPOOL_BWD:
-      k_maxpool_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_AVGPOOL_FWD:
-      k_avgpool_fwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_AVGPOOL_BWD:
-      k_avgpool_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_pool>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_XENT: k_xent<<<np, kBlock, o.ntile, st>>>(dp<pk_cnn_head>(g, o), np); break;
-    case PK_CNN_BIAS_ACT_BWD:
-      k_bias_act_bwd<<<nb, kBlock, 0, st>>>(dp<pk_cnn_bias>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_SPLIT_REDUCE:
-      k_split_reduce<<<nb, kBlock, 0, st>>>(dp<pk_cnn_reduce>(g, o), db(g, o), np);
-      break;
+    case PK_CNN_BN_STATS: return launch_packs<pk_cnn_bn>(o, k_bn_stats, st);
+    case PK_CNN_BN_APPLY: return launch_packs<pk_cnn_bn>(o, k_bn_apply, st);
+    case PK_CNN_BN_BWD_REDUCE: return launch_packs<pk_cnn_bn>(o, k_bn_bwd_reduce, st);
+    case PK_CNN_BN_BWD_APPLY: return launch_packs<pk_cnn_bn>(o, k_bn_bwd_apply, st);
+    case PK_CNN_DW_FPROP: return launch_packs<pk_cnn_dw>(o, k_dw_fprop, st);
+    case PK_CNN_DW_DGRAD: return launch_packs<pk_cnn_dw>(o, k_dw_dgrad, st);
+    case PK_CNN_DW_WGRAD: return launch_packs<pk_cnn_dw>(o, k_dw_wgrad, st);
+    case PK_CNN_MAXPOOL_FWD: return launch_packs<pk_cnn_pool>(o, k_maxpool_fwd, st);
+    case PK_CNN_MAXPOOL_BWD: return launch_packs<pk_cnn_pool>(o, k_maxpool_bwd, st);
+    case PK_CNN_AVGPOOL_FWD: return launch_packs<pk_cnn_pool>(o, k_avgpool_fwd, st);
+    case PK_CNN_AVGPOOL_BWD: return launch_packs<pk_cnn_pool>(o, k_avgpool_bwd, st);
+    case PK_CNN_XENT: return launch_packs<pk_cnn_head>(o, k_xent, st, o.ntile);
+    case PK_CNN_BIAS_ACT_BWD: return launch_packs<pk_cnn_bias>(o, k_bias_act_bwd, st);
+    case PK_CNN_SPLIT_REDUCE: return launch_packs<pk_cnn_reduce>(o, k_split_reduce, st);
     case PK_CNN_OPT: k_opt<<<nb, kBlock, 0, st>>>(dp<pk_cnn_opt_seg>(g, o), db(g, o), np); break;
-    case PK_CNN_PUBLISH_T:
-      k_publish_t<<<nb, kBlock, 0, st>>>(dp<pk_cnn_tpose>(g, o), db(g, o), np);
-      break;
-    case PK_CNN_GATHER: k_gather<<<nb, kBlock, 0, st>>>(dp<pk_cnn_gather>(g, o), db(g, o), np); break;
+    case PK_CNN_PUBLISH_T: return launch_packs<pk_cnn_tpose>(o, k_publish_t, st);
+    case PK_CNN_GATHER: return launch_packs<pk_cnn_gather>(o, k_gather, st);
     case PK_CNN_COMMIT:
       k_commit<<<cdiv(np, 128), 128, 0, st>>>(dp<pk_cnn_commit>(g, o), np, o.ntile);
       break;
@@ -529,11 +551,50 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
     }
     r.nblocks = blk[op.nprob];
     if (op.kind == PK_CNN_COMMIT) r.ntile = op.cfg0;  // mode
-    if (op.kind == PK_CNN_XENT) {
-      int mx = 0;
-      for (int j = 0; j < op.nprob; ++j)
-        mx = std::max(mx, reinterpret_cast<const pk_cnn_head*>(src)[j].rows);
-      r.ntile = mx * 16;  // dynamic smem bytes
+    if (op.kind != PK_CNN_OPT && op.kind != PK_CNN_COMMIT) {
+      if (op.kind == PK_CNN_XENT) {
+        int mx = 0;
+        for (int j = 0; j < op.nprob; ++j)
+          mx = std::max(mx, reinterpret_cast<const pk_cnn_head*>(src)[j].rows);
+        r.ntile = mx * 16;  // dynamic smem bytes
+      }
+      switch (op.kind) {
+        case PK_CNN_BN_STATS:
+        case PK_CNN_BN_APPLY:
+        case PK_CNN_BN_BWD_REDUCE:
+        case PK_CNN_BN_BWD_APPLY:
+          make_packs(r, static_cast<const pk_cnn_bn*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_DW_FPROP:
+        case PK_CNN_DW_DGRAD:
+        case PK_CNN_DW_WGRAD:
+          make_packs(r, static_cast<const pk_cnn_dw*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_MAXPOOL_FWD:
+        case PK_CNN_MAXPOOL_BWD:
+        case PK_CNN_AVGPOOL_FWD:
+        case PK_CNN_AVGPOOL_BWD:
+          make_packs(r, static_cast<const pk_cnn_pool*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_XENT:
+          make_packs(r, static_cast<const pk_cnn_head*>(op.probs), op.nprob, head_blocks);
+          break;
+        case PK_CNN_BIAS_ACT_BWD:
+          make_packs(r, static_cast<const pk_cnn_bias*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_SPLIT_REDUCE:
+          make_packs(r, static_cast<const pk_cnn_reduce*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_PUBLISH_T:
+          make_packs(r, static_cast<const pk_cnn_tpose*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_GATHER:
+          make_packs(r, static_cast<const pk_cnn_gather*>(op.probs), op.nprob, prob_blocks);
+          break;
+      }
+      g->launches += (int)r.packs.size();
+      g->ops.push_back(std::move(r));
+      continue;
     }
     align(64);
     r.probs_off = host.size();

@@ -11,8 +11,8 @@
 // bias and depthwise weight gradients, the softmax head) sums a fixed row
 // partition of the member's own rows in a fixed order: per-block fp32 partial
 // sums over `rpb` rows (chosen by the planner from the member's own row count)
-// → workspace → the last block to finish (atomic ticket) adds the partials in
-// fp64 along a fixed lane split.  Results depend only on the member's shape,
+// → workspace → a two-level ticket tree (tree_reduce) adds them in fp64 in
+// block order.  Results depend only on the member's shape,
 // never on which members share the launch, so packed == standalone bit for bit.
 #pragma once
 #include <cuda_bf16.h>
@@ -29,6 +29,27 @@ __device__ __forceinline__ int find_prob(const int* blk0, int nprob, int b) {
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (__ldg(blk0 + mid) <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Up to kPack problems of one launch travel in the kernel parameters (constant
+// bank): a block's problem lookup and descriptor reads are then cached
+// constant loads instead of a dependent chain of global loads.
+constexpr int kPack = 16;
+template <class T>
+struct Pack {
+  int nprob;
+  int blk0[kPack + 1];
+  T p[kPack];
+};
+template <class T>
+__device__ __forceinline__ int pack_prob(const Pack<T>& G, int b) {
+  int lo = 0, hi = G.nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (G.blk0[mid] <= b) lo = mid;
     else hi = mid - 1;
   }
   return lo;
@@ -77,20 +98,6 @@ __device__ __forceinline__ float act_bwd(float out, int act) {
   return 1.f;
 }
 
-// last-block ticket: true in exactly one block, after all blocks' partials are visible
-__device__ __forceinline__ bool last_block(int* counter, int nblk) {
-  __shared__ int s_last;
-  __threadfence();  // every thread's partial-sum stores before the block's ticket
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int prev = atomicAdd(counter, 1);
-    s_last = (prev == nblk - 1);
-  }
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last != 0;
-}
-
 // ------------------------------------------------------------------------------
 // Column (channel) partial sums of up to two per-element quantities over rows
 // [r0, r1) of one block.  F(row, ch0, a[8], b[8]) fills the two values of the 8
@@ -100,13 +107,14 @@ template <class F>
 __device__ __forceinline__ void col_partials(int r0, int r1, int c, int blk, float* ws, F f) {
   __shared__ float sh[2][2048];
   const int cgs = c >> 3;
-  const int nr = kBlock / cgs;  // row lanes (cgs <= 256)
-  const int t = threadIdx.x;
-  const int rl = t / cgs, j = t - rl * cgs;
+  int cgp = 1;  // channel groups rounded up to a power of two (<= 256)
+  while (cgp < cgs) cgp <<= 1;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int j = t & (cgp - 1), rl = t / cgp, nr = kBlock / cgp;
   float s1[8], s2[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
-  if (rl < nr) {
+  if (j < cgs) {
 #pragma unroll 4
     for (int r = r0 + rl; r < r1; r += nr) {
       float a[8], b[8];
@@ -118,98 +126,121 @@ __device__ __forceinline__ void col_partials(int r0, int r1, int c, int blk, flo
       }
     }
   }
-  // fixed-order combine over the row lanes, 2048/c lanes per pass; thread t
-  // owns channels t, t+256, ... (c <= 2048)
-  const int lanes_per_pass = 2048 / c;
-  float acc1[8], acc2[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc1[q] = acc2[q] = 0.f;
-  for (int base = 0; base < nr; base += lanes_per_pass) {
-    __syncthreads();
-    if (rl < nr && rl >= base && rl < base + lanes_per_pass) {
+  if (cgp <= 32) {
+    // lanes l, l ^ cgp, l ^ 2cgp, ... of a warp share channel group j: fixed xor tree
+    for (int o = 16; o >= cgp; o >>= 1) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        sh[0][(rl - base) * c + 8 * j + e] = s1[e];
-        sh[1][(rl - base) * c + 8 * j + e] = s2[e];
+        s1[e] += __shfl_xor_sync(0xffffffffu, s1[e], o);
+        s2[e] += __shfl_xor_sync(0xffffffffu, s2[e], o);
+      }
+    }
+    if (lane < cgp && j < cgs) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        sh[0][warp * c + 8 * j + e] = s1[e];
+        sh[1][warp * c + 8 * j + e] = s2[e];
       }
     }
     __syncthreads();
-    const int nl = min(lanes_per_pass, nr - base);
+    float* out = ws + (long long)blk * 2 * c;
+    for (int ch = t; ch < c; ch += kBlock) {
+      float a = 0.f, b = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int ch = q * kBlock + t;
-      if (ch < c)
-        for (int l = 0; l < nl; ++l) {
-          acc1[q] += sh[0][l * c + ch];
-          acc2[q] += sh[1][l * c + ch];
-        }
+      for (int w = 0; w < kBlock / 32; ++w) {
+        a += sh[0][w * c + ch];
+        b += sh[1][w * c + ch];
+      }
+      out[ch] = a;
+      out[c + ch] = b;
     }
-  }
-  float* out1 = ws + (long long)blk * 2 * c;
+  } else {
+    // nr (<= 4) row lanes, each a set of whole warps: combine through shared memory
+    if (j < cgs) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int ch = q * kBlock + t;
-    if (ch < c) {
-      out1[ch] = acc1[q];
-      out1[c + ch] = acc2[q];
-    }
-  }
-}
-
-// Last block: tot[i] = Σ_b ws[b*stride + i] for i < nout, in fp64, along a
-// fixed split of the blocks over lanes (thread t: item t % nout, lane t / nout),
-// lanes combined in order.  tot (nout doubles) may live in global memory; it is
-// visible to the whole block on return.
-__device__ __forceinline__ void final_reduce(const float* ws, int nblk, int nout, int stride,
-                                             double* tot) {
-  __shared__ double part[kBlock];
-  const int t = threadIdx.x;
-  if (nout >= kBlock / 2) {
-    for (int i = t; i < nout; i += kBlock) {
-      double s = 0.0;
-#pragma unroll 8
-      for (int b = 0; b < nblk; ++b) s += __ldcg(ws + (long long)b * stride + i);
-      tot[i] = s;
+      for (int e = 0; e < 8; ++e) {
+        sh[0][rl * c + 8 * j + e] = s1[e];
+        sh[1][rl * c + 8 * j + e] = s2[e];
+      }
     }
     __syncthreads();
-    return;
+    float* out = ws + (long long)blk * 2 * c;
+    for (int ch = t; ch < c; ch += kBlock) {
+      float a = 0.f, b = 0.f;
+      for (int l = 0; l < nr; ++l) {
+        a += sh[0][l * c + ch];
+        b += sh[1][l * c + ch];
+      }
+      out[ch] = a;
+      out[c + ch] = b;
+    }
   }
-  const int lanes = min(kBlock / nout, nblk);
-  const int item = t % nout, lane = t / nout;
-  double s = 0.0;
-  if (lane < lanes) {
-#pragma unroll 8
-    for (int b = lane; b < nblk; b += lanes) s += __ldcg(ws + (long long)b * stride + item);
-    part[lane * nout + item] = s;
-  }
-  __syncthreads();
-  if (t < nout) {
-    double v = 0.0;
-    for (int l = 0; l < lanes; ++l) v += part[l * nout + t];
-    tot[t] = v;
-  }
-  __syncthreads();
 }
 
-__device__ __forceinline__ double* tot_area(float* ws, long long floats) {
-  return reinterpret_cast<double*>(ws + ((floats + 1) & ~1LL));
+// Two-level fixed-order reduction of per-block partial records.
+// Every block has written ws[blk*stride + i], i < nout.  Blocks form groups of
+// kRedGroup; the last block of a group to arrive (atomic ticket on
+// counters[1 + group]) sums its group's records in block order into an fp64
+// group record; the last group reducer (ticket on counters[0]) sums the group
+// records in group order into tot[0..nout) and returns true — in exactly one
+// block.  Tickets reset themselves, so the counters are reusable (graph replay).
+// Workspace layout: [nblk*stride floats][ngroups*nout doubles][nout doubles].
+constexpr int kRedGroup = 16;
+constexpr int kRedMaxBlocks = kRedGroup * kRedGroup;  // planner keeps nblk <= this
+
+__device__ __forceinline__ bool ticket(int* counter, int n) {
+  __shared__ int s_last;
+  // the CTA barrier orders every thread's stores before thread 0's gpu-scope
+  // fence + atomic (PTX release cumulativity), so one fence per block suffices
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(counter, 1);
+    s_last = (prev == n - 1);
+    if (s_last) *counter = 0;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+__device__ __forceinline__ bool tree_reduce(float* ws, int blk, int nblk, int nout, int stride,
+                                            int* counters, double** tot_out) {
+  const int ngroups = (nblk + kRedGroup - 1) / kRedGroup;
+  const int grp = blk / kRedGroup;
+  const int b0 = grp * kRedGroup, b1 = min(nblk, b0 + kRedGroup);
+  double* grec = reinterpret_cast<double*>(ws + (((long long)nblk * stride + 1) & ~1LL));
+  double* tot = grec + (long long)ngroups * nout;
+  *tot_out = tot;
+  if (!ticket(counters + 1 + grp, b1 - b0)) return false;
+  for (int i = threadIdx.x; i < nout; i += kBlock) {
+    double v = 0.0;
+    for (int b = b0; b < b1; ++b) v += __ldcg(ws + (long long)b * stride + i);
+    grec[(long long)grp * nout + i] = v;
+  }
+  if (!ticket(counters, ngroups)) return false;
+  for (int i = threadIdx.x; i < nout; i += kBlock) {
+    double v = 0.0;
+    for (int g = 0; g < ngroups; ++g) v += __ldcg(grec + (long long)g * nout + i);
+    tot[i] = v;
+  }
+  __syncthreads();
+  return true;
 }
 
 // ============================== batch norm =====================================
-__global__ void __launch_bounds__(kBlock) k_bn_stats(const pk_cnn_bn* probs, const int* blk0,
-                                                     int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_bn& P = probs[pi];
-  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+__global__ void __launch_bounds__(kBlock, 3) k_bn_stats(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bn& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
   col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     ld8(bptr(P.x, r, P.ldx, ch), a);
 #pragma unroll
     for (int e = 0; e < 8; ++e) b[e] = a[e] * a[e];
   });
-  if (!last_block(P.counter, nblk)) return;
-  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
-  final_reduce(P.ws, nblk, 2 * P.c, 2 * P.c, tot);
+  double* tot;
+  if (!tree_reduce(P.ws, blk, nblk, 2 * P.c, 2 * P.c, P.counter, &tot)) return;
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
     const double mean = tot[ch] / P.rows;
     const double var = fmax(tot[P.c + ch] / P.rows - mean * mean, 0.0);
@@ -221,7 +252,6 @@ __global__ void __launch_bounds__(kBlock) k_bn_stats(const pk_cnn_bn* probs, con
       P.run_var[ch] = (float)((1.0 - P.momentum) * P.run_var[ch] + P.momentum * unb);
     }
   }
-  if (threadIdx.x == 0) *P.counter = 0;
 }
 
 __device__ __forceinline__ void bn_coef(const pk_cnn_bn& P, int ch, float (&mean)[8],
@@ -238,14 +268,13 @@ __device__ __forceinline__ void bn_coef(const pk_cnn_bn& P, int ch, float (&mean
   }
 }
 
-constexpr int kApplyRows = 4;  // rows per thread in the BN apply kernels
+constexpr int kApplyRows = 2;  // rows per thread in the BN apply kernels
 
-__global__ void __launch_bounds__(kBlock) k_bn_apply(const pk_cnn_bn* probs, const int* blk0,
-                                                     int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_bn& P = probs[pi];
+__global__ void __launch_bounds__(kBlock, 4) k_bn_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bn& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long rg = item / cgs;  // group of kApplyRows rows
   if (rg * kApplyRows >= P.rows) return;
   const int ch = 8 * (int)(item - rg * cgs);
@@ -296,11 +325,10 @@ __device__ __forceinline__ void bn_g_xhat(const pk_cnn_bn& P, long long r, int c
   }
 }
 
-__global__ void __launch_bounds__(kBlock) k_bn_bwd_reduce(const pk_cnn_bn* probs,
-                                                          const int* blk0, int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_bn& P = probs[pi];
-  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+__global__ void __launch_bounds__(kBlock, 3) k_bn_bwd_reduce(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bn& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
   col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     float xh[8];
@@ -308,9 +336,8 @@ __global__ void __launch_bounds__(kBlock) k_bn_bwd_reduce(const pk_cnn_bn* probs
 #pragma unroll
     for (int e = 0; e < 8; ++e) b[e] = a[e] * xh[e];
   });
-  if (!last_block(P.counter, nblk)) return;
-  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
-  final_reduce(P.ws, nblk, 2 * P.c, 2 * P.c, tot);
+  double* tot;
+  if (!tree_reduce(P.ws, blk, nblk, 2 * P.c, 2 * P.c, P.counter, &tot)) return;
   bool bad = false;
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
     const double s1 = tot[ch], s2 = tot[P.c + ch];
@@ -321,15 +348,13 @@ __global__ void __launch_bounds__(kBlock) k_bn_bwd_reduce(const pk_cnn_bn* probs
     bad |= !isfinite(s1) || !isfinite(s2);
   }
   if (bad) *P.flag = 1;
-  if (threadIdx.x == 0) *P.counter = 0;
 }
 
-__global__ void __launch_bounds__(kBlock) k_bn_bwd_apply(const pk_cnn_bn* probs,
-                                                         const int* blk0, int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_bn& P = probs[pi];
+__global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bn& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long rg = item / cgs;
   if (rg * kApplyRows >= P.rows) return;
   const int ch = 8 * (int)(item - rg * cgs);
@@ -374,12 +399,11 @@ __global__ void __launch_bounds__(kBlock) k_bn_bwd_apply(const pk_cnn_bn* probs,
 }
 
 // ============================ depthwise conv =====================================
-__global__ void __launch_bounds__(kBlock) k_dw_fprop(const pk_cnn_dw* probs, const int* blk0,
-                                                     int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_dw& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_dw_fprop(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.p * P.q;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -405,12 +429,11 @@ __global__ void __launch_bounds__(kBlock) k_dw_fprop(const pk_cnn_dw* probs, con
   st8(bptr(P.y, m, P.ldy, ch), acc);
 }
 
-__global__ void __launch_bounds__(kBlock) k_dw_dgrad(const pk_cnn_dw* probs, const int* blk0,
-                                                     int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_dw& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_dw_dgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.h * P.w;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -440,15 +463,50 @@ __global__ void __launch_bounds__(kBlock) k_dw_dgrad(const pk_cnn_dw* probs, con
   st8(bptr(P.y, m, P.ldx, ch), acc);
 }
 
+// Σ over a block's row lanes of each thread's 8-channel vector v (thread t owns
+// channel group t % cgp of row lane t / cgp, cgp = pow2 >= c/8), written to
+// out[0..c): fixed xor-shuffle tree inside warps, then warps / lanes in order.
+__device__ __forceinline__ void lane_sum8(float (&v)[8], int c, int cgs, int cgp, float* sh,
+                                          float* out) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int j = t & (cgp - 1), rl = t / cgp, nr = kBlock / cgp;
+  int parts;
+  if (cgp <= 32) {
+    for (int o = 16; o >= cgp; o >>= 1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] += __shfl_xor_sync(0xffffffffu, v[e], o);
+    }
+    if (lane < cgp && j < cgs) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sh[warp * c + 8 * j + e] = v[e];
+    }
+    parts = kBlock / 32;
+  } else {
+    if (j < cgs) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sh[rl * c + 8 * j + e] = v[e];
+    }
+    parts = nr;
+  }
+  __syncthreads();
+  for (int ch = t; ch < c; ch += kBlock) {
+    float a = 0.f;
+    for (int w = 0; w < parts; ++w) a += sh[w * c + ch];
+    out[ch] = a;
+  }
+  __syncthreads();
+}
+
 // dw[tap][c] = Σ_pix dy[pix][c] · x[im2col(pix, tap)][c]
-__global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, const int* blk0,
-                                                     int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_dw& P = probs[pi];
-  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+__global__ void __launch_bounds__(kBlock) k_dw_wgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int taps = P.r * P.s;  // <= 9
-  const int cgs = P.c >> 3, nr = kBlock / cgs;
-  const int t = threadIdx.x, rl = t / cgs, j = t - rl * cgs, ch = 8 * j;
+  const int cgs = P.c >> 3;
+  int cgp = 1;
+  while (cgp < cgs) cgp <<= 1;
+  const int t = threadIdx.x, j = t & (cgp - 1), rl = t / cgp, nr = kBlock / cgp, ch = 8 * j;
   const int pq = P.p * P.q;
   const long long M = (long long)P.n * pq;
   const long long m0 = (long long)blk * P.ppb, m1 = min(M, m0 + P.ppb);
@@ -457,7 +515,7 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, con
   for (int k = 0; k < 9; ++k)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
-  if (rl < nr) {
+  if (j < cgs) {
     for (long long m = m0 + rl; m < m1; m += nr) {
       const int n = (int)(m / pq), rem = (int)(m - (long long)n * pq);
       const int oy = rem / P.q, ox = rem - oy * P.q;
@@ -477,51 +535,29 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const pk_cnn_dw* probs, con
     }
   }
   __shared__ float sh[2048];
-  const int lanes_per_pass = 2048 / P.c;
   float* out = P.ws + (long long)blk * taps * P.c;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     if (k >= taps) break;
-    float tot[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) tot[q] = 0.f;
-    for (int base = 0; base < nr; base += lanes_per_pass) {
-      __syncthreads();
-      if (rl < nr && rl >= base && rl < base + lanes_per_pass) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sh[(rl - base) * P.c + ch + e] = acc[k][e];
-      }
-      __syncthreads();
-      const int nl = min(lanes_per_pass, nr - base);
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q * kBlock + t < P.c)
-          for (int l = 0; l < nl; ++l) tot[q] += sh[l * P.c + q * kBlock + t];
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q * kBlock + t < P.c) out[k * P.c + q * kBlock + t] = tot[q];
+    lane_sum8(acc[k], P.c, cgs, cgp, sh, out + k * P.c);
   }
-  if (!last_block(P.counter, nblk)) return;
   const int nout = taps * P.c;
-  double* tot = tot_area(P.ws, (long long)nblk * nout);
-  final_reduce(P.ws, nblk, nout, nout, tot);
+  double* tot;
+  if (!tree_reduce(P.ws, blk, nblk, nout, nout, P.counter, &tot)) return;
   bool bad = false;
   for (int i = threadIdx.x; i < nout; i += kBlock) {
     P.dw[i] = (float)tot[i];
     bad |= !isfinite(tot[i]);
   }
   if (bad) *P.flag = 1;
-  if (threadIdx.x == 0) *P.counter = 0;
 }
 
 // ================================ pooling ========================================
-__global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const pk_cnn_pool* probs, const int* blk0,
-                                                        int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_pool& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.p * P.q;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -558,12 +594,11 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const pk_cnn_pool* probs
   *reinterpret_cast<uint2*>(P.arg + m * P.c + ch) = a;
 }
 
-__global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const pk_cnn_pool* probs, const int* blk0,
-                                                        int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_pool& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.h * P.w;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -603,12 +638,11 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const pk_cnn_pool* probs
   st8(bptr(P.dx, m, P.ldx, ch), acc);
 }
 
-__global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const pk_cnn_pool* probs, const int* blk0,
-                                                        int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_pool& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.p * P.q;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -636,12 +670,11 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const pk_cnn_pool* probs
   st8(bptr(P.y, m, P.ldy, ch), acc);
 }
 
-__global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const pk_cnn_pool* probs, const int* blk0,
-                                                        int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_pool& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.h * P.w;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -681,8 +714,8 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const pk_cnn_pool* probs
 
 // ======================== softmax cross-entropy head ============================
 // one block per member; reference engine.py:211-230 (loss) and :252-264 (dlogits)
-__global__ void __launch_bounds__(kBlock) k_xent(const pk_cnn_head* probs, int nprob) {
-  const pk_cnn_head& P = probs[blockIdx.x];
+__global__ void __launch_bounds__(kBlock) k_xent(const __grid_constant__ Pack<pk_cnn_head> G) {
+  const pk_cnn_head& P = G.p[blockIdx.x];
   extern __shared__ float xs[];
   float* rmax = xs;
   float* rsum = xs + P.rows;
@@ -741,11 +774,10 @@ __global__ void __launch_bounds__(kBlock) k_xent(const pk_cnn_head* probs, int n
 }
 
 // =================== bias + activation backward (LeNet layers) =====================
-__global__ void __launch_bounds__(kBlock) k_bias_act_bwd(const pk_cnn_bias* probs, const int* blk0,
-                                                         int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_bias& P = probs[pi];
-  const int blk = blockIdx.x - blk0[pi], nblk = blk0[pi + 1] - blk0[pi];
+__global__ void __launch_bounds__(kBlock, 3) k_bias_act_bwd(const __grid_constant__ Pack<pk_cnn_bias> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bias& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
   col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
     ld8(bptr(P.dy, r, P.ld, ch), a);
@@ -759,24 +791,21 @@ __global__ void __launch_bounds__(kBlock) k_bias_act_bwd(const pk_cnn_bias* prob
 #pragma unroll
     for (int e = 0; e < 8; ++e) b[e] = 0.f;
   });
-  if (!last_block(P.counter, nblk)) return;
-  double* tot = tot_area(P.ws, (long long)nblk * 2 * P.c);
-  final_reduce(P.ws, nblk, P.c, 2 * P.c, tot);
+  double* tot;
+  if (!tree_reduce(P.ws, blk, nblk, P.c, 2 * P.c, P.counter, &tot)) return;
   bool bad = false;
   for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
     P.dbias[ch] = (float)tot[ch];
     bad |= !isfinite(tot[ch]);
   }
   if (bad) *P.flag = 1;
-  if (threadIdx.x == 0) *P.counter = 0;
 }
 
 // ========================== WGRAD split reduction ================================
-__global__ void __launch_bounds__(kBlock) k_split_reduce(const pk_cnn_reduce* probs,
-                                                         const int* blk0, int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_reduce& P = probs[pi];
-  const long long i4 = (long long)(blockIdx.x - blk0[pi]) * kBlock + threadIdx.x;
+__global__ void __launch_bounds__(kBlock) k_split_reduce(const __grid_constant__ Pack<pk_cnn_reduce> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_reduce& P = G.p[pi];
+  const long long i4 = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   if (i4 * 4 >= P.len) return;
   float4 s = __ldcg(reinterpret_cast<const float4*>(P.src) + i4);
   for (int j = 1; j < P.splits; ++j) {
@@ -841,12 +870,11 @@ __global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, cons
 }
 
 // ================= transposed bf16 weights for DGRAD (B operand) ===================
-__global__ void __launch_bounds__(kBlock) k_publish_t(const pk_cnn_tpose* probs, const int* blk0,
-                                                      int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_tpose& P = probs[pi];
+__global__ void __launch_bounds__(kBlock) k_publish_t(const __grid_constant__ Pack<pk_cnn_tpose> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_tpose& P = G.p[pi];
   const int tk = (P.k + 31) / 32, tc = (P.c + 31) / 32;
-  int b = blockIdx.x - blk0[pi];
+  int b = blockIdx.x - G.blk0[pi];
   const int tap = b / (tk * tc);
   b -= tap * tk * tc;
   const int kt = b / tc, ct = b - kt * tc;
@@ -892,11 +920,10 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
 
 // batch gather: one block per 4 KB of rows, 16-byte vectors
 constexpr int kGatherChunk = 4096;
-__global__ void __launch_bounds__(kBlock) k_gather(const pk_cnn_gather* probs, const int* blk0,
-                                                   int nprob) {
-  const int pi = find_prob(blk0, nprob, blockIdx.x);
-  const pk_cnn_gather& P = probs[pi];
-  const long long v0 = (long long)(blockIdx.x - blk0[pi]) * (kGatherChunk / 16);
+__global__ void __launch_bounds__(kBlock) k_gather(const __grid_constant__ Pack<pk_cnn_gather> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_gather& P = G.p[pi];
+  const long long v0 = (long long)(blockIdx.x - G.blk0[pi]) * (kGatherChunk / 16);
   const long long vrow = P.row_bytes / 16, total = vrow * P.rows;
   for (long long v = v0 + threadIdx.x; v < min(total, v0 + kGatherChunk / 16); v += kBlock) {
     const long long r = v / vrow, c = v - r * vrow;
