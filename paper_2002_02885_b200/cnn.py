@@ -445,10 +445,15 @@ def _stages(ntile, budget=110 * 1024):
 
 
 def _wgrad_cfg(k, rsc, pix):
-    ntile = 128 if rsc <= 128 else 256
-    if rsc <= 64:
+    """(N tile, pixel splits) of a WGRAD problem from the member's own shape.
+    co <= 64: the swapped orientation (GEMM M = r·s·c, N = co, N tile 64);
+    else M = co, N = r·s·c with 128-wide tiles (two persistent CTAs per SM)."""
+    if k <= 64:
         ntile = 64
-    base = cdiv(k, 128) * cdiv(rsc, ntile)
+        base = cdiv(rsc, 128)
+    else:
+        ntile = 64 if rsc <= 64 else 128
+        base = cdiv(k, 128) * cdiv(rsc, ntile)
     want = max(1, min(pix // 1024, cdiv(2 * 148, base)))
     kper = rup(cdiv(pix, want), 64)
     splits = cdiv(pix, kper)

@@ -390,6 +390,11 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
                                     g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, 64);
           if (!ok || !make_map_2d(&L.tmA[j], g.dy, (uint64_t)pix, g.k, g.ldy, 64))
             return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
+          if (g.k <= 64 && ntile == 64) {  // swapped orientation (see cg::Problem::swap)
+            p.swap = 1;
+            p.M = g.r * g.s * g.c;
+            p.N = g.k;
+          }
         }
         p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
         p.OH = g.p; p.OW = g.q; p.ald = g.ldy;
@@ -402,6 +407,19 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
       tiles += p.tiles_m * p.tiles_n * p.splits;
     }
     L.total_tiles = tiles;
+    // persistent when every problem's operands come by TMA (the epilogue warps are free)
+    bool all_tma = true;
+    for (int j = 0; j < L.nprob; ++j)
+      all_tma = all_tma && (kind == PK_CNN_CONV_WGRAD ? L.p[j].b_mode != 0 : L.p[j].a_mode != 0);
+    if (all_tma && tiles > 0) {
+      static int sms = 0;
+      if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      const int per_sm = 2 * ntile <= 256 ? 2 : 1;  // TMEM: 2 x NT columns per CTA
+      const size_t budget = (size_t)(227 * 1024) / per_sm - 2048;
+      L.stages = (int)std::min<size_t>(8, budget / cg::stage_bytes(ntile));
+      L.persistent = 1;
+      L.grid = std::min(tiles, per_sm * std::max(sms, 1));
+    }
     out.push_back(L);
   }
   return PK_OK;
@@ -409,8 +427,19 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
 
 template <int MODE>
 cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
-  static bool attr_set = false;
+  static bool attr_set = false, attr_set_p = false;
   if (L.total_tiles == 0) return cudaSuccess;
+  if (L.persistent) {
+    if (!attr_set_p) {
+      cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_p<MODE>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr_set_p = true;
+    }
+    cg::k_conv_gemm_p<MODE>
+        <<<L.grid, cg::kThreads, cg::smem_bytes(L.ntile, L.stages), st>>>(L);
+    return cudaGetLastError();
+  }
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -59,6 +59,8 @@ struct Problem {
                               //   2 TMA im2col (FPROP/DGRAD: A; WGRAD: A=dY is TMA 2-D
                               //   whenever b_mode != 0)
   int b_mode;                 // WGRAD X operand: 0 gather, 1 TMA 2-D tile, 2 TMA im2col
+  int swap;                   // WGRAD (TMA, co <= 64): GEMM M = (r,s,c), N = co, so the
+                              //   M = 128 MMA is not half empty; dst written transposed
   long long dseg;             // elements between dst segments
   long long split_stride;     // WGRAD: elements between split partials
 };
@@ -69,13 +71,223 @@ struct Launch {
   Problem p[kMaxProblems];
   int nprob;
   int ntile;   // N tile: multiple of 16 in [16, 256] (multiple of 64 for WGRAD)
-  int stages;  // 2..6
+  int stages;  // pipeline depth
   int total_tiles;
+  int persistent;  // every problem TMA-fed: k_conv_gemm_p, grid < total_tiles
+  int grid;
 };
 
 __host__ __device__ inline uint32_t stage_bytes(int ntile) { return 16384u + (uint32_t)ntile * 128u; }
 __host__ inline size_t smem_bytes(int ntile, int stages) {
-  return 1024 + (size_t)stages * stage_bytes(ntile) + 8 * (2 * stages + 1) + 16;
+  return 1024 + (size_t)stages * stage_bytes(ntile) + 8 * (2 * stages + 4) + 16;
+}
+
+// Issue the TMA loads of one 64-deep k-block (reduction offset kk) of tile
+// (tm, tn) of problem pi into one pipeline stage, completing on `bar`.
+//   FPROP/DGRAD: B = weights (2-D), and A when tma_all (2-D tile or im2col);
+//   WGRAD (tma_all only): A = dY (2-D, two 64-wide M atoms), B = X (2-D or
+//   im2col, NT/64 N atoms).
+template <int MODE>
+__device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int tn, int kk,
+                                           bool tma_all, uint8_t* stage, uint64_t* bar, int NT) {
+  const Problem& P = L.p[pi];
+  const int ohw = P.OH * P.OW;
+  if (MODE == WGRAD) {
+    umma::mbar_arrive_expect_tx(bar, 16384u + (uint32_t)NT * 128u);
+    uint8_t* b_s = stage + 16384;
+    const int img = kk / ohw, rem = kk - img * ohw;
+    const int py = rem / P.OW, px = rem - py * P.OW;
+    // one 64-wide atom of the X operand: columns n .. n+63 of (r, s, c)
+    auto x_atom = [&](uint8_t* dst, int n) {
+      if (P.b_mode == 1) {
+        tc::tma_load_2d(dst, &L.tm[pi], n, kk, bar);
+      } else {
+        const int tap = n / P.SC, c0 = n - tap * P.SC;
+        const int fr = tap / P.S, fs = tap - fr * P.S;
+        tc::tma_im2col_4d(dst, &L.tm[pi], c0, px * P.stride - P.pad, py * P.stride - P.pad, img,
+                          (uint16_t)fs, (uint16_t)fr, bar);
+      }
+    };
+    if (P.swap) {  // A = X (M = (r,s,c)), B = dY (N = co)
+      x_atom(stage, tm * BM);
+      x_atom(stage + 8192, tm * BM + 64);
+      for (int j = 0; j < NT / 64; ++j) tc::tma_load_2d(b_s + j * 8192, &L.tmA[pi], tn * NT + j * 64, kk, bar);
+    } else {       // A = dY (M = co), B = X (N = (r,s,c))
+      tc::tma_load_2d(stage, &L.tmA[pi], tm * BM, kk, bar);
+      tc::tma_load_2d(stage + 8192, &L.tmA[pi], tm * BM + 64, kk, bar);
+      for (int j = 0; j < NT / 64; ++j) x_atom(b_s + j * 8192, tn * NT + j * 64);
+    }
+    return;
+  }
+  umma::mbar_arrive_expect_tx(bar, (uint32_t)NT * 128u + (tma_all ? 16384u : 0u));
+  const int m0 = tm * BM;
+  if (P.a_mode == 1) {
+    tc::tma_load_2d(stage, &L.tmA[pi], kk, m0, bar);
+  } else if (P.a_mode == 2) {
+    const int img = m0 / ohw, rem = m0 - img * ohw;
+    const int py = rem / P.OW, px = rem - py * P.OW;
+    const int tap = kk / P.SC, c0 = kk - tap * P.SC;
+    const int fr = tap / P.S, fs = tap - fr * P.S;
+    if (MODE == FPROP)
+      tc::tma_im2col_4d(stage, &L.tmA[pi], c0, px * P.stride - P.pad, py * P.stride - P.pad, img,
+                        (uint16_t)fs, (uint16_t)fr, bar);
+    else  // stride-1 data gradient: dY window of dX pixel (y, x), taps reversed
+      tc::tma_im2col_4d(stage, &L.tmA[pi], c0, px + P.pad - (P.S - 1), py + P.pad - (P.R - 1),
+                        img, (uint16_t)(P.S - 1 - fs), (uint16_t)(P.R - 1 - fr), bar);
+  }
+  tc::tma_load_2d(stage + 16384, &L.tm[pi], kk, P.brow0 + tn * NT, bar);
+}
+
+// 4 UMMA K-steps (K = 16 each) of one stage into the accumulator at tmem_d
+template <int MODE>
+__device__ __forceinline__ void mma_kblock(uint32_t tmem_d, uint32_t a_s, uint32_t idesc,
+                                           bool first) {
+  const uint32_t b_s = a_s + 16384;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint64_t ad, bd;
+    if (MODE == WGRAD) {
+      ad = tc::sdesc_sw128(a_s + ks * 2048, 8192, 1024);
+      bd = tc::sdesc_sw128(b_s + ks * 2048, 8192, 1024);
+    } else {
+      ad = tc::sdesc_sw128(a_s + ks * 32, 16, 1024);
+      bd = tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
+    }
+    tc::mma_bf16(tmem_d, ad, bd, idesc, (!first || ks) ? 1u : 0u);
+  }
+}
+
+struct TileInfo {
+  int pi, split, tm, tn, k0, nkb;
+};
+__device__ __forceinline__ TileInfo decode_tile(const Launch& L, int t, bool wgrad) {
+  TileInfo T;
+  int pi = 0;
+  while (pi + 1 < L.nprob && t >= L.p[pi + 1].tile0) ++pi;
+  const Problem& P = L.p[pi];
+  int lt = t - P.tile0;
+  const int per_split = P.tiles_m * P.tiles_n;
+  T.pi = pi;
+  T.split = lt / per_split;
+  lt -= T.split * per_split;
+  T.tm = lt % P.tiles_m;
+  T.tn = lt / P.tiles_m;
+  int k0 = 0, kend = P.K;
+  if (wgrad) {
+    k0 = T.split * P.kper;
+    kend = min(P.K, k0 + P.kper);
+  }
+  T.k0 = k0;
+  T.nkb = (kend - k0 + BK - 1) / BK;
+  return T;
+}
+
+// TMEM accumulator (columns [tcol, tcol + NT) of this CTA's allocation) of one
+// output tile → global: bias / activation / fp32 / concat-N / accumulate per
+// the problem, non-finite flag for WGRAD.  Warps 0-3, lane quarter = warp.
+template <int MODE>
+__device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int warp, int lane,
+                                         int tm, int tn, int split, int nkb, int NT) {
+  const int row = warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const int m = tm * BM + row;
+  for (int c0 = 0; c0 < NT; c0 += 16) {
+    float v[16];
+    if (nkb > 0) {
+      tc::tmem_ld16(trow + c0, v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = 0.f;
+    }
+    const int n0 = tn * NT + c0;
+    if (m >= P.M || n0 >= P.N) continue;
+    if (MODE == FPROP && (P.bias || P.act)) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float x = v[e];
+        if (P.bias) x += (n0 + e < P.N) ? __ldg(P.bias + n0 + e) : 0.f;
+        if (P.act == 1) x = fmaxf(x, 0.f);
+        else if (P.act == 2) x = fminf(fmaxf(x, 0.f), 6.f);
+        v[e] = x;
+      }
+    }
+    if (MODE == WGRAD && P.flag) {
+      bool bad = false;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) bad |= (n0 + e < P.N) && !isfinite(v[e]);
+      if (bad) *P.flag = 1;
+    }
+    if (MODE == FPROP && P.out_f32) {
+      float* d = static_cast<float*>(P.dst) + (long long)m * P.dld + n0;
+      if (n0 + 16 <= P.N && (P.dld & 3) == 0) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      } else {
+        for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
+      }
+    } else if (MODE == WGRAD && P.swap) {
+      // accumulator row m = (r,s,c) column of dW, columns = co rows of dW
+      float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride + m;
+      for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[(long long)(n0 + e) * P.dld] = v[e];
+    } else if (MODE == WGRAD) {
+      float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride +
+                 (long long)m * P.dld + n0;
+      if (n0 + 16 <= P.N) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      } else {
+        for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
+      }
+    } else {
+      int seg = 0, nn = n0;
+      if (P.nseg > 0) {
+        seg = n0 / P.nseg;
+        nn = n0 - seg * P.nseg;
+      }
+      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(P.dst) + (long long)seg * P.dseg +
+                         (long long)m * P.dld + nn;
+      const bool vec = n0 + 16 <= P.N && (P.nseg == 0 || nn + 16 <= P.nseg);
+      if (vec) {
+        if (P.accumulate) {
+          const uint4 o0 = reinterpret_cast<const uint4*>(d)[0];
+          const uint4 o1 = reinterpret_cast<const uint4*>(d)[1];
+          const __nv_bfloat16* ob0 = reinterpret_cast<const __nv_bfloat16*>(&o0);
+          const __nv_bfloat16* ob1 = reinterpret_cast<const __nv_bfloat16*>(&o1);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            v[e] += __bfloat162float(ob0[e]);
+            v[e + 8] += __bfloat162float(ob1[e]);
+          }
+        }
+        uint4 w0, w1;
+        w0.x = tc::pack_bf16(v[0], v[1]);
+        w0.y = tc::pack_bf16(v[2], v[3]);
+        w0.z = tc::pack_bf16(v[4], v[5]);
+        w0.w = tc::pack_bf16(v[6], v[7]);
+        w1.x = tc::pack_bf16(v[8], v[9]);
+        w1.y = tc::pack_bf16(v[10], v[11]);
+        w1.z = tc::pack_bf16(v[12], v[13]);
+        w1.w = tc::pack_bf16(v[14], v[15]);
+        reinterpret_cast<uint4*>(d)[0] = w0;
+        reinterpret_cast<uint4*>(d)[1] = w1;
+      } else {
+        for (int e = 0; e < 16 && n0 + e < P.N; ++e) {
+          int sg = seg, cn = nn + e;
+          if (P.nseg > 0 && cn >= P.nseg) {
+            sg += cn / P.nseg;
+            cn -= (cn / P.nseg) * P.nseg;
+          }
+          __nv_bfloat16* de = static_cast<__nv_bfloat16*>(P.dst) + (long long)sg * P.dseg +
+                              (long long)m * P.dld + cn;
+          float x = v[e];
+          if (P.accumulate) x += __bfloat162float(*de);
+          *de = __float2bfloat16_rn(x);
+        }
+      }
+    }
+  }
 }
 
 template <int MODE>
@@ -246,102 +458,7 @@ k_conv_gemm(const __grid_constant__ Launch L) {
     // =========================== epilogue ===========================
     umma::mbar_wait(done, 0);
     umma::fence_after();
-    const int row = warp * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    const int m = tm * BM + row;
-    for (int c0 = 0; c0 < NT; c0 += 16) {
-      float v[16];
-      if (nkb > 0) {
-        tc::tmem_ld16(trow + c0, v);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = 0.f;
-      }
-      const int n0 = tn * NT + c0;
-      if (m >= P.M || n0 >= P.N) continue;
-      if (MODE == FPROP && (P.bias || P.act)) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float x = v[e];
-          if (P.bias) x += (n0 + e < P.N) ? __ldg(P.bias + n0 + e) : 0.f;
-          if (P.act == 1) x = fmaxf(x, 0.f);
-          else if (P.act == 2) x = fminf(fmaxf(x, 0.f), 6.f);
-          v[e] = x;
-        }
-      }
-      if (MODE == WGRAD && P.flag) {
-        bool bad = false;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) bad |= (n0 + e < P.N) && !isfinite(v[e]);
-        if (bad) *P.flag = 1;
-      }
-      if (MODE == FPROP && P.out_f32) {
-        float* d = static_cast<float*>(P.dst) + (long long)m * P.dld + n0;
-        if (n0 + 16 <= P.N && (P.dld & 3) == 0) {
-#pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-        } else {
-          for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
-        }
-      } else if (MODE == WGRAD) {
-        float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride +
-                   (long long)m * P.dld + n0;
-        if (n0 + 16 <= P.N) {
-#pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            *reinterpret_cast<float4*>(d + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-        } else {
-          for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[e] = v[e];
-        }
-      } else {
-        int seg = 0, nn = n0;
-        if (P.nseg > 0) {
-          seg = n0 / P.nseg;
-          nn = n0 - seg * P.nseg;
-        }
-        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(P.dst) + (long long)seg * P.dseg +
-                           (long long)m * P.dld + nn;
-        const bool vec = n0 + 16 <= P.N && (P.nseg == 0 || nn + 16 <= P.nseg);
-        if (vec) {
-          if (P.accumulate) {
-            const uint4 o0 = reinterpret_cast<const uint4*>(d)[0];
-            const uint4 o1 = reinterpret_cast<const uint4*>(d)[1];
-            const __nv_bfloat16* ob0 = reinterpret_cast<const __nv_bfloat16*>(&o0);
-            const __nv_bfloat16* ob1 = reinterpret_cast<const __nv_bfloat16*>(&o1);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              v[e] += __bfloat162float(ob0[e]);
-              v[e + 8] += __bfloat162float(ob1[e]);
-            }
-          }
-          uint4 w0, w1;
-          w0.x = tc::pack_bf16(v[0], v[1]);
-          w0.y = tc::pack_bf16(v[2], v[3]);
-          w0.z = tc::pack_bf16(v[4], v[5]);
-          w0.w = tc::pack_bf16(v[6], v[7]);
-          w1.x = tc::pack_bf16(v[8], v[9]);
-          w1.y = tc::pack_bf16(v[10], v[11]);
-          w1.z = tc::pack_bf16(v[12], v[13]);
-          w1.w = tc::pack_bf16(v[14], v[15]);
-          reinterpret_cast<uint4*>(d)[0] = w0;
-          reinterpret_cast<uint4*>(d)[1] = w1;
-        } else {
-          for (int e = 0; e < 16 && n0 + e < P.N; ++e) {
-            int sg = seg, cn = nn + e;
-            if (P.nseg > 0 && cn >= P.nseg) {
-              sg += cn / P.nseg;
-              cn -= (cn / P.nseg) * P.nseg;
-            }
-            __nv_bfloat16* de = static_cast<__nv_bfloat16*>(P.dst) + (long long)sg * P.dseg +
-                                (long long)m * P.dld + cn;
-            float x = v[e];
-            if (P.accumulate) x += __bfloat162float(*de);
-            *de = __float2bfloat16_rn(x);
-          }
-        }
-      }
-    }
+    epilogue<MODE>(P, tmem, warp, lane, tm, tn, split, nkb, NT);
   } else if (warp == 4) {
     // =========================== MMA issuer ===========================
     if (lane == 0) {
@@ -352,19 +469,7 @@ k_conv_gemm(const __grid_constant__ Launch L) {
         const int s = kb % ST;
         umma::mbar_wait(&full[s], (kb / ST) & 1);
         umma::fence_after();
-        const uint32_t a_s = sbase + s * SB, b_s = a_s + 16384;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          uint64_t ad, bd;
-          if (mn) {
-            ad = tc::sdesc_sw128(a_s + ks * 2048, 8192, 1024);
-            bd = tc::sdesc_sw128(b_s + ks * 2048, 8192, 1024);
-          } else {
-            ad = tc::sdesc_sw128(a_s + ks * 32, 16, 1024);
-            bd = tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
-          }
-          tc::mma_bf16(tmem, ad, bd, idesc, (kb | ks) != 0);
-        }
+        mma_kblock<MODE>(tmem, sbase + s * SB, idesc, kb == 0);
         umma::commit(&empty[s]);
       }
       umma::commit(done);
@@ -372,63 +477,112 @@ k_conv_gemm(const __grid_constant__ Launch L) {
     __syncwarp();
   } else if (kTma && warp == 5 && lane == 0) {
     // =========================== TMA ===========================
-    const int ohw = P.OH * P.OW;
-    if (MODE == WGRAD) {
-      // A = dY [pix][co] (2-D box {64 co, 64 pix}, two 64-wide M atoms);
-      // B = X im2col / 2-D [pix][c] (box {64 c, 64 pix}, NT/64 N atoms)
-      const uint32_t bytes = 16384u + (uint32_t)NT * 128u;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % ST;
-        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
-        umma::mbar_arrive_expect_tx(&full[s], bytes);
-        uint8_t* a_s = smem + s * SB;
-        uint8_t* b_s = a_s + 16384;
-        const int pix0 = k0 + kb * BK;
-        tc::tma_load_2d(a_s, &L.tmA[pi], tm * BM, pix0, &full[s]);
-        tc::tma_load_2d(a_s + 8192, &L.tmA[pi], tm * BM + 64, pix0, &full[s]);
-        const int img = pix0 / ohw, rem = pix0 - img * ohw;
-        const int py = rem / P.OW, px = rem - py * P.OW;
-        for (int j = 0; j < NT / 64; ++j) {
-          const int n = tn * NT + j * 64;
-          if (P.b_mode == 1) {
-            tc::tma_load_2d(b_s + j * 8192, &L.tm[pi], n, pix0, &full[s]);
-          } else {
-            const int tap = n / P.SC, c0 = n - tap * P.SC;
-            const int fr = tap / P.S, fs = tap - fr * P.S;
-            tc::tma_im2col_4d(b_s + j * 8192, &L.tm[pi], c0, px * P.stride - P.pad,
-                              py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, &full[s]);
-          }
-        }
-      }
-    } else {
-      const uint32_t bbytes = (uint32_t)NT * 128u;
-      const uint32_t bytes = bbytes + (tma_all ? 16384u : 0u);
-      const int m0 = tm * BM;
-      const int img = m0 / ohw, rem = m0 - img * ohw;
-      const int py = rem / P.OW, px = rem - py * P.OW;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % ST;
-        if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
-        umma::mbar_arrive_expect_tx(&full[s], bytes);
-        const int kk = k0 + kb * BK;
-        if (P.a_mode == 1) {
-          tc::tma_load_2d(smem + s * SB, &L.tmA[pi], kk, m0, &full[s]);
-        } else if (P.a_mode == 2) {
-          const int tap = kk / P.SC, c0 = kk - tap * P.SC;
-          const int fr = tap / P.S, fs = tap - fr * P.S;
-          if (MODE == FPROP)
-            tc::tma_im2col_4d(smem + s * SB, &L.tmA[pi], c0, px * P.stride - P.pad,
-                              py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, &full[s]);
-          else  // stride-1 data gradient: dY window of dX pixel (y, x), taps reversed
-            tc::tma_im2col_4d(smem + s * SB, &L.tmA[pi], c0, px + P.pad - (P.S - 1),
-                              py + P.pad - (P.R - 1), img, (uint16_t)(P.S - 1 - fs),
-                              (uint16_t)(P.R - 1 - fr), &full[s]);
-        }
-        tc::tma_load_2d(smem + s * SB + 16384, &L.tm[pi], kk, P.brow0 + tn * NT, &full[s]);
-      }
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % ST;
+      if (kb >= ST) umma::mbar_wait(&empty[s], ((kb / ST) + 1) & 1);
+      tma_kblock<MODE>(L, pi, tm, tn, k0 + kb * BK, tma_all, smem + s * SB, &full[s], NT);
     }
   }
 
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Persistent variant, for launches whose operands all arrive by TMA.  A CTA
+// walks tiles blockIdx.x, +gridDim.x, ...; the smem ring runs continuously
+// across tiles (warp 5 keeps loading the next tile's k-blocks while the last
+// ones are multiplied), and two TMEM accumulators (columns [0, NT) and
+// [S, S+NT), S = half the power-of-two allocation) alternate between tiles so warps 0-3 drain tile i while warp 4
+// issues tile i+1's MMAs.  Tile arithmetic is the one-tile kernel's, so
+// results are identical bit for bit.
+// ------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_constant__ Launch L) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile, ST = L.stages;
+  const uint32_t SB = stage_bytes(NT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * SB);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr bool wg = MODE == WGRAD;
+  if (tid == 160) {
+    for (int s = 0; s < ST; ++s) {
+      umma::mbar_init(&full[s], 1);
+      umma::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 128);
+    }
+    umma::mbar_fence_init();
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)(2 * NT));
+  if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t bstride = tcols / 2;  // accumulator buffer b at columns [b*bstride, +NT)
+  const int T = L.total_tiles;
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---- TMA producer ----
+      int g = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const TileInfo ti = decode_tile(L, t, wg);
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          if (g >= ST) umma::mbar_wait(&empty[s], ((g / ST) + 1) & 1);
+          tma_kblock<MODE>(L, ti.pi, ti.tm, ti.tn, ti.k0 + kb * BK, true, smem + s * SB, &full[s],
+                           NT);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = tc::idesc_bf16(BM, NT, wg, wg);
+      const uint32_t sbase = tc::smem_u32(smem);
+      int g = 0, it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+        const TileInfo ti = decode_tile(L, t, wg);
+        const int buf = it & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[buf], ((it >> 1) + 1) & 1);
+        umma::fence_after();
+        const uint32_t acc = tmem + (uint32_t)buf * bstride;
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          umma::mbar_wait(&full[s], (g / ST) & 1);
+          umma::fence_after();
+          mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0);
+          umma::commit(&empty[s]);
+        }
+        umma::commit(&tfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- warps 0-3: epilogue ----
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+      const TileInfo ti = decode_tile(L, t, wg);
+      const int buf = it & 1;
+      umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      umma::fence_after();
+      epilogue<MODE>(L.p[ti.pi], tmem + (uint32_t)buf * bstride, warp, lane, ti.tm, ti.tn, ti.split,
+                     ti.nkb, NT);
+      umma::fence_before();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
   umma::fence_before();
   __syncthreads();
   if (warp == 4) {

@@ -148,6 +148,7 @@ PROG_SHAPES = [
     (2, 16, 16, 64, 64, 7, 7, 2, 3),            # 2, 0, 2
     (2, 7, 7, 512, 512, 3, 3, 1, 1),            # 2, 2, 2 (deep K)
     (2, 12, 12, 8, 64, 7, 7, 2, 3),             # 0, 0, 0 (first-layer shape)
+    (3, 10, 10, 40, 48, 1, 1, 1, 0),            # 1, 1, 1 + swapped WGRAD (co 48)
 ]
 
 
@@ -198,7 +199,8 @@ def test_prog_fprop_dgrad_wgrad(shape):
         if -(-pix // kper) != splits:
             continue
         outw = torch.zeros(splits, k, kpad, device="cuda")
+        # k <= 64 with a 64-wide N tile takes the swapped orientation (M = r·s·c)
         _prog_conv("CONV_WGRAD", g, _nhwc(x).bfloat16(), None, _nhwc(dy).bfloat16(), outw,
-                   128, splits)
+                   64 if k <= 64 else 128, splits)
         got = outw.double().sum(0)[:, :r * s * c]
         _close(got, ref, 1e-5, bf16_out=False)
