@@ -2,22 +2,30 @@
 """Packed-training throughput on B200 — the BASELINE.json metric.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
-                    [--workload config0|k16]
+                    [--workload config1|config1_lenet|config2|config0|k16|wide16]
+
+Default workload: BASELINE configs[1] — K = 16 MobileNetV2-w0.5 members
+(mixed SGD / Momentum / Adam / Adagrad, lr sweep) on synthetic CIFAR-shape
+32x32 batches of 128, bf16 (tools/bench_cnn.py).  configs[2] is
+`--workload config2` (K = 4 ResNet-18 variants, 224², b = 32); configs[0]
+(the reference-runnable MLP pack) is `--workload config0`.
 
 A "step" is one packed train step (forward + backward + every member's
 optimizer update) of the workload's K members over one batch each.
   value  = K x b / device time of the step, inputs resident in HBM, L2
            flushed (256 MiB write) before every timed step; max over ranks.
   e2e    = the same metric through the public drop-in API
-           (`packing.packed_step` on host numpy datasets): per step the step
-           descriptor goes H2D from pinned memory and losses come back D2H.
+           (`packing.packed_step`) with host-resident inputs: per step the
+           batch crosses PCIe (H2D) and losses come back D2H.
   speedup_vs_unpacked = the same K members trained one after another as
            one-member packs (standalone_step) on the same GPU.
-Multi-GPU (torchrun): one independent pack per GPU (weak scaling, no
-collective on the data path; the timing max uses NCCL).
-`--impl reference` times the reference's own CPU path (`packtrain.packed_step`
-installed unmodified in baseline/_ref; the oracle/ port if absent) on this
-host's cores for the same workload.
+Multi-GPU (torchrun, or `--gpus N` which self-launches N ranks): one
+independent pack per GPU (weak scaling, no collective on the data path; the
+timing max uses NCCL).
+`--impl reference` times the reference's own CPU path on this host's cores
+for the same workload: `packtrain.packed_step` installed unmodified in
+baseline/_ref for the MLP configs, the oracle port (oracle/cnn64.py, torch
+CPU float64) for the conv configs, which the reference has no engine for.
 """
 from __future__ import annotations
 
@@ -639,7 +647,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="config0",
+    ap.add_argument("--workload", default="config1",
                     choices=sorted(WORKLOADS) + sorted(_cnn_workloads()))
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

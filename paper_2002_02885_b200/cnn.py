@@ -52,6 +52,13 @@ def cdiv(a, b):
     return (a + b - 1) // b
 
 
+def input_channels(c):
+    """Padded channel count of a network input: 16 for narrow images (the first
+    conv then reads 16-channel im2col boxes by TMA, csrc/pk_convgemm.cuh
+    a_mode 3), else a multiple of 8."""
+    return 16 if c < 16 else rup(c, 8)
+
+
 # =============================================================================
 # Member architectures
 # =============================================================================
@@ -93,6 +100,7 @@ class PSpec:
     fan: tuple = ()
     w16: bool = False
     dgrad: bool = False   # conv weight whose layer needs a data gradient (Wt16 copy)
+    cin_p: int = 0        # conv weight: padded input channels of the device layout
 
     @property
     def numel(self):
@@ -114,7 +122,7 @@ class Net:
     def __init__(self, arch: ConvArch):
         self.arch = arch
         c, h, w = arch.image
-        self.tensors = {"input": TSpec(h, w, rup(c, 8), c)}
+        self.tensors = {"input": TSpec(h, w, input_channels(c), c)}
         self.ops: list[Op] = []
         self.params: list[PSpec] = []
         self.n = 0
@@ -136,7 +144,8 @@ class Net:
         li = self.n - 1
         kpad = rup(r * s * tx.c, 64)
         W = PSpec(f"{name}/W", "convw", (k, r, s, tx.creal), (kp, kpad), li,
-                  fan=(tx.creal * r * s, k * r * s), w16=True, dgrad=(x != "input"))
+                  fan=(tx.creal * r * s, k * r * s), w16=True, dgrad=(x != "input"),
+                  cin_p=tx.c)
         ps = [W]
         if bias:
             ps.append(PSpec(f"{name}/b", "bias", (k,), (kp,), li))
@@ -319,7 +328,7 @@ def to_dev_layout(p: PSpec, a: np.ndarray) -> np.ndarray:
     if p.kind == "convw":
         k, r, s, c = p.shape
         kp, kpad = p.dev_shape
-        cp = rup(c, 8)
+        cp = p.cin_p
         v = np.zeros((kp, r, s, cp), dtype=np.float32)
         v[:k, :, :, :c] = a
         out[:, :r * s * cp] = v.reshape(kp, r * s * cp)
@@ -336,7 +345,7 @@ def from_dev_layout(p: PSpec, d: np.ndarray) -> np.ndarray:
     if p.kind == "convw":
         k, r, s, c = p.shape
         kp, kpad = p.dev_shape
-        cp = rup(c, 8)
+        cp = p.cin_p
         return d[:, :r * s * cp].reshape(kp, r, s, cp)[:k, :, :, :c].astype(np.float64)
     if p.kind == "dww":
         r, s, c = p.shape
@@ -390,7 +399,7 @@ class DeviceConvDataset:
         if ds.features.shape[1] != c * h * w:
             raise ValueError(f"dataset rows hold {ds.features.shape[1]} features, "
                              f"the conv members expect {c}x{h}x{w}")
-        cp = rup(c, 8)
+        cp = input_channels(c)
         self.n, self.image, self.cp = n, image, cp
         x = np.zeros((n, h, w, cp), dtype=np.float32)
         x[..., :c] = np.asarray(ds.features, dtype=np.float32).reshape(n, c, h, w).transpose(
@@ -564,7 +573,7 @@ class ConvPack:
                 if p.dgrad:
                     kp, kpad = p.dev_shape
                     _, r, s, _c = p.shape
-                    cp = rup(_c, 8)
+                    cp = p.cin_p
                     WT[p.name] = z(cp, rup(r * s * kp, 64), dt=torch.bfloat16)
             self.params.append(P)
             self.grads.append(G)
@@ -659,7 +668,7 @@ class ConvPack:
             if p.dgrad:
                 kp, kpad = p.dev_shape
                 _, r, s, c = p.shape
-                cp = rup(c, 8)
+                cp = p.cin_p
                 wt = np.zeros(tuple(self.wt16[k][p.name].shape), dtype=np.float32)
                 v = d[:, :r * s * cp].reshape(kp, r * s, cp).transpose(2, 1, 0)  # [cp][rs][kp]
                 wt[:, :r * s * kp] = v.reshape(cp, r * s * kp)
@@ -781,10 +790,10 @@ class ConvPack:
 
     def _input(self, lead, data):
         """(source, index list) the first conv of a member led by `lead` reads:
-        the resident dataset through the batch indices, or the leader's
-        staging buffer that the step's GATHER filled (streamed inputs)."""
-        if not data.host:
-            return data.x.data_ptr(), self.idx[lead].data_ptr()
+        the leader's batch buffer, which the step's first op (GATHER) fills
+        from the dataset rows idx[...] — in HBM, or over PCIe from page-locked
+        host memory (streamed inputs).  One contiguous batch per input group
+        keeps the index indirection out of the GEMMs' operand loads."""
         st = self.staging.get(lead)
         if st is None:
             _, h, w = self.members[lead].net.arch.image
@@ -989,7 +998,7 @@ class ConvPack:
             t = _lib.CnnTpose()
             t.src = self.w16[k][p.name].data_ptr()
             t.dst = self.wt16[k][p.name].data_ptr()
-            t.k, t.c, t.taps = kp, rup(c, 8), r * s
+            t.k, t.c, t.taps = kp, p.cin_p, r * s
             t.kpad, t.kpadt = kpad, self.wt16[k][p.name].shape[1]
             steps.append((CNN["PUBLISH_T"], None, t, None))
         return steps
@@ -1069,16 +1078,16 @@ class ConvPack:
         K = len(self.members)
         act = [k for k in range(K) if takes[k] > 0]
         ops = []
-        if data.host:  # streamed inputs: each group's batch rows over PCIe, once
-            gs = []
-            for lead in sorted({leads[k] for k in act}):
-                g = _lib.CnnGather()
-                g.src = data.x.data_ptr()
-                g.dst = self._input(lead, data)[0]
-                g.idx = self.idx[lead].data_ptr()
-                g.row_bytes, g.rows = data.row_bytes, takes[lead]
-                gs.append(g)
-            ops.append((CNN["GATHER"], None, gs))
+        # each input group's batch rows, gathered once (over PCIe when data.host)
+        gs = []
+        for lead in sorted({leads[k] for k in act}):
+            g = _lib.CnnGather()
+            g.src = data.x.data_ptr()
+            g.dst = self._input(lead, data)[0]
+            g.idx = self.idx[lead].data_ptr()
+            g.row_bytes, g.rows = data.row_bytes, takes[lead]
+            gs.append(g)
+        ops.append((CNN["GATHER"], None, gs))
         ops += self._group([self._fwd_steps(k, takes[k], leads[k], data) for k in act])
         ops += self._group([self._bwd_steps(k, takes[k], leads[k], data) for k in act])
         if with_update:

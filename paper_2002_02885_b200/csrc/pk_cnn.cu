@@ -40,7 +40,7 @@ int g_driver_version = 0;
 // lower/upper: the pixel box corners {w, h} (CUTLASS sm100 conv conventions).
 bool make_map_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int c, int ld,
                      int lower_w, int lower_h, int upper_w, int upper_h, int stride,
-                     int pixels) {
+                     int pixels, int chans = 64) {
   std::call_once(g_i2c_once, [] {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -57,8 +57,10 @@ bool make_map_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int 
   int lower[2] = {lower_w, lower_h}, upper[2] = {upper_w, upper_h};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   if (g_encode_i2c(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
-                   lower, upper, 64, (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   lower, upper, (cuuint32_t)chans, (cuuint32_t)pixels, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   chans == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   // the driver workaround CUTLASS applies to im2col maps of tensors < 128 KiB on
@@ -69,16 +71,18 @@ bool make_map_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int 
   return true;
 }
 
-// 2-D bf16 tensor map [rows][cols] (row pitch `ld` elements), box {64, box_rows}, SW128
+// 2-D bf16 tensor map [rows][cols] (row pitch `ld` elements), box {box_cols, box_rows},
+// SW128 for 64-column boxes, SW32 for 16-column boxes
 bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                 uint32_t box_rows) {
+                 uint32_t box_rows, uint32_t box_cols = 64) {
   if (!encode_fn()) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -174,10 +178,14 @@ int prob_blocks(int kind, const void* pr) {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       return cdiv((long long)P.n * P.p * P.q, P.ppb);
     }
-    case PK_CNN_MAXPOOL_FWD:
-    case PK_CNN_AVGPOOL_FWD: {
+    case PK_CNN_MAXPOOL_FWD: {
       const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
       return blocks_of(items((long long)P.n * P.p * P.q, P.c));
+    }
+    case PK_CNN_AVGPOOL_FWD: {
+      const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
+      const bool global = P.r == P.h && P.s == P.w && P.pad == 0 && P.p == 1 && P.q == 1;
+      return blocks_of(items((long long)P.n * P.p * P.q, P.c) * (global ? cnn::kPoolLanes : 1));
     }
     case PK_CNN_MAXPOOL_BWD:
     case PK_CNN_AVGPOOL_BWD: {
@@ -337,6 +345,11 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
           if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.h, g.w, g.c, g.ldx, -g.pad, -g.pad,
                                g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, cg::BM))
             return fail(PK_ERR_CUDA, "conv: FPROP im2col map");
+        } else if (!g.idx && g.c == 16 && g.ldx == 16 && g.r * g.s <= 255) {
+          p.a_mode = 3;  // 16-channel input: one tap per 16-deep K chunk, SW32
+          if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.h, g.w, 16, 16, -g.pad, -g.pad,
+                               g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, cg::BM, 16))
+            return fail(PK_ERR_CUDA, "conv: FPROP 16-channel im2col map");
         }
         p.src = static_cast<const __nv_bfloat16*>(g.src);
         p.idx = reinterpret_cast<const long long*>(g.idx);
@@ -345,7 +358,7 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         p.M = g.n * g.p * g.q; p.N = g.k; p.K = g.r * g.s * g.c;
         p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
         p.OH = g.p; p.OW = g.q; p.dld = g.ldo;
-        if (!make_map_2d(&L.tm[j], g.wt, g.k, kpad, kpad, ntile))
+        if (!make_map_2d(&L.tm[j], g.wt, g.k, kpad, kpad, ntile, p.a_mode == 3 ? 16 : 64))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (FPROP weights)");
         p.splits = 1;
       } else if (kind == PK_CNN_CONV_DGRAD) {
@@ -382,12 +395,14 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         p.splits = cdiv(pix, p.kper);
         if (p.splits != sp) return fail(PK_ERR_ARG, "conv: WGRAD splits leave an empty split");
         p.flag = p.splits == 1 ? g.flag : nullptr;
-        if (!g.idx && (one || g.c % 64 == 0)) {
-          p.b_mode = one ? 1 : 2;
+        const bool c16 = g.c == 16 && g.ldx == 16 && !one;
+        if (!g.idx && (one || g.c % 64 == 0 || c16)) {
+          p.b_mode = one ? 1 : (c16 ? 3 : 2);
           const bool ok =
               one ? make_map_2d(&L.tm[j], g.src, (uint64_t)g.n * g.h * g.w, g.c, g.ldx, 64)
                   : make_map_im2col(&L.tm[j], g.src, g.n, g.h, g.w, g.c, g.ldx, -g.pad, -g.pad,
-                                    g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, 64);
+                                    g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, 64,
+                                    c16 ? 16 : 64);
           if (!ok || !make_map_2d(&L.tmA[j], g.dy, (uint64_t)pix, g.k, g.ldy, 64))
             return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
           if (g.k <= 64 && ntile == 64) {  // swapped orientation (see cg::Problem::swap)

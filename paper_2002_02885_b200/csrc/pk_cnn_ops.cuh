@@ -37,7 +37,7 @@ __device__ __forceinline__ int find_prob(const int* blk0, int nprob, int b) {
 // Up to kPack problems of one launch travel in the kernel parameters (constant
 // bank): a block's problem lookup and descriptor reads are then cached
 // constant loads instead of a dependent chain of global loads.
-constexpr int kPack = 16;
+constexpr int kPack = 64;
 template <class T>
 struct Pack {
   int nprob;
@@ -366,18 +366,27 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constan
   ld8f(P.stats + 3 * P.c + ch, mgx);
   const long long r0 = rg * kApplyRows;
   const int nr = (int)min((long long)kApplyRows, P.rows - r0);
-  for (int i = 0; i < nr; ++i) {
+  const bool act = P.act != PK_CNN_ACT_NONE;
+  // all loads of the thread's rows first (memory-level parallelism), then math
+  float d[kApplyRows][8], x[kApplyRows][8], fo[kApplyRows][8];
+#pragma unroll
+  for (int i = 0; i < kApplyRows; ++i)
+    if (i < nr) {
+      ld8(bptr(P.dout, r0 + i, P.ldd, ch), d[i]);
+      ld8(bptr(P.x, r0 + i, P.ldx, ch), x[i]);
+      if (act) ld8(bptr(P.fout, r0 + i, P.ldo, ch), fo[i]);
+    }
+#pragma unroll
+  for (int i = 0; i < kApplyRows; ++i) {
+    if (i >= nr) break;
     const long long r = r0 + i;
-    float d[8], fo[8], x[8], dx[8];
-    ld8(bptr(P.dout, r, P.ldd, ch), d);
-    ld8(bptr(P.x, r, P.ldx, ch), x);
-    if (P.act != PK_CNN_ACT_NONE) ld8(bptr(P.fout, r, P.ldo, ch), fo);
+    float dx[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float g = P.act != PK_CNN_ACT_NONE ? d[e] * act_bwd(fo[e], P.act) : d[e];
-      const float xh = (x[e] - mean[e]) * rs[e];
+      const float g = act ? d[i][e] * act_bwd(fo[i][e], P.act) : d[i][e];
+      const float xh = (x[i][e] - mean[e]) * rs[e];
       dx[e] = ga[e] * rs[e] * (g - mg[e] - xh * mgx[e]);
-      d[e] = g;
+      d[i][e] = g;
     }
     if (P.accumulate) {
       float o[8];
@@ -391,9 +400,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constan
         float o[8];
         ld8(bptr(P.dres, r, P.ldr, ch), o);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) d[e] += o[e];
+        for (int e = 0; e < 8; ++e) d[i][e] += o[e];
       }
-      st8(bptr(P.dres, r, P.ldr, ch), d);
+      st8(bptr(P.dres, r, P.ldr, ch), d[i]);
     }
   }
 }
@@ -553,15 +562,11 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const __grid_constant__ Pac
 }
 
 // ================================ pooling ========================================
-__global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_pool& P = G.p[pi];
-  const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long M = (long long)P.n * P.p * P.q;
-  if (item >= M * cgs) return;
-  const long long m = item / cgs;
-  const int ch = 8 * (int)(item - m * cgs);
+// Bodies are templates on the window / stride (0 = runtime value) so the
+// common shapes (3x3/2 ResNet stem, 2x2/2 LeNet) unroll their tap loops.
+template <int R_, int S_, int ST_>
+__device__ __forceinline__ void maxpool_fwd_item(const pk_cnn_pool& P, long long m, int ch) {
+  const int R = R_ ? R_ : P.r, S = S_ ? S_ : P.s, ST = ST_ ? ST_ : P.stride;
   const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
   const int oy = rem / P.q, ox = rem - oy * P.q;
   float best[8];
@@ -571,20 +576,26 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ 
     best[e] = -INFINITY;
     arg[e] = 0;
   }
-  for (int r = 0; r < P.r; ++r) {
-    const int iy = oy * P.stride - P.pad + r;
-    if ((unsigned)iy >= (unsigned)P.h) continue;
-    for (int s = 0; s < P.s; ++s) {
-      const int ix = ox * P.stride - P.pad + s;
-      if ((unsigned)ix >= (unsigned)P.w) continue;
-      float x[8];
-      ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (x[e] > best[e]) {
-          best[e] = x[e];
-          arg[e] = (uint8_t)(r * P.s + s);
+  for (int r = 0; r < (R_ ? R_ : 1); ++r) {
+    for (int rr = r; rr < R; rr += (R_ ? R : 1)) {
+      const int iy = oy * ST - P.pad + rr;
+      if ((unsigned)iy >= (unsigned)P.h) continue;
+#pragma unroll
+      for (int s = 0; s < (S_ ? S_ : 1); ++s) {
+        for (int ss = s; ss < S; ss += (S_ ? S : 1)) {
+          const int ix = ox * ST - P.pad + ss;
+          if ((unsigned)ix >= (unsigned)P.w) continue;
+          float x[8];
+          ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (x[e] > best[e]) {
+              best[e] = x[e];
+              arg[e] = (uint8_t)(rr * S + ss);
+            }
         }
+      }
     }
   }
   st8(bptr(P.y, m, P.ldy, ch), best);
@@ -594,40 +605,51 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ 
   *reinterpret_cast<uint2*>(P.arg + m * P.c + ch) = a;
 }
 
-__global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_pool& P = G.p[pi];
-  const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long M = (long long)P.n * P.h * P.w;
-  if (item >= M * cgs) return;
-  const long long m = item / cgs;
-  const int ch = 8 * (int)(item - m * cgs);
+// input pixel (iy, ix) receives dy of every window whose argmax is its tap
+template <int R_, int S_, int ST_, bool AVG>
+__device__ __forceinline__ void pool_bwd_item(const pk_cnn_pool& P, long long m, int ch) {
+  const int R = R_ ? R_ : P.r, S = S_ ? S_ : P.s, ST = ST_ ? ST_ : P.stride;
   const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
   const int iy = rem / P.w, ix = rem - iy * P.w;
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  for (int r = 0; r < P.r; ++r) {
-    const int ty = iy + P.pad - r;
-    if (ty < 0 || ty % P.stride) continue;
-    const int oy = ty / P.stride;
-    if (oy >= P.p) continue;
-    for (int s = 0; s < P.s; ++s) {
-      const int tx = ix + P.pad - s;
-      if (tx < 0 || tx % P.stride) continue;
-      const int ox = tx / P.stride;
-      if (ox >= P.q) continue;
-      const long long o = ((long long)n * P.p + oy) * P.q + ox;
-      const uint2 a = *reinterpret_cast<const uint2*>(P.arg + o * P.c + ch);
-      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
-      const int tap = r * P.s + s;
-      float d[8];
-      ld8(bptr(P.dy, o, P.ldy, ch), d);
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (ab[e] == tap) acc[e] += d[e];
+  for (int r = 0; r < (R_ ? R_ : 1); ++r) {
+    for (int rr = r; rr < R; rr += (R_ ? R : 1)) {
+      const int ty = iy + P.pad - rr;
+      if (ty < 0 || ty % ST) continue;
+      const int oy = ty / ST;
+      if (oy >= P.p) continue;
+#pragma unroll
+      for (int s = 0; s < (S_ ? S_ : 1); ++s) {
+        for (int ss = s; ss < S; ss += (S_ ? S : 1)) {
+          const int tx = ix + P.pad - ss;
+          if (tx < 0 || tx % ST) continue;
+          const int ox = tx / ST;
+          if (ox >= P.q) continue;
+          const long long o = ((long long)n * P.p + oy) * P.q + ox;
+          float d[8];
+          ld8(bptr(P.dy, o, P.ldy, ch), d);
+          if (AVG) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += d[e];
+          } else {
+            const uint2 a = *reinterpret_cast<const uint2*>(P.arg + o * P.c + ch);
+            const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
+            const int tap = rr * S + ss;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (ab[e] == tap) acc[e] += d[e];
+          }
+        }
+      }
     }
+  }
+  if (AVG) {
+    const float inv = 1.f / (float)(R * S);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
   }
   if (P.accumulate) {
     float o[8];
@@ -638,30 +660,78 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ 
   st8(bptr(P.dx, m, P.ldx, ch), acc);
 }
 
-__global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+__global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
   const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long M = (long long)P.n * P.p * P.q;
-  if (item >= M * cgs) return;
+  if (item >= (long long)P.n * P.p * P.q * cgs) return;
   const long long m = item / cgs;
   const int ch = 8 * (int)(item - m * cgs);
-  const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
-  const int oy = rem / P.q, ox = rem - oy * P.q;
+  if (P.r == 3 && P.s == 3 && P.stride == 2) maxpool_fwd_item<3, 3, 2>(P, m, ch);
+  else if (P.r == 2 && P.s == 2 && P.stride == 2) maxpool_fwd_item<2, 2, 2>(P, m, ch);
+  else maxpool_fwd_item<0, 0, 0>(P, m, ch);
+}
+
+__global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
+  const int cgs = P.c >> 3;
+  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
+  if (item >= (long long)P.n * P.h * P.w * cgs) return;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
+  if (P.r == 3 && P.s == 3 && P.stride == 2) pool_bwd_item<3, 3, 2, false>(P, m, ch);
+  else if (P.r == 2 && P.s == 2 && P.stride == 2) pool_bwd_item<2, 2, 2, false>(P, m, ch);
+  else pool_bwd_item<0, 0, 0, false>(P, m, ch);
+}
+
+// average pool; the global case (window = the whole map) splits each output's
+// window over kPoolLanes threads and combines them with a fixed xor tree
+constexpr int kPoolLanes = 8;
+__global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_pool& P = G.p[pi];
+  const int cgs = P.c >> 3;
+  const bool global = P.r == P.h && P.s == P.w && P.pad == 0 && P.p == 1 && P.q == 1;
+  const int lanes = global ? kPoolLanes : 1;
+  const long long item = ((long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x) / lanes;
+  const int lane = threadIdx.x % lanes;
+  const long long total = (long long)P.n * P.p * P.q * cgs;
+  const long long m = item / cgs;
+  const int ch = 8 * (int)(item - m * cgs);
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  for (int r = 0; r < P.r; ++r) {
-    const int iy = oy * P.stride - P.pad + r;
-    if ((unsigned)iy >= (unsigned)P.h) continue;
-    for (int s = 0; s < P.s; ++s) {
-      const int ix = ox * P.stride - P.pad + s;
-      if ((unsigned)ix >= (unsigned)P.w) continue;
-      float x[8];
-      ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+  if (global) {
+    const int hw = P.h * P.w;
+    if (item < total)
+      for (int i = lane; i < hw; i += lanes) {
+        float x[8];
+        ld8(bptr(P.x, m * hw + i, P.ldx, ch), x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += x[e];
+        for (int e = 0; e < 8; ++e) acc[e] += x[e];
+      }
+#pragma unroll
+    for (int o = kPoolLanes / 2; o; o >>= 1)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (item >= total || lane != 0) return;
+  } else {
+    if (item >= total) return;
+    const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
+    const int oy = rem / P.q, ox = rem - oy * P.q;
+    for (int r = 0; r < P.r; ++r) {
+      const int iy = oy * P.stride - P.pad + r;
+      if ((unsigned)iy >= (unsigned)P.h) continue;
+      for (int s = 0; s < P.s; ++s) {
+        const int ix = ox * P.stride - P.pad + s;
+        if ((unsigned)ix >= (unsigned)P.w) continue;
+        float x[8];
+        ld8(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch), x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += x[e];
+      }
     }
   }
   const float inv = 1.f / (float)(P.r * P.s);
@@ -675,41 +745,11 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const __grid_constant__ 
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
   const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long M = (long long)P.n * P.h * P.w;
-  if (item >= M * cgs) return;
+  if (item >= (long long)P.n * P.h * P.w * cgs) return;
   const long long m = item / cgs;
   const int ch = 8 * (int)(item - m * cgs);
-  const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
-  const int iy = rem / P.w, ix = rem - iy * P.w;
-  float acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  for (int r = 0; r < P.r; ++r) {
-    const int ty = iy + P.pad - r;
-    if (ty < 0 || ty % P.stride) continue;
-    const int oy = ty / P.stride;
-    if (oy >= P.p) continue;
-    for (int s = 0; s < P.s; ++s) {
-      const int tx = ix + P.pad - s;
-      if (tx < 0 || tx % P.stride) continue;
-      const int ox = tx / P.stride;
-      if (ox >= P.q) continue;
-      float d[8];
-      ld8(bptr(P.dy, ((long long)n * P.p + oy) * P.q + ox, P.ldy, ch), d);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += d[e];
-    }
-  }
-  const float inv = 1.f / (float)(P.r * P.s);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] *= inv;
-  if (P.accumulate) {
-    float o[8];
-    ld8(bptr(P.dx, m, P.ldx, ch), o);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] += o[e];
-  }
-  st8(bptr(P.dx, m, P.ldx, ch), acc);
+  if (P.r == 2 && P.s == 2 && P.stride == 2) pool_bwd_item<2, 2, 2, true>(P, m, ch);
+  else pool_bwd_item<0, 0, 0, true>(P, m, ch);
 }
 
 // ======================== softmax cross-entropy head ============================

@@ -56,9 +56,12 @@ struct Problem {
   int act;                    // FPROP epilogue activation after bias: 0 none, 1 relu, 2 relu6
   int out_f32;                // FPROP: dst is fp32
   int a_mode;                 // activation operand: 0 cp.async gather, 1 TMA 2-D tile,
-                              //   2 TMA im2col (FPROP/DGRAD: A; WGRAD: A=dY is TMA 2-D
-                              //   whenever b_mode != 0)
-  int b_mode;                 // WGRAD X operand: 0 gather, 1 TMA 2-D tile, 2 TMA im2col
+                              //   2 TMA im2col (C % 64 == 0, SW128), 3 TMA im2col of a
+                              //   16-channel input (one tap per 16-deep K chunk, SW32;
+                              //   weights then also SW32) (FPROP/DGRAD: A; WGRAD: A=dY
+                              //   is TMA 2-D whenever b_mode != 0)
+  int b_mode;                 // WGRAD X operand: 0 gather, 1 TMA 2-D tile, 2 TMA im2col,
+                              //   3 TMA im2col of a 16-channel input (SW32)
   int swap;                   // WGRAD (TMA, co <= 64): GEMM M = (r,s,c), N = co, so the
                               //   M = 128 MMA is not half empty; dst written transposed
   long long dseg;             // elements between dst segments
@@ -99,7 +102,13 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
     const int py = rem / P.OW, px = rem - py * P.OW;
     // one 64-wide atom of the X operand: columns n .. n+63 of (r, s, c)
     auto x_atom = [&](uint8_t* dst, int n) {
-      if (P.b_mode == 1) {
+      if (P.b_mode == 3) {  // four 16-channel taps, 2 KB SW32 boxes
+        for (int i = 0; i < 4; ++i) {
+          const int tap = (n >> 4) + i, fr = tap / P.S, fs = tap - fr * P.S;
+          tc::tma_im2col_4d(dst + i * 2048, &L.tm[pi], 0, px * P.stride - P.pad,
+                            py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, bar);
+        }
+      } else if (P.b_mode == 1) {
         tc::tma_load_2d(dst, &L.tm[pi], n, kk, bar);
       } else {
         const int tap = n / P.SC, c0 = n - tap * P.SC;
@@ -121,6 +130,18 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
   }
   umma::mbar_arrive_expect_tx(bar, (uint32_t)NT * 128u + (tma_all ? 16384u : 0u));
   const int m0 = tm * BM;
+  if (P.a_mode == 3) {  // four taps of a 16-channel input: A and B in 16-deep SW32 slabs
+    const int img = m0 / ohw, rem = m0 - img * ohw;
+    const int py = rem / P.OW, px = rem - py * P.OW;
+    for (int i = 0; i < 4; ++i) {
+      const int tap = (kk >> 4) + i, fr = tap / P.S, fs = tap - fr * P.S;
+      tc::tma_im2col_4d(stage + i * 4096, &L.tmA[pi], 0, px * P.stride - P.pad,
+                        py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, bar);
+      tc::tma_load_2d(stage + 16384 + i * NT * 32, &L.tm[pi], kk + 16 * i, P.brow0 + tn * NT,
+                      bar);
+    }
+    return;
+  }
   if (P.a_mode == 1) {
     tc::tma_load_2d(stage, &L.tmA[pi], kk, m0, bar);
   } else if (P.a_mode == 2) {
@@ -138,22 +159,39 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
   tc::tma_load_2d(stage + 16384, &L.tm[pi], kk, P.brow0 + tn * NT, bar);
 }
 
-// 4 UMMA K-steps (K = 16 each) of one stage into the accumulator at tmem_d
+// 4 UMMA K-steps (K = 16 each) of one stage into the accumulator at tmem_d.
+// sw32a / sw32b: that operand is in 32-byte-swizzled slabs (16-channel input).
 template <int MODE>
 __device__ __forceinline__ void mma_kblock(uint32_t tmem_d, uint32_t a_s, uint32_t idesc,
-                                           bool first) {
+                                           bool first, bool sw32a = false, bool sw32b = false,
+                                           int NT = 0) {
   const uint32_t b_s = a_s + 16384;
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     uint64_t ad, bd;
-    if (MODE == WGRAD) {
-      ad = tc::sdesc_sw128(a_s + ks * 2048, 8192, 1024);
-      bd = tc::sdesc_sw128(b_s + ks * 2048, 8192, 1024);
-    } else {
-      ad = tc::sdesc_sw128(a_s + ks * 32, 16, 1024);
-      bd = tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
+    if (MODE == WGRAD) {  // MN-major operands
+      ad = sw32a ? tc::sdesc_sw32(a_s + ks * 512, 2048, 256)
+                 : tc::sdesc_sw128(a_s + ks * 2048, 8192, 1024);
+      bd = sw32b ? tc::sdesc_sw32(b_s + ks * 512, 2048, 256)
+                 : tc::sdesc_sw128(b_s + ks * 2048, 8192, 1024);
+    } else {              // K-major operands
+      ad = sw32a ? tc::sdesc_sw32(a_s + ks * 4096, 16, 256)
+                 : tc::sdesc_sw128(a_s + ks * 32, 16, 1024);
+      bd = sw32b ? tc::sdesc_sw32(b_s + ks * NT * 32, 16, 256)
+                 : tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
     }
     tc::mma_bf16(tmem_d, ad, bd, idesc, (!first || ks) ? 1u : 0u);
+  }
+}
+
+// which operands of problem P sit in SW32 slabs
+__device__ __forceinline__ void sw32_flags(const Problem& P, bool wgrad, bool& a, bool& b) {
+  if (wgrad) {
+    const bool x = P.b_mode == 3;
+    a = P.swap ? x : false;
+    b = P.swap ? false : x;
+  } else {
+    a = b = P.a_mode == 3;
   }
 }
 
@@ -469,7 +507,9 @@ k_conv_gemm(const __grid_constant__ Launch L) {
         const int s = kb % ST;
         umma::mbar_wait(&full[s], (kb / ST) & 1);
         umma::fence_after();
-        mma_kblock<MODE>(tmem, sbase + s * SB, idesc, kb == 0);
+        bool fa, fb;
+        sw32_flags(P, MODE == WGRAD, fa, fb);
+        mma_kblock<MODE>(tmem, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
         umma::commit(&empty[s]);
       }
       umma::commit(done);
@@ -563,7 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_consta
           const int s = g % ST;
           umma::mbar_wait(&full[s], (g / ST) & 1);
           umma::fence_after();
-          mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0);
+          bool fa, fb;
+          sw32_flags(L.p[ti.pi], wg, fa, fb);
+          mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
           umma::commit(&empty[s]);
         }
         umma::commit(&tfull[buf]);

@@ -39,6 +39,22 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   return d;
 }
 
+// SWIZZLE_32B (layout_type 6): 32-byte rows (16 bf16), 8-row atoms of 256 B.
+//   K-major : one atom column = 16 K; an MMA K-step (16) is one whole slab of
+//             rows x 32 B, so only SBO (8-row groups, 256 B) matters.
+//   MN-major: atoms of 16 MN x 8 K; LBO = stride between 16-wide MN atoms,
+//             SBO = stride between 8-row K groups (256 B).
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo_bytes,
+                                               uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)6 << 61;  // SWIZZLE_32B
+  return d;
+}
+
 // instruction descriptor: kind::f16 with bf16 A/B, fp32 accumulate, dense
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4)                     // c_format = F32

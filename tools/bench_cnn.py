@@ -165,6 +165,13 @@ def run_b200(args, world, rank, local, Clocks, flush_bytes):
     by_kind = {}
     for kd, t in zip(prog.kinds, op_ms):
         by_kind[kinds[kd]] = by_kind.get(kinds[kd], 0.0) + t
+    top_ops = []
+    for i in sorted(range(len(op_ms)), key=lambda i: -op_ms[i])[:12]:
+        st = prog._keep[i][0]
+        desc = {f: getattr(st, f) for f in ("n", "h", "w", "c", "k", "r", "s", "stride", "rows",
+                                             "p", "q") if hasattr(st, f)}
+        top_ops.append({"op": i, "kernel": kinds[prog.kinds[i]], "ms": op_ms[i],
+                        "problems": prog.sizes[i], "shape": desc})
 
     # algorithmic work per step, all members
     flops, nbytes = {}, {}
@@ -270,6 +277,7 @@ def run_b200(args, world, rank, local, Clocks, flush_bytes):
                      "gemm_all": {"ms": gemm_ms, "tflops": gemm_fl / (gemm_ms / 1e3) / 1e12,
                                   "frac": gemm_fl / (gemm_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}},
         "kernels": table,
+        "top_ops": top_ops,
         "step_flops": sum(flops.values()),
         "gpu_launches": prog.launches * args.steps,
         "clocks": clk,

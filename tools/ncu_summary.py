@@ -86,8 +86,10 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--workload", default="config0")
     ap.add_argument("--title", default="")
+    ap.add_argument("--launches", default="launches.csv", help="launch list file in <tag>")
+    ap.add_argument("--full", default="full.ncu-rep", help="--set full report in <tag>")
     a = ap.parse_args()
-    L = launches(os.path.join(a.tag, "launches.csv"))
+    L = launches(os.path.join(a.tag, a.launches))
     with open(a.out + "_launches.csv", "w") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "grid", "block", "ns"])
@@ -96,8 +98,7 @@ def main():
     for k, g, b, ns in L:
         agg.setdefault(k, []).append(ns)
     total = sum(ns for *_, ns in L)
-    F = full(os.path.join(a.tag, "full.ncu-rep")) if os.path.exists(
-        os.path.join(a.tag, "full.ncu-rep")) else []
+    F = full(os.path.join(a.tag, a.full)) if os.path.exists(os.path.join(a.tag, a.full)) else []
     byk = collections.defaultdict(list)
     for d in F:
         byk[d["kernel"]].append(d)
