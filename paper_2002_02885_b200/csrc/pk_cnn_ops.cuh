@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bn_bwd_reduce(const __grid_consta
   if (bad) *P.flag = 1;
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+__global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
   const int cgs = P.c >> 3;
@@ -358,12 +358,22 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constan
   const long long rg = item / cgs;
   if (rg * kApplyRows >= P.rows) return;
   const int ch = 8 * (int)(item - rg * cgs);
-  float ga[8], mg[8], mgx[8], rs[8], mean[8];
-  ld8f(P.gamma + ch, ga);
-  ld8f(P.stats + ch, mean);
-  ld8f(P.stats + P.c + ch, rs);
-  ld8f(P.stats + 2 * P.c + ch, mg);
-  ld8f(P.stats + 3 * P.c + ch, mgx);
+  // dx = γ·rstd·(g − mean(g) − xhat·mean(g·xhat)) = ca·g + cb·x + cc per channel
+  float ca[8], cb[8], cc[8];
+  {
+    float ga[8], mg[8], mgx[8], rs[8], mean[8];
+    ld8f(P.gamma + ch, ga);
+    ld8f(P.stats + ch, mean);
+    ld8f(P.stats + P.c + ch, rs);
+    ld8f(P.stats + 2 * P.c + ch, mg);
+    ld8f(P.stats + 3 * P.c + ch, mgx);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      ca[e] = ga[e] * rs[e];
+      cb[e] = -ca[e] * rs[e] * mgx[e];
+      cc[e] = -ca[e] * mg[e] - cb[e] * mean[e];
+    }
+  }
   const long long r0 = rg * kApplyRows;
   const int nr = (int)min((long long)kApplyRows, P.rows - r0);
   const bool act = P.act != PK_CNN_ACT_NONE;
@@ -384,8 +394,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_bwd_apply(const __grid_constan
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float g = act ? d[i][e] * act_bwd(fo[i][e], P.act) : d[i][e];
-      const float xh = (x[i][e] - mean[e]) * rs[e];
-      dx[e] = ga[e] * rs[e] * (g - mg[e] - xh * mgx[e]);
+      dx[e] = fmaf(ca[e], g, fmaf(cb[e], x[i][e], cc[e]));
       d[i][e] = g;
     }
     if (P.accumulate) {
