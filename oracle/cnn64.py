@@ -61,8 +61,23 @@ class Spec:
         self.family, self.classes, self.image, self.width = family, classes, image, width
         self.layers = []   # dicts
         self.shapes = {"input": (image[0], image[1], image[2])}   # name -> (C, H, W)
+        self.views = {}    # name -> (base, ch0, c): a channel slice of a concat buffer
         self.n = 0
         getattr(self, "_" + family)()
+
+    def buffer(self, c, h, w):
+        name = f"B{sum(1 for n in self.shapes if n.startswith('B'))}"
+        self.shapes[name] = (c, h, w)
+        return name
+
+    def view(self, base, ch0, c):
+        bc, h, w = self.shapes[base]
+        if ch0 == 0 and c == bc:
+            return base
+        name = f"{base}[{ch0}:{ch0 + c}]"
+        self.shapes[name] = (c, h, w)
+        self.views[name] = (base, ch0, c)
+        return name
 
     # builders (same order / numbering as the device planner) -----------------
     def _new(self):
@@ -70,11 +85,12 @@ class Spec:
         self.n += 1
         return name
 
-    def conv(self, x, k, r, stride=1, pad=0, bias=False, act="none", out_f32=False, s=None):
+    def conv(self, x, k, r, stride=1, pad=0, bias=False, act="none", out_f32=False, s=None,
+             out=None):
         s = r if s is None else s
         c, h, w = self.shapes[x]
         name = self._new()
-        y = name + ".y"
+        y = out if out is not None else name + ".y"
         self.shapes[y] = (k, (h + 2 * pad - r) // stride + 1, (w + 2 * pad - s) // stride + 1)
         self.layers.append(dict(kind="conv", name=name, x=x, y=y, k=k, c=c, r=r, s=s,
                                 stride=stride, pad=pad, bias=bias, act=act, out_f32=out_f32))
@@ -96,10 +112,10 @@ class Spec:
         self.layers.append(dict(kind="dw", name=name, x=x, y=y, c=c, r=r, stride=stride, pad=pad))
         return y
 
-    def pool(self, kind, x, r, stride, pad=0):
+    def pool(self, kind, x, r, stride, pad=0, out=None):
         c, h, w = self.shapes[x]
         name = self._new()
-        y = name + ".y"
+        y = out if out is not None else name + ".y"
         self.shapes[y] = (c, (h + 2 * pad - r) // stride + 1, (w + 2 * pad - r) // stride + 1)
         self.layers.append(dict(kind=kind, name=name, x=x, y=y, r=r, stride=stride, pad=pad))
         return y
@@ -151,6 +167,33 @@ class Spec:
                     if (st != 1 or cin != cout) else x
                 x = self.bn(y2, "relu", res=sc)
                 cin = cout
+        x = self.pool("avgpool", x, self.shapes[x][1], 1)
+        self.logits = self.conv(x, self.classes, 1, bias=True, out_f32=True)
+
+    def _densenet121(self, blocks=(6, 12, 24, 16), growth=32, bn_size=4, c0=64):
+        """torchvision DenseNet-121; torch.cat of the dense layers restated as
+        writes into channel slices of one buffer per block."""
+        x = self.bn(self.conv("input", c0, 7, stride=2, pad=3), "relu")
+        _, h, w = self.shapes[x]
+        h, w = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1
+        c = c0
+        buf = self.buffer(c + blocks[0] * growth, h, w)
+        self.pool("maxpool", x, 3, 2, 1, out=self.view(buf, 0, c))
+        for bi, nl in enumerate(blocks):
+            for _ in range(nl):
+                y = self.bn(self.view(buf, 0, c), "relu")
+                y = self.conv(y, bn_size * growth, 1)
+                y = self.bn(y, "relu")
+                self.conv(y, growth, 3, pad=1, out=self.view(buf, c, growth))
+                c += growth
+            if bi + 1 < len(blocks):
+                y = self.conv(self.bn(buf, "relu"), c // 2, 1)
+                c //= 2
+                h, w = h // 2, w // 2
+                nbuf = self.buffer(c + blocks[bi + 1] * growth, h, w)
+                self.pool("avgpool", y, 2, 2, out=self.view(nbuf, 0, c))
+                buf = nbuf
+        x = self.bn(buf, "relu")
         x = self.pool("avgpool", x, self.shapes[x][1], 1)
         self.logits = self.conv(x, self.classes, 1, bias=True, out_f32=True)
 
@@ -218,6 +261,40 @@ def _maxpool_arg(x, r, stride, pad):
     p = (h + 2 * pad - r) // stride + 1
     q = (w + 2 * pad - r) // stride + 1
     return val.view(n, c, p, q), arg.view(n, c, p, q)
+
+
+class Store(dict):
+    """name -> NCHW tensor, with channel views of concat buffers resolved to
+    slices of their base (writes go into the base)."""
+
+    def __init__(self, spec, batch):
+        super().__init__()
+        self.spec, self.batch = spec, batch
+
+    def _base(self, name):
+        base, ch0, c = self.spec.views[name]
+        if not dict.__contains__(self, base):
+            C, H, W = self.spec.shapes[base]
+            dict.__setitem__(self, base, torch.zeros(self.batch, C, H, W, dtype=torch.float64))
+        return dict.__getitem__(self, base), ch0, c
+
+    def __getitem__(self, name):
+        if name in self.spec.views:
+            b, ch0, c = self._base(name)
+            return b[:, ch0:ch0 + c]
+        return dict.__getitem__(self, name)
+
+    def __setitem__(self, name, value):
+        if name in self.spec.views:
+            b, ch0, c = self._base(name)
+            b[:, ch0:ch0 + c] = value
+        else:
+            dict.__setitem__(self, name, value)
+
+    def __contains__(self, name):
+        if name in self.spec.views:
+            return dict.__contains__(self, self.spec.views[name][0])
+        return dict.__contains__(self, name)
 
 
 def fwd_op(L, vals, T, mirror=True, train=True, run_stats=None):
@@ -348,7 +425,8 @@ def forward_backward(spec: Spec, params: dict, x, labels, mirror=True, run_stats
     (member-relative names).  Returns (loss, grads {name: np}, new run_stats)."""
     R = lambda t: _rnd(t, mirror)  # noqa: E731
     T = params_tensors(params, mirror)
-    vals = {"input": R(x)}
+    vals = Store(spec, x.shape[0])
+    vals["input"] = R(x)
     cache = {}
     rs_new = {} if run_stats is None else {k: (a.copy(), b.copy()) for k, (a, b) in
                                            run_stats.items()}
@@ -369,7 +447,8 @@ def forward_backward(spec: Spec, params: dict, x, labels, mirror=True, run_stats
     if not train:
         return loss, None, rs_new
     grads = {spec.layers[-1]["name"] + "/b": dbias}
-    gv = {spec.logits: d.view(b, -1, 1, 1)}
+    gv = Store(spec, b)
+    gv[spec.logits] = d.view(b, -1, 1, 1)
     for L in reversed(spec.layers):
         if L["y"] not in gv:
             continue

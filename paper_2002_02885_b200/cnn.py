@@ -67,7 +67,7 @@ class ConvArch:
     """A conv member's architecture (the conv counterpart of MLPArch,
     packing.py:32-38).  `image` is the (C, H, W) shape a dataset row holds in
     NCHW order; `width` is MobileNetV2's width multiplier."""
-    family: str                 # lenet5 | mobilenetv2 | resnet18
+    family: str                 # lenet5 | mobilenetv2 | resnet18 | densenet121
     classes: int = 10
     image: tuple = (3, 32, 32)
     width: float = 1.0
@@ -88,6 +88,8 @@ class TSpec:
     w: int
     c: int          # padded channels (multiple of 8)
     creal: int
+    base: str | None = None   # a view: channels [ch0, ch0 + c) of tensor `base`
+    ch0: int = 0
 
 
 @dataclass
@@ -134,7 +136,23 @@ class Net:
         self.n += 1
         return name
 
-    def conv(self, x, k, r, s=None, stride=1, pad=0, bias=False, act="none", out_f32=False):
+    def buffer(self, h, w, c):
+        """A tensor no op produces whole: a concat buffer written through views."""
+        name = f"B{sum(1 for n in self.tensors if n.startswith('B'))}"
+        self.tensors[name] = TSpec(h, w, c, c)
+        return name
+
+    def view(self, base, ch0, c):
+        """Channels [ch0, ch0 + c) of `base` (row stride = base's channels)."""
+        b = self.tensors[base]
+        if ch0 == 0 and c == b.c:
+            return base
+        name = f"{base}[{ch0}:{ch0 + c}]"
+        self.tensors[name] = TSpec(b.h, b.w, c, c, base=base, ch0=ch0)
+        return name
+
+    def conv(self, x, k, r, s=None, stride=1, pad=0, bias=False, act="none", out_f32=False,
+             out=None):
         s = r if s is None else s
         tx = self.tensors[x]
         kp = rup(k, 8)
@@ -150,8 +168,13 @@ class Net:
         if bias:
             ps.append(PSpec(f"{name}/b", "bias", (k,), (kp,), li))
         self.params += ps
-        y = f"{name}.y"
-        self.tensors[y] = TSpec(p, q, kp, k)
+        if out is not None:
+            t = self.tensors[out]
+            assert (t.h, t.w, t.c) == (p, q, kp), (out, t, p, q, kp)
+            y = out
+        else:
+            y = f"{name}.y"
+            self.tensors[y] = TSpec(p, q, kp, k)
         self.ops.append(Op("conv", name, x, y,
                            dict(k=kp, r=r, s=s, stride=stride, pad=pad, act=act,
                                 out_f32=out_f32, bias=bias),
@@ -184,13 +207,18 @@ class Net:
         self.ops.append(Op("dw", name, x, y, dict(r=r, s=r, stride=stride, pad=pad), [W.name]))
         return y
 
-    def pool(self, kind, x, r, stride, pad=0):
+    def pool(self, kind, x, r, stride, pad=0, out=None):
         tx = self.tensors[x]
         name = self._layer()
         p = (tx.h + 2 * pad - r) // stride + 1
         q = (tx.w + 2 * pad - r) // stride + 1
-        y = f"{name}.y"
-        self.tensors[y] = TSpec(p, q, tx.c, tx.creal)
+        if out is not None:
+            t = self.tensors[out]
+            assert (t.h, t.w, t.c) == (p, q, tx.c), (out, t, p, q)
+            y = out
+        else:
+            y = f"{name}.y"
+            self.tensors[y] = TSpec(p, q, tx.c, tx.creal)
         self.ops.append(Op(kind, name, x, y, dict(r=r, s=r, stride=stride, pad=pad)))
         return y
 
@@ -281,7 +309,41 @@ def _resnet18(net: Net):
     net.head(x)
 
 
-FAMILIES = {"lenet5": _lenet5, "mobilenetv2": _mobilenetv2, "resnet18": _resnet18}
+def _densenet121(net: Net, blocks=(6, 12, 24, 16), growth=32, bn_size=4, c0=64):
+    """torchvision DenseNet-121 topology (pre-activation dense layers, 2x2
+    average-pool transitions, norm5 + ReLU before the classifier).  The
+    concatenations are block buffers: every layer's 3x3 conv writes its
+    `growth` channels straight into its slice, and every BN reads a channel
+    prefix of the buffer (no copies)."""
+    x = net.bn(net.conv("input", c0, 7, stride=2, pad=3), "relu")
+    t = net.tensors[x]
+    h, w = (t.h + 2 - 3) // 2 + 1, (t.w + 2 - 3) // 2 + 1
+    c = c0
+    buf = net.buffer(h, w, c + blocks[0] * growth)
+    net.pool("maxpool", x, 3, 2, 1, out=net.view(buf, 0, c))
+    for bi, nl in enumerate(blocks):
+        for _ in range(nl):
+            y = net.bn(net.view(buf, 0, c), "relu")
+            y = net.conv(y, bn_size * growth, 1)
+            y = net.bn(y, "relu")
+            net.conv(y, growth, 3, pad=1, out=net.view(buf, c, growth))
+            c += growth
+        if bi + 1 < len(blocks):
+            y = net.bn(buf, "relu")
+            y = net.conv(y, c // 2, 1)
+            c //= 2
+            h, w = h // 2, w // 2
+            nbuf = net.buffer(h, w, c + blocks[bi + 1] * growth)
+            net.pool("avgpool", y, 2, 2, out=net.view(nbuf, 0, c))
+            buf = nbuf
+    x = net.bn(buf, "relu")
+    x = net.pool("avgpool", x, net.tensors[x].h, 1)
+    x = net.conv(x, net.arch.classes, 1, bias=True, out_f32=True)
+    net.head(x)
+
+
+FAMILIES = {"lenet5": _lenet5, "mobilenetv2": _mobilenetv2, "resnet18": _resnet18,
+            "densenet121": _densenet121}
 _NET_CACHE: dict = {}
 
 
@@ -595,8 +657,8 @@ class ConvPack:
         k = self.members.index(m)
         shared = self.first_shared.get(k)
         for name, t in net.tensors.items():
-            if name == "input":
-                continue
+            if name == "input" or t.base is not None:
+                continue  # the network input lives in the group batch buffer; views alias
             rows = b * t.h * t.w
             if name == net.logits:
                 A["val"][name] = z(rows, t.c)
@@ -722,6 +784,30 @@ class ConvPack:
         return from_dev_layout(p, self.grads[k][pname].cpu().numpy())
 
     # -- program construction -------------------------------------------------------
+    def _ptr(self, k, name, which):
+        """device address of tensor `name` ("val" or "grad") of member k; a
+        view points into its base buffer"""
+        t = self.members[k].net.tensors[name]
+        A = self.acts[k]
+        if t.base is not None:
+            return A[which][t.base].data_ptr() + 2 * t.ch0
+        return A[which][name].data_ptr()
+
+    def _ld(self, k, name):
+        """row (pixel) stride in elements of tensor `name` of member k"""
+        net = self.members[k].net
+        t = net.tensors[name]
+        return net.tensors[t.base].c if t.base is not None else t.c
+
+    def tensor(self, k, name, which, rows):
+        """[rows][c] torch view of a member tensor (tests / diagnostics)"""
+        net = self.members[k].net
+        t = net.tensors[name]
+        A = self.acts[k]
+        if t.base is not None:
+            return A[which][t.base][:rows, t.ch0:t.ch0 + t.c]
+        return A[which][name][:rows]
+
     def _counter(self, k, slot):
         """int32[17] ticket counters of (op, slot) of member k (tree_reduce)"""
         c = self.acts[k]["counters"]
@@ -741,17 +827,18 @@ class ConvPack:
             if op.kind == "conv":
                 ty = net.tensors[op.y]
                 first = op.x == "input"
-                src, fidx = self._input(lead, data) if first else (A["val"][op.x].data_ptr(), 0)
+                src, fidx = self._input(lead, data) if first else (self._ptr(k, op.x, "val"), 0)
                 cs = _lib.CnnConv()
                 cs.src = src
                 cs.idx = fidx
                 cs.wt = self.w16[k][op.params[0]].data_ptr()
-                cs.dst = A["val"][op.y].data_ptr()
+                cs.dst = self._ptr(k, op.y, "val")
                 cs.bias = self.params[k][op.params[1]].data_ptr() if op.a["bias"] else 0
                 cs.n, cs.h, cs.w, cs.c = take, tx.h, tx.w, tx.c
                 cs.k, cs.r, cs.s = ty.c, op.a["r"], op.a["s"]
                 cs.stride, cs.pad, cs.p, cs.q = op.a["stride"], op.a["pad"], ty.h, ty.w
-                cs.ldx, cs.ldo = tx.c, ty.c
+                cs.ldx = tx.c if first else self._ld(k, op.x)
+                cs.ldo = self._ld(k, op.y)
                 cs.act = CNN_ACT[op.a["act"]]
                 cs.out_f32 = int(op.a["out_f32"])
                 nt = _pick_ntile(ty.c)
@@ -776,10 +863,10 @@ class ConvPack:
             elif op.kind == "head":
                 t = net.tensors[op.x]
                 h = _lib.CnnHead()
-                h.logits = A["val"][op.x].data_ptr()
+                h.logits = self._ptr(k, op.x, "val")
                 h.labels = data.y.data_ptr()
                 h.idx = idx
-                h.dlogits = A["grad"][op.x].data_ptr()
+                h.dlogits = self._ptr(k, op.x, "grad")
                 last = net.ops[oi - 1]
                 h.dbias = self.grads[k][last.params[1]].data_ptr()
                 h.loss = self.state.data_ptr() + 16 * k + 12
@@ -806,12 +893,12 @@ class ConvPack:
         net, A = m.net, self.acts[k]
         tx = net.tensors[op.x]
         b = _lib.CnnBn()
-        b.x = A["val"][op.x].data_ptr()
-        b.res = A["val"][op.res].data_ptr() if op.res else 0
-        b.out = A["val"][op.y].data_ptr()
-        b.dout = A["grad"][op.y].data_ptr()
-        b.fout = A["val"][op.y].data_ptr()
-        b.dx = A["grad"][op.x].data_ptr()
+        b.x = self._ptr(k, op.x, "val")
+        b.res = self._ptr(k, op.res, "val") if op.res else 0
+        b.out = self._ptr(k, op.y, "val")
+        b.dout = self._ptr(k, op.y, "grad")
+        b.fout = self._ptr(k, op.y, "val")
+        b.dx = self._ptr(k, op.x, "grad")
         b.gamma = self.params[k][op.params[0]].data_ptr()
         b.beta = self.params[k][op.params[1]].data_ptr()
         b.dgamma = self.grads[k][op.params[0]].data_ptr()
@@ -824,7 +911,9 @@ class ConvPack:
         b.flag = self._flag(k)
         b.rows, b.c = rows, tx.c
         b.rpb = rows_per_block(rows, tx.c)
-        b.ldx = b.ldo = b.ldr = b.ldd = b.ldx2 = tx.c
+        b.ldx = b.ldx2 = self._ld(k, op.x)
+        b.ldo = b.ldd = self._ld(k, op.y)
+        b.ldr = self._ld(k, op.res) if op.res else 0
         b.act = CNN_ACT[op.a["act"]]
         b.eps, b.momentum = _BN_EPS, _BN_MOMENTUM
         return b
@@ -834,10 +923,10 @@ class ConvPack:
         net, A = m.net, self.acts[k]
         tx, ty = net.tensors[op.x], net.tensors[op.y]
         d = _lib.CnnDw()
-        d.x = A["val"][op.x].data_ptr()
+        d.x = self._ptr(k, op.x, "val")
         d.wt = self.w16[k][op.params[0]].data_ptr()
-        d.dy = A["grad"][op.y].data_ptr()
-        d.y = A["val"][op.y].data_ptr()
+        d.dy = self._ptr(k, op.y, "grad")
+        d.y = self._ptr(k, op.y, "val")
         d.dw = self.grads[k][op.params[0]].data_ptr()
         d.ws = A["ws"][op.name].data_ptr()
         d.counter = self._counter(k, 4 * net.ops.index(op))
@@ -845,7 +934,7 @@ class ConvPack:
         d.n, d.h, d.w, d.c = take, tx.h, tx.w, tx.c
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
-        d.ldx, d.ldy = tx.c, ty.c
+        d.ldx, d.ldy = self._ld(k, op.x), self._ld(k, op.y)
         d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
         return d
 
@@ -854,15 +943,15 @@ class ConvPack:
         net, A = m.net, self.acts[k]
         tx, ty = net.tensors[op.x], net.tensors[op.y]
         p = _lib.CnnPool()
-        p.x = A["val"][op.x].data_ptr()
-        p.y = A["val"][op.y].data_ptr()
-        p.dy = A["grad"][op.y].data_ptr()
-        p.dx = A["grad"][op.x].data_ptr()
+        p.x = self._ptr(k, op.x, "val")
+        p.y = self._ptr(k, op.y, "val")
+        p.dy = self._ptr(k, op.y, "grad")
+        p.dx = self._ptr(k, op.x, "grad")
         p.arg = A["arg"][op.name].data_ptr() if op.kind == "maxpool" else 0
         p.n, p.h, p.w, p.c = take, tx.h, tx.w, tx.c
         p.r, p.s, p.stride, p.pad, p.p, p.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
-        p.ldx, p.ldy = tx.c, ty.c
+        p.ldx, p.ldy = self._ld(k, op.x), self._ld(k, op.y)
         return p
 
     def _bwd_steps(self, k, take, lead, data):
@@ -870,12 +959,22 @@ class ConvPack:
         net, A = m.net, self.acts[k]
         idx = self.idx[lead].data_ptr()
         steps = []
-        written = set()   # tensors whose gradient buffer already holds a contribution
+        written = {}   # base tensor -> channel intervals whose gradient holds a contribution
 
         def acc(name):
-            a = name in written
-            written.add(name)
-            return int(a)
+            """1 if the gradient of `name` (a tensor or a channel view) already
+            holds a contribution — the next writer accumulates — else 0"""
+            t = net.tensors[name]
+            base = t.base or name
+            lo, hi = t.ch0, t.ch0 + t.c
+            iv = written.setdefault(base, [])
+            cov = sum(max(0, min(hi, b) - max(lo, a)) for a, b in iv)
+            if cov == hi - lo:
+                return 1
+            if cov == 0:
+                iv.append((lo, hi))
+                return 0
+            raise NotImplementedError(f"gradient of {name} is partially accumulated")
 
         for op in reversed(net.ops):
             tx = net.tensors[op.x] if op.x else None
@@ -887,13 +986,13 @@ class ConvPack:
                 if op.a["bias"] and not op.a["out_f32"]:
                     rows = take * ty.h * ty.w
                     bs = _lib.CnnBias()
-                    bs.dy = bs.g = A["grad"][op.y].data_ptr()
-                    bs.fout = A["val"][op.y].data_ptr()
+                    bs.dy = bs.g = self._ptr(k, op.y, "grad")
+                    bs.fout = self._ptr(k, op.y, "val")
                     bs.dbias = self.grads[k][op.params[1]].data_ptr()
                     bs.ws = A["ws"][op.name].data_ptr()
                     bs.counter = self._counter(k, 4 * net.ops.index(op) + 1)
                     bs.flag = self._flag(k)
-                    bs.rows, bs.c, bs.ld = rows, ty.c, ty.c
+                    bs.rows, bs.c, bs.ld = rows, ty.c, self._ld(k, op.y)
                     bs.rpb = rows_per_block(rows, ty.c)
                     bs.act = CNN_ACT[op.a["act"]]
                     steps.append((CNN["BIAS_ACT_BWD"], None, bs, None))
@@ -905,12 +1004,13 @@ class ConvPack:
                 splits = min(splits, bsplits) if op.name in A["split"] else 1
                 cs = _lib.CnnConv()
                 cs.src, cs.idx = self._input(lead, data) if first else (
-                    A["val"][op.x].data_ptr(), 0)
-                cs.dy = A["grad"][op.y].data_ptr()
+                    self._ptr(k, op.x, "val"), 0)
+                cs.dy = self._ptr(k, op.y, "grad")
                 cs.n, cs.h, cs.w, cs.c = take, tx.h, tx.w, tx.c
                 cs.k, cs.r, cs.s = ty.c, op.a["r"], op.a["s"]
                 cs.stride, cs.pad, cs.p, cs.q = op.a["stride"], op.a["pad"], ty.h, ty.w
-                cs.ldx, cs.ldy = tx.c, ty.c
+                cs.ldx = tx.c if first else self._ld(k, op.x)
+                cs.ldy = self._ld(k, op.y)
                 cs.flag = self._flag(k)
                 # fix the split count so the pixel partition is valid for this take
                 while splits > 1 and cdiv(pix, rup(cdiv(pix, splits), 64)) != splits:
@@ -930,13 +1030,13 @@ class ConvPack:
                     steps.append((CNN["SPLIT_REDUCE"], None, rd, None))
                 if not first:
                     ds = _lib.CnnConv()
-                    ds.src = A["grad"][op.y].data_ptr()
+                    ds.src = self._ptr(k, op.y, "grad")
                     ds.wt = self.wt16[k][op.params[0]].data_ptr()
-                    ds.dst = A["grad"][op.x].data_ptr()
+                    ds.dst = self._ptr(k, op.x, "grad")
                     ds.n, ds.h, ds.w, ds.c = take, tx.h, tx.w, tx.c
                     ds.k, ds.r, ds.s = ty.c, op.a["r"], op.a["s"]
                     ds.stride, ds.pad, ds.p, ds.q = op.a["stride"], op.a["pad"], ty.h, ty.w
-                    ds.ldy, ds.ldo = ty.c, tx.c
+                    ds.ldy, ds.ldo = self._ld(k, op.y), self._ld(k, op.x)
                     ds.accumulate = acc(op.x)
                     ntd = _pick_ntile(tx.c)
                     steps.append((CNN["CONV_DGRAD"], (ntd, _stages(ntd)), ds, None))
@@ -949,7 +1049,7 @@ class ConvPack:
                 b2.counter = self._counter(k, 4 * net.ops.index(op) + 1)
                 b2.accumulate = acc(op.x)
                 if op.res:
-                    b2.dres = A["grad"][op.res].data_ptr()
+                    b2.dres = self._ptr(k, op.res, "grad")
                     b2.res_accumulate = acc(op.res)
                 steps.append((CNN["BN_BWD_APPLY"], None, b2, None))
             elif op.kind == "dw":
@@ -957,7 +1057,7 @@ class ConvPack:
                 d.counter = self._counter(k, 4 * net.ops.index(op) + 1)
                 steps.append((CNN["DW_WGRAD"], None, d, None))
                 d2 = self._dw_struct(k, op, take)
-                d2.y = A["grad"][op.x].data_ptr()
+                d2.y = self._ptr(k, op.x, "grad")
                 if acc(op.x):
                     raise NotImplementedError("depthwise input with two consumers")
                 steps.append((CNN["DW_DGRAD"], None, d2, None))

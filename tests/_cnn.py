@@ -7,7 +7,9 @@ under a 1e-3 input perturbation).
 
 Stated bf16 tolerances (elementwise, `ref` = oracle of the same inputs):
   * bf16 activations:            |Δ| <= 2^-7 |ref| + 2e-3 max|ref|   (1-ulp flips)
-  * bf16 activation gradients:   |Δ| <= 2^-6 |ref| + 4e-3 max|ref|   (accumulated in bf16)
+  * bf16 activation gradients:   |Δ| <= 2^-7 (1 + √n) |ref| + 4e-3 max|ref|, n = the
+                                 contributions accumulated in bf16 into that tensor
+                                 (n = 1 → 2^-6; DenseNet block buffers take up to 17)
   * fp32 parameter gradients:    |Δ| <= 1e-3 |ref| + 1e-4 max|ref|,  normwise <= 1e-3
                                  (BN dgamma sums g·xhat with heavy cancellation)
   * fp32 logits / loss:          rel 1e-5
@@ -22,11 +24,11 @@ from oracle import cnn64 as O
 
 
 def dev_tensor(cp, k, name, which, take):
-    net = cp.members[k].net
-    t = net.tensors[name]
-    a = cp.acts[k][which][name]
+    """member k's tensor `name` (a view reads its slice of the base buffer) as
+    NCHW float64"""
+    t = cp.members[k].net.tensors[name]
     rows = take * t.h * t.w
-    v = a[:rows].float().cpu().numpy().astype(np.float64)
+    v = cp.tensor(k, name, which, rows).float().cpu().numpy().astype(np.float64)
     v = v.reshape(take, t.h, t.w, t.c)[..., :t.creal]
     return torch.from_numpy(np.ascontiguousarray(v.transpose(0, 3, 1, 2)))
 
@@ -72,18 +74,31 @@ def teacher_forced(cp, k, params_before, x, labels, take, loss_dev, report=None)
     _check(gdev[spec.logits].reshape(take, -1)[:, :spec.classes], d, 2.0 ** -7, 1e-3,
            "dlogits", report)
     pgrads = {spec.layers[-1]["name"] + "/b": dbias}
-    contrib = {}
+    contrib = {}   # base tensor -> summed input-gradient contributions (channel space)
+    ncontrib = {}
+
+    def add(n, t):
+        base, ch0 = n, 0
+        if n in spec.views:
+            base, ch0, _ = spec.views[n]
+        if base not in contrib:
+            C, H, W = spec.shapes[base]
+            contrib[base] = torch.zeros(take, C, H, W, dtype=torch.float64)
+        contrib[base][:, ch0:ch0 + t.shape[1]] += t
+        ncontrib[base] = ncontrib.get(base, 0) + 1
+
     for L in reversed(spec.layers):
         g, c, _ = O.bwd_op(L, gdev[L["y"]], vals, T, caches[L["name"]])
         pgrads.update(g)
         for n, t in c.items():
-            contrib[n] = t if n not in contrib else contrib[n] + t
+            add(n, t)
     producer = {L["y"]: L for L in spec.layers}
     for n, ref in contrib.items():
         L = producer.get(n)
         if L is not None and L["kind"] == "conv" and L["bias"] and not L["out_f32"]:
             ref = ref * O._dact(vals[n], L["act"])  # the device folds act' in place (BIAS_ACT_BWD)
-        _check(gdev[n], ref, 2.0 ** -6, 4e-3, "grad " + n, report)
+        got = gdev[n] if n in gdev else dev_tensor(cp, k, n, "grad", take)
+        _check(got, ref, 2.0 ** -7 * (1 + ncontrib[n] ** 0.5), 4e-3, "grad " + n, report)
     for p in m.net.params:
         got = torch.from_numpy(cp.grad_of(k, p.name))
         ref = pgrads[p.name]

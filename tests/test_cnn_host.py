@@ -16,37 +16,56 @@ from oracle import cnn64 as O
 from paper_2002_02885_b200 import _lib, cnn, packing
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-FAMS = [("lenet5", 32, 1.0), ("mobilenetv2", 32, 0.5), ("resnet18", 32, 1.0)]
+FAMS = [("lenet5", 32, 1.0), ("mobilenetv2", 32, 0.5), ("resnet18", 32, 1.0),
+        ("densenet121", 32, 1.0)]
 
 
 def _autograd(spec, params, x, y):
     """torch autograd over the same net (fp64, training-mode BN)."""
     P = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in params.items()}
     vals = {"input": x}
+    pieces = {}   # concat buffer -> [(ch0, tensor)] written so far (DenseNet)
+
+    def get(name):
+        if name in spec.views:
+            base, ch0, c = spec.views[name]
+            parts = sorted(pieces[base], key=lambda t: t[0])
+            return torch.cat([t for _, t in parts], dim=1)[:, ch0:ch0 + c]
+        if name in pieces:
+            return torch.cat([t for _, t in sorted(pieces[name], key=lambda t: t[0])], dim=1)
+        return vals[name]
+
+    def put(name, t):
+        if name in spec.views:
+            base, ch0, _ = spec.views[name]
+            pieces.setdefault(base, []).append((ch0, t))
+        else:
+            vals[name] = t
+
     for L in spec.layers:
-        n, xin = L["name"], vals[L["x"]]
+        n, xin = L["name"], get(L["x"])
         if L["kind"] == "conv":
             yv = F.conv2d(xin, P[n + "/W"].permute(0, 3, 1, 2), stride=L["stride"],
                           padding=L["pad"])
             if L["bias"]:
                 yv = yv + P[n + "/b"].view(1, -1, 1, 1)
-            vals[L["y"]] = O._act(yv, L["act"])
+            put(L["y"], O._act(yv, L["act"]))
         elif L["kind"] == "bn":
             m = xin.mean(dim=(0, 2, 3))
             v = xin.var(dim=(0, 2, 3), unbiased=False)
             yv = ((xin - m.view(1, -1, 1, 1)) / torch.sqrt(v.view(1, -1, 1, 1) + O.BN_EPS)
                   * P[n + "/gamma"].view(1, -1, 1, 1) + P[n + "/beta"].view(1, -1, 1, 1))
             if L["res"]:
-                yv = yv + vals[L["res"]]
-            vals[L["y"]] = O._act(yv, L["act"])
+                yv = yv + get(L["res"])
+            put(L["y"], O._act(yv, L["act"]))
         elif L["kind"] == "dw":
             vals[L["y"]] = F.conv2d(xin, P[n + "/W"].permute(2, 0, 1).unsqueeze(1),
                                     stride=L["stride"], padding=L["pad"], groups=L["c"])
         elif L["kind"] == "maxpool":
-            vals[L["y"]] = F.max_pool2d(xin, L["r"], L["stride"], L["pad"])
+            put(L["y"], F.max_pool2d(xin, L["r"], L["stride"], L["pad"]))
         elif L["kind"] == "avgpool":
-            vals[L["y"]] = F.avg_pool2d(xin, L["r"], L["stride"], L["pad"])
-    loss = F.cross_entropy(vals[spec.logits].reshape(x.shape[0], -1), y)
+            put(L["y"], F.avg_pool2d(xin, L["r"], L["stride"], L["pad"]))
+    loss = F.cross_entropy(get(spec.logits).reshape(x.shape[0], -1), y)
     loss.backward()
     return float(loss.detach()), {k: v.grad.numpy() for k, v in P.items()}
 
@@ -86,6 +105,7 @@ def test_planner_and_oracle_agree(fam, img, w):
 
 def test_param_counts_match_torchvision_topologies():
     assert cnn.build_net(cnn.ConvArch("lenet5")).param_count == 62006
+    assert cnn.build_net(cnn.ConvArch("densenet121", 1000, (3, 224, 224))).param_count == 7978856
     assert cnn.build_net(cnn.ConvArch("resnet18", 1000, (3, 224, 224))).param_count == 11689512
     # torchvision mobilenet_v2(width_mult=0.5, num_classes=10)
     assert cnn.build_net(cnn.ConvArch("mobilenetv2", 10, (3, 32, 32), 0.5)).param_count == 700490

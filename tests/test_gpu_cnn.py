@@ -49,7 +49,8 @@ def _batch(ds, arch, epoch, pos, take):
 
 
 @pytest.mark.parametrize("fam,K,b", [("lenet5", 2, 32), ("mobilenetv2", 2, 32),
-                                     ("resnet18", 2, 16), ("lenet5", 5, 20)])
+                                     ("resnet18", 2, 16), ("lenet5", 5, 20),
+                                     ("densenet121", 2, 8)])
 def test_teacher_forced_step(fam, K, b):
     arch = _arch(fam)
     ds = _ds()
@@ -162,3 +163,39 @@ def test_training_reduces_loss():
         last = packing.packed_step(packed, {"train": ds})
     for h in hs:
         assert last[h.model_id] < first[h.model_id], (first, last)
+
+
+def _hetero(prefix="h", b=8):
+    """BASELINE configs[3] shape at 32x32: MobileNetV2 + ResNet-18 + DenseNet-121
+    on one input stream (ragged grouped launches; ResNet and DenseNet share the
+    concatenated-N 7x7 stem)."""
+    out = []
+    for i, (fam, w, opt) in enumerate((("mobilenetv2", 1.0, "sgd"), ("resnet18", 1.0, "adam"),
+                                       ("densenet121", 1.0, "momentum"))):
+        arch = cnn.ConvArch(fam, 10, (3, 32, 32), w)
+        out.append(packing.make_handle(f"{prefix}{i}", arch, opt, 0.01, b, 20, "train", 0,
+                                       weight_decay=1e-4))
+    return out
+
+
+def test_heterogeneous_pack_teacher_forced_and_standalone():
+    ds = _ds()
+    hs = _hetero()
+    before = [{n.split("/", 1)[1]: v.copy() for n, v in h.params.items()} for h in hs]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    losses = packing.packed_step(packed, {"train": ds})
+    assert packed.last_step_stats == {"physical_inputs": 1, "groups": 1, "driver_batch": 8}
+    x, y = _batch(ds, hs[0].arch, 0, 0, 8)
+    for k, h in enumerate(hs):
+        _cnn.teacher_forced(packed._cp, k, before[k], x, y, 8, losses[h.model_id])
+    solo = _hetero()
+    for h in solo:
+        assert packing.standalone_step(h, {"train": ds}) == losses[h.model_id]
+    for _ in range(2):
+        lp = packing.packed_step(packed, {"train": ds})
+        for h in solo:
+            assert packing.standalone_step(h, {"train": ds}) == lp[h.model_id]
+    for a, s_ in zip(hs, solo):
+        pa, ps = a.params, s_.params
+        for n in pa:
+            assert np.array_equal(pa[n], ps[n]), n

@@ -33,6 +33,12 @@ WORKLOADS = {
                           batch=128, K=16, sweep=(2, 4, 8, 16),
                           members=[(OPTS[i % 4], 10.0 ** -(1 + i % 4), 0.0)
                                    for i in range(16)]),
+    # configs[3]: heterogeneous MobileNetV2 + ResNet-18 + DenseNet-121 on one input stream
+    "config3": dict(family="hetero", width=1.0, image=(3, 224, 224), classes=1000, n=256,
+                    batch=32, K=3, sweep=(3,),
+                    archs=[("mobilenetv2", 1.0), ("resnet18", 1.0), ("densenet121", 1.0)],
+                    members=[("momentum", 0.05, 1e-4), ("momentum", 0.1, 1e-4),
+                             ("momentum", 0.1, 1e-4)]),
     # configs[2]: K = 4 ResNet-18 variants differing in lr / weight decay, 224², b = 32
     "config2": dict(family="resnet18", width=1.0, image=(3, 224, 224), classes=1000, n=512,
                     batch=32, K=4, sweep=(2, 4),
@@ -48,11 +54,16 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
+def _arch(wl, cnn, i):
+    fam, width = wl["archs"][i] if "archs" in wl else (wl["family"], wl["width"])
+    return cnn.ConvArch(fam, wl["classes"], tuple(wl["image"]), width)
+
+
 def _handles(wl, packing, cnn, K=None, prefix="m"):
-    arch = cnn.ConvArch(wl["family"], wl["classes"], tuple(wl["image"]), wl["width"])
     ms = wl["members"][:K or wl["K"]]
-    return arch, [packing.make_handle(f"{prefix}{i}", arch, o, lr, wl["batch"], 10 ** 9, "train",
-                                      i, weight_decay=wd) for i, (o, lr, wd) in enumerate(ms)]
+    return _arch(wl, cnn, 0), [
+        packing.make_handle(f"{prefix}{i}", _arch(wl, cnn, i), o, lr, wl["batch"], 10 ** 9,
+                            "train", i, weight_decay=wd) for i, (o, lr, wd) in enumerate(ms)]
 
 
 # ---------------------------------------------------------------- work model --
@@ -252,6 +263,7 @@ def run_b200(args, world, rank, local, Clocks, flush_bytes):
         "data": "synthetic (reference synth_dataset, seeded, spread 1.0; rows read as NCHW "
                 "images), random-init weights (the reference's Xavier draw per member)",
         "config": {"workload": args.workload, "family": wl["family"], "width": wl["width"],
+                   "archs": wl.get("archs"),
                    "image": list(wl["image"]), "classes": wl["classes"], "members": K,
                    "batch": b, "optimizers": [o for o, _, _ in wl["members"][:K]],
                    "lr": [lr for _, lr, _ in wl["members"][:K]],
@@ -302,7 +314,10 @@ def cpu_baseline(workload, seconds=10.0, steps=None):
     c, h, w = wl["image"]
     b = wl["batch"]
     ds = data.synth_dataset(max(b, 64), c * h * w, wl["classes"], seed=0, spread=1.0)
-    spec = O.Spec(wl["family"], wl["classes"], tuple(wl["image"]), wl["width"])
+    specs = [O.Spec(*(wl["archs"][i] if "archs" in wl else (wl["family"], wl["width"]))[:1],
+                    wl["classes"], tuple(wl["image"]),
+                    (wl["archs"][i] if "archs" in wl else (wl["family"], wl["width"]))[1])
+             for i in range(wl["K"])]
     rows = np.arange(b) % ds.n
     x = O.batch_images(ds.features, wl["image"], rows)
     y = torch.from_numpy(ds.labels[rows].astype(np.int64))
@@ -311,6 +326,7 @@ def cpu_baseline(workload, seconds=10.0, steps=None):
     while True:
         i = done % wl["K"]
         o, lr, wd = wl["members"][i]
+        spec = specs[i]
         p = spec.init(f"m{i}", i)
         t1 = time.perf_counter()
         _, g, _ = O.forward_backward(spec, p, x, y, mirror=False)
