@@ -434,6 +434,20 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
 SLOTS = {"sgd": (), "momentum": ("velocity",), "adagrad": ("accum",), "adam": ("m", "v")}
 
 
+def member_device_bytes(net: Net, optimizer: str, batch: int) -> int:
+    """HBM a conv member occupies in a pack (ConvPack allocations): fp32
+    masters, gradients and slots, bf16 GEMM mirrors, bf16 activations and
+    their gradients for `batch` rows, BN statistics / workspaces (~5 %)."""
+    P = sum(p.numel for p in net.params)
+    mirrors = sum(2 * p.numel for p in net.params if p.w16) * 2
+    act = 0
+    for name, t in net.tensors.items():
+        if name == "input" or t.base is not None:
+            continue
+        act += batch * t.h * t.w * t.c * 2 * 2
+    return int((4 * P * (2 + len(SLOTS[optimizer])) + mirrors + act) * 1.05)
+
+
 # =============================================================================
 # Device pack: buffers + programs
 # =============================================================================
@@ -562,6 +576,7 @@ class ConvPack:
         z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=self.dev)  # noqa: E731
         self._z = z
         self.state = z(K, 4, dt=torch.int32)        # step, flag, verdict, loss bits
+        self.eval_loss = z(K)                        # eval-program loss per member
         # batch image indices, one buffer per member; a step's program reads the
         # buffer of each input group's leader (the first member of the group)
         self.idx = [z(m.batch, dt=torch.int64) for m in members]
@@ -816,8 +831,10 @@ class ConvPack:
     def _flag(self, k):
         return self.state.data_ptr() + 16 * k + 4
 
-    def _fwd_steps(self, k, take, lead, data):
-        """Per-member forward kernel steps: list of (kind, cfg, struct, tag)."""
+    def _fwd_steps(self, k, take, lead, data, train=True):
+        """Per-member forward kernel steps: list of (kind, cfg, struct, tag).
+        train=False: the eval forward (BN normalises with the running
+        statistics and leaves them untouched; the head only sums the loss)."""
         m = self.members[k]
         net, A = m.net, self.acts[k]
         steps = []
@@ -843,14 +860,15 @@ class ConvPack:
                 cs.out_f32 = int(op.a["out_f32"])
                 nt = _pick_ntile(ty.c)
                 tag = None
-                if first and k in self.first_shared:
+                if train and first and k in self.first_shared:
                     gi2, li, j, ks = self.first_shared[k]
                     tag = ("first", gi2, li, j, lead)
                 steps.append((CNN["CONV_FPROP"], (nt, _stages(nt)), cs, tag))
             elif op.kind == "bn":
                 rows = take * tx.h * tx.w
-                for kind in ("BN_STATS", "BN_APPLY"):
+                for kind in ("BN_STATS", "BN_APPLY") if train else ("BN_APPLY",):
                     b = self._bn_struct(k, op, rows)
+                    b.use_running = 0 if train else 1
                     steps.append((CNN[kind], None, b, None))
             elif op.kind == "dw":
                 ty = net.tensors[op.y]
@@ -866,11 +884,14 @@ class ConvPack:
                 h.logits = self._ptr(k, op.x, "val")
                 h.labels = data.y.data_ptr()
                 h.idx = idx
-                h.dlogits = self._ptr(k, op.x, "grad")
                 last = net.ops[oi - 1]
-                h.dbias = self.grads[k][last.params[1]].data_ptr()
-                h.loss = self.state.data_ptr() + 16 * k + 12
-                h.flag = self._flag(k)
+                if train:
+                    h.dlogits = self._ptr(k, op.x, "grad")
+                    h.dbias = self.grads[k][last.params[1]].data_ptr()
+                    h.loss = self.state.data_ptr() + 16 * k + 12
+                    h.flag = self._flag(k)
+                else:
+                    h.loss = self.eval_loss.data_ptr() + 4 * k
                 h.rows, h.classes, h.ldl = take, op.a["classes"], t.c
                 steps.append((CNN["XENT"], None, h, None))
         return steps
@@ -1206,6 +1227,37 @@ class ConvPack:
                 ops.append((CNN["PUBLISH_T"], None, [st for _, _, st, _ in pub]))
             ops.append((CNN["COMMIT"], (1, 0), cm))
         return ops
+
+    def eval_program(self, k, take, data):
+        """forward-only program of member k on `take` rows (its own batch buffer
+        as the input group): the validation loss of tuner.py:460-464"""
+        key = ("eval", k, take, id(data))
+        pr = self._progs.get(key)
+        if pr is None:
+            g = _lib.CnnGather()
+            g.src = data.x.data_ptr()
+            g.dst = self._input(k, data)[0]
+            g.idx = self.idx[k].data_ptr()
+            g.row_bytes, g.rows = data.row_bytes, take
+            ops = [(CNN["GATHER"], None, [g])]
+            ops += self._group([self._fwd_steps(k, take, k, data, train=False)])
+            pr = CnnProgram(ops, self.device)
+            self._progs[key] = pr
+        return pr
+
+    def val_loss(self, k, data, rows_dev, n):
+        """mean softmax cross-entropy of member k over dataset rows rows_dev[:n]
+        (device int64), in chunks of its batch size; BN in eval mode."""
+        torch = self.torch
+        b = self.members[k].batch
+        tot = 0.0
+        with torch.cuda.stream(self.stream):
+            for i0 in range(0, n, b):
+                take = min(b, n - i0)
+                self.idx[k][:take].copy_(rows_dev[i0:i0 + take], non_blocking=True)
+                self.eval_program(k, take, data).run(self.stream.cuda_stream)
+                tot += float(self.eval_loss[k].item()) * take
+        return tot / n
 
     def program(self, takes, leads, data):
         """The step program for per-member valid rows `takes` (0 = inactive)

@@ -199,3 +199,25 @@ def test_heterogeneous_pack_teacher_forced_and_standalone():
         pa, ps = a.params, s_.params
         for n in pa:
             assert np.array_equal(pa[n], ps[n]), n
+
+
+def test_conv_hyperband_packed_matches_unpacked():
+    """BASELINE configs[4] at toy scale: pack-aware Hyperband (tuner.py:285-337)
+    over LeNet-5 members with the conv executor.  Every config trains the same
+    trajectory packed (knn groups) or alone (original) — the kernels are
+    K-invariant — so records (config, rung epochs, loss) and the selected
+    config are identical across strategies."""
+    from paper_2002_02885_b200 import tuner
+    ds = data.synth_dataset(400, 3 * 32 * 32, 10, seed=5, spread=1.0)
+    res = {}
+    for strat in ("original", "knn"):
+        ex = tuner.B200ConvExecutor(ds, family="lenet5", width=1.0, seed=0)
+        res[strat] = tuner.packed_hyperband(9, 3, ex, seed=1, strategy=strat)
+    key = lambda r: sorted((x.config_id, x.epochs, x.loss) for x in r.records)  # noqa: E731
+    assert key(res["original"]) == key(res["knn"])
+    assert res["original"].best_config.config_id == res["knn"].best_config.config_id
+    assert all(np.isfinite(x.loss) for x in res["knn"].records)
+    sizes = {}
+    for x in res["knn"].records:
+        sizes[(x.bracket, x.rung, x.group)] = sizes.get((x.bracket, x.rung, x.group), 0) + 1
+    assert max(sizes.values()) >= 2  # knn really packed members
