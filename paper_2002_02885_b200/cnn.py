@@ -493,7 +493,15 @@ class DeviceConvDataset:
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
-def rows_per_block(rows, c=8, per_thread=4):
+def _cgp(c):
+    """channel groups (of 8) rounded up to a power of two (csrc lanes_of)"""
+    g = 1
+    while g < max(1, c // 8):
+        g *= 2
+    return g
+
+
+def rows_per_block(rows, c=8, per_thread=8):
     """Rows per partial block of a column reduction over `c` channels: a
     function of the member's own shape only (K-invariant).  Each of a block's
     256/pow2(c/8) row lanes sums ~`per_thread` rows; at most 256 blocks (the
@@ -710,7 +718,7 @@ class ConvPack:
                 ty = net.tensors[op.y]
                 pix = b * ty.h * ty.w
                 nout = op.a["r"] * op.a["s"] * tx.c
-                A["ws"][op.name] = z(_red_ws(nout, red_blocks_max(pix, nout), nout))
+                A["ws"][op.name] = z(_red_ws(nout, 256, nout))  # <= 256 blocks either path
             elif op.kind == "maxpool":
                 ty = net.tensors[op.y]
                 A["arg"][op.name] = z(b * ty.h * ty.w * ty.c, dt=torch.uint8)
@@ -956,7 +964,15 @@ class ConvPack:
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
         d.ldx, d.ldy = self._ld(k, op.x), self._ld(k, op.y)
-        d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
+        if d.r == 3 and d.s == 3 and d.stride in (1, 2) and tx.c <= 512:
+            # 3x3 fast path (csrc/pk_cnn_ops.cuh dw_fast_wgrad): ~16 K channel-pixels
+            # per block (<= 256 blocks), a multiple of the block's pixel lanes
+            lanes = (256 // _cgp(tx.c)) // 3
+            pix = take * ty.h * ty.w
+            nblk = min(256, max(1, cdiv(pix * tx.c, 16384)))
+            d.ppb = rup(cdiv(pix, nblk), lanes)
+        else:
+            d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
         return d
 
     def _pool_struct(self, k, op, take):

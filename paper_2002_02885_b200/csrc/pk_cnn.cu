@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "packtrain_b200.h"
@@ -151,6 +152,11 @@ size_t prob_size(int kind) {
 }
 
 long long items(long long rows, int c) { return rows * (c / 8); }
+int cgp_of(int c) {  // channel groups rounded up to a power of two (cnn::lanes_of)
+  int g = 1;
+  while (g < c / 8) g <<= 1;
+  return g;
+}
 int blocks_of(long long n) { return (int)((n + cnn::kBlock - 1) / cnn::kBlock); }
 
 // blocks one problem of a non-conv kind needs
@@ -164,15 +170,13 @@ int prob_blocks(int kind, const void* pr) {
     case PK_CNN_BN_APPLY:
     case PK_CNN_BN_BWD_APPLY: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
-      return blocks_of(items(cdiv(P.rows, cnn::kApplyRows), P.c));
+      return cnn::apply_blocks(P.rows, P.c);
     }
-    case PK_CNN_DW_FPROP: {
-      const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
-      return blocks_of(items((long long)P.n * P.p * P.q, P.c));
-    }
+    case PK_CNN_DW_FPROP:
     case PK_CNN_DW_DGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
-      return blocks_of(items((long long)P.n * P.h * P.w, P.c));
+      return blocks_of(items((long long)P.n * (kind == PK_CNN_DW_FPROP ? P.p * P.q : P.h * P.w),
+                             P.c));
     }
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
@@ -238,8 +242,10 @@ std::string check_prob(int kind, const void* pr) {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
       if (kind == PK_CNN_DW_WGRAD &&
-          (P.ppb < 1 || cdiv((long long)P.n * P.p * P.q, P.ppb) > cnn::kRedMaxBlocks))
-        return "dw: pixels per block >= 1, <= 256 blocks";
+          (P.ppb < 1 || prob_blocks(kind, pr) > cnn::kRedMaxBlocks ||
+           (cnn::dw_fast(P, kind) && P.ppb % cnn::dw_wgrad_lanes(cgp_of(P.c)))))
+        return "dw: units/pixels per block >= 1 (3x3: a multiple of the unit lanes), <= 256 "
+               "blocks";
       break;
     }
     case PK_CNN_MAXPOOL_FWD:
@@ -440,6 +446,30 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
   return PK_OK;
 }
 
+// Every launch of a step program after its first carries the programmatic-
+// stream-serialization attribute (PDL): the kernels open with pdl_gate(), so the
+// next launch is placed while the current one drains.  t_pdl is cleared at the
+// start of a program (its first launch follows unrelated stream work) and by the
+// per-op profiler / the single-GEMM test entry (events between launches).
+thread_local bool t_pdl = false;
+
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = t_pdl ? 1 : 0;
+  t_pdl = true;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int MODE>
 cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
   static bool attr_set = false, attr_set_p = false;
@@ -451,9 +481,8 @@ cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       attr_set_p = true;
     }
-    cg::k_conv_gemm_p<MODE>
-        <<<L.grid, cg::kThreads, cg::smem_bytes(L.ntile, L.stages), st>>>(L);
-    return cudaGetLastError();
+    return launch_k(cg::k_conv_gemm_p<MODE>, L.grid, cg::kThreads,
+                    cg::smem_bytes(L.ntile, L.stages), st, L);
   }
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm<MODE>,
@@ -461,8 +490,8 @@ cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  cg::k_conv_gemm<MODE><<<L.total_tiles, cg::kThreads, cg::smem_bytes(L.ntile, L.stages), st>>>(L);
-  return cudaGetLastError();
+  return launch_k(cg::k_conv_gemm<MODE>, L.total_tiles, cg::kThreads,
+                  cg::smem_bytes(L.ntile, L.stages), st, L);
 }
 
 template <class P>
@@ -478,9 +507,8 @@ cudaError_t launch_packs(const OpRec& o, void (*kern)(cnn::Pack<T>), cudaStream_
                          int smem = 0) {
   for (size_t i = 0; i < o.packs.size(); ++i) {
     if (o.pack_blocks[i] == 0) continue;
-    kern<<<o.pack_blocks[i], cnn::kBlock, smem, st>>>(
-        *reinterpret_cast<const cnn::Pack<T>*>(o.packs[i].data()));
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(kern, o.pack_blocks[i], cnn::kBlock, smem, st,
+                             *reinterpret_cast<const cnn::Pack<T>*>(o.packs[i].data()));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -522,17 +550,17 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
     case PK_CNN_XENT: return launch_packs<pk_cnn_head>(o, k_xent, st, o.ntile);
     case PK_CNN_BIAS_ACT_BWD: return launch_packs<pk_cnn_bias>(o, k_bias_act_bwd, st);
     case PK_CNN_SPLIT_REDUCE: return launch_packs<pk_cnn_reduce>(o, k_split_reduce, st);
-    case PK_CNN_OPT: k_opt<<<nb, kBlock, 0, st>>>(dp<pk_cnn_opt_seg>(g, o), db(g, o), np); break;
+    case PK_CNN_OPT: return launch_k(k_opt, nb, kBlock, 0, st, dp<pk_cnn_opt_seg>(g, o), db(g, o), np);
     case PK_CNN_PUBLISH_T: return launch_packs<pk_cnn_tpose>(o, k_publish_t, st);
     case PK_CNN_GATHER: return launch_packs<pk_cnn_gather>(o, k_gather, st);
     case PK_CNN_COMMIT:
-      k_commit<<<cdiv(np, 128), 128, 0, st>>>(dp<pk_cnn_commit>(g, o), np, o.ntile);
-      break;
+      return launch_k(k_commit, cdiv(np, 128), 128, 0, st, dp<pk_cnn_commit>(g, o), np, o.ntile);
   }
   return cudaGetLastError();
 }
 
 int run_all(pk_cnn_prog* g, cudaStream_t st) {
+  t_pdl = false;
   for (size_t i = 0; i < g->ops.size(); ++i) {
     cudaError_t e = run_op(g, g->ops[i], st);
     if (e != cudaSuccess)
@@ -710,6 +738,7 @@ extern "C" int pk_cnn_prog_profile(pk_cnn_prog* g, void* stream, float* op_ms) {
   int rc = PK_OK;
   cudaEventRecord(ev[0], st);
   for (size_t i = 0; i < n && rc == PK_OK; ++i) {
+    t_pdl = false;
     cudaError_t e = run_op(g, g->ops[i], st);
     if (e != cudaSuccess) rc = fail(PK_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ev[i + 1], st);

@@ -24,6 +24,19 @@ namespace cnn {
 
 constexpr int kBlock = 256;
 
+// Programmatic dependent launch (every launch of a step program after the
+// first carries the PDL attribute, pk_cnn.cu launch_k): a block first lets the
+// next launch of the chain start — its blocks are placed as SM resources free
+// up and park in griddepcontrol.wait — then waits for its predecessor's
+// completion and memory flush before it touches global data.  This hides the
+// launch + ramp of each of a step's few hundred launches behind the previous
+// one's tail.  A block waits unconditionally, so completion stays transitive
+// along the chain.  (Without the attribute both instructions are no-ops.)
+__device__ __forceinline__ void pdl_gate() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ int find_prob(const int* blk0, int nprob, int b) {
   int lo = 0, hi = nprob - 1;
   while (lo < hi) {
@@ -99,81 +112,104 @@ __device__ __forceinline__ float act_bwd(float out, int act) {
 }
 
 // ------------------------------------------------------------------------------
-// Column (channel) partial sums of up to two per-element quantities over rows
-// [r0, r1) of one block.  F(row, ch0, a[8], b[8]) fills the two values of the 8
-// channels ch0.. of `row`.  Writes ws[blk][2][c].
+// Row-strided column reductions.  Thread t owns channel group j = t % cgp
+// (cgp = pow2 >= c/8, 8 channels = one 16-byte vector) of row lane
+// rl = t / cgp, and visits rows r0 + rl, + nr, ... < r1 (nr = 256 / cgp),
+// kU rows per round with every load of the round issued before any use (the
+// memory-level parallelism these HBM/L2-bound kernels live on).  Per-thread
+// sums become the block's partial record in a fixed order (smem transpose, row
+// lanes summed in lane order), so a block's record depends only on its rows.
 // ------------------------------------------------------------------------------
-template <class F>
-__device__ __forceinline__ void col_partials(int r0, int r1, int c, int blk, float* ws, F f) {
-  __shared__ float sh[2][2048];
-  const int cgs = c >> 3;
-  int cgp = 1;  // channel groups rounded up to a power of two (<= 256)
-  while (cgp < cgs) cgp <<= 1;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int j = t & (cgp - 1), rl = t / cgp, nr = kBlock / cgp;
-  float s1[8], s2[8];
+constexpr int kU = 4;
+
+struct Lanes {
+  int cgs, cgp, rl, nr, ch;
+  bool on;
+};
+__device__ __forceinline__ Lanes lanes_of(int c) {
+  Lanes L;
+  L.cgs = c >> 3;
+  L.cgp = 1;
+  while (L.cgp < L.cgs) L.cgp <<= 1;
+  const int t = threadIdx.x, j = t & (L.cgp - 1);
+  L.rl = t / L.cgp;
+  L.nr = kBlock / L.cgp;
+  L.ch = 8 * j;
+  L.on = j < L.cgs;
+  return L;
+}
+
+__device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
-  if (j < cgs) {
-#pragma unroll 4
-    for (int r = r0 + rl; r < r1; r += nr) {
-      float a[8], b[8];
-      f(r, 8 * j, a, b);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        s1[e] += a[e];
-        s2[e] += b[e];
-      }
-    }
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
   }
-  if (cgp <= 32) {
-    // lanes l, l ^ cgp, l ^ 2cgp, ... of a warp share channel group j: fixed xor tree
-    for (int o = 16; o >= cgp; o >>= 1) {
+}
+__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        s1[e] += __shfl_xor_sync(0xffffffffu, s1[e], o);
-        s2[e] += __shfl_xor_sync(0xffffffffu, s2[e], o);
-      }
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  return u;
+}
+
+// Σ over the block's row lanes of s1 / s2 → out[0..c) / out[c..2c).
+__device__ __forceinline__ void block_colsum2(const Lanes& L, int c, const float (&s1)[8],
+                                              const float (&s2)[8], float* out) {
+  __shared__ __align__(16) float sh[2 * 2048];  // nr * 2c <= 4096
+  const int n2 = 2 * c;
+  if (L.on) {
+    float4* d1 = reinterpret_cast<float4*>(sh + L.rl * n2 + L.ch);
+    float4* d2 = reinterpret_cast<float4*>(sh + L.rl * n2 + c + L.ch);
+    d1[0] = make_float4(s1[0], s1[1], s1[2], s1[3]);
+    d1[1] = make_float4(s1[4], s1[5], s1[6], s1[7]);
+    d2[0] = make_float4(s2[0], s2[1], s2[2], s2[3]);
+    d2[1] = make_float4(s2[4], s2[5], s2[6], s2[7]);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < n2; o += kBlock) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int l = 0;
+    for (; l + 4 <= L.nr; l += 4) {
+      a0 += sh[l * n2 + o];
+      a1 += sh[(l + 1) * n2 + o];
+      a2 += sh[(l + 2) * n2 + o];
+      a3 += sh[(l + 3) * n2 + o];
     }
-    if (lane < cgp && j < cgs) {
+    for (; l < L.nr; ++l) a0 += sh[l * n2 + o];
+    out[o] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+// Row loop of a column reduction over NIN bf16 tensors: base[i] points at the
+// thread's channel group of row 0 of tensor i (pitch bytes per row).  fn(v)
+// folds row r's NIN vectors into the thread's sums.
+template <int NIN, class Fn>
+__device__ __forceinline__ void row_loop(const Lanes& L, int r0, int r1,
+                                         const uint8_t* const (&base)[NIN],
+                                         const size_t (&pitch)[NIN], Fn&& fn) {
+  if (!L.on) return;
+  int r = r0 + L.rl;
+  for (; r + (kU - 1) * L.nr < r1; r += kU * L.nr) {
+    uint4 v[kU][NIN];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        sh[0][warp * c + 8 * j + e] = s1[e];
-        sh[1][warp * c + 8 * j + e] = s2[e];
-      }
-    }
-    __syncthreads();
-    float* out = ws + (long long)blk * 2 * c;
-    for (int ch = t; ch < c; ch += kBlock) {
-      float a = 0.f, b = 0.f;
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
-      for (int w = 0; w < kBlock / 32; ++w) {
-        a += sh[0][w * c + ch];
-        b += sh[1][w * c + ch];
-      }
-      out[ch] = a;
-      out[c + ch] = b;
-    }
-  } else {
-    // nr (<= 4) row lanes, each a set of whole warps: combine through shared memory
-    if (j < cgs) {
+      for (int i = 0; i < NIN; ++i) v[u][i] = ldg16(base[i] + (size_t)(r + u * L.nr) * pitch[i]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        sh[0][rl * c + 8 * j + e] = s1[e];
-        sh[1][rl * c + 8 * j + e] = s2[e];
-      }
-    }
-    __syncthreads();
-    float* out = ws + (long long)blk * 2 * c;
-    for (int ch = t; ch < c; ch += kBlock) {
-      float a = 0.f, b = 0.f;
-      for (int l = 0; l < nr; ++l) {
-        a += sh[0][l * c + ch];
-        b += sh[1][l * c + ch];
-      }
-      out[ch] = a;
-      out[c + ch] = b;
-    }
+    for (int u = 0; u < kU; ++u) fn(v[u], r + u * L.nr);
+  }
+  for (; r < r1; r += L.nr) {
+    uint4 v[NIN];
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) v[i] = ldg16(base[i] + (size_t)r * pitch[i]);
+    fn(v, r);
   }
 }
 
@@ -228,200 +264,301 @@ __device__ __forceinline__ bool tree_reduce(float* ws, int blk, int nblk, int no
   return true;
 }
 
+// Partial records consumed by the NEXT kernel (BN statistics, BN backward):
+// every block writes its fp32 record ws[blk][nout]; when the member has more
+// than kRedGroup blocks, the last block of each group (ticket) also folds the
+// group's records, in block order, into an fp64 group record.  No second
+// ticket level: the consumer (the apply kernel) sums the <= kRedGroup records
+// of a column itself, in a fixed order — the same sums tree_reduce forms, one
+// dependent global round trip shorter on the producer's critical path.
+__device__ __forceinline__ void group_fold(float* ws, int blk, int nblk, int nout, int* counters) {
+  if (nblk <= kRedGroup) return;
+  const int grp = blk / kRedGroup;
+  const int b0 = grp * kRedGroup, b1 = min(nblk, b0 + kRedGroup);
+  double* grec = reinterpret_cast<double*>(ws + (((long long)nblk * nout + 1) & ~1LL));
+  if (!ticket(counters + 1 + grp, b1 - b0)) return;
+  for (int i = threadIdx.x; i < nout; i += kBlock) {
+    double v = 0.0;
+    for (int b = b0; b < b1; ++b) v += __ldcg(ws + (long long)b * nout + i);
+    grec[(long long)grp * nout + i] = v;
+  }
+}
+__device__ __forceinline__ double record_total(const float* ws, int nblk, int nout, int i) {
+  double v = 0.0;
+  if (nblk <= kRedGroup) {
+    for (int b = 0; b < nblk; ++b) v += __ldcg(ws + (long long)b * nout + i);
+  } else {
+    const double* grec =
+        reinterpret_cast<const double*>(ws + (((long long)nblk * nout + 1) & ~1LL));
+    const int ng = (nblk + kRedGroup - 1) / kRedGroup;
+    for (int g = 0; g < ng; ++g) v += __ldcg(grec + (long long)g * nout + i);
+  }
+  return v;
+}
+
 // ============================== batch norm =====================================
 __global__ void __launch_bounds__(kBlock, 3) k_bn_stats(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
   const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
-  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
-    ld8(bptr(P.x, r, P.ldx, ch), a);
+  const Lanes L = lanes_of(P.c);
+  float s1[8], s2[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) b[e] = a[e] * a[e];
-  });
-  double* tot;
-  if (!tree_reduce(P.ws, blk, nblk, 2 * P.c, 2 * P.c, P.counter, &tot)) return;
-  for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
-    const double mean = tot[ch] / P.rows;
-    const double var = fmax(tot[P.c + ch] / P.rows - mean * mean, 0.0);
-    P.stats[ch] = (float)mean;
-    P.stats[P.c + ch] = (float)(1.0 / sqrt(var + (double)P.eps));
-    if (P.run_mean) {
-      const double unb = P.rows > 1 ? var * P.rows / (P.rows - 1) : var;
-      P.run_mean[ch] = (float)((1.0 - P.momentum) * P.run_mean[ch] + P.momentum * mean);
-      P.run_var[ch] = (float)((1.0 - P.momentum) * P.run_var[ch] + P.momentum * unb);
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
+  const uint8_t* const base[1] = {static_cast<const uint8_t*>(P.x) + 2 * L.ch};
+  const size_t pitch[1] = {(size_t)P.ldx * 2};
+  row_loop<1>(L, r0, r1, base, pitch, [&](const uint4 (&v)[1], int) {
+    float a[8];
+    unpack8(v[0], a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      s1[e] += a[e];
+      s2[e] = fmaf(a[e], a[e], s2[e]);
     }
-  }
+  });
+  block_colsum2(L, P.c, s1, s2, P.ws + (size_t)blk * 2 * P.c);
+  group_fold(P.ws, blk, nblk, 2 * P.c, P.counter);
 }
 
-__device__ __forceinline__ void bn_coef(const pk_cnn_bn& P, int ch, float (&mean)[8],
-                                        float (&rs)[8]) {
-  if (P.use_running) {
-    float v[8];
-    ld8f(P.run_mean + ch, mean);
-    ld8f(P.run_var + ch, v);
+// g = dout · act'(fout); xhat = (x - mean)·rstd; partial sums of g and g·xhat
+__global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_reduce(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  pdl_gate();
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_bn& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
+  const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
+  const Lanes L = lanes_of(P.c);
+  float s1[8], s2[8], mean[8], rs[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) rs[e] = (float)(1.0 / sqrt((double)v[e] + (double)P.eps));
-  } else {
-    ld8f(P.stats + ch, mean);
-    ld8f(P.stats + P.c + ch, rs);
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
+  if (L.on) {
+    ld8f(P.stats + L.ch, mean);
+    ld8f(P.stats + P.c + L.ch, rs);
   }
+  auto fold = [&](const float (&d)[8], const float (&x)[8], const float* fo) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float g = fo ? d[e] * act_bwd(fo[e], P.act) : d[e];
+      s1[e] += g;
+      s2[e] = fmaf(g, (x[e] - mean[e]) * rs[e], s2[e]);
+    }
+  };
+  if (P.act != PK_CNN_ACT_NONE) {
+    const uint8_t* const base[3] = {static_cast<const uint8_t*>(P.dout) + 2 * L.ch,
+                                    static_cast<const uint8_t*>(P.x) + 2 * L.ch,
+                                    static_cast<const uint8_t*>(P.fout) + 2 * L.ch};
+    const size_t pitch[3] = {(size_t)P.ldd * 2, (size_t)P.ldx * 2, (size_t)P.ldo * 2};
+    row_loop<3>(L, r0, r1, base, pitch, [&](const uint4 (&v)[3], int) {
+      float d[8], x[8], fo[8];
+      unpack8(v[0], d);
+      unpack8(v[1], x);
+      unpack8(v[2], fo);
+      fold(d, x, fo);
+    });
+  } else {
+    const uint8_t* const base[2] = {static_cast<const uint8_t*>(P.dout) + 2 * L.ch,
+                                    static_cast<const uint8_t*>(P.x) + 2 * L.ch};
+    const size_t pitch[2] = {(size_t)P.ldd * 2, (size_t)P.ldx * 2};
+    row_loop<2>(L, r0, r1, base, pitch, [&](const uint4 (&v)[2], int) {
+      float d[8], x[8];
+      unpack8(v[0], d);
+      unpack8(v[1], x);
+      fold(d, x, nullptr);
+    });
+  }
+  block_colsum2(L, P.c, s1, s2, P.ws + (size_t)blk * 2 * P.c);
+  group_fold(P.ws, blk, nblk, 2 * P.c, P.counter);
 }
 
-constexpr int kApplyRows = 2;  // rows per thread in the BN apply kernels
+// ------------------------------------------------------------------------------
+// BN apply kernels: a block owns a tile of rows [r0, r0 + R) x channel groups
+// [g0, g0 + gw) (gw <= kApplyGroups), R = kApplyItems / min(cgs, kApplyGroups);
+// its per-channel coefficients are computed once into shared memory, then each
+// thread handles items t, t + 256, ... (kU of them, loads issued together).
+// ------------------------------------------------------------------------------
+constexpr int kApplyGroups = 32, kApplyItems = kU * kBlock;
+
+struct ApplyTile {
+  int r0, R, g0, gw;
+};
+__host__ __device__ __forceinline__ int apply_groups(int c) {
+  return (c >> 3) < kApplyGroups ? (c >> 3) : kApplyGroups;
+}
+__host__ __device__ __forceinline__ int apply_blocks(int rows, int c) {
+  const int G = apply_groups(c), R = kApplyItems / G;
+  return ((rows + R - 1) / R) * (((c >> 3) + G - 1) / G);
+}
+__device__ __forceinline__ ApplyTile apply_tile(int b, int rows, int c) {
+  const int cgs = c >> 3, G = apply_groups(c), ncg = (cgs + G - 1) / G;
+  ApplyTile T;
+  T.R = kApplyItems / G;
+  const int tr = b / ncg, tg = b - tr * ncg;
+  T.r0 = tr * T.R;
+  T.g0 = tg * G;
+  T.gw = min(G, cgs - T.g0);
+  return T;
+}
 
 __global__ void __launch_bounds__(kBlock, 4) k_bn_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
-  const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long rg = item / cgs;  // group of kApplyRows rows
-  if (rg * kApplyRows >= P.rows) return;
-  const int ch = 8 * (int)(item - rg * cgs);
-  float mean[8], rs[8], g[8], b[8];
-  bn_coef(P, ch, mean, rs);
-  ld8f(P.gamma + ch, g);
-  ld8f(P.beta + ch, b);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    g[e] *= rs[e];
-    b[e] -= mean[e] * g[e];  // y = x·(γ·rstd) + (β − mean·γ·rstd)
-  }
-  const long long r0 = rg * kApplyRows;
-  const int nr = (int)min((long long)kApplyRows, P.rows - r0);
-  float x[kApplyRows][8], res[kApplyRows][8];
-#pragma unroll
-  for (int i = 0; i < kApplyRows; ++i)
-    if (i < nr) {
-      ld8(bptr(P.x, r0 + i, P.ldx, ch), x[i]);
-      if (P.res) ld8(bptr(P.res, r0 + i, P.ldr, ch), res[i]);
-    }
-#pragma unroll
-  for (int i = 0; i < kApplyRows; ++i)
-    if (i < nr) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float y = fmaf(x[i][e], g[e], b[e]);
-        if (P.res) y += res[i][e];
-        x[i][e] = act_fwd(y, P.act);
+  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c);
+  __shared__ float scale[kApplyGroups * 8], shift[kApplyGroups * 8];
+  const int t = threadIdx.x;
+  if (t < T.gw * 8) {  // y = x·(γ·rstd) + (β − mean·γ·rstd)
+    const int ch = T.g0 * 8 + t;
+    float mean, rs;
+    if (P.use_running) {
+      mean = P.run_mean[ch];
+      rs = (float)(1.0 / sqrt((double)P.run_var[ch] + (double)P.eps));
+    } else {
+      // batch statistics from k_bn_stats' partial records; the tiles of row
+      // block 0 publish them (and the running statistics) exactly once
+      const int nblk = (P.rows + P.rpb - 1) / P.rpb;
+      const double dm = record_total(P.ws, nblk, 2 * P.c, ch) / P.rows;
+      const double var = fmax(record_total(P.ws, nblk, 2 * P.c, P.c + ch) / P.rows - dm * dm, 0.0);
+      mean = (float)dm;
+      rs = (float)(1.0 / sqrt(var + (double)P.eps));
+      if (T.r0 == 0) {
+        P.stats[ch] = mean;
+        P.stats[P.c + ch] = rs;
+        if (P.run_mean) {
+          const double unb = P.rows > 1 ? var * P.rows / (P.rows - 1) : var;
+          P.run_mean[ch] = (float)((1.0 - P.momentum) * P.run_mean[ch] + P.momentum * dm);
+          P.run_var[ch] = (float)((1.0 - P.momentum) * P.run_var[ch] + P.momentum * unb);
+        }
       }
-      st8(bptr(P.out, r0 + i, P.ldo, ch), x[i]);
     }
-}
-
-// g = dout · act'(fout); xhat = (x - mean)·rstd
-__device__ __forceinline__ void bn_g_xhat(const pk_cnn_bn& P, long long r, int ch, float (&g)[8],
-                                          float (&xh)[8]) {
-  float d[8], fo[8], x[8], mean[8], rs[8];
-  ld8(bptr(P.dout, r, P.ldd, ch), d);
-  ld8(bptr(P.x, r, P.ldx, ch), x);
-  ld8f(P.stats + ch, mean);
-  ld8f(P.stats + P.c + ch, rs);
-  if (P.act != PK_CNN_ACT_NONE) ld8(bptr(P.fout, r, P.ldo, ch), fo);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    g[e] = P.act != PK_CNN_ACT_NONE ? d[e] * act_bwd(fo[e], P.act) : d[e];
-    xh[e] = (x[e] - mean[e]) * rs[e];
+    const float g = P.gamma[ch] * rs;
+    scale[t] = g;
+    shift[t] = P.beta[ch] - mean * g;
   }
-}
-
-__global__ void __launch_bounds__(kBlock, 3) k_bn_bwd_reduce(const __grid_constant__ Pack<pk_cnn_bn> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_bn& P = G.p[pi];
-  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
-  const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
-  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
-    float xh[8];
-    bn_g_xhat(P, r, ch, a, xh);
+  __syncthreads();
+  const int nitems = T.R * T.gw;
+  int row[kU], cg[kU];
+  uint4 x[kU], rv[kU];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) b[e] = a[e] * xh[e];
-  });
-  double* tot;
-  if (!tree_reduce(P.ws, blk, nblk, 2 * P.c, 2 * P.c, P.counter, &tot)) return;
-  bool bad = false;
-  for (int ch = threadIdx.x; ch < P.c; ch += kBlock) {
-    const double s1 = tot[ch], s2 = tot[P.c + ch];
-    P.dbeta[ch] = (float)s1;
-    P.dgamma[ch] = (float)s2;
-    P.stats[2 * P.c + ch] = (float)(s1 / P.rows);
-    P.stats[3 * P.c + ch] = (float)(s2 / P.rows);
-    bad |= !isfinite(s1) || !isfinite(s2);
+  for (int u = 0; u < kU; ++u) {
+    const int i = t + u * kBlock, rr = i / T.gw;
+    row[u] = T.r0 + rr;
+    cg[u] = i - rr * T.gw;
+    if (i < nitems && row[u] < P.rows) {
+      const int ch = (T.g0 + cg[u]) * 8;
+      x[u] = ldg16(bptr(P.x, row[u], P.ldx, ch));
+      if (P.res) rv[u] = ldg16(bptr(P.res, row[u], P.ldr, ch));
+    } else {
+      row[u] = -1;
+    }
   }
-  if (bad) *P.flag = 1;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    if (row[u] < 0) continue;
+    float v[8], r[8];
+    unpack8(x[u], v);
+    if (P.res) unpack8(rv[u], r);
+    const float* sc = scale + 8 * cg[u];
+    const float* sf = shift + 8 * cg[u];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float y = fmaf(v[e], sc[e], sf[e]);
+      if (P.res) y += r[e];
+      v[e] = act_fwd(y, P.act);
+    }
+    *reinterpret_cast<uint4*>(bptr(P.out, row[u], P.ldo, (T.g0 + cg[u]) * 8)) = pack8(v);
+  }
 }
 
 __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
-  const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  const long long rg = item / cgs;
-  if (rg * kApplyRows >= P.rows) return;
-  const int ch = 8 * (int)(item - rg * cgs);
+  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c);
   // dx = γ·rstd·(g − mean(g) − xhat·mean(g·xhat)) = ca·g + cb·x + cc per channel
-  float ca[8], cb[8], cc[8];
-  {
-    float ga[8], mg[8], mgx[8], rs[8], mean[8];
-    ld8f(P.gamma + ch, ga);
-    ld8f(P.stats + ch, mean);
-    ld8f(P.stats + P.c + ch, rs);
-    ld8f(P.stats + 2 * P.c + ch, mg);
-    ld8f(P.stats + 3 * P.c + ch, mgx);
+  __shared__ float cas[kApplyGroups * 8], cbs[kApplyGroups * 8], ccs[kApplyGroups * 8];
+  const int t = threadIdx.x;
+  if (t < T.gw * 8) {
+    const int ch = T.g0 * 8 + t;
+    const float mean = P.stats[ch], rs = P.stats[P.c + ch];
+    // Σg and Σg·xhat from k_bn_bwd_reduce's partial records; the tiles of row
+    // block 0 publish dβ / dγ (and the non-finite flag) exactly once
+    const int nblk = (P.rows + P.rpb - 1) / P.rpb;
+    const double t1 = record_total(P.ws, nblk, 2 * P.c, ch);
+    const double t2 = record_total(P.ws, nblk, 2 * P.c, P.c + ch);
+    const float mg = (float)(t1 / P.rows), mgx = (float)(t2 / P.rows);
+    if (T.r0 == 0) {
+      P.dbeta[ch] = (float)t1;
+      P.dgamma[ch] = (float)t2;
+      if (!isfinite(t1) || !isfinite(t2)) *P.flag = 1;
+    }
+    const float ca = P.gamma[ch] * rs, cb = -ca * rs * mgx;
+    cas[t] = ca;
+    cbs[t] = cb;
+    ccs[t] = -ca * mg - cb * mean;
+  }
+  __syncthreads();
+  const bool act = P.act != PK_CNN_ACT_NONE;
+  const int nitems = T.R * T.gw;
+  int row[kU], cg[kU];
+  uint4 d[kU], x[kU], fo[kU];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      ca[e] = ga[e] * rs[e];
-      cb[e] = -ca[e] * rs[e] * mgx[e];
-      cc[e] = -ca[e] * mg[e] - cb[e] * mean[e];
+  for (int u = 0; u < kU; ++u) {
+    const int i = t + u * kBlock, rr = i / T.gw;
+    row[u] = T.r0 + rr;
+    cg[u] = i - rr * T.gw;
+    if (i < nitems && row[u] < P.rows) {
+      const int ch = (T.g0 + cg[u]) * 8;
+      d[u] = ldg16(bptr(P.dout, row[u], P.ldd, ch));
+      x[u] = ldg16(bptr(P.x, row[u], P.ldx, ch));
+      if (act) fo[u] = ldg16(bptr(P.fout, row[u], P.ldo, ch));
+    } else {
+      row[u] = -1;
     }
   }
-  const long long r0 = rg * kApplyRows;
-  const int nr = (int)min((long long)kApplyRows, P.rows - r0);
-  const bool act = P.act != PK_CNN_ACT_NONE;
-  // all loads of the thread's rows first (memory-level parallelism), then math
-  float d[kApplyRows][8], x[kApplyRows][8], fo[kApplyRows][8];
 #pragma unroll
-  for (int i = 0; i < kApplyRows; ++i)
-    if (i < nr) {
-      ld8(bptr(P.dout, r0 + i, P.ldd, ch), d[i]);
-      ld8(bptr(P.x, r0 + i, P.ldx, ch), x[i]);
-      if (act) ld8(bptr(P.fout, r0 + i, P.ldo, ch), fo[i]);
-    }
-#pragma unroll
-  for (int i = 0; i < kApplyRows; ++i) {
-    if (i >= nr) break;
-    const long long r = r0 + i;
-    float dx[8];
+  for (int u = 0; u < kU; ++u) {
+    if (row[u] < 0) continue;
+    const int ch = (T.g0 + cg[u]) * 8;
+    float g[8], xv[8], f[8], dx[8];
+    unpack8(d[u], g);
+    unpack8(x[u], xv);
+    if (act) unpack8(fo[u], f);
+    const float* ca = cas + 8 * cg[u];
+    const float* cb = cbs + 8 * cg[u];
+    const float* cc = ccs + 8 * cg[u];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float g = act ? d[i][e] * act_bwd(fo[i][e], P.act) : d[i][e];
-      dx[e] = fmaf(ca[e], g, fmaf(cb[e], x[i][e], cc[e]));
-      d[i][e] = g;
+      if (act) g[e] *= act_bwd(f[e], P.act);
+      dx[e] = fmaf(ca[e], g[e], fmaf(cb[e], xv[e], cc[e]));
     }
+    uint8_t* pdx = bptr(P.dx, row[u], P.ldx2, ch);
     if (P.accumulate) {
       float o[8];
-      ld8(bptr(P.dx, r, P.ldx2, ch), o);
+      ld8(pdx, o);
 #pragma unroll
       for (int e = 0; e < 8; ++e) dx[e] += o[e];
     }
-    st8(bptr(P.dx, r, P.ldx2, ch), dx);
+    *reinterpret_cast<uint4*>(pdx) = pack8(dx);
     if (P.dres) {
+      uint8_t* pr = bptr(P.dres, row[u], P.ldr, ch);
       if (P.res_accumulate) {
         float o[8];
-        ld8(bptr(P.dres, r, P.ldr, ch), o);
+        ld8(pr, o);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) d[i][e] += o[e];
+        for (int e = 0; e < 8; ++e) g[e] += o[e];
       }
-      st8(bptr(P.dres, r, P.ldr, ch), d[i]);
+      *reinterpret_cast<uint4*>(pr) = pack8(g);
     }
   }
 }
 
 // ============================ depthwise conv =====================================
-__global__ void __launch_bounds__(kBlock) k_dw_fprop(const __grid_constant__ Pack<pk_cnn_dw> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_dw& P = G.p[pi];
+// generic shapes: one thread per (output pixel, channel group)
+__device__ __forceinline__ void dw_fprop_items(const pk_cnn_dw& P, int blk) {
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)blk * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.p * P.q;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -447,11 +584,9 @@ __global__ void __launch_bounds__(kBlock) k_dw_fprop(const __grid_constant__ Pac
   st8(bptr(P.y, m, P.ldy, ch), acc);
 }
 
-__global__ void __launch_bounds__(kBlock) k_dw_dgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_dw& P = G.p[pi];
+__device__ __forceinline__ void dw_dgrad_items(const pk_cnn_dw& P, int blk) {
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
+  const long long item = (long long)blk * kBlock + threadIdx.x;
   const long long M = (long long)P.n * P.h * P.w;
   if (item >= M * cgs) return;
   const long long m = item / cgs;
@@ -516,10 +651,7 @@ __device__ __forceinline__ void lane_sum8(float (&v)[8], int c, int cgs, int cgp
 }
 
 // dw[tap][c] = Σ_pix dy[pix][c] · x[im2col(pix, tap)][c]
-__global__ void __launch_bounds__(kBlock) k_dw_wgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
-  const int pi = pack_prob(G, blockIdx.x);
-  const pk_cnn_dw& P = G.p[pi];
-  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
+__device__ __forceinline__ void dw_wgrad_generic(const pk_cnn_dw& P, int blk, int nblk) {
   const int taps = P.r * P.s;  // <= 9
   const int cgs = P.c >> 3;
   int cgp = 1;
@@ -568,6 +700,183 @@ __global__ void __launch_bounds__(kBlock) k_dw_wgrad(const __grid_constant__ Pac
     bad |= !isfinite(tot[i]);
   }
   if (bad) *P.flag = 1;
+}
+
+// ------------------------------------------------------------------------------
+// 3x3 depthwise fast paths.
+//   FPROP / DGRAD: one thread per (pixel, channel group) of the output plane, all
+//     nine source vectors and nine weight vectors loaded before any FMA, 32-bit
+//     index math (the generic path below walks taps with data-dependent skips).
+//   WGRAD: thread = (channel group j, kernel row r, pixel lane); a block owns
+//     ppb output pixels (planner: enough blocks to spread the member, few enough
+//     that the [9][c] block records stay small next to the inputs), a lane every
+//     lanes-th of them, kU pixels' loads (dy + the row's three x vectors) issued
+//     before their FMAs.  24 accumulators per thread.  Needs cgp <= 64 (c <= 512).
+// ------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ bool dw_fast(const pk_cnn_dw& P, int mode) {
+  if (P.r != 3 || P.s != 3 || (P.stride != 1 && P.stride != 2)) return false;
+  return mode != PK_CNN_DW_WGRAD || P.c <= 512;
+}
+// WGRAD pixel lanes of a 256-thread block: (256 / cgp) / 3 kernel-row triples
+__host__ __device__ __forceinline__ int dw_wgrad_lanes(int cgp) { return (256 / cgp) / 3; }
+
+template <int MODE>
+__device__ __forceinline__ void dw_items3(const pk_cnn_dw& P, int blk) {
+  const int cgs = P.c >> 3;
+  const int oh = MODE == PK_CNN_DW_DGRAD ? P.h : P.p, ow = MODE == PK_CNN_DW_DGRAD ? P.w : P.q;
+  const int item = blk * kBlock + (int)threadIdx.x;
+  if (item >= P.n * oh * ow * cgs) return;
+  const int m = item / cgs, ch = 8 * (item - m * cgs);
+  const int n = m / (oh * ow), rem = m - n * (oh * ow);
+  const int y = rem / ow, x = rem - y * ow;
+  const uint8_t* src = static_cast<const uint8_t*>(MODE == PK_CNN_DW_DGRAD ? P.dy : P.x) + 2 * ch;
+  const int sh = MODE == PK_CNN_DW_DGRAD ? P.p : P.h, sw = MODE == PK_CNN_DW_DGRAD ? P.q : P.w;
+  const size_t pitch = (size_t)(MODE == PK_CNN_DW_DGRAD ? P.ldy : P.ldx) * 2;
+  uint4 v[9], wv[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      int sy, sx;
+      bool ok;
+      if (MODE == PK_CNN_DW_DGRAD) {  // dx(y,x) += dy((y+pad-r)/st, (x+pad-s)/st)·w[r][s]
+        const int ty = y + P.pad - r, tx = x + P.pad - s;
+        sy = ty / P.stride;
+        sx = tx / P.stride;
+        ok = ty >= 0 && tx >= 0 && sy * P.stride == ty && sx * P.stride == tx && sy < sh &&
+             sx < sw;
+      } else {
+        sy = y * P.stride - P.pad + r;
+        sx = x * P.stride - P.pad + s;
+        ok = (unsigned)sy < (unsigned)sh && (unsigned)sx < (unsigned)sw;
+      }
+      v[3 * r + s] = ok ? ldg16(src + ((size_t)(n * sh + sy) * sw + sx) * pitch)
+                        : make_uint4(0, 0, 0, 0);
+      wv[3 * r + s] = ldg16(bptr(P.wt, 3 * r + s, P.c, ch));
+    }
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {  // taps in (r, s) order, as the generic path
+    float a[8], w[8];
+    unpack8(v[k], a);
+    unpack8(wv[k], w);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = fmaf(a[e], w[e], acc[e]);
+  }
+  const int old = MODE == PK_CNN_DW_DGRAD ? P.ldx : P.ldy;
+  *reinterpret_cast<uint4*>(bptr(P.y, m, old, ch)) = pack8(acc);
+}
+
+__device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk, int nblk) {
+  int cgp = 1;
+  while (cgp < (P.c >> 3)) cgp <<= 1;
+  const int t = threadIdx.x, j = t & (cgp - 1), rest = t / cgp;
+  const int lanes = dw_wgrad_lanes(cgp);
+  const int r = rest % 3, rl = rest / 3, ch = 8 * j;
+  const bool on = j < (P.c >> 3) && rl < lanes;
+  float acc[3][8];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+  if (on) {
+    const uint8_t* xb = static_cast<const uint8_t*>(P.x) + 2 * ch;
+    const uint8_t* dyb = static_cast<const uint8_t*>(P.dy) + 2 * ch;
+    const size_t xp = (size_t)P.ldx * 2, dp = (size_t)P.ldy * 2;
+    const int pq = P.p * P.q, M = P.n * pq;
+    const int m1 = min(M, (blk + 1) * P.ppb);
+    // one pixel: dy vector + the three x vectors of kernel row r
+    auto load = [&](int m, uint4& d, uint4 (&xv)[3]) {
+      const int n = m / pq, rem = m - n * pq, oy = rem / P.q, ox = rem - oy * P.q;
+      d = ldg16(dyb + (size_t)m * dp);
+      const int iy = oy * P.stride - P.pad + r, ix0 = ox * P.stride - P.pad;
+      const bool rok = (unsigned)iy < (unsigned)P.h;
+      const uint8_t* xr = xb + (size_t)(n * P.h + iy) * P.w * xp;
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+        xv[s] = rok && (unsigned)(ix0 + s) < (unsigned)P.w ? ldg16(xr + (size_t)(ix0 + s) * xp)
+                                                          : make_uint4(0, 0, 0, 0);
+    };
+    auto fold = [&](const uint4& d, const uint4 (&xv)[3]) {
+      float dv[8];
+      unpack8(d, dv);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        float a[8];
+        unpack8(xv[s], a);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[s][e] = fmaf(dv[e], a[e], acc[s][e]);
+      }
+    };
+    int m = blk * P.ppb + rl;
+    for (; m + (kU - 1) * lanes < m1; m += kU * lanes) {  // kU pixels' loads, then math
+      uint4 d[kU], xv[kU][3];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) load(m + u * lanes, d[u], xv[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) fold(d[u], xv[u]);
+    }
+    for (; m < m1; m += lanes) {
+      uint4 d, xv[3];
+      load(m, d, xv);
+      fold(d, xv);
+    }
+  }
+  // block record [tap][c]: thread (j, r, rl) holds taps 3r .. 3r+2 of channels ch..
+  __shared__ __align__(16) float sh[6144];  // lanes * 9c <= (256 / cgp / 3) * 72 cgp
+  const int n9 = 9 * P.c;
+  if (on) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      float4* dst = reinterpret_cast<float4*>(sh + rl * n9 + (3 * r + s) * P.c + ch);
+      dst[0] = make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]);
+      dst[1] = make_float4(acc[s][4], acc[s][5], acc[s][6], acc[s][7]);
+    }
+  }
+  __syncthreads();
+  float* out = P.ws + (long long)blk * n9;
+  for (int o = threadIdx.x; o < n9; o += kBlock) {
+    float a = 0.f;
+    for (int l = 0; l < lanes; ++l) a += sh[l * n9 + o];
+    out[o] = a;
+  }
+  double* tot;
+  if (!tree_reduce(P.ws, blk, nblk, n9, n9, P.counter, &tot)) return;
+  bool bad = false;
+  for (int i = threadIdx.x; i < n9; i += kBlock) {
+    P.dw[i] = (float)tot[i];
+    bad |= !isfinite(tot[i]);
+  }
+  if (bad) *P.flag = 1;
+}
+
+__global__ void __launch_bounds__(kBlock) k_dw_fprop(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  pdl_gate();
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi];
+  if (dw_fast(P, PK_CNN_DW_FPROP)) dw_items3<PK_CNN_DW_FPROP>(P, blk);
+  else dw_fprop_items(P, blk);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dw_dgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  pdl_gate();
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi];
+  if (dw_fast(P, PK_CNN_DW_DGRAD)) dw_items3<PK_CNN_DW_DGRAD>(P, blk);
+  else dw_dgrad_items(P, blk);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_dw_wgrad(const __grid_constant__ Pack<pk_cnn_dw> G) {
+  pdl_gate();
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_dw& P = G.p[pi];
+  const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
+  if (dw_fast(P, PK_CNN_DW_WGRAD)) dw_fast_wgrad(P, blk, nblk);
+  else dw_wgrad_generic(P, blk, nblk);
 }
 
 // ================================ pooling ========================================
@@ -670,6 +979,7 @@ __device__ __forceinline__ void pool_bwd_item(const pk_cnn_pool& P, long long m,
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
@@ -683,6 +993,7 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ 
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
@@ -699,6 +1010,7 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ 
 // window over kPoolLanes threads and combines them with a fixed xor tree
 constexpr int kPoolLanes = 8;
 __global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
@@ -750,6 +1062,7 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ 
 }
 
 __global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
@@ -764,6 +1077,7 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const __grid_constant__ 
 // ======================== softmax cross-entropy head ============================
 // one block per member; reference engine.py:211-230 (loss) and :252-264 (dlogits)
 __global__ void __launch_bounds__(kBlock) k_xent(const __grid_constant__ Pack<pk_cnn_head> G) {
+  pdl_gate();
   const pk_cnn_head& P = G.p[blockIdx.x];
   extern __shared__ float xs[];
   float* rmax = xs;
@@ -823,23 +1137,44 @@ __global__ void __launch_bounds__(kBlock) k_xent(const __grid_constant__ Pack<pk
 }
 
 // =================== bias + activation backward (LeNet layers) =====================
-__global__ void __launch_bounds__(kBlock, 3) k_bias_act_bwd(const __grid_constant__ Pack<pk_cnn_bias> G) {
+__global__ void __launch_bounds__(kBlock, 2) k_bias_act_bwd(const __grid_constant__ Pack<pk_cnn_bias> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bias& P = G.p[pi];
   const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
   const int r0 = blk * P.rpb, r1 = min(P.rows, r0 + P.rpb);
-  col_partials(r0, r1, P.c, blk, P.ws, [&](int r, int ch, float (&a)[8], float (&b)[8]) {
-    ld8(bptr(P.dy, r, P.ld, ch), a);
-    if (P.act != PK_CNN_ACT_NONE) {
-      float fo[8];
-      ld8(bptr(P.fout, r, P.ld, ch), fo);
+  const Lanes L = lanes_of(P.c);
+  float s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
+  const bool act = P.act != PK_CNN_ACT_NONE, store = act || P.g != P.dy;
+  auto fold = [&](float (&a)[8], int r) {
+    if (store) *reinterpret_cast<uint4*>(bptr(P.g, r, P.ld, L.ch)) = pack8(a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s1[e] += a[e];
+  };
+  if (act) {
+    const uint8_t* const base[2] = {static_cast<const uint8_t*>(P.dy) + 2 * L.ch,
+                                    static_cast<const uint8_t*>(P.fout) + 2 * L.ch};
+    const size_t pitch[2] = {(size_t)P.ld * 2, (size_t)P.ld * 2};
+    row_loop<2>(L, r0, r1, base, pitch, [&](const uint4 (&v)[2], int r) {
+      float a[8], fo[8];
+      unpack8(v[0], a);
+      unpack8(v[1], fo);
 #pragma unroll
       for (int e = 0; e < 8; ++e) a[e] *= act_bwd(fo[e], P.act);
-    }
-    if (P.act != PK_CNN_ACT_NONE || P.g != P.dy) st8(bptr(P.g, r, P.ld, ch), a);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) b[e] = 0.f;
-  });
+      fold(a, r);
+    });
+  } else {
+    const uint8_t* const base[1] = {static_cast<const uint8_t*>(P.dy) + 2 * L.ch};
+    const size_t pitch[1] = {(size_t)P.ld * 2};
+    row_loop<1>(L, r0, r1, base, pitch, [&](const uint4 (&v)[1], int r) {
+      float a[8];
+      unpack8(v[0], a);
+      fold(a, r);
+    });
+  }
+  block_colsum2(L, P.c, s1, s2, P.ws + (size_t)blk * 2 * P.c);
   double* tot;
   if (!tree_reduce(P.ws, blk, nblk, P.c, 2 * P.c, P.counter, &tot)) return;
   bool bad = false;
@@ -852,6 +1187,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bias_act_bwd(const __grid_constan
 
 // ========================== WGRAD split reduction ================================
 __global__ void __launch_bounds__(kBlock) k_split_reduce(const __grid_constant__ Pack<pk_cnn_reduce> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_reduce& P = G.p[pi];
   const long long i4 = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
@@ -872,6 +1208,7 @@ __global__ void __launch_bounds__(kBlock) k_split_reduce(const __grid_constant__
 constexpr int kOptChunk = 4096;  // elements per block
 __global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, const int* blk0,
                                                 int nseg) {
+  pdl_gate();
   const int si = find_prob(blk0, nseg, blockIdx.x);
   const pk_cnn_opt_seg& S = segs[si];
   if (*S.flag) return;  // the member's commit verdict (k_commit mode 0)
@@ -920,6 +1257,7 @@ __global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, cons
 
 // ================= transposed bf16 weights for DGRAD (B operand) ===================
 __global__ void __launch_bounds__(kBlock) k_publish_t(const __grid_constant__ Pack<pk_cnn_tpose> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_tpose& P = G.p[pi];
   const int tk = (P.k + 31) / 32, tc = (P.c + 31) / 32;
@@ -948,6 +1286,7 @@ __global__ void __launch_bounds__(kBlock) k_publish_t(const __grid_constant__ Pa
 // flagged.  mode 0 (before the optimizer, one thread): verdict = prefix-OR of
 // the flags; mode 1 (after it): step += !verdict, verdict |= flag << 1, flag = 0.
 __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
+  pdl_gate();
   if (mode == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       int run = 0;
@@ -970,6 +1309,7 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
 // batch gather: one block per 4 KB of rows, 16-byte vectors
 constexpr int kGatherChunk = 4096;
 __global__ void __launch_bounds__(kBlock) k_gather(const __grid_constant__ Pack<pk_cnn_gather> G) {
+  pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_gather& P = G.p[pi];
   const long long v0 = (long long)(blockIdx.x - G.blk0[pi]) * (kGatherChunk / 16);

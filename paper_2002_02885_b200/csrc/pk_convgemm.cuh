@@ -379,6 +379,7 @@ k_conv_gemm(const __grid_constant__ Launch L) {
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
 
   if (warp < 4) {
     // =========================== producers ===========================
@@ -572,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_consta
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
   const uint32_t bstride = tcols / 2;  // accumulator buffer b at columns [b*bstride, +NT)
   const int T = L.total_tiles;
 

@@ -151,4 +151,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Programmatic dependent launch gate (see cnn::pdl_gate): called by the conv
+// GEMMs after their TMEM allocation, so a parked dependent CTA can never hold
+// TMEM columns a running CTA of the chain still has to allocate.
+__device__ __forceinline__ void pdl_gate() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 }  // namespace tc
