@@ -316,14 +316,18 @@ typedef struct pk_cnn_conv {
   const int64_t* idx;     /* FPROP/WGRAD: batch image i reads source image idx[i] */
   const float* bias;      /* FPROP: per output channel (NULL = none) */
   int32_t* flag;          /* WGRAD (splits == 1): member's non-finite flag */
-  int64_t dseg;           /* FPROP concat-N: elements between member segments of dst */
+  int64_t dseg;           /* FPROP concat-N: elements between member segments of dst;
+                             WGRAD concat-N: elements between the members' dy buffers */
   int32_t n, h, w, c, k, r, s, stride, pad, p, q;
   int32_t ldx, ldy, ldo;
   int32_t act;            /* FPROP: PK_CNN_ACT_* after bias */
   int32_t out_f32;        /* FPROP: dst fp32 */
   int32_t accumulate;     /* DGRAD: dst += result */
   int32_t splits;         /* WGRAD: pixel splits */
-  int32_t nseg;           /* FPROP concat-N: output channels per member segment (0 = one) */
+  int32_t nseg;           /* FPROP concat-N: output channels per member segment (0 = one);
+                             WGRAD concat-N (k = members x 64, nseg = 64, splits >= 2): one
+                             GEMM over the shared input for all members, member j's fp32
+                             partials [splits][64][kpad] at dst + j*splits*64*kpad */
 } pk_cnn_conv;
 
 /* batch norm over the `rows` valid rows of one member (BN_* kinds) */

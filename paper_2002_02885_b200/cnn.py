@@ -695,13 +695,21 @@ class ConvPack:
             gi, li, j, ks = shared
             key = ("first", gi, li)
             if not hasattr(self, "_first_out"):
-                self._first_out = {}
+                self._first_out, self._first_grad, self._first_split = {}, {}, {}
             t = net.tensors[net.ops[0].y]
             rows = b * t.h * t.w
             if key not in self._first_out:
                 self._first_out[key] = z(len(ks), rows, t.c, dt=torch.bfloat16)
+                # gradients of the first output and the WGRAD split partials also
+                # back to back per member: one concatenated-N WGRAD reads them all
+                self._first_grad[key] = z(len(ks), rows, t.c, dt=torch.bfloat16)
+                op0 = net.ops[0]
+                W0 = net.param(op0.params[0])
+                _, sp0 = _wgrad_cfg(t.c, op0.a["r"] * op0.a["s"] * net.tensors[op0.x].c, rows)
+                if sp0 > 1:
+                    self._first_split[key] = z(len(ks), sp0 * W0.numel)
             A["val"][net.ops[0].y] = self._first_out[key][j]
-            A["grad"][net.ops[0].y] = z(rows, t.c, dt=torch.bfloat16)
+            A["grad"][net.ops[0].y] = self._first_grad[key][j]
         for op in net.ops:
             tx = net.tensors[op.x]
             if op.kind in ("bn",):
@@ -727,7 +735,12 @@ class ConvPack:
                 W = net.param(op.params[0])
                 _, splits = _wgrad_cfg(ty.c, op.a["r"] * op.a["s"] * tx.c, b * ty.h * ty.w)
                 if splits > 1:
-                    A["split"][op.name] = z(splits * W.numel)
+                    fkey = ("first",) + shared[:2] if shared is not None and op is net.ops[0] \
+                        else None
+                    if fkey is not None and fkey in self._first_split:
+                        A["split"][op.name] = self._first_split[fkey][shared[2]]
+                    else:
+                        A["split"][op.name] = z(splits * W.numel)
         A["counters"] = z(17 * (4 * len(net.ops) + 4), dt=torch.int32)
         return A
 
@@ -1057,7 +1070,12 @@ class ConvPack:
                     cs.dst = A["split"][op.name].data_ptr()
                 else:
                     cs.dst = self.grads[k][op.params[0]].data_ptr()
-                steps.append((CNN["CONV_WGRAD"], (nt, _stages(nt)), cs, None))
+                wtag = None
+                if first and k in self.first_shared and splits > 1 and ty.c == 64 \
+                        and nt == 64:
+                    gi2, li, j, ks = self.first_shared[k]
+                    wtag = ("firstw", gi2, li, j, lead)
+                steps.append((CNN["CONV_WGRAD"], (nt, _stages(nt)), cs, wtag))
                 if splits > 1:
                     rd = _lib.CnnReduce()
                     rd.src = A["split"][op.name].data_ptr()
@@ -1166,8 +1184,52 @@ class ConvPack:
                     if len(items) != n0:  # a concatenated-N problem: tile over its full N
                         nt = max(_pick_ntile(st.k) for st, _ in items)
                         cfg = (nt, _stages(nt))
+                elif kind == CNN["CONV_WGRAD"] and any(t is not None for _, t in items):
+                    merged = self._merge_first_wgrad(items)
+                    plain = [(st, None) for st, t in items if t is None]
+                    if plain:
+                        ops.append((kind, cfg, [st for st, _ in plain]))
+                    for st in merged:  # one launch per concatenated problem, N tile <= 256
+                        nt = min(256, st.k)
+                        ops.append((kind, (nt, _stages(nt)), [st]))
+                    continue
                 ops.append((kind, cfg, [st for st, _ in items]))
         return ops
+
+    def _merge_first_wgrad(self, items):
+        """The first-layer WGRAD problems of a shared input group (tag
+        ("firstw", gi, li, j, lead)) as one concatenated-N problem: GEMM
+        M = r·s·c over the shared input, N = members x 64 (csrc pk_cnn.cu
+        conv_to_launches, cg::Problem::wseg); each member keeps its own pixel
+        splits, so its partials are bit-identical to its standalone WGRAD."""
+        merged, order = {}, []
+        for st, tag in items:
+            if tag is None:
+                continue
+            _, gi, li, j, lead = tag
+            if (gi, li, lead) not in merged:
+                merged[(gi, li, lead)] = []
+                order.append((gi, li, lead))
+            merged[(gi, li, lead)].append((j, st))
+        res = []
+        for key in order:
+            parts = sorted(merged[key], key=lambda t: t[0])
+            js = [j for j, _ in parts]
+            base = parts[0][1]
+            fkey = ("first",) + key[:2]
+            if len(parts) == 1 or js != list(range(js[0], js[0] + len(js))):
+                res += [p for _, p in parts]  # (kept as separate launches below)
+                continue
+            m = _lib.CnnConv()
+            C.pointer(m)[0] = base
+            g = self._first_grad[fkey]
+            m.k = 64 * len(parts)
+            m.nseg = 64
+            m.dy = g[js[0]].data_ptr()
+            m.dseg = g.shape[1] * g.shape[2]
+            m.dst = self._first_split[fkey][js[0]].data_ptr()
+            res.append(m)
+        return res
 
     def _merge_first(self, items):
         out, merged = [], {}

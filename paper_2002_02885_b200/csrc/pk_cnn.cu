@@ -88,6 +88,21 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D bf16 tensor map [depth][rows][cols] (row pitch `ld`, depth pitch `dstride`
+// elements), box {64 cols, box_rows, 1}, SW128
+bool make_map_3d(CUtensorMap* m, const void* base, uint64_t depth, uint64_t rows, uint64_t cols,
+                 uint64_t ld, uint64_t dstride, uint32_t box_rows) {
+  if (!encode_fn()) return false;
+  cuuint64_t dims[3] = {cols, rows, depth};
+  cuuint64_t strides[2] = {ld * 2, dstride * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline int rup(int a, int b) { return (a + b - 1) / b * b; }
 
@@ -409,18 +424,37 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
                   : make_map_im2col(&L.tm[j], g.src, g.n, g.h, g.w, g.c, g.ldx, -g.pad, -g.pad,
                                     g.pad - (g.s - 1), g.pad - (g.r - 1), g.stride, 64,
                                     c16 ? 16 : 64);
-          if (!ok || !make_map_2d(&L.tmA[j], g.dy, (uint64_t)pix, g.k, g.ldy, 64))
-            return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
-          if (g.k <= 64 && ntile == 64) {  // swapped orientation (see cg::Problem::swap)
+          if (g.nseg > 0) {  // members concatenated along N (shared-input first layer)
+            if (g.nseg != 64 || g.k % 64 || p.splits < 2)
+              return fail(PK_ERR_ARG, "conv: concatenated WGRAD needs 64 channels per member "
+                                      "and pixel splits");
+            if (!ok || !make_map_3d(&L.tmA[j], g.dy, (uint64_t)(g.k / 64), (uint64_t)pix, 64,
+                                    g.ldy, (uint64_t)g.dseg, 64))
+              return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
             p.swap = 1;
+            p.wseg = 64;
             p.M = g.r * g.s * g.c;
             p.N = g.k;
+          } else {
+            if (!ok || !make_map_2d(&L.tmA[j], g.dy, (uint64_t)pix, g.k, g.ldy, 64))
+              return fail(PK_ERR_CUDA, "conv: WGRAD operand maps");
+            if (g.k <= 64 && ntile == 64) {  // swapped orientation (see cg::Problem::swap)
+              p.swap = 1;
+              p.M = g.r * g.s * g.c;
+              p.N = g.k;
+            }
           }
+        } else if (g.nseg > 0) {
+          return fail(PK_ERR_ARG, "conv: concatenated WGRAD needs TMA-fed operands");
         }
         p.SH = g.h; p.SW = g.w; p.SC = g.c; p.sld = g.ldx;
         p.OH = g.p; p.OW = g.q; p.ald = g.ldy;
         p.dld = kpad;
         p.split_stride = (long long)g.k * kpad;
+        if (p.wseg) {  // each member's partials [splits][64][kpad], members back to back
+          p.split_stride = 64LL * kpad;
+          p.dseg = (long long)p.splits * 64 * kpad;
+        }
       }
       p.tiles_m = cdiv(p.M, cg::BM);
       p.tiles_n = cdiv(p.N, ntile);

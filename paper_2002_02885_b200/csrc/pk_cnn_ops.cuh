@@ -381,27 +381,41 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_reduce(const __grid_consta
 constexpr int kApplyGroups = 32, kApplyItems = kU * kBlock;
 
 struct ApplyTile {
-  int r0, R, g0, gw;
+  int r0, r1, R, g0, gw;  // the block's rows [r0, r1) in steps of R rows
 };
+constexpr int kApplyMaxBlocks = 4 * 148;  // per problem; larger layers loop over row tiles
 __host__ __device__ __forceinline__ int apply_groups(int c) {
   return (c >> 3) < kApplyGroups ? (c >> 3) : kApplyGroups;
 }
+// row tiles per block of a problem: spans of rt row tiles (elementwise kernels:
+// any partition gives the same result)
+__host__ __device__ __forceinline__ void apply_shape(int rows, int c, int& ncg, int& nrt, int& rt) {
+  const int cgs = c >> 3, G = apply_groups(c), R = kApplyItems / G;
+  ncg = (cgs + G - 1) / G;
+  nrt = (rows + R - 1) / R;
+  const int spans = max(1, kApplyMaxBlocks / ncg);
+  rt = (nrt + spans - 1) / spans;
+}
 __host__ __device__ __forceinline__ int apply_blocks(int rows, int c) {
-  const int G = apply_groups(c), R = kApplyItems / G;
-  return ((rows + R - 1) / R) * (((c >> 3) + G - 1) / G);
+  int ncg, nrt, rt;
+  apply_shape(rows, c, ncg, nrt, rt);
+  return ((nrt + rt - 1) / rt) * ncg;
 }
 __device__ __forceinline__ ApplyTile apply_tile(int b, int rows, int c) {
-  const int cgs = c >> 3, G = apply_groups(c), ncg = (cgs + G - 1) / G;
+  const int cgs = c >> 3, G = apply_groups(c);
+  int ncg, nrt, rt;
+  apply_shape(rows, c, ncg, nrt, rt);
   ApplyTile T;
   T.R = kApplyItems / G;
   const int tr = b / ncg, tg = b - tr * ncg;
-  T.r0 = tr * T.R;
+  T.r0 = tr * rt * T.R;
+  T.r1 = min(rows, T.r0 + rt * T.R);
   T.g0 = tg * G;
   T.gw = min(G, cgs - T.g0);
   return T;
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_bn_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
+__global__ void __launch_bounds__(kBlock, 3) k_bn_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
@@ -438,14 +452,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_apply(const __grid_constant__ 
   }
   __syncthreads();
   const int nitems = T.R * T.gw;
+  for (int rb = T.r0; rb < T.r1; rb += T.R) {
   int row[kU], cg[kU];
   uint4 x[kU], rv[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int i = t + u * kBlock, rr = i / T.gw;
-    row[u] = T.r0 + rr;
+    row[u] = rb + rr;
     cg[u] = i - rr * T.gw;
-    if (i < nitems && row[u] < P.rows) {
+    if (i < nitems && row[u] < T.r1) {
       const int ch = (T.g0 + cg[u]) * 8;
       x[u] = ldg16(bptr(P.x, row[u], P.ldx, ch));
       if (P.res) rv[u] = ldg16(bptr(P.res, row[u], P.ldr, ch));
@@ -468,6 +483,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_bn_apply(const __grid_constant__ 
       v[e] = act_fwd(y, P.act);
     }
     *reinterpret_cast<uint4*>(bptr(P.out, row[u], P.ldo, (T.g0 + cg[u]) * 8)) = pack8(v);
+  }
   }
 }
 
@@ -501,14 +517,15 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
   __syncthreads();
   const bool act = P.act != PK_CNN_ACT_NONE;
   const int nitems = T.R * T.gw;
+  for (int rb = T.r0; rb < T.r1; rb += T.R) {
   int row[kU], cg[kU];
   uint4 d[kU], x[kU], fo[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int i = t + u * kBlock, rr = i / T.gw;
-    row[u] = T.r0 + rr;
+    row[u] = rb + rr;
     cg[u] = i - rr * T.gw;
-    if (i < nitems && row[u] < P.rows) {
+    if (i < nitems && row[u] < T.r1) {
       const int ch = (T.g0 + cg[u]) * 8;
       d[u] = ldg16(bptr(P.dout, row[u], P.ldd, ch));
       x[u] = ldg16(bptr(P.x, row[u], P.ldx, ch));
@@ -551,6 +568,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
       }
       *reinterpret_cast<uint4*>(pr) = pack8(g);
     }
+  }
   }
 }
 
@@ -720,7 +738,7 @@ __host__ __device__ __forceinline__ bool dw_fast(const pk_cnn_dw& P, int mode) {
 // WGRAD pixel lanes of a 256-thread block: (256 / cgp) / 3 kernel-row triples
 __host__ __device__ __forceinline__ int dw_wgrad_lanes(int cgp) { return (256 / cgp) / 3; }
 
-template <int MODE>
+template <int MODE, int ST>
 __device__ __forceinline__ void dw_items3(const pk_cnn_dw& P, int blk) {
   const int cgs = P.c >> 3;
   const int oh = MODE == PK_CNN_DW_DGRAD ? P.h : P.p, ow = MODE == PK_CNN_DW_DGRAD ? P.w : P.q;
@@ -741,13 +759,12 @@ __device__ __forceinline__ void dw_items3(const pk_cnn_dw& P, int blk) {
       bool ok;
       if (MODE == PK_CNN_DW_DGRAD) {  // dx(y,x) += dy((y+pad-r)/st, (x+pad-s)/st)·w[r][s]
         const int ty = y + P.pad - r, tx = x + P.pad - s;
-        sy = ty / P.stride;
-        sx = tx / P.stride;
-        ok = ty >= 0 && tx >= 0 && sy * P.stride == ty && sx * P.stride == tx && sy < sh &&
-             sx < sw;
+        sy = ST == 1 ? ty : ty >> 1;
+        sx = ST == 1 ? tx : tx >> 1;
+        ok = ty >= 0 && tx >= 0 && (ST == 1 || ((ty | tx) & 1) == 0) && sy < sh && sx < sw;
       } else {
-        sy = y * P.stride - P.pad + r;
-        sx = x * P.stride - P.pad + s;
+        sy = y * ST - P.pad + r;
+        sx = x * ST - P.pad + s;
         ok = (unsigned)sy < (unsigned)sh && (unsigned)sx < (unsigned)sw;
       }
       v[3 * r + s] = ok ? ldg16(src + ((size_t)(n * sh + sy) * sw + sx) * pitch)
@@ -857,7 +874,10 @@ __global__ void __launch_bounds__(kBlock) k_dw_fprop(const __grid_constant__ Pac
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_dw& P = G.p[pi];
   const int blk = blockIdx.x - G.blk0[pi];
-  if (dw_fast(P, PK_CNN_DW_FPROP)) dw_items3<PK_CNN_DW_FPROP>(P, blk);
+  if (dw_fast(P, PK_CNN_DW_FPROP)) {
+    if (P.stride == 1) dw_items3<PK_CNN_DW_FPROP, 1>(P, blk);
+    else dw_items3<PK_CNN_DW_FPROP, 2>(P, blk);
+  }
   else dw_fprop_items(P, blk);
 }
 
@@ -866,7 +886,10 @@ __global__ void __launch_bounds__(kBlock) k_dw_dgrad(const __grid_constant__ Pac
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_dw& P = G.p[pi];
   const int blk = blockIdx.x - G.blk0[pi];
-  if (dw_fast(P, PK_CNN_DW_DGRAD)) dw_items3<PK_CNN_DW_DGRAD>(P, blk);
+  if (dw_fast(P, PK_CNN_DW_DGRAD)) {
+    if (P.stride == 1) dw_items3<PK_CNN_DW_DGRAD, 1>(P, blk);
+    else dw_items3<PK_CNN_DW_DGRAD, 2>(P, blk);
+  }
   else dw_dgrad_items(P, blk);
 }
 

@@ -64,6 +64,10 @@ struct Problem {
                               //   3 TMA im2col of a 16-channel input (SW32)
   int swap;                   // WGRAD (TMA, co <= 64): GEMM M = (r,s,c), N = co, so the
                               //   M = 128 MMA is not half empty; dst written transposed
+  int wseg;                   // WGRAD, swapped: members concatenated along N (the shared-
+                              //   input first layer), wseg = 64 columns each; dY atoms come
+                              //   from a 3-D map {co, pixel, member}, member seg's partials
+                              //   at dst + seg * dseg
   long long dseg;             // elements between dst segments
   long long split_stride;     // WGRAD: elements between split partials
 };
@@ -120,7 +124,12 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
     if (P.swap) {  // A = X (M = (r,s,c)), B = dY (N = co)
       x_atom(stage, tm * BM);
       x_atom(stage + 8192, tm * BM + 64);
-      for (int j = 0; j < NT / 64; ++j) tc::tma_load_2d(b_s + j * 8192, &L.tmA[pi], tn * NT + j * 64, kk, bar);
+      for (int j = 0; j < NT / 64; ++j) {
+        if (P.wseg)
+          tc::tma_load_3d(b_s + j * 8192, &L.tmA[pi], 0, kk, (tn * NT) / 64 + j, bar);
+        else
+          tc::tma_load_2d(b_s + j * 8192, &L.tmA[pi], tn * NT + j * 64, kk, bar);
+      }
     } else {       // A = dY (M = co), B = X (N = (r,s,c))
       tc::tma_load_2d(stage, &L.tmA[pi], tm * BM, kk, bar);
       tc::tma_load_2d(stage + 8192, &L.tmA[pi], tm * BM + 64, kk, bar);
@@ -267,6 +276,10 @@ __device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int wa
     } else if (MODE == WGRAD && P.swap) {
       // accumulator row m = (r,s,c) column of dW, columns = co rows of dW
       float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride + m;
+      if (P.wseg) {  // 16 | wseg: the 16 columns belong to one member
+        const int seg = n0 / P.wseg;
+        d += seg * P.dseg - (long long)seg * P.wseg * P.dld;
+      }
       for (int e = 0; e < 16 && n0 + e < P.N; ++e) d[(long long)(n0 + e) * P.dld] = v[e];
     } else if (MODE == WGRAD) {
       float* d = static_cast<float*>(P.dst) + (long long)split * P.split_stride +

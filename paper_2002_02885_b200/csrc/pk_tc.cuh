@@ -106,6 +106,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int
       : "memory");
 }
 
+// 3-D tile {x (inner), y, z} of tensor map `m` → shared `dst`
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int x, int y, int z,
+                                            uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar))
+      : "memory");
+}
+
 // 4-D im2col box of tensor map `m` (NHWC: {c, w, h, n} base coordinates of the box's
 // first pixel, filter offsets {ow, oh} added per pixel) → shared `dst`
 __device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* m, int c, int w,
