@@ -100,6 +100,29 @@ typedef struct {
   int32_t committed; /* members whose update committed */
 } pk_status;
 
+/* ---- kernel plan (MLP pack path) ----------------------------------------
+   Which kernel family trains which member is decided when a pack is created,
+   from the member shapes and these process-wide options.  The defaults are the
+   production plan; the other values exist for A/B measurements and for tests
+   that pin a family.  pk_pack_kernel_plan() reports what a pack actually got. */
+typedef struct pk_plan_options {
+  int32_t fwd;          /* tensor-path forward: 0 auto (k_m1c_fwd when its clusters fit one
+                           wave, k_m1s_fwd past two waves, else k_m1t_fwd), 1 split-K clusters
+                           k_m1t_fwd only, 2 streaming k_m1s_fwd whenever it fits */
+  int32_t fwd_cluster;  /* cap on the k_m1c_fwd cluster size (0 = none) */
+  int32_t tcgen05;      /* 1: tensor path for eligible fp32 one-hidden-layer members */
+  int32_t mlp1;         /* 1: fused FFMA one-hidden-layer kernels where eligible */
+  int32_t m1x;          /* 1: one-launch FFMA cluster step k_m1x_step (experimental; slower) */
+  int32_t fwd_split;    /* 1: k_phase FWD input ranges */
+  int32_t wgrad_narrow; /* 1: 64x16 WGRAD tiles for layers with <= 16 outputs */
+  int32_t inline_desc;  /* 1: step descriptors inline in the graph's kernel parameters */
+  int32_t run_batch;    /* steps per graph launch in pk_pack_run (0 = 8) */
+  int32_t trace;        /* 1: %globaltimer stage stamps (pk_pack_trace) */
+  int32_t reserved[6];
+} pk_plan_options;
+int pk_plan_options_get(pk_plan_options* out);
+int pk_plan_options_set(const pk_plan_options* in); /* NULL restores the defaults */
+
 /* ---- context ------------------------------------------------------------ */
 int pk_abi_version(void);
 int pk_ctx_create(int32_t device, int32_t dtype, pk_ctx** out);
@@ -470,6 +493,12 @@ typedef struct pk_cnn_op {
   int32_t nprob;
   int32_t cfg0;           /* CONV: GEMM N tile */
   int32_t cfg1;           /* CONV: pipeline stages */
+  int32_t lane;           /* 0: the program's stream.  L > 0: an independent chain (the
+                             members of one architecture in a heterogeneous pack) that
+                             forks from lane 0 after the last lane-0 op before it and
+                             joins lane 0 before the next lane-0 op, so different lanes'
+                             launches overlap on the GPU */
+  int32_t pad0;
   const void* probs;      /* nprob structs of the kind's type (host, copied) */
 } pk_cnn_op;
 

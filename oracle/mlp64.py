@@ -144,8 +144,10 @@ def member_forward_loss(layers, act, x, y, n_valid=None, check=True):
                          "y": y, "nv": nv}
 
 
-def member_backward(layers, act, cache):
-    """Backward of the summed head (engine.py:241-292); returns [(dW, db)]."""
+def member_backward(layers, act, cache, scales=None):
+    """Backward of the summed head (engine.py:241-292); returns [(dW, db)].
+    scales (test tolerance support): receives [(|x|ᵀ|d|, Σ|d|)] per layer, the
+    magnitude an fp32 GEMM's rounding error of each gradient element scales with."""
     p, y, nv = cache["p"], cache["y"], cache["nv"]
     d = np.zeros_like(p)
     if nv:
@@ -157,6 +159,8 @@ def member_backward(layers, act, cache):
         w, _ = layers[i]
         x_in = cache["ins"][i]
         grads[i] = (x_in.T @ d, d.sum(axis=0))
+        if scales is not None:
+            scales.insert(0, (np.abs(x_in).T @ np.abs(d), np.abs(d).sum(axis=0)))
         if i == 0:
             break
         da = d @ w.T
@@ -299,7 +303,7 @@ def _next_batch(m: OracleMember, ds: OracleDataset):
 
 
 def oracle_packed_step(members, datasets, share_inputs=True,
-                       stop_at_epoch_end=False):
+                       stop_at_epoch_end=False, grads_out=None):
     """One synchronized packed step (packing.py:185-264).
 
     Pads each input group to the driver batch and masks the pad rows exactly
@@ -339,8 +343,12 @@ def oracle_packed_step(members, datasets, share_inputs=True,
         loss, cache = member_forward_loss(m.layers, m.act, xp, yp, take)
         caches[m.model_id] = cache
         losses[m.model_id] = loss
-    grads = {m.model_id: member_backward(m.layers, m.act, caches[m.model_id])
-             for m in active}
+    grads = {}
+    for m in active:
+        sc = [] if grads_out is not None else None
+        grads[m.model_id] = member_backward(m.layers, m.act, caches[m.model_id], sc)
+        if grads_out is not None:
+            grads_out[m.model_id] = (grads[m.model_id], sc)
     for m in active:
         m.t = optimizer_step(m.opt, m.lr, m.t, m.layers, m.slots,
                              grads[m.model_id], m.weight_decay)

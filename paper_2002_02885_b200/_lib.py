@@ -22,7 +22,7 @@ OPT_CODES = {"sgd": 0, "momentum": 1, "adam": 2, "adagrad": 3}
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "pk_abi_version", "pk_ctx_create", "pk_ctx_destroy", "pk_ctx_last_error",
+    "pk_abi_version", "pk_plan_options_get", "pk_plan_options_set", "pk_ctx_create", "pk_ctx_destroy", "pk_ctx_last_error",
     "pk_ctx_set_stream", "pk_ctx_synchronize", "pk_ctx_mem_info",
     "pk_dataset_create", "pk_dataset_write", "pk_dataset_write_rows", "pk_dataset_gather_rows",
     "pk_pack_run", "pk_host_map", "pk_host_unmap",
@@ -38,6 +38,60 @@ EXPORTS = (
     "pk_cnn_prog_create", "pk_cnn_prog_destroy", "pk_cnn_prog_run", "pk_cnn_prog_profile",
     "pk_cnn_prog_launches", "pk_cnn_last_error",
 )
+
+
+class PlanOptions(C.Structure):
+    """packtrain_b200.h pk_plan_options: the MLP path's kernel plan."""
+    _fields_ = [(n, C.c_int32) for n in ("fwd", "fwd_cluster", "tcgen05", "mlp1", "m1x",
+                                         "fwd_split", "wgrad_narrow", "inline_desc",
+                                         "run_batch", "trace")] + [("reserved", C.c_int32 * 6)]
+
+
+PLAN_FIELDS = ("fwd", "fwd_cluster", "tcgen05", "mlp1", "m1x", "fwd_split", "wgrad_narrow",
+               "inline_desc", "run_batch", "trace")
+FWD_PLANS = {"auto": 0, "split": 1, "stream": 2}
+
+
+def plan_options() -> dict:
+    """The current kernel plan (pk_plan_options_get) as a dict."""
+    o = PlanOptions()
+    if lib().pk_plan_options_get(C.byref(o)) != PK_OK:
+        raise PKError(PK_ERR_ARG, "pk_plan_options_get failed")
+    return {f: int(getattr(o, f)) for f in PLAN_FIELDS}
+
+
+def set_plan_options(**kw) -> dict:
+    """Update fields of the kernel plan (read when a pack is created); returns
+    the previous plan.  set_plan_options() with no fields restores the defaults."""
+    prev = plan_options()
+    if not kw:
+        lib().pk_plan_options_set(None)
+        return prev
+    o = PlanOptions()
+    cur = dict(prev)
+    for k, v in kw.items():
+        if k not in cur:
+            raise KeyError(f"unknown plan option {k!r}")
+        cur[k] = FWD_PLANS[v] if k == "fwd" and isinstance(v, str) else int(v)
+    for f in PLAN_FIELDS:
+        setattr(o, f, cur[f])
+    if lib().pk_plan_options_set(C.byref(o)) != PK_OK:
+        raise PKError(PK_ERR_ARG, f"invalid kernel plan {kw}")
+    return prev
+
+
+class kernel_plan:
+    """with kernel_plan(fwd="stream"): ... — a scoped kernel plan."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        self.prev = set_plan_options(**self.kw)
+        return self
+
+    def __exit__(self, *exc):
+        set_plan_options(**self.prev)
 
 
 class MemberDesc(C.Structure):
@@ -164,7 +218,7 @@ class CnnGather(C.Structure):
 
 class CnnOp(C.Structure):
     _fields_ = [("kind", _i32), ("nprob", _i32), ("cfg0", _i32), ("cfg1", _i32),
-                ("probs", _vp)]
+                ("lane", _i32), ("pad0", _i32), ("probs", _vp)]
 
 
 CNN_STRUCT = {}
@@ -242,6 +296,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            P(i32), P(dbl), P(Status)]),
         "pk_pack_trace": (i64, [vp, vp, i64]),
         "pk_pack_launches_per_step": (i32, [vp]),
+        "pk_plan_options_get": (C.c_int, [P(PlanOptions)]),
+        "pk_plan_options_set": (C.c_int, [P(PlanOptions)]),
         "pk_conv_gemm_test": (C.c_int, [i32, P(ConvGeom), vp, vp, vp, vp, i32, i32, i32, vp]),
         "pk_cnn_prog_create": (C.c_int, [P(CnnOp), i32, i32, P(vp)]),
         "pk_cnn_prog_destroy": (None, [vp]),

@@ -130,6 +130,11 @@ class Net:
         self.n = 0
         self.logits = None
 
+    @property
+    def signature(self):
+        """identical nets (same architecture) share launches in a pack"""
+        return (self.arch.family, self.arch.classes, tuple(self.arch.image), self.arch.width)
+
     # -- builders -------------------------------------------------------------
     def _layer(self):
         name = f"L{self.n}"
@@ -1273,6 +1278,18 @@ class ConvPack:
             res.append((m, None))
         return res
 
+    def _lanes(self, act):
+        """Active members split by architecture (identical nets are grouped into
+        shared launches; different nets go to separate lanes, at most 8)."""
+        by = {}
+        for k in act:
+            by.setdefault(self.members[k].net.signature, []).append(k)
+        lanes = list(by.values())
+        while len(lanes) > 8:  # fold the smallest lanes together
+            lanes.sort(key=len)
+            lanes = [lanes[0] + lanes[1]] + lanes[2:]
+        return lanes
+
     def _build_ops(self, takes, leads, data, with_update=True):
         K = len(self.members)
         act = [k for k in range(K) if takes[k] > 0]
@@ -1287,8 +1304,31 @@ class ConvPack:
             g.row_bytes, g.rows = data.row_bytes, takes[lead]
             gs.append(g)
         ops.append((CNN["GATHER"], None, gs))
-        ops += self._group([self._fwd_steps(k, takes[k], leads[k], data) for k in act])
-        ops += self._group([self._bwd_steps(k, takes[k], leads[k], data) for k in act])
+        fwd = {k: self._fwd_steps(k, takes[k], leads[k], data) for k in act}
+        bwd = {k: self._bwd_steps(k, takes[k], leads[k], data) for k in act}
+        lanes = self._lanes(act)
+        if len(lanes) == 1:
+            ops += self._group([fwd[k] for k in act])
+            ops += self._group([bwd[k] for k in act])
+        else:
+            # heterogeneous pack: one lane (stream) per architecture, so the
+            # different nets' launches overlap; the shared-input first layer's
+            # concatenated FPROP runs before the fork, its WGRAD after the join
+            pre, post = [], []
+            for k in act:
+                if fwd[k] and fwd[k][0][3] is not None:
+                    pre.append([fwd[k].pop(0)])
+                cut = next((i for i, st in enumerate(bwd[k])
+                            if st[3] is not None and st[3][0] == "firstw"), None)
+                if cut is not None:
+                    post.append(bwd[k][cut:])
+                    bwd[k] = bwd[k][:cut]
+            ops += self._group(pre)
+            for li, lane in enumerate(lanes, 1):
+                for op in (self._group([fwd[k] for k in lane])
+                           + self._group([bwd[k] for k in lane])):
+                    ops.append(op + (li,))
+            ops += self._group(post)
         if with_update:
             cm = []
             for k in act:
@@ -1354,11 +1394,14 @@ class CnnProgram:
 
     def __init__(self, ops, device):
         self.lib = _lib.lib()
-        self.kinds = [k for k, _, _ in ops]
-        self.sizes = [len(s) for _, _, s in ops]
+        self.kinds = [op[0] for op in ops]
+        self.sizes = [len(op[2]) for op in ops]
+        self.lanes = [op[3] if len(op) > 3 else 0 for op in ops]
         self._keep = []
         arr = (_lib.CnnOp * len(ops))()
-        for i, (kind, cfg, structs) in enumerate(ops):
+        for i, op in enumerate(ops):
+            kind, cfg, structs = op[:3]
+            arr[i].lane = op[3] if len(op) > 3 else 0
             T = _lib.CNN_STRUCT[kind]
             buf = (T * len(structs))(*structs)
             self._keep.append(buf)

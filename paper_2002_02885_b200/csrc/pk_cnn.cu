@@ -298,7 +298,7 @@ std::string check_prob(int kind, const void* pr) {
 }
 
 struct OpRec {
-  int kind = 0, nprob = 0, nblocks = 0;
+  int kind = 0, nprob = 0, nblocks = 0, lane = 0;
   int ntile = 0, stages = 0;
   size_t probs_off = 0, blk_off = 0;  // offsets into the device descriptor block (OPT, COMMIT)
   std::vector<cg::Launch> conv;       // conv ops: launches of <= kMaxProblems problems
@@ -327,9 +327,13 @@ void make_packs(OpRec& r, const T* pr, int n, int (*blocks)(int, const void*)) {
 
 }  // namespace
 
+constexpr int kMaxLanes = 8;
+
 struct pk_cnn_prog {
   int device = 0;
   std::vector<OpRec> ops;
+  cudaStream_t lane_st[kMaxLanes + 1] = {};  // side streams of lanes 1..kMaxLanes
+  cudaEvent_t fork_ev = nullptr, join_ev[kMaxLanes + 1] = {};
   uint8_t* dmem = nullptr;
   int launches = 0;
   cudaGraphExec_t gexec = nullptr;
@@ -593,13 +597,56 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Lanes: lane-0 ops run on `st`; a lane L > 0 forks from `st` (event) at its
+// first op after a lane-0 op and joins `st` (event) before the next lane-0 op.
+// PDL chains each lane's launches; the first launch after a fork or a join
+// carries no PDL attribute (its predecessor is an event, not a kernel).
 int run_all(pk_cnn_prog* g, cudaStream_t st) {
-  t_pdl = false;
+  bool pdl[kMaxLanes + 1] = {}, open[kMaxLanes + 1] = {};
+  bool any_open = false, forked = false;
   for (size_t i = 0; i < g->ops.size(); ++i) {
-    cudaError_t e = run_op(g, g->ops[i], st);
+    const int L = g->ops[i].lane;
+    cudaError_t e = cudaSuccess;
+    if (L == 0 && any_open) {  // join every lane opened since the last lane-0 op
+      for (int l = 1; l <= kMaxLanes && e == cudaSuccess; ++l)
+        if (open[l]) {
+          e = cudaEventRecord(g->join_ev[l], g->lane_st[l]);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->join_ev[l], 0);
+          open[l] = false;
+        }
+      any_open = forked = false;
+      pdl[0] = false;
+    } else if (L > 0 && !open[L]) {
+      if (!g->lane_st[L]) {
+        e = cudaStreamCreateWithFlags(&g->lane_st[L], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->join_ev[L], cudaEventDisableTiming);
+        if (e == cudaSuccess && !g->fork_ev)
+          e = cudaEventCreateWithFlags(&g->fork_ev, cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess && !forked) {
+        e = cudaEventRecord(g->fork_ev, st);
+        forked = true;
+      }
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(g->lane_st[L], g->fork_ev, 0);
+      open[L] = any_open = true;
+      pdl[L] = false;
+    }
+    if (e == cudaSuccess) {
+      t_pdl = pdl[L];
+      e = run_op(g, g->ops[i], L ? g->lane_st[L] : st);
+      pdl[L] = t_pdl;
+    }
     if (e != cudaSuccess)
       return fail(PK_ERR_CUDA, "op " + std::to_string(i) + " (kind " +
                                    std::to_string(g->ops[i].kind) + "): " + cudaGetErrorString(e));
+  }
+  if (any_open) {  // a program ending in lane ops still joins
+    for (int l = 1; l <= kMaxLanes; ++l)
+      if (open[l]) {
+        cudaError_t e = cudaEventRecord(g->join_ev[l], g->lane_st[l]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->join_ev[l], 0);
+        if (e != cudaSuccess) return fail(PK_ERR_CUDA, cudaGetErrorString(e));
+      }
   }
   return PK_OK;
 }
@@ -622,6 +669,11 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
     OpRec r;
     r.kind = op.kind;
     r.nprob = op.nprob;
+    r.lane = op.lane;
+    if (op.lane < 0 || op.lane > kMaxLanes) {
+      delete g;
+      return fail(PK_ERR_ARG, "op " + std::to_string(i) + ": lane out of range");
+    }
     const size_t ps = prob_size(op.kind);
     if (!ps || op.nprob <= 0 || !op.probs) {
       delete g;
@@ -730,6 +782,11 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
 extern "C" void pk_cnn_prog_destroy(pk_cnn_prog* g) {
   if (!g) return;
   if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  for (int l = 1; l <= kMaxLanes; ++l) {
+    if (g->lane_st[l]) cudaStreamDestroy(g->lane_st[l]);
+    if (g->join_ev[l]) cudaEventDestroy(g->join_ev[l]);
+  }
+  if (g->fork_ev) cudaEventDestroy(g->fork_ev);
   if (g->dmem) cudaFree(g->dmem);
   delete g;
 }

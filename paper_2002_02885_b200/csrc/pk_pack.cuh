@@ -123,6 +123,15 @@ static size_t feed_size(int dtype) {
 
 // dynamic shared memory a k_phase CTA may use (opt-in limit minus the
 // kernel's static smem), set once per precision by pk_pack_create
+// the process-wide kernel plan (packtrain_b200.h pk_plan_options)
+static pk_plan_options plan_defaults() {
+  pk_plan_options o;
+  memset(&o, 0, sizeof(o));
+  o.tcgen05 = o.mlp1 = o.fwd_split = o.wgrad_narrow = o.inline_desc = 1;
+  return o;
+}
+static pk_plan_options g_plan = plan_defaults();
+
 static int g_smem_max[2] = {0, 0};
 
 static int smem_budget(int dtype) { return g_smem_max[dtype]; }
@@ -192,7 +201,7 @@ constexpr int kStaticSmemMargin = 16 * 1024;
 
 static bool mlp1_eligible(const pk_member_desc& d, int dtype, int device) {
   if (d.n_layers != 2 || d.dims[2] > pk::M1_MAXC || d.max_rows > pk::M1_MAXR) return false;
-  if (getenv("PK_NO_MLP1")) return false;  // A/B switch for measurements
+  if (!g_plan.mlp1) return false;
   // f64 members: the phase kernels are faster at every Hyperband shape
   // (784-16-10: 45 vs 78 µs per step at K=1, 74 vs 128 at K=8 — its 8-unit
   // column blocks leave a narrow member with 2 CTAs walking all 784 inputs)
@@ -217,7 +226,7 @@ static bool m1t_eligible(const pk_member_desc& d, int dtype, int device) {
   const int D = d.dims[0], H = d.dims[1], C = d.dims[2];
   if (C > pk::T_MAXC || d.max_rows > pk::T_MAXR || H % 4 != 0 || D % 4 != 0) return false;
   if (pk::t_nsplit(D) > pk::T_MAXCS) return false;  // one cluster per unit tile
-  if (getenv("PK_NO_TCGEN05")) return false;  // A/B switch for measurements
+  if (!g_plan.tcgen05) return false;
   int optin = 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
       cudaSuccess)
@@ -243,8 +252,8 @@ static bool m1x_eligible(const pk_member_desc& d, int dtype, int device) {
   if (dtype != PK_F32 || d.n_layers != 2) return false;
   const int D = d.dims[0], H = d.dims[1], C = d.dims[2];
   if (C > pk::X_MAXC || d.max_rows > pk::X_MAXR || H % 4 != 0 || D % 4 != 0) return false;
-  // opt-in while its step time trails the tcgen05 path's (PK_M1X=1)
-  if (getenv("PK_NO_M1X") || !getenv("PK_M1X")) return false;
+  // opt-in while its step time trails the tcgen05 path's (plan option m1x)
+  if (!g_plan.m1x) return false;
   int optin = 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
       cudaSuccess)
@@ -288,7 +297,7 @@ static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, in
       // CTAs per tile (ng) from the phase's room, which never changes the sums
       const int nch = cdiv(d.dims[l], pk::FWD_KC);
       int cps = 0, nr = 1;
-      if (nch >= 3 && !getenv("PK_NO_FWD_SPLIT")) {
+      if (nch >= 3 && g_plan.fwd_split) {
         cps = std::max(2, cdiv(nch, pk::kFwdMaxRanges));
         nr = cdiv(nch, cps);
         if (cps > 127) cps = 0, nr = 1;
@@ -316,7 +325,7 @@ static void emit(std::vector<Tile>& out, int k, const pk_member* m, int kind, in
           out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::DG_BM, nb * pk::DG_BN});
       break;
     default:  // WGRAD over W_l [in x out]
-      if (d.dims[l + 1] <= pk::WGN_BN && !getenv("PK_NO_WGRAD_NARROW")) {
+      if (d.dims[l + 1] <= pk::WGN_BN && g_plan.wgrad_narrow) {
         // narrow layer: 64 x 16 tiles (pk_kernels.cuh WgradNG), flagged by n0 bit 20
         for (int mb = 0; mb < cdiv(d.dims[l], pk::WGN_BM); ++mb)
           out.push_back(Tile{k, (int16_t)l, (int16_t)kind, mb * pk::WGN_BM, 1 << 20});
@@ -536,9 +545,8 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     phases.push_back(m1b);
   }
   // default forward: cluster-streaming (k_m1c_fwd) with the cluster size that
-  // fills about one wave; PK_FWD=split|stream selects the older variants
-  const char* fv = getenv("PK_FWD");
-  if (!eval && !tf.host.empty() && !fv) {
+  // fills about one wave; plan option fwd = 1 | 2 pins the other variants
+  if (!eval && !tf.host.empty() && g_plan.fwd == 0) {
     int n_tiles = 0, cs_lo = 1, ns_max = 1, sm = 0;
     for (int k = 0; k < p->K; ++k) {
       const pk_member* m = p->members[k];
@@ -554,7 +562,7 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
     int CS = cs_lo;
     bool one_wave = false;
     int cs_hi = std::min(ns_max, pk::T_MAXCS);
-    if (const char* e = getenv("PK_FWD_CS")) cs_hi = std::max(cs_lo, std::min(cs_hi, atoi(e)));
+    if (g_plan.fwd_cluster > 0) cs_hi = std::max(cs_lo, std::min(cs_hi, g_plan.fwd_cluster));
     for (int cs = cs_hi; cs >= cs_lo; --cs) {
       if (dt != PK_F32) break;
       cudaLaunchConfig_t cfg{};
@@ -593,8 +601,9 @@ static void build_phases(pk_pack* p, bool eval, std::vector<Phase>& phases) {
   }
   // many clusters (several waves): stream the input dimension instead, one CTA
   // per unit tile, when every tensor member's streaming smem fits
-  if (!eval && tf.special == 3 && (int)tf.host.size() > 2 * 148 &&
-      !(fv && !strcmp(fv, "split"))) {  // (also reached when no m1c cluster size fits a wave)
+  if (!eval && tf.special == 3 && g_plan.fwd != 1 &&
+      ((int)tf.host.size() > 2 * 148 || g_plan.fwd == 2)) {
+    // (also reached when no m1c cluster size fits a wave)
     bool fits = true;
     int sm = 0;
     for (int k = 0; k < p->K; ++k) {
@@ -766,7 +775,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
   p->ctx = c;
   p->members.assign(members, members + k);
   p->K = k;
-  p->inline_desc = k <= pk::kInlineFeeds && !getenv("PK_NO_INLINE_DESC");
+  p->inline_desc = k <= pk::kInlineFeeds && g_plan.inline_desc;
   size_t mdsz = c->dtype == PK_F64 ? sizeof(MemberDev<double>) : sizeof(MemberDev<float>);
   std::vector<char> hm(mdsz * k);
   for (int i = 0; i < k; ++i) {
@@ -845,8 +854,7 @@ extern "C" int pk_pack_create(pk_ctx* c, pk_member* const* members, int32_t k, p
     p->ev[i] = ctx_event(c);
     p->ev_pending[i] = false;
   }
-  const char* tr = getenv("PK_TRACE");
-  if (tr && tr[0] == '1') {
+  if (g_plan.trace) {
     for (auto& ph : p->train) p->trace_len += (size_t)ph.ntiles * pk::kTraceSlots;
     if ((e = cudaMalloc((void**)&p->d_trace, p->trace_len * 8)) != cudaSuccess) return fail(e);
     cudaMemsetAsync(p->d_trace, 0, p->trace_len * 8, c->stream);
@@ -1124,4 +1132,21 @@ extern "C" int pk_pack_profile_step(pk_pack* p, const pk_feed* feeds, float* pha
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return read_result(p, slot, losses, st);
+}
+
+
+extern "C" int pk_plan_options_get(pk_plan_options* out) {
+  if (!out) return PK_ERR_ARG;
+  *out = g_plan;
+  return PK_OK;
+}
+
+extern "C" int pk_plan_options_set(const pk_plan_options* in) {
+  if (!in) {
+    g_plan = plan_defaults();
+    return PK_OK;
+  }
+  if (in->fwd < 0 || in->fwd > 2 || in->fwd_cluster < 0 || in->run_batch < 0) return PK_ERR_ARG;
+  g_plan = *in;
+  return PK_OK;
 }

@@ -239,7 +239,7 @@ extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset*
   int rc = PK_OK;
   // steps per graph launch (whole steps chained by PDL in one graph)
   int nb = 8;  // measured: config0 30.2 → 27.4 (4) → 26.3 µs/step (8)
-  if (const char* e = getenv("PK_RUN_BATCH")) nb = std::max(1, atoi(e));
+  if (g_plan.run_batch > 0) nb = g_plan.run_batch;
   if (!p->inline_desc) nb = 1;
   nb = std::min(nb, depth);
   std::vector<RunStep> pend;     // planned, not yet launched

@@ -10,7 +10,6 @@ interface so `pack_opt_*` and `load_model(device=...)` work unchanged.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 _CTL_BYTES = 80          # sizeof(pk::MemberCtl)
@@ -67,13 +66,17 @@ def _m1x_smem(RP, U, C, ns, Sb):
                 + _r4(RP * (C + 1)) + _r4(U) + 32) + 8 * RP
 
 
+def _plan():
+    """the library's current kernel plan (csrc eligibility reads the same)"""
+    from . import _lib
+    return _lib.plan_options()
+
+
 def uses_m1x(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
     """Mirror of csrc m1x_eligible(): the one-launch cluster step (fp32, one
     hidden layer, <= 32 classes, <= 64 rows, H and D multiples of 4, one
     cluster of <= 16 CTAs covers the hidden layer within the smem budget)."""
-    import os
-    if precision != "f32" or len(arch.hidden) != 1 or os.environ.get("PK_NO_M1X") \
-            or not os.environ.get("PK_M1X"):
+    if precision != "f32" or len(arch.hidden) != 1 or not _plan()["m1x"]:
         return False
     D, H, C = arch.input_dim, arch.hidden[0], arch.classes
     if C > _X_MAXC or batch_size > _X_MAXR or H % 4 or D % 4:
@@ -90,8 +93,7 @@ def uses_m1t(arch, optimizer: str, batch_size: int, precision="f32") -> bool:
     """Mirror of csrc m1t_eligible(): the tcgen05 3xTF32 one-hidden-layer
     step (fp32, <= 32 classes, <= 128 rows, H and D multiples of 4, smem fits),
     for members the one-launch cluster step does not take."""
-    import os
-    if precision != "f32" or len(arch.hidden) != 1 or os.environ.get("PK_NO_TCGEN05"):
+    if precision != "f32" or len(arch.hidden) != 1 or not _plan()["tcgen05"]:
         return False
     if uses_m1x(arch, optimizer, batch_size, precision):
         return False
@@ -118,7 +120,7 @@ def uses_fused_mlp1(arch, optimizer: str, batch_size: int, precision="f32") -> b
         return False
     if len(arch.hidden) != 1 or arch.classes > _M1_MAXC or batch_size > _M1_MAXR:
         return False
-    if precision == "f64" or os.environ.get("PK_NO_MLP1"):  # phase kernels win in f64
+    if precision == "f64" or not _plan()["mlp1"]:  # phase kernels win in f64
         return False
     es = 8 if precision == "f64" else 4
     vec = 16 // es

@@ -571,7 +571,7 @@ def _native_run(packed: PackedModel, datasets, max_steps: int, depth: int):
             keep += [orders, oa]
             if stream:
                 d.host_x, d.host_ld = x.ctypes.data, x.strides[0] // x.itemsize
-                if not _rt.env_flag("PK_HOST_GATHER"):
+                if not _rt.option("host_gather"):
                     d.mapped_x, d.mapped_y = rt.host_rows_mapped(ds)
             else:
                 dev = rt.dataset(ds)
@@ -624,7 +624,7 @@ def packed_run(packed: PackedModel, datasets, max_steps: int, depth: int = 16,
     anything the native loop hands back).  Both produce the reference
     packed_step loop's state bit for bit."""
     out = []
-    if native and max_steps > 0 and not _rt.env_flag("PK_PY_RUN"):
+    if native and max_steps > 0 and not _rt.option("py_run"):
         out, finished = _native_run(packed, datasets, max_steps, depth)
         packed._spec = None
         if finished or len(out) >= max_steps:

@@ -34,9 +34,25 @@ def set_input_mode(mode: str):
     _DEFAULT["inputs"] = mode
 
 
-def env_flag(name: str) -> bool:
-    """A set, non-empty environment switch (measurement / A-B toggles)."""
-    return bool(os.environ.get(name))
+# host-side transport / driver options (the device kernel plan is
+# _lib.set_plan_options): host_gather = streamed inputs gathered by the host into
+# pinned memory + H2D copy instead of the device pulling rows over PCIe;
+# py_run = packed_run stepped from Python instead of the native pk_pack_run
+_OPTIONS = {"host_gather": False, "py_run": False}
+
+
+def set_options(**kw) -> dict:
+    """Set host-side runtime options; returns the previous values."""
+    prev = dict(_OPTIONS)
+    for k, v in kw.items():
+        if k not in _OPTIONS:
+            raise KeyError(f"unknown runtime option {k!r}")
+        _OPTIONS[k] = bool(v)
+    return prev
+
+
+def option(name: str) -> bool:
+    return _OPTIONS[name]
 
 
 def input_mode() -> str:

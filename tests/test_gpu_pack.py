@@ -437,18 +437,15 @@ def test_fwd_input_ranges_lockstep_parity():
     lockstep(packing.dedup_inputs(packing.pack_models(hs)), datasets, 5, packing=packing)
 
 
-def test_narrow_wgrad_tiles_match_square_tiles_bitwise(monkeypatch):
+def test_narrow_wgrad_tiles_match_square_tiles_bitwise(plan):
     """Weight-gradient tiles of narrow layers (out <= 16) are 64x16 instead of
     32x32: the per-element sums keep their order, so the trajectories are
-    bit-identical to the 32x32 tiles (PK_NO_WGRAD_NARROW=1)."""
+    bit-identical to the 32x32 tiles (plan option wgrad_narrow=0)."""
     datasets = _ds(n=300, d=100, c=10, seed=4)
     arch = packing.MLPArch(100, (16, 12), 10, "tanh")
     runs = []
     for narrow in (True, False):
-        if narrow:
-            monkeypatch.delenv("PK_NO_WGRAD_NARROW", raising=False)
-        else:
-            monkeypatch.setenv("PK_NO_WGRAD_NARROW", "1")
+        plan(wgrad_narrow=int(narrow))
         hs = [packing.make_handle(f"w{i}", arch, opt, 0.01, 24, 20, "d", i)
               for i, opt in enumerate(("adam", "momentum"))]
         packed = packing.pack_models(hs)
@@ -639,11 +636,11 @@ def test_costmodel_calibrates_on_device():
 
 # ------------------------------------------- tcgen05 path: schedule shapes --
 
-def test_tensor_path_grouped_input_tiles_lockstep(monkeypatch):
+def test_tensor_path_grouped_input_tiles_lockstep(plan):
     """8 wide members (mixed optimizers) on the tcgen05 path: the backward
     groups several 128-input tiles per CTA (G > 1) with two cp.async stages;
     one-step parity with the f64 oracle and packed == standalone bitwise."""
-    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
+    plan(m1x=0)  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=7, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "tanh")
@@ -659,10 +656,10 @@ def test_tensor_path_grouped_input_tiles_lockstep(monkeypatch):
     assert _maxdiff(hs[5], solo) == 0.0
 
 
-def test_tensor_path_batch_128_rows_lockstep(monkeypatch):
+def test_tensor_path_batch_128_rows_lockstep(plan):
     """RP = 128 rows (batch 100): four 32-row K chunks per backward tile and
     one input-tile stage; parity with the oracle."""
-    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
+    plan(m1x=0)  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"t": data.synth_dataset(1000, 200, 7, seed=8, spread=0.5)}
     arch = packing.MLPArch(200, (36,), 7, "sigmoid")
@@ -687,11 +684,11 @@ def test_pack_beyond_inline_descriptors():
     assert _maxdiff(hs[7], solo) == 0.0
 
 
-def test_streaming_forward_large_pack_lockstep(monkeypatch):
+def test_streaming_forward_large_pack_lockstep(plan):
     """12 x 784-256-10 members: the split-K clusters would take > 2 waves, so
     the forward streams the input dimension in one CTA per unit tile
     (k_m1s_fwd); parity with the oracle, packed == standalone bitwise."""
-    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
+    plan(m1x=0)  # exercise the tcgen05 path
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=11, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "leaky_relu")
     opts = ("sgd", "momentum", "adagrad", "adam")
@@ -707,12 +704,12 @@ def test_streaming_forward_large_pack_lockstep(monkeypatch):
     assert _maxdiff(hs[4], solo) == 0.0
 
 
-def test_tensor_path_ragged_heterogeneous_pack(monkeypatch):
+def test_tensor_path_ragged_heterogeneous_pack(plan):
     """Config-3-style heterogeneous pack on the tensor path: members with
     different hidden widths, class counts, batch sizes and input datasets
     (dimensions) share one pack — dummy cluster splits for the shallower
     inputs, ragged unit tiles; oracle parity and K-invariance."""
-    monkeypatch.setenv("PK_NO_M1X", "1")  # exercise the tcgen05 path
+    plan(m1x=0)  # exercise the tcgen05 path
     from paper_2002_02885_b200 import device
     ds = {"a": data.synth_dataset(800, 784, 10, seed=12, spread=0.5),
           "b": data.synth_dataset(600, 256, 32, seed=13, spread=0.5)}
@@ -732,12 +729,12 @@ def test_tensor_path_ragged_heterogeneous_pack(monkeypatch):
 
 # ------------------------------------- one-launch cluster step (k_m1x) --
 
-def test_m1x_mixed_optimizers_lockstep_and_cluster_size_invariance(monkeypatch):
+def test_m1x_mixed_optimizers_lockstep_and_cluster_size_invariance(plan):
     """8 x 784-256-10 members (all four optimizers) on the one-launch cluster
     step: parity with the f64 oracle per step, and the packed member equals
     its standalone run bit for bit although the pack runs 8-CTA clusters
     (2 unit blocks per CTA) and the singleton 16-CTA clusters (1 block)."""
-    monkeypatch.setenv("PK_M1X", "1")
+    plan(m1x=1)
     from paper_2002_02885_b200 import device
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=31, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "relu")
@@ -754,12 +751,12 @@ def test_m1x_mixed_optimizers_lockstep_and_cluster_size_invariance(monkeypatch):
         assert _maxdiff(hs[i], solo) == 0.0
 
 
-def test_m1x_ragged_units_rows_and_classes_lockstep(monkeypatch):
+def test_m1x_ragged_units_rows_and_classes_lockstep(plan):
     """Members whose hidden width is not a multiple of the 16-unit block
     (partial last block, idle cluster ranks), 64-row padding (batch 50),
     odd class counts and every activation, in one heterogeneous pack with two
     input datasets; oracle parity and packed == standalone."""
-    monkeypatch.setenv("PK_M1X", "1")
+    plan(m1x=1)
     from paper_2002_02885_b200 import device
     ds = {"a": data.synth_dataset(700, 64, 7, seed=32, spread=0.5),
           "b": data.synth_dataset(500, 100, 3, seed=33, spread=0.5)}
@@ -778,16 +775,14 @@ def test_m1x_ragged_units_rows_and_classes_lockstep(monkeypatch):
     assert _maxdiff(hs[2], solo) == 0.0
 
 
-def test_m1x_and_tensor_path_agree(monkeypatch):
+def test_m1x_and_tensor_path_agree(plan):
     """The same member trained by the one-launch FFMA step and by the tcgen05
     3xTF32 path: both within the stated fp32 tolerance of each other."""
     ds = {"t": data.synth_dataset(2000, 784, 10, seed=34, spread=0.5)}
     arch = packing.MLPArch(784, (128,), 10, "tanh")
     out = {}
     for path in ("m1x", "m1t"):
-        monkeypatch.setenv("PK_M1X", "1")
-        if path == "m1t":
-            monkeypatch.setenv("PK_NO_M1X", "1")
+        plan(m1x=int(path == "m1x"))
         h = packing.make_handle("a", arch, "momentum", 0.02, 32, 50, "t", 3)
         for _ in range(4):
             loss = packing.standalone_step(h, ds)
@@ -830,7 +825,7 @@ def test_packed_run_equals_packed_step_loop():
 
 
 @pytest.mark.parametrize("mode", ["resident", "stream"])
-def test_native_run_matches_python_loop_two_datasets(mode, monkeypatch):
+def test_native_run_matches_python_loop_two_datasets(mode):
     """pk_pack_run (the library's multi-step driver) against the Python
     sliding window and the packed_step loop: two datasets, four batch sizes
     (several input groups), many epoch rolls (the driver returns for the next
@@ -854,10 +849,11 @@ def test_native_run_matches_python_loop_two_datasets(mode, monkeypatch):
             ll.append(packing.packed_step(pl, ds))
         hn, pn = make()
         ln = packing.packed_run(pn, ds, 1 << 30, depth=8)
-        monkeypatch.setenv("PK_PY_RUN", "1")
+        runtime.set_options(py_run=True)
         hp, pp = make()
         lp = packing.packed_run(pp, ds, 1 << 30, depth=8)
     finally:
+        runtime.set_options(py_run=False)
         runtime.set_input_mode("resident")
     assert ll == ln == lp
     for a, b, c in zip(hl, hn, hp):
@@ -968,3 +964,103 @@ def test_packed_run_stops_exactly_at_a_failing_step():
         assert _maxdiff(a, b) == 0.0
         assert a.cursor.steps_done == b.cursor.steps_done
         assert a.optimizer.step_counter == b.optimizer.step_counter
+
+
+# ------------------------------- which kernel a step launched (kind codes) --
+# pk_pack_profile_step kind codes (packtrain_b200.h): 17 k_mlp1_fwd, 18 k_mlp1_bwd,
+# 19 k_m1t_fwd, 20 k_m1t_bwd, 21 k_m1s_fwd, 22 k_m1c_fwd, 23 k_m1x_step
+K_M1T_FWD, K_M1T_BWD, K_M1S_FWD, K_M1C_FWD = 19, 20, 21, 22
+
+
+def _profiled_step(packed, datasets):
+    """one real packed step run un-graphed through pk_pack_profile_step; returns
+    the launched kernels' kind codes (the step commits like packed_step)"""
+    active = packing._active_members(packed, datasets, False)
+    plan_ = packing._plan_step(packed, active, datasets, None, None)
+    code, phases, losses = plan_.dpack.profile()
+    packing._apply_result(packed, active, plan_, code, -1, -1, losses)
+    return [kind for kind, _, _, _ in phases]
+
+
+def test_forced_streaming_forward_lockstep_and_kernel(plan):
+    """plan fwd='stream': the tensor-path forward is k_m1s_fwd even for a small
+    pack; it is checked launched, one-step parity with the f64 oracle for all
+    four optimizers, and its trajectory equals the default plan's (k_m1c_fwd /
+    split-K) bit for bit — the streaming forward reproduces the split order."""
+    ds = {"t": data.synth_dataset(2000, 784, 10, seed=41, spread=0.5)}
+    arch = packing.MLPArch(784, (256,), 10, "relu")
+    opts = ("sgd", "adam", "momentum", "adagrad")
+
+    def mk(prefix):
+        return [packing.make_handle(f"{prefix}{i}", arch, opts[i], 0.01 / (1 + i), 32, 50, "t", i)
+                for i in range(4)]
+    plan(fwd="stream")
+    hs = mk("s")
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    kinds = _profiled_step(packed, ds)
+    assert K_M1S_FWD in kinds and K_M1T_BWD in kinds, kinds
+    lockstep(packed, ds, 2, packing=packing)
+    plan(fwd="auto")
+    ref = mk("s")
+    pr = packing.dedup_inputs(packing.pack_models(ref))
+    kinds = _profiled_step(pr, ds)
+    assert K_M1S_FWD not in kinds and (K_M1C_FWD in kinds or K_M1T_FWD in kinds), kinds
+    for _ in range(2):
+        packing.packed_step(pr, ds)
+    for a, b in zip(hs, ref):
+        assert _maxdiff(a, b) == 0.0
+
+
+def test_k16_shape_default_plan_uses_cluster_forward():
+    """BASELINE k16 mix (16 x 784-256-10, b = 32, four optimizers): the default
+    plan's forward is the cluster-resident k_m1c_fwd (one wave); parity per step
+    with the oracle."""
+    ds = {"t": data.synth_dataset(2000, 784, 10, seed=42, spread=0.5)}
+    arch = packing.MLPArch(784, (256,), 10, "relu")
+    opts = ("sgd", "adam", "momentum", "adagrad")
+    hs = [packing.make_handle(f"k{i}", arch, opts[i % 4], 10.0 ** -(1 + i % 4), 32, 50, "t", i)
+          for i in range(16)]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    kinds = _profiled_step(packed, ds)
+    assert K_M1C_FWD in kinds and K_M1T_BWD in kinds, kinds
+    lockstep(packed, ds, 1, packing=packing)
+
+
+def test_wide16_shape_streaming_forward_lockstep():
+    """The wide16 bench shape (16 x 784-1024-10, b = 128, four optimizers): no
+    cluster size fits one wave, so the default plan streams (k_m1s_fwd); four
+    32-row chunks per backward tile, H = 1024; one-step parity per member."""
+    ds = {"t": data.synth_dataset(1000, 784, 10, seed=43, spread=0.5)}
+    arch = packing.MLPArch(784, (1024,), 10, "relu")
+    opts = ("sgd", "adam", "momentum", "adagrad")
+    hs = [packing.make_handle(f"w{i}", arch, opts[i % 4], 10.0 ** -(1 + i % 4), 128, 20, "t", i)
+          for i in range(16)]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    kinds = _profiled_step(packed, ds)
+    assert K_M1S_FWD in kinds and K_M1T_BWD in kinds, kinds
+    lockstep(packed, ds, 1, packing=packing)
+
+
+def test_f64_hyperband_shape_lockstep():
+    """The f64 Hyperband member shape (784-16-10 on k_phase<double> with forward
+    input ranges), 8 members with every optimizer: lockstep against the oracle
+    at the f64 tolerance (rel 1e-10)."""
+    runtime.set_precision("f64")
+    try:
+        ds = {"t": data.synth_dataset(600, 784, 10, seed=44)}
+        arch = packing.MLPArch(784, (16,), 10, "relu")
+        opts = ("sgd", "adam", "momentum", "adagrad")
+        hs = [packing.make_handle(f"f{i}", arch, opts[i % 4], 0.01 * (1 + i % 3), 40, 30, "t", i)
+              for i in range(8)]
+        packed = packing.dedup_inputs(packing.pack_models(hs))
+        odata = {k: oracle_dataset(v, round32=False) for k, v in ds.items()}
+        for s in range(3):
+            oms = [oracle_from_handle(h) for h in packed.members]
+            want, _ = O.oracle_packed_step(oms, odata)
+            got = packing.packed_step(packed, ds)
+            for k in want:
+                assert abs(got[k] - want[k]) <= 1e-10 * abs(want[k]) + 1e-12, (s, k)
+            for h, m in zip(packed.members, oms):
+                assert_close_member(h, m, rtol=1e-10, atol=1e-12, what=f"f64 step {s}")
+    finally:
+        runtime.set_precision("f32")

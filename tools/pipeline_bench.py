@@ -1,6 +1,6 @@
 """Pipelined packed_run time per step (native driver), streamed and resident inputs:
     python tools/pipeline_bench.py [config0|k16|wide16]
-(PK_RUN_BATCH=n sets the steps per graph launch)."""
+(_lib.set_plan_options(run_batch=n) sets the steps per graph launch)."""
 import sys, time
 sys.path.insert(0, ".")
 import bench

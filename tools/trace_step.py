@@ -1,6 +1,6 @@
 """Stage timeline of one packed step from in-kernel %globaltimer stamps.
 
-    PK_TRACE=1 python tools/trace_step.py [--workload config0] [--warm]
+    python tools/trace_step.py [--workload config0] [--warm]   (sets plan option trace=1)
 
 Runs warm-up steps, flushes L2 (unless --warm), runs one traced step through
 the CUDA graph and prints, per phase, when its CTAs entered, had operands,
@@ -13,13 +13,14 @@ import os
 import statistics
 import sys
 
-os.environ.setdefault("PK_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2002_02885_b200 import data, packing, runtime  # noqa: E402
+from paper_2002_02885_b200 import _lib, data, packing, runtime  # noqa: E402
+
+_lib.set_plan_options(trace=1)
 
 STAGES = ("entry", "ready", "gemm", "epi1", "epi2", "done", "fin0", "fin1",
           "s8", "s9", "s10", "s11", "s12", "s13", "s14", "s15")
@@ -50,7 +51,7 @@ def main():
     dp = packed._dev[1]
     n = rt.lib.pk_pack_trace(dp.ptr, None, 0)
     if n < 0:
-        sys.exit("tracing is off (PK_TRACE=1 must be set before the pack is created)")
+        sys.exit("tracing is off (plan option trace=1 must be set before the pack is created)")
     buf = (C.c_uint64 * n)()
     rt.lib.pk_pack_trace(dp.ptr, buf, n)
     arr = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(-1, len(STAGES))
