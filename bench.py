@@ -614,6 +614,15 @@ def _cnn_line(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     line = bench_cnn.run_b200(args, world, rank, local, Clocks, L2_FLUSH_BYTES)
+    cpu = (bench_cnn.cpu_baseline(args.workload, seconds=args.cpu_seconds)
+           if args.cpu_seconds > 0 and world == 1 and rank == 0 else None)
+    hyper = None
+    if args.conv_hyperband_r > 0 and args.workload == "config1":
+        group = dist.new_group(backend="gloo") if world > 1 else None
+        hyper = bench_cnn.run_hyperband(
+            args.conv_hyperband_r, args.conv_hyperband_n, world, group,
+            cpu_ms_per_sample=(cpu["ms_per_member_step"] / bench_cnn.WORKLOADS["config1"]["batch"]
+                               if cpu else None))
     if world > 1:
         dist.destroy_process_group()
     if line is None:
@@ -621,8 +630,9 @@ def _cnn_line(args):
     out = {"metric": METRIC, "unit": UNIT}
     out.update(line)
     out["e2e"]["unit"] = UNIT
-    out["cpu_baseline"] = (bench_cnn.cpu_baseline(args.workload, seconds=args.cpu_seconds)
-                           if args.cpu_seconds > 0 and world == 1 else None)
+    out["cpu_baseline"] = cpu
+    if hyper is not None:
+        out["hyperband"] = hyper
     return out
 
 
@@ -654,6 +664,11 @@ def main():
     ap.add_argument("--hyperband-r", type=int, default=81,
                     help="pack-aware Hyperband R on the GPUs (0 = skip)")
     ap.add_argument("--hyperband-precision", default="f64", choices=["f32", "f64"])
+    ap.add_argument("--conv-hyperband-r", type=int, default=27,
+                    help="configs[4]: conv pack-aware Hyperband R with the config1 line "
+                         "(0 = skip)")
+    ap.add_argument("--conv-hyperband-n", type=int, default=600,
+                    help="configs[4]: synthetic CIFAR-shape dataset rows (10 %% validation)")
     ap.add_argument("--hyperband-ref-r", type=int, default=81,
                     help="the same Hyperband on the CPU reference (0 = skip)")
     args = ap.parse_args()

@@ -7,8 +7,8 @@
 //
 //   k_m1t_fwd  (member, 128-unit tile, 64-deep input split) per CTA:
 //              TMEM[128 units x RP rows] = W0[split, tile]ᵀ · X[rows, split]ᵀ
-//              W0 rows and the gathered X rows arrive by bulk copy (TMA
-//              engine) into shared memory; one staging pass splits them into
+//              W0 rows and the gathered X rows arrive by 16-byte cp.async
+//              into shared memory; one staging pass splits them into
 //              tf32 hi/lo K-major operands; one thread issues
 //              3 x 8 tcgen05.mma.kind::tf32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi).
 //              The splits of a tile form one thread-block cluster; partials
@@ -1071,7 +1071,7 @@ __device__ void m1c_fwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
 // One CTA per (member, 32-unit tile, group of `ng` consecutive 128-input
 // tiles).  The per-unit-tile work — logits, softmax-xent, dZ0 — is done once
 // and the group's W0 tiles (+ slots, + X columns) stream through S shared-
-// memory stages by bulk copy while the previous tile's MMA and optimizer
+// memory stages by 16-byte cp.async while the previous tile's MMA and optimizer
 // epilogue run.  Which CTA updates an element never changes its arithmetic,
 // so the grouping (chosen per pack for occupancy) keeps K-invariance.
 // The tensor / cluster paths' optimizer on one fp32 element (engine.py:302-324).

@@ -151,15 +151,7 @@ __device__ __forceinline__ float4 dsmem_ld4(uint32_t la, uint32_t rank) {
   return v;
 }
 
-// ---- bulk copies (TMA engine, no tensor map) ---------------------------------
-// dst/src 16-byte aligned, bytes a multiple of 16; completes tx on `mbar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar))
-      : "memory");
-}
+// ---- mbarrier transaction counts (TMA loads complete on them) ----------------
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
                "r"(bytes)

@@ -685,9 +685,11 @@ def test_pack_beyond_inline_descriptors():
 
 
 def test_streaming_forward_large_pack_lockstep(plan):
-    """12 x 784-256-10 members: the split-K clusters would take > 2 waves, so
-    the forward streams the input dimension in one CTA per unit tile
-    (k_m1s_fwd); parity with the oracle, packed == standalone bitwise."""
+    """12 x 784-256-10 members under the default plan: the forward is the
+    cluster-resident k_m1c_fwd here (its clusters fit one wave; the streaming
+    k_m1s_fwd is pinned by test_forced_streaming_forward_lockstep_and_kernel and
+    reached by default at the wide16 shape); parity with the oracle, packed ==
+    standalone (split-K cluster forward) bitwise."""
     plan(m1x=0)  # exercise the tcgen05 path
     ds = {"t": data.synth_dataset(3000, 784, 10, seed=11, spread=0.5)}
     arch = packing.MLPArch(784, (256,), 10, "leaky_relu")

@@ -342,3 +342,59 @@ def cpu_baseline(workload, seconds=10.0, steps=None):
             "sample": f"{done} member-steps of {wl['family']} at batch {b} (members cycled), "
                       f"oracle/cnn64.py float64 on torch CPU, {cores} threads; a K-member step "
                       f"costs K member-steps on the CPU"}
+
+
+# ------------------------------------------------- configs[4]: conv Hyperband --
+def run_hyperband(R, n, world, group, cpu_ms_per_sample=None, family="mobilenetv2",
+                  width=0.5, seed=0):
+    """BASELINE configs[4]: pack-aware Hyperband (tuner.packed_hyperband,
+    reference tuner.py:285-337) over the Table-4 space with conv members
+    (B200ConvExecutor: MobileNetV2-w0.5 on synthetic CIFAR-shape data, 10 %
+    validation split), rung groups sharded over the job's GPUs by
+    hyperband_pool (LPT, gloo control plane, no NCCL).  `original` trains every
+    config alone (the unpacked Hyperband), `knn` packs similar configs.  Wall
+    time is the max over ranks.  The reference has no conv engine, so the CPU
+    figure is an estimate: the oracle's measured float64 time per sample times
+    the samples the schedule trains."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_02885_b200 import data, hyperband_pool, tuner
+
+    ds = data.synth_dataset(n, 3 * 32 * 32, 10, seed=seed, spread=1.0)
+    # context, programs' code and the kernels' first launches outside the timing
+    warm = tuner.B200ConvExecutor(data.synth_dataset(64, 3 * 32 * 32, 10, seed=1, spread=1.0),
+                                  family=family, width=width, seed=seed)
+    warm.evaluate([tuner.ConfigSpace().config(0), tuner.ConfigSpace().config(1)], 1)
+    out = {}
+    for strategy in ("original", "knn"):
+        ex = tuner.B200ConvExecutor(ds, family=family, width=width, seed=seed)
+        if world > 1:
+            dist.barrier(group=group)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res, pool = hyperband_pool.sharded_hyperband(R, 3, ex, seed, strategy=strategy,
+                                                     group=group)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        t = torch.tensor([wall], dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        samples = res.total_epochs * ex.train.n
+        out[strategy] = {"wall_s": float(t.item()), "best_config": res.best_config.config_id,
+                         "best_loss": res.best_loss, "epochs": res.total_epochs,
+                         "evaluations": len(res.records), "packed_steps": ex.steps,
+                         "migrations": pool.migrations, "samples_trained": samples}
+    line = {"R": R, "eta": 3, "n": n, "n_train": out["knn"]["samples_trained"]
+            // max(1, out["knn"]["epochs"]), "family": family, "width": width,
+            "image": [3, 32, 32], "dtype": "bf16", "n_gpus": world,
+            "sharding": "rung groups LPT over GPUs (gloo control plane, no NCCL)",
+            "strategies": out,
+            "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
+    if cpu_ms_per_sample:
+        line["cpu_estimate"] = {
+            "original_s": out["original"]["samples_trained"] * cpu_ms_per_sample / 1e3,
+            "method": "oracle/cnn64.py float64 torch-CPU time per sample (bench cpu_baseline, "
+                      "batch 128) x samples the schedule trains; the reference has no conv "
+                      "engine (SPEC.md:15)"}
+    return line
