@@ -131,6 +131,16 @@ class Net:
         self.logits = None
 
     @property
+    def op_index(self):
+        """op name -> position in ops (ops are dataclasses: list.index compares
+        every field)"""
+        d = self.__dict__.get("_op_index")
+        if d is None or len(d) != len(self.ops):
+            d = {op.name: i for i, op in enumerate(self.ops)}
+            self.__dict__["_op_index"] = d
+        return d
+
+    @property
     def signature(self):
         """identical nets (same architecture) share launches in a pack"""
         return (self.arch.family, self.arch.classes, tuple(self.arch.image), self.arch.width)
@@ -566,6 +576,41 @@ class MemberSpec:
         self.optimizer, self.lr, self.wd = optimizer, float(lr), float(wd)
 
 
+class _Arena:
+    """Bump allocator for a ConvPack's buffers: zeros(*shape, dt=) returns a view
+    of a large uint8 chunk (256-byte aligned); finish() zeroes every chunk's
+    used bytes with one memset each.  The views are only read after finish()."""
+
+    CHUNK = 64 << 20
+
+    def __init__(self, torch, dev):
+        self.torch, self.dev = torch, dev
+        self.chunks = []  # [buffer, used bytes]
+        self._es = {}
+
+    def zeros(self, *shape, dt=None):
+        torch = self.torch
+        dt = torch.float32 if dt is None else dt
+        n = 1
+        for d in shape:
+            n *= int(d)
+        es = self._es.get(dt)
+        if es is None:
+            es = self._es[dt] = torch.empty((), dtype=dt).element_size()
+        nbytes = n * es
+        if not self.chunks or self.chunks[-1][1] + nbytes > self.chunks[-1][0].numel():
+            self.chunks.append([torch.empty(max(self.CHUNK, rup(nbytes, 256)),
+                                            dtype=torch.uint8, device=self.dev), 0])
+        buf, off = self.chunks[-1]
+        self.chunks[-1][1] = rup(off + nbytes, 256)
+        return buf[off:off + nbytes].view(dt).view(*shape)
+
+    def finish(self):
+        for buf, used in self.chunks:
+            if used:
+                buf[:used].zero_()
+
+
 class ConvPack:
     """HBM state and step programs of one conv pack.
 
@@ -586,7 +631,10 @@ class ConvPack:
             for k in g:
                 self.group_of[k] = gi
         K = len(members)
-        z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=self.dev)  # noqa: E731
+        # the pack's buffers come from a few large zeroed chunks (one allocation and
+        # one memset per 64 MiB instead of one fill kernel per tensor)
+        arena = _Arena(torch, self.dev)
+        z = arena.zeros
         self._z = z
         self.state = z(K, 4, dt=torch.int32)        # step, flag, verdict, loss bits
         self.eval_loss = z(K)                        # eval-program loss per member
@@ -599,6 +647,9 @@ class ConvPack:
         self.acts = []
         for m in members:
             self.acts.append(self._alloc_acts(m))
+        arena.finish()
+        self._z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=self.dev)  # noqa: E731
+        self._arena = arena
         self._progs = {}
         self.staging = {}   # leader -> device batch buffer (streamed inputs)
         # programs are captured / replayed on this stream (graph capture cannot use the
@@ -954,7 +1005,7 @@ class ConvPack:
         rm, rv = self.run_stats[k][op.name]
         b.run_mean, b.run_var = rm.data_ptr(), rv.data_ptr()
         b.ws = A["ws"][op.name].data_ptr()
-        b.counter = self._counter(k, 4 * net.ops.index(op))
+        b.counter = self._counter(k, 4 * net.op_index[op.name])
         b.flag = self._flag(k)
         b.rows, b.c = rows, tx.c
         b.rpb = rows_per_block(rows, tx.c)
@@ -976,7 +1027,7 @@ class ConvPack:
         d.y = self._ptr(k, op.y, "val")
         d.dw = self.grads[k][op.params[0]].data_ptr()
         d.ws = A["ws"][op.name].data_ptr()
-        d.counter = self._counter(k, 4 * net.ops.index(op))
+        d.counter = self._counter(k, 4 * net.op_index[op.name])
         d.flag = self._flag(k)
         d.n, d.h, d.w, d.c = take, tx.h, tx.w, tx.c
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
@@ -1045,7 +1096,7 @@ class ConvPack:
                     bs.fout = self._ptr(k, op.y, "val")
                     bs.dbias = self.grads[k][op.params[1]].data_ptr()
                     bs.ws = A["ws"][op.name].data_ptr()
-                    bs.counter = self._counter(k, 4 * net.ops.index(op) + 1)
+                    bs.counter = self._counter(k, 4 * net.op_index[op.name] + 1)
                     bs.flag = self._flag(k)
                     bs.rows, bs.c, bs.ld = rows, ty.c, self._ld(k, op.y)
                     bs.rpb = rows_per_block(rows, ty.c)
@@ -1103,10 +1154,10 @@ class ConvPack:
             elif op.kind == "bn":
                 rows = take * tx.h * tx.w
                 b = self._bn_struct(k, op, rows)
-                b.counter = self._counter(k, 4 * net.ops.index(op) + 1)
+                b.counter = self._counter(k, 4 * net.op_index[op.name] + 1)
                 steps.append((CNN["BN_BWD_REDUCE"], None, b, None))
                 b2 = self._bn_struct(k, op, rows)
-                b2.counter = self._counter(k, 4 * net.ops.index(op) + 1)
+                b2.counter = self._counter(k, 4 * net.op_index[op.name] + 1)
                 b2.accumulate = acc(op.x)
                 if op.res:
                     b2.dres = self._ptr(k, op.res, "grad")
@@ -1114,7 +1165,7 @@ class ConvPack:
                 steps.append((CNN["BN_BWD_APPLY"], None, b2, None))
             elif op.kind == "dw":
                 d = self._dw_struct(k, op, take)
-                d.counter = self._counter(k, 4 * net.ops.index(op) + 1)
+                d.counter = self._counter(k, 4 * net.op_index[op.name] + 1)
                 steps.append((CNN["DW_WGRAD"], None, d, None))
                 d2 = self._dw_struct(k, op, take)
                 d2.y = self._ptr(k, op.x, "grad")
