@@ -225,7 +225,7 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_PUBLISH_T: {
       const pk_cnn_tpose& P = *static_cast<const pk_cnn_tpose*>(pr);
-      return P.taps * cdiv(P.k, 32) * cdiv(P.c, 32);
+      return P.taps * cdiv(P.k, cnn::kTposeTile) * cdiv(P.c, cnn::kTposeTile);
     }
     case PK_CNN_GATHER: {
       const pk_cnn_gather& P = *static_cast<const pk_cnn_gather*>(pr);
@@ -269,6 +269,8 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_AVGPOOL_BWD: {
       const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
       if (P.c % 8 || P.r * P.s > 255 || P.stride < 1) return "pool: c % 8, window <= 255";
+      if ((long long)P.n * std::max(P.h * P.w, P.p * P.q) * (P.c / 8) >= (1LL << 31))
+        return "pool: n*h*w*c/8 must stay below 2^31";
       break;
     }
     case PK_CNN_BIAS_ACT_BWD: {

@@ -906,9 +906,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_dw_wgrad(const __grid_constant__ 
 // Bodies are templates on the window / stride (0 = runtime value) so the
 // common shapes (3x3/2 ResNet stem, 2x2/2 LeNet) unroll their tap loops.
 template <int R_, int S_, int ST_>
-__device__ __forceinline__ void maxpool_fwd_item(const pk_cnn_pool& P, long long m, int ch) {
+__device__ __forceinline__ void maxpool_fwd_item(const pk_cnn_pool& P, int m, int ch) {
   const int R = R_ ? R_ : P.r, S = S_ ? S_ : P.s, ST = ST_ ? ST_ : P.stride;
-  const int n = (int)(m / (P.p * P.q)), rem = (int)(m - (long long)n * P.p * P.q);
+  const int n = m / (P.p * P.q), rem = m - n * P.p * P.q;
   const int oy = rem / P.q, ox = rem - oy * P.q;
   float best[8];
   uint8_t arg[8];
@@ -948,9 +948,9 @@ __device__ __forceinline__ void maxpool_fwd_item(const pk_cnn_pool& P, long long
 
 // input pixel (iy, ix) receives dy of every window whose argmax is its tap
 template <int R_, int S_, int ST_, bool AVG>
-__device__ __forceinline__ void pool_bwd_item(const pk_cnn_pool& P, long long m, int ch) {
+__device__ __forceinline__ void pool_bwd_item(const pk_cnn_pool& P, int m, int ch) {
   const int R = R_ ? R_ : P.r, S = S_ ? S_ : P.s, ST = ST_ ? ST_ : P.stride;
-  const int n = (int)(m / (P.h * P.w)), rem = (int)(m - (long long)n * P.h * P.w);
+  const int n = m / (P.h * P.w), rem = m - n * P.h * P.w;
   const int iy = rem / P.w, ix = rem - iy * P.w;
   float acc[8];
 #pragma unroll
@@ -1006,10 +1006,10 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ 
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  if (item >= (long long)P.n * P.p * P.q * cgs) return;
-  const long long m = item / cgs;
-  const int ch = 8 * (int)(item - m * cgs);
+  const int item = (blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;  // < 2^31 (host check)
+  if (item >= P.n * P.p * P.q * cgs) return;
+  const int m = item / cgs;
+  const int ch = 8 * (item - m * cgs);
   if (P.r == 3 && P.s == 3 && P.stride == 2) maxpool_fwd_item<3, 3, 2>(P, m, ch);
   else if (P.r == 2 && P.s == 2 && P.stride == 2) maxpool_fwd_item<2, 2, 2>(P, m, ch);
   else maxpool_fwd_item<0, 0, 0>(P, m, ch);
@@ -1020,10 +1020,10 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ 
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  if (item >= (long long)P.n * P.h * P.w * cgs) return;
-  const long long m = item / cgs;
-  const int ch = 8 * (int)(item - m * cgs);
+  const int item = (blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;  // < 2^31 (host check)
+  if (item >= P.n * P.h * P.w * cgs) return;
+  const int m = item / cgs;
+  const int ch = 8 * (item - m * cgs);
   if (P.r == 3 && P.s == 3 && P.stride == 2) pool_bwd_item<3, 3, 2, false>(P, m, ch);
   else if (P.r == 2 && P.s == 2 && P.stride == 2) pool_bwd_item<2, 2, 2, false>(P, m, ch);
   else pool_bwd_item<0, 0, 0, false>(P, m, ch);
@@ -1089,10 +1089,10 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_bwd(const __grid_constant__ 
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
-  const long long item = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
-  if (item >= (long long)P.n * P.h * P.w * cgs) return;
-  const long long m = item / cgs;
-  const int ch = 8 * (int)(item - m * cgs);
+  const int item = (blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;  // < 2^31 (host check)
+  if (item >= P.n * P.h * P.w * cgs) return;
+  const int m = item / cgs;
+  const int ch = 8 * (item - m * cgs);
   if (P.r == 2 && P.s == 2 && P.stride == 2) pool_bwd_item<2, 2, 2, true>(P, m, ch);
   else pool_bwd_item<0, 0, 0, true>(P, m, ch);
 }
@@ -1279,27 +1279,44 @@ __global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, cons
 }
 
 // ================= transposed bf16 weights for DGRAD (B operand) ===================
+// 64 x 64 (co x ci) tiles of one tap; 16-byte loads and stores (k, c are
+// multiples of 8, so a vector is either inside the matrix or outside it)
+constexpr int kTposeTile = 64;
 __global__ void __launch_bounds__(kBlock) k_publish_t(const __grid_constant__ Pack<pk_cnn_tpose> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_tpose& P = G.p[pi];
-  const int tk = (P.k + 31) / 32, tc = (P.c + 31) / 32;
+  const int tk = (P.k + kTposeTile - 1) / kTposeTile, tc = (P.c + kTposeTile - 1) / kTposeTile;
   int b = blockIdx.x - G.blk0[pi];
   const int tap = b / (tk * tc);
   b -= tap * tk * tc;
   const int kt = b / tc, ct = b - kt * tc;
-  __shared__ uint16_t tile[32][33];
+  __shared__ __align__(16) uint16_t tile[kTposeTile][kTposeTile + 8];
   const uint16_t* src = static_cast<const uint16_t*>(P.src);
   uint16_t* dst = static_cast<uint16_t*>(P.dst);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int co = kt * 32 + i, ci = ct * 32 + tx;
-    tile[i][tx] = (co < P.k && ci < P.c) ? src[(long long)co * P.kpad + tap * P.c + ci] : 0;
+  const int t = threadIdx.x, j = t & 7, r = t >> 3;  // 32 rows x 8 vectors per pass
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = r + 32 * h, co = kt * kTposeTile + i, ci = ct * kTposeTile + 8 * j;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (co < P.k && ci < P.c)
+      v = __ldg(reinterpret_cast<const uint4*>(src + (long long)co * P.kpad + tap * P.c + ci));
+    *reinterpret_cast<uint4*>(&tile[i][8 * j]) = v;
   }
   __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    const int ci = ct * 32 + i, co = kt * 32 + tx;
-    if (ci < P.c && co < P.k) dst[(long long)ci * P.kpadt + tap * P.k + co] = tile[tx][i];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = r + 32 * h, ci = ct * kTposeTile + o, co = kt * kTposeTile + 8 * j;
+    if (ci >= P.c || co >= P.k) continue;
+    uint16_t e[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) e[q] = tile[8 * j + q][o];
+    uint4 v;
+    v.x = e[0] | ((uint32_t)e[1] << 16);
+    v.y = e[2] | ((uint32_t)e[3] << 16);
+    v.z = e[4] | ((uint32_t)e[5] << 16);
+    v.w = e[6] | ((uint32_t)e[7] << 16);
+    *reinterpret_cast<uint4*>(dst + (long long)ci * P.kpadt + tap * P.k + co) = v;
   }
 }
 

@@ -255,13 +255,73 @@ extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset*
     } else {
       for (int i = 0; i < n; ++i) {
         int r = pk_pack_step_async(p, pfeeds.data() + (size_t)i * K, &pend[i].ticket);
-        if (r) return r;
+        if (r) {  // the steps already launched are in flight: account for them
+          for (int q = 0; q < i; ++q) fly.push_back(std::move(pend[q]));
+          pend.clear();
+          pfeeds.clear();
+          return r;
+        }
       }
     }
     for (auto& q : pend) fly.push_back(std::move(q));
     pend.clear();
     pfeeds.clear();
     return PK_OK;
+  };
+  // result of the oldest in-flight step → the real cursors (the reference's
+  // bookkeeping); `failed`: the step hit a non-finite value / gradient, the
+  // later in-flight steps were skipped on the device (halt flag)
+  auto apply_oldest = [&](bool& failed) -> int {
+    RunStep& s = fly[head++];
+    double* L = losses + (size_t)applied * K;
+    pk_status rs{};
+    int r = pk_pack_step_wait(p, s.ticket, L, &rs);
+    if (r != PK_OK && r != PK_ERR_NONFINITE_VALUE && r != PK_ERR_NONFINITE_GRAD) return r;
+    uint8_t* A = active + (size_t)applied * K;
+    memset(A, 0, K);
+    if (applied > 0)  // the reference rolls at the top of every later step
+      for (int k : s.member) run_roll(mem[k], ds[mem[k].dataset]);
+    const bool fail = rs.code != PK_OK;
+    for (size_t q = 0; q < s.member.size(); ++q) {
+      const int k = s.member[q];
+      if (rs.code == PK_ERR_NONFINITE_VALUE) break;
+      if (rs.code == PK_ERR_NONFINITE_GRAD && k >= rs.member) continue;  // pack order
+      pk_run_member& m = mem[k];
+      m.steps_done += 1;
+      m.pos += s.take[q];
+      if (m.samples_used)
+        for (int32_t r2 = 0; r2 < s.take[q]; ++r2) m.samples_used[s.idx[q][r2]] += 1;
+      A[k] = 1;
+    }
+    stats[3 * applied] = s.groups;
+    stats[3 * applied + 1] = s.physical;
+    stats[3 * applied + 2] = s.driver;
+    if (fail) {
+      *st = rs;
+      *stop = PK_RUN_FAILED;
+      *done = applied;  // the failed step is reported through st, not counted
+      for (size_t i = head; i < fly.size(); ++i) {  // skipped on the device (halt)
+        pk_status sk{};
+        pk_pack_step_wait(p, fly[i].ticket, L, &sk);
+      }
+      head = fly.size();
+      failed = true;
+      return PK_OK;
+    }
+    ++applied;
+    *done = applied;
+    return PK_OK;
+  };
+  // an error after steps were launched: their results still reach the cursors
+  // (they commit on the device), so *done and the host state stay in step with
+  // the device; then the error is returned
+  auto bail = [&](int err) -> int {
+    while (head < fly.size()) {
+      bool failed = false;
+      if (apply_oldest(failed) || failed) break;
+    }
+    *done = applied;
+    return err;
   };
   while (applied < max_steps) {
     // ---- plan + enqueue while the window has room --------------------------
@@ -327,14 +387,15 @@ extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset*
         pk_feed f{};
         if (d.host_x) {  // streamed: gather into this slot's pinned staging, H2D
           pk_pack::RunStage* g = run_stage(p, slot, gi, std::max<int64_t>(take, driver), d.dim);
-          if (!g) return arg_err(c, "run: staging allocation failed");
+          if (!g) return bail(arg_err(c, "run: staging allocation failed"));
           if ((rc = run_gather(p, slot, g, take, d, perm + key.pos, key.pos,
                                key.epoch - d.epoch0)))
-            return rc;
+            return bail(rc);
           f = pk_feed{g->d, nullptr, 0, take, gi};
         } else {
           const int64_t e = key.epoch - d.epoch0;
-          if (!d.device || !d.order || !d.order[e]) return arg_err(c, "run: missing device order");
+          if (!d.device || !d.order || !d.order[e])
+            return bail(arg_err(c, "run: missing device order"));
           f = pk_feed{d.device, d.order[e], key.pos, take, gi};
         }
         for (size_t q = i; q < j; ++q) {
@@ -356,49 +417,17 @@ extern "C" int pk_pack_run(pk_pack* p, pk_run_member* mem, const pk_run_dataset*
       pfeeds.insert(pfeeds.end(), feeds.begin(), feeds.end());
       pend.push_back(std::move(s));
       ++planned;
-      if ((int)pend.size() == nb && (rc = flush())) return rc;
+      if ((int)pend.size() == nb && (rc = flush())) return bail(rc);
     }
     // a partial batch launches when nothing more can be planned (or nothing
     // older is left to wait for)
     if (!pend.empty() && (!more || planned >= max_steps || fly.size() == head))
-      if ((rc = flush())) return rc;
+      if ((rc = flush())) return bail(rc);
     if (fly.size() == head) break;
     // ---- oldest step: result → the real cursors ------------------------------
-    RunStep& s = fly[head++];
-    double* L = losses + (size_t)applied * K;
-    pk_status rs{};
-    rc = pk_pack_step_wait(p, s.ticket, L, &rs);
-    if (rc != PK_OK && rc != PK_ERR_NONFINITE_VALUE && rc != PK_ERR_NONFINITE_GRAD) return rc;
-    uint8_t* A = active + (size_t)applied * K;
-    memset(A, 0, K);
-    if (applied > 0)  // the reference rolls at the top of every later step
-      for (int k : s.member) run_roll(mem[k], ds[mem[k].dataset]);
-    const bool fail = rs.code != PK_OK;
-    for (size_t q = 0; q < s.member.size(); ++q) {
-      const int k = s.member[q];
-      if (rs.code == PK_ERR_NONFINITE_VALUE) break;
-      if (rs.code == PK_ERR_NONFINITE_GRAD && k >= rs.member) continue;  // pack order
-      pk_run_member& m = mem[k];
-      m.steps_done += 1;
-      m.pos += s.take[q];
-      if (m.samples_used)
-        for (int32_t r = 0; r < s.take[q]; ++r) m.samples_used[s.idx[q][r]] += 1;
-      A[k] = 1;
-    }
-    stats[3 * applied] = s.groups;
-    stats[3 * applied + 1] = s.physical;
-    stats[3 * applied + 2] = s.driver;
-    if (fail) {
-      *st = rs;
-      *stop = PK_RUN_FAILED;
-      *done = applied;  // the failed step is reported through st, not counted
-      for (size_t i = head; i < fly.size(); ++i) {  // skipped on the device (halt)
-        pk_status sk{};
-        pk_pack_step_wait(p, fly[i].ticket, L, &sk);
-      }
-      return PK_OK;
-    }
-    ++applied;
+    bool failed = false;
+    if ((rc = apply_oldest(failed))) return bail(rc);
+    if (failed) return PK_OK;
   }
   *done = applied;
   return PK_OK;

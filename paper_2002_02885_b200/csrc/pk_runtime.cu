@@ -59,6 +59,10 @@ struct pk_ctx {
 
 static const char* const kAllocKind[] = {"device", "pinned", "mapped"};
 constexpr size_t kArenaBlock = size_t(8) << 20, kArenaBytes = size_t(64) << 20;
+// arenas are never returned while the context lives (their blocks are recycled
+// through the block cache); past this many, small blocks get their own
+// cudaMalloc and fall under the cache's entry / byte bound like large ones
+constexpr size_t kMaxArenas = 16;
 
 // a cached block of `kind` with bytes <= cap <= slack·bytes, else a fresh one
 static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size_t* cap,
@@ -79,8 +83,9 @@ static cudaError_t ctx_alloc(pk_ctx* c, int kind, size_t bytes, void** out, size
     return cudaSuccess;
   }
   *cap = bytes;
-  if (kind == 0 && bytes <= kArenaBlock) {
-    const size_t need = (bytes + 255) & ~size_t(255);
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (kind == 0 && bytes <= kArenaBlock &&
+      (c->arena_left >= need || c->arenas.size() < kMaxArenas)) {
     if (c->arena_left < need) {
       char* a = nullptr;
       cudaError_t e = cudaMalloc(&a, kArenaBytes);
