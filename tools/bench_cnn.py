@@ -47,6 +47,15 @@ WORKLOADS = {
 }
 
 
+def _traffic(workload, kind):
+    """measured DRAM bytes per step of a kernel kind (ncu, profiles/ncu_traffic.json,
+    tools/traffic_summary.py) or None"""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[workload][kind]
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -284,7 +293,7 @@ def run_b200(args, world, rank, local, Clocks, flush_bytes):
                        "op pulls its batch rows over PCIe; losses + commit verdicts D2H"},
         "roofline": {"bound": top["bound"], "kernel": top["kernel"], "achieved": top["achieved"],
                      "peak": peaks["bf16_tflops"] if top["bound"] == "tensor" else peaks["hbm_gbs"],
-                     "unit": top["unit"], "frac": top["frac"], "traffic": None,
+                     "unit": top["unit"], "frac": top["frac"], "traffic": _traffic(args.workload, top["kernel"]),
                      "launch_ms": top["ms"], "peak_source": peak_kind,
                      "gemm_all": {"ms": gemm_ms, "tflops": gemm_fl / (gemm_ms / 1e3) / 1e12,
                                   "frac": gemm_fl / (gemm_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}},

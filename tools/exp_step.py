@@ -1,7 +1,8 @@
 """Probe: device time of one packed conv step (bench_cnn's timing loop, L2
 flushed before every step) for a workload, optionally with a planner knob
 overridden.   python tools/exp_step.py config1 [steps] [knob=value ...]
-knobs: rpt=<rows per thread of the column reductions (cnn.rows_per_block)>"""
+knobs: rpt=<rows per thread of the column reductions (cnn.rows_per_block)>,
+       nt=wide (256-wide N tiles for N >= 256), wgnt=<WGRAD N tile for co > 64>"""
 import os
 import statistics
 import sys
@@ -23,6 +24,22 @@ if "rpt" in knobs:
     orig = cnn.rows_per_block
     cnn.rows_per_block = lambda rows, c=8, per_thread=4: orig(rows, c, rpt)
 
+if "nt" in knobs:  # N tile rule: "wide" prefers 256-wide tiles for N >= 256
+    if knobs["nt"] == "wide":
+        cnn._pick_ntile = lambda n, cap=256: cnn.rup(n, 16) if n <= cap else 256
+if "wgnt" in knobs:  # WGRAD N tile for co > 64 (rsc > 64): 128 (default) or 256
+    wg = int(knobs["wgnt"])
+    orig_wg = cnn._wgrad_cfg
+
+    def _wgcfg(k, rsc, pix, _o=orig_wg, _w=wg):
+        nt, sp = _o(k, rsc, pix)
+        if k > 64 and rsc > 64:
+            base = cnn.cdiv(k, 128) * cnn.cdiv(rsc, _w)
+            want = max(1, min(pix // 1024, cnn.cdiv(2 * 148, base)))
+            kper = cnn.rup(cnn.cdiv(pix, want), 64)
+            return _w, cnn.cdiv(pix, kper)
+        return nt, sp
+    cnn._wgrad_cfg = _wgcfg
 wl = bench_cnn.WORKLOADS[wl_name]
 K, b = wl["K"], wl["batch"]
 c, h, w = wl["image"]

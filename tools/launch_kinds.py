@@ -8,8 +8,10 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+mi = h.index("Metric Name") if "Metric Name" in h else None
 seq = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", "")) / 1e3)
-       for r in rows[hi + 1:] if len(r) > vi and "at::" not in r[ki]]
+       for r in rows[hi + 1:] if len(r) > vi and "at::" not in r[ki]
+       and (mi is None or r[mi] == "gpu__time_duration.sum")]
 starts = [i for i, (n, _) in enumerate(seq) if n.endswith("k_gather")] or [0]
 step = seq[starts[-1]:] if len(starts) > 1 else seq[len(seq) // 2:]
 agg = collections.OrderedDict()
