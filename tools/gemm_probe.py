@@ -68,6 +68,17 @@ def probe(mode, n, h, w, c, k, r, stride, K=4, nt=None, reps=20):
           f"{ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s", flush=True)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "ab":  # conv_cluster A/B on FPROP / DGRAD
+    for cl in (0, 1):
+        _lib.set_plan_options(conv_cluster=cl)
+        print("conv_cluster", cl)
+        for mode in ("FPROP", "DGRAD"):
+            probe(mode, 32, 56, 56, 64, 64, 3, 1)
+            probe(mode, 32, 28, 28, 128, 128, 3, 1)
+            probe(mode, 32, 14, 14, 256, 256, 3, 1)
+            probe(mode, 32, 7, 7, 512, 512, 3, 1)
+            probe(mode, 32, 56, 56, 256, 256, 1, 1)
+    sys.exit(0)
 for mode in ("FPROP", "DGRAD", "WGRAD"):
     probe(mode, 32, 56, 56, 64, 64, 3, 1)
     probe(mode, 32, 28, 28, 128, 128, 3, 1)

@@ -47,7 +47,9 @@ def launches(path):
     hdr = rows[0]
     ik, iv, ig, ib = (hdr.index(x) for x in ("Kernel Name", "Metric Value", "Grid Size",
                                              "Block Size"))
-    return [(short(r[ik]), r[ig], r[ib], float(r[iv].replace(",", ""))) for r in rows[1:]]
+    im = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    return [(short(r[ik]), r[ig], r[ib], float(r[iv].replace(",", ""))) for r in rows[1:]
+            if (im is None or r[im] == "gpu__time_duration.sum") and "at::" not in r[ik]]
 
 
 def full(path):
