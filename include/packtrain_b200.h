@@ -118,7 +118,12 @@ typedef struct pk_plan_options {
   int32_t inline_desc;  /* 1: step descriptors inline in the graph's kernel parameters */
   int32_t run_batch;    /* steps per graph launch in pk_pack_run (0 = 8) */
   int32_t trace;        /* 1: %globaltimer stage stamps (pk_pack_trace) */
-  int32_t reserved[6];
+  int32_t conv_cluster; /* conv path, read when a program is created: 1 (default) FPROP /
+                           DGRAD GEMMs with TMA-fed operands and K >= 512 run on CTA pairs
+                           that multicast the weight tile (k_conv_gemm_pc); 2 = CTA-pair
+                           M=256 tcgen05.mma.cta_group::2 (k_conv_gemm_p2, bit-identical,
+                           no measured gain); 0 = one CTA per tile */
+  int32_t reserved[5];
 } pk_plan_options;
 int pk_plan_options_get(pk_plan_options* out);
 int pk_plan_options_set(const pk_plan_options* in); /* NULL restores the defaults */

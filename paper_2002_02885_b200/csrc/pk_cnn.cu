@@ -480,6 +480,43 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
       L.stages = (int)std::min<size_t>(8, budget / cg::stage_bytes(ntile));
       L.persistent = 1;
       L.grid = std::min(tiles, per_sm * std::max(sms, 1));
+      // CTA pairs sharing the weight tile (k_conv_gemm_pc): FPROP / DGRAD whose
+      // activations come by 2-D / im2col TMA maps; the weight maps are re-encoded
+      // with half-height boxes (each CTA of a pair loads and multicasts one half)
+      pk_plan_options po;
+      pk_plan_options_get(&po);
+      bool pair = po.conv_cluster && kind != PK_CNN_CONV_WGRAD && ntile % 32 == 0;
+      // (short-K GEMMs — 1x1 convs with K < 512 — are epilogue-bound: no gain, measured)
+      for (int j = 0; j < L.nprob && pair; ++j)
+        pair = (L.p[j].a_mode == 1 || L.p[j].a_mode == 2) && L.p[j].splits == 1 &&
+               L.p[j].K >= 512;
+      if (pair) {
+        int pairs = 0;
+        for (int j = 0; j < L.nprob; ++j) {
+          const pk_cnn_conv& g = pr[i0 + j];
+          cg::Problem& p = L.p[j];
+          const bool ok =
+              kind == PK_CNN_CONV_FPROP
+                  ? make_map_2d(&L.tm[j], g.wt, g.k, rup(g.r * g.s * g.c, 64),
+                                rup(g.r * g.s * g.c, 64), ntile / 2)
+                  : make_map_2d(&L.tm[j], g.wt, g.c, rup(g.r * g.s * g.k, 64),
+                                rup(g.r * g.s * g.k, 64), ntile / 2);
+          if (!ok) return fail(PK_ERR_CUDA, "conv: half-box weight map");
+          p.pair0 = pairs;
+          pairs += (p.tiles_m + 1) / 2 * p.tiles_n;
+        }
+        L.cluster = 2;
+        L.total_pairs = pairs;
+        L.grid = 2 * std::min(pairs, std::max(1, per_sm * std::max(sms, 1) / 2));
+        if (po.conv_cluster == 2 && (ntile == 128 || ntile == 256)) {
+          // CTA-pair MMA: half of B per CTA → deeper rings in the same smem
+          L.pair_mma = 1;
+          const int ps = ntile == 256 ? 1 : 2;  // TMEM: 2 x NT columns per CTA
+          const size_t budget2 = (size_t)(227 * 1024) / ps - 2048;
+          L.stages = (int)std::min<size_t>(8, budget2 / cg::stage_bytes_pair(ntile));
+          L.grid = 2 * std::min(pairs, std::max(1, ps * std::max(sms, 1) / 2));
+        }
+      }
     }
     out.push_back(L);
   }
@@ -494,26 +531,72 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
 thread_local bool t_pdl = false;
 
 template <class... KArgs, class... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
-                     Args&&... args) {
+cudaError_t launch_kx(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                      int cluster, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (t_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = t_pdl ? 1 : 0;
+  cfg.numAttrs = na;
   t_pdl = true;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  return launch_kx(kern, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
 template <int MODE>
 cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
-  static bool attr_set = false, attr_set_p = false;
+  static bool attr_set = false, attr_set_p = false, attr_set_c = false;
   if (L.total_tiles == 0) return cudaSuccess;
+  if (L.cluster == 2 && L.pair_mma) {
+    if constexpr (MODE != cg::WGRAD) {
+      static bool attr_set_2 = false;
+      if (!attr_set_2) {
+        cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_p2<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set_2 = true;
+      }
+      const size_t sm2 = 1024 + (size_t)L.stages * cg::stage_bytes_pair(L.ntile) +
+                         8 * (2 * L.stages + 4) + 16;
+      return launch_kx(cg::k_conv_gemm_p2<MODE>, L.grid, cg::kThreads, sm2, st, 2, L);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (L.cluster == 2) {
+    if constexpr (MODE != cg::WGRAD) {
+      if (!attr_set_c) {
+        cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_pc<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set_c = true;
+      }
+      return launch_kx(cg::k_conv_gemm_pc<MODE>, L.grid, cg::kThreads,
+                       cg::smem_bytes(L.ntile, L.stages), st, 2, L);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (L.persistent) {
     if (!attr_set_p) {
       cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_p<MODE>,

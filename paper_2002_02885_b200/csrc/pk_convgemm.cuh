@@ -45,6 +45,7 @@ struct Problem {
   int M, N, K;                // GEMM extents (K = true reduction extent, unpadded)
   int kper;                   // WGRAD: pixels per split (multiple of 64); else 0
   int tiles_m, tiles_n, splits, tile0;
+  int pair0;                  // clustered launches: first M-tile pair of this problem
   int brow0;                  // FPROP/DGRAD: first row of this problem's B in its map
   int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
   int OH, OW;                 // spatial dims of the GEMM's pixel space
@@ -82,6 +83,11 @@ struct Launch {
   int total_tiles;
   int persistent;  // every problem TMA-fed: k_conv_gemm_p, grid < total_tiles
   int grid;
+  int cluster;     // 2: k_conv_gemm_pc — CTA pairs own adjacent M tiles and multicast
+                   //    the shared B operand (weights), each loading one half
+  int pair_mma;    // with cluster 2: k_conv_gemm_p2 — one M=256 tcgen05.mma.cta_group::2
+                   //    per k-step over the pair (each CTA holds its A rows + half of B)
+  int total_pairs;
 };
 
 __host__ __device__ inline uint32_t stage_bytes(int ntile) { return 16384u + (uint32_t)ntile * 128u; }
@@ -645,6 +651,289 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_consta
   if (warp == 4) {
     umma::fence_after();
     umma::tmem_dealloc(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Clustered persistent variant (FPROP / DGRAD with TMA-fed activations): the two
+// CTAs of a cluster own M tiles 2i and 2i+1 of the same (problem, N tile) and
+// share its B operand (the weights): each CTA's TMA thread loads its own A tile
+// and HALF of the B box (NT/2 rows), multicast to both CTAs, so the L2 → SM
+// traffic of B halves.  A stage is reusable only when both CTAs' MMAs have
+// consumed it: every CTA commits its MMAs to the `empty` barrier of both CTAs
+// (count 2).  The arithmetic per output element is the one-CTA kernel's, so
+// results are identical bit for bit.
+// ------------------------------------------------------------------------------
+__device__ __forceinline__ TileInfo decode_pair(const Launch& L, int t2, int rank) {
+  TileInfo T;
+  int pi = 0;
+  while (pi + 1 < L.nprob && t2 >= L.p[pi + 1].pair0) ++pi;
+  const Problem& P = L.p[pi];
+  const int tm2 = (P.tiles_m + 1) / 2;
+  int lt = t2 - P.pair0;
+  T.pi = pi;
+  T.split = 0;
+  T.tm = 2 * (lt % tm2) + rank;
+  T.tn = lt / tm2;
+  T.k0 = 0;
+  T.nkb = (P.K + BK - 1) / BK;
+  return T;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_pc(const __grid_constant__ Launch L) {
+  static_assert(MODE != WGRAD, "clustered variant: FPROP / DGRAD");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile, ST = L.stages;
+  const uint32_t SB = stage_bytes(NT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * SB);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)tc::cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (tid == 160) {
+    for (int s = 0; s < ST; ++s) {
+      umma::mbar_init(&full[s], 1);
+      umma::mbar_init(&empty[s], 2);  // both CTAs' MMAs release a stage
+    }
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 128);
+    }
+    umma::mbar_fence_init();
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)(2 * NT));
+  if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::cluster_sync();  // the peer's barriers are initialised before any remote arrive
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
+  const uint32_t bstride = tcols / 2;
+  const int T2 = L.total_pairs;
+  const uint32_t half = (uint32_t)NT * 64u;  // bytes of half the B box (NT/2 rows x 128 B)
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---- TMA producer: own A, half of the shared B (multicast) ----
+      int g = 0;
+      for (int t = cid; t < T2; t += ncl) {
+        const TileInfo ti = decode_pair(L, t, rank);
+        const Problem& P = L.p[ti.pi];
+        const int ohw = P.OH * P.OW, m0 = ti.tm * BM;
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          if (g >= ST) umma::mbar_wait(&empty[s], ((g / ST) + 1) & 1);
+          uint8_t* stage = smem + s * SB;
+          const int kk = kb * BK;
+          umma::mbar_arrive_expect_tx(&full[s], 16384u + (uint32_t)NT * 128u);
+          if (P.a_mode == 1) {
+            tc::tma_load_2d(stage, &L.tmA[ti.pi], kk, m0, &full[s]);
+          } else {
+            const int img = m0 / ohw, rem = m0 - img * ohw;
+            const int py = rem / P.OW, px = rem - py * P.OW;
+            const int tap = kk / P.SC, c0 = kk - tap * P.SC;
+            const int fr = tap / P.S, fs = tap - fr * P.S;
+            if (MODE == FPROP)
+              tc::tma_im2col_4d(stage, &L.tmA[ti.pi], c0, px * P.stride - P.pad,
+                                py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, &full[s]);
+            else
+              tc::tma_im2col_4d(stage, &L.tmA[ti.pi], c0, px + P.pad - (P.S - 1),
+                                py + P.pad - (P.R - 1), img, (uint16_t)(P.S - 1 - fs),
+                                (uint16_t)(P.R - 1 - fr), &full[s]);
+          }
+          tc::tma_load_2d_mc(stage + 16384 + rank * half, &L.tm[ti.pi], kk,
+                             P.brow0 + ti.tn * NT + rank * (NT / 2), &full[s], (uint16_t)3);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = tc::idesc_bf16(BM, NT, false, false);
+      const uint32_t sbase = tc::smem_u32(smem);
+      int g = 0, it = 0;
+      for (int t = cid; t < T2; t += ncl, ++it) {
+        const TileInfo ti = decode_pair(L, t, rank);
+        const int buf = it & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[buf], ((it >> 1) + 1) & 1);
+        umma::fence_after();
+        const uint32_t acc = tmem + (uint32_t)buf * bstride;
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          umma::mbar_wait(&full[s], (g / ST) & 1);
+          umma::fence_after();
+          mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0, false, false, NT);
+          tc::commit_mc(&empty[s], (uint16_t)3);
+        }
+        umma::commit(&tfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- warps 0-3: epilogue ----
+    int it = 0;
+    for (int t = cid; t < T2; t += ncl, ++it) {
+      const TileInfo ti = decode_pair(L, t, rank);
+      const int buf = it & 1;
+      umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      umma::fence_after();
+      epilogue<MODE>(L.p[ti.pi], tmem + (uint32_t)buf * bstride, warp, lane, ti.tm, ti.tn, 0,
+                     ti.nkb, NT);
+      umma::fence_before();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::cluster_sync();  // no CTA leaves while its peer may still arrive on its barriers
+  if (warp == 4) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// CTA-pair MMA variant (FPROP / DGRAD, TMA-fed activations).  The two CTAs of a
+// cluster compute M tiles 2i, 2i+1 with ONE tcgen05.mma.cta_group::2 (M = 256)
+// per K step, issued by the leader (rank 0): each CTA's smem holds its own 128 A
+// rows and HALF of the B tile (NT/2 rows), so a stage costs 16 KB + NT·64 B per
+// CTA instead of 16 KB + NT·128 B — deeper pipelines in the same shared memory.
+// Both CTAs' TMA loads complete on the leader's `full` barrier; the leader's
+// commits arrive on both CTAs' `empty` / `tfull` barriers (multicast); both
+// epilogues release a TMEM buffer on the leader's `tempty` (8 warp arrivals).
+// Each CTA's TMEM holds its 128 rows x NT columns: the epilogue is unchanged, and
+// every output element's K order is the one-CTA kernel's.
+// ------------------------------------------------------------------------------
+__host__ __device__ inline uint32_t stage_bytes_pair(int ntile) {
+  return 16384u + (uint32_t)ntile * 64u;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p2(const __grid_constant__ Launch L) {
+  static_assert(MODE != WGRAD, "CTA-pair variant: FPROP / DGRAD");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile, ST = L.stages;
+  const uint32_t SB = stage_bytes_pair(NT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * SB);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)tc::cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (tid == 160) {
+    for (int s = 0; s < ST; ++s) {
+      umma::mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      umma::mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast)
+    }
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 8);  // leader: 4 epilogue warps of each CTA
+    }
+    umma::mbar_fence_init();
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)(2 * NT));
+  if (warp == 4) tc::tmem_alloc_pair(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::cluster_sync();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
+  const uint32_t bstride = tcols / 2;
+  const int T2 = L.total_pairs;
+  const uint32_t half = (uint32_t)NT * 64u;
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs) ----
+      int g = 0;
+      for (int t = cid; t < T2; t += ncl) {
+        const TileInfo ti = decode_pair(L, t, rank);
+        const Problem& P = L.p[ti.pi];
+        const int ohw = P.OH * P.OW, m0 = ti.tm * BM;
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          if (g >= ST) umma::mbar_wait(&empty[s], ((g / ST) + 1) & 1);
+          uint8_t* stage = smem + s * SB;
+          const uint32_t fb = tc::mapa(&full[s], 0);
+          const int kk = kb * BK;
+          if (leader) umma::mbar_arrive_expect_tx(&full[s], 2u * SB);
+          if (P.a_mode == 1) {
+            tc::tma_load_2d_pair(stage, &L.tmA[ti.pi], kk, m0, fb);
+          } else {
+            const int img = m0 / ohw, rem = m0 - img * ohw;
+            const int py = rem / P.OW, px = rem - py * P.OW;
+            const int tap = kk / P.SC, c0 = kk - tap * P.SC;
+            const int fr = tap / P.S, fs = tap - fr * P.S;
+            if (MODE == FPROP)
+              tc::tma_im2col_4d_pair(stage, &L.tmA[ti.pi], c0, px * P.stride - P.pad,
+                                     py * P.stride - P.pad, img, (uint16_t)fs, (uint16_t)fr, fb);
+            else
+              tc::tma_im2col_4d_pair(stage, &L.tmA[ti.pi], c0, px + P.pad - (P.S - 1),
+                                     py + P.pad - (P.R - 1), img, (uint16_t)(P.S - 1 - fs),
+                                     (uint16_t)(P.R - 1 - fr), fb);
+          }
+          tc::tma_load_2d_pair(stage + 16384, &L.tm[ti.pi], kk,
+                               P.brow0 + ti.tn * NT + rank * (NT / 2), fb);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0 && leader) {  // ---- MMA issuer (leader only) ----
+      const uint32_t idesc = tc::idesc_bf16(2 * BM, NT, false, false);
+      const uint32_t sbase = tc::smem_u32(smem);
+      int g = 0, it = 0;
+      for (int t = cid; t < T2; t += ncl, ++it) {
+        const TileInfo ti = decode_pair(L, t, 0);
+        const int buf = it & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[buf], ((it >> 1) + 1) & 1);
+        umma::fence_after();
+        const uint32_t acc = tmem + (uint32_t)buf * bstride;
+        for (int kb = 0; kb < ti.nkb; ++kb, ++g) {
+          const int s = g % ST;
+          umma::mbar_wait(&full[s], (g / ST) & 1);
+          umma::fence_after();
+          const uint32_t a_s = sbase + s * SB, b_s = a_s + 16384;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_bf16_pair(acc, tc::sdesc_sw128(a_s + ks * 32, 16, 1024),
+                              tc::sdesc_sw128(b_s + ks * 32, 16, 1024), idesc,
+                              (kb || ks) ? 1u : 0u);
+          tc::commit_pair(&empty[s], (uint16_t)3);
+        }
+        tc::commit_pair(&tfull[buf], (uint16_t)3);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- warps 0-3: epilogue (both CTAs) ----
+    const uint32_t te0 = tc::mapa(&tempty[0], 0), te1 = tc::mapa(&tempty[1], 0);
+    int it = 0;
+    for (int t = cid; t < T2; t += ncl, ++it) {
+      const TileInfo ti = decode_pair(L, t, rank);
+      const int buf = it & 1;
+      umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      umma::fence_after();
+      epilogue<MODE>(L.p[ti.pi], tmem + (uint32_t)buf * bstride, warp, lane, ti.tm, ti.tn, 0,
+                     ti.nkb, NT);
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(buf ? te1 : te0);
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::cluster_sync();
+  if (warp == 4) {
+    umma::fence_after();
+    tc::tmem_dealloc_pair(tmem, tcols);
   }
 }
 

@@ -69,7 +69,7 @@ def probe(mode, n, h, w, c, k, r, stride, K=4, nt=None, reps=20):
 
 
 if len(sys.argv) > 1 and sys.argv[1] == "ab":  # conv_cluster A/B on FPROP / DGRAD
-    for cl in (0, 1):
+    for cl in [int(a) for a in sys.argv[2:]] or (0, 1, 2):
         _lib.set_plan_options(conv_cluster=cl)
         print("conv_cluster", cl)
         for mode in ("FPROP", "DGRAD"):
