@@ -60,3 +60,28 @@ def test_ctx_create_without_gpu_fails_loudly(so):
     ptr = ctypes.c_void_p()
     rc = so.pk_ctx_create(0, 0, ctypes.byref(ptr))
     assert rc != 0  # no silent CPU fallback
+
+
+def test_kernel_plan_roundtrip(so):
+    """pk_plan_options: the production defaults, a scoped change, invalid values
+    rejected (packtrain_b200.h)."""
+    d = _lib.plan_options()
+    assert d == {"fwd": 0, "fwd_cluster": 0, "tcgen05": 1, "mlp1": 1, "m1x": 0, "fwd_split": 1,
+                 "wgrad_narrow": 1, "inline_desc": 1, "run_batch": 0, "trace": 0,
+                 "conv_cluster": 1}
+    with _lib.kernel_plan(fwd="stream", conv_cluster=0):
+        cur = _lib.plan_options()
+        assert cur["fwd"] == 2 and cur["conv_cluster"] == 0 and cur["tcgen05"] == 1
+    assert _lib.plan_options() == d
+    with pytest.raises(_lib.PKError):
+        _lib.set_plan_options(fwd=7)
+    assert _lib.plan_options() == d
+    with pytest.raises(KeyError):
+        _lib.set_plan_options(no_such_option=1)
+
+
+def test_cnn_op_layout():
+    """pk_cnn_op: kind, nprob, cfg0, cfg1, lane, pad0 (int32) then the problems pointer."""
+    assert ctypes.sizeof(_lib.CnnOp) == 32
+    assert _lib.CnnOp.lane.offset == 16 and _lib.CnnOp.probs.offset == 24
+    assert ctypes.sizeof(_lib.PlanOptions) == 16 * 4
