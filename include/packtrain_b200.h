@@ -123,7 +123,11 @@ typedef struct pk_plan_options {
                            that multicast the weight tile (k_conv_gemm_pc); 2 = CTA-pair
                            M=256 tcgen05.mma.cta_group::2 (k_conv_gemm_p2, bit-identical,
                            no measured gain); 0 = one CTA per tile */
-  int32_t reserved[5];
+  int32_t conv_halo;    /* conv path: 1 (default) 3x3 stride-1 FPROP / DGRAD with C % 64 == 0,
+                           >= 14-wide outputs and 256-wide N tiles stage one halo box per
+                           channel block and run the nine taps on shifted operand
+                           descriptors (k_conv_gemm_halo); 0 = TMA im2col per tap */
+  int32_t reserved[4];
 } pk_plan_options;
 int pk_plan_options_get(pk_plan_options* out);
 int pk_plan_options_set(const pk_plan_options* in); /* NULL restores the defaults */

@@ -44,12 +44,12 @@ class PlanOptions(C.Structure):
     """packtrain_b200.h pk_plan_options: the MLP path's kernel plan."""
     _fields_ = [(n, C.c_int32) for n in ("fwd", "fwd_cluster", "tcgen05", "mlp1", "m1x",
                                          "fwd_split", "wgrad_narrow", "inline_desc",
-                                         "run_batch", "trace", "conv_cluster")] \
-        + [("reserved", C.c_int32 * 5)]
+                                         "run_batch", "trace", "conv_cluster", "conv_halo")] \
+        + [("reserved", C.c_int32 * 4)]
 
 
 PLAN_FIELDS = ("fwd", "fwd_cluster", "tcgen05", "mlp1", "m1x", "fwd_split", "wgrad_narrow",
-               "inline_desc", "run_batch", "trace", "conv_cluster")
+               "inline_desc", "run_batch", "trace", "conv_cluster", "conv_halo")
 FWD_PLANS = {"auto": 0, "split": 1, "stream": 2}
 
 

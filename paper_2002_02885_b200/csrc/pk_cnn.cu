@@ -468,6 +468,62 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
       tiles += p.tiles_m * p.tiles_n * p.splits;
     }
     L.total_tiles = tiles;
+    // halo tiles (k_conv_gemm_halo): every problem a 3x3 stride-1 pad-1 FPROP / DGRAD on
+    // a TMA-fed plane with C % 64 == 0 and >= 14-wide rows
+    {
+      pk_plan_options po;
+      pk_plan_options_get(&po);
+      // (measured, tools/gemm_probe.py halo: 14x14x256 N=256 tiles 46.6 -> 38.4 us; with
+      // N <= 128 the one-CTA-per-SM halo kernel trails the two-CTA im2col kernel)
+      bool halo = po.conv_halo && kind != PK_CNN_CONV_WGRAD && ntile == 256;
+      int maxab = 0;
+      for (int j = 0; j < L.nprob && halo; ++j) {
+        const cg::Problem& p = L.p[j];
+        const int pw = p.OW + 2, hrows = 4 + cg::BM / pw;
+        halo = p.a_mode == 2 && p.R == 3 && p.S == 3 && p.stride == 1 && p.pad == 1 &&
+               p.SC % 64 == 0 && p.OW >= 14 && pw <= 256 && p.OH == p.SH && p.OW == p.SW &&
+               hrows * pw * 128 <= 64 * 1024;
+        maxab = std::max(maxab, rup(hrows * pw * 128, 1024));
+      }
+      if (halo) {
+        tiles = 0;
+        for (int j = 0; j < L.nprob; ++j) {
+          const pk_cnn_conv& g = pr[i0 + j];
+          cg::Problem& p = L.p[j];
+          p.pw = p.OW + 2;
+          p.hrows = 4 + cg::BM / p.pw;
+          p.tpi = cdiv((long long)p.OH * p.pw, cg::BM);
+          p.tiles_m = g.n * p.tpi;
+          p.tile0 = tiles;
+          tiles += p.tiles_m * p.tiles_n;
+          // the input plane as a tiled 4-D map {C, W, H, N}, box {64, W + 2, hrows, 1}
+          cuuint64_t dims[4] = {(cuuint64_t)p.SC, (cuuint64_t)p.SW, (cuuint64_t)p.SH,
+                                (cuuint64_t)g.n};
+          cuuint64_t strides[3] = {(cuuint64_t)p.sld * 2, (cuuint64_t)p.SW * p.sld * 2,
+                                   (cuuint64_t)p.SH * p.SW * p.sld * 2};
+          cuuint32_t box[4] = {64, (cuuint32_t)p.pw, (cuuint32_t)p.hrows, 1};
+          cuuint32_t es[4] = {1, 1, 1, 1};
+          if (!encode_fn() ||
+              g_encode(&L.tmA[j], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(
+                           static_cast<const void*>(p.src)), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(PK_ERR_CUDA, "conv: halo tensor map");
+        }
+        L.total_tiles = tiles;
+        L.halo = 1;
+        L.abytes = maxab;
+        static int sms_h = 0;
+        if (!sms_h) cudaDeviceGetAttribute(&sms_h, cudaDevAttrMultiProcessorCount, 0);
+        const size_t room = (size_t)(227 * 1024) - 2 * (size_t)maxab - 4096;
+        L.stages = (int)std::min<size_t>(8, room / ((size_t)ntile * 128));
+        L.persistent = 1;
+        L.grid = std::min(tiles, std::max(sms_h, 1));
+        out.push_back(L);
+        continue;
+      }
+    }
     // persistent when every problem's operands come by TMA (the epilogue warps are free)
     bool all_tma = true;
     for (int j = 0; j < L.nprob; ++j)
@@ -567,6 +623,22 @@ template <int MODE>
 cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
   static bool attr_set = false, attr_set_p = false, attr_set_c = false;
   if (L.total_tiles == 0) return cudaSuccess;
+  if (L.halo) {
+    if constexpr (MODE != cg::WGRAD) {
+      static bool attr_set_h = false;
+      if (!attr_set_h) {
+        cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_halo<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set_h = true;
+      }
+      const size_t smh = 1024 + 2 * (size_t)L.abytes + (size_t)L.stages * L.ntile * 128 +
+                         8 * (2 * L.stages + 8) + 16;
+      return launch_k(cg::k_conv_gemm_halo<MODE>, L.grid, cg::kThreads, smh, st, L);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (L.cluster == 2 && L.pair_mma) {
     if constexpr (MODE != cg::WGRAD) {
       static bool attr_set_2 = false;

@@ -46,6 +46,10 @@ struct Problem {
   int kper;                   // WGRAD: pixels per split (multiple of 64); else 0
   int tiles_m, tiles_n, splits, tile0;
   int pair0;                  // clustered launches: first M-tile pair of this problem
+  int pw;                     // halo launches (k_conv_gemm_halo): padded row width W + 2 of the
+                              //   output-pixel index space (0 = plain m = (n, y, x) rows)
+  int tpi;                    // halo: M tiles per image
+  int hrows;                  // halo: input rows per halo buffer
   int brow0;                  // FPROP/DGRAD: first row of this problem's B in its map
   int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
   int OH, OW;                 // spatial dims of the GEMM's pixel space
@@ -88,6 +92,8 @@ struct Launch {
   int pair_mma;    // with cluster 2: k_conv_gemm_p2 — one M=256 tcgen05.mma.cta_group::2
                    //    per k-step over the pair (each CTA holds its A rows + half of B)
   int total_pairs;
+  int halo;        // k_conv_gemm_halo (3x3 stride-1 FPROP / DGRAD, C % 64 == 0)
+  int abytes;      // halo: bytes of one halo buffer (1024-aligned)
 };
 
 __host__ __device__ inline uint32_t stage_bytes(int ntile) { return 16384u + (uint32_t)ntile * 128u; }
@@ -243,7 +249,12 @@ __device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int wa
                                          int tm, int tn, int split, int nkb, int NT) {
   const int row = warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int m = tm * BM + row;
+  int m = tm * BM + row;
+  if (P.pw) {  // halo tiles: rows index the padded (W + 2)-wide pixels of one image
+    const int img = tm / P.tpi, o = (tm - img * P.tpi) * BM + row;
+    const int y = o / P.pw, x = o - y * P.pw;
+    m = (y < P.OH && x < P.OW) ? (img * P.OH + y) * P.OW + x : P.M;  // junk → skipped
+  }
   for (int c0 = 0; c0 < NT; c0 += 16) {
     float v[16];
     if (nkb > 0) {
@@ -934,6 +945,146 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p2(const __grid_const
   if (warp == 4) {
     umma::fence_after();
     tc::tmem_dealloc_pair(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Halo-tile variant for 3x3 stride-1 convolutions (FPROP on X, and DGRAD on dY
+// with the rotated taps), input planes with C % 64 == 0.  An M tile is 128
+// consecutive pixels of the PADDED output index o = y·(W+2) + x of one image
+// (x >= W: junk rows the epilogue drops).  Per 64-channel block, ONE 4-D TMA box
+// {64 ch, W+2 cols from x = -1, hrows rows from y = y0 - 1, 1 image} (zero fill
+// outside the image) holds every input pixel the tile's nine taps touch, laid
+// out as the same padded index; tap (r, s)'s A operand is that buffer shifted by
+// x0 + r·(W+2) + s rows (the SW128 swizzle is address-based, so a shifted K-major
+// descriptor is exact — tools/shift_test.cu).  TMA writes ≈ 1.3-2.3x the tile's
+// pixels instead of the im2col 9x.  Two rings: halo buffers (2) and weight tiles
+// (ST stages of NT x 64 K).  K order per output element: channel block outer, tap
+// inner (for C == 64 that is the im2col kernels' k order; for C > 64 it differs
+// from theirs) — fixed by the layer's shape, so packed == standalone bit for bit.
+// ------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_halo(const __grid_constant__ Launch L) {
+  static_assert(MODE != WGRAD, "halo variant: FPROP / DGRAD");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile, ST = L.stages;
+  const uint32_t AB = (uint32_t)L.abytes, BB = (uint32_t)NT * 128u;
+  uint8_t* abuf = smem;                       // 2 x AB
+  uint8_t* bbuf = smem + 2 * AB;              // ST x BB
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(bbuf + ST * BB);
+  uint64_t* bempty = bfull + ST;
+  uint64_t* afull = bempty + ST;
+  uint64_t* aempty = afull + 2;
+  uint64_t* tfull = aempty + 2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 160) {
+    for (int s = 0; s < ST; ++s) {
+      umma::mbar_init(&bfull[s], 1);
+      umma::mbar_init(&bempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&afull[b], 1);
+      umma::mbar_init(&aempty[b], 1);
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 128);
+    }
+    umma::mbar_fence_init();
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)(2 * NT));
+  if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
+  const uint32_t bstride = tcols / 2;
+  const int T = L.total_tiles;
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---- TMA producer ----
+      int g = 0, ga = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const TileInfo ti = decode_tile(L, t, false);
+        const Problem& P = L.p[ti.pi];
+        const int img = ti.tm / P.tpi, o0 = (ti.tm - img * P.tpi) * BM;
+        const int y0 = o0 / P.pw;
+        const int ncb = P.SC / 64;
+        for (int cb = 0; cb < ncb; ++cb, ++ga) {
+          const int as = ga & 1;
+          if (ga >= 2) umma::mbar_wait(&aempty[as], ((ga >> 1) + 1) & 1);
+          umma::mbar_arrive_expect_tx(&afull[as], (uint32_t)(P.hrows * P.pw * 128));
+          tc::tma_load_4d(abuf + as * AB, &L.tmA[ti.pi], cb * 64, -1, y0 - 1, img, &afull[as]);
+          for (int tap = 0; tap < 9; ++tap, ++g) {
+            const int s = g % ST;
+            if (g >= ST) umma::mbar_wait(&bempty[s], ((g / ST) + 1) & 1);
+            umma::mbar_arrive_expect_tx(&bfull[s], BB);
+            tc::tma_load_2d(bbuf + s * BB, &L.tm[ti.pi], tap * P.SC + cb * 64,
+                            P.brow0 + ti.tn * NT, &bfull[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = tc::idesc_bf16(BM, NT, false, false);
+      const uint32_t abase = tc::smem_u32(abuf), bbase = tc::smem_u32(bbuf);
+      int g = 0, ga = 0, it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+        const TileInfo ti = decode_tile(L, t, false);
+        const Problem& P = L.p[ti.pi];
+        const int img = ti.tm / P.tpi, o0 = (ti.tm - img * P.tpi) * BM;
+        const int x0 = o0 - (o0 / P.pw) * P.pw;
+        const int ncb = P.SC / 64;
+        const int buf = it & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[buf], ((it >> 1) + 1) & 1);
+        umma::fence_after();
+        const uint32_t acc = tmem + (uint32_t)buf * bstride;
+        for (int cb = 0; cb < ncb; ++cb, ++ga) {
+          const int as = ga & 1;
+          umma::mbar_wait(&afull[as], (ga >> 1) & 1);
+          umma::fence_after();
+          for (int tap = 0; tap < 9; ++tap, ++g) {
+            const int s = g % ST;
+            umma::mbar_wait(&bfull[s], (g / ST) & 1);
+            umma::fence_after();
+            const int r = tap / 3, q = tap - 3 * r;
+            const int off = MODE == FPROP ? x0 + r * P.pw + q : x0 + (2 - r) * P.pw + (2 - q);
+            const uint32_t a_s = abase + as * AB + (uint32_t)off * 128u, b_s = bbase + s * BB;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              tc::mma_bf16(acc, tc::sdesc_sw128(a_s + ks * 32, 16, 1024),
+                           tc::sdesc_sw128(b_s + ks * 32, 16, 1024), idesc,
+                           (cb || tap || ks) ? 1u : 0u);
+            umma::commit(&bempty[s]);
+          }
+          umma::commit(&aempty[as]);
+        }
+        umma::commit(&tfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- warps 0-3: epilogue ----
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+      const TileInfo ti = decode_tile(L, t, false);
+      const int buf = it & 1;
+      umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      umma::fence_after();
+      epilogue<MODE>(L.p[ti.pi], tmem + (uint32_t)buf * bstride, warp, lane, ti.tm, ti.tn, 0, 1,
+                     NT);
+      umma::fence_before();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, tcols);
   }
 }
 

@@ -128,6 +128,7 @@ static pk_plan_options plan_defaults() {
   pk_plan_options o;
   memset(&o, 0, sizeof(o));
   o.tcgen05 = o.mlp1 = o.fwd_split = o.wgrad_narrow = o.inline_desc = o.conv_cluster = 1;
+  o.conv_halo = 1;
   return o;
 }
 static pk_plan_options g_plan = plan_defaults();

@@ -185,6 +185,16 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
                : "memory");
 }
 
+// 4-D tile {c (inner), x, y, n} of a tiled tensor map (OOB → zero fill)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, int c, int x, int y,
+                                            int n, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c), "r"(x), "r"(y), "r"(n), "r"(smem_u32(mbar))
+      : "memory");
+}
+
 // 3-D tile {x (inner), y, z} of tensor map `m` → shared `dst`
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int x, int y, int z,
                                             uint64_t* mbar) {

@@ -68,7 +68,7 @@ def test_kernel_plan_roundtrip(so):
     d = _lib.plan_options()
     assert d == {"fwd": 0, "fwd_cluster": 0, "tcgen05": 1, "mlp1": 1, "m1x": 0, "fwd_split": 1,
                  "wgrad_narrow": 1, "inline_desc": 1, "run_batch": 0, "trace": 0,
-                 "conv_cluster": 1}
+                 "conv_cluster": 1, "conv_halo": 1}
     with _lib.kernel_plan(fwd="stream", conv_cluster=0):
         cur = _lib.plan_options()
         assert cur["fwd"] == 2 and cur["conv_cluster"] == 0 and cur["tcgen05"] == 1

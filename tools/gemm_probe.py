@@ -68,6 +68,15 @@ def probe(mode, n, h, w, c, k, r, stride, K=4, nt=None, reps=20):
           f"{ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s", flush=True)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "halo":  # conv_halo A/B (cluster off / on)
+    for hl, cl in ((0, 1), (1, 1)):
+        _lib.set_plan_options(conv_halo=hl, conv_cluster=cl)
+        print("conv_halo", hl, "conv_cluster", cl)
+        for mode in ("FPROP", "DGRAD"):
+            probe(mode, 32, 56, 56, 64, 64, 3, 1)
+            probe(mode, 32, 28, 28, 128, 128, 3, 1)
+            probe(mode, 32, 14, 14, 256, 256, 3, 1)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "ab":  # conv_cluster A/B on FPROP / DGRAD
     for cl in [int(a) for a in sys.argv[2:]] or (0, 1, 2):
         _lib.set_plan_options(conv_cluster=cl)

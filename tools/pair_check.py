@@ -1,5 +1,8 @@
-"""Check: CTA-pair GEMM (plan conv_cluster=2) equals the one-CTA GEMM bit for bit
-on FPROP / DGRAD problems (256 / 128-wide N tiles, odd M-tile counts)."""
+"""Check: a conv GEMM plan variant against the plain one-CTA TMA im2col GEMM on
+FPROP / DGRAD problems.   python tools/pair_check.py [pair|halo]
+  pair: plan conv_cluster=2 (CTA-pair MMA) must be bit-identical;
+  halo: plan conv_halo=1 (halo tiles) bit-identical for C == 64, else within
+        fp32 reordering (|Δ| <= 2^-7 |ref| + 1e-3 max|ref| on the bf16 outputs)."""
 import os
 import sys
 
@@ -12,8 +15,14 @@ from paper_2002_02885_b200 import _lib, cnn  # noqa: E402
 dev = torch.device("cuda", 0)
 
 
-def run(mode, n, h, w, c, k, r, cl):
-    _lib.set_plan_options(conv_cluster=cl)
+VARIANT = sys.argv[1] if len(sys.argv) > 1 else "pair"
+
+
+def run(mode, n, h, w, c, k, r, on):
+    if VARIANT == "pair":
+        _lib.set_plan_options(conv_cluster=2 if on else 0, conv_halo=0)
+    else:
+        _lib.set_plan_options(conv_cluster=0, conv_halo=1 if on else 0)
     torch.manual_seed(0)
     pad = r // 2
     p, q = h, w
@@ -42,12 +51,21 @@ def run(mode, n, h, w, c, k, r, cl):
 
 
 ok = True
-for args in (("FPROP", 8, 14, 14, 256, 256, 3), ("DGRAD", 8, 14, 14, 256, 256, 3),
-             ("FPROP", 3, 7, 7, 512, 512, 3), ("FPROP", 4, 28, 28, 128, 128, 3),
-             ("DGRAD", 4, 28, 28, 128, 128, 3), ("FPROP", 5, 9, 9, 256, 256, 1)):
-    a = run(*args, 0)
-    b = run(*args, 2)
+cases = ((("FPROP", 8, 14, 14, 256, 256, 3), ("DGRAD", 8, 14, 14, 256, 256, 3),
+          ("FPROP", 3, 7, 7, 512, 512, 3), ("FPROP", 4, 28, 28, 128, 128, 3),
+          ("DGRAD", 4, 28, 28, 128, 128, 3), ("FPROP", 5, 9, 9, 256, 256, 1))
+         if VARIANT == "pair" else
+         (("FPROP", 4, 56, 56, 64, 64, 3), ("DGRAD", 4, 56, 56, 64, 64, 3),
+          ("FPROP", 3, 28, 28, 128, 128, 3), ("DGRAD", 3, 28, 28, 128, 128, 3),
+          ("FPROP", 5, 14, 14, 256, 256, 3), ("DGRAD", 5, 14, 14, 256, 256, 3),
+          ("FPROP", 2, 15, 17, 64, 96, 3), ("FPROP", 2, 14, 14, 64, 32, 3)))
+for args in cases:
+    a = run(*args, False)
+    b = run(*args, True)
     same = torch.equal(a, b)
-    ok &= same
-    print(args, "pair == one-CTA:", same, "max |diff|", float((a - b).abs().max()), flush=True)
+    d = float((a - b).abs().max())
+    close = bool(((a - b).abs() <= 2 ** -7 * a.abs() + 1e-3 * a.abs().max()).all())
+    good = same if (VARIANT == "pair" or args[4 if args[0] == "FPROP" else 5] == 64) else close
+    ok &= good
+    print(args, VARIANT, "identical:", same, "close:", close, "max |diff|", d, flush=True)
 print("ALL OK" if ok else "MISMATCH")
