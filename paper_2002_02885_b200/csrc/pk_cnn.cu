@@ -475,7 +475,9 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
       pk_plan_options_get(&po);
       // (measured, tools/gemm_probe.py halo: 14x14x256 N=256 tiles 46.6 -> 38.4 us; with
       // N <= 128 the one-CTA-per-SM halo kernel trails the two-CTA im2col kernel)
-      bool halo = po.conv_halo && kind != PK_CNN_CONV_WGRAD && ntile == 256;
+      // C == 64 with <= 64-wide N tiles: the weights-resident form (k_conv_gemm_halo_res)
+      bool halo = po.conv_halo && kind != PK_CNN_CONV_WGRAD && (ntile == 256 || ntile <= 64);
+      bool res = ntile <= 64;
       int maxab = 0;
       for (int j = 0; j < L.nprob && halo; ++j) {
         const cg::Problem& p = L.p[j];
@@ -484,7 +486,9 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
                p.SC % 64 == 0 && p.OW >= 14 && pw <= 256 && p.OH == p.SH && p.OW == p.SW &&
                hrows * pw * 128 <= 64 * 1024;
         maxab = std::max(maxab, rup(hrows * pw * 128, 1024));
+        res = res && p.SC == 64 && p.tiles_n == 1;
       }
+      if (halo && ntile <= 64 && !res) halo = false;
       if (halo) {
         tiles = 0;
         for (int j = 0; j < L.nprob; ++j) {
@@ -512,7 +516,7 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
             return fail(PK_ERR_CUDA, "conv: halo tensor map");
         }
         L.total_tiles = tiles;
-        L.halo = 1;
+        L.halo = res ? 2 : 1;
         L.abytes = maxab;
         static int sms_h = 0;
         if (!sms_h) cudaDeviceGetAttribute(&sms_h, cudaDevAttrMultiProcessorCount, 0);
@@ -623,6 +627,21 @@ template <int MODE>
 cudaError_t launch_conv(const cg::Launch& L, cudaStream_t st) {
   static bool attr_set = false, attr_set_p = false, attr_set_c = false;
   if (L.total_tiles == 0) return cudaSuccess;
+  if (L.halo == 2) {
+    if constexpr (MODE != cg::WGRAD) {
+      static bool attr_set_r = false;
+      if (!attr_set_r) {
+        cudaError_t e = cudaFuncSetAttribute(cg::k_conv_gemm_halo_res<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set_r = true;
+      }
+      const size_t smr = 1024 + 2 * (size_t)L.abytes + 9 * (size_t)L.ntile * 128 + 8 * 10 + 16;
+      return launch_k(cg::k_conv_gemm_halo_res<MODE>, L.grid, cg::kThreads, smr, st, L);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (L.halo) {
     if constexpr (MODE != cg::WGRAD) {
       static bool attr_set_h = false;

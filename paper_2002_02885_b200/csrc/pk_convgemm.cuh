@@ -92,7 +92,8 @@ struct Launch {
   int pair_mma;    // with cluster 2: k_conv_gemm_p2 — one M=256 tcgen05.mma.cta_group::2
                    //    per k-step over the pair (each CTA holds its A rows + half of B)
   int total_pairs;
-  int halo;        // k_conv_gemm_halo (3x3 stride-1 FPROP / DGRAD, C % 64 == 0)
+  int halo;        // k_conv_gemm_halo (3x3 stride-1 FPROP / DGRAD, C % 64 == 0);
+                   // 2: the weights-resident form k_conv_gemm_halo_res (C == 64, N <= 64)
   int abytes;      // halo: bytes of one halo buffer (1024-aligned)
 };
 
@@ -1070,6 +1071,133 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_halo(const __grid_con
   } else {  // ---- warps 0-3: epilogue ----
     int it = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+      const TileInfo ti = decode_tile(L, t, false);
+      const int buf = it & 1;
+      umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      umma::fence_after();
+      epilogue<MODE>(L.p[ti.pi], tmem + (uint32_t)buf * bstride, warp, lane, ti.tm, ti.tn, 0, 1,
+                     NT);
+      umma::fence_before();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Weights-resident halo variant (C == 64, N tile <= 64: ResNet's 56x56x64 layers).
+// The nine 64-deep weight tiles of a problem (9 x NT x 128 B <= 72 KB) are loaded
+// once per problem into shared memory; a CTA owns a CONTIGUOUS range of tiles
+// (mostly one problem) and per tile waits for one halo box only, then issues its
+// 36 MMAs back to back — no per-tap barrier round trips for these short MMAs.
+// Same tap order and operands as k_conv_gemm_halo: identical results.
+// ------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_halo_res(const __grid_constant__ Launch L) {
+  static_assert(MODE != WGRAD, "halo variant: FPROP / DGRAD");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int NT = L.ntile;
+  const uint32_t AB = (uint32_t)L.abytes, BB = (uint32_t)NT * 128u;
+  uint8_t* abuf = smem;                 // 2 x AB halo buffers
+  uint8_t* bres = smem + 2 * AB;        // 9 x BB resident weight tiles
+  uint64_t* afull = reinterpret_cast<uint64_t*>(bres + 9 * BB);
+  uint64_t* aempty = afull + 2;
+  uint64_t* tfull = aempty + 2;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* wfull = tempty + 2;
+  uint64_t* wempty = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 160) {
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&afull[b], 1);
+      umma::mbar_init(&aempty[b], 1);
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 128);
+    }
+    umma::mbar_init(wfull, 1);
+    umma::mbar_init(wempty, 1);
+    umma::mbar_fence_init();
+  }
+  const uint32_t tcols = umma::tmem_cols_pow2((uint32_t)(2 * NT));
+  if (warp == 4) umma::tmem_alloc(tmem_slot, tcols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  tc::pdl_gate();
+  const uint32_t bstride = tcols / 2;
+  const int T = L.total_tiles, G = gridDim.x;
+  const int t0 = (int)((long long)T * blockIdx.x / G), t1 = (int)((long long)T * (blockIdx.x + 1) / G);
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---- TMA producer ----
+      int ga = 0, cur = -1, nw = 0;
+      for (int t = t0; t < t1; ++t, ++ga) {
+        const TileInfo ti = decode_tile(L, t, false);
+        const Problem& P = L.p[ti.pi];
+        if (ti.pi != cur) {  // this problem's weights (after the previous ones are used)
+          if (nw > 0) umma::mbar_wait(wempty, (nw - 1) & 1);
+          umma::mbar_arrive_expect_tx(wfull, 9u * BB);
+          for (int tap = 0; tap < 9; ++tap)
+            tc::tma_load_2d(bres + tap * BB, &L.tm[ti.pi], tap * 64, P.brow0 + ti.tn * NT, wfull);
+          cur = ti.pi;
+          ++nw;
+        }
+        const int img = ti.tm / P.tpi, o0 = (ti.tm - img * P.tpi) * BM;
+        const int as = ga & 1;
+        if (ga >= 2) umma::mbar_wait(&aempty[as], ((ga >> 1) + 1) & 1);
+        umma::mbar_arrive_expect_tx(&afull[as], (uint32_t)(P.hrows * P.pw * 128));
+        tc::tma_load_4d(abuf + as * AB, &L.tmA[ti.pi], 0, -1, o0 / P.pw - 1, img, &afull[as]);
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = tc::idesc_bf16(BM, NT, false, false);
+      const uint32_t abase = tc::smem_u32(abuf), bbase = tc::smem_u32(bres);
+      int ga = 0, it = 0, cur = -1, nw = 0;
+      for (int t = t0; t < t1; ++t, ++ga, ++it) {
+        const TileInfo ti = decode_tile(L, t, false);
+        const Problem& P = L.p[ti.pi];
+        if (ti.pi != cur) {
+          umma::mbar_wait(wfull, nw & 1);
+          cur = ti.pi;
+          ++nw;
+        }
+        const int img = ti.tm / P.tpi, o0 = (ti.tm - img * P.tpi) * BM;
+        const int x0 = o0 - (o0 / P.pw) * P.pw;
+        const int buf = it & 1, as = ga & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[buf], ((it >> 1) + 1) & 1);
+        umma::mbar_wait(&afull[as], (ga >> 1) & 1);
+        umma::fence_after();
+        const uint32_t acc = tmem + (uint32_t)buf * bstride;
+        for (int tap = 0; tap < 9; ++tap) {
+          const int r = tap / 3, q = tap - 3 * r;
+          const int off = MODE == FPROP ? x0 + r * P.pw + q : x0 + (2 - r) * P.pw + (2 - q);
+          const uint32_t a_s = abase + as * AB + (uint32_t)off * 128u, b_s = bbase + tap * BB;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_bf16(acc, tc::sdesc_sw128(a_s + ks * 32, 16, 1024),
+                         tc::sdesc_sw128(b_s + ks * 32, 16, 1024), idesc,
+                         (tap || ks) ? 1u : 0u);
+        }
+        umma::commit(&aempty[as]);
+        umma::commit(&tfull[buf]);
+        // last tile of this problem in the range: its weights may be replaced
+        if (t + 1 >= t1 || decode_tile(L, t + 1, false).pi != cur) umma::commit(wempty);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- warps 0-3: epilogue ----
+    int it = 0;
+    for (int t = t0; t < t1; ++t, ++it) {
       const TileInfo ti = decode_tile(L, t, false);
       const int buf = it & 1;
       umma::mbar_wait(&tfull[buf], (it >> 1) & 1);
