@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -185,7 +186,7 @@ int prob_blocks(int kind, const void* pr) {
     case PK_CNN_BN_APPLY:
     case PK_CNN_BN_BWD_APPLY: {
       const pk_cnn_bn& P = *static_cast<const pk_cnn_bn*>(pr);
-      return cnn::apply_blocks(P.rows, P.c);
+      return cnn::apply_blocks(P.rows, P.c, P.pad0);
     }
     case PK_CNN_DW_FPROP:
     case PK_CNN_DW_DGRAD: {
@@ -318,7 +319,13 @@ void make_packs(OpRec& r, const T* pr, int n, int (*blocks)(int, const void*)) {
     P.nprob = std::min(cnn::kPack, n - i0);
     for (int j = 0; j < P.nprob; ++j) {
       P.p[j] = pr[i0 + j];
-      P.blk0[j + 1] = P.blk0[j] + blocks(r.kind, &pr[i0 + j]);
+      if constexpr (std::is_same<T, pk_cnn_bn>::value) {
+        // BN apply kinds: about two waves of blocks for the whole launch (the row
+        // tiles of larger layers are looped over; an elementwise partition)
+        if (r.kind == PK_CNN_BN_APPLY || r.kind == PK_CNN_BN_BWD_APPLY)
+          P.p[j].pad0 = std::max(16, 2 * 148 * 3 / P.nprob);
+      }
+      P.blk0[j + 1] = P.blk0[j] + blocks(r.kind, &P.p[j]);
     }
     std::vector<uint8_t> raw(sizeof(P));
     memcpy(raw.data(), &P, sizeof(P));

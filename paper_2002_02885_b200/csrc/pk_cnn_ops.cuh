@@ -389,22 +389,25 @@ __host__ __device__ __forceinline__ int apply_groups(int c) {
 }
 // row tiles per block of a problem: spans of rt row tiles (elementwise kernels:
 // any partition gives the same result)
-__host__ __device__ __forceinline__ void apply_shape(int rows, int c, int& ncg, int& nrt, int& rt) {
+// maxb: block budget of the problem (pk_cnn_bn.pad0, set per launch by the host
+// from the number of problems sharing it; 0 = kApplyMaxBlocks)
+__host__ __device__ __forceinline__ void apply_shape(int rows, int c, int maxb, int& ncg, int& nrt,
+                                                     int& rt) {
   const int cgs = c >> 3, G = apply_groups(c), R = kApplyItems / G;
   ncg = (cgs + G - 1) / G;
   nrt = (rows + R - 1) / R;
-  const int spans = max(1, kApplyMaxBlocks / ncg);
+  const int spans = max(1, (maxb > 0 ? maxb : kApplyMaxBlocks) / ncg);
   rt = (nrt + spans - 1) / spans;
 }
-__host__ __device__ __forceinline__ int apply_blocks(int rows, int c) {
+__host__ __device__ __forceinline__ int apply_blocks(int rows, int c, int maxb) {
   int ncg, nrt, rt;
-  apply_shape(rows, c, ncg, nrt, rt);
+  apply_shape(rows, c, maxb, ncg, nrt, rt);
   return ((nrt + rt - 1) / rt) * ncg;
 }
-__device__ __forceinline__ ApplyTile apply_tile(int b, int rows, int c) {
+__device__ __forceinline__ ApplyTile apply_tile(int b, int rows, int c, int maxb) {
   const int cgs = c >> 3, G = apply_groups(c);
   int ncg, nrt, rt;
-  apply_shape(rows, c, ncg, nrt, rt);
+  apply_shape(rows, c, maxb, ncg, nrt, rt);
   ApplyTile T;
   T.R = kApplyItems / G;
   const int tr = b / ncg, tg = b - tr * ncg;
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bn_apply(const __grid_constant__ 
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
-  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c);
+  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c, P.pad0);
   __shared__ float scale[kApplyGroups * 8], shift[kApplyGroups * 8];
   const int t = threadIdx.x;
   if (t < T.gw * 8) {  // y = x·(γ·rstd) + (β − mean·γ·rstd)
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
-  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c);
+  const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c, P.pad0);
   // dx = γ·rstd·(g − mean(g) − xhat·mean(g·xhat)) = ca·g + cb·x + cc per channel
   __shared__ float cas[kApplyGroups * 8], cbs[kApplyGroups * 8], ccs[kApplyGroups * 8];
   const int t = threadIdx.x;
