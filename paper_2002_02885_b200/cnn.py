@@ -508,6 +508,11 @@ class DeviceConvDataset:
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
+# depthwise WGRAD fast path: channel-pixels per partial block (the planner's
+# trade-off between per-thread serial latency and partial-record traffic)
+DW_CHANNEL_PIXELS_PER_BLOCK = 4096
+
+
 def _cgp(c):
     """channel groups (of 8) rounded up to a power of two (csrc lanes_of)"""
     g = 1
@@ -1038,7 +1043,7 @@ class ConvPack:
             # per block (<= 256 blocks), a multiple of the block's pixel lanes
             lanes = (256 // _cgp(tx.c)) // 3
             pix = take * ty.h * ty.w
-            nblk = min(256, max(1, cdiv(pix * tx.c, 16384)))
+            nblk = min(256, max(1, cdiv(pix * tx.c, DW_CHANNEL_PIXELS_PER_BLOCK)))
             d.ppb = rup(cdiv(pix, nblk), lanes)
         else:
             d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)

@@ -1007,19 +1007,24 @@ extern "C" int pk_cnn_prog_profile(pk_cnn_prog* g, void* stream, float* op_ms) {
   if (!g || !op_ms) return fail(PK_ERR_ARG, "pk_cnn_prog_profile: null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t n = g->ops.size();
-  std::vector<cudaEvent_t> ev(n + 1);
+  // events around every op; a ~40 µs device spin ahead of each op keeps the GPU
+  // busy while the host enqueues the op, so an op's time is its own device time
+  // (its kernels' launch on the GPU included), not the host's enqueue latency
+  std::vector<cudaEvent_t> ev(2 * n);
   for (auto& e : ev) cudaEventCreate(&e);
   int rc = PK_OK;
-  cudaEventRecord(ev[0], st);
   for (size_t i = 0; i < n && rc == PK_OK; ++i) {
+    cnn::k_spin<<<1, 32, 0, st>>>(80000);
+    cudaEventRecord(ev[2 * i], st);
     t_pdl = false;
     cudaError_t e = run_op(g, g->ops[i], st);
     if (e != cudaSuccess) rc = fail(PK_ERR_CUDA, cudaGetErrorString(e));
-    cudaEventRecord(ev[i + 1], st);
+    cudaEventRecord(ev[2 * i + 1], st);
   }
-  if (cudaEventSynchronize(ev[n]) != cudaSuccess && rc == PK_OK)
+  if (n && cudaEventSynchronize(ev[2 * n - 1]) != cudaSuccess && rc == PK_OK)
     rc = fail(PK_ERR_CUDA, "pk_cnn_prog_profile: synchronize failed");
-  for (size_t i = 0; i < n && rc == PK_OK; ++i) cudaEventElapsedTime(&op_ms[i], ev[i], ev[i + 1]);
+  for (size_t i = 0; i < n && rc == PK_OK; ++i)
+    cudaEventElapsedTime(&op_ms[i], ev[2 * i], ev[2 * i + 1]);
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
 }

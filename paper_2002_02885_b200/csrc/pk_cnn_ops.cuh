@@ -296,6 +296,13 @@ __device__ __forceinline__ double record_total(const float* ws, int nblk, int no
   return v;
 }
 
+// profiling helper (pk_cnn_prog_profile): keep the stream busy for `cycles`
+__global__ void k_spin(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
+
 // ============================== batch norm =====================================
 __global__ void __launch_bounds__(kBlock, 3) k_bn_stats(const __grid_constant__ Pack<pk_cnn_bn> G) {
   pdl_gate();

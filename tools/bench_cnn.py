@@ -174,7 +174,8 @@ def run_b200(args, world, rank, local, Clocks, flush_bytes):
     clk = clocks.stop()
     dev_ms = sum(per)
 
-    # per-kind profile (events around every op, un-graphed)
+    # per-kind profile: events around every op, un-graphed, a device spin ahead of
+    # each op so host enqueue latency is not counted (pk_cnn_prog_profile)
     kinds = {v: k for k, v in cnn.CNN.items()}
     prof = []
     for _ in range(5):

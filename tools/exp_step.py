@@ -24,6 +24,8 @@ if "rpt" in knobs:
     orig = cnn.rows_per_block
     cnn.rows_per_block = lambda rows, c=8, per_thread=4: orig(rows, c, rpt)
 
+if "dwcp" in knobs:  # depthwise WGRAD channel-pixels per block
+    cnn.DW_CHANNEL_PIXELS_PER_BLOCK = int(knobs["dwcp"])
 if "nt" in knobs:  # N tile rule: "wide" prefers 256-wide tiles for N >= 256
     if knobs["nt"] == "wide":
         cnn._pick_ntile = lambda n, cap=256: cnn.rup(n, 16) if n <= cap else 256
