@@ -469,7 +469,7 @@ def _hyperband_b200(R, world, group, precision="f64"):
         if world > 1:
             dist.barrier(group=group)
         t0 = time.perf_counter()
-        res, pool = hyperband_pool.sharded_hyperband(R, HB["eta"], ex, HB["seed"],
+        res, pool = hyperband_pool.overlapped_hyperband(R, HB["eta"], ex, HB["seed"],
                                                      strategy=strategy, group=group)
         wall = time.perf_counter() - t0
         t = torch.tensor([wall], dtype=torch.float64)
@@ -477,10 +477,11 @@ def _hyperband_b200(R, world, group, precision="f64"):
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         out[strategy] = {"wall_s": float(t.item()), "best_config": res.best_config.config_id,
                          "best_loss": res.best_loss, "epochs": res.total_epochs,
-                         "evaluations": len(res.records), "migrations": pool.migrations}
+                         "evaluations": len(res.records), "migrations": pool.migrations,
+                         "rounds": pool.rungs}
     runtime.set_precision(prev)
     return {"R": R, "dtype": precision, "eta": HB["eta"], "n_train": int(HB["n"] * 0.9), "arch": [HB["dim"], *HB["hidden"], HB["classes"]],
-            "n_gpus": world, "sharding": "rung groups LPT over GPUs (gloo control plane, no NCCL)",
+            "n_gpus": world, "sharding": "independent brackets overlapped; each round's groups LPT over GPUs; member state moves point to point (gloo control plane, no NCCL)",
             "strategies": out,
             "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
 

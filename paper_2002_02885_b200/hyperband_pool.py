@@ -17,7 +17,8 @@ its `rung_runner`:
   across rungs and brackets exactly as in EngineExecutor (tuner.py:446-458).
   It lives on the rank that last trained it; when a later rung places the
   member elsewhere its state moves as a PKCK checkpoint (packing.py:335-417,
-  bit-exact f64 carrier of the device's values) before the rung runs.
+  bit-exact f64 carrier of the device's values) before the rung runs —
+  point to point from the owning rank to the new one on the control group.
 * The rung barrier is the gather of per-group (losses, ms): a host
   collective on the control-plane process group (gloo), never NCCL — no
   tensor of the training path crosses GPUs.  Results merge in group order,
@@ -113,18 +114,37 @@ class PackPool:
                     moves[c.config_id] = (src, dst)
         if not moves:
             return
-        mine = {}
-        for cid, (src, _dst) in sorted(moves.items()):
+        if self.world == 1:
+            self.migrations += len(moves)
+            return
+        # point to point: each moved state travels once, src → dst (a length
+        # header, then the bytes), posted asynchronously in config_id order
+        import torch
+        dist = _dist()
+        reqs, inbox = [], []
+        for cid, (src, dst) in sorted(moves.items()):
             if src == self.rank:
                 raw = executor.export_state(cid)
-                if raw is not None:
-                    mine[cid] = raw
                 executor.drop_state(cid)
-        for payload in self._all_gather(mine):
-            for cid, raw in payload.items():
-                if moves[cid][1] == self.rank:
-                    executor.import_state(cid, raw)
+                raw = raw or b""
+                hdr = torch.tensor([len(raw)], dtype=torch.int64)
+                reqs.append(dist.isend(hdr, dst, group=self.group))
+                if raw:
+                    buf = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+                    reqs.append(dist.isend(buf, dst, group=self.group))
+                    inbox.append((None, buf))  # keep the buffer alive until sent
                 self.migrated_bytes += len(raw)
+            elif dst == self.rank:
+                hdr = torch.zeros(1, dtype=torch.int64)
+                dist.recv(hdr, src, group=self.group)
+                n = int(hdr.item())
+                if n:
+                    buf = torch.empty(n, dtype=torch.uint8)
+                    dist.recv(buf, src, group=self.group)
+                    executor.import_state(cid, bytes(buf.numpy()))
+                self.migrated_bytes += n
+        for r in reqs:
+            r.wait()
         self.migrations += len(moves)
 
     # ---- the rung -------------------------------------------------------------
@@ -154,6 +174,142 @@ class PackPool:
             if kind == "error":
                 raise _unpack_exc(a)
         return [(merged[gi][1], merged[gi][2]) for gi in range(len(groups))]
+
+
+    def run_many(self, executor, tasks):
+        """One round over several rungs (overlapped brackets): tasks =
+        [(groups, r_i)]; all their groups are placed together (LPT), run, and
+        gathered in one collective.  Returns per task either ("ok", [(losses,
+        t_ms)] in group order) or ("error", exception) — the first failing group
+        of the task in group order, as the task's own rung would have raised."""
+        flat = [(ti, gi, g, r_i) for ti, (groups, r_i) in enumerate(tasks)
+                for gi, g in enumerate(groups)]
+        costs = [self.group_cost(executor, g.members, r_i) for _, _, g, r_i in flat]
+        order = sorted(range(len(flat)), key=lambda i: (-costs[i], i))
+        load = [0.0] * self.world
+        where = [0] * len(flat)
+        for i in order:
+            held = [0] * self.world
+            for c in flat[i][2].members:
+                r = self.owner.get(c.config_id)
+                if r is not None:
+                    held[r] += 1
+            best = min(range(self.world), key=lambda r: (load[r], -held[r], r))
+            where[i] = best
+            load[best] += costs[i]
+        self._migrate(executor, [g for _, _, g, _ in flat], where)
+        mine = {}
+        t0 = time.perf_counter()
+        for i, (ti, gi, g, r_i) in enumerate(flat):
+            if where[i] != self.rank:
+                continue
+            try:
+                got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
+                mine[i] = ("ok", got, t_ms)
+            except Exception as exc:  # noqa: BLE001 - returned to the task's bracket
+                mine[i] = ("error", _pack_exc(exc), 0.0)
+        self.busy_ms += (time.perf_counter() - t0) * 1000.0
+        merged = {}
+        for part in self._all_gather(mine):
+            merged.update(part)
+        for i, (_, _, g, _) in enumerate(flat):
+            for c in g.members:
+                self.owner[c.config_id] = where[i]
+        self.rungs += 1
+        out = [None] * len(tasks)
+        for i, (ti, gi, g, r_i) in enumerate(flat):
+            kind, a, t_ms = merged[i]
+            if out[ti] is not None and out[ti][0] == "error":
+                continue
+            if kind == "error":
+                out[ti] = ("error", _unpack_exc(a))
+            else:
+                out[ti] = out[ti] or ("ok", [])
+                out[ti][1].append((a, t_ms))
+        return out
+
+
+def overlapped_hyperband(R, eta, executor, seed, strategy="knn", group=None, space=None,
+                         threshold=6.0, m=27, metric="indexsum"):
+    """`tuner.packed_hyperband` (reference tuner.py:285-337) with independent
+    brackets overlapped: each round runs the next rung of every bracket whose
+    predecessors are done, all their groups placed over the ranks together.
+    Brackets are independent except through member state, which is kept per
+    config_id across brackets (tuner.py:446-458): a bracket sharing a config_id
+    with an earlier bracket waits for it, so every member sees the serial
+    order of its training.  Sampling and grouping are seeded per (bracket,
+    rung), so records, survivors, failures and the best config equal the
+    serial run's (records are reported in the serial order).  A non-executor
+    exception is raised as the serial run would raise it: that of the earliest
+    failing bracket, after every earlier bracket has finished."""
+    import math as _m
+    space = space or tuner.ConfigSpace()
+    pool = PackPool(group)
+    t0 = time.perf_counter()
+    br = []
+    for bi, (s, n, r) in enumerate(tuner.bracket_schedule(R, eta)):
+        cfgs = tuner.sample_configs(space, n, (seed, s))
+        ids = {c.config_id for c in cfgs}
+        br.append({"s": s, "r": r, "configs": cfgs, "ids": ids, "i": 0, "done": False,
+                   "deps": [bj for bj in range(bi) if ids & br[bj]["ids"]], "records": [],
+                   "bests": [], "ms": 0.0, "epochs": 0, "failure": None, "raised": None})
+    while True:
+        raised = [bi for bi, b in enumerate(br) if b["raised"] is not None]
+        stop_at = raised[0] if raised else len(br)
+        live = [bi for bi in range(stop_at) if not br[bi]["done"]]
+        if not live:
+            break
+        runnable = [bi for bi in live if all(br[d]["done"] for d in br[bi]["deps"])]
+        tasks = []
+        for bi in runnable:
+            b = br[bi]
+            r_i = max(1, int(round(b["r"] * eta ** b["i"])))
+            groups = tuner.make_groups(strategy, b["configs"], executor,
+                                       tuner._rng("group", seed, b["s"], b["i"]), threshold, m,
+                                       metric)
+            tasks.append((bi, groups, r_i))
+        results = pool.run_many(executor, [(g, r_i) for _, g, r_i in tasks])
+        for (bi, groups, r_i), res in zip(tasks, results):
+            b = br[bi]
+            if res[0] == "error":
+                exc = res[1]
+                b["done"] = True
+                if isinstance(exc, tuner.ExecutorError):
+                    b["failure"] = (b["s"], str(exc))
+                else:
+                    b["raised"] = exc
+                continue
+            losses = {}
+            for gi, (g, (got, t_ms)) in enumerate(zip(groups, res[1])):
+                b["ms"] += t_ms
+                losses.update(got)
+                for cfg in sorted(g.members, key=lambda c: c.config_id):
+                    b["records"].append(tuner.AuditRecord(b["s"], b["i"], gi, cfg.config_id, r_i,
+                                                          got[cfg.config_id], t_ms))
+                b["epochs"] += r_i * len(g.members)
+            ranked = sorted(b["configs"], key=lambda c: (losses[c.config_id], c.config_id))
+            b["bests"].append((losses[ranked[0].config_id], ranked[0]))
+            b["configs"] = ranked[:len(b["configs"]) // eta]
+            b["i"] += 1
+            if not b["configs"] or b["i"] > b["s"]:
+                b["done"] = True
+    raised = [b["raised"] for b in br if b["raised"] is not None]
+    if raised:
+        raise raised[0]
+    records, failures, total_ms, total_epochs = [], [], 0.0, 0
+    best_loss, best = _m.inf, None
+    for b in br:
+        records += b["records"]
+        total_ms += b["ms"]
+        total_epochs += b["epochs"]
+        for loss, cfg in b["bests"]:
+            if loss < best_loss:
+                best_loss, best = loss, cfg
+        if b["failure"] is not None:
+            failures.append(b["failure"])
+    res = tuner.TuneResult(best, best_loss, records, total_ms, total_epochs, failures,
+                           wall_time_ms=(time.perf_counter() - t0) * 1000.0)
+    return res, pool
 
 
 def _pack_exc(exc):

@@ -69,12 +69,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, strategy, fail_on, q, diverge_on=None):
+def _worker(rank, world, port, strategy, fail_on, q, diverge_on=None, overlap=False, R=27):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        res, pool = hyperband_pool.sharded_hyperband(27, 3, StatefulStub(fail_on, diverge_on),
-                                                     seed=3, strategy=strategy)
+        run = hyperband_pool.overlapped_hyperband if overlap else hyperband_pool.sharded_hyperband
+        res, pool = run(R, 3, StatefulStub(fail_on, diverge_on), seed=3, strategy=strategy)
         q.put((rank, _summary(res), pool.migrations, pool.rungs))
     except Exception as exc:  # noqa: BLE001 - reported to the test
         q.put((rank, ("raised", type(exc).__name__, str(exc)), -1, -1))
@@ -82,11 +82,12 @@ def _worker(rank, world, port, strategy, fail_on, q, diverge_on=None):
         dist.destroy_process_group()
 
 
-def _run_world(world, strategy, fail_on=None, diverge_on=None):
+def _run_world(world, strategy, fail_on=None, diverge_on=None, overlap=False, R=27):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, strategy, fail_on, q, diverge_on))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, strategy, fail_on, q, diverge_on,
+                                            overlap, R))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -149,3 +150,35 @@ def test_sharded_engine_error_raises_on_every_rank():
     out = _run_world(2, "knn", diverge_on=victim)
     for _, summ, _, _ in out:
         assert summ == ("raised", "NonFiniteGradient", str(ref.value))
+
+
+@pytest.mark.parametrize("strategy", ["knn", "original"])
+def test_overlapped_brackets_match_serial_world4(strategy):
+    """Brackets that share no config_id overlap (one round runs the next rung of
+    every ready bracket, all their groups LPT-placed over 4 ranks): records,
+    survivors, best config and failures equal the serial run's, in fewer
+    synchronised rounds than serial rungs."""
+    serial = tuner.packed_hyperband(81, 3, StatefulStub(), seed=3, strategy=strategy)
+    out = _run_world(4, strategy, overlap=True, R=81)
+    rungs_serial = len({(r.bracket, r.rung) for r in serial.records})
+    for rank, summ, migrations, rounds in out:
+        assert summ == _summary(serial), f"rank {rank} diverged from the serial run"
+        assert 0 < rounds < rungs_serial
+    assert len({o[2] for o in out}) == 1  # replicated ownership: same migrations everywhere
+
+
+def test_overlapped_failures_match_serial():
+    """An ExecutorError aborts only its bracket; a diverging config raises on every
+    rank the exception the serial run raises (earliest failing bracket first)."""
+    serial = tuner.packed_hyperband(27, 3, StatefulStub(), seed=3, strategy="knn")
+    victim = serial.records[5].config_id
+    ref = tuner.packed_hyperband(27, 3, StatefulStub(fail_on=victim), seed=3, strategy="knn")
+    got, _ = hyperband_pool.overlapped_hyperband(27, 3, StatefulStub(fail_on=victim), seed=3,
+                                                 strategy="knn")
+    assert _summary(got) == _summary(ref)
+    victim = serial.records[7].config_id
+    with pytest.raises(engine.NonFiniteGradient) as a:
+        tuner.packed_hyperband(27, 3, StatefulStub(diverge_on=victim), seed=3, strategy="knn")
+    out = _run_world(2, "knn", diverge_on=victim, overlap=True)
+    for _, summ, _, _ in out:
+        assert summ == ("raised", "NonFiniteGradient", str(a.value))

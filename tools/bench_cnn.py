@@ -383,7 +383,7 @@ def run_hyperband(R, n, world, group, cpu_ms_per_sample=None, family="mobilenetv
             dist.barrier(group=group)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res, pool = hyperband_pool.sharded_hyperband(R, 3, ex, seed, strategy=strategy,
+        res, pool = hyperband_pool.overlapped_hyperband(R, 3, ex, seed, strategy=strategy,
                                                      group=group)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -394,11 +394,12 @@ def run_hyperband(R, n, world, group, cpu_ms_per_sample=None, family="mobilenetv
         out[strategy] = {"wall_s": float(t.item()), "best_config": res.best_config.config_id,
                          "best_loss": res.best_loss, "epochs": res.total_epochs,
                          "evaluations": len(res.records), "packed_steps": ex.steps,
-                         "migrations": pool.migrations, "samples_trained": samples}
+                         "migrations": pool.migrations, "rounds": pool.rungs,
+                         "samples_trained": samples}
     line = {"R": R, "eta": 3, "n": n, "n_train": out["knn"]["samples_trained"]
             // max(1, out["knn"]["epochs"]), "family": family, "width": width,
             "image": [3, 32, 32], "dtype": "bf16", "n_gpus": world,
-            "sharding": "rung groups LPT over GPUs (gloo control plane, no NCCL)",
+            "sharding": "independent brackets overlapped; each round's groups LPT over GPUs; member state moves point to point (gloo control plane, no NCCL)",
             "strategies": out,
             "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
     if cpu_ms_per_sample:
