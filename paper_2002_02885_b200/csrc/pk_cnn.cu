@@ -575,7 +575,7 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         L.cluster = 2;
         L.total_pairs = pairs;
         L.grid = 2 * std::min(pairs, std::max(1, per_sm * std::max(sms, 1) / 2));
-        if (po.conv_cluster == 2 && (ntile == 128 || ntile == 256)) {
+        if (po.conv_cluster == 2 && (ntile == 64 || ntile == 128 || ntile == 256)) {
           // CTA-pair MMA: half of B per CTA → deeper rings in the same smem
           L.pair_mma = 1;
           const int ps = ntile == 256 ? 1 : 2;  // TMEM: 2 x NT columns per CTA

@@ -256,16 +256,9 @@ __device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int wa
     const int y = o / P.pw, x = o - y * P.pw;
     m = (y < P.OH && x < P.OW) ? (img * P.OH + y) * P.OW + x : P.M;  // junk → skipped
   }
-  for (int c0 = 0; c0 < NT; c0 += 16) {
-    float v[16];
-    if (nkb > 0) {
-      tc::tmem_ld16(trow + c0, v);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = 0.f;
-    }
-    const int n0 = tn * NT + c0;
-    if (m >= P.M || n0 >= P.N) continue;
+  // one 16-column chunk of the accumulator row → global
+  auto chunk = [&](int c0, float (&v)[16]) {    const int n0 = tn * NT + c0;
+    if (m >= P.M || n0 >= P.N) return;
     if (MODE == FPROP && (P.bias || P.act)) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
@@ -356,6 +349,20 @@ __device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int wa
         }
       }
     }
+    };
+  // TMEM → registers 32 columns per tcgen05.ld (one wait per 32 columns)
+  for (int c1 = 0; c1 < NT; c1 += 32) {
+    float w[2][16];
+    const bool two = c1 + 32 <= NT;
+    if (nkb > 0) {
+      if (two) tc::tmem_ld32(trow + c1, w[0], w[1]);
+      else tc::tmem_ld16(trow + c1, w[0]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) w[0][e] = w[1][e] = 0.f;
+    }
+    chunk(c1, w[0]);
+    if (two) chunk(c1 + 16, w[1]);
   }
 }
 

@@ -68,6 +68,19 @@ def probe(mode, n, h, w, c, k, r, stride, K=4, nt=None, reps=20):
           f"{ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s", flush=True)
 
 
+if __name__ != "__main__":
+    pass
+elif len(sys.argv) > 1 and sys.argv[1] == "one":  # one launch for ncu: one MODE n h w c k r halo cluster
+    a = sys.argv[2:]
+    _lib.set_plan_options(conv_halo=int(a[7]), conv_cluster=int(a[8]))
+    probe(a[0], int(a[1]), int(a[2]), int(a[3]), int(a[4]), int(a[5]), int(a[6]), 1, reps=3)
+elif len(sys.argv) > 1 and sys.argv[1] == "n64":  # N = 64 layers: im2col / pair MMA / halo
+    for hl, cl in ((0, 0), (0, 1), (0, 2), (1, 1)):
+        _lib.set_plan_options(conv_halo=hl, conv_cluster=cl)
+        print("conv_halo", hl, "conv_cluster", cl)
+        for mode in ("FPROP", "DGRAD"):
+            probe(mode, 32, 56, 56, 64, 64, 3, 1)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "halo":  # conv_halo A/B (cluster off / on)
     for hl, cl in ((0, 1), (1, 1)):
         _lib.set_plan_options(conv_halo=hl, conv_cluster=cl)
@@ -88,13 +101,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "ab":  # conv_cluster A/B on FPROP / DGR
             probe(mode, 32, 7, 7, 512, 512, 3, 1)
             probe(mode, 32, 56, 56, 256, 256, 1, 1)
     sys.exit(0)
-for mode in ("FPROP", "DGRAD", "WGRAD"):
+if __name__ == "__main__" and (len(sys.argv) == 1):
+  for mode in ("FPROP", "DGRAD", "WGRAD"):
     probe(mode, 32, 56, 56, 64, 64, 3, 1)
     probe(mode, 32, 28, 28, 128, 128, 3, 1)
     probe(mode, 32, 14, 14, 256, 256, 3, 1)
     probe(mode, 32, 7, 7, 512, 512, 3, 1)
     probe(mode, 32, 56, 56, 256, 256, 1, 1)   # a plain GEMM (1x1): M=100352, N=K=256
     probe(mode, 32, 56, 56, 256, 256, 1, 1, K=1)
-for nt in (64, 128, 256):
+  for nt in (64, 128, 256):
     probe("FPROP", 32, 14, 14, 256, 256, 3, 1, nt=nt)
     probe("FPROP", 32, 56, 56, 256, 256, 1, 1, nt=nt)

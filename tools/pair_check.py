@@ -52,6 +52,7 @@ def run(mode, n, h, w, c, k, r, on):
 
 ok = True
 cases = ((("FPROP", 8, 14, 14, 256, 256, 3), ("DGRAD", 8, 14, 14, 256, 256, 3),
+          ("FPROP", 4, 56, 56, 64, 64, 3), ("DGRAD", 3, 28, 28, 64, 64, 3),
           ("FPROP", 3, 7, 7, 512, 512, 3), ("FPROP", 4, 28, 28, 128, 128, 3),
           ("DGRAD", 4, 28, 28, 128, 128, 3), ("FPROP", 5, 9, 9, 256, 256, 1))
          if VARIANT == "pair" else
