@@ -431,7 +431,9 @@ def _cnn_workloads():
     return bench_cnn.WORKLOADS
 
 
-HB = dict(n=2000, dim=784, classes=10, hidden=(16,), eta=3, seed=0,
+# spread 0.1 (SURVEY §8d's non-degenerate trajectory): with the default 4.0 the losses
+# collapse to 0 within an epoch and selection degenerates to config_id tie-breaks
+HB = dict(n=2000, dim=784, classes=10, hidden=(16,), eta=3, seed=0, spread=0.1,
           strategies=("original", "knn"))
 
 
@@ -452,7 +454,7 @@ def _hyperband_b200(R, world, group, precision="f64"):
     import torch
     import torch.distributed as dist
     from paper_2002_02885_b200 import data, hyperband_pool, runtime, tuner
-    ds = data.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0)
+    ds = data.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0, spread=HB["spread"])
     out = {}
     # float64 device arithmetic: the reference trains in f64, and some
     # Table-4 configs (e.g. momentum lr 0.1) grow activations past the fp32
@@ -480,7 +482,8 @@ def _hyperband_b200(R, world, group, precision="f64"):
                          "evaluations": len(res.records), "migrations": pool.migrations,
                          "rounds": pool.rungs}
     runtime.set_precision(prev)
-    return {"R": R, "dtype": precision, "eta": HB["eta"], "n_train": int(HB["n"] * 0.9), "arch": [HB["dim"], *HB["hidden"], HB["classes"]],
+    return {"R": R, "dtype": precision, "eta": HB["eta"], "n_train": int(HB["n"] * 0.9),
+            "spread": HB["spread"], "arch": [HB["dim"], *HB["hidden"], HB["classes"]],
             "n_gpus": world, "sharding": "independent brackets overlapped; each round's groups LPT over GPUs; member state moves point to point (gloo control plane, no NCCL)",
             "strategies": out,
             "speedup_knn_vs_original": out["original"]["wall_s"] / out["knn"]["wall_s"]}
@@ -491,7 +494,7 @@ def _hyperband_reference(R):
     if _ref_packtrain() is None:
         return None
     from packtrain import data as rdata, tuner as rtuner
-    ds = rdata.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0)
+    ds = rdata.synth_dataset(HB["n"], HB["dim"], HB["classes"], seed=0, spread=HB["spread"])
     out = {}
     for strategy in HB["strategies"]:
         ex = rtuner.EngineExecutor(ds, hidden=HB["hidden"], seed=HB["seed"])
