@@ -351,8 +351,36 @@ struct pk_cnn_prog {
 
 namespace {
 
-int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stages,
+// stride-2 DGRAD of a 3x3 pad-1 or 1x1 pad-0 conv on even planes runs as four
+// stride-1 problems, one per dX parity class (a, b) = (y & 1, x & 1): class pixels
+// (2i + a, 2j + b) read dY at (i + dr, j + ds) for the taps (r, s) with r ≡ a + pad,
+// s ≡ b + pad (mod 2) — no zero taps reach the tensor cores (a 3x3 class has 1, 2
+// or 4 taps; a 1x1 conv's odd classes have none and write zeros / keep the sum)
+bool dgrad_parity(const pk_cnn_conv& g) {
+  return g.stride == 2 && g.h == 2 * g.p && g.w == 2 * g.q && g.k % 64 == 0 &&
+         ((g.r == 3 && g.s == 3 && g.pad == 1) || (g.r == 1 && g.s == 1 && g.pad == 0));
+}
+
+int conv_to_launches(int kind, const pk_cnn_conv* pr0, int n0, int ntile, int stages,
                      std::vector<cg::Launch>& out) {
+  // (problem, parity class or -1) items; parity DGRADs expand to four
+  std::vector<pk_cnn_conv> exp;
+  std::vector<int> cls;
+  for (int i = 0; i < n0; ++i) {
+    if (kind == PK_CNN_CONV_DGRAD && dgrad_parity(pr0[i])) {
+      // a 1x1 conv's odd classes have no tap: needed only to write zeros
+      const int ncls = pr0[i].r == 1 && pr0[i].accumulate ? 1 : 4;
+      for (int c = 0; c < ncls; ++c) {
+        exp.push_back(pr0[i]);
+        cls.push_back(c);
+      }
+    } else {
+      exp.push_back(pr0[i]);
+      cls.push_back(-1);
+    }
+  }
+  const pk_cnn_conv* pr = exp.data();
+  const int n = (int)exp.size();
   for (int i0 = 0; i0 < n; i0 += cg::kMaxProblems) {
     cg::Launch L;
     memset(&L, 0, sizeof(L));
@@ -363,6 +391,7 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
     for (int j = 0; j < L.nprob; ++j) {
       const pk_cnn_conv& g = pr[i0 + j];
       cg::Problem& p = L.p[j];
+      p.par = cls[i0 + j];
       if (g.c % 8 || g.k % 8 || (g.stride != 1 && g.stride != 2))
         return fail(PK_ERR_ARG, "conv: c, k multiples of 8; stride 1 or 2");
       p.R = g.r; p.S = g.s; p.stride = g.stride; p.pad = g.pad;
@@ -394,6 +423,37 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
         p.OH = g.p; p.OW = g.q; p.dld = g.ldo;
         if (!make_map_2d(&L.tm[j], g.wt, g.k, kpad, kpad, ntile, p.a_mode == 3 ? 16 : 64))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (FPROP weights)");
+        p.splits = 1;
+      } else if (kind == PK_CNN_CONV_DGRAD && p.par >= 0) {
+        const int kpadt = rup(g.r * g.s * g.k, 64);
+        const int a = p.par >> 1, b = p.par & 1;
+        p.ntap = 0;
+        for (int r = 0; r < g.r; ++r)
+          for (int q = 0; q < g.s; ++q)
+            if (((a + g.pad - r) & 1) == 0 && ((b + g.pad - q) & 1) == 0) {
+              p.tapk[p.ntap] = r * g.s + q;
+              p.tdr[p.ntap] = (a + g.pad - r) / 2;
+              p.tds[p.ntap] = (b + g.pad - q) / 2;
+              ++p.ntap;
+            }
+        if (g.r == 1) {  // 1x1: class (0, 0) is a plain GEMM over dY rows, the rest K = 0
+          p.a_mode = 1;
+          if (!make_map_2d(&L.tmA[j], g.src, (uint64_t)g.n * g.p * g.q, g.k, g.ldy, cg::BM))
+            return fail(PK_ERR_CUDA, "conv: DGRAD parity activation map");
+        } else {  // 3x3: dY windows (i + {0,1}, j + {0,1}), zero fill past the plane
+          p.a_mode = 5;
+          if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.p, g.q, g.k, g.ldy, 0, 0, 0, 0, 1,
+                               cg::BM))
+            return fail(PK_ERR_CUDA, "conv: DGRAD parity im2col map");
+        }
+        p.src = static_cast<const __nv_bfloat16*>(g.src);
+        p.accumulate = g.accumulate;
+        p.M = g.n * g.p * g.q; p.N = g.c; p.K = p.ntap * g.k;
+        p.SH = g.p; p.SW = g.q; p.SC = g.k; p.sld = g.ldy;
+        p.OH = g.p; p.OW = g.q; p.dld = g.ldo;
+        p.DH = g.h; p.DW = g.w;
+        if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile))
+          return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (DGRAD weights)");
         p.splits = 1;
       } else if (kind == PK_CNN_CONV_DGRAD) {
         const int kpadt = rup(g.r * g.s * g.k, 64);
@@ -556,7 +616,7 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr, int n, int ntile, int stag
       // (short-K GEMMs — 1x1 convs with K < 512 — are epilogue-bound: no gain, measured)
       for (int j = 0; j < L.nprob && pair; ++j)
         pair = (L.p[j].a_mode == 1 || L.p[j].a_mode == 2) && L.p[j].splits == 1 &&
-               L.p[j].K >= 512;
+               L.p[j].K >= 512 && L.p[j].par < 0;
       if (pair) {
         int pairs = 0;
         for (int j = 0; j < L.nprob; ++j) {
@@ -1039,6 +1099,7 @@ extern "C" int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void
   static cg::Launch L;
   memset(&L, 0, sizeof(L));
   L.nprob = 1;
+  L.p[0].par = -1;
   L.ntile = ntile;
   L.stages = stages;
   cg::Problem& p = L.p[0];

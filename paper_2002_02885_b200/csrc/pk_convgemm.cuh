@@ -50,6 +50,12 @@ struct Problem {
                               //   output-pixel index space (0 = plain m = (n, y, x) rows)
   int tpi;                    // halo: M tiles per image
   int hrows;                  // halo: input rows per halo buffer
+  int par;                    // stride-2 DGRAD parity class a·2 + b of the dX pixels
+                              //   (2i + a, 2j + b) this problem computes, -1 = none; the
+                              //   GEMM's pixel space is the (i, j) sub-grid OH x OW
+  int DH, DW;                 // parity: dX plane dims
+  int ntap;                   // parity (a_mode 5): the class's taps: global tap index r·S + s
+  int tapk[4], tdr[4], tds[4];//   and the dY offsets (dr, ds) of (i, j) it reads
   int brow0;                  // FPROP/DGRAD: first row of this problem's B in its map
   int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
   int OH, OW;                 // spatial dims of the GEMM's pixel space
@@ -152,6 +158,15 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
   }
   umma::mbar_arrive_expect_tx(bar, (uint32_t)NT * 128u + (tma_all ? 16384u : 0u));
   const int m0 = tm * BM;
+  if (P.a_mode == 5) {  // stride-2 DGRAD parity class: tap t of the class, dY at (i+dr, j+ds)
+    const int img = m0 / ohw, rem = m0 - img * ohw;
+    const int py = rem / P.OW, px = rem - py * P.OW;
+    const int t = kk / P.SC, c0 = kk - t * P.SC;
+    tc::tma_im2col_4d(stage, &L.tmA[pi], c0, px, py, img, (uint16_t)P.tds[t], (uint16_t)P.tdr[t],
+                      bar);
+    tc::tma_load_2d(stage + 16384, &L.tm[pi], P.tapk[t] * P.SC + c0, P.brow0 + tn * NT, bar);
+    return;
+  }
   if (P.a_mode == 3) {  // four taps of a 16-channel input: A and B in 16-deep SW32 slabs
     const int img = m0 / ohw, rem = m0 - img * ohw;
     const int py = rem / P.OW, px = rem - py * P.OW;
@@ -250,15 +265,22 @@ __device__ __forceinline__ void epilogue(const Problem& P, uint32_t tmem, int wa
                                          int tm, int tn, int split, int nkb, int NT) {
   const int row = warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  int m = tm * BM + row;
+  int m = tm * BM + row;     // the output row written (dst row index)
+  bool mvalid = m < P.M;
+  if (P.par >= 0) {  // stride-2 DGRAD parity class: (n, i, j) → dX pixel (2i + a, 2j + b)
+    const int ohw = P.OH * P.OW, n = m / ohw, rem = m - n * ohw;
+    const int i = rem / P.OW, j = rem - i * P.OW;
+    m = (n * P.DH + 2 * i + (P.par >> 1)) * P.DW + 2 * j + (P.par & 1);
+  }
   if (P.pw) {  // halo tiles: rows index the padded (W + 2)-wide pixels of one image
     const int img = tm / P.tpi, o = (tm - img * P.tpi) * BM + row;
     const int y = o / P.pw, x = o - y * P.pw;
-    m = (y < P.OH && x < P.OW) ? (img * P.OH + y) * P.OW + x : P.M;  // junk → skipped
+    mvalid = y < P.OH && x < P.OW;  // junk columns / rows past the image are dropped
+    m = mvalid ? (img * P.OH + y) * P.OW + x : 0;
   }
   // one 16-column chunk of the accumulator row → global
   auto chunk = [&](int c0, float (&v)[16]) {    const int n0 = tn * NT + c0;
-    if (m >= P.M || n0 >= P.N) return;
+    if (!mvalid || n0 >= P.N) return;
     if (MODE == FPROP && (P.bias || P.act)) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
