@@ -61,7 +61,8 @@ bool make_map_im2col(CUtensorMap* m, const void* base, int n, int h, int w, int 
   if (g_encode_i2c(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                    lower, upper, (cuuint32_t)chans, (cuuint32_t)pixels, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   chans == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   chans == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                               : (chans == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
@@ -84,7 +85,9 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
   cuuint32_t es[2] = {1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : (box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                   : CU_TENSOR_MAP_SWIZZLE_128B),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -467,13 +470,21 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr0, int n0, int ntile, int st
                                g.pad - (g.r - 1), g.pad - (g.s - 1) + g.w - g.q,
                                g.pad - (g.r - 1) + g.h - g.p, 1, cg::BM))
             return fail(PK_ERR_CUDA, "conv: DGRAD im2col map");
+        } else if (g.stride == 1 && g.k == 32 && g.ldy % 8 == 0) {
+          // 32-channel dY (DenseNet growth convs): two taps per 64-deep k-block, each
+          // a 128-pixel x 32-channel SW64 im2col box (cg::Problem a_mode 6)
+          p.a_mode = 6;
+          if (!make_map_im2col(&L.tmA[j], g.src, g.n, g.p, g.q, 32, g.ldy, g.pad - (g.s - 1),
+                               g.pad - (g.r - 1), g.pad - (g.s - 1) + g.w - g.q,
+                               g.pad - (g.r - 1) + g.h - g.p, 1, cg::BM, 32))
+            return fail(PK_ERR_CUDA, "conv: DGRAD 32-channel im2col map");
         }
         p.src = static_cast<const __nv_bfloat16*>(g.src);
         p.accumulate = g.accumulate;
         p.M = g.n * g.h * g.w; p.N = g.c; p.K = g.r * g.s * g.k;
         p.SH = g.p; p.SW = g.q; p.SC = g.k; p.sld = g.ldy;
         p.OH = g.h; p.OW = g.w; p.dld = g.ldo;
-        if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile))
+        if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile, p.a_mode == 6 ? 32 : 64))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (DGRAD weights)");
         p.splits = 1;
       } else {

@@ -158,6 +158,21 @@ __device__ __forceinline__ void tma_kblock(const Launch& L, int pi, int tm, int 
   }
   umma::mbar_arrive_expect_tx(bar, (uint32_t)NT * 128u + (tma_all ? 16384u : 0u));
   const int m0 = tm * BM;
+  if (P.a_mode == 6) {  // 32-channel plane: taps 2kb, 2kb+1, one SW64 slab each (DGRAD)
+    const int img = m0 / ohw, rem = m0 - img * ohw;
+    const int py = rem / P.OW, px = rem - py * P.OW;
+    const int kb = kk / BK, ntaps = P.R * P.S;
+    for (int u = 0; u < 2; ++u) {
+      const int tb = 2 * kb + u;           // B: past the last tap these are zero columns
+      const int tap = min(tb, ntaps - 1);  // A: a real (finite) tap that meets zero B rows
+      const int fr = tap / P.S, fs = tap - fr * P.S;
+      tc::tma_im2col_4d(stage + u * 8192, &L.tmA[pi], 0, px + P.pad - (P.S - 1),
+                        py + P.pad - (P.R - 1), img, (uint16_t)(P.S - 1 - fs),
+                        (uint16_t)(P.R - 1 - fr), bar);
+      tc::tma_load_2d(stage + 16384 + u * NT * 64, &L.tm[pi], tb * 32, P.brow0 + tn * NT, bar);
+    }
+    return;
+  }
   if (P.a_mode == 5) {  // stride-2 DGRAD parity class: tap t of the class, dY at (i+dr, j+ds)
     const int img = m0 / ohw, rem = m0 - img * ohw;
     const int py = rem / P.OW, px = rem - py * P.OW;
@@ -218,6 +233,19 @@ __device__ __forceinline__ void mma_kblock(uint32_t tmem_d, uint32_t a_s, uint32
                  : tc::sdesc_sw128(b_s + ks * 32, 16, 1024);
     }
     tc::mma_bf16(tmem_d, ad, bd, idesc, (!first || ks) ? 1u : 0u);
+  }
+}
+
+// 4 UMMA K-steps of a 32-channel (a_mode 6) stage: two SW64 slabs of 32 K each
+__device__ __forceinline__ void mma_kblock_sw64(uint32_t tmem_d, uint32_t a_s, uint32_t idesc,
+                                                bool first, int NT) {
+  const uint32_t b_s = a_s + 16384;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const uint32_t u = ks >> 1, h = (ks & 1) * 32;
+    tc::mma_bf16(tmem_d, tc::sdesc_sw64(a_s + u * 8192 + h, 16, 512),
+                 tc::sdesc_sw64(b_s + u * NT * 64 + h, 16, 512), idesc,
+                 (!first || ks) ? 1u : 0u);
   }
 }
 
@@ -570,7 +598,10 @@ k_conv_gemm(const __grid_constant__ Launch L) {
         umma::fence_after();
         bool fa, fb;
         sw32_flags(P, MODE == WGRAD, fa, fb);
-        mma_kblock<MODE>(tmem, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
+        if (MODE != WGRAD && P.a_mode == 6)
+          mma_kblock_sw64(tmem, sbase + s * SB, idesc, kb == 0, NT);
+        else
+          mma_kblock<MODE>(tmem, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
         umma::commit(&empty[s]);
       }
       umma::commit(done);
@@ -667,7 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_consta
           umma::fence_after();
           bool fa, fb;
           sw32_flags(L.p[ti.pi], wg, fa, fb);
-          mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
+          if (!wg && L.p[ti.pi].a_mode == 6)
+            mma_kblock_sw64(acc, sbase + s * SB, idesc, kb == 0, NT);
+          else
+            mma_kblock<MODE>(acc, sbase + s * SB, idesc, kb == 0, fa, fb, NT);
           umma::commit(&empty[s]);
         }
         umma::commit(&tfull[buf]);

@@ -55,6 +55,19 @@ __device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo_byte
   return d;
 }
 
+// SWIZZLE_64B (layout_type 4), K-major: 64-byte rows (32 bf16 of K), 8-row atoms of
+// 512 B (SBO); an MMA K-step (16) advances the start by 32 B inside the row
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo_bytes,
+                                               uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+
 // instruction descriptor: kind::f16 with bf16 A/B, fp32 accumulate, dense
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4)                     // c_format = F32
