@@ -508,6 +508,11 @@ class DeviceConvDataset:
         self.max_label = int(np.max(ds.labels)) if n else -1
 
 
+# conv / depthwise WGRAD and split sums on an async lane of the step program
+# (single-architecture packs): they overlap the data-gradient chain and join before
+# the commit
+ASYNC_WGRAD = True
+
 # depthwise WGRAD fast path: channel-pixels per partial block (the planner's
 # trade-off between per-thread serial latency and partial-record traffic)
 DW_CHANNEL_PIXELS_PER_BLOCK = 4096
@@ -1365,7 +1370,12 @@ class ConvPack:
         lanes = self._lanes(act)
         if len(lanes) == 1:
             ops += self._group([fwd[k] for k in act])
-            ops += self._group([bwd[k] for k in act])
+            # weight gradients (and their split sums) only feed the optimizer: an async
+            # lane (pk_cnn_op.lane 16 + 1) runs them beside the data-gradient chain
+            for op in self._group([bwd[k] for k in act]):
+                async_ok = op[0] in (CNN["CONV_WGRAD"], CNN["SPLIT_REDUCE"],
+                                     CNN["DW_WGRAD"]) and ASYNC_WGRAD
+                ops.append(op + (17,) if async_ok else op)
         else:
             # heterogeneous pack: one lane (stream) per architecture, so the
             # different nets' launches overlap; the shared-input first layer's

@@ -346,6 +346,10 @@ struct pk_cnn_prog {
   std::vector<OpRec> ops;
   cudaStream_t lane_st[kMaxLanes + 1] = {};  // side streams of lanes 1..kMaxLanes
   cudaEvent_t fork_ev = nullptr, join_ev[kMaxLanes + 1] = {};
+  // async lanes (op lane 16 + a): ops that only feed the end of the step (weight
+  // gradients) run on these, each forking from the program stream where it sits
+  cudaStream_t async_st[kMaxLanes + 1] = {};
+  cudaEvent_t async_fork[kMaxLanes + 1] = {}, async_join[kMaxLanes + 1] = {};
   uint8_t* dmem = nullptr;
   int launches = 0;
   cudaGraphExec_t gexec = nullptr;
@@ -856,12 +860,45 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
 // PDL chains each lane's launches; the first launch after a fork or a join
 // carries no PDL attribute (its predecessor is an event, not a kernel).
 int run_all(pk_cnn_prog* g, cudaStream_t st) {
-  bool pdl[kMaxLanes + 1] = {}, open[kMaxLanes + 1] = {};
-  bool any_open = false, forked = false;
+  bool pdl[kMaxLanes + 1] = {}, open[kMaxLanes + 1] = {}, aopen[kMaxLanes + 1] = {};
+  bool any_open = false, forked = false, any_async = false;
+  // async lanes join the program stream before the commit / optimizer ops (and at the end)
+  auto join_async = [&]() -> cudaError_t {
+    cudaError_t e = cudaSuccess;
+    for (int a = 1; a <= kMaxLanes && e == cudaSuccess; ++a)
+      if (aopen[a]) {
+        e = cudaEventRecord(g->async_join[a], g->async_st[a]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->async_join[a], 0);
+        aopen[a] = false;
+      }
+    any_async = false;
+    pdl[0] = false;
+    return e;
+  };
   for (size_t i = 0; i < g->ops.size(); ++i) {
     const int L = g->ops[i].lane;
     cudaError_t e = cudaSuccess;
-    if (L == 0 && any_open) {  // join every lane opened since the last lane-0 op
+    if (L >= 16) {  // async op: waits for everything the program stream has issued so far
+      const int a = L - 16;
+      if (!g->async_st[a]) {
+        e = cudaStreamCreateWithFlags(&g->async_st[a], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->async_fork[a], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->async_join[a], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(g->async_fork[a], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(g->async_st[a], g->async_fork[a], 0);
+      if (e == cudaSuccess) {
+        t_pdl = false;
+        e = run_op(g, g->ops[i], g->async_st[a]);
+      }
+      aopen[a] = any_async = true;
+      if (e != cudaSuccess)
+        return fail(PK_ERR_CUDA, "op " + std::to_string(i) + " (async): " + cudaGetErrorString(e));
+      continue;
+    }
+    if (any_async && (g->ops[i].kind == PK_CNN_COMMIT || g->ops[i].kind == PK_CNN_OPT))
+      e = join_async();
+    if (e == cudaSuccess && L == 0 && any_open) {  // join every lane opened since the last lane-0 op
       for (int l = 1; l <= kMaxLanes && e == cudaSuccess; ++l)
         if (open[l]) {
           e = cudaEventRecord(g->join_ev[l], g->lane_st[l]);
@@ -902,6 +939,10 @@ int run_all(pk_cnn_prog* g, cudaStream_t st) {
         if (e != cudaSuccess) return fail(PK_ERR_CUDA, cudaGetErrorString(e));
       }
   }
+  if (any_async) {
+    cudaError_t e = join_async();
+    if (e != cudaSuccess) return fail(PK_ERR_CUDA, cudaGetErrorString(e));
+  }
   return PK_OK;
 }
 
@@ -924,7 +965,7 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
     r.kind = op.kind;
     r.nprob = op.nprob;
     r.lane = op.lane;
-    if (op.lane < 0 || op.lane > kMaxLanes) {
+    if (op.lane < 0 || (op.lane > kMaxLanes && (op.lane < 17 || op.lane > 16 + kMaxLanes))) {
       delete g;
       return fail(PK_ERR_ARG, "op " + std::to_string(i) + ": lane out of range");
     }
@@ -1039,6 +1080,9 @@ extern "C" void pk_cnn_prog_destroy(pk_cnn_prog* g) {
   for (int l = 1; l <= kMaxLanes; ++l) {
     if (g->lane_st[l]) cudaStreamDestroy(g->lane_st[l]);
     if (g->join_ev[l]) cudaEventDestroy(g->join_ev[l]);
+    if (g->async_st[l]) cudaStreamDestroy(g->async_st[l]);
+    if (g->async_fork[l]) cudaEventDestroy(g->async_fork[l]);
+    if (g->async_join[l]) cudaEventDestroy(g->async_join[l]);
   }
   if (g->fork_ev) cudaEventDestroy(g->fork_ev);
   if (g->dmem) cudaFree(g->dmem);

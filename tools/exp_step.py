@@ -24,6 +24,8 @@ if "rpt" in knobs:
     orig = cnn.rows_per_block
     cnn.rows_per_block = lambda rows, c=8, per_thread=4: orig(rows, c, rpt)
 
+if "async" in knobs:  # conv WGRAD on an async lane (1) or in the chain (0)
+    cnn.ASYNC_WGRAD = bool(int(knobs["async"]))
 if "dwcp" in knobs:  # depthwise WGRAD channel-pixels per block
     cnn.DW_CHANNEL_PIXELS_PER_BLOCK = int(knobs["dwcp"])
 if "nt" in knobs:  # N tile rule: "wide" prefers 256-wide tiles for N >= 256
