@@ -507,8 +507,9 @@ typedef struct pk_cnn_op {
                              forks from lane 0 after the last lane-0 op before it and
                              joins lane 0 before the next lane-0 op, so different lanes'
                              launches overlap on the GPU.  16 + a (a = 1..8): async lane
-                             a — the op waits for everything the program stream issued
-                             before it and lane 0 joins it only before the next COMMIT /
+                             a — the op waits for everything its parent stream (lane a
+                             while that lane is open, else the program stream) issued
+                             before it, and lane 0 joins it only before the next COMMIT /
                              OPT op (weight gradients overlap the rest of the backward) */
   int32_t pad0;
   const void* probs;      /* nprob structs of the kind's type (host, copied) */

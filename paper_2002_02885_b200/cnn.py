@@ -1391,9 +1391,12 @@ class ConvPack:
                     bwd[k] = bwd[k][:cut]
             ops += self._group(pre)
             for li, lane in enumerate(lanes, 1):
-                for op in (self._group([fwd[k] for k in lane])
-                           + self._group([bwd[k] for k in lane])):
+                for op in self._group([fwd[k] for k in lane]):
                     ops.append(op + (li,))
+                for op in self._group([bwd[k] for k in lane]):
+                    async_ok = op[0] in (CNN["CONV_WGRAD"], CNN["SPLIT_REDUCE"],
+                                         CNN["DW_WGRAD"]) and ASYNC_WGRAD
+                    ops.append(op + ((16 + li) if async_ok else li,))
             ops += self._group(post)
         if with_update:
             cm = []

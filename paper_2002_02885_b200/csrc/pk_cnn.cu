@@ -885,7 +885,10 @@ int run_all(pk_cnn_prog* g, cudaStream_t st) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->async_fork[a], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->async_join[a], cudaEventDisableTiming);
       }
-      if (e == cudaSuccess) e = cudaEventRecord(g->async_fork[a], st);
+      // parent: the sync lane a while it is open (heterogeneous packs), else the program
+      // stream
+      cudaStream_t parent = open[a] ? g->lane_st[a] : st;
+      if (e == cudaSuccess) e = cudaEventRecord(g->async_fork[a], parent);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(g->async_st[a], g->async_fork[a], 0);
       if (e == cudaSuccess) {
         t_pdl = false;
