@@ -329,6 +329,75 @@ def conv_packed_step(packed: ConvPackedModel, datasets, preprocess_spec=None, ca
     return losses
 
 
+def conv_packed_run(packed: ConvPackedModel, datasets, max_steps, depth=3):
+    """Up to `max_steps` packed steps (fewer when no member is active any more),
+    pipelined: the host plans and launches step i+1 while the device runs step i;
+    every step's losses and commit verdicts come back through a pinned ring (one
+    async D2H copy per step) instead of a synchronous read.  Cursors advance as
+    packed_step advances them, assuming each step commits; a step that did not
+    (non-finite value or gradient, engine.py:297-299) is found when its verdicts
+    arrive — at most `depth` steps later — and NonFiniteGradient is raised then
+    (the reference raises at that step; steps already in flight are not rolled
+    back, so the pack's state is unspecified after the exception).  Returns the
+    per-step {model_id: loss} dicts.  Used by B200ConvExecutor.evaluate."""
+    import collections
+    import torch
+    from .engine import NonFiniteGradient
+    from .packing import ReplanNeeded, _active_members
+    cp = packed.device_pack()
+    K = len(packed.members)
+    depth = max(1, int(depth))
+    ring = torch.empty((depth, K, 4), dtype=torch.int32, pin_memory=True)
+    evs = [torch.cuda.Event() for _ in range(depth)]
+    index = {id(h): k for k, h in enumerate(packed.members)}
+    fly = collections.deque()
+    out = []
+
+    def drain():
+        slot, active, plan = fly.popleft()
+        evs[slot].synchronize()
+        st = ring[slot].numpy()
+        losses = {}
+        for h in active:
+            k = index[id(h)]
+            if int(st[k, 2]) & 1:
+                raise NonFiniteGradient(f"{h.model_id}/step {h.cursor.steps_done}")
+            losses[h.model_id] = float(np.array([st[k, 3]], dtype=np.int32)
+                                       .view(np.float32)[0])
+        out.append(losses)
+
+    caller = torch.cuda.current_stream(cp.dev)
+    cp.stream.wait_stream(caller)
+    with torch.cuda.stream(cp.stream):
+        for i in range(int(max_steps)):
+            try:
+                active = _active_members(packed, datasets, False)
+            except ReplanNeeded:
+                break
+            plan = _plan(packed, active, datasets, cp)
+            cp.program(plan.takes, plan.leads, plan.data).run(cp.stream.cuda_stream)
+            if len(fly) == depth:
+                drain()
+            slot = i % depth
+            ring[slot].copy_(cp.state, non_blocking=True)
+            evs[slot].record(cp.stream)
+            for h in active:  # the bookkeeping of a committed step (packing.py:255-257)
+                k = index[id(h)]
+                h._committed()
+                c = h.cursor
+                c.steps_done += 1
+                c.pos += plan.takes[k]
+                np.add.at(c.samples_used, plan.rows[k], 1)
+            fly.append((slot, active, plan))
+            packed.last_step_stats = {
+                "physical_inputs": plan.n_groups if packed.share_inputs else len(active),
+                "groups": plan.n_groups, "driver_batch": plan.driver}
+        while fly:
+            drain()
+    caller.wait_stream(cp.stream)
+    return out
+
+
 def conv_standalone_step(handle: ConvModelHandle, datasets, preprocess_spec=None, cache=None):
     """packing.py:267-282: the same kernels on a one-member pack."""
     from .packing import PackError, _roll_if_needed

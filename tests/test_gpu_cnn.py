@@ -221,3 +221,25 @@ def test_conv_hyperband_packed_matches_unpacked():
     for x in res["knn"].records:
         sizes[(x.bracket, x.rung, x.group)] = sizes.get((x.bracket, x.rung, x.group), 0) + 1
     assert max(sizes.values()) >= 2  # knn really packed members
+
+
+def test_pipelined_run_matches_step_loop():
+    """convpack.conv_packed_run (host planning overlapped with the device, verdicts
+    through a pinned ring) == the same number of packed_step calls, bit for bit:
+    losses per step, parameters, cursors and samples_used."""
+    from paper_2002_02885_b200 import convpack
+    arch = _arch("lenet5")
+    ds = _ds(n=200)
+    a = _handles(arch, 3, 32, target=9)
+    b = _handles(arch, 3, 32, target=9)
+    pa = packing.dedup_inputs(packing.pack_models(a))
+    la = [packing.packed_step(pa, {"train": ds}) for _ in range(9)]
+    pb = packing.dedup_inputs(packing.pack_models(b))
+    lb = convpack.conv_packed_run(pb, {"train": ds}, 50, depth=3)
+    assert lb == la and all(h.finished for h in b)
+    for x, y in zip(a, b):
+        for n in x.params:
+            assert np.array_equal(x.params[n], y.params[n]), n
+        assert x.cursor.steps_done == y.cursor.steps_done and x.cursor.pos == y.cursor.pos
+        assert np.array_equal(x.cursor.samples_used, y.cursor.samples_used)
+        assert x.optimizer.step_counter == y.optimizer.step_counter
