@@ -515,7 +515,7 @@ ASYNC_WGRAD = True
 
 # depthwise WGRAD fast path: channel-pixels per partial block (the planner's
 # trade-off between per-thread serial latency and partial-record traffic)
-DW_CHANNEL_PIXELS_PER_BLOCK = 4096
+DW_CHANNEL_PIXELS_PER_BLOCK = 8192
 
 
 def _cgp(c):
@@ -1044,12 +1044,14 @@ class ConvPack:
                                                ty.h, ty.w)
         d.ldx, d.ldy = self._ld(k, op.x), self._ld(k, op.y)
         if d.r == 3 and d.s == 3 and d.stride in (1, 2) and tx.c <= 512:
-            # 3x3 fast path (csrc/pk_cnn_ops.cuh dw_fast_wgrad): ~16 K channel-pixels
-            # per block (<= 256 blocks), a multiple of the block's pixel lanes
-            lanes = (256 // _cgp(tx.c)) // 3
+            # 3x3 fast path (csrc/pk_cnn_ops.cuh dw_fast_wgrad): blocks own a chunk of
+            # <= 64 channels x one of <= 16 pixel splits (~DW_CHANNEL_PIXELS_PER_BLOCK
+            # channel-pixels each), a multiple of the block's pixel lanes
+            cgb = min(_cgp(tx.c), 8)
+            lanes = (256 // cgb) // 3
             pix = take * ty.h * ty.w
-            nblk = min(256, max(1, cdiv(pix * tx.c, DW_CHANNEL_PIXELS_PER_BLOCK)))
-            d.ppb = rup(cdiv(pix, nblk), lanes)
+            nsplit = min(16, max(1, cdiv(pix * 8 * cgb, DW_CHANNEL_PIXELS_PER_BLOCK)))
+            d.ppb = rup(cdiv(pix, nsplit), lanes)
         else:
             d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
         return d

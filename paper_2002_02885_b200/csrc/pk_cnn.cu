@@ -199,7 +199,8 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
-      return cdiv((long long)P.n * P.p * P.q, P.ppb);
+      const int splits = cdiv((long long)P.n * P.p * P.q, P.ppb);
+      return cnn::dw_fast(P, kind) ? splits * cnn::dw_wgrad_chunks(P.c) : splits;
     }
     case PK_CNN_MAXPOOL_FWD: {
       const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
@@ -260,11 +261,15 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
-      if (kind == PK_CNN_DW_WGRAD &&
-          (P.ppb < 1 || prob_blocks(kind, pr) > cnn::kRedMaxBlocks ||
-           (cnn::dw_fast(P, kind) && P.ppb % cnn::dw_wgrad_lanes(cgp_of(P.c)))))
-        return "dw: units/pixels per block >= 1 (3x3: a multiple of the unit lanes), <= 256 "
-               "blocks";
+      if (kind == PK_CNN_DW_WGRAD && P.ppb < 1) return "dw: pixels per block >= 1";
+      if (kind == PK_CNN_DW_WGRAD && cnn::dw_fast(P, kind) &&
+          (P.ppb % cnn::dw_wgrad_lanes(P.c) ||
+           cdiv((long long)P.n * P.p * P.q, P.ppb) > cnn::kDwMaxSplits))
+        return "dw: 3x3 WGRAD pixels per block must be a multiple of the pixel lanes, <= 16 "
+               "splits";
+      if (kind == PK_CNN_DW_WGRAD && !cnn::dw_fast(P, kind) &&
+          prob_blocks(kind, pr) > cnn::kRedMaxBlocks)
+        return "dw: <= 256 pixel blocks";
       break;
     }
     case PK_CNN_MAXPOOL_FWD:

@@ -735,18 +735,33 @@ __device__ __forceinline__ void dw_wgrad_generic(const pk_cnn_dw& P, int blk, in
 //   FPROP / DGRAD: one thread per (pixel, channel group) of the output plane, all
 //     nine source vectors and nine weight vectors loaded before any FMA, 32-bit
 //     index math (the generic path below walks taps with data-dependent skips).
-//   WGRAD: thread = (channel group j, kernel row r, pixel lane); a block owns
-//     ppb output pixels (planner: enough blocks to spread the member, few enough
-//     that the [9][c] block records stay small next to the inputs), a lane every
-//     lanes-th of them, kU pixels' loads (dy + the row's three x vectors) issued
-//     before their FMAs.  24 accumulators per thread.  Needs cgp <= 64 (c <= 512).
+//   WGRAD: a block owns one CHUNK of <= 8 channel groups (64 channels) and one
+//     split of the member's output pixels; thread = (channel group j, kernel
+//     row r, pixel lane), kU pixels' loads (dy + the row's three x vectors)
+//     issued before their FMAs, 24 accumulators per thread.  The block's
+//     [9][64] record is summed over its lanes in lane order; a member's
+//     <= 16 splits of a chunk are folded in split order (fp64) by the chunk's
+//     last block (one ticket), whose loads are all issued before the adds.
+//     Small records and one short fold instead of [9][c] records per block
+//     and a two-level tree (a 1x1x480 layer: 44 -> a few us).  c <= 512.
 // ------------------------------------------------------------------------------
 __host__ __device__ __forceinline__ bool dw_fast(const pk_cnn_dw& P, int mode) {
   if (P.r != 3 || P.s != 3 || (P.stride != 1 && P.stride != 2)) return false;
   return mode != PK_CNN_DW_WGRAD || P.c <= 512;
 }
-// WGRAD pixel lanes of a 256-thread block: (256 / cgp) / 3 kernel-row triples
-__host__ __device__ __forceinline__ int dw_wgrad_lanes(int cgp) { return (256 / cgp) / 3; }
+// WGRAD channel groups per block (a chunk), chunks per member, pixel lanes of
+// a 256-thread block ((256 / groups) / 3 kernel-row triples), splits per chunk
+constexpr int kDwChunkGroups = 8, kDwMaxSplits = 16;
+__host__ __device__ __forceinline__ int dw_wgrad_cgb(int c) {
+  int g = 1;
+  while (g < (c >> 3)) g <<= 1;
+  return g < kDwChunkGroups ? g : kDwChunkGroups;
+}
+__host__ __device__ __forceinline__ int dw_wgrad_chunks(int c) {
+  const int b = dw_wgrad_cgb(c);
+  return ((c >> 3) + b - 1) / b;
+}
+__host__ __device__ __forceinline__ int dw_wgrad_lanes(int c) { return (256 / dw_wgrad_cgb(c)) / 3; }
 
 template <int MODE, int ST>
 __device__ __forceinline__ void dw_items3(const pk_cnn_dw& P, int blk) {
@@ -796,13 +811,15 @@ __device__ __forceinline__ void dw_items3(const pk_cnn_dw& P, int blk) {
   *reinterpret_cast<uint4*>(bptr(P.y, m, old, ch)) = pack8(acc);
 }
 
-__device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk, int nblk) {
-  int cgp = 1;
-  while (cgp < (P.c >> 3)) cgp <<= 1;
-  const int t = threadIdx.x, j = t & (cgp - 1), rest = t / cgp;
-  const int lanes = dw_wgrad_lanes(cgp);
-  const int r = rest % 3, rl = rest / 3, ch = 8 * j;
-  const bool on = j < (P.c >> 3) && rl < lanes;
+__device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk) {
+  const int cgb = dw_wgrad_cgb(P.c), CC = 8 * cgb, n9 = 9 * CC;
+  const int pq = P.p * P.q, M = P.n * pq;
+  const int nsplit = (M + P.ppb - 1) / P.ppb;
+  const int chunk = blk / nsplit, split = blk - chunk * nsplit;
+  const int t = threadIdx.x, j = t % cgb, rest = t / cgb;
+  const int lanes = dw_wgrad_lanes(P.c);
+  const int r = rest % 3, rl = rest / 3, ch = 8 * (chunk * cgb + j);
+  const bool on = ch < P.c && rl < lanes;
   float acc[3][8];
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -812,8 +829,7 @@ __device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk, int n
     const uint8_t* xb = static_cast<const uint8_t*>(P.x) + 2 * ch;
     const uint8_t* dyb = static_cast<const uint8_t*>(P.dy) + 2 * ch;
     const size_t xp = (size_t)P.ldx * 2, dp = (size_t)P.ldy * 2;
-    const int pq = P.p * P.q, M = P.n * pq;
-    const int m1 = min(M, (blk + 1) * P.ppb);
+    const int m1 = min(M, (split + 1) * P.ppb);
     // one pixel: dy vector + the three x vectors of kernel row r
     auto load = [&](int m, uint4& d, uint4 (&xv)[3]) {
       const int n = m / pq, rem = m - n * pq, oy = rem / P.q, ox = rem - oy * P.q;
@@ -837,7 +853,7 @@ __device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk, int n
         for (int e = 0; e < 8; ++e) acc[s][e] = fmaf(dv[e], a[e], acc[s][e]);
       }
     };
-    int m = blk * P.ppb + rl;
+    int m = split * P.ppb + rl;
     for (; m + (kU - 1) * lanes < m1; m += kU * lanes) {  // kU pixels' loads, then math
       uint4 d[kU], xv[kU][3];
 #pragma unroll
@@ -851,30 +867,58 @@ __device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk, int n
       fold(d, xv);
     }
   }
-  // block record [tap][c]: thread (j, r, rl) holds taps 3r .. 3r+2 of channels ch..
-  __shared__ __align__(16) float sh[6144];  // lanes * 9c <= (256 / cgp / 3) * 72 cgp
-  const int n9 = 9 * P.c;
-  if (on) {
+  // block record [tap][CC]: thread (j, r, rl) holds taps 3r .. 3r+2 of its 8 channels
+  __shared__ __align__(16) float sh[6144];  // lanes * 9 * CC <= (256 / cgb / 3) * 72 cgb
+  if (rl < lanes) {
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      float4* dst = reinterpret_cast<float4*>(sh + rl * n9 + (3 * r + s) * P.c + ch);
+      float4* dst = reinterpret_cast<float4*>(sh + rl * n9 + (3 * r + s) * CC + 8 * j);
       dst[0] = make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]);
       dst[1] = make_float4(acc[s][4], acc[s][5], acc[s][6], acc[s][7]);
     }
   }
   __syncthreads();
-  float* out = P.ws + (long long)blk * n9;
-  for (int o = threadIdx.x; o < n9; o += kBlock) {
+  const int c0 = chunk * CC;
+  auto out_index = [&](int o, int& di) {  // record slot -> dw[tap][c] (false: padding)
+    const int tap = o / CC, cc = o - tap * CC;
+    di = tap * P.c + c0 + cc;
+    return c0 + cc < P.c;
+  };
+  bool bad = false;
+  if (nsplit == 1) {  // the chunk's only block: its record is the gradient
+    for (int o = t; o < n9; o += kBlock) {
+      float a = 0.f;
+      for (int l = 0; l < lanes; ++l) a += sh[l * n9 + o];
+      int di;
+      if (out_index(o, di)) {
+        P.dw[di] = a;
+        bad |= !isfinite(a);
+      }
+    }
+    if (bad) *P.flag = 1;
+    return;
+  }
+  float* rec = P.ws + (long long)blk * n9;  // chunk-major, split order
+  for (int o = t; o < n9; o += kBlock) {
     float a = 0.f;
     for (int l = 0; l < lanes; ++l) a += sh[l * n9 + o];
-    out[o] = a;
+    rec[o] = a;
   }
-  double* tot;
-  if (!tree_reduce(P.ws, blk, nblk, n9, n9, P.counter, &tot)) return;
-  bool bad = false;
-  for (int i = threadIdx.x; i < n9; i += kBlock) {
-    P.dw[i] = (float)tot[i];
-    bad |= !isfinite(tot[i]);
+  if (!ticket(P.counter + chunk, nsplit)) return;
+  const float* r0 = P.ws + (long long)chunk * nsplit * n9;
+  for (int o = t; o < n9; o += kBlock) {
+    float v[kDwMaxSplits];
+#pragma unroll
+    for (int sp = 0; sp < kDwMaxSplits; ++sp) v[sp] = sp < nsplit ? __ldcg(r0 + (long long)sp * n9 + o) : 0.f;
+    double tot = 0.0;
+#pragma unroll
+    for (int sp = 0; sp < kDwMaxSplits; ++sp)
+      if (sp < nsplit) tot += v[sp];
+    int di;
+    if (out_index(o, di)) {
+      P.dw[di] = (float)tot;
+      bad |= !isfinite(tot);
+    }
   }
   if (bad) *P.flag = 1;
 }
@@ -908,7 +952,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dw_wgrad(const __grid_constant__ 
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_dw& P = G.p[pi];
   const int blk = blockIdx.x - G.blk0[pi], nblk = G.blk0[pi + 1] - G.blk0[pi];
-  if (dw_fast(P, PK_CNN_DW_WGRAD)) dw_fast_wgrad(P, blk, nblk);
+  if (dw_fast(P, PK_CNN_DW_WGRAD)) dw_fast_wgrad(P, blk);
   else dw_wgrad_generic(P, blk, nblk);
 }
 
