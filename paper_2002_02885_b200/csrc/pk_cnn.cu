@@ -194,8 +194,11 @@ int prob_blocks(int kind, const void* pr) {
     case PK_CNN_DW_FPROP:
     case PK_CNN_DW_DGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
-      return blocks_of(items((long long)P.n * (kind == PK_CNN_DW_FPROP ? P.p * P.q : P.h * P.w),
-                             P.c));
+      const int oh = kind == PK_CNN_DW_FPROP ? P.p : P.h, ow = kind == PK_CNN_DW_FPROP ? P.q : P.w;
+      if (cnn::dw_strip_ok(P))  // output strips of dw_strip_xs pixels
+        return blocks_of(items((long long)P.n * oh * cdiv(ow, cnn::dw_strip_xs(kind, P.stride)),
+                               P.c));
+      return blocks_of(items((long long)P.n * oh * ow, P.c));
     }
     case PK_CNN_DW_WGRAD: {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
