@@ -332,7 +332,8 @@ int pk_conv_gemm_test(int32_t mode, const pk_conv_geom* g, const void* x, const 
 #define PK_CNN_PUBLISH_T 18     /* transposed bf16 weights for DGRAD             */
 #define PK_CNN_COMMIT 19        /* per-member step counter / non-finite verdict  */
 #define PK_CNN_GATHER 20        /* batch rows src[idx[i]] -> dst[i] (e.g. over PCIe) */
-#define PK_CNN_NUM_KINDS 21
+#define PK_CNN_IM2COL 21        /* dense im2col rows of a narrow input (first conv)  */
+#define PK_CNN_NUM_KINDS 22
 
 #define PK_CNN_ACT_NONE 0
 #define PK_CNN_ACT_RELU 1
@@ -496,6 +497,18 @@ typedef struct pk_cnn_gather {
   int64_t row_bytes;
   int32_t rows, pad0;
 } pk_cnn_gather;
+
+/* Dense im2col of a narrow network input for the first conv: dst row m =
+ * (n, oy, ox) holds the r*s*c real input values of its window, (tap, channel)
+ * order, zero past the plane, zero-padded to ldo (a multiple of 8) columns.
+ * The first conv then runs as a 1x1 GEMM over these rows with K = ldo instead
+ * of r*s*cp (cp = the input's padded channel pitch, 16): a 7x7x3 stem reads
+ * 152 columns instead of 784. */
+typedef struct pk_cnn_im2col {
+  const void* src; /* bf16 [n][h][w][cp] */
+  void* dst;       /* bf16 [n*p*q][ldo]  */
+  int32_t n, h, w, cp, c, r, s, stride, pad, p, q, ldo;
+} pk_cnn_im2col;
 
 typedef struct pk_cnn_op {
   int32_t kind;           /* PK_CNN_* */

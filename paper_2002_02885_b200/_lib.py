@@ -145,7 +145,7 @@ class ConvGeom(C.Structure):
 CNN_KINDS = ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD", "BN_STATS", "BN_APPLY", "BN_BWD_REDUCE",
              "BN_BWD_APPLY", "DW_FPROP", "DW_DGRAD", "DW_WGRAD", "MAXPOOL_FWD", "MAXPOOL_BWD",
              "AVGPOOL_FWD", "AVGPOOL_BWD", "XENT", "BIAS_ACT_BWD", "SPLIT_REDUCE", "OPT",
-             "PUBLISH_T", "COMMIT", "GATHER")
+             "PUBLISH_T", "COMMIT", "GATHER", "IM2COL")
 CNN = {k: i for i, k in enumerate(CNN_KINDS)}
 CNN_ACT = {"none": 0, "relu": 1, "relu6": 2}
 _vp, _i32, _i64, _f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
@@ -217,6 +217,11 @@ class CnnGather(C.Structure):
                 ("pad0", _i32)]
 
 
+class CnnIm2col(C.Structure):
+    _fields_ = [("src", _vp), ("dst", _vp)] + _ints("n", "h", "w", "cp", "c", "r", "s", "stride",
+                                                    "pad", "p", "q", "ldo")
+
+
 class CnnOp(C.Structure):
     _fields_ = [("kind", _i32), ("nprob", _i32), ("cfg0", _i32), ("cfg1", _i32),
                 ("lane", _i32), ("pad0", _i32), ("probs", _vp)]
@@ -238,6 +243,7 @@ CNN_STRUCT[CNN["OPT"]] = CnnOptSeg
 CNN_STRUCT[CNN["PUBLISH_T"]] = CnnTpose
 CNN_STRUCT[CNN["COMMIT"]] = CnnCommit
 CNN_STRUCT[CNN["GATHER"]] = CnnGather
+CNN_STRUCT[CNN["IM2COL"]] = CnnIm2col
 
 
 class PKError(RuntimeError):

@@ -103,6 +103,7 @@ class PSpec:
     w16: bool = False
     dgrad: bool = False   # conv weight whose layer needs a data gradient (Wt16 copy)
     cin_p: int = 0        # conv weight: padded input channels of the device layout
+    im2col: int = 0       # first conv on a narrow input: dense (tap, channel) columns
 
     @property
     def numel(self):
@@ -176,9 +177,15 @@ class Net:
         name = self._layer()
         li = self.n - 1
         kpad = rup(r * s * tx.c, 64)
+        cols = 0
+        if x == "input" and DENSE_FIRST and tx.creal < tx.c:
+            # a narrow input's first conv runs as a 1x1 GEMM over dense im2col rows
+            # (IM2COL op): K = r·s·creal (rounded to 8) instead of r·s·cp
+            cols = rup(r * s * tx.creal, 8)
+            kpad = rup(cols, 64)
         W = PSpec(f"{name}/W", "convw", (k, r, s, tx.creal), (kp, kpad), li,
                   fan=(tx.creal * r * s, k * r * s), w16=True, dgrad=(x != "input"),
-                  cin_p=tx.c)
+                  cin_p=tx.c, im2col=cols)
         ps = [W]
         if bias:
             ps.append(PSpec(f"{name}/b", "bias", (k,), (kp,), li))
@@ -402,7 +409,10 @@ def to_dev_layout(p: PSpec, a: np.ndarray) -> np.ndarray:
     """Logical (host) array → padded device layout, float32."""
     out = np.zeros(p.dev_shape, dtype=np.float32)
     a = np.asarray(a, dtype=np.float64)
-    if p.kind == "convw":
+    if p.kind == "convw" and p.im2col:  # dense (tap, channel) columns
+        k, r, s, c = p.shape
+        out[:k, :r * s * c] = a.reshape(k, r * s * c)
+    elif p.kind == "convw":
         k, r, s, c = p.shape
         kp, kpad = p.dev_shape
         cp = p.cin_p
@@ -419,6 +429,9 @@ def to_dev_layout(p: PSpec, a: np.ndarray) -> np.ndarray:
 
 def from_dev_layout(p: PSpec, d: np.ndarray) -> np.ndarray:
     d = np.asarray(d, dtype=np.float32).reshape(p.dev_shape)
+    if p.kind == "convw" and p.im2col:
+        k, r, s, c = p.shape
+        return d[:k, :r * s * c].reshape(k, r, s, c).astype(np.float64)
     if p.kind == "convw":
         k, r, s, c = p.shape
         kp, kpad = p.dev_shape
@@ -460,6 +473,10 @@ def member_device_bytes(net: Net, optimizer: str, batch: int) -> int:
         if name == "input" or t.base is not None:
             continue
         act += batch * t.h * t.w * t.c * 2 * 2
+    op0 = net.ops[0]
+    if op0.kind == "conv" and net.param(op0.params[0]).im2col:  # IM2COL rows
+        t = net.tensors[op0.y]
+        act += batch * t.h * t.w * net.param(op0.params[0]).im2col * 2
     return int((4 * P * (2 + len(SLOTS[optimizer])) + mirrors + act) * 1.05)
 
 
@@ -512,6 +529,9 @@ class DeviceConvDataset:
 # (single-architecture packs): they overlap the data-gradient chain and join before
 # the commit
 ASYNC_WGRAD = True
+
+# a narrow input's first conv: dense im2col rows + a 1x1 GEMM (Net.conv, IM2COL op)
+DENSE_FIRST = True
 
 # depthwise WGRAD fast path: channel-pixels per partial block (the planner's
 # trade-off between per-thread serial latency and partial-record traffic)
@@ -771,7 +791,8 @@ class ConvPack:
                 self._first_grad[key] = z(len(ks), rows, t.c, dt=torch.bfloat16)
                 op0 = net.ops[0]
                 W0 = net.param(op0.params[0])
-                _, sp0 = _wgrad_cfg(t.c, op0.a["r"] * op0.a["s"] * net.tensors[op0.x].c, rows)
+                _, sp0 = _wgrad_cfg(t.c, W0.im2col or op0.a["r"] * op0.a["s"] *
+                                    net.tensors[op0.x].c, rows)
                 if sp0 > 1:
                     self._first_split[key] = z(len(ks), sp0 * W0.numel)
             A["val"][net.ops[0].y] = self._first_out[key][j]
@@ -799,7 +820,8 @@ class ConvPack:
             if op.kind == "conv":
                 ty = net.tensors[op.y]
                 W = net.param(op.params[0])
-                _, splits = _wgrad_cfg(ty.c, op.a["r"] * op.a["s"] * tx.c, b * ty.h * ty.w)
+                _, splits = _wgrad_cfg(ty.c, W.im2col or op.a["r"] * op.a["s"] * tx.c,
+                                       b * ty.h * ty.w)
                 if splits > 1:
                     fkey = ("first",) + shared[:2] if shared is not None and op is net.ops[0] \
                         else None
@@ -942,6 +964,8 @@ class ConvPack:
                 cs.k, cs.r, cs.s = ty.c, op.a["r"], op.a["s"]
                 cs.stride, cs.pad, cs.p, cs.q = op.a["stride"], op.a["pad"], ty.h, ty.w
                 cs.ldx = tx.c if first else self._ld(k, op.x)
+                if first:
+                    self._dense_geometry(cs, k, op, lead, take)
                 cs.ldo = self._ld(k, op.y)
                 cs.act = CNN_ACT[op.a["act"]]
                 cs.out_f32 = int(op.a["out_f32"])
@@ -995,6 +1019,62 @@ class ConvPack:
             st = self._z(self.members[lead].batch, h, w, data.cp, dt=self.torch.bfloat16)
             self.staging[lead] = st
         return st.data_ptr(), 0
+
+    def _cols_key(self, k, lead):
+        """(lead, r, s, stride, pad, columns) of member k's dense first conv, or None"""
+        op = self.members[k].net.ops[0]
+        if op.kind != "conv" or op.x != "input":
+            return None
+        W = self.members[k].net.param(op.params[0])
+        if not W.im2col:
+            return None
+        return (lead, op.a["r"], op.a["s"], op.a["stride"], op.a["pad"], W.im2col)
+
+    def _cols(self, key):
+        """the IM2COL rows buffer [batch·p·q][columns] of an input group's leader
+        and first-conv geometry"""
+        buf = self._cols_bufs.get(key) if hasattr(self, "_cols_bufs") else None
+        if buf is None:
+            if not hasattr(self, "_cols_bufs"):
+                self._cols_bufs = {}
+            lead, r, s, stv, pad, cols = key
+            net = self.members[lead].net
+            ty = net.tensors[net.ops[0].y]
+            buf = self._z(self.members[lead].batch * ty.h * ty.w, cols, dt=self.torch.bfloat16)
+            self._cols_bufs[key] = buf
+        return buf
+
+    def _dense_geometry(self, cs, k, op, lead, take):
+        """a dense first conv as a 1x1 GEMM over its IM2COL rows"""
+        key = self._cols_key(k, lead)
+        if key is None:
+            return
+        ty = self.members[k].net.tensors[op.y]
+        cs.src, cs.idx = self._cols(key).data_ptr(), 0
+        cs.n, cs.h, cs.w, cs.c = take, ty.h, ty.w, key[5]
+        cs.r = cs.s = cs.stride = 1
+        cs.pad = 0
+        cs.ldx = key[5]
+
+    def _im2col_op(self, pairs, data):
+        """one IM2COL launch filling the dense first-conv rows of every
+        (member, lead) pair's input group (after GATHER), or None"""
+        seen, ims = set(), []
+        for k, lead, take in pairs:
+            key = self._cols_key(k, lead)
+            if key is None or key in seen:
+                continue
+            seen.add(key)
+            _, r, s, stv, pad, cols = key
+            net = self.members[lead].net
+            tx, ty = net.tensors["input"], net.tensors[net.ops[0].y]
+            im = _lib.CnnIm2col()
+            im.src = self._input(lead, data)[0]
+            im.dst = self._cols(key).data_ptr()
+            im.n, im.h, im.w, im.cp, im.c = take, tx.h, tx.w, data.cp, tx.creal
+            im.r, im.s, im.stride, im.pad, im.p, im.q, im.ldo = r, s, stv, pad, ty.h, ty.w, cols
+            ims.append(im)
+        return (CNN["IM2COL"], None, ims) if ims else None
 
     def _bn_struct(self, k, op, rows):
         m = self.members[k]
@@ -1116,7 +1196,7 @@ class ConvPack:
                     steps.append((CNN["BIAS_ACT_BWD"], None, bs, None))
                 W = net.param(op.params[0])
                 pix = take * ty.h * ty.w
-                rsc = op.a["r"] * op.a["s"] * tx.c
+                rsc = W.im2col or op.a["r"] * op.a["s"] * tx.c
                 nt, splits = _wgrad_cfg(ty.c, rsc, pix)
                 bsplits = _wgrad_cfg(ty.c, rsc, m.batch * ty.h * ty.w)[1]
                 splits = min(splits, bsplits) if op.name in A["split"] else 1
@@ -1128,6 +1208,8 @@ class ConvPack:
                 cs.k, cs.r, cs.s = ty.c, op.a["r"], op.a["s"]
                 cs.stride, cs.pad, cs.p, cs.q = op.a["stride"], op.a["pad"], ty.h, ty.w
                 cs.ldx = tx.c if first else self._ld(k, op.x)
+                if first:
+                    self._dense_geometry(cs, k, op, lead, take)
                 cs.ldy = self._ld(k, op.y)
                 cs.flag = self._flag(k)
                 # fix the split count so the pixel partition is valid for this take
@@ -1367,6 +1449,9 @@ class ConvPack:
             g.row_bytes, g.rows = data.row_bytes, takes[lead]
             gs.append(g)
         ops.append((CNN["GATHER"], None, gs))
+        im = self._im2col_op([(k, leads[k], takes[leads[k]]) for k in act], data)
+        if im is not None:
+            ops.append(im)
         fwd = {k: self._fwd_steps(k, takes[k], leads[k], data) for k in act}
         bwd = {k: self._bwd_steps(k, takes[k], leads[k], data) for k in act}
         lanes = self._lanes(act)
@@ -1429,6 +1514,9 @@ class ConvPack:
             g.idx = self.idx[k].data_ptr()
             g.row_bytes, g.rows = data.row_bytes, take
             ops = [(CNN["GATHER"], None, [g])]
+            im = self._im2col_op([(k, k, take)], data)
+            if im is not None:
+                ops.append(im)
             ops += self._group([self._fwd_steps(k, take, k, data, train=False)])
             pr = CnnProgram(ops, self.device)
             self._progs[key] = pr

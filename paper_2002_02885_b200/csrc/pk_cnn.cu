@@ -166,6 +166,7 @@ size_t prob_size(int kind) {
     case PK_CNN_PUBLISH_T: return sizeof(pk_cnn_tpose);
     case PK_CNN_COMMIT: return sizeof(pk_cnn_commit);
     case PK_CNN_GATHER: return sizeof(pk_cnn_gather);
+    case PK_CNN_IM2COL: return sizeof(pk_cnn_im2col);
   }
   return 0;
 }
@@ -239,6 +240,10 @@ int prob_blocks(int kind, const void* pr) {
       const pk_cnn_gather& P = *static_cast<const pk_cnn_gather*>(pr);
       return (int)((P.row_bytes * P.rows + cnn::kGatherChunk - 1) / cnn::kGatherChunk);
     }
+    case PK_CNN_IM2COL: {
+      const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
+      return blocks_of(items((long long)P.n * P.p * P.q, P.ldo));
+    }
   }
   return 0;
 }
@@ -305,6 +310,13 @@ std::string check_prob(int kind, const void* pr) {
     case PK_CNN_GATHER: {
       const pk_cnn_gather& P = *static_cast<const pk_cnn_gather*>(pr);
       if (P.row_bytes % 16 || P.rows < 0) return "gather: row_bytes % 16";
+      break;
+    }
+    case PK_CNN_IM2COL: {
+      const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
+      if (P.ldo % 8 || P.cp % 8 || P.c < 1 || P.c > P.cp || P.r * P.s * P.c > P.ldo ||
+          P.stride < 1 || (long long)P.n * P.p * P.q * (P.ldo / 8) >= (1LL << 31))
+        return "im2col: ldo, cp multiples of 8, r*s*c <= ldo, c <= cp";
       break;
     }
   }
@@ -857,6 +869,7 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
     case PK_CNN_OPT: return launch_k(k_opt, nb, kBlock, 0, st, dp<pk_cnn_opt_seg>(g, o), db(g, o), np);
     case PK_CNN_PUBLISH_T: return launch_packs<pk_cnn_tpose>(o, k_publish_t, st);
     case PK_CNN_GATHER: return launch_packs<pk_cnn_gather>(o, k_gather, st);
+    case PK_CNN_IM2COL: return launch_packs<pk_cnn_im2col>(o, k_im2col, st);
     case PK_CNN_COMMIT:
       return launch_k(k_commit, cdiv(np, 128), 128, 0, st, dp<pk_cnn_commit>(g, o), np, o.ntile);
   }
@@ -1054,6 +1067,9 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
           break;
         case PK_CNN_GATHER:
           make_packs(r, static_cast<const pk_cnn_gather*>(op.probs), op.nprob, prob_blocks);
+          break;
+        case PK_CNN_IM2COL:
+          make_packs(r, static_cast<const pk_cnn_im2col*>(op.probs), op.nprob, prob_blocks);
           break;
       }
       g->launches += (int)r.packs.size();

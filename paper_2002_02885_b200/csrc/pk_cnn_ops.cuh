@@ -1503,6 +1503,46 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
 
 // batch gather: one block per 4 KB of rows, 16-byte vectors
 constexpr int kGatherChunk = 4096;
+// Dense im2col (pk_cnn_im2col): thread = (output pixel, 8 columns); the 8
+// columns span <= 8 taps of c real channels; a tap's channels are read as one
+// 16-byte vector of the (cp-pitched) input row.
+__global__ void __launch_bounds__(kBlock) k_im2col(const __grid_constant__ Pack<pk_cnn_im2col> G) {
+  pdl_gate();
+  const int pi = pack_prob(G, blockIdx.x);
+  const pk_cnn_im2col& P = G.p[pi];
+  const int cgo = P.ldo >> 3;
+  const int item = (blockIdx.x - G.blk0[pi]) * kBlock + (int)threadIdx.x;
+  if (item >= P.n * P.p * P.q * cgo) return;
+  const int m = item / cgo, k0 = 8 * (item - m * cgo);
+  const int n = m / (P.p * P.q), rem = m - n * (P.p * P.q);
+  const int oy = rem / P.q, ox = rem - oy * P.q;
+  const int kr = P.r * P.s * P.c;
+  const uint8_t* src = static_cast<const uint8_t*>(P.src);
+  __nv_bfloat16 out[8];
+  int last = -1;
+  uint4 v = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int k = k0 + e;
+    out[e] = __float2bfloat16(0.f);
+    if (k < kr) {
+      const int tap = k / P.c, ch = k - tap * P.c;
+      const int rr = tap / P.s, ss = tap - rr * P.s;
+      const int iy = oy * P.stride - P.pad + rr, ix = ox * P.stride - P.pad + ss;
+      if ((unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w) {
+        const int key = (tap << 8) | (ch >> 3);
+        if (key != last) {
+          v = ldg16(src + (((size_t)(n * P.h + iy) * P.w + ix) * P.cp + (ch & ~7)) * 2);
+          last = key;
+        }
+        out[e] = reinterpret_cast<const __nv_bfloat16*>(&v)[ch & 7];
+      }
+    }
+  }
+  *reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + ((size_t)m * P.ldo + k0) * 2) =
+      *reinterpret_cast<const uint4*>(out);
+}
+
 __global__ void __launch_bounds__(kBlock) k_gather(const __grid_constant__ Pack<pk_cnn_gather> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
