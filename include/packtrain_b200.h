@@ -505,7 +505,7 @@ typedef struct pk_cnn_gather {
  * of r*s*cp (cp = the input's padded channel pitch, 16): a 7x7x3 stem reads
  * 152 columns instead of 784. */
 typedef struct pk_cnn_im2col {
-  const void* src; /* bf16 [n][h][w][cp] */
+  const void* src; /* bf16 [n][h][w][cp], c <= 8 real channels */
   void* dst;       /* bf16 [n*p*q][ldo]  */
   int32_t n, h, w, cp, c, r, s, stride, pad, p, q, ldo;
 } pk_cnn_im2col;

@@ -242,7 +242,7 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_IM2COL: {
       const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
-      return blocks_of(items((long long)P.n * P.p * P.q, P.ldo));
+      return cdiv((long long)P.n * P.p * P.q, cnn::kIm2colPix);
     }
   }
   return 0;
@@ -314,9 +314,10 @@ std::string check_prob(int kind, const void* pr) {
     }
     case PK_CNN_IM2COL: {
       const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
-      if (P.ldo % 8 || P.cp % 8 || P.c < 1 || P.c > P.cp || P.r * P.s * P.c > P.ldo ||
+      if (P.ldo % 8 || P.ldo > 256 || P.cp % 8 || P.c < 1 || P.c > 8 || P.c > P.cp ||
+          P.r * P.s * P.c > P.ldo ||
           P.stride < 1 || (long long)P.n * P.p * P.q * (P.ldo / 8) >= (1LL << 31))
-        return "im2col: ldo, cp multiples of 8, r*s*c <= ldo, c <= cp";
+        return "im2col: ldo <= 256, ldo and cp multiples of 8, r*s*c <= ldo, c <= min(cp, 8)";
       break;
     }
   }

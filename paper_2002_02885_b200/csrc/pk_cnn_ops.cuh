@@ -1503,44 +1503,68 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
 
 // batch gather: one block per 4 KB of rows, 16-byte vectors
 constexpr int kGatherChunk = 4096;
-// Dense im2col (pk_cnn_im2col): thread = (output pixel, 8 columns); the 8
-// columns span <= 8 taps of c real channels; a tap's channels are read as one
-// 16-byte vector of the (cp-pitched) input row.
+// Dense im2col (pk_cnn_im2col, c <= 8): a block assembles kIm2colPix output
+// rows in shared memory and writes them out as coalesced 16-byte vectors
+// (zero columns past r·s·c).  Thread = (tap t % 64, pixel lane t / 64): its
+// tap's (r, s) is fixed, the block's pixels' window origins come from shared
+// memory, kU pixels' 16-byte channel vectors are loaded before their c values
+// are stored — no per-element index division.
+constexpr int kIm2colPix = 64;
 __global__ void __launch_bounds__(kBlock) k_im2col(const __grid_constant__ Pack<pk_cnn_im2col> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_im2col& P = G.p[pi];
-  const int cgo = P.ldo >> 3;
-  const int item = (blockIdx.x - G.blk0[pi]) * kBlock + (int)threadIdx.x;
-  if (item >= P.n * P.p * P.q * cgo) return;
-  const int m = item / cgo, k0 = 8 * (item - m * cgo);
-  const int n = m / (P.p * P.q), rem = m - n * (P.p * P.q);
-  const int oy = rem / P.q, ox = rem - oy * P.q;
-  const int kr = P.r * P.s * P.c;
+  __shared__ __align__(16) __nv_bfloat16 rows[kIm2colPix * 256];  // ldo <= 256
+  __shared__ int org[kIm2colPix][3];                                // n, iy0, ix0
+  const int M = P.n * P.p * P.q, taps = P.r * P.s, kr = taps * P.c;
+  const int m0 = (blockIdx.x - G.blk0[pi]) * kIm2colPix;
+  const int np = min(kIm2colPix, M - m0);
+  const int t = threadIdx.x;
+  if (t < np) {
+    const int m = m0 + t, n = m / (P.p * P.q), rem = m - n * (P.p * P.q);
+    const int oy = rem / P.q;
+    org[t][0] = n;
+    org[t][1] = oy * P.stride - P.pad;
+    org[t][2] = (rem - oy * P.q) * P.stride - P.pad;
+  }
+  for (int i = t; i < np * (P.ldo - kr); i += kBlock) {
+    const int pl = i / (P.ldo - kr);
+    rows[pl * P.ldo + kr + (i - pl * (P.ldo - kr))] = __float2bfloat16(0.f);
+  }
+  __syncthreads();
   const uint8_t* src = static_cast<const uint8_t*>(P.src);
-  __nv_bfloat16 out[8];
-  int last = -1;
-  uint4 v = make_uint4(0, 0, 0, 0);
+  const size_t pitch = (size_t)P.cp * 2;
+  for (int tap = t & 63; tap < taps; tap += 64) {
+    const int rr = tap / P.s, ss = tap - rr * P.s;
+    for (int p0 = t >> 6; p0 < np; p0 += 32) {
+      uint4 v[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int k = k0 + e;
-    out[e] = __float2bfloat16(0.f);
-    if (k < kr) {
-      const int tap = k / P.c, ch = k - tap * P.c;
-      const int rr = tap / P.s, ss = tap - rr * P.s;
-      const int iy = oy * P.stride - P.pad + rr, ix = ox * P.stride - P.pad + ss;
-      if ((unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w) {
-        const int key = (tap << 8) | (ch >> 3);
-        if (key != last) {
-          v = ldg16(src + (((size_t)(n * P.h + iy) * P.w + ix) * P.cp + (ch & ~7)) * 2);
-          last = key;
+      for (int u = 0; u < 8; ++u) {
+        const int pl = p0 + 4 * u;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (pl < np) {
+          const int iy = org[pl][1] + rr, ix = org[pl][2] + ss;
+          if ((unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w)
+            v[u] = ldg16(src + ((size_t)(org[pl][0] * P.h + iy) * P.w + ix) * pitch);
         }
-        out[e] = reinterpret_cast<const __nv_bfloat16*>(&v)[ch & 7];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pl = p0 + 4 * u;
+        if (pl >= np) continue;
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        uint16_t* d = reinterpret_cast<uint16_t*>(rows) + pl * P.ldo + tap * P.c;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch)
+          if (ch < P.c) d[ch] = (uint16_t)(w[ch >> 1] >> (16 * (ch & 1)));
       }
     }
   }
-  *reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + ((size_t)m * P.ldo + k0) * 2) =
-      *reinterpret_cast<const uint4*>(out);
+  __syncthreads();
+  const int vpr = P.ldo >> 3;  // 16-byte vectors per row
+  uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + (size_t)m0 * P.ldo * 2);
+  const uint4* sv = reinterpret_cast<const uint4*>(rows);
+  for (int i = t; i < np * vpr; i += kBlock) dst[i] = sv[i];
 }
 
 __global__ void __launch_bounds__(kBlock) k_gather(const __grid_constant__ Pack<pk_cnn_gather> G) {

@@ -84,4 +84,6 @@ def test_cnn_op_layout():
     """pk_cnn_op: kind, nprob, cfg0, cfg1, lane, pad0 (int32) then the problems pointer."""
     assert ctypes.sizeof(_lib.CnnOp) == 32
     assert _lib.CnnOp.lane.offset == 16 and _lib.CnnOp.probs.offset == 24
+    # pk_cnn_im2col: two pointers then twelve int32
+    assert ctypes.sizeof(_lib.CnnIm2col) == 64 and _lib.CnnIm2col.ldo.offset == 60
     assert ctypes.sizeof(_lib.PlanOptions) == 16 * 4
