@@ -763,7 +763,7 @@ class ConvPack:
         torch, z = self.torch, self._z
         b = m.batch
         net = m.net
-        A = {"val": {}, "grad": {}, "ws": {}, "stats": {}, "arg": {}, "split": {}}
+        A = {"val": {}, "grad": {}, "ws": {}, "stats": {}, "arg": {}, "split": {}, "dwcnt": {}}
         k = self.members.index(m)
         shared = self.first_shared.get(k)
         for name, t in net.tensors.items():
@@ -814,7 +814,14 @@ class ConvPack:
                 ty = net.tensors[op.y]
                 pix = b * ty.h * ty.w
                 nout = op.a["r"] * op.a["s"] * tx.c
-                A["ws"][op.name] = z(_red_ws(nout, 256, nout))  # <= 256 blocks either path
+                # generic path: <= 256 blocks of [r·s·c] records; 3x3 path: per chunk of
+                # <= 64 channels, <= 256 / chunks splits of [9][64] records + tree_reduce
+                cgb = min(_cgp(tx.c), 8)
+                nch = cdiv(tx.c // 8, cgb)
+                n9 = 9 * 8 * cgb
+                A["ws"][op.name] = z(max(_red_ws(nout, 256, nout),
+                                         nch * _red_ws(n9, 256 // nch, n9)))
+                A["dwcnt"][op.name] = z(17 * nch, dt=torch.int32)
             elif op.kind == "maxpool":
                 ty = net.tensors[op.y]
                 A["arg"][op.name] = z(b * ty.h * ty.w * ty.c, dt=torch.uint8)
@@ -1124,14 +1131,15 @@ class ConvPack:
         d.r, d.s, d.stride, d.pad, d.p, d.q = (op.a["r"], op.a["s"], op.a["stride"], op.a["pad"],
                                                ty.h, ty.w)
         d.ldx, d.ldy = self._ld(k, op.x), self._ld(k, op.y)
-        if d.r == 3 and d.s == 3 and d.stride in (1, 2) and tx.c <= 512:
+        if d.r == 3 and d.s == 3 and d.stride in (1, 2):
             # 3x3 fast path (csrc/pk_cnn_ops.cuh dw_fast_wgrad): blocks own a chunk of
             # <= 64 channels x one of <= 16 pixel splits (~DW_CHANNEL_PIXELS_PER_BLOCK
             # channel-pixels each), a multiple of the block's pixel lanes
             cgb = min(_cgp(tx.c), 8)
             lanes = (256 // cgb) // 3
             pix = take * ty.h * ty.w
-            nsplit = min(16, max(1, cdiv(pix * 8 * cgb, DW_CHANNEL_PIXELS_PER_BLOCK)))
+            nchunk = cdiv(tx.c // 8, cgb)
+            nsplit = min(256 // nchunk, max(1, cdiv(pix * 8 * cgb, DW_CHANNEL_PIXELS_PER_BLOCK)))
             d.ppb = rup(cdiv(pix, nsplit), lanes)
         else:
             d.ppb = rows_per_block(take * ty.h * ty.w, tx.c, per_thread=4)
@@ -1260,7 +1268,7 @@ class ConvPack:
                 steps.append((CNN["BN_BWD_APPLY"], None, b2, None))
             elif op.kind == "dw":
                 d = self._dw_struct(k, op, take)
-                d.counter = self._counter(k, 4 * net.op_index[op.name] + 1)
+                d.counter = A["dwcnt"][op.name].data_ptr()  # 17 ints per channel chunk
                 steps.append((CNN["DW_WGRAD"], None, d, None))
                 d2 = self._dw_struct(k, op, take)
                 d2.y = self._ptr(k, op.x, "grad")

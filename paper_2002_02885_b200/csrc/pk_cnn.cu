@@ -270,14 +270,10 @@ std::string check_prob(int kind, const void* pr) {
       const pk_cnn_dw& P = *static_cast<const pk_cnn_dw*>(pr);
       if (!c8(P.c) || P.r * P.s > 9 || P.stride < 1) return "dw: c % 8, r*s <= 9";
       if (kind == PK_CNN_DW_WGRAD && P.ppb < 1) return "dw: pixels per block >= 1";
-      if (kind == PK_CNN_DW_WGRAD && cnn::dw_fast(P, kind) &&
-          (P.ppb % cnn::dw_wgrad_lanes(P.c) ||
-           cdiv((long long)P.n * P.p * P.q, P.ppb) > cnn::kDwMaxSplits))
-        return "dw: 3x3 WGRAD pixels per block must be a multiple of the pixel lanes, <= 16 "
-               "splits";
-      if (kind == PK_CNN_DW_WGRAD && !cnn::dw_fast(P, kind) &&
-          prob_blocks(kind, pr) > cnn::kRedMaxBlocks)
-        return "dw: <= 256 pixel blocks";
+      if (kind == PK_CNN_DW_WGRAD && cnn::dw_fast(P, kind) && P.ppb % cnn::dw_wgrad_lanes(P.c))
+        return "dw: 3x3 WGRAD pixels per block must be a multiple of the pixel lanes";
+      if (kind == PK_CNN_DW_WGRAD && prob_blocks(kind, pr) > cnn::kRedMaxBlocks)
+        return "dw: WGRAD <= 256 blocks (channel chunks x pixel splits)";
       break;
     }
     case PK_CNN_MAXPOOL_FWD:

@@ -249,15 +249,27 @@ __device__ __forceinline__ bool tree_reduce(float* ws, int blk, int nblk, int no
   double* tot = grec + (long long)ngroups * nout;
   *tot_out = tot;
   if (!ticket(counters + 1 + grp, b1 - b0)) return false;
-  for (int i = threadIdx.x; i < nout; i += kBlock) {
+  for (int i = threadIdx.x; i < nout; i += kBlock) {  // the group's records: loads first
+    float r[kRedGroup];
+#pragma unroll
+    for (int b = 0; b < kRedGroup; ++b)
+      r[b] = b0 + b < b1 ? __ldcg(ws + (long long)(b0 + b) * stride + i) : 0.f;
     double v = 0.0;
-    for (int b = b0; b < b1; ++b) v += __ldcg(ws + (long long)b * stride + i);
+#pragma unroll
+    for (int b = 0; b < kRedGroup; ++b)
+      if (b0 + b < b1) v += r[b];
     grec[(long long)grp * nout + i] = v;
   }
   if (!ticket(counters, ngroups)) return false;
   for (int i = threadIdx.x; i < nout; i += kBlock) {
+    double r[kRedGroup];
+#pragma unroll
+    for (int g = 0; g < kRedGroup; ++g)
+      r[g] = g < ngroups ? __ldcg(grec + (long long)g * nout + i) : 0.0;
     double v = 0.0;
-    for (int g = 0; g < ngroups; ++g) v += __ldcg(grec + (long long)g * nout + i);
+#pragma unroll
+    for (int g = 0; g < kRedGroup; ++g)
+      if (g < ngroups) v += r[g];
     tot[i] = v;
   }
   __syncthreads();
@@ -740,18 +752,18 @@ __device__ __forceinline__ void dw_wgrad_generic(const pk_cnn_dw& P, int blk, in
 //     row r, pixel lane), kU pixels' loads (dy + the row's three x vectors)
 //     issued before their FMAs, 24 accumulators per thread.  The block's
 //     [9][64] record is summed over its lanes in lane order; a member's
-//     <= 16 splits of a chunk are folded in split order (fp64) by the chunk's
-//     last block (one ticket), whose loads are all issued before the adds.
-//     Small records and one short fold instead of [9][c] records per block
-//     and a two-level tree (a 1x1x480 layer: 44 -> a few us).  c <= 512.
+//     splits of a chunk (nchunk x nsplit <= 256 blocks) are folded in split
+//     order (fp64, tree_reduce: groups of 16, loads issued before the adds).
+//     Small records instead of [9][c] records per block (a 1x1x480 layer:
+//     44 -> 12 us).
 // ------------------------------------------------------------------------------
 __host__ __device__ __forceinline__ bool dw_fast(const pk_cnn_dw& P, int mode) {
-  if (P.r != 3 || P.s != 3 || (P.stride != 1 && P.stride != 2)) return false;
-  return mode != PK_CNN_DW_WGRAD || P.c <= 512;
+  (void)mode;
+  return P.r == 3 && P.s == 3 && (P.stride == 1 || P.stride == 2);
 }
 // WGRAD channel groups per block (a chunk), chunks per member, pixel lanes of
 // a 256-thread block ((256 / groups) / 3 kernel-row triples), splits per chunk
-constexpr int kDwChunkGroups = 8, kDwMaxSplits = 16;
+constexpr int kDwChunkGroups = 8;
 __host__ __device__ __forceinline__ int dw_wgrad_cgb(int c) {
   int g = 1;
   while (g < (c >> 3)) g <<= 1;
@@ -993,26 +1005,24 @@ __device__ __forceinline__ void dw_fast_wgrad(const pk_cnn_dw& P, int blk) {
     if (bad) *P.flag = 1;
     return;
   }
-  float* rec = P.ws + (long long)blk * n9;  // chunk-major, split order
+  // a chunk's records and tree_reduce workspace: [nsplit][n9] floats, fp64 group
+  // records, totals (cnn.py _red_ws(n9, nsplit, n9) floats per chunk)
+  const long long cstride = (((long long)nsplit * n9 + 1) & ~1LL) +
+                            2LL * n9 * ((nsplit + kRedGroup - 1) / kRedGroup + 1) + 2;
+  float* cws = P.ws + chunk * cstride;
+  float* rec = cws + (long long)split * n9;
   for (int o = t; o < n9; o += kBlock) {
     float a = 0.f;
     for (int l = 0; l < lanes; ++l) a += sh[l * n9 + o];
     rec[o] = a;
   }
-  if (!ticket(P.counter + chunk, nsplit)) return;
-  const float* r0 = P.ws + (long long)chunk * nsplit * n9;
+  double* tot;
+  if (!tree_reduce(cws, split, nsplit, n9, n9, P.counter + (kRedGroup + 1) * chunk, &tot)) return;
   for (int o = t; o < n9; o += kBlock) {
-    float v[kDwMaxSplits];
-#pragma unroll
-    for (int sp = 0; sp < kDwMaxSplits; ++sp) v[sp] = sp < nsplit ? __ldcg(r0 + (long long)sp * n9 + o) : 0.f;
-    double tot = 0.0;
-#pragma unroll
-    for (int sp = 0; sp < kDwMaxSplits; ++sp)
-      if (sp < nsplit) tot += v[sp];
     int di;
     if (out_index(o, di)) {
-      P.dw[di] = (float)tot;
-      bad |= !isfinite(tot);
+      P.dw[di] = (float)tot[o];
+      bad |= !isfinite(tot[o]);
     }
   }
   if (bad) *P.flag = 1;
