@@ -1166,6 +1166,101 @@ __device__ __forceinline__ void pool_bwd_item(const pk_cnn_pool& P, int m, int c
   st8(bptr(P.dx, m, P.ldx, ch), acc);
 }
 
+// Square-window max pooling with a compile-time window / stride: every tap's
+// source vector (forward) or every window's dY / argmax pair (backward: an
+// input pixel lies in <= ceil(R/ST)^2 windows, rr ≡ iy + pad mod ST) is loaded
+// before any is used; the taps / windows are then visited in the (r, s) order
+// of maxpool_fwd_item / pool_bwd_item, so the results are the same.
+template <int R, int ST>
+__device__ __forceinline__ void maxpool_fwd_fast(const pk_cnn_pool& P, int m, int ch) {
+  const int n = m / (P.p * P.q), rem = m - n * (P.p * P.q);
+  const int oy = rem / P.q, ox = rem - oy * P.q;
+  uint4 v[R][R];
+  bool ok[R][R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int iy = oy * ST - P.pad + r, ix = ox * ST - P.pad + s;
+      ok[r][s] = (unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w;
+      v[r][s] = ok[r][s] ? ldg16(bptr(P.x, ((long long)n * P.h + iy) * P.w + ix, P.ldx, ch))
+                         : make_uint4(0, 0, 0, 0);
+    }
+  float best[8];
+  uint8_t arg[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    best[e] = -INFINITY;
+    arg[e] = 0;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (!ok[r][s]) continue;
+      float x[8];
+      unpack8(v[r][s], x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (x[e] > best[e]) {
+          best[e] = x[e];
+          arg[e] = (uint8_t)(r * R + s);
+        }
+    }
+  st8(bptr(P.y, m, P.ldy, ch), best);
+  uint2 a;
+  a.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | ((uint32_t)arg[3] << 24);
+  a.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | ((uint32_t)arg[7] << 24);
+  *reinterpret_cast<uint2*>(P.arg + m * P.c + ch) = a;
+}
+
+template <int R, int ST>
+__device__ __forceinline__ void maxpool_bwd_fast(const pk_cnn_pool& P, int m, int ch) {
+  constexpr int NW = (R + ST - 1) / ST;  // candidate windows per axis
+  const int n = m / (P.h * P.w), rem = m - n * (P.h * P.w);
+  const int iy = rem / P.w, ix = rem - iy * P.w;
+  const int ry = (iy + P.pad) % ST, rx = (ix + P.pad) % ST;
+  uint4 d[NW][NW];
+  uint2 a[NW][NW];
+  bool ok[NW][NW];
+#pragma unroll
+  for (int j = 0; j < NW; ++j)
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const int rr = ry + j * ST, ss = rx + k * ST;
+      const int ty = iy + P.pad - rr, tx = ix + P.pad - ss;
+      ok[j][k] = rr < R && ss < R && ty >= 0 && tx >= 0 && ty / ST < P.p && tx / ST < P.q;
+      if (ok[j][k]) {
+        const long long o = ((long long)n * P.p + ty / ST) * P.q + tx / ST;
+        d[j][k] = ldg16(bptr(P.dy, o, P.ldy, ch));
+        a[j][k] = __ldg(reinterpret_cast<const uint2*>(P.arg + o * P.c + ch));
+      }
+    }
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+  for (int j = 0; j < NW; ++j)
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      if (!ok[j][k]) continue;
+      float dv[8];
+      unpack8(d[j][k], dv);
+      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a[j][k]);
+      const int tap = (ry + j * ST) * R + rx + k * ST;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (ab[e] == tap) acc[e] += dv[e];
+    }
+  if (P.accumulate) {
+    float o[8];
+    ld8(bptr(P.dx, m, P.ldx, ch), o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += o[e];
+  }
+  st8(bptr(P.dx, m, P.ldx, ch), acc);
+}
+
 __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
@@ -1175,8 +1270,8 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_fwd(const __grid_constant__ 
   if (item >= P.n * P.p * P.q * cgs) return;
   const int m = item / cgs;
   const int ch = 8 * (item - m * cgs);
-  if (P.r == 3 && P.s == 3 && P.stride == 2) maxpool_fwd_item<3, 3, 2>(P, m, ch);
-  else if (P.r == 2 && P.s == 2 && P.stride == 2) maxpool_fwd_item<2, 2, 2>(P, m, ch);
+  if (P.r == 3 && P.s == 3 && P.stride == 2) maxpool_fwd_fast<3, 2>(P, m, ch);
+  else if (P.r == 2 && P.s == 2 && P.stride == 2) maxpool_fwd_fast<2, 2>(P, m, ch);
   else maxpool_fwd_item<0, 0, 0>(P, m, ch);
 }
 
@@ -1189,8 +1284,8 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ 
   if (item >= P.n * P.h * P.w * cgs) return;
   const int m = item / cgs;
   const int ch = 8 * (item - m * cgs);
-  if (P.r == 3 && P.s == 3 && P.stride == 2) pool_bwd_item<3, 3, 2, false>(P, m, ch);
-  else if (P.r == 2 && P.s == 2 && P.stride == 2) pool_bwd_item<2, 2, 2, false>(P, m, ch);
+  if (P.r == 3 && P.s == 3 && P.stride == 2) maxpool_bwd_fast<3, 2>(P, m, ch);
+  else if (P.r == 2 && P.s == 2 && P.stride == 2) maxpool_bwd_fast<2, 2>(P, m, ch);
   else pool_bwd_item<0, 0, 0, false>(P, m, ch);
 }
 
