@@ -68,6 +68,30 @@ def test_teacher_forced_step(fam, K, b):
         assert h.optimizer.step_counter == 1 and h.cursor.steps_done == 1 and h.cursor.pos == b
 
 
+@pytest.mark.parametrize("fam,K,b,img", [("mobilenetv2", 2, 4, 56), ("resnet18", 2, 2, 40),
+                                         ("lenet5", 2, 8, 28)])
+def test_teacher_forced_odd_planes(fam, K, b, img):
+    """Planes whose widths are odd or not a multiple of the depthwise strip (56²:
+    28, 14, 7, 4, 2; 40²: 20, 10, 5, 3, 2), stride-2 layers on odd planes, and the
+    dense first conv (IM2COL) off the 32² / 224² shapes: every kernel of one packed
+    step teacher-forced against the oracle, packed == standalone bit for bit."""
+    arch = _arch(fam, img)
+    ds = _ds(n=64, img=img)
+    hs = _handles(arch, K, b, wd=1e-3)
+    before = [{n.split("/", 1)[1]: v.copy() for n, v in h.params.items()} for h in hs]
+    packed = packing.dedup_inputs(packing.pack_models(hs))
+    losses = packing.packed_step(packed, {"train": ds})
+    x, y = _batch(ds, arch, 0, 0, b)
+    for k, h in enumerate(hs):
+        _cnn.teacher_forced(packed._cp, k, before[k], x, y, b, losses[h.model_id])
+    solo = _handles(arch, K, b, wd=1e-3)
+    for h in solo:
+        assert packing.standalone_step(h, {"train": ds}) == losses[h.model_id]
+    for a, s_ in zip(hs, solo):
+        for n in a.params:
+            assert np.array_equal(a.params[n], s_.params[n]), n
+
+
 def test_end_to_end_loss_vs_oracle():
     """Whole-net forward from identical state: LeNet (no BN) matches the
     mirrored oracle to fp32 precision; BN nets within 1 % (bf16 chaos)."""
