@@ -1287,6 +1287,18 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   }
   pdl_wait();  // k_m1t_fwd's Z0 / A0 / partial logits are visible
   PK_TRACE(1);
+  // Z0 / A0 of the tile's units (dZ0 below) do not depend on the logits: their
+  // loads fly while the logits are summed and the softmax-xent runs
+  constexpr int PER = (T_MAXR * T_BU + BT - 1) / BT;  // elements per thread
+  float zr[PER], ar[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = tid + i * BT, r = e / T_BU, j = e % T_BU;
+    const bool ok = e < RP * T_BU && r < R && j < nu;
+    const int64_t g = (int64_t)r * H + u0 + j;
+    zr[i] = ok ? M.Z[0][g] : 0.f;
+    ar[i] = ok ? M.A[0][g] : 0.f;
+  }
   // ---- logits = Σ_blk partials + b1 → softmax-xent → dZ1 (in sL) ----------
   const int nb = t_nblk(H);
   const bool owner = (kt0 == 0 && utile == 0);
@@ -1336,16 +1348,6 @@ __device__ void m1t_bwd_tile(char* sm, const MemberDev<float>& M, const FeedDev<
   }
   // ---- dZ0[:, units] = (dZ1 · W1[units, :]ᵀ) ⊙ act'(Z0, A0) ----------------
   {
-    constexpr int PER = (T_MAXR * T_BU + BT - 1) / BT;  // elements per thread
-    float zr[PER], ar[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {  // every Z0/A0 load in flight at once
-      const int e = tid + i * BT, r = e / T_BU, j = e % T_BU;
-      const bool ok = e < RP * T_BU && r < R && j < nu;
-      const int64_t g = (int64_t)r * H + u0 + j;
-      zr[i] = ok ? M.Z[0][g] : 0.f;
-      ar[i] = ok ? M.A[0][g] : 0.f;
-    }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // park Z0 / A0 in shared memory (own elements)
       const int e = tid + i * BT;
