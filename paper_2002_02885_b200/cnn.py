@@ -886,7 +886,10 @@ class ConvPack:
 
     def get_member_state(self, k, want_slots=True):
         m = self.members[k]
-        self.torch.cuda.synchronize(self.dev)
+        # the pack's steps and the caller's uploads — not a device-wide sync, which
+        # would stall (and, mid-capture, break) other threads' concurrent packs
+        self.stream.synchronize()
+        self.torch.cuda.current_stream(self.dev).synchronize()
         params, slots = {}, {}
         for p in m.net.params:
             full = f"{m.model_id}/{p.name}"

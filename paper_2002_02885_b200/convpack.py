@@ -14,6 +14,7 @@ stream; losses and commit verdicts come back in one 16·K-byte read.
 """
 from __future__ import annotations
 
+import threading
 import weakref
 from dataclasses import dataclass, field
 
@@ -179,23 +180,27 @@ def conv_pack_models(handles) -> ConvPackedModel:
 
 # ---- device datasets and epoch orders ---------------------------------------------
 _DATA: dict = {}   # id(dataset) -> {(image, device): DeviceConvDataset}
+_LOCK = threading.RLock()  # the caches below are shared by concurrent packs' threads
 
 
 def device_dataset(ds, image, device, host=False):
     """The NHWC bf16 copy of `ds` the step reads (made once per dataset object,
     device and placement): HBM-resident, or page-locked host memory for the
     streamed input mode (runtime.set_input_mode("stream"))."""
-    per = _DATA.get(id(ds))
-    if per is None:
-        per = {}
-        _DATA[id(ds)] = per
-        weakref.finalize(ds, _DATA.pop, id(ds), None)
-    key = (tuple(image), device, host)
-    d = per.get(key)
-    if d is None:
-        d = cnn.DeviceConvDataset(ds, image, device, host)
-        per[key] = d
-    return d
+    with _LOCK:
+        per = _DATA.get(id(ds))
+        if per is None:
+            per = {}
+            _DATA[id(ds)] = per
+            weakref.finalize(ds, _DATA.pop, id(ds), None)
+        key = (tuple(image), device, host)
+        d = per.get(key)
+        if d is None:
+            import torch
+            d = cnn.DeviceConvDataset(ds, image, device, host)
+            torch.cuda.current_stream(device).synchronize()  # read on other packs' streams
+            per[key] = d
+        return d
 
 
 class _Orders:
@@ -207,15 +212,18 @@ class _Orders:
     def get(self, ds, epoch, device):
         import torch
         key = (ds.dataset_id, ds.n, epoch, device)
-        v = self.cache.pop(key, None)
-        if v is None:
-            perm = epoch_permutation(ds.dataset_id, ds.n, epoch)
-            v = (perm, torch.from_numpy(perm.astype(np.int64)).to(
-                torch.device("cuda", device)))
-        self.cache[key] = v
-        while len(self.cache) > 4:
-            self.cache.pop(next(iter(self.cache)))
-        return v
+        with _LOCK:
+            v = self.cache.pop(key, None)
+            if v is None:
+                perm = epoch_permutation(ds.dataset_id, ds.n, epoch)
+                v = (perm, torch.from_numpy(perm.astype(np.int64)).to(
+                    torch.device("cuda", device)))
+                # other threads' packs read this order on their own streams
+                torch.cuda.current_stream(device).synchronize()
+            self.cache[key] = v
+            while len(self.cache) > 4:
+                self.cache.pop(next(iter(self.cache)))
+            return v
 
 
 _ORDERS = _Orders()

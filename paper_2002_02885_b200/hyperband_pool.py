@@ -33,10 +33,17 @@ its `rung_runner`:
   the bracket, tuner.py:332-334; anything else propagates) instead of the
   healthy ranks blocking in the gather.
 
+* Concurrent packs on one GPU: a rank's groups of one round are independent
+  packs, each a chain of small latency-bound launches that fills a fraction of
+  the B200.  Executors that declare `concurrent_groups = n > 1` (the conv
+  executor) run up to n of them at once, one host thread and CUDA stream per
+  pack; results are keyed by group, so records are the serial run's.
+
 Executors used with the pool expose, besides the reference protocol
 (`device`, `memory_bytes(cfg)`, `evaluate(cfgs, epochs)`):
 `export_state(config_id) -> bytes | None`, `import_state(config_id, bytes)`
-and `drop_state(config_id)`; optional `group_cost(cfgs, epochs)`.
+and `drop_state(config_id)`; optional `group_cost(cfgs, epochs)` and
+`concurrent_groups`.
 """
 from __future__ import annotations
 
@@ -51,6 +58,37 @@ from .device import OOMError
 def _dist():
     import torch.distributed as dist
     return dist
+
+
+def _evaluate_group(executor, g, r_i, own_stream):
+    """One group's rung: ("ok", losses, ms) or ("error", packed exception, 0).
+    own_stream: run on a private CUDA stream (concurrent packs must not meet on
+    the legacy default stream, which serialises against every other stream)."""
+    try:
+        if own_stream:
+            import torch
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
+            st.synchronize()
+        else:
+            got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
+        return ("ok", got, t_ms)
+    except Exception as exc:  # noqa: BLE001 - re-raised after the merge
+        return ("error", _pack_exc(exc), 0.0)
+
+
+def _run_local(executor, items):
+    """items = [(key, group, r_i)] this rank trains: sequentially, or up to
+    executor.concurrent_groups packs at once (largest first)."""
+    n = int(getattr(executor, "concurrent_groups", 1) or 1)
+    if n <= 1 or len(items) <= 1:
+        return {key: _evaluate_group(executor, g, r_i, False) for key, g, r_i in items}
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(n, len(items))) as tp:
+        futs = {key: tp.submit(_evaluate_group, executor, g, r_i, True)
+                for key, g, r_i in items}
+        return {key: f.result() for key, f in futs.items()}
 
 
 class PackPool:
@@ -151,16 +189,9 @@ class PackPool:
     def __call__(self, executor, groups, r_i):
         where = self.assign(executor, groups, r_i)
         self._migrate(executor, groups, where)
-        mine = {}
         t0 = time.perf_counter()
-        for gi, (g, r) in enumerate(zip(groups, where)):
-            if r != self.rank:
-                continue
-            try:
-                got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
-                mine[gi] = ("ok", got, t_ms)
-            except Exception as exc:  # noqa: BLE001 - re-raised on every rank below
-                mine[gi] = ("error", _pack_exc(exc), 0.0)
+        mine = _run_local(executor, [(gi, g, r_i) for gi, (g, r) in enumerate(zip(groups, where))
+                                     if r == self.rank])
         self.busy_ms += (time.perf_counter() - t0) * 1000.0
         merged = {}
         for part in self._all_gather(mine):
@@ -198,16 +229,10 @@ class PackPool:
             where[i] = best
             load[best] += costs[i]
         self._migrate(executor, [g for _, _, g, _ in flat], where)
-        mine = {}
         t0 = time.perf_counter()
-        for i, (ti, gi, g, r_i) in enumerate(flat):
-            if where[i] != self.rank:
-                continue
-            try:
-                got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]
-                mine[i] = ("ok", got, t_ms)
-            except Exception as exc:  # noqa: BLE001 - returned to the task's bracket
-                mine[i] = ("error", _pack_exc(exc), 0.0)
+        local = sorted((i for i in range(len(flat)) if where[i] == self.rank),
+                       key=lambda i: (-costs[i], i))  # largest packs start first
+        mine = _run_local(executor, [(i, flat[i][2], flat[i][3]) for i in local])
         self.busy_ms += (time.perf_counter() - t0) * 1000.0
         merged = {}
         for part in self._all_gather(mine):

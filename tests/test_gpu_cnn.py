@@ -247,6 +247,24 @@ def test_conv_hyperband_packed_matches_unpacked():
     assert max(sizes.values()) >= 2  # knn really packed members
 
 
+def test_conv_hyperband_concurrent_packs_match_serial():
+    """The pool's concurrent packs (executor.concurrent_groups > 1: a round's
+    groups train at once, one host thread and CUDA stream per pack) give the
+    serial run's records, selection and member trajectories."""
+    from paper_2002_02885_b200 import hyperband_pool, tuner
+    ds = data.synth_dataset(300, 3 * 32 * 32, 10, seed=7, spread=1.0)
+    res = {}
+    for conc in (1, 4):
+        ex = tuner.B200ConvExecutor(ds, family="lenet5", width=1.0, seed=0)
+        ex.concurrent_groups = conc
+        res[conc] = hyperband_pool.overlapped_hyperband(9, 3, ex, seed=2, strategy="knn")[0]
+    key = lambda r: [(x.bracket, x.rung, x.group, x.config_id, x.epochs, x.loss)  # noqa: E731
+                     for x in r.records]
+    assert key(res[1]) == key(res[4])
+    assert res[1].best_config.config_id == res[4].best_config.config_id
+    assert len(res[4].records) > 8
+
+
 def test_pipelined_run_matches_step_loop():
     """convpack.conv_packed_run (host planning overlapped with the device, verdicts
     through a pinned ring) == the same number of packed_step calls, bit for bit:
