@@ -1030,7 +1030,7 @@ extern "C" int pk_cnn_prog_create(const pk_cnn_op* ops, int32_t nops, int32_t de
         int mx = 0;
         for (int j = 0; j < op.nprob; ++j)
           mx = std::max(mx, reinterpret_cast<const pk_cnn_head*>(src)[j].rows);
-        r.ntile = mx * 16;  // dynamic smem bytes
+        r.ntile = mx * 16 + cdiv(mx, 32) * 32 * 4;  // dynamic smem bytes (k_xent layout)
       }
       switch (op.kind) {
         case PK_CNN_BN_STATS:

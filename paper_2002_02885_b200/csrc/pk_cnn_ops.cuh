@@ -1369,6 +1369,69 @@ __global__ void __launch_bounds__(kBlock) k_xent(const __grid_constant__ Pack<pk
   int* rlab = reinterpret_cast<int*>(xs + 3 * P.rows);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float inv = 1.f / (float)P.rows;
+  if (P.classes <= 32) {
+    // narrow heads (CIFAR's 10 classes): a thread per row, every row's logits and
+    // label loaded at once (one round trip, not four per row in a warp's
+    // sequence); dbias from fixed-order xor-tree sums over each warp's 32 rows
+    float* part = xs + 4 * P.rows;  // [ceil(rows / 32)][classes <= 32] warp partials
+    const int nrw = (P.rows + 31) / 32;
+    for (int r0 = 0; r0 < P.rows; r0 += kBlock) {
+      const int r = r0 + threadIdx.x;
+      const bool on = r < P.rows;
+      const float* z = P.logits + (long long)(on ? r : 0) * P.ldl;
+      float zv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) zv[j] = on && j < P.classes ? z[j] : -INFINITY;
+      const int lab = on ? (int)P.labels[P.idx ? P.idx[r] : r] : 0;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mx = fmaxf(mx, zv[j]);
+      float se = 0.f, zl = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < P.classes) se += expf(zv[j] - mx);
+        zl = j == lab ? zv[j] : zl;
+      }
+      if (on) rloss[r] = logf(se) - (zl - mx);
+      const float is = 1.f / se;
+      if (on && P.dlogits) {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(P.dlogits) + (long long)r * P.ldl;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < P.classes) d[j] = __float2bfloat16_rn((expf(zv[j] - mx) * is - (j == lab ? 1.f : 0.f)) * inv);
+        for (int j = P.classes; j < P.ldl; ++j) d[j] = __float2bfloat16_rn(0.f);
+      }
+      if (P.dbias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j >= P.classes) break;
+          float g = on ? (expf(zv[j] - mx) / se - (j == lab ? 1.f : 0.f)) * inv : 0.f;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+          if (lane == 0 && r0 + warp * 32 < P.rows) part[(r0 / 32 + warp) * P.classes + j] = g;
+        }
+      }
+    }
+    __syncthreads();
+    bool bad = false;
+    if (P.dbias) {
+      for (int j = threadIdx.x; j < P.classes; j += kBlock) {
+        float s = 0.f;
+        for (int w = 0; w < nrw; ++w) s += part[w * P.classes + j];
+        P.dbias[j] = s;
+        bad |= !isfinite(s);
+      }
+    }
+    if (threadIdx.x == 0) {
+      double l = 0.0;
+      for (int r = 0; r < P.rows; ++r) l += rloss[r];
+      l /= P.rows;
+      *P.loss = (float)l;
+      bad |= !isfinite(l);
+    }
+    if (bad && P.flag) *P.flag = 1;
+    return;
+  }
   for (int r = warp; r < P.rows; r += kBlock / 32) {
     const float* z = P.logits + (long long)r * P.ldl;
     float mx = -INFINITY;
