@@ -213,7 +213,8 @@ int prob_blocks(int kind, const void* pr) {
     case PK_CNN_AVGPOOL_FWD: {
       const pk_cnn_pool& P = *static_cast<const pk_cnn_pool*>(pr);
       const bool global = P.r == P.h && P.s == P.w && P.pad == 0 && P.p == 1 && P.q == 1;
-      return blocks_of(items((long long)P.n * P.p * P.q, P.c) * (global ? cnn::kPoolLanes : 1));
+      return blocks_of(items((long long)P.n * P.p * P.q, P.c) *
+                       (global ? cnn::avgpool_lanes(P.h * P.w) : 1));
     }
     case PK_CNN_MAXPOOL_BWD:
     case PK_CNN_AVGPOOL_BWD: {

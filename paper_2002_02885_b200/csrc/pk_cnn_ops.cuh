@@ -1290,15 +1290,17 @@ __global__ void __launch_bounds__(kBlock) k_maxpool_bwd(const __grid_constant__ 
 }
 
 // average pool; the global case (window = the whole map) splits each output's
-// window over kPoolLanes threads and combines them with a fixed xor tree
+// window over kPoolLanes threads and combines them with a fixed xor tree — for
+// maps of >= 16 pixels; smaller maps (CIFAR nets end at 1x1 / 2x2) use one thread
 constexpr int kPoolLanes = 8;
+__host__ __device__ __forceinline__ int avgpool_lanes(int hw) { return hw >= 16 ? kPoolLanes : 1; }
 __global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ Pack<pk_cnn_pool> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_pool& P = G.p[pi];
   const int cgs = P.c >> 3;
   const bool global = P.r == P.h && P.s == P.w && P.pad == 0 && P.p == 1 && P.q == 1;
-  const int lanes = global ? kPoolLanes : 1;
+  const int lanes = global ? avgpool_lanes(P.h * P.w) : 1;
   const long long item = ((long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x) / lanes;
   const int lane = threadIdx.x % lanes;
   const long long total = (long long)P.n * P.p * P.q * cgs;
@@ -1316,10 +1318,12 @@ __global__ void __launch_bounds__(kBlock) k_avgpool_fwd(const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] += x[e];
       }
+    if (lanes > 1) {  // uniform per problem (a block never mixes problems)
 #pragma unroll
-    for (int o = kPoolLanes / 2; o; o >>= 1)
+      for (int o = kPoolLanes / 2; o; o >>= 1)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+        for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    }
     if (item >= total || lane != 0) return;
   } else {
     if (item >= total) return;
