@@ -204,26 +204,38 @@ def device_dataset(ds, image, device, host=False):
 
 
 class _Orders:
-    """Host + device epoch permutations, one per (dataset, epoch), LRU of 4."""
+    """Host + device epoch permutations, one per (dataset, epoch), LRU of 64.
+    A new order is uploaded from page-locked memory on a side stream and
+    published with an event: the step that needs it waits on the GPU
+    (`cudaStreamWaitEvent`), so an epoch boundary does not drain the
+    pipelined step loop, and concurrent packs on other streams see the copy."""
 
     def __init__(self):
         self.cache = {}
+        self.side = {}
 
     def get(self, ds, epoch, device):
+        """(host order, device order, ready event)"""
         import torch
         key = (ds.dataset_id, ds.n, epoch, device)
         with _LOCK:
             v = self.cache.pop(key, None)
             if v is None:
                 perm = epoch_permutation(ds.dataset_id, ds.n, epoch)
-                v = (perm, torch.from_numpy(perm.astype(np.int64)).to(
-                    torch.device("cuda", device)))
-                # other threads' packs read this order on their own streams
-                torch.cuda.current_stream(device).synchronize()
+                st = self.side.get(device)
+                if st is None:
+                    st = self.side[device] = torch.cuda.Stream(device=device)
+                host = torch.from_numpy(perm.astype(np.int64)).pin_memory()
+                with torch.cuda.stream(st):
+                    dev = host.to(torch.device("cuda", device), non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                v = (perm, dev, ev, host)  # host: the pinned source lives as long as the copy
             self.cache[key] = v
-            while len(self.cache) > 4:
-                self.cache.pop(next(iter(self.cache)))
-            return v
+            while len(self.cache) > 64:  # members of a pack sit at different epochs
+                old = self.cache.pop(next(iter(self.cache)))
+                old[2].synchronize()      # (long done) before its pinned source goes
+            return v[:3]
 
 
 _ORDERS = _Orders()
@@ -270,8 +282,9 @@ def _plan(packed: ConvPackedModel, active, datasets, cp):
                 raise IndexError(f"label out of bounds for member {h.model_id!r} "
                                  f"with {h.arch.classes} classes")
         take = min(b, ds.n - pos)
-        perm, dperm = _ORDERS.get(ds, epoch, cp.device)
+        perm, dperm, ready = _ORDERS.get(ds, epoch, cp.device)
         lead = index[id(grp[0])]
+        torch.cuda.current_stream(cp.device).wait_event(ready)
         cp.idx[lead][:take].copy_(dperm[pos:pos + take], non_blocking=True)
         rows = perm[pos:pos + take]
         for h in grp:
