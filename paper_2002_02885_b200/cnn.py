@@ -1088,6 +1088,21 @@ class ConvPack:
         return (CNN["IM2COL"], None, ims) if ims else None
 
     def _bn_struct(self, k, op, rows):
+        """member k's BN problem over `rows` rows: a copy of the (k, op) template
+        (every pointer / stride field is fixed for the pack's life) with the row
+        count and partition filled in — program builds are host work per new
+        takes tuple, so the Hyperband legs make hundreds of them"""
+        tpl = self._bn_tpl.get((k, op.name)) if hasattr(self, "_bn_tpl") else None
+        if tpl is None:
+            if not hasattr(self, "_bn_tpl"):
+                self._bn_tpl = {}
+            tpl = self._bn_tpl[(k, op.name)] = self._bn_template(k, op)
+        b = _lib.CnnBn.from_buffer_copy(tpl)
+        b.rows = rows
+        b.rpb = rows_per_block(rows, b.c)
+        return b
+
+    def _bn_template(self, k, op):
         m = self.members[k]
         net, A = m.net, self.acts[k]
         tx = net.tensors[op.x]
@@ -1108,8 +1123,7 @@ class ConvPack:
         b.ws = A["ws"][op.name].data_ptr()
         b.counter = self._counter(k, 4 * net.op_index[op.name])
         b.flag = self._flag(k)
-        b.rows, b.c = rows, tx.c
-        b.rpb = rows_per_block(rows, tx.c)
+        b.c = tx.c
         b.ldx = b.ldx2 = self._ld(k, op.x)
         b.ldo = b.ldd = self._ld(k, op.y)
         b.ldr = self._ld(k, op.res) if op.res else 0
