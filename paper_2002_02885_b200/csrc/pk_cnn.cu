@@ -448,6 +448,8 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr0, int n0, int ntile, int st
         p.OH = g.p; p.OW = g.q; p.dld = g.ldo;
         if (!make_map_2d(&L.tm[j], g.wt, g.k, kpad, kpad, ntile, p.a_mode == 3 ? 16 : 64))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (FPROP weights)");
+        p.wbase = static_cast<const uint8_t*>(g.wt);
+        p.wpitch = kpad * 2;
         p.splits = 1;
       } else if (kind == PK_CNN_CONV_DGRAD && p.par >= 0) {
         const int kpadt = rup(g.r * g.s * g.k, 64);
@@ -479,6 +481,8 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr0, int n0, int ntile, int st
         p.DH = g.h; p.DW = g.w;
         if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (DGRAD weights)");
+        p.wbase = static_cast<const uint8_t*>(g.wt);
+        p.wpitch = kpadt * 2;
         p.splits = 1;
       } else if (kind == PK_CNN_CONV_DGRAD) {
         const int kpadt = rup(g.r * g.s * g.k, 64);
@@ -508,6 +512,8 @@ int conv_to_launches(int kind, const pk_cnn_conv* pr0, int n0, int ntile, int st
         p.OH = g.h; p.OW = g.w; p.dld = g.ldo;
         if (!make_map_2d(&L.tm[j], g.wt, g.c, kpadt, kpadt, ntile, p.a_mode == 6 ? 32 : 64))
           return fail(PK_ERR_CUDA, "conv: cuTensorMapEncodeTiled failed (DGRAD weights)");
+        p.wbase = static_cast<const uint8_t*>(g.wt);
+        p.wpitch = kpadt * 2;
         p.splits = 1;
       } else {
         if (ntile % 64) return fail(PK_ERR_ARG, "conv: WGRAD N tile must be a multiple of 64");

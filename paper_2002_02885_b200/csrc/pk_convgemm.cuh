@@ -57,6 +57,8 @@ struct Problem {
   int ntap;                   // parity (a_mode 5): the class's taps: global tap index r·S + s
   int tapk[4], tdr[4], tds[4];//   and the dY offsets (dr, ds) of (i, j) it reads
   int brow0;                  // FPROP/DGRAD: first row of this problem's B in its map
+  const uint8_t* wbase;       // FPROP/DGRAD: the B (weight) matrix, row pitch wpitch bytes
+  int wpitch;                 //   (L2 prefetch of a tile's panel before the PDL wait; 0 = off)
   int SH, SW, SC, sld;        // source tensor: spatial dims, channels, pixel stride
   int OH, OW;                 // spatial dims of the GEMM's pixel space
   int R, S, stride, pad;
@@ -285,6 +287,27 @@ __device__ __forceinline__ TileInfo decode_tile(const Launch& L, int t, bool wgr
   return T;
 }
 
+// The weights do not depend on the previous kernel of the step (they were written by
+// the previous step's optimizer / transpose, in an earlier graph launch), so the TMA
+// producer pulls its first tile's weight panel into L2 before griddepcontrol.wait:
+// the first k-blocks' B loads then hit L2 while A waits on the predecessor.
+template <int MODE>
+__device__ __forceinline__ void prefetch_b_panel(const Launch& L, int t, int NT) {
+  if (MODE == WGRAD || t >= L.total_tiles) return;
+  const TileInfo ti = decode_tile(L, t, false);
+  const Problem& P = L.p[ti.pi];
+  if (!P.wbase || P.wpitch <= 0) return;
+  const int rows = min(NT, P.N - ti.tn * NT);
+  if (rows <= 0) return;
+  const uint8_t* a = P.wbase + ((long long)P.brow0 + (long long)ti.tn * NT) * P.wpitch;
+  // short-K GEMMs only (<= four 64-deep k-blocks: the 1x1 convs of the small nets, whose
+  // launches are latency-bound): the whole panel in one contiguous bulk prefetch. Longer
+  // rows measured slower (config3 +0.05-0.12 ms: per-row prefetches delay the producer)
+  if (P.wpitch <= 4 * BK * 2)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a),
+                 "r"((uint32_t)(rows * P.wpitch)) : "memory");
+}
+
 // TMEM accumulator (columns [tcol, tcol + NT) of this CTA's allocation) of one
 // output tile → global: bias / activation / fp32 / concat-N / accumulate per
 // the problem, non-finite flag for WGRAD.  Warps 0-3, lane quarter = warp.
@@ -467,6 +490,8 @@ k_conv_gemm(const __grid_constant__ Launch L) {
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
 
   if (warp < 4) {
@@ -664,6 +689,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p(const __grid_consta
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
   const uint32_t bstride = tcols / 2;  // accumulator buffer b at columns [b*bstride, +NT)
   const int T = L.total_tiles;
@@ -789,6 +816,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_pc(const __grid_const
   umma::cluster_sync();  // the peer's barriers are initialised before any remote arrive
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
   const uint32_t bstride = tcols / 2;
   const int T2 = L.total_pairs;
@@ -922,6 +951,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_p2(const __grid_const
   umma::cluster_sync();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
   const uint32_t bstride = tcols / 2;
   const int T2 = L.total_pairs;
@@ -1064,6 +1095,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_halo(const __grid_con
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
   const uint32_t bstride = tcols / 2;
   const int T = L.total_tiles;
@@ -1195,6 +1228,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_gemm_halo_res(const __grid
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 160) prefetch_b_panel<MODE>(L, blockIdx.x, L.ntile);
+
   tc::pdl_gate();
   const uint32_t bstride = tcols / 2;
   const int T = L.total_tiles, G = gridDim.x;
