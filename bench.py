@@ -2,7 +2,7 @@
 """Packed-training throughput on B200 — the BASELINE.json metric.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
-                    [--workload config1|config1_lenet|config2|config0|k16|wide16]
+                    [--workload config1|config1_lenet|config2|config3|config0|k16|wide16]
 
 Default workload: BASELINE configs[1] — K = 16 MobileNetV2-w0.5 members
 (mixed SGD / Momentum / Adam / Adagrad, lr sweep) on synthetic CIFAR-shape
