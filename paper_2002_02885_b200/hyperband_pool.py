@@ -65,8 +65,8 @@ def _evaluate_group(executor, g, r_i, own_stream):
     own_stream: run on a private CUDA stream (concurrent packs must not meet on
     the legacy default stream, which serialises against every other stream)."""
     try:
-        if own_stream:
-            import torch
+        import torch
+        if own_stream and torch.cuda.is_available():
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
                 got, t_ms = tuner.run_rung_groups(executor, [g], r_i)[0]

@@ -182,3 +182,34 @@ def test_overlapped_failures_match_serial():
     out = _run_world(2, "knn", diverge_on=victim, overlap=True)
     for _, summ, _, _ in out:
         assert summ == ("raised", "NonFiniteGradient", str(a.value))
+
+
+class ConcurrentStub(StatefulStub):
+    """The stub with the pool's concurrent packs switched on (a round's groups
+    evaluated by a thread pool, as the conv executor's packs are)."""
+    concurrent_groups = 4
+
+
+@pytest.mark.parametrize("strategy", ["original", "knn"])
+def test_concurrent_groups_match_serial(strategy):
+    """Groups of a round evaluated concurrently (hyperband_pool._run_local):
+    records, selection and failures equal the serial run's, including an
+    ExecutorError aborting its bracket and a diverging config raising the serial
+    run's exception."""
+    serial = tuner.packed_hyperband(81, 3, StatefulStub(), seed=3, strategy=strategy)
+    got, _ = hyperband_pool.overlapped_hyperband(81, 3, ConcurrentStub(), seed=3,
+                                                 strategy=strategy)
+    assert _summary(got) == _summary(serial)
+    serial = tuner.packed_hyperband(27, 3, StatefulStub(), seed=3, strategy=strategy)
+    victim = serial.records[5].config_id
+    ref = tuner.packed_hyperband(27, 3, StatefulStub(fail_on=victim), seed=3, strategy=strategy)
+    got, _ = hyperband_pool.overlapped_hyperband(27, 3, ConcurrentStub(fail_on=victim), seed=3,
+                                                 strategy=strategy)
+    assert _summary(got) == _summary(ref)
+    victim = serial.records[7].config_id
+    with pytest.raises(engine.NonFiniteGradient) as a:
+        tuner.packed_hyperband(27, 3, StatefulStub(diverge_on=victim), seed=3, strategy=strategy)
+    with pytest.raises(engine.NonFiniteGradient) as b:
+        hyperband_pool.overlapped_hyperband(27, 3, ConcurrentStub(diverge_on=victim), seed=3,
+                                            strategy=strategy)
+    assert str(a.value) == str(b.value)
