@@ -634,6 +634,31 @@ def test_costmodel_calibrates_on_device():
     assert metric(space.config(0), space.config(1)) >= 0
 
 
+def test_hyperband_with_calibrated_traintime_metric():
+    """§8f-4 in use: a pack-aware Hyperband run grouping by the training-time
+    distance with the B200-calibrated cost model (tuner.py:118-127 with measured
+    coefficients) instead of the index-sum distance.  Grouping changes which
+    configs share packs, never a config's trajectory: every (config, rung) loss
+    and the selected config equal the unpacked run's."""
+    from paper_2002_02885_b200 import costmodel as cm
+    dev, model = cm.calibrate(input_dim=784, hidden=(16,), classes=10, batches=(20, 45, 70),
+                              kinds=("sgd", "adam", "momentum", "adagrad"), pack_sizes=(2, 4),
+                              steps=10)
+    metric = cm.make_traintime_metric(model, dev)
+    ds = data.synth_dataset(600, 784, 10, seed=11, spread=0.1)
+    res = {}
+    for strat, kw in (("original", {}), ("knn", {"metric": metric, "threshold": 0.5})):
+        ex = tuner.B200Executor(ds, hidden=(16,), seed=0)
+        res[strat] = tuner.packed_hyperband(9, 3, ex, seed=4, strategy=strat, **kw)
+    key = lambda r: sorted((x.config_id, x.epochs, x.loss) for x in r.records)  # noqa: E731
+    assert key(res["original"]) == key(res["knn"])
+    assert res["original"].best_config.config_id == res["knn"].best_config.config_id
+    sizes = {}
+    for x in res["knn"].records:
+        sizes[(x.bracket, x.rung, x.group)] = sizes.get((x.bracket, x.rung, x.group), 0) + 1
+    assert max(sizes.values()) >= 2  # the traintime distance really packed configs
+
+
 # ------------------------------------------- tcgen05 path: schedule shapes --
 
 def test_tensor_path_grouped_input_tiles_lockstep(plan):
