@@ -859,7 +859,21 @@ cudaError_t run_op(const pk_cnn_prog* g, const OpRec& o, cudaStream_t st) {
     case PK_CNN_BN_STATS: return launch_packs<pk_cnn_bn>(o, k_bn_stats, st);
     case PK_CNN_BN_APPLY: return launch_packs<pk_cnn_bn>(o, k_bn_apply, st);
     case PK_CNN_BN_BWD_REDUCE: return launch_packs<pk_cnn_bn>(o, k_bn_bwd_reduce, st);
-    case PK_CNN_BN_BWD_APPLY: return launch_packs<pk_cnn_bn>(o, k_bn_bwd_apply, st);
+    case PK_CNN_BN_BWD_APPLY:
+      for (size_t i = 0; i < o.packs.size(); ++i) {  // variant per pack: activation, side outputs
+        if (o.pack_blocks[i] == 0) continue;
+        const auto& P = *reinterpret_cast<const cnn::Pack<pk_cnn_bn>*>(o.packs[i].data());
+        bool act = false, side = false;
+        for (int j = 0; j < P.nprob; ++j) {
+          act = act || P.p[j].act != PK_CNN_ACT_NONE;
+          side = side || P.p[j].accumulate || P.p[j].dres;
+        }
+        auto kern = act ? (side ? k_bn_bwd_apply_t<true, true> : k_bn_bwd_apply_t<true, false>)
+                        : (side ? k_bn_bwd_apply_t<false, true> : k_bn_bwd_apply_t<false, false>);
+        cudaError_t e = launch_k(kern, o.pack_blocks[i], kBlock, 0, st, P);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
     case PK_CNN_DW_FPROP: return launch_packs<pk_cnn_dw>(o, k_dw_fprop, st);
     case PK_CNN_DW_DGRAD: return launch_packs<pk_cnn_dw>(o, k_dw_dgrad, st);
     case PK_CNN_DW_WGRAD: return launch_packs<pk_cnn_dw>(o, k_dw_wgrad, st);

@@ -509,8 +509,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_bn_apply(const __grid_constant__ 
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constant__ Pack<pk_cnn_bn> G) {
-  pdl_gate();
+template <bool ACT, bool SIDE>
+__device__ __forceinline__ void bn_bwd_apply_impl(const Pack<pk_cnn_bn>& G) {
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
   const ApplyTile T = apply_tile(blockIdx.x - G.blk0[pi], P.rows, P.c, P.pad0);
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
     ccs[t] = -ca * mg - cb * mean;
   }
   __syncthreads();
-  const bool act = P.act != PK_CNN_ACT_NONE;
+  constexpr bool act = ACT;
   const int nitems = T.R * T.gw;
   for (int rb = T.r0; rb < T.r1; rb += T.R) {
   int row[kU], cg[kU];
@@ -573,14 +573,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
       dx[e] = fmaf(ca[e], g[e], fmaf(cb[e], xv[e], cc[e]));
     }
     uint8_t* pdx = bptr(P.dx, row[u], P.ldx2, ch);
-    if (P.accumulate) {
+    if (SIDE && P.accumulate) {
       float o[8];
       ld8(pdx, o);
 #pragma unroll
       for (int e = 0; e < 8; ++e) dx[e] += o[e];
     }
     *reinterpret_cast<uint4*>(pdx) = pack8(dx);
-    if (P.dres) {
+    if (SIDE && P.dres) {
       uint8_t* pr = bptr(P.dres, row[u], P.ldr, ch);
       if (P.res_accumulate) {
         float o[8];
@@ -592,6 +592,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_bn_bwd_apply(const __grid_constan
     }
   }
   }
+}
+
+// specialised on the activation and on the side outputs (accumulated dX, the
+// residual gradient): the plain form needs fewer registers (3 blocks / SM)
+template <bool ACT, bool SIDE>
+__global__ void __launch_bounds__(kBlock, (SIDE || ACT) ? 2 : 3) k_bn_bwd_apply_t(const __grid_constant__ Pack<pk_cnn_bn> G) {
+  pdl_gate();
+  bn_bwd_apply_impl<ACT, SIDE>(G);
 }
 
 // ============================ depthwise conv =====================================

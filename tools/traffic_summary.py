@@ -19,7 +19,7 @@ KIND = {"k_bn_stats": "BN_STATS", "k_bn_apply": "BN_APPLY", "k_bn_bwd_reduce": "
         "k_conv_gemm<1>": "CONV_DGRAD", "k_conv_gemm_p<1>": "CONV_DGRAD",
         "k_conv_gemm<2>": "CONV_WGRAD", "k_conv_gemm_p<2>": "CONV_WGRAD",
         "k_split_reduce": "SPLIT_REDUCE", "k_publish_t": "PUBLISH_T", "k_xent": "XENT",
-        "k_gather": "GATHER", "k_commit": "COMMIT"}
+        "k_gather": "GATHER", "k_commit": "COMMIT", "k_im2col": "IM2COL"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -34,7 +34,14 @@ def main(path, workload):
         if len(r) <= vi or "at::" in r[ki]:
             continue
         name = r[ki].split("(")[0].replace("void ", "").split("::")[-1]
-        d = per.setdefault(r[ii], {"kind": KIND.get(name, name)})
+        base = name.split("<")[0]
+        base = base[:-2] if base.endswith("_t") else base  # specialised kernels (k_*_t<...>)
+        kind = KIND.get(name) or KIND.get(base) or (
+            {"k_conv_gemm_pc": "CONV", "k_conv_gemm_p2": "CONV", "k_conv_gemm_halo": "CONV",
+             "k_conv_gemm_halo_res": "CONV"}.get(base, name))
+        if kind == "CONV":
+            kind = ("CONV_FPROP", "CONV_DGRAD", "CONV_WGRAD")[int(name.split("<")[1][0])]
+        d = per.setdefault(r[ii], {"kind": kind})
         d[r[ni]] = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
     launches = list(per.values())
     starts = [i for i, d in enumerate(launches) if d["kind"] == "GATHER"]
