@@ -1564,7 +1564,11 @@ __global__ void __launch_bounds__(kBlock) k_split_reduce(const __grid_constant__
 // rule, as the north_star's per-member extension).  A flagged member (non-finite
 // gradient anywhere) is left untouched, engine.py:297-299.
 constexpr int kOptChunk = 4096;  // elements per block
-__global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, const int* blk0,
+__device__ __forceinline__ uint32_t tc_pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // .x = lo (low half), .y = hi
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__global__ void __launch_bounds__(kBlock, 4) k_opt(const pk_cnn_opt_seg* segs, const int* blk0,
                                                 int nseg) {
   pdl_gate();
   const int si = find_prob(blk0, nseg, blockIdx.x);
@@ -1578,6 +1582,77 @@ __global__ void __launch_bounds__(kBlock) k_opt(const pk_cnn_opt_seg* segs, cons
     c2 = (float)(1.0 - pow(0.999, (double)t));
   }
   const float lr = S.lr, wd = S.wd;
+  // full, 16-byte-aligned chunks: every thread's four float4 groups of each stream
+  // are loaded before any update is stored (the scalar loop below serialises a
+  // round trip per element, since its stores may alias the next loads); the same
+  // per-element arithmetic, so the results are identical
+  const bool al = ((reinterpret_cast<uintptr_t>(S.w) | reinterpret_cast<uintptr_t>(S.g) |
+                    reinterpret_cast<uintptr_t>(S.s1) | reinterpret_cast<uintptr_t>(S.s2) |
+                    reinterpret_cast<uintptr_t>(S.w16)) & 15) == 0;
+  if (al && base + kOptChunk <= S.len) {
+    constexpr int NV = 2;  // float4 groups per thread in flight (two passes per chunk)
+    const bool one = S.kind != PK_OPT_SGD, two = S.kind == PK_OPT_ADAM;
+#pragma unroll 1
+    for (int pass = 0; pass < kOptChunk / (4 * kBlock * NV); ++pass) {
+    float4 w[NV], g[NV], a[NV], b[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const long long i = base + 4LL * (threadIdx.x + (pass * NV + j) * kBlock);
+      w[j] = *reinterpret_cast<const float4*>(S.w + i);
+      g[j] = *reinterpret_cast<const float4*>(S.g + i);
+      if (one) a[j] = *reinterpret_cast<const float4*>(S.s1 + i);
+      if (two) b[j] = *reinterpret_cast<const float4*>(S.s2 + i);
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float* wp = &w[j].x;
+      float* gp = &g[j].x;
+      float* ap = &a[j].x;
+      float* bp = &b[j].x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float wv = wp[e], gv = gp[e];
+        if (wd != 0.f) gv = fmaf(wd, wv, gv);
+        switch (S.kind) {
+          case PK_OPT_SGD:
+            wv -= lr * gv;
+            break;
+          case PK_OPT_MOMENTUM: {
+            const float v = 0.9f * ap[e] + gv;
+            ap[e] = v;
+            wv -= lr * v;
+            break;
+          }
+          case PK_OPT_ADAGRAD: {
+            const float acc = ap[e] + gv * gv;
+            ap[e] = acc;
+            wv -= lr * gv / (sqrtf(acc) + 1e-10f);
+            break;
+          }
+          default: {  // adam
+            const float m = 0.9f * ap[e] + 0.1f * gv;
+            const float v = 0.999f * bp[e] + 0.001f * (gv * gv);
+            ap[e] = m;
+            bp[e] = v;
+            wv -= lr * (m / c1) / (sqrtf(v / c2) + 1e-8f);
+          }
+        }
+        wp[e] = wv;
+      }
+      const long long i = base + 4LL * (threadIdx.x + (pass * NV + j) * kBlock);
+      *reinterpret_cast<float4*>(S.w + i) = w[j];
+      if (one) *reinterpret_cast<float4*>(S.s1 + i) = a[j];
+      if (two) *reinterpret_cast<float4*>(S.s2 + i) = b[j];
+      if (S.w16) {
+        uint2 h;
+        h.x = tc_pack_bf16(w[j].x, w[j].y);
+        h.y = tc_pack_bf16(w[j].z, w[j].w);
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(S.w16) + i) = h;
+      }
+    }
+    }
+    return;
+  }
   for (int k = threadIdx.x; k < kOptChunk; k += kBlock) {
     const long long i = base + k;
     if (i >= S.len) break;
