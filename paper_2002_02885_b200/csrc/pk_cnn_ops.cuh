@@ -1551,9 +1551,17 @@ __global__ void __launch_bounds__(kBlock) k_split_reduce(const __grid_constant__
   const long long i4 = (long long)(blockIdx.x - G.blk0[pi]) * kBlock + threadIdx.x;
   if (i4 * 4 >= P.len) return;
   float4 s = __ldcg(reinterpret_cast<const float4*>(P.src) + i4);
-  for (int j = 1; j < P.splits; ++j) {
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(P.src + (long long)j * P.len) + i4);
-    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  for (int j0 = 1; j0 < P.splits; j0 += 8) {  // eight partials' loads in flight, summed in order
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < P.splits)
+        v[u] = __ldcg(reinterpret_cast<const float4*>(P.src + (long long)(j0 + u) * P.len) + i4);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < P.splits) {
+        s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w;
+      }
   }
   reinterpret_cast<float4*>(P.dst)[i4] = s;
   if (!isfinite(s.x) || !isfinite(s.y) || !isfinite(s.z) || !isfinite(s.w)) *P.flag = 1;
