@@ -296,6 +296,8 @@ __device__ __forceinline__ void group_fold(float* ws, int blk, int nblk, int nou
   }
 }
 __device__ __forceinline__ double record_total(const float* ws, int nblk, int nout, int i) {
+  // <= kRedGroup records either way; the group records of large members (the
+  // bandwidth-bound layers) are all loaded before they are summed in order
   double v = 0.0;
   if (nblk <= kRedGroup) {
     for (int b = 0; b < nblk; ++b) v += __ldcg(ws + (long long)b * nout + i);
@@ -303,7 +305,12 @@ __device__ __forceinline__ double record_total(const float* ws, int nblk, int no
     const double* grec =
         reinterpret_cast<const double*>(ws + (((long long)nblk * nout + 1) & ~1LL));
     const int ng = (nblk + kRedGroup - 1) / kRedGroup;
-    for (int g = 0; g < ng; ++g) v += __ldcg(grec + (long long)g * nout + i);
+    double r[kRedGroup];
+#pragma unroll
+    for (int g = 0; g < kRedGroup; ++g) r[g] = g < ng ? __ldcg(grec + (long long)g * nout + i) : 0.0;
+#pragma unroll
+    for (int g = 0; g < kRedGroup; ++g)
+      if (g < ng) v += r[g];
   }
   return v;
 }
