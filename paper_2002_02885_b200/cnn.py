@@ -179,7 +179,7 @@ class Net:
         kpad = rup(r * s * tx.c, 64)
         cols = 0
         if x == "input" and DENSE_FIRST and tx.creal < tx.c and tx.creal <= 8 \
-                and rup(r * s * tx.creal, 8) <= 256:
+                and rup(r * s * tx.creal, 8) <= 256 and r * (63 * stride + s) <= 1024:
             # a narrow input's first conv runs as a 1x1 GEMM over dense im2col rows
             # (IM2COL op): K = r·s·creal (rounded to 8) instead of r·s·cp
             cols = rup(r * s * tx.creal, 8)

@@ -243,7 +243,7 @@ int prob_blocks(int kind, const void* pr) {
     }
     case PK_CNN_IM2COL: {
       const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
-      return cdiv((long long)P.n * P.p * P.q, cnn::kIm2colPix);
+      return P.n * P.p * cdiv(P.q, cnn::kIm2colPix);  // runs of an output row
     }
   }
   return 0;
@@ -313,8 +313,10 @@ std::string check_prob(int kind, const void* pr) {
       const pk_cnn_im2col& P = *static_cast<const pk_cnn_im2col*>(pr);
       if (P.ldo % 8 || P.ldo > 256 || P.cp % 8 || P.c < 1 || P.c > 8 || P.c > P.cp ||
           P.r * P.s * P.c > P.ldo ||
+          P.r * cnn::im2col_stage_cols(P.s, P.stride) > cnn::kIm2colStage ||
           P.stride < 1 || (long long)P.n * P.p * P.q * (P.ldo / 8) >= (1LL << 31))
-        return "im2col: ldo <= 256, ldo and cp multiples of 8, r*s*c <= ldo, c <= min(cp, 8)";
+        return "im2col: ldo <= 256, ldo and cp multiples of 8, r*s*c <= ldo, c <= min(cp, 8), "
+               "r*(63*stride+s) <= 1024";
       break;
     }
   }

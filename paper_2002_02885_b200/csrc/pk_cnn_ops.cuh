@@ -1773,66 +1773,61 @@ __global__ void k_commit(const pk_cnn_commit* probs, int nprob, int mode) {
 
 // batch gather: one block per 4 KB of rows, 16-byte vectors
 constexpr int kGatherChunk = 4096;
-// Dense im2col (pk_cnn_im2col, c <= 8): a block assembles kIm2colPix output
-// rows in shared memory and writes them out as coalesced 16-byte vectors
-// (zero columns past r·s·c).  Thread = (tap t % 64, pixel lane t / 64): its
-// tap's (r, s) is fixed, the block's pixels' window origins come from shared
-// memory, kU pixels' 16-byte channel vectors are loaded before their c values
-// are stored — no per-element index division.
-constexpr int kIm2colPix = 64;
+// Dense im2col (pk_cnn_im2col, c <= 8): a block owns one run of up to kIm2colPix
+// output pixels of one output row.  The input window rows that run touches
+// (R rows x ((kIm2colPix - 1)·stride + S) columns, one 16-byte channel vector
+// each) are staged in shared memory once — every input vector is read from L2
+// once per block instead of once per tap — then each thread (tap t % 64, pixel
+// lane t / 64) copies its tap's c values into the block's output rows, which
+// leave as coalesced 16-byte vectors (zero columns past r·s·c).
+constexpr int kIm2colPix = 64, kIm2colStage = 1024;  // staged input vectors <= 16 KB
+__host__ __device__ __forceinline__ int im2col_stage_cols(int s, int stride) {
+  return (kIm2colPix - 1) * stride + s;
+}
 __global__ void __launch_bounds__(kBlock) k_im2col(const __grid_constant__ Pack<pk_cnn_im2col> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_im2col& P = G.p[pi];
   __shared__ __align__(16) __nv_bfloat16 rows[kIm2colPix * 256];  // ldo <= 256
-  __shared__ int org[kIm2colPix][3];                                // n, iy0, ix0
-  const int M = P.n * P.p * P.q, taps = P.r * P.s, kr = taps * P.c;
-  const int m0 = (blockIdx.x - G.blk0[pi]) * kIm2colPix;
-  const int np = min(kIm2colPix, M - m0);
+  __shared__ __align__(16) uint4 stage[kIm2colStage];
+  const int taps = P.r * P.s, kr = taps * P.c;
+  const int segs = (P.q + kIm2colPix - 1) / kIm2colPix;
+  int b = blockIdx.x - G.blk0[pi];
+  const int seg = b % segs;
+  b /= segs;
+  const int oy = b % P.p, n = b / P.p;
+  const int ox0 = seg * kIm2colPix, np = min(kIm2colPix, P.q - ox0);
+  const int iy0 = oy * P.stride - P.pad, ix0 = ox0 * P.stride - P.pad;
+  const int W = im2col_stage_cols(P.s, P.stride);
   const int t = threadIdx.x;
-  if (t < np) {
-    const int m = m0 + t, n = m / (P.p * P.q), rem = m - n * (P.p * P.q);
-    const int oy = rem / P.q;
-    org[t][0] = n;
-    org[t][1] = oy * P.stride - P.pad;
-    org[t][2] = (rem - oy * P.q) * P.stride - P.pad;
+  const uint8_t* src = static_cast<const uint8_t*>(P.src);
+  const size_t pitch = (size_t)P.cp * 2;
+  for (int i = t; i < P.r * W; i += kBlock) {  // the window rows, zero outside the plane
+    const int rr = i / W, cx = i - rr * W, iy = iy0 + rr, ix = ix0 + cx;
+    stage[i] = (unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w
+                   ? ldg16(src + ((size_t)(n * P.h + iy) * P.w + ix) * pitch)
+                   : make_uint4(0, 0, 0, 0);
   }
   for (int i = t; i < np * (P.ldo - kr); i += kBlock) {
     const int pl = i / (P.ldo - kr);
     rows[pl * P.ldo + kr + (i - pl * (P.ldo - kr))] = __float2bfloat16(0.f);
   }
   __syncthreads();
-  const uint8_t* src = static_cast<const uint8_t*>(P.src);
-  const size_t pitch = (size_t)P.cp * 2;
   for (int tap = t & 63; tap < taps; tap += 64) {
     const int rr = tap / P.s, ss = tap - rr * P.s;
-    for (int p0 = t >> 6; p0 < np; p0 += 32) {
-      uint4 v[8];
+    for (int pl = t >> 6; pl < np; pl += 4) {
+      const uint4 v = stage[rr * W + pl * P.stride + ss];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint16_t* d = reinterpret_cast<uint16_t*>(rows) + pl * P.ldo + tap * P.c;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pl = p0 + 4 * u;
-        v[u] = make_uint4(0, 0, 0, 0);
-        if (pl < np) {
-          const int iy = org[pl][1] + rr, ix = org[pl][2] + ss;
-          if ((unsigned)iy < (unsigned)P.h && (unsigned)ix < (unsigned)P.w)
-            v[u] = ldg16(src + ((size_t)(org[pl][0] * P.h + iy) * P.w + ix) * pitch);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pl = p0 + 4 * u;
-        if (pl >= np) continue;
-        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-        uint16_t* d = reinterpret_cast<uint16_t*>(rows) + pl * P.ldo + tap * P.c;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          if (ch < P.c) d[ch] = (uint16_t)(w[ch >> 1] >> (16 * (ch & 1)));
-      }
+      for (int ch = 0; ch < 8; ++ch)
+        if (ch < P.c) d[ch] = (uint16_t)(w[ch >> 1] >> (16 * (ch & 1)));
     }
   }
   __syncthreads();
   const int vpr = P.ldo >> 3;  // 16-byte vectors per row
-  uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + (size_t)m0 * P.ldo * 2);
+  const long long m0 = ((long long)n * P.p + oy) * P.q + ox0;
+  uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(P.dst) + m0 * P.ldo * 2);
   const uint4* sv = reinterpret_cast<const uint4*>(rows);
   for (int i = t; i < np * vpr; i += kBlock) dst[i] = sv[i];
 }
