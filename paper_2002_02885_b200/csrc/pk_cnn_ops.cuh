@@ -323,7 +323,7 @@ __global__ void k_spin(long long cycles) {
 }
 
 // ============================== batch norm =====================================
-__global__ void __launch_bounds__(kBlock, 3) k_bn_stats(const __grid_constant__ Pack<pk_cnn_bn> G) {
+__global__ void __launch_bounds__(kBlock, 4) k_bn_stats(const __grid_constant__ Pack<pk_cnn_bn> G) {
   pdl_gate();
   const int pi = pack_prob(G, blockIdx.x);
   const pk_cnn_bn& P = G.p[pi];
